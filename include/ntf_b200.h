@@ -1,0 +1,162 @@
+/*
+ * ntf_b200.h — C ABI of the B200 (sm_100a) NTF hot path.
+ *
+ * Drop-in boundary for the per-mode update of the reference's ADMoM
+ * non-negative CP solver (package `cpadmm`, /root/reference/pkg/src/cpadmm).
+ * The reference is pure Python with no FFI; its boundary is the Python call
+ * `cpadmm.fit(t, rank, specs=None, config=None) -> FitResult` (solver.py:340).
+ * The Python package `paper_1409_2383_b200` mirrors that call and binds the
+ * entry points below with ctypes (INTEGRATION.md shows the binding).  Each
+ * entry point names the reference function it replaces.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated; no torch types.
+ *  - `stream` is a cudaStream_t passed as an opaque pointer.  Every call is
+ *    stream-ordered and asynchronous; nothing synchronises the host.
+ *  - Tensors are dense, order 3, row-major X[i][j][k] (tensors.py:40-48),
+ *    element type NTF_F32 or NTF_F64.  Factors/aux/duals are row-major
+ *    fp64 (rows x R), R <= NTF_MAX_RANK.
+ *  - Return value: NTF_OK or an NTF_ERR_* code; `ntf_last_error()` gives a
+ *    thread-local message.  Device-side numerical failures (Cholesky
+ *    breakdown, non-finite projection input) are reported through the
+ *    int status word the caller passes in and map to the reference's
+ *    InvalidPenaltyError (solver.py:31-32, 167-175) and ValueError
+ *    (constraints.py:108-109).
+ *  - Reentrant: no global mutable state besides the thread-local message;
+ *    a plan owns its own scratch memory.
+ */
+#ifndef NTF_B200_H
+#define NTF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTF_ABI_VERSION 1
+#define NTF_MAX_RANK 128
+
+typedef void* ntf_stream_t;
+
+enum ntf_status {
+  NTF_OK = 0,
+  NTF_ERR_INVALID = 1,     /* bad argument (ValueError in the shim)          */
+  NTF_ERR_NOT_PD = 2,      /* InvalidPenaltyError                           */
+  NTF_ERR_NONFINITE = 3,   /* ValueError: non-finite entries                */
+  NTF_ERR_CUDA = 4,        /* CUDA runtime/launch failure (RuntimeError)     */
+  NTF_ERR_UNSUPPORTED = 5  /* configuration outside the kernels' envelope    */
+};
+
+enum ntf_dtype { NTF_F32 = 0, NTF_F64 = 1 };
+
+/* MTTKRP engine selection (NTF_ENGINE_AUTO picks by rank and dtype). */
+enum ntf_engine { NTF_ENGINE_AUTO = 0, NTF_ENGINE_CUDA_CORE = 1, NTF_ENGINE_TCGEN05 = 2 };
+
+int ntf_abi_version(void);
+const char* ntf_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Dense MTTKRP, one mode:  out = X_(mode) * KR(companions, highest first).
+ * Replaces tensors.mttkrp_factors dense branch (tensors.py:254-262), i.e.
+ * khatri_rao (tensors.py:203-220) + the unfolding GEMM (tensors.py:262),
+ * without the unfolding copy (tensors.py:63-71) or the materialised KR.
+ * out: M x R fp64 (M = dims[mode-1]).  `workspace` holds split partials.
+ * ------------------------------------------------------------------------- */
+size_t ntf_mttkrp_workspace_bytes(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R,
+                                  int engine);
+int ntf_mttkrp(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
+               const double* A, const double* B, const double* C, int R, double* out,
+               void* workspace, size_t workspace_bytes, int engine, ntf_stream_t stream);
+
+/* Gram matrix G = F^T F (R x R fp64) — the per-factor term of
+ * solver.companion_gram (solver.py:196-204) / tensors.gram_hadamard
+ * (tensors.py:228-240).  Deterministic fixed-order reduction. */
+size_t ntf_gram_workspace_bytes(int64_t rows, int R);
+int ntf_gram(const double* F, int64_t rows, int R, double* G, void* workspace,
+             size_t workspace_bytes, ntf_stream_t stream);
+
+/* Sum of squares over a dense tensor and of its residual against a Kruskal
+ * model: out2[0] = sum x^2, out2[1] = sum (x - [[A,B,C]])^2, fp64
+ * accumulation, fixed-order reduction.  Replaces DenseTensor.norm
+ * (tensors.py:57-61) and tensors.rfe dense (tensors.py:282-290,
+ * reconstruct tensors.py:276-279).  A/B/C may be NULL (only out2[0]). */
+size_t ntf_sq_error_workspace_bytes(int64_t I, int64_t J, int64_t K);
+int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, const double* A,
+                 const double* B, const double* C, int R, double* out2, void* workspace,
+                 size_t workspace_bytes, ntf_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Solver plan: device-resident ADMoM outer iterations for one order-3 dense
+ * tensor and nonneg constraints on every mode.  Replaces solver.iterate
+ * (solver.py:295-327) and the per-iteration part of solver.fit
+ * (solver.py:375-387): Gauss-Seidel sweeps of _factor_update_core
+ * (solver.py:207-219), aux/dual updates fused into each mode's last sweep
+ * (as mesh.py:220-223), residuals (solver.py:247-255), check_stop
+ * (solver.py:258-269) and adapt_penalties (solver.py:272-292), with the
+ * penalties, histories and stop flag kept on the device.
+ * ------------------------------------------------------------------------- */
+typedef struct ntf_plan ntf_plan;
+
+typedef struct ntf_plan_desc {
+  /* problem: the tensor as seen by each mode's MTTKRP.  Single GPU: all
+   * three entries are the whole tensor.  Sharded (P GPUs): entry
+   * m is this rank's mode-m slab (X[I_p,:,:], X[:,J_p,:], X[:,:,K_p]) and
+   * x_dims[m] its extents; mode-m rows [row_offset[m], +row_count[m]) of the
+   * factor are owned here (blocks.PartitionPlan.uniform, blocks.py:47-61). */
+  int x_dtype;
+  const void* x_mode[3];
+  int64_t x_dims[3][3];
+  int64_t dims[3];          /* full extents (factor row counts)             */
+  int64_t row_offset[3];
+  int64_t row_count[3];
+  int rank;
+  int engine;               /* ntf_engine                                   */
+  int fuse_gram;            /* 1: refresh grams[m] inside the mode update   */
+  /* SolverConfig (solver.py:35-49) */
+  double eps_abs, eps_rel, mu, tau_incr, tau_decr;
+  int inner_sweeps;
+  int adapt;
+  /* state, caller-owned device buffers (fp64 row-major) */
+  double* factors[3];       /* dims[m] x R  working factors (replicated)    */
+  double* aux[3];           /* row_count[m] x R  auxiliary copies (owned)   */
+  double* duals[3];         /* row_count[m] x R  scaled duals Y (owned)     */
+  double* grams[3];         /* R x R        F_m^T F_m                       */
+  double* rho;              /* [3]          per-mode penalties              */
+  double* norm_acc;         /* [3][5]  per-mode sums of squares of the last
+                               sweep: F-aux, aux-aux_prev, F, aux, Y (all-
+                               reduced by the caller before finalize if P>1) */
+  /* per-iteration outputs: row `it` written by iteration `it` */
+  int64_t history_capacity; /* rows available in the history buffers        */
+  double* resid_history;    /* [cap][6]  primal[3], dual[3]                 */
+  double* rho_history;      /* [cap][3]  rho after adaptation               */
+  int* counters;            /* [4]: iteration, stop flag, status, spare     */
+} ntf_plan_desc;
+
+int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);
+/* Recompute grams[m] from factors[m] (after the caller (re)initialises state). */
+int ntf_plan_sync_grams(ntf_plan* plan, ntf_stream_t stream);
+/* Enqueue `n_iters` outer iterations.  Iterations after the stop flag is set
+ * are no-ops (kernels observe the flag), so a chunk may be enqueued ahead.
+ * use_graph != 0 replays one captured outer iteration (CUDA graph). */
+int ntf_plan_run(ntf_plan* plan, int n_iters, int use_graph, ntf_stream_t stream);
+/* Single per-mode update, for tests and the sharded engine:  mode 1..3,
+ * last_sweep != 0 also applies the projection, dual step and norm partials. */
+int ntf_plan_mode_update(ntf_plan* plan, int mode, int last_sweep, ntf_stream_t stream);
+/* Close one outer iteration after the sweeps: residuals, stop test, adaptation. */
+int ntf_plan_finalize(ntf_plan* plan, ntf_stream_t stream);
+/* Optional per-launch timing: when enabled, the plan records CUDA events
+ * around every MTTKRP and every row-update launch of an outer iteration (also
+ * inside the captured graph).  ntf_plan_kernel_times writes, for the most
+ * recent iteration, 2 floats (MTTKRP ms, update ms) per mode update in sweep
+ * order and returns how many floats were written (or a negative status). */
+int ntf_plan_set_timing(ntf_plan* plan, int enable);
+int ntf_plan_kernel_times(ntf_plan* plan, float* ms_out, int capacity);
+void ntf_plan_destroy(ntf_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NTF_B200_H */

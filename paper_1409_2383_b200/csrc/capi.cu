@@ -1,0 +1,426 @@
+// C ABI (include/ntf_b200.h) and the solver-plan runtime.
+//
+// The plan owns the launch geometry, scratch memory and a captured CUDA graph
+// of one outer iteration: inner_sweeps x 3 x (MTTKRP -> fused ridge/ADMM row
+// update) followed by the finalize kernel, i.e. solver.iterate
+// (reference solver.py:295-327) with aux/dual fused into each mode's last
+// sweep exactly as mesh.py:220-223 does.  Nothing here synchronises the host.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "mttkrp_cc.cuh"
+#include "mttkrp_tc.cuh"
+#include "solver_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return NTF_ERR_CUDA;
+}
+
+#define NTF_CUDA_TRY(expr)                              \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+int check_dims(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
+  if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
+  if (x_dtype != NTF_F32 && x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "bad dtype");
+  if (I < 1 || J < 1 || K < 1) return fail(NTF_ERR_INVALID, "all extents must be >= 1");
+  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
+  const int64_t Q = mode == 1 ? J * K : (mode == 2 ? I * K : I * J);
+  if (Q >= (int64_t(1) << 31)) return fail(NTF_ERR_UNSUPPORTED, "reduction length >= 2^31");
+  return NTF_OK;
+}
+
+bool use_tc(int engine, int x_dtype, int R) {
+  if (engine == NTF_ENGINE_CUDA_CORE) return false;
+  if (engine == NTF_ENGINE_TCGEN05) return true;
+  return ntf::mttkrp_tc_auto(x_dtype, R);
+}
+
+// One MTTKRP engine instance for one (mode, shape): geometry + launcher.
+struct MttkrpOp {
+  bool tc = false;
+  ntf::MttkrpCCLaunch cc{};
+  ntf::MttkrpTCLaunch tcl{};
+  int splits() const { return tc ? tcl.splits : cc.splits; }
+  size_t ws_bytes(int R) const {
+    return tc ? ntf::mttkrp_tc_workspace_bytes(tcl, R) : ntf::mttkrp_cc_workspace_bytes(cc, R);
+  }
+};
+
+MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, int engine) {
+  MttkrpOp op;
+  op.tc = use_tc(engine, x_dtype, R);
+  if (op.tc)
+    op.tcl = ntf::mttkrp_tc_plan(mode, x_dtype, I, J, K, R);
+  else
+    op.cc = ntf::mttkrp_cc_plan(mode, x_dtype, I, J, K, R);
+  return op;
+}
+
+cudaError_t run_op(const MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
+                   int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
+                   const int* stop, cudaStream_t s) {
+  if (op.tc) return ntf::mttkrp_tc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.tcl, ws, stop, s);
+  return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
+}
+
+}  // namespace
+
+struct ntf_plan {
+  ntf_plan_desc d;
+  MttkrpOp op[3];
+  int blocks[3];
+  double* mtt_ws = nullptr;
+  double* norm_partials = nullptr;
+  double* gram_partials = nullptr;
+  double* gram_ws = nullptr;
+  unsigned* done = nullptr;
+  cudaStream_t capture_stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  // per-launch timing events: 3 per mode update (before MTTKRP, after MTTKRP,
+  // after the row update), inner_sweeps * 3 mode updates per iteration
+  int timing = 0;
+  int n_events = 0;
+  int cursor = 0;
+  cudaEvent_t* events = nullptr;
+};
+
+namespace {
+
+int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
+  const ntf_plan_desc& d = pl->d;
+  const int m = mode - 1;
+  const int R = d.rank;
+  const int64_t* xd = d.x_dims[m];
+  cudaEvent_t* ev = nullptr;
+  if (pl->timing && pl->events) {
+    ev = pl->events + 3 * pl->cursor;
+    pl->cursor = (pl->cursor + 1) % (pl->n_events / 3);
+    NTF_CUDA_TRY(cudaEventRecord(ev[0], s));
+  }
+  NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2], d.factors[0],
+                      d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s));
+  if (ev) NTF_CUDA_TRY(cudaEventRecord(ev[1], s));
+  // companions, highest mode first (solver.py:196-204)
+  static const int comp[3][2] = {{2, 1}, {2, 0}, {1, 0}};
+  ntf::FactorUpdateParams fp{};
+  fp.mode = mode;
+  fp.R = R;
+  fp.rows = d.row_count[m];
+  fp.row_offset = d.row_offset[m];
+  fp.mtt = pl->mtt_ws;
+  fp.splits = pl->op[m].splits();
+  fp.Ga = d.grams[comp[m][0]];
+  fp.Gb = d.grams[comp[m][1]];
+  fp.rho = d.rho;
+  fp.F = d.factors[m];
+  fp.aux = d.aux[m];
+  fp.dual = d.duals[m];
+  fp.last_sweep = last;
+  fp.fuse_gram = d.fuse_gram;
+  fp.norm_partials = pl->norm_partials;
+  fp.gram_partials = pl->gram_partials;
+  fp.G_out = d.grams[m];
+  fp.norm_acc = d.norm_acc + 5 * m;
+  fp.done_counter = pl->done + m;
+  fp.status = d.counters + 2;
+  fp.stop_flag = d.counters + 1;
+  NTF_CUDA_TRY(ntf::factor_update_launch(fp, s));
+  if (ev) NTF_CUDA_TRY(cudaEventRecord(ev[2], s));
+  return NTF_OK;
+}
+
+int enqueue_finalize(ntf_plan* pl, cudaStream_t s) {
+  const ntf_plan_desc& d = pl->d;
+  ntf::FinalizeParams fz{};
+  fz.norm_acc = d.norm_acc;
+  fz.rho = d.rho;
+  for (int m = 0; m < 3; ++m) fz.dims[m] = d.dims[m];
+  fz.R = d.rank;
+  fz.eps_abs = d.eps_abs;
+  fz.eps_rel = d.eps_rel;
+  fz.mu = d.mu;
+  fz.tau_incr = d.tau_incr;
+  fz.tau_decr = d.tau_decr;
+  fz.adapt = d.adapt;
+  fz.history_capacity = d.history_capacity;
+  fz.resid_history = d.resid_history;
+  fz.rho_history = d.rho_history;
+  fz.counters = d.counters;
+  NTF_CUDA_TRY(ntf::finalize_launch(fz, s));
+  return NTF_OK;
+}
+
+int enqueue_iteration(ntf_plan* pl, cudaStream_t s) {
+  const int sweeps = pl->d.inner_sweeps;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int mode = 1; mode <= 3; ++mode) {
+      const int rc = enqueue_mode_update(pl, mode, sw == sweeps - 1, s);
+      if (rc != NTF_OK) return rc;
+    }
+  return enqueue_finalize(pl, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ntf_abi_version(void) { return NTF_ABI_VERSION; }
+
+const char* ntf_last_error(void) { return g_err.c_str(); }
+
+size_t ntf_mttkrp_workspace_bytes(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R,
+                                  int engine) {
+  if (check_dims(mode, x_dtype, I, J, K, R) != NTF_OK) return 0;
+  const MttkrpOp op = make_op(mode, x_dtype, I, J, K, R, engine);
+  return op.ws_bytes(R);
+}
+
+int ntf_mttkrp(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
+               const double* A, const double* B, const double* C, int R, double* out,
+               void* workspace, size_t workspace_bytes, int engine, ntf_stream_t stream) {
+  int rc = check_dims(mode, x_dtype, I, J, K, R);
+  if (rc != NTF_OK) return rc;
+  if (!X || !out || !workspace) return fail(NTF_ERR_INVALID, "null pointer");
+  if ((mode != 1 && !A) || (mode != 2 && !B) || (mode != 3 && !C))
+    return fail(NTF_ERR_INVALID, "missing companion factor");
+  if (engine == NTF_ENGINE_TCGEN05 && !ntf::mttkrp_tc_supported(x_dtype, R))
+    return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank");
+  const MttkrpOp op = make_op(mode, x_dtype, I, J, K, R, engine);
+  if (workspace_bytes < op.ws_bytes(R)) return fail(NTF_ERR_INVALID, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* ws = static_cast<double*>(workspace);
+  NTF_CUDA_TRY(run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s));
+  const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
+  NTF_CUDA_TRY(ntf::mttkrp_reduce_launch(ws, op.splits(), M, R, out, nullptr, s));
+  return NTF_OK;
+}
+
+size_t ntf_gram_workspace_bytes(int64_t rows, int R) { return ntf::gram_workspace_bytes(rows, R); }
+
+int ntf_gram(const double* F, int64_t rows, int R, double* G, void* workspace,
+             size_t workspace_bytes, ntf_stream_t stream) {
+  if (!F || !G || !workspace) return fail(NTF_ERR_INVALID, "null pointer");
+  if (rows < 1 || R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_INVALID, "bad shape");
+  if (workspace_bytes < ntf::gram_workspace_bytes(rows, R))
+    return fail(NTF_ERR_INVALID, "workspace too small");
+  NTF_CUDA_TRY(ntf::gram_launch(F, rows, R, G, static_cast<double*>(workspace),
+                                static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
+size_t ntf_sq_error_workspace_bytes(int64_t I, int64_t J, int64_t K) {
+  return ntf::sq_error_workspace_bytes(I, J, K, NTF_MAX_RANK);
+}
+
+int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, const double* A,
+                 const double* B, const double* C, int R, double* out2, void* workspace,
+                 size_t workspace_bytes, ntf_stream_t stream) {
+  if (!X || !out2 || !workspace) return fail(NTF_ERR_INVALID, "null pointer");
+  if (x_dtype != NTF_F32 && x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "bad dtype");
+  if (I < 1 || J < 1 || K < 1) return fail(NTF_ERR_INVALID, "bad shape");
+  if (A && (!B || !C || R < 1 || R > NTF_MAX_RANK)) return fail(NTF_ERR_INVALID, "bad model");
+  if (workspace_bytes < ntf::sq_error_workspace_bytes(I, J, K, A ? R : 0))
+    return fail(NTF_ERR_INVALID, "workspace too small");
+  NTF_CUDA_TRY(ntf::sq_error_launch(x_dtype, X, I, J, K, A, B, C, A ? R : 0, out2, workspace,
+                                    static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
+int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
+  if (!desc || !out) return fail(NTF_ERR_INVALID, "null pointer");
+  *out = nullptr;
+  const ntf_plan_desc& d = *desc;
+  const int R = d.rank;
+  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
+  if (d.inner_sweeps < 1) return fail(NTF_ERR_INVALID, "inner_sweeps must be >= 1");
+  if (!d.rho || !d.norm_acc || !d.counters || !d.resid_history || !d.rho_history)
+    return fail(NTF_ERR_INVALID, "null plan buffer");
+  for (int m = 0; m < 3; ++m) {
+    const int64_t* xd = d.x_dims[m];
+    int rc = check_dims(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R);
+    if (rc != NTF_OK) return rc;
+    if (!d.x_mode[m] || !d.factors[m] || !d.aux[m] || !d.duals[m] || !d.grams[m])
+      return fail(NTF_ERR_INVALID, "null state buffer");
+    if (xd[m] != d.row_count[m]) return fail(NTF_ERR_INVALID, "slab extent != owned row count");
+    if (d.row_offset[m] < 0 || d.row_offset[m] + d.row_count[m] > d.dims[m])
+      return fail(NTF_ERR_INVALID, "owned rows out of range");
+    for (int a = 0; a < 3; ++a)
+      if (a != m && xd[a] != d.dims[a]) return fail(NTF_ERR_INVALID, "slab companion extent");
+  }
+  if (d.engine == NTF_ENGINE_TCGEN05 && !ntf::mttkrp_tc_supported(d.x_dtype, R))
+    return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank");
+
+  ntf_plan* pl = new (std::nothrow) ntf_plan();
+  if (!pl) return fail(NTF_ERR_INVALID, "out of host memory");
+  pl->d = d;
+  size_t ws = 0;
+  int maxb = 1;
+  int64_t max_rows = 1;
+  for (int m = 0; m < 3; ++m) {
+    const int64_t* xd = d.x_dims[m];
+    pl->op[m] = make_op(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R, d.engine);
+    ws = std::max(ws, pl->op[m].ws_bytes(R));
+    pl->blocks[m] = ntf::factor_update_blocks(d.row_count[m]);
+    maxb = std::max(maxb, pl->blocks[m]);
+    max_rows = std::max(max_rows, d.dims[m]);
+  }
+  cudaError_t e = cudaSuccess;
+  auto cleanup = [&](int rc) {
+    ntf_plan_destroy(pl);
+    return rc;
+  };
+  if ((e = cudaMalloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
+  if ((e = cudaMalloc(&pl->norm_partials, sizeof(double) * 5 * maxb)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc norm"));
+  if ((e = cudaMalloc(&pl->gram_partials, sizeof(double) * R * R * maxb)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc gram"));
+  if ((e = cudaMalloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc gram ws"));
+  if ((e = cudaMalloc(&pl->done, sizeof(unsigned) * 4)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc counters"));
+  if ((e = cudaMemset(pl->done, 0, sizeof(unsigned) * 4)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMemset"));
+  if ((e = ntf::factor_update_prepare(R)) != cudaSuccess) return cleanup(cuda_fail(e, "prepare"));
+  for (int m = 0; m < 3; ++m) {
+    if (pl->op[m].tc) {
+      if ((e = ntf::mttkrp_tc_prepare(pl->op[m].tcl)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "tc prepare"));
+    }
+  }
+  *out = pl;
+  return NTF_OK;
+}
+
+int ntf_plan_sync_grams(ntf_plan* pl, ntf_stream_t stream) {
+  if (!pl) return fail(NTF_ERR_INVALID, "null plan");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int m = 0; m < 3; ++m)
+    NTF_CUDA_TRY(ntf::gram_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank, pl->d.grams[m],
+                                  pl->gram_ws, s));
+  return NTF_OK;
+}
+
+int ntf_plan_mode_update(ntf_plan* pl, int mode, int last_sweep, ntf_stream_t stream) {
+  if (!pl) return fail(NTF_ERR_INVALID, "null plan");
+  if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
+  return enqueue_mode_update(pl, mode, last_sweep ? 1 : 0, static_cast<cudaStream_t>(stream));
+}
+
+int ntf_plan_finalize(ntf_plan* pl, ntf_stream_t stream) {
+  if (!pl) return fail(NTF_ERR_INVALID, "null plan");
+  return enqueue_finalize(pl, static_cast<cudaStream_t>(stream));
+}
+
+int ntf_plan_run(ntf_plan* pl, int n_iters, int use_graph, ntf_stream_t stream) {
+  if (!pl) return fail(NTF_ERR_INVALID, "null plan");
+  if (n_iters < 0) return fail(NTF_ERR_INVALID, "n_iters < 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!use_graph) {
+    for (int i = 0; i < n_iters; ++i) {
+      const int rc = enqueue_iteration(pl, s);
+      if (rc != NTF_OK) return rc;
+    }
+    return NTF_OK;
+  }
+  if (!pl->graph) {
+    if (!pl->capture_stream)
+      NTF_CUDA_TRY(cudaStreamCreateWithFlags(&pl->capture_stream, cudaStreamNonBlocking));
+    NTF_CUDA_TRY(cudaStreamBeginCapture(pl->capture_stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue_iteration(pl, pl->capture_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(pl->capture_stream, &g);
+    if (rc != NTF_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&pl->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  }
+  for (int i = 0; i < n_iters; ++i) NTF_CUDA_TRY(cudaGraphLaunch(pl->graph, s));
+  return NTF_OK;
+}
+
+static void free_events(ntf_plan* pl) {
+  if (pl->events) {
+    for (int i = 0; i < pl->n_events; ++i) cudaEventDestroy(pl->events[i]);
+    delete[] pl->events;
+  }
+  pl->events = nullptr;
+  pl->n_events = 0;
+  pl->cursor = 0;
+}
+
+int ntf_plan_set_timing(ntf_plan* pl, int enable) {
+  if (!pl) return fail(NTF_ERR_INVALID, "null plan");
+  if (pl->graph) {
+    cudaGraphExecDestroy(pl->graph);
+    pl->graph = nullptr;
+  }
+  free_events(pl);
+  pl->timing = enable ? 1 : 0;
+  if (!enable) return NTF_OK;
+  const int n = 3 * 3 * pl->d.inner_sweeps;
+  pl->events = new (std::nothrow) cudaEvent_t[n];
+  if (!pl->events) return fail(NTF_ERR_INVALID, "out of host memory");
+  for (int i = 0; i < n; ++i) {
+    cudaError_t e = cudaEventCreate(&pl->events[i]);
+    if (e != cudaSuccess) {
+      pl->n_events = i;
+      free_events(pl);
+      return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  pl->n_events = n;
+  return NTF_OK;
+}
+
+int ntf_plan_kernel_times(ntf_plan* pl, float* ms_out, int capacity) {
+  if (!pl || !ms_out) return -fail(NTF_ERR_INVALID, "null pointer");
+  if (!pl->timing || !pl->events) return -fail(NTF_ERR_INVALID, "timing not enabled");
+  const int nupd = pl->n_events / 3;
+  if (capacity < 2 * nupd) return -fail(NTF_ERR_INVALID, "capacity too small");
+  cudaError_t e = cudaEventSynchronize(pl->events[pl->n_events - 1]);
+  if (e != cudaSuccess) return -cuda_fail(e, "cudaEventSynchronize");
+  for (int u = 0; u < nupd; ++u) {
+    float a = 0.f, b = 0.f;
+    e = cudaEventElapsedTime(&a, pl->events[3 * u], pl->events[3 * u + 1]);
+    if (e != cudaSuccess) return -cuda_fail(e, "cudaEventElapsedTime");
+    e = cudaEventElapsedTime(&b, pl->events[3 * u + 1], pl->events[3 * u + 2]);
+    if (e != cudaSuccess) return -cuda_fail(e, "cudaEventElapsedTime");
+    ms_out[2 * u] = a;
+    ms_out[2 * u + 1] = b;
+  }
+  return 2 * nupd;
+}
+
+void ntf_plan_destroy(ntf_plan* pl) {
+  if (!pl) return;
+  free_events(pl);
+  if (pl->graph) cudaGraphExecDestroy(pl->graph);
+  if (pl->capture_stream) cudaStreamDestroy(pl->capture_stream);
+  cudaFree(pl->mtt_ws);
+  cudaFree(pl->norm_partials);
+  cudaFree(pl->gram_partials);
+  cudaFree(pl->gram_ws);
+  cudaFree(pl->done);
+  delete pl;
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// Declarations for the per-mode update / Gram / finalize / norm kernels.
+#pragma once
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ntf {
+
+struct FactorUpdateParams {
+  int mode;                 // 1..3
+  int R;
+  int64_t rows;             // owned rows
+  int64_t row_offset;       // first owned row within the full factor
+  const double* mtt;        // [splits][rows][R] MTTKRP partials
+  int splits;
+  const double* Ga;         // companion Grams (highest mode first)
+  const double* Gb;
+  const double* rho;        // device [3]
+  double* F;                // full factor (rows written at row_offset)
+  double* aux;              // owned rows
+  double* dual;             // owned rows
+  int last_sweep;
+  int fuse_gram;
+  double* norm_partials;    // [blocks][5]
+  double* gram_partials;    // [blocks][R][R]
+  double* G_out;            // R x R (fuse_gram)
+  double* norm_acc;         // [5] this mode
+  unsigned* done_counter;
+  int* status;
+  const int* stop_flag;
+};
+
+struct FinalizeParams {
+  const double* norm_acc;   // [3][5]
+  double* rho;              // [3] in/out
+  int64_t dims[3];
+  int R;
+  double eps_abs, eps_rel, mu, tau_incr, tau_decr;
+  int adapt;
+  int64_t history_capacity;
+  double* resid_history;    // [cap][6]
+  double* rho_history;      // [cap][3]
+  int* counters;            // [0] iteration, [1] stop flag
+};
+
+int factor_update_blocks(int64_t rows);
+size_t factor_update_smem(int R);
+cudaError_t factor_update_prepare(int R);
+cudaError_t factor_update_launch(const FactorUpdateParams& p, cudaStream_t stream);
+
+size_t gram_workspace_bytes(int64_t rows, int R);
+cudaError_t gram_launch(const double* F, int64_t rows, int R, double* G, double* ws,
+                        cudaStream_t stream);
+
+cudaError_t finalize_launch(const FinalizeParams& p, cudaStream_t stream);
+
+size_t sq_error_workspace_bytes(int64_t I, int64_t J, int64_t K, int R);
+cudaError_t sq_error_launch(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
+                            const double* A, const double* B, const double* C, int R, double* out2,
+                            void* ws, cudaStream_t stream);
+
+}  // namespace ntf

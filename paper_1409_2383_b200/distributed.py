@@ -1,0 +1,238 @@
+"""Sharded multi-GPU fit: one process per GPU, NCCL over NVLink.
+
+Follows the paper's block-row partitioning (§V, reference
+blocks.py:171-196 and the mesh data flow mesh.py:149-237) re-cast for GPUs
+(SURVEY 8(e)): rank p owns factor rows ``PartitionPlan.uniform(dims, P)``
+(blocks.py:47-61) and holds the three slabs X[I_p,:,:], X[:,J_p,:],
+X[:,:,K_p].  A mode-n update is then entirely local (MTTKRP of the owned rows
+from the local slab, the shared ridge Cholesky, the row solves and the fused
+aux/dual step); the one exchange per mode update is an all-gather of the
+updated row block, after which every rank recomputes the same Gram locally.
+Once per outer iteration the 15 residual sums of squares are all-reduced so
+the stop test and the penalty adaptation are replicated bit-identically.
+
+``sharded_iteration`` is written against a small problem interface so the
+collective logic can be exercised on CPU with the gloo backend
+(tests/test_distributed_gloo.py) as well as on GPUs with NCCL.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from .constraints import normalize_specs
+from .solver import FitResult, SolverConfig, _engine_code, _run_fit
+from .tensors import as_dense
+
+
+@dataclass(frozen=True)
+class PartitionPlan:
+    """Per-mode row extents (reference blocks.PartitionPlan, blocks.py:36-61)."""
+
+    extents: tuple
+
+    @classmethod
+    def uniform(cls, dims: Sequence[int], blocks: int | Sequence[int]) -> "PartitionPlan":
+        if isinstance(blocks, int):
+            blocks = [blocks] * len(dims)
+        if len(blocks) != len(dims):
+            raise ValueError("need one block count per mode")
+        ext = []
+        for d, n in zip(dims, blocks):
+            if not 1 <= n <= d:
+                raise ValueError(f"block count {n} invalid for extent {d}")
+            base, extra = divmod(int(d), int(n))
+            ext.append(tuple(base + (1 if i < extra else 0) for i in range(n)))
+        return cls(tuple(ext))
+
+    @property
+    def dims(self) -> tuple:
+        return tuple(sum(e) for e in self.extents)
+
+    @property
+    def counts(self) -> tuple:
+        return tuple(len(e) for e in self.extents)
+
+    def offsets(self, mode: int) -> list:
+        out = [0]
+        for e in self.extents[mode - 1]:
+            out.append(out[-1] + e)
+        return out
+
+    def row_slice(self, mode: int, block: int) -> slice:
+        o = self.offsets(mode)
+        return slice(o[block], o[block + 1])
+
+
+class Comm:
+    """torch.distributed collectives used by the sharded iteration."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def all_reduce_(self, t) -> None:
+        self.dist.all_reduce(t, group=self.group)
+
+    def gather_rows(self, full, offsets: Sequence[int], counts: Sequence[int]) -> None:
+        """In place: every rank's owned block of ``full`` (rows offsets[p] ..
+        +counts[p]) is broadcast to all ranks.  Blocks are padded to the
+        largest count because the uniform plan is uneven."""
+        import torch
+
+        maxc = max(counts)
+        p = self.rank
+        send = full.new_zeros((maxc,) + tuple(full.shape[1:]))
+        send[: counts[p]].copy_(full[offsets[p]: offsets[p] + counts[p]])
+        recv = full.new_empty((self.size * maxc,) + tuple(full.shape[1:]))
+        self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        for q in range(self.size):
+            if q == p:
+                continue
+            full[offsets[q]: offsets[q] + counts[q]].copy_(recv[q * maxc: q * maxc + counts[q]])
+        del torch
+
+
+def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
+    """One outer iteration of the sharded solver (reference solver.py:295-327
+    semantics; mesh.py:149-237 data flow).  ``prob`` provides mode_update,
+    refresh_gram, finalize, factors, norm_acc, offsets/counts."""
+    sweeps = config.inner_sweeps
+    for sw in range(sweeps):
+        for mode in (1, 2, 3):
+            m = mode - 1
+            prob.mode_update(mode, sw == sweeps - 1)
+            comm.gather_rows(prob.factors[m], prob.offsets[m], prob.counts[m])
+            prob.refresh_gram(m)
+    comm.all_reduce_(prob.norm_acc)
+    prob.finalize()
+
+
+def _sharded_problem_class():
+    from .engine import DeviceProblem, Slabs, gram_device, mttkrp_device, sq_error
+
+    class ShardedProblem(DeviceProblem):
+        def __init__(self, x_slabs, dims, rank, config, cap, engine, plan: PartitionPlan, comm: Comm):
+            p = comm.rank
+            self.comm = comm
+            self.plan = plan
+            self.offsets = [plan.offsets(m + 1)[:-1] for m in range(3)]
+            self.counts = [list(plan.extents[m]) for m in range(3)]
+            own_off = tuple(self.offsets[m][p] for m in range(3))
+            own_cnt = tuple(self.counts[m][p] for m in range(3))
+            super().__init__(x_slabs[0], dims, rank, config, cap, engine,
+                             slabs=Slabs(list(x_slabs), own_off, own_cnt))
+
+        def step(self) -> None:
+            torch = self.torch
+            with torch.cuda.stream(self.stream):
+                sharded_iteration(self, self.comm, self.config)
+
+        def final_sq_error(self, aux):
+            torch = self.torch
+            p = self.comm.rank
+            rows = self.plan.row_slice(1, p)
+            with torch.cuda.stream(self.stream):
+                own = [aux[0][rows], aux[1], aux[2]]
+                out = sq_error(self.slabs.x_mode[0], own, stream=self.stream)
+                self.comm.all_reduce_(out)
+                return float(out[0].item()), float(out[1].item())
+
+        def aux_model_rfe(self, x_norm: float) -> float:
+            torch = self.torch
+            p = self.comm.rank
+            with torch.cuda.stream(self.stream):
+                full = [torch.zeros_like(f) for f in self.factors]
+                for m in range(3):
+                    o, c = self.offsets[m][p], self.counts[m][p]
+                    full[m][o:o + c].copy_(self.aux[m])
+                    self.comm.gather_rows(full[m], self.offsets[m], self.counts[m])
+                own = full[0][self.plan.row_slice(1, p)]
+                mt = mttkrp_device(self.slabs.x_mode[0], [own, full[1], full[2]], 1,
+                                   self._desc.engine, stream=self.stream)
+                g = gram_device(full[2], stream=self.stream) * gram_device(full[1], stream=self.stream)
+                part = torch.stack([torch.sum(own * mt), torch.sum((own.T @ own) * g)])
+                self.comm.all_reduce_(part)
+                cross, quad = (float(v) for v in part.cpu())
+            sq = x_norm ** 2 - 2.0 * cross + quad
+            return math.sqrt(max(sq, 0.0)) / x_norm
+
+        def gather_state(self, aux, duals):
+            torch = self.torch
+            p = self.comm.rank
+            out_a, out_y = [], []
+            for m in range(3):
+                o, c = self.offsets[m][p], self.counts[m][p]
+                full_a = torch.zeros((self.dims[m], self.R), dtype=torch.float64, device=self.device)
+                full_y = torch.zeros_like(full_a)
+                full_a[o:o + c].copy_(torch.from_numpy(aux[m]))
+                full_y[o:o + c].copy_(torch.from_numpy(duals[m]))
+                self.comm.gather_rows(full_a, self.offsets[m], self.counts[m])
+                self.comm.gather_rows(full_y, self.offsets[m], self.counts[m])
+                out_a.append(full_a.cpu().numpy())
+                out_y.append(full_y.cpu().numpy())
+            return out_a, out_y
+
+    return ShardedProblem
+
+
+def make_slabs(values, plan: PartitionPlan, rank_id: int, device):
+    """This rank's three slabs of a host tensor, uploaded to ``device``."""
+    import torch
+
+    x = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values))
+    s1 = x[plan.row_slice(1, rank_id)]
+    s2 = x[:, plan.row_slice(2, rank_id)]
+    s3 = x[:, :, plan.row_slice(3, rank_id)]
+    return [s.contiguous().to(device) for s in (s1, s2, s3)]
+
+
+def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None,
+                    plan: PartitionPlan | int | None = None, trace_path: str | None = None,
+                    *, engine=None, group=None) -> FitResult:
+    """Block-parallel fit over the ranks of ``torch.distributed`` (reference
+    mesh.distributed_fit, mesh.py:331-350).  Without an initialised process
+    group (or with one rank) this is exactly ``fit``.  ``trace_path`` (the
+    simulator's message trace) has no NCCL equivalent and is ignored."""
+    import torch
+    import torch.distributed as dist
+
+    from .solver import fit
+
+    config = config or SolverConfig()
+    t = as_dense(t)
+    normalize_specs(specs, t.order)
+    if rank < 1:
+        raise ValueError("rank must be >= 1")
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return fit(t, rank, specs, config, engine=engine)
+    comm = Comm(group)
+    if plan is None or isinstance(plan, int):
+        plan = PartitionPlan.uniform(t.dims, comm.size)
+    if plan.dims != t.dims or set(plan.counts) != {comm.size}:
+        raise ValueError("partition plan must give every mode one block per rank")
+    device = torch.device("cuda", torch.cuda.current_device())
+    vals = t.values
+    slabs = make_slabs(vals, plan, comm.rank, device)
+    # ||X||^2 from the mode-1 slabs
+    from .engine import sq_error
+
+    sq = sq_error(slabs[0])
+    comm.all_reduce_(sq)
+    x_norm = math.sqrt(float(sq[0].item()))
+    if x_norm == 0.0:
+        raise ValueError("cannot factorize a zero tensor")
+    cls = _sharded_problem_class()
+    prob = cls(slabs, t.dims, rank, config, config.n_max, _engine_code(engine), plan, comm)
+    try:
+        return _run_fit(prob, slabs[0], t.dims, rank, config, x_norm, gather=prob.gather_state)
+    finally:
+        prob.close()

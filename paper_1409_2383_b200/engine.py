@@ -1,0 +1,329 @@
+"""Device-resident solver state and the C-ABI plan that drives it.
+
+``DeviceProblem`` owns (through torch's caching allocator) the HBM copy of the
+tensor, the per-mode state (factors, aux, duals, Grams, penalties) and the
+per-iteration history buffers, and wraps one ``ntf_plan`` (include/ntf_b200.h)
+that enqueues outer iterations on a dedicated CUDA stream.  The host never
+synchronises inside a run; histories are copied back once.
+
+HBM layout (row-major, fp64 unless noted):
+  X                  I*J*K   fp32 or fp64 (the tensor is read, never copied)
+  factors[m]         I_m x R   working factors (replicated across ranks)
+  aux[m], duals[m]   I_m x R   (owned rows only when sharded)
+  grams[m]           R x R     F_m^T F_m, refreshed by each mode update
+  rho[3], norm_acc[15], counters int32[4]
+  resid_history      cap x 6,  rho_history cap x 3
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover
+        raise N.NativeUnavailable("torch is required for device memory") from exc
+    if not torch.cuda.is_available():
+        raise N.NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
+    return torch
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def device_tensor(t, device=None):
+    """Return the HBM copy of DenseTensor ``t`` (uploaded once and cached on it;
+    pinned host buffers upload asynchronously)."""
+    torch = _torch()
+    dev = torch.device(device or "cuda")
+    vals = t.values
+    cache = getattr(t, "_device_cache", None)
+    if cache is not None and cache.device == dev:
+        return cache
+    if isinstance(vals, np.ndarray):
+        host = torch.from_numpy(np.ascontiguousarray(vals))
+        x = host.to(dev)
+    else:
+        x = vals.to(dev, non_blocking=bool(vals.is_pinned()) if vals.device.type == "cpu" else False)
+    x = x.contiguous()
+    try:
+        t._device_cache = x
+    except AttributeError:
+        pass
+    return x
+
+
+def dtype_code(x) -> int:
+    torch = _torch()
+    if x.dtype == torch.float32:
+        return N.NTF_F32
+    if x.dtype == torch.float64:
+        return N.NTF_F64
+    raise ValueError("tensor must be float32 or float64")
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def sq_error(x, factors=None, stream=None):
+    """(sum x^2, sum (x - [[A,B,C]])^2) on the device, fp64 accumulation."""
+    torch = _torch()
+    lib = N.load()
+    I, J, K = (int(d) for d in x.shape)
+    ws_bytes = lib.ntf_sq_error_workspace_bytes(I, J, K)
+    ws = torch.empty(max(1, ws_bytes // 8 + 1), dtype=torch.float64, device=x.device)
+    out = torch.zeros(2, dtype=torch.float64, device=x.device)
+    s = stream or torch.cuda.current_stream(x.device)
+    if factors is None:
+        a = b = c = None
+        R = 0
+    else:
+        f = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).to(x.device)
+             if isinstance(v, np.ndarray) else v.contiguous() for v in factors]
+        a, b, c = (_ptr(v) for v in f)
+        R = int(f[0].shape[1])
+    N.check(lib.ntf_sq_error(dtype_code(x), _ptr(x), I, J, K, a, b, c, R, _ptr(out), _ptr(ws),
+                             ws.numel() * 8, _stream_handle(s)))
+    return out
+
+
+def tensor_norm(t) -> float:
+    x = device_tensor(t)
+    return float(np.sqrt(sq_error(x)[0].item()))
+
+
+def mttkrp_device(x, factors, mode: int, engine: int = N.ENGINE_AUTO, stream=None):
+    """Dense MTTKRP of the device tensor ``x`` with device fp64 factors."""
+    torch = _torch()
+    lib = N.load()
+    I, J, K = (int(d) for d in x.shape)
+    R = int(factors[0].shape[1])
+    code = dtype_code(x)
+    wsb = lib.ntf_mttkrp_workspace_bytes(mode, code, I, J, K, R, engine)
+    if wsb == 0:
+        N.check(N.NTF_ERR_INVALID)
+    ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=x.device)
+    M = (I, J, K)[mode - 1]
+    out = torch.empty((M, R), dtype=torch.float64, device=x.device)
+    s = stream or torch.cuda.current_stream(x.device)
+    a, b, c = (_ptr(f) for f in factors)
+    N.check(lib.ntf_mttkrp(mode, code, _ptr(x), I, J, K, a, b, c, R, _ptr(out), _ptr(ws),
+                           ws.numel() * 8, engine, _stream_handle(s)))
+    return out
+
+
+def gram_device(F, stream=None):
+    torch = _torch()
+    lib = N.load()
+    rows, R = (int(d) for d in F.shape)
+    wsb = lib.ntf_gram_workspace_bytes(rows, R)
+    ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=F.device)
+    G = torch.empty((R, R), dtype=torch.float64, device=F.device)
+    s = stream or torch.cuda.current_stream(F.device)
+    N.check(lib.ntf_gram(_ptr(F), rows, R, _ptr(G), _ptr(ws), ws.numel() * 8, _stream_handle(s)))
+    return G
+
+
+@dataclass
+class Slabs:
+    """This rank's view of the tensor for each mode."""
+
+    x_mode: list            # 3 device tensors
+    row_offset: tuple
+    row_count: tuple
+
+
+class DeviceProblem:
+    """HBM state of one fit and its C-ABI plan."""
+
+    def __init__(self, x, dims, rank: int, config, history_capacity: int, engine: int = N.ENGINE_AUTO,
+                 slabs: Slabs | None = None, stream=None):
+        torch = _torch()
+        self.torch = torch
+        self.lib = N.load()
+        self.device = x.device
+        self.dims = tuple(int(d) for d in dims)
+        self.R = int(rank)
+        self.config = config
+        self.x = x
+        self.stream = stream or torch.cuda.Stream(device=self.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        self.sharded = slabs is not None
+        if slabs is None:
+            slabs = Slabs([x, x, x], (0, 0, 0), self.dims)
+        self.slabs = slabs
+        dev, f64 = self.device, torch.float64
+        R = self.R
+        with torch.cuda.stream(self.stream):
+            self.factors = [torch.zeros((d, R), dtype=f64, device=dev) for d in self.dims]
+            self.aux = [torch.zeros((c, R), dtype=f64, device=dev) for c in slabs.row_count]
+            self.duals = [torch.zeros((c, R), dtype=f64, device=dev) for c in slabs.row_count]
+            self.grams = [torch.zeros((R, R), dtype=f64, device=dev) for _ in range(3)]
+            self.rho = torch.zeros(3, dtype=f64, device=dev)
+            self.norm_acc = torch.zeros(15, dtype=f64, device=dev)
+            cap = max(1, int(history_capacity))
+            self.cap = cap
+            self.resid_hist = torch.zeros((cap, 6), dtype=f64, device=dev)
+            self.rho_hist = torch.zeros((cap, 3), dtype=f64, device=dev)
+            self.counters = torch.zeros(4, dtype=torch.int32, device=dev)
+        d = N.PlanDesc()
+        d.x_dtype = dtype_code(x)
+        for m in range(3):
+            xs = slabs.x_mode[m]
+            d.x_mode[m] = _ptr(xs)
+            for a in range(3):
+                d.x_dims[m][a] = int(xs.shape[a])
+            d.dims[m] = self.dims[m]
+            d.row_offset[m] = int(slabs.row_offset[m])
+            d.row_count[m] = int(slabs.row_count[m])
+            d.factors[m] = _ptr(self.factors[m])
+            d.aux[m] = _ptr(self.aux[m])
+            d.duals[m] = _ptr(self.duals[m])
+            d.grams[m] = _ptr(self.grams[m])
+        d.rank = R
+        d.engine = int(engine)
+        d.fuse_gram = 0 if self.sharded else 1
+        d.eps_abs = float(config.eps_abs)
+        d.eps_rel = float(config.eps_rel)
+        d.mu = float(config.mu)
+        d.tau_incr = float(config.tau_incr)
+        d.tau_decr = float(config.tau_decr)
+        d.inner_sweeps = int(config.inner_sweeps)
+        d.adapt = 1 if config.adapt else 0
+        d.rho = _ptr(self.rho)
+        d.norm_acc = _ptr(self.norm_acc)
+        d.history_capacity = cap
+        d.resid_history = _ptr(self.resid_hist)
+        d.rho_history = _ptr(self.rho_hist)
+        d.counters = _ptr(self.counters)
+        self._desc = d
+        handle = ctypes.c_void_p()
+        N.check(self.lib.ntf_plan_create(ctypes.byref(d), ctypes.byref(handle)))
+        self._plan = handle
+        self._sh = _stream_handle(self.stream)
+
+    # -- state transfer ------------------------------------------------------
+    def load_state(self, factors, aux, duals, rho) -> None:
+        """Host (numpy) state -> HBM, counters reset, Grams refreshed."""
+        torch = self.torch
+        off, cnt = self.slabs.row_offset, self.slabs.row_count
+        with torch.cuda.stream(self.stream):
+            for m in range(3):
+                self.factors[m].copy_(torch.from_numpy(np.ascontiguousarray(factors[m], dtype=np.float64)))
+                a = np.ascontiguousarray(aux[m], dtype=np.float64)
+                y = np.ascontiguousarray(duals[m], dtype=np.float64)
+                if a.shape[0] != cnt[m]:
+                    a = a[off[m]:off[m] + cnt[m]]
+                    y = y[off[m]:off[m] + cnt[m]]
+                self.aux[m].copy_(torch.from_numpy(np.ascontiguousarray(a)))
+                self.duals[m].copy_(torch.from_numpy(np.ascontiguousarray(y)))
+            self.rho.copy_(torch.tensor([float(r) for r in rho], dtype=torch.float64))
+            self.counters.zero_()
+            self.norm_acc.zero_()
+        N.check(self.lib.ntf_plan_sync_grams(self._plan, self._sh))
+
+    def run(self, n_iters: int, use_graph: bool = True) -> None:
+        N.check(self.lib.ntf_plan_run(self._plan, int(n_iters), 1 if use_graph else 0, self._sh))
+
+    def set_timing(self, enable: bool) -> None:
+        N.check(self.lib.ntf_plan_set_timing(self._plan, 1 if enable else 0))
+
+    def kernel_times(self) -> np.ndarray:
+        """[n_mode_updates][2] ms (MTTKRP, row update) of the latest iteration."""
+        n = 2 * 3 * int(self.config.inner_sweeps)
+        buf = (ctypes.c_float * n)()
+        got = self.lib.ntf_plan_kernel_times(self._plan, buf, n)
+        if got < 0:
+            N.check(-got)
+        return np.array(buf[:got], dtype=np.float64).reshape(-1, 2)
+
+    def step(self) -> None:
+        """One outer iteration (graph replay)."""
+        self.run(1)
+
+    def final_sq_error(self, aux):
+        """(sum x^2, sum (x - [[aux]])^2) over the whole tensor, on the device."""
+        with self.torch.cuda.stream(self.stream):
+            out = sq_error(self.x, aux, stream=self.stream)
+            return float(out[0].item()), float(out[1].item())
+
+    def aux_model_rfe(self, x_norm: float) -> float:
+        """Gram-identity RFE of the auxiliary model (reference solver.aux_model_rfe,
+        solver.py:330-337): ||X||^2 - 2<A, MTTKRP_1(aux)> + <A^T A, G_23>."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            aux = self.aux
+            m = mttkrp_device(self.x, aux, 1, self._desc.engine, stream=self.stream)
+            g = gram_device(aux[2], stream=self.stream) * gram_device(aux[1], stream=self.stream)
+            ga = gram_device(aux[0], stream=self.stream)
+            cross = float(torch.sum(aux[0] * m).item())
+            quad = float(torch.sum(ga * g).item())
+        sq = x_norm ** 2 - 2.0 * cross + quad
+        return float(np.sqrt(max(sq, 0.0))) / x_norm
+
+    def mode_update(self, mode: int, last_sweep: bool) -> None:
+        N.check(self.lib.ntf_plan_mode_update(self._plan, mode, 1 if last_sweep else 0, self._sh))
+
+    def finalize(self) -> None:
+        N.check(self.lib.ntf_plan_finalize(self._plan, self._sh))
+
+    def refresh_gram(self, m: int) -> None:
+        lib = self.lib
+        rows = self.dims[m]
+        torch = self.torch
+        wsb = lib.ntf_gram_workspace_bytes(rows, self.R)
+        if not hasattr(self, "_gram_ws") or self._gram_ws.numel() * 8 < wsb:
+            with torch.cuda.stream(self.stream):
+                self._gram_ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=self.device)
+        N.check(lib.ntf_gram(_ptr(self.factors[m]), rows, self.R, _ptr(self.grams[m]),
+                             _ptr(self._gram_ws), self._gram_ws.numel() * 8, self._sh))
+
+    def counters_host(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.counters.cpu().numpy()
+
+    def check_status(self) -> tuple[int, bool]:
+        """(iterations done, stopped); raises on device-side numerical failure."""
+        c = self.counters_host()
+        if c[2] == 1:
+            from .solver import InvalidPenaltyError
+
+            raise InvalidPenaltyError("ridge system not positive definite")
+        if c[2] == 2:
+            raise ValueError("cannot project a matrix with non-finite entries")
+        return int(c[0]), bool(c[1])
+
+    def histories(self, n: int):
+        self.stream.synchronize()
+        n = min(n, self.cap)
+        return self.resid_hist[:n].cpu().numpy(), self.rho_hist[:n].cpu().numpy()
+
+    def read_factors(self) -> list[np.ndarray]:
+        self.stream.synchronize()
+        return [f.cpu().numpy() for f in self.factors]
+
+    def read_state(self):
+        self.stream.synchronize()
+        return ([f.cpu().numpy() for f in self.factors], [a.cpu().numpy() for a in self.aux],
+                [y.cpu().numpy() for y in self.duals], [float(r) for r in self.rho.cpu().numpy()])
+
+    def close(self) -> None:
+        if getattr(self, "_plan", None):
+            self.stream.synchronize()
+            self.lib.ntf_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,277 @@
+"""Drop-in ``fit`` for the reference ADMoM NTF solver, running on a B200.
+
+Mirrors the reference module ``cpadmm.solver`` (reference solver.py): same
+types (``SolverConfig``, ``SolverState``, ``Residuals``, ``FitResult``,
+``InvalidPenaltyError``), same seeds, same restart loop and the same
+``fit(t, rank, specs=None, config=None) -> FitResult`` signature
+(solver.py:340-345).  The outer iterations run on the device through the
+C-ABI plan (engine.py / include/ntf_b200.h); the host only seeds the state,
+reads the counters and copies the histories back.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .constraints import ConstraintSpec, normalize_specs
+from .tensors import DenseTensor, KruskalModel, as_dense
+
+
+class InvalidPenaltyError(RuntimeError):
+    """Ridge system not positive definite (reference solver.py:31-32)."""
+
+
+@dataclass
+class SolverConfig:
+    """Reference SolverConfig (solver.py:35-61): same fields and checks."""
+
+    eps_abs: float = 1e-4
+    eps_rel: float = 1e-4
+    rho_init: float = 1.0
+    mu: float = 8.0
+    tau_incr: float = 4.0
+    tau_decr: float = 2.0
+    n_max: int = 400
+    max_restarts: int = 10
+    inner_sweeps: int = 1
+    seed: int = 0
+    adapt: bool = True
+    track_rfe: bool = False
+    track_factors: bool = False
+
+    def __post_init__(self):
+        if self.eps_abs < 0 or self.eps_rel < 0:
+            raise ValueError("stopping tolerances must be >= 0")
+        if self.rho_init <= 0:
+            raise ValueError("rho_init must be positive")
+        if min(self.mu, self.tau_incr, self.tau_decr) <= 1:
+            raise ValueError("adaptation parameters mu, tau_incr, tau_decr must be > 1")
+        if self.n_max < 1 or self.inner_sweeps < 1 or self.max_restarts < 0:
+            raise ValueError("n_max, inner_sweeps must be >= 1 and max_restarts >= 0")
+
+
+@dataclass
+class SolverState:
+    """Reference SolverState (solver.py:64-78), host numpy arrays."""
+
+    factors: list
+    aux: list
+    duals: list
+    rho: list
+    iteration: int = 0
+
+    @property
+    def order(self) -> int:
+        return len(self.factors)
+
+    @property
+    def dims(self) -> tuple[int, ...]:
+        return tuple(f.shape[0] for f in self.factors)
+
+
+@dataclass(frozen=True)
+class Residuals:
+    """Primal/dual residual norms per mode (solver.py:81-86)."""
+
+    primal: tuple
+    dual: tuple
+
+
+@dataclass
+class FitResult:
+    """Reference FitResult (solver.py:89-99)."""
+
+    model: KruskalModel
+    rfe: float
+    iterations: int
+    restarts: int
+    converged: bool
+    residual_history: list = field(default_factory=list)
+    rfe_history: list = field(default_factory=list)
+    factor_history: list | None = None
+    state: SolverState | None = None
+    rho_history: list = field(default_factory=list)
+
+
+# -- seeds (solver.py:122-151): numpy PCG64 streams, bit-identical starts ----
+
+def derive_seed(base: int, *key: int) -> int:
+    ss = np.random.SeedSequence((int(base),) + tuple(int(k) for k in key))
+    return int(ss.generate_state(1, np.uint64)[0])
+
+
+def attempt_entropy(seed: int, attempt: int):
+    return int(seed) if attempt == 0 else derive_seed(seed, attempt)
+
+
+def init_factors(dims: Sequence[int], rank: int, entropy) -> list[np.ndarray]:
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy)))
+    out = [np.zeros((int(dims[0]), rank))]
+    for d in dims[1:]:
+        out.append(rng.random((int(d), rank)))
+    return out
+
+
+def init_state(dims: Sequence[int], rank: int, config: SolverConfig, attempt: int = 0) -> SolverState:
+    if rank < 1:
+        raise ValueError("rank must be >= 1")
+    f = init_factors(dims, rank, attempt_entropy(config.seed, attempt))
+    return SolverState(f, [np.zeros_like(x) for x in f], [np.zeros_like(x) for x in f],
+                       [config.rho_init] * len(f))
+
+
+# -- device helpers -----------------------------------------------------------
+
+_ENGINE = {"auto": N.ENGINE_AUTO, "cuda_core": N.ENGINE_CUDA_CORE, "tcgen05": N.ENGINE_TCGEN05}
+
+
+def _engine_code(engine) -> int:
+    if engine is None:
+        import os
+
+        engine = os.environ.get("NTF_B200_ENGINE", "auto")
+    if isinstance(engine, int):
+        return engine
+    return _ENGINE[str(engine)]
+
+
+def mttkrp_factors(t, factors: Sequence[np.ndarray], mode: int, engine=None) -> np.ndarray:
+    """Device MTTKRP (replaces tensors.mttkrp_factors, tensors.py:254-262)."""
+    from .engine import _torch, device_tensor, mttkrp_device
+
+    torch = _torch()
+    t = as_dense(t)
+    if not 1 <= mode <= 3:
+        raise ValueError(f"mode must be in 1..3, got {mode}")
+    x = device_tensor(t)
+    f = [torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(x.device) for v in factors]
+    for m, v in enumerate(f):
+        if v.shape[0] != t.dims[m]:
+            raise ValueError("factor dims do not match tensor dims")
+    out = mttkrp_device(x, f, mode, _engine_code(engine))
+    torch.cuda.current_stream(x.device).synchronize()
+    return out.cpu().numpy()
+
+
+def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = None,
+        config: SolverConfig | None = None, *, engine=None, device=None) -> FitResult:
+    """Constrained (non-negative) CP fit with restarts (reference solver.py:340-403).
+
+    Same semantics as the reference: per outer iteration ``inner_sweeps``
+    Gauss-Seidel sweeps of the ridge update over modes 1..3, then the aux
+    projection, dual ascent, residuals, adaptation and the stop test; restarts
+    from fresh seeds on non-convergence; the model is the auxiliary copies and
+    ``rfe`` is computed by explicit reconstruction (fp64 accumulation).
+    """
+    from .engine import DeviceProblem, device_tensor, sq_error
+
+    config = config or SolverConfig()
+    t = as_dense(t)
+    specs = normalize_specs(specs, t.order)
+    if rank < 1:
+        raise ValueError("rank must be >= 1")
+    x = device_tensor(t, device)
+    x_norm = math.sqrt(float(sq_error(x)[0].item()))
+    if x_norm == 0.0:
+        raise ValueError("cannot factorize a zero tensor")
+    prob = DeviceProblem(x, t.dims, rank, config, history_capacity=config.n_max,
+                         engine=_engine_code(engine))
+    try:
+        return _run_fit(prob, x, t.dims, rank, config, x_norm)
+    finally:
+        prob.close()
+
+
+def _run_fit(prob, x, dims, rank: int, config: SolverConfig, x_norm: float,
+             gather=None) -> FitResult:
+    """Restart loop shared by ``fit`` and ``distributed_fit``.  ``gather``
+    (sharded runs) returns the full aux/dual matrices from the owned rows."""
+    per_iter_host = config.track_factors or config.track_rfe or gather is not None
+    stoppable = config.eps_abs > 0 or config.eps_rel > 0
+    total = 0
+    converged = False
+    attempt = 0
+    res_hist: list = []
+    rfe_hist: list = []
+    fac_hist: list = []
+    rho_hist: list = []
+    for attempt in range(config.max_restarts + 1):
+        st = init_state(dims, rank, config, attempt)
+        prob.load_state(st.factors, st.aux, st.duals, st.rho)
+        res_hist, rfe_hist, fac_hist = [], [], []
+        done = 0
+        stopped = False
+        if per_iter_host:
+            while done < config.n_max and not stopped:
+                prob.step()
+                done, stopped = prob.check_status()
+                if config.track_factors:
+                    fac_hist.append(prob.read_factors())
+                if config.track_rfe:
+                    rfe_hist.append(prob.aux_model_rfe(x_norm))
+        else:
+            chunk = 16 if stoppable else config.n_max
+            while done < config.n_max and not stopped:
+                n = min(chunk, config.n_max - done)
+                prob.run(n)
+                done, stopped = prob.check_status()
+        total += done
+        r, rh = prob.histories(done)
+        res_hist = [Residuals(tuple(float(v) for v in row[:3]), tuple(float(v) for v in row[3:]))
+                    for row in r]
+        rho_hist = [list(map(float, row)) for row in rh]
+        if stopped:
+            converged = True
+            break
+    factors, aux, duals, rho = prob.read_state()
+    if gather is not None:
+        aux, duals = gather(aux, duals)
+    state = SolverState(factors, aux, duals, rho, iteration=len(res_hist))
+    model = KruskalModel(aux)
+    _, err_sq = prob.final_sq_error(aux)
+    return FitResult(
+        model=model,
+        rfe=math.sqrt(err_sq) / x_norm,
+        iterations=total,
+        restarts=attempt,
+        converged=converged,
+        residual_history=res_hist,
+        rfe_history=rfe_hist,
+        factor_history=fac_hist if config.track_factors else None,
+        state=state,
+        rho_history=rho_hist,
+    )
+
+
+_ITER_CACHE: dict = {}
+
+
+def iterate(state: SolverState, t, specs=None, config: SolverConfig | None = None,
+            *, engine=None) -> tuple[SolverState, Residuals]:
+    """One outer iteration from ``state`` (reference solver.py:295-327)."""
+    from .engine import DeviceProblem, device_tensor
+
+    config = config or SolverConfig()
+    t = as_dense(t)
+    normalize_specs(specs, t.order)
+    rank = state.factors[0].shape[1]
+    x = device_tensor(t)
+    key = (id(t), rank, config.inner_sweeps, config.adapt, config.mu, config.tau_incr,
+           config.tau_decr, config.eps_abs, config.eps_rel, _engine_code(engine))
+    prob = _ITER_CACHE.get(key)
+    if prob is None or prob.x is not x:
+        _ITER_CACHE.clear()
+        prob = DeviceProblem(x, t.dims, rank, config, history_capacity=1, engine=_engine_code(engine))
+        _ITER_CACHE[key] = prob
+    prob.load_state(state.factors, state.aux, state.duals, state.rho)
+    prob.run(1, use_graph=False)
+    prob.check_status()
+    r, _ = prob.histories(1)
+    factors, aux, duals, rho = prob.read_state()
+    res = Residuals(tuple(float(v) for v in r[0][:3]), tuple(float(v) for v in r[0][3:]))
+    return SolverState(factors, aux, duals, rho, state.iteration + 1), res

@@ -1,0 +1,146 @@
+"""Generate golden fixtures by running the REFERENCE package (cpadmm) itself.
+
+Run in the build container only (``/root/reference`` does not exist on the GPU
+box):  ``python tests/golden/make_golden.py``.  Outputs small ``.npz`` files in
+this directory which the tests load at run time.  Inputs are regenerated from
+seeds where they are large (the c1 tensor), so only trajectories are stored.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import cpadmm  # noqa: E402
+from cpadmm import bench, solver, tensors  # noqa: E402
+from cpadmm.mesh import distributed_fit  # noqa: E402
+
+from oracle import ntf_oracle as O  # noqa: E402
+
+
+def rebuild_rho(res_hist, rho0, cfg):
+    rho = [rho0] * 3
+    out = []
+    for r in res_hist:
+        if cfg.adapt:
+            rho = solver.adapt_penalties(rho, r, cfg)
+        out.append(list(rho))
+    return np.array(out)
+
+
+def pack_fit(prefix, res, cfg, store, every=1):
+    store[f"{prefix}_rfe"] = np.array(res.rfe)
+    store[f"{prefix}_iterations"] = np.array(res.iterations)
+    store[f"{prefix}_restarts"] = np.array(res.restarts)
+    store[f"{prefix}_converged"] = np.array(res.converged)
+    store[f"{prefix}_primal"] = np.array([r.primal for r in res.residual_history])
+    store[f"{prefix}_dual"] = np.array([r.dual for r in res.residual_history])
+    store[f"{prefix}_rho"] = rebuild_rho(res.residual_history, cfg.rho_init, cfg)
+    for m, a in enumerate(res.model.factors):
+        store[f"{prefix}_aux{m}"] = np.asarray(a)
+    if res.factor_history is not None:
+        idx = list(range(0, len(res.factor_history), every))
+        if idx[-1] != len(res.factor_history) - 1:
+            idx.append(len(res.factor_history) - 1)
+        store[f"{prefix}_hist_idx"] = np.array(idx)
+        for m in range(3):
+            store[f"{prefix}_hist{m}"] = np.stack([res.factor_history[i][m] for i in idx])
+    if res.rfe_history:
+        store[f"{prefix}_rfe_hist"] = np.array(res.rfe_history)
+
+
+def algebra():
+    rng = np.random.default_rng(20240817)
+    st = {}
+    for case, dims in enumerate([(3, 4, 5), (7, 2, 6), (1, 5, 3)]):
+        vals = rng.random(dims)
+        fac = [rng.random((d, 3)) for d in dims]
+        t = tensors.DenseTensor(vals)
+        st[f"c{case}_x"] = vals
+        for m in range(3):
+            st[f"c{case}_f{m}"] = fac[m]
+            st[f"c{case}_mttkrp{m + 1}"] = tensors.mttkrp_factors(t, fac, m + 1)
+            st[f"c{case}_gram{m + 1}"] = solver.companion_gram(fac, m + 1)
+            st[f"c{case}_unfold{m + 1}"] = tensors.unfold(t, m + 1)
+        st[f"c{case}_kr"] = tensors.khatri_rao([fac[2], fac[1]])
+        st[f"c{case}_recon"] = tensors.reconstruct(tensors.KruskalModel(fac)).values
+    np.savez_compressed(os.path.join(HERE, "algebra.npz"), **st)
+
+
+SMALL_CASES = [
+    # name, dims, rank, sigma2, data_seed, cfg kwargs
+    ("noiseless12", (12, 12, 12), 3, 0.0, 1000, dict(seed=0, eps_abs=0.0, eps_rel=0.0, n_max=20,
+                                                   max_restarts=0, track_factors=True)),
+    ("sweeps3", (10, 8, 6), 2, 1e-2, 17, dict(seed=4, eps_abs=0.0, eps_rel=0.0, n_max=12,
+                                            max_restarts=0, inner_sweeps=3, track_factors=True,
+                                            track_rfe=True)),
+    ("converge", (8, 7, 6), 2, 1e-4, 4, dict(seed=1)),
+    ("restarts", (6, 6, 6), 2, 1e-2, 9, dict(seed=0, n_max=3, max_restarts=2, track_factors=True)),
+    ("noadapt", (9, 11, 7), 4, 1e-3, 23, dict(seed=8, eps_abs=0.0, eps_rel=0.0, n_max=10,
+                                            max_restarts=0, adapt=False, inner_sweeps=2,
+                                            track_factors=True)),
+    ("ragged", (1, 13, 5), 2, 1e-2, 31, dict(seed=2, eps_abs=0.0, eps_rel=0.0, n_max=8,
+                                           max_restarts=0, track_factors=True)),
+    ("bigrho", (20, 16, 12), 5, 1e-2, 40, dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=15,
+                                             max_restarts=0, rho_init=300.0, inner_sweeps=4,
+                                             track_factors=True)),
+]
+
+
+def small_fits():
+    st = {}
+    for name, dims, rank, s2, dseed, kw in SMALL_CASES:
+        t, _ = bench.generate(dims, rank, s2, seed=dseed)
+        cfg = solver.SolverConfig(**kw)
+        res = cpadmm.fit(t, rank, None, cfg)
+        st[f"{name}_x"] = np.asarray(t.values)
+        st[f"{name}_rank"] = np.array(rank)
+        pack_fit(name, res, cfg, st)
+    # mesh equivalence fixture (distributed semantics, plan=2)
+    t, _ = bench.generate((12, 12, 12), 3, 0.0, seed=1003)
+    cfg = solver.SolverConfig(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=20, max_restarts=0,
+                              track_factors=True, inner_sweeps=2)
+    res = distributed_fit(t, 3, None, cfg, plan=2)
+    st["mesh2_x"] = np.asarray(t.values)
+    st["mesh2_rank"] = np.array(3)
+    pack_fit("mesh2", res, cfg, st)
+    np.savez_compressed(os.path.join(HERE, "small_fits.npz"), **st)
+
+
+def c1_fixture():
+    """BASELINE config c1 (100^3, R=10, fp64, 10 inner x 50 outer, 20 dB),
+    inputs from the SURVEY §8(d) generator (regenerated from seeds at test
+    time), fit with both rho^0 readings."""
+    dseed = O.derive_seed(0, O.DATA_SALT, 0)
+    fseed = O.derive_seed(0, O.FIT_SALT, 0)
+    x, truth, sigma = O.generate((100, 100, 100), 10, 20.0, dseed)
+    t = tensors.DenseTensor(x)
+    st = {"data_seed": np.array(dseed), "fit_seed": np.array(fseed), "sigma": np.array(sigma),
+          "x_norm": np.array(t.norm()), "x_sha256": np.array(hashlib.sha256(x.tobytes()).hexdigest())}
+    init = solver.init_state(t.dims, 10, solver.SolverConfig(seed=fseed))
+    g = (init.factors[2].T @ init.factors[2]) * (init.factors[1].T @ init.factors[1])
+    rho_tr = float(np.trace(g)) / 10
+    for tag, rho0 in (("rho1", 1.0), ("rhotr", rho_tr)):
+        cfg = solver.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=50, max_restarts=0,
+                                  inner_sweeps=10, rho_init=rho0, track_factors=True)
+        res = cpadmm.fit(t, 10, None, cfg)
+        pack_fit(tag, res, cfg, st, every=7)
+        st[f"{tag}_rho0"] = np.array(rho0)
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), **st)
+
+
+if __name__ == "__main__":
+    algebra()
+    small_fits()
+    c1_fixture()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))

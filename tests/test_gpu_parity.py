@@ -1,0 +1,233 @@
+"""Parity of the B200 path against the CPU oracle and the reference fixtures.
+
+All tests here need a CUDA device and call the product through the C ABI
+(libntf_b200.so).  Tolerances: fp64 <= 1e-12 for the MTTKRP (test_tensors.py
+bar) and <= 1e-9 per-iteration working-factor difference for fits (north
+star); fp32 tensors: final RFE within 1e-4 relative of the oracle, and the
+fp32 MTTKRP within 1e-6 relative of the fp64 oracle.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import MESH2_CFG, SMALL_CASES, rel
+from oracle import ntf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1409_2383_b200 as P  # noqa: E402
+from paper_1409_2383_b200 import _native  # noqa: E402
+from paper_1409_2383_b200 import synth  # noqa: E402
+
+
+def _factors(rng, dims, R):
+    return [rng.random((d, R)) for d in dims]
+
+
+@pytest.mark.parametrize("dims,R", [((3, 4, 5), 2), ((7, 2, 6), 3), ((1, 5, 3), 1), ((33, 17, 65), 7),
+                                    ((40, 50, 60), 20), ((9, 130, 11), 33), ((64, 64, 64), 128),
+                                    ((129, 3, 257), 10)])
+@pytest.mark.parametrize("engine", ["auto", "cuda_core"])
+def test_mttkrp_fp64_matches_oracle(dims, R, engine):
+    rng = np.random.default_rng(11)
+    x = rng.random(dims)
+    f = _factors(rng, dims, R)
+    t = O.OracleTensor(x)
+    for mode in (1, 2, 3):
+        got = P.mttkrp_factors(P.DenseTensor(x), f, mode, engine=engine)
+        assert rel(got, O.mttkrp(t, f, mode)) <= 1e-12
+
+
+def test_mttkrp_golden_ones():  # reference test_tensors.py:143-146
+    x = np.einsum("i,j,k->ijk", [1.0, 2.0], np.ones(2), np.ones(2))
+    got = P.mttkrp_factors(P.DenseTensor(x), [np.ones((2, 1))] * 3, 1)
+    assert got.tolist() == [[4.0], [8.0]]
+
+
+def test_mttkrp_reference_fixture(golden_algebra):
+    g = golden_algebra
+    for case in range(3):
+        x = g[f"c{case}_x"]
+        fac = [g[f"c{case}_f{m}"] for m in range(3)]
+        for mode in (1, 2, 3):
+            got = P.mttkrp_factors(P.DenseTensor(x), fac, mode)
+            assert rel(got, g[f"c{case}_mttkrp{mode}"]) <= 1e-12
+
+
+@pytest.mark.parametrize("dims,R", [((50, 60, 70), 20), ((128, 64, 100), 32), ((31, 45, 29), 50),
+                                    ((100, 100, 100), 100)])
+def test_mttkrp_fp32_accuracy(dims, R):
+    """fp32 tensor, fp64 factors: error must be at the iid-rounding level
+    (recipe of SURVEY 8(d)), far below the 1e-7 structured-rounding level."""
+    rng = np.random.default_rng(5)
+    x32 = rng.random(dims).astype(np.float32)
+    f = _factors(rng, dims, R)
+    t = O.OracleTensor(x32.astype(np.float64))
+    for mode in (1, 2, 3):
+        got = P.mttkrp_factors(P.DenseTensor(x32), f, mode)
+        assert rel(got, O.mttkrp(t, f, mode)) <= 2e-8
+
+
+def test_mttkrp_mode_consistency_c2_full_size():
+    """Size-independent property at BASELINE c2 size: for every column r,
+    sum_i M1[i,r] A[i,r] = sum_j M2[j,r] B[j,r] = sum_k M3[k,r] C[k,r]."""
+    w = synth.CONFIGS["c2"]
+    rng = np.random.default_rng(1)
+    x = rng.random(w.dims, dtype=np.float32)
+    f = _factors(rng, w.dims, w.rank)
+    t = P.DenseTensor(x)
+    v = [np.sum(P.mttkrp_factors(t, f, m) * f[m - 1], axis=0) for m in (1, 2, 3)]
+    assert rel(v[1], v[0]) <= 1e-9 and rel(v[2], v[0]) <= 1e-9
+
+
+def test_norm_and_rfe_kernel():
+    rng = np.random.default_rng(2)
+    dims = (13, 9, 21)
+    f = _factors(rng, dims, 4)
+    x = O.reconstruct(f) + 0.01 * rng.standard_normal(dims)
+    t = P.DenseTensor(x)
+    assert t.norm() == pytest.approx(np.linalg.norm(x), rel=1e-14)
+    from paper_1409_2383_b200.engine import device_tensor, sq_error
+
+    out = sq_error(device_tensor(t), f).cpu().numpy()
+    assert out[1] == pytest.approx(np.linalg.norm(x - O.reconstruct(f)) ** 2, rel=1e-12)
+
+
+def _cmp_fit(res, g, name, tol=1e-9):
+    assert res.iterations == int(g[f"{name}_iterations"])
+    assert res.restarts == int(g[f"{name}_restarts"])
+    assert res.converged == bool(g[f"{name}_converged"])
+    assert np.allclose(np.array([r.primal for r in res.residual_history]), g[f"{name}_primal"],
+                       rtol=1e-8, atol=1e-12)
+    assert np.allclose(np.array([r.dual for r in res.residual_history]), g[f"{name}_dual"],
+                       rtol=1e-8, atol=1e-12)
+    assert np.array_equal(np.array(res.rho_history), g[f"{name}_rho"])
+    assert res.rfe == pytest.approx(float(g[f"{name}_rfe"]), rel=1e-9)
+    worst = 0.0
+    if f"{name}_hist_idx" in g:
+        for n, it in enumerate(g[f"{name}_hist_idx"]):
+            for m in range(3):
+                worst = max(worst, rel(res.factor_history[it][m], g[f"{name}_hist{m}"][n]))
+    for m in range(3):
+        worst = max(worst, rel(res.model.factors[m], g[f"{name}_aux{m}"]))
+    assert worst <= tol, worst
+    return worst
+
+
+@pytest.mark.parametrize("name", sorted(SMALL_CASES))
+def test_small_fits_match_reference(golden_small, name):
+    g = golden_small
+    res = P.fit(g[f"{name}_x"], int(g[f"{name}_rank"]), None, P.SolverConfig(**SMALL_CASES[name]))
+    _cmp_fit(res, g, name)
+    if f"{name}_rfe_hist" in g:
+        assert np.allclose(res.rfe_history, g[f"{name}_rfe_hist"], rtol=1e-9, atol=1e-12)
+
+
+def test_reference_densetensor_accepted(golden_small):
+    """A foreign DenseTensor-like object (.values/.dims) is accepted as is."""
+    g = golden_small
+
+    class Foreign:
+        def __init__(self, v):
+            self.values = v
+            self.dims = v.shape
+
+    res = P.fit(Foreign(g["noiseless12_x"]), 3, None, P.SolverConfig(**SMALL_CASES["noiseless12"]))
+    _cmp_fit(res, g, "noiseless12")
+
+
+@pytest.mark.parametrize("tag", ["rho1", "rhotr"])
+def test_c1_per_iteration_parity(golden_c1, tag):
+    """BASELINE config 1 (100^3, R=10, fp64, 10 inner x 50 outer): max
+    per-iteration working-factor relative difference <= 1e-9."""
+    g = golden_c1
+    w = synth.CONFIGS["c1"]
+    dseed, fseed = synth.seeds()
+    x, _ = synth.generate(w.dims, w.rank, w.snr_db, dseed)
+    cfg = P.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=50, max_restarts=0,
+                         inner_sweeps=10, rho_init=float(g[f"{tag}_rho0"]), track_factors=True)
+    res = P.fit(x, 10, None, cfg)
+    worst = _cmp_fit(res, g, tag, tol=1e-9)
+    print(f"c1 {tag}: max per-iteration factor rel diff {worst:.3e}")
+
+
+def test_fp32_final_rfe_parity():
+    """fp32 tensor (200^3, R=20, 20 dB, 10 inner x 20 outer): final RFE within
+    1e-4 relative of the oracle on the identical (upcast) values."""
+    dseed, fseed = synth.seeds()
+    x, _ = synth.generate((200, 200, 200), 20, 20.0, dseed, dtype=np.float32)
+    cfg = P.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=20, max_restarts=0,
+                         inner_sweeps=10)
+    got = P.fit(P.DenseTensor(x), 20, None, cfg)
+    want = O.fit(x.astype(np.float64), 20, O.Config(**vars(cfg)))
+    d = abs(got.rfe - want.rfe) / want.rfe
+    print(f"fp32 200^3 R=20: rfe gpu {got.rfe:.10f} oracle {want.rfe:.10f} rel {d:.2e}")
+    assert d <= 1e-4
+
+
+def test_iterate_matches_oracle(golden_small):
+    g = golden_small
+    x = g["sweeps3_x"]
+    cfg = P.SolverConfig(seed=4, inner_sweeps=3)
+    st = P.init_state(x.shape, 2, cfg)
+    ost = O.init_state(x.shape, 2, O.Config(seed=4, inner_sweeps=3))
+    t = P.DenseTensor(x)
+    ot = O.OracleTensor(x)
+    for _ in range(4):
+        st, res = P.iterate(st, t, None, cfg)
+        ost, (p, d) = O.iterate(ost, ot, O.Config(seed=4, inner_sweeps=3))
+        for m in range(3):
+            assert rel(st.factors[m], ost.factors[m]) <= 1e-12
+            assert rel(st.aux[m], ost.aux[m]) <= 1e-12
+            assert rel(st.duals[m], ost.duals[m]) <= 1e-11
+        assert np.allclose(res.primal, p, rtol=1e-9) and np.allclose(res.dual, d, rtol=1e-9)
+        assert st.rho == ost.rho
+
+
+def test_errors_match_reference():
+    with pytest.raises(ValueError):
+        P.fit(np.zeros((2, 2, 2)), 1)
+    with pytest.raises(ValueError):
+        P.fit(np.ones((2, 2, 2)), 0)
+    x = np.ones((3, 3, 3))
+    x[1, 1, 1] = np.nan
+    with pytest.raises(ValueError):
+        P.fit(x, 1, None, P.SolverConfig(n_max=2, max_restarts=0))
+    with pytest.raises(NotImplementedError):
+        P.fit(np.ones((3, 3, 3)), 1, P.ConstraintSpec.row_stochastic())
+
+
+def test_deterministic_and_graph_equals_eager(golden_small):
+    g = golden_small
+    x = g["bigrho_x"]
+    cfg = P.SolverConfig(**{**SMALL_CASES["bigrho"], "track_factors": False})
+    a = P.fit(x, 5, None, cfg)
+    b = P.fit(x, 5, None, cfg)
+    for m in range(3):
+        assert np.array_equal(a.model.factors[m], b.model.factors[m])
+    assert a.residual_history == b.residual_history
+    c = P.fit(x, 5, None, P.SolverConfig(**SMALL_CASES["bigrho"]))  # per-iteration host path
+    for m in range(3):
+        assert np.array_equal(a.model.factors[m], c.model.factors[m])
+
+
+def test_distributed_fit_single_rank_is_fit(golden_small):
+    g = golden_small
+    res = P.distributed_fit(g["mesh2_x"], 3, None, P.SolverConfig(**MESH2_CFG), plan=1)
+    want = O.fit(g["mesh2_x"], 3, O.Config(**MESH2_CFG))
+    for it in range(len(want.factor_history)):
+        for m in range(3):
+            assert rel(res.factor_history[it][m], want.factor_history[it][m]) <= 1e-9
+
+
+def test_library_is_the_one_loaded():
+    lib = _native.load()
+    assert lib.ntf_abi_version() == 1
+    import os
+
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert "libntf_b200.so" in maps
