@@ -132,6 +132,10 @@ typedef struct ntf_plan_desc {
   double* resid_history;    /* [cap][6]  primal[3], dual[3]                 */
   double* rho_history;      /* [cap][3]  rho after adaptation               */
   int* counters;            /* [4]: iteration, stop flag, status, spare     */
+  /* Verification hook: when non-NULL, iteration `it` sets rho to row `it`
+   * of this [cap][3] device array instead of applying adapt_penalties, so a
+   * trajectory can be replayed under the reference's penalty sequence. */
+  const double* rho_schedule;
 } ntf_plan_desc;
 
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);

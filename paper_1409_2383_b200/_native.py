@@ -96,6 +96,7 @@ class PlanDesc(ctypes.Structure):
         ("resid_history", c_vp),
         ("rho_history", c_vp),
         ("counters", c_vp),
+        ("rho_schedule", c_vp),
     ]
 
 

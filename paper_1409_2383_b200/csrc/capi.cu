@@ -55,7 +55,7 @@ struct MttkrpOp {
   bool tc = false;
   ntf::MttkrpCCLaunch cc{};
   ntf::MttkrpTCLaunch tcl{};
-  int splits() const { return tc ? tcl.splits : cc.splits; }
+  int splits() const { return tc ? tcl.splits : cc.groups; }
   size_t ws_bytes(int R) const {
     return tc ? ntf::mttkrp_tc_workspace_bytes(tcl, R) : ntf::mttkrp_cc_workspace_bytes(cc, R);
   }
@@ -76,6 +76,12 @@ cudaError_t run_op(const MttkrpOp& op, int mode, int x_dtype, const void* X, int
                    const int* stop, cudaStream_t s) {
   if (op.tc) return ntf::mttkrp_tc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.tcl, ws, stop, s);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
+}
+
+// Function attributes (dynamic smem opt-in) are set once, outside any capture.
+cudaError_t prepare_op(const MttkrpOp& op, int mode, int x_dtype) {
+  if (op.tc) return ntf::mttkrp_tc_prepare(op.tcl);
+  return ntf::mttkrp_cc_prepare(mode, x_dtype, op.cc);
 }
 
 }  // namespace
@@ -101,6 +107,17 @@ struct ntf_plan {
 
 namespace {
 
+// Inside stream capture an event record must be an *external* node to be
+// observable from the host after the graph runs.
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &st);
+  if (e != cudaSuccess) return e;
+  if (st == cudaStreamCaptureStatusActive)
+    return cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  return cudaEventRecord(ev, s);
+}
+
 int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   const ntf_plan_desc& d = pl->d;
   const int m = mode - 1;
@@ -110,11 +127,11 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   if (pl->timing && pl->events) {
     ev = pl->events + 3 * pl->cursor;
     pl->cursor = (pl->cursor + 1) % (pl->n_events / 3);
-    NTF_CUDA_TRY(cudaEventRecord(ev[0], s));
+    NTF_CUDA_TRY(record_event(ev[0], s));
   }
   NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2], d.factors[0],
                       d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s));
-  if (ev) NTF_CUDA_TRY(cudaEventRecord(ev[1], s));
+  if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
   // companions, highest mode first (solver.py:196-204)
   static const int comp[3][2] = {{2, 1}, {2, 0}, {1, 0}};
   ntf::FactorUpdateParams fp{};
@@ -140,7 +157,7 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   fp.status = d.counters + 2;
   fp.stop_flag = d.counters + 1;
   NTF_CUDA_TRY(ntf::factor_update_launch(fp, s));
-  if (ev) NTF_CUDA_TRY(cudaEventRecord(ev[2], s));
+  if (ev) NTF_CUDA_TRY(record_event(ev[2], s));
   return NTF_OK;
 }
 
@@ -161,6 +178,7 @@ int enqueue_finalize(ntf_plan* pl, cudaStream_t s) {
   fz.resid_history = d.resid_history;
   fz.rho_history = d.rho_history;
   fz.counters = d.counters;
+  fz.rho_schedule = d.rho_schedule;
   NTF_CUDA_TRY(ntf::finalize_launch(fz, s));
   return NTF_OK;
 }
@@ -204,6 +222,7 @@ int ntf_mttkrp(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64
   if (workspace_bytes < op.ws_bytes(R)) return fail(NTF_ERR_INVALID, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* ws = static_cast<double*>(workspace);
+  NTF_CUDA_TRY(prepare_op(op, mode, x_dtype));
   NTF_CUDA_TRY(run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s));
   const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
   NTF_CUDA_TRY(ntf::mttkrp_reduce_launch(ws, op.splits(), M, R, out, nullptr, s));
@@ -297,10 +316,8 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaMemset"));
   if ((e = ntf::factor_update_prepare(R)) != cudaSuccess) return cleanup(cuda_fail(e, "prepare"));
   for (int m = 0; m < 3; ++m) {
-    if (pl->op[m].tc) {
-      if ((e = ntf::mttkrp_tc_prepare(pl->op[m].tcl)) != cudaSuccess)
-        return cleanup(cuda_fail(e, "tc prepare"));
-    }
+    if ((e = prepare_op(pl->op[m], m + 1, d.x_dtype)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "mttkrp prepare"));
   }
   *out = pl;
   return NTF_OK;

@@ -7,52 +7,44 @@
 // native row-major X[i][j][k] exactly once.
 //
 // GEMM view used for all modes:  out[m, r] = sum_q X(m, q) * W(q, r),
-//   W(q, r) = F_hi[q_hi, r] * F_lo[q_lo, r]   (KR row formed on the fly)
-//   KIND_Q (modes 1, 2):  q = o*K + k, k the contiguous tensor index,
-//       mode 1: m = i, o = j  (X(m,q) = X[i*JK + q]),   W = B[j] * C[k]
-//       mode 2: m = j, o = i  (X(m,q) = X[i*JK + j*K + k]), W = A[i] * C[k]
-//   KIND_M (mode 3):       q = p = i*J + j, m = k contiguous,  W = A[i] * B[j]
+//   W(q, r) = F_hi[q / L, r] * F_lo[q % L, r]   (KR row formed on the fly)
+//   KIND_Q (modes 1, 2):  q = o*K + k, k the contiguous tensor index, L = K
+//       mode 1: m = i, o = j  (X(m,q) = X[i*JK + q]),        W = B[j] * C[k]
+//       mode 2: m = j, o = i  (X(m,q) = X[i*JK + j*K + k]),  W = A[i] * C[k]
+//   KIND_M (mode 3):       q = p = i*J + j, m = k contiguous, L = J, W = A[i] * B[j]
 //
-// Tiling: a CTA owns BM = 32*TM output rows and all R columns; warp w owns
-// columns [w*TR, (w+1)*TR).  Lane l owns rows l + 32*t (t < TM).  The
-// reduction range is cut into chunks of BQ q-values; a CTA streams a
-// contiguous run of chunks (split-K) through a 3-stage cp.async ring, forms
-// the chunk's KR rows W (fp64 product rounded once to the compute type) in
-// shared memory, and accumulates with register-tiled FMAs where W is a warp
-// broadcast.  Precision recipe for fp32 tensors: fp32 FMA chains
-// of BQ terms, folded into a double-float (hi, lo) accumulator each chunk, so
-// no structured rounding of the factors and no long fp32 chains.  Each CTA
-// writes its fp64 partial; splits are summed in a fixed order by the consumer
-// (deterministic, no float atomics).
+// Tiling.  A CTA owns BM = 32*TM output rows and all R columns; warp w owns
+// columns [w*TR, (w+1)*TR); lane l owns rows l + 32*t (t < TM).  The
+// reduction range is cut into chunks of BQ = 32 q-values.  Each chunk's stage
+// (X tile + the fp64 factor rows its KR rows need) is streamed by 16-byte
+// cp.async through a 3-stage ring; the chunk's KR rows W (fp64 product rounded
+// once to the compute type) are formed from shared memory and read by the FMA
+// loop as warp broadcasts.  KIND_Q tiles keep the natural [m][q] layout with a
+// 16-byte row pad (pitch BQ+4 floats), which makes both the 16-byte cp.async
+// writes and the per-lane 16-byte row reads bank-conflict free.
+//
+// Precision (fp32 tensors): fp32 FMA chains of BQ terms folded
+// into a double-float (hi, lo) accumulator each chunk — no structured rounding
+// of the factors and no long fp32 chains.  fp64 tensors accumulate in fp64.
+//
+// Split-K.  CTAs of one m-tile stream contiguous chunk ranges.  The CTAs of a
+// thread-block cluster (CS splits) reduce their fp64 partial tiles through
+// distributed shared memory in fixed rank order, so only S/CS partials reach
+// HBM; the consumer sums those in fixed order.  No float atomics: results are
+// bitwise run-to-run deterministic.
+#include <cooperative_groups.h>
+
 #include "mttkrp_cc.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ntf {
 
 namespace {
 
-template <typename XT>
-struct ComputeTraits;
-template <>
-struct ComputeTraits<float> {
-  using acc_t = float;
-};
-template <>
-struct ComputeTraits<double> {
-  using acc_t = double;
-};
-
-template <typename XT, int TM>
-struct TileGeom {
-  static constexpr int BM = 32 * TM;
-  static constexpr int BQ = 32;
-  static constexpr int STAGES = 3;
-  // KIND_Q tile [BM][BQ+1] (odd pitch -> conflict-free column reads)
-  static constexpr int kPitchQ = BQ + 1;
-  static constexpr int kTileQ = BM * kPitchQ;
-  // KIND_M tile [BQ][BM]
-  static constexpr int kTileM = BQ * BM;
-  static constexpr int kTile = kTileQ > kTileM ? kTileQ : kTileM;
-};
+constexpr int kBQ = 32;
+constexpr int kStages = 3;
+constexpr int kClusterSplits = 8;
 
 __device__ __forceinline__ void fast_two_sum_acc(float& hi, float& lo, float a) {
   // (hi, lo) += a with Fast2Sum: exact when |hi| >= |a|, which holds after the
@@ -63,178 +55,252 @@ __device__ __forceinline__ void fast_two_sum_acc(float& hi, float& lo, float a) 
   lo += err;
 }
 
-template <typename XT, int TM, int TR, bool KIND_M, int VEC>
+template <typename XT, int TM, bool KIND_M, bool VEC>
+struct Geom {
+  static constexpr int BM = 32 * TM;
+  static constexpr int VW = 16 / sizeof(XT);                       // elements per 16 B
+  static constexpr int kPitchQ = VEC ? kBQ + VW : kBQ + 1;         // KIND_Q row pitch
+  static constexpr int kTileElems = KIND_M ? kBQ * BM : BM * kPitchQ;
+};
+
+template <typename XT, int TM, int TR, bool KIND_M, bool VEC>
 __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
-  using G = TileGeom<XT, TM>;
-  using acc_t = typename ComputeTraits<XT>::acc_t;
+  using G = Geom<XT, TM, KIND_M, VEC>;
   constexpr int BM = G::BM;
-  constexpr int BQ = G::BQ;
-  constexpr int STAGES = G::STAGES;
+  constexpr int VW = G::VW;
   constexpr bool kTwoLevel = sizeof(XT) == 4;
 
   if (p.stop_flag && *p.stop_flag) return;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  XT* xs = reinterpret_cast<XT*>(smem_raw);                 // [STAGES][kTile]
-  XT* ws = xs + STAGES * G::kTile;                           // [2][BQ][R_pad]
-
+  // stage s: [X tile | hi rows (max_hi x R2 doubles) | lo rows (BQ x R2)]
   const int R = p.R;
+  const int R2 = (R + 1) & ~1;
   const int R_pad = p.R_pad;
+  unsigned char* stage_base = smem_raw;
+  const int stage_bytes = p.stage_bytes;
+  XT* wbuf = reinterpret_cast<XT*>(smem_raw + kStages * stage_bytes);  // [2][BQ][R_pad]
+  auto x_tile = [&](int s) { return reinterpret_cast<XT*>(stage_base + s * stage_bytes); };
+  auto hi_rows = [&](int s) {
+    return reinterpret_cast<double*>(stage_base + s * stage_bytes + G::kTileElems * sizeof(XT));
+  };
+  auto lo_rows = [&](int s) { return hi_rows(s) + p.max_hi * R2; };
+
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
+  const int nwarps = nthreads >> 5;
   const int r0 = warp * TR;
 
-  const int mtile = blockIdx.x;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
   const int split = blockIdx.y;
-  const int64_t m0 = static_cast<int64_t>(mtile) * BM;
   const int64_t c_begin = static_cast<int64_t>(split) * p.chunks_per_split;
   int64_t c_end = c_begin + p.chunks_per_split;
   if (c_end > p.n_chunks) c_end = p.n_chunks;
 
   const XT* __restrict__ X = static_cast<const XT*>(p.X);
-  const double* __restrict__ Fhi = p.Fhi;
-  const double* __restrict__ Flo = p.Flo;
+  const uint32_t L = p.lo_extent;
 
-  // ---------------- stage loaders ----------------
-  auto load_x = [&](int64_t c, int stage) {
-    XT* dst = xs + stage * G::kTile;
-    const int64_t q0 = c * BQ;
+  // ---------------- stage loader: X tile + factor rows of chunk c ----------
+  auto load_stage = [&](int64_t c, int s) {
+    const uint32_t q0 = static_cast<uint32_t>(c * kBQ);
+    XT* xt = x_tile(s);
     if constexpr (!KIND_M) {
-      // tile [BM][BQ]: element (m, kk) at dst[m*pitch + kk]; lanes run along kk
-      const int kk = tid % BQ;
-      const uint32_t q = static_cast<uint32_t>(q0) + kk;
-      const bool qvalid = q < p.Q;
-      const uint32_t o = qvalid ? q / static_cast<uint32_t>(p.K) : 0u;
-      const uint32_t k = qvalid ? q - o * static_cast<uint32_t>(p.K) : 0u;
-      const int64_t base = static_cast<int64_t>(o) * p.s_o + k;
-      const int rstep = nthreads / BQ;
-      for (int m = tid / BQ; m < BM; m += rstep) {
-        const int64_t gm = m0 + m;
-        const bool valid = qvalid && gm < p.M;
-        const XT* src = valid ? X + gm * p.s_m + base : X;
-        cp_async_ca<sizeof(XT)>(dst + m * G::kPitchQ + kk, src, valid);
+      if constexpr (VEC) {
+        constexpr int VPR = kBQ / VW;  // vectors per row
+        const int vq = tid % VPR;
+        const uint32_t q = q0 + vq * VW;
+        const bool qv = q < p.Q;
+        const uint32_t o = qv ? q / static_cast<uint32_t>(p.K) : 0u;
+        const uint32_t k = qv ? q - o * static_cast<uint32_t>(p.K) : 0u;
+        const int64_t base = static_cast<int64_t>(o) * p.s_o + k;
+        for (int m = tid / VPR; m < BM; m += nthreads / VPR) {
+          const int64_t gm = m0 + m;
+          const bool valid = qv && gm < p.M;
+          cp_async_cg16(xt + m * G::kPitchQ + vq * VW, valid ? X + gm * p.s_m + base : X, valid);
+        }
+      } else {
+        const int kk = tid % kBQ;
+        const uint32_t q = q0 + kk;
+        const bool qv = q < p.Q;
+        const uint32_t o = qv ? q / static_cast<uint32_t>(p.K) : 0u;
+        const uint32_t k = qv ? q - o * static_cast<uint32_t>(p.K) : 0u;
+        const int64_t base = static_cast<int64_t>(o) * p.s_o + k;
+        for (int m = tid / kBQ; m < BM; m += nthreads / kBQ) {
+          const int64_t gm = m0 + m;
+          const bool valid = qv && gm < p.M;
+          cp_async_ca<sizeof(XT)>(xt + m * G::kPitchQ + kk, valid ? X + gm * p.s_m + base : X,
+                                  valid);
+        }
       }
     } else {
-      // tile [BQ][BM]: element (qq, m) at dst[qq*BM + m]; contiguous along m
-      constexpr int EPV = VEC / sizeof(XT);  // elements per vector
-      constexpr int VPR = BM / EPV;          // vectors per row
-      for (int v = tid; v < BQ * VPR; v += nthreads) {
-        const int qq = v / VPR;
-        const int m = (v % VPR) * EPV;
-        const int64_t q = q0 + qq;
-        const int64_t gm = m0 + m;
-        if constexpr (VEC == 16) {
-          const bool valid = q < p.Q && gm < p.M;  // M % EPV == 0 guaranteed by host
-          const XT* src = valid ? X + q * p.s_m + gm : X;
-          cp_async_cg16(dst + qq * BM + m, src, valid);
-        } else {
+      if constexpr (VEC) {
+        constexpr int VPR = BM / VW;
+        const int vm = tid % VPR;
+        const int64_t gm = m0 + vm * VW;
+        for (int qq = tid / VPR; qq < kBQ; qq += nthreads / VPR) {
+          const uint32_t q = q0 + qq;
+          const bool valid = q < p.Q && gm < p.M;  // host guarantees M % VW == 0
+          cp_async_cg16(xt + qq * BM + vm * VW, valid ? X + static_cast<int64_t>(q) * p.s_m + gm : X,
+                        valid);
+        }
+      } else {
+        for (int e = tid; e < kBQ * BM; e += nthreads) {
+          const int qq = e / BM, m = e - (e / BM) * BM;
+          const uint32_t q = q0 + qq;
+          const int64_t gm = m0 + m;
           const bool valid = q < p.Q && gm < p.M;
-          const XT* src = valid ? X + q * p.s_m + gm : X;
-          cp_async_ca<sizeof(XT)>(dst + qq * BM + m, src, valid);
+          cp_async_ca<sizeof(XT)>(xt + e, valid ? X + static_cast<int64_t>(q) * p.s_m + gm : X,
+                                  valid);
+        }
+      }
+    }
+    // factor rows: hi rows h0 .. h0+max_hi-1, lo rows lo(qq) for qq < BQ
+    const uint32_t h0 = q0 / L;
+    const uint32_t l0 = q0 - h0 * L;
+    double* hs = hi_rows(s);
+    double* ls = lo_rows(s);
+    if ((R & 1) == 0) {
+      const int vpr = R >> 1;  // 16-byte vectors per row
+      const int nh = p.max_hi * vpr;
+      for (int e = tid; e < nh + kBQ * vpr; e += nthreads) {
+        if (e < nh) {
+          const int row = e / vpr, v = e - (e / vpr) * vpr;
+          const uint32_t h = h0 + row;
+          const bool valid = h < p.hi_extent;
+          cp_async_cg16(hs + row * R2 + 2 * v, valid ? p.Fhi + static_cast<int64_t>(h) * R + 2 * v : p.Fhi,
+                        valid);
+        } else {
+          const int e2 = e - nh;
+          const int qq = e2 / vpr, v = e2 - (e2 / vpr) * vpr;
+          const uint32_t lo = (l0 + qq) % L;
+          cp_async_cg16(ls + qq * R2 + 2 * v, p.Flo + static_cast<int64_t>(lo) * R + 2 * v, true);
+        }
+      }
+    } else {
+      const int nh = p.max_hi * R;
+      for (int e = tid; e < nh + kBQ * R; e += nthreads) {
+        if (e < nh) {
+          const int row = e / R, r = e - (e / R) * R;
+          const uint32_t h = h0 + row;
+          const bool valid = h < p.hi_extent;
+          cp_async_ca<8>(hs + row * R2 + r, valid ? p.Fhi + static_cast<int64_t>(h) * R + r : p.Fhi,
+                         valid);
+        } else {
+          const int e2 = e - nh;
+          const int qq = e2 / R, r = e2 - (e2 / R) * R;
+          const uint32_t lo = (l0 + qq) % L;
+          cp_async_ca<8>(ls + qq * R2 + r, p.Flo + static_cast<int64_t>(lo) * R + r, true);
         }
       }
     }
   };
 
-  // KR rows of chunk c: W[qq][r] = Fhi[hi(q)][r] * Flo[lo(q)][r] in fp64, rounded
-  // once to the compute type.  One warp per q-row (indices advanced
-  // incrementally, no per-element division), lanes along r (coalesced).
-  auto form_w = [&](int64_t c, int buf) {
-    XT* dst = ws + buf * BQ * R_pad;
-    const int nwarps = nthreads >> 5;
-    uint32_t q = static_cast<uint32_t>(c * BQ) + warp;
-    uint32_t hi_i = q / p.lo_extent;
-    uint32_t lo_i = q - hi_i * p.lo_extent;
-    for (int qq = warp; qq < BQ; qq += nwarps) {
+  // KR rows of chunk c from the staged factor rows: one warp per q-row,
+  // lanes along r (no per-element division).
+  auto form_w = [&](int64_t c, int s, int buf) {
+    XT* dst = wbuf + buf * kBQ * R_pad;
+    const uint32_t q0 = static_cast<uint32_t>(c * kBQ);
+    const uint32_t h0 = q0 / L;
+    const uint32_t l0 = q0 - h0 * L;
+    const double* hs = hi_rows(s);
+    const double* ls = lo_rows(s);
+    for (int qq = warp; qq < kBQ; qq += nwarps) {
+      const uint32_t q = q0 + qq;
       const bool qv = q < p.Q;
-      const double* fh = Fhi + static_cast<int64_t>(hi_i) * R;
-      const double* fl = Flo + static_cast<int64_t>(lo_i) * R;
+      const int hoff = static_cast<int>((l0 + qq) / L);
+      const double* fh = hs + hoff * R2;
+      const double* fl = ls + qq * R2;
       for (int r = lane; r < R_pad; r += 32) {
         XT w = XT(0);
         if (qv && r < R) w = static_cast<XT>(fh[r] * fl[r]);
         dst[qq * R_pad + r] = w;
       }
-      q += nwarps;
-      lo_i += nwarps;
-      while (lo_i >= p.lo_extent) {
-        lo_i -= p.lo_extent;
-        ++hi_i;
-      }
     }
   };
 
   // ---------------- accumulators ----------------
+  using acc_t = XT;
   acc_t acc[TM][TR];
   float hi[kTwoLevel ? TM : 1][kTwoLevel ? TR : 1];
   float lo[kTwoLevel ? TM : 1][kTwoLevel ? TR : 1];
 #pragma unroll
   for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int j = 0; j < TR; ++j) acc[t][j] = acc_t(0);
-  if constexpr (kTwoLevel) {
-#pragma unroll
-    for (int t = 0; t < TM; ++t)
-#pragma unroll
-      for (int j = 0; j < TR; ++j) {
+    for (int j = 0; j < TR; ++j) {
+      acc[t][j] = acc_t(0);
+      if constexpr (kTwoLevel) {
         hi[t][j] = 0.f;
         lo[t][j] = 0.f;
       }
-  }
+    }
 
   const bool active_r = r0 < R;  // warps entirely in the padding skip the math
 
   if (c_begin < c_end) {
-    load_x(c_begin, 0);
+    load_stage(c_begin, 0);
     cp_async_commit();
-    if (c_begin + 1 < c_end) load_x(c_begin + 1, 1);
+    if (c_begin + 1 < c_end) load_stage(c_begin + 1, 1);
     cp_async_commit();
-    form_w(c_begin, 0);
+    cp_async_wait<1>();
+    __syncthreads();
+    form_w(c_begin, 0, 0);
 
     for (int64_t c = c_begin; c < c_end; ++c) {
       const int it = static_cast<int>(c - c_begin);
-      cp_async_wait<1>();
       __syncthreads();
-      if (c + 2 < c_end) load_x(c + 2, (it + 2) % STAGES);
+      if (c + 2 < c_end) load_stage(c + 2, (it + 2) % kStages);
       cp_async_commit();
 
       if (active_r) {
-        const XT* xt = xs + (it % STAGES) * G::kTile;
-        const XT* wt = ws + (it & 1) * BQ * R_pad + r0;
-#pragma unroll 4
-        for (int qq = 0; qq < BQ; ++qq) {
-          XT xv[TM];
-#pragma unroll
-          for (int t = 0; t < TM; ++t) {
-            const int m = lane + 32 * t;
-            xv[t] = KIND_M ? xt[qq * BM + m] : xt[m * G::kPitchQ + qq];
-          }
+        const XT* xt = x_tile(it % kStages);
+        const XT* wt = wbuf + r0;
+        auto fma_step = [&](const XT (&xv)[TM], int qq) {
           XT wv[TR];
-          if constexpr (sizeof(XT) == 4 && TR % 4 == 0) {
 #pragma unroll
-            for (int j = 0; j < TR; j += 4) {
-              const float4 v = *reinterpret_cast<const float4*>(wt + qq * R_pad + j);
-              wv[j] = v.x;
-              wv[j + 1] = v.y;
-              wv[j + 2] = v.z;
-              wv[j + 3] = v.w;
-            }
-          } else if constexpr (sizeof(XT) == 8 && TR % 2 == 0) {
+          for (int j = 0; j < TR; j += VW) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(wt + qq * R_pad + j);
+            const XT* pv = reinterpret_cast<const XT*>(&raw);
 #pragma unroll
-            for (int j = 0; j < TR; j += 2) {
-              const double2 v = *reinterpret_cast<const double2*>(wt + qq * R_pad + j);
-              wv[j] = v.x;
-              wv[j + 1] = v.y;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < TR; ++j) wv[j] = wt[qq * R_pad + j];
+            for (int u = 0; u < VW; ++u) wv[j + u] = pv[u];
           }
 #pragma unroll
           for (int t = 0; t < TM; ++t)
 #pragma unroll
             for (int j = 0; j < TR; ++j) acc[t][j] = fma(xv[t], wv[j], acc[t][j]);
+        };
+        if constexpr (!KIND_M && VEC) {
+#pragma unroll 2
+          for (int q4 = 0; q4 < kBQ; q4 += VW) {
+            XT xr[TM][VW];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+              const uint4 raw =
+                  *reinterpret_cast<const uint4*>(xt + (lane + 32 * t) * G::kPitchQ + q4);
+              const XT* pv = reinterpret_cast<const XT*>(&raw);
+#pragma unroll
+              for (int u = 0; u < VW; ++u) xr[t][u] = pv[u];
+            }
+#pragma unroll
+            for (int u = 0; u < VW; ++u) {
+              XT xv[TM];
+#pragma unroll
+              for (int t = 0; t < TM; ++t) xv[t] = xr[t][u];
+              fma_step(xv, q4 + u);
+            }
+          }
+        } else {
+#pragma unroll 4
+          for (int qq = 0; qq < kBQ; ++qq) {
+            XT xv[TM];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+              const int m = lane + 32 * t;
+              xv[t] = KIND_M ? xt[qq * BM + m] : xt[m * G::kPitchQ + qq];
+            }
+            fma_step(xv, qq);
+          }
         }
         if constexpr (kTwoLevel) {
 #pragma unroll
@@ -246,61 +312,129 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
             }
         }
       }
-      if (c + 1 < c_end) form_w(c + 1, (it + 1) & 1);
+      if (c + 1 < c_end) {
+        cp_async_wait<1>();
+        __syncthreads();
+        form_w(c + 1, (it + 1) % kStages, 0);
+      }
     }
     cp_async_wait<0>();
   }
 
-  // ---------------- write this split's fp64 partial ----------------
-  if (!active_r) return;
-  double* out = p.ws + static_cast<int64_t>(split) * p.M * R;
+  // ------------- cluster (DSMEM) reduction of the split partials -------------
+  cg::cluster_group cluster = cg::this_cluster();
+  __syncthreads();
+  double* part = reinterpret_cast<double*>(smem_raw);  // [BM][R], reuses the stage ring
+  if (active_r) {
 #pragma unroll
-  for (int t = 0; t < TM; ++t) {
-    const int64_t gm = m0 + lane + 32 * t;
-    if (gm >= p.M) continue;
+    for (int t = 0; t < TM; ++t) {
+      const int m = lane + 32 * t;
 #pragma unroll
-    for (int j = 0; j < TR; ++j) {
-      const int r = r0 + j;
-      if (r >= R) continue;
-      double v;
-      if constexpr (kTwoLevel)
-        v = static_cast<double>(hi[t][j]) + static_cast<double>(lo[t][j]);
-      else
-        v = static_cast<double>(acc[t][j]);
-      out[gm * R + r] = v;
+      for (int j = 0; j < TR; ++j) {
+        const int r = r0 + j;
+        if (r >= R) continue;
+        double v;
+        if constexpr (kTwoLevel)
+          v = static_cast<double>(hi[t][j]) + static_cast<double>(lo[t][j]);
+        else
+          v = static_cast<double>(acc[t][j]);
+        part[m * R + r] = v;
+      }
     }
   }
+  cluster.sync();
+  const int cs = static_cast<int>(cluster.num_blocks());
+  const int crank = static_cast<int>(cluster.block_rank());
+  const int rows_per = BM / cs;
+  const int64_t group = split / cs;
+  double* out = p.ws + group * p.M * R;
+  for (int e = tid; e < rows_per * R; e += nthreads) {
+    const int lm = crank * rows_per + e / R;
+    const int r = e - (e / R) * R;
+    double s = 0.0;
+    for (int b = 0; b < cs; ++b) {
+      const double* rp = cluster.map_shared_rank(part, b);
+      s += rp[lm * R + r];
+    }
+    const int64_t gm = m0 + lm;
+    if (gm < p.M) out[gm * R + r] = s;
+  }
+  cluster.sync();
 }
 
-// Sum the split partials in a fixed order: out[m, r] = sum_s ws[s][m][r].
-__global__ void mttkrp_reduce_kernel(const double* __restrict__ ws, int64_t splits, int64_t n,
+// Sum the split-group partials in a fixed order: out[m, r] = sum_g ws[g][m][r].
+__global__ void mttkrp_reduce_kernel(const double* __restrict__ ws, int64_t groups, int64_t n,
                                      double* __restrict__ out, const int* stop_flag) {
   if (stop_flag && *stop_flag) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int64_t k = 0; k < splits; ++k) s += ws[k * n + e];
+    for (int64_t k = 0; k < groups; ++k) s += ws[k * n + e];
     out[e] = s;
   }
 }
 
-template <typename XT, int TM, int TR, bool KIND_M, int VEC>
-cudaError_t launch_variant(const MttkrpCCParams& p, const MttkrpCCLaunch& L, cudaStream_t stream) {
+enum VariantOp { kLaunch = 0, kPrepare = 1, kQueryClusters = 2 };
+thread_local int g_active_clusters = 0;
+
+template <typename XT, int TM, int TR, bool KIND_M, bool VEC>
+cudaError_t launch_variant(const MttkrpCCParams& p, const MttkrpCCLaunch& L, cudaStream_t stream,
+                           int op) {
   auto kern = mttkrp_cc_kernel<XT, TM, TR, KIND_M, VEC>;
-  cudaError_t err =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
-  if (err != cudaSuccess) return err;
-  kern<<<dim3(L.n_mtiles, L.splits), L.threads, L.smem_bytes, stream>>>(p);
-  return cudaGetLastError();
+  if (op != kLaunch) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
+    if (e != cudaSuccess || op == kPrepare) return e;
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(1, L.cluster, 1);
+    q.blockDim = dim3(L.threads, 1, 1);
+    q.dynamicSmemBytes = L.smem_bytes;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = 1;
+    a[0].val.clusterDim.y = L.cluster;
+    a[0].val.clusterDim.z = 1;
+    q.attrs = a;
+    q.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(&g_active_clusters, kern, &q);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(L.n_mtiles, L.splits, 1);
+  cfg.blockDim = dim3(L.threads, 1, 1);
+  cfg.dynamicSmemBytes = L.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = L.cluster;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-}  // namespace
+template <typename XT, int TM, int TR>
+cudaError_t dispatch_kind(int mode, const MttkrpCCParams& p, const MttkrpCCLaunch& L,
+                          cudaStream_t stream, int prep) {
+  if (mode == 3)
+    return L.vec ? launch_variant<XT, TM, TR, true, true>(p, L, stream, prep)
+                 : launch_variant<XT, TM, TR, true, false>(p, L, stream, prep);
+  return L.vec ? launch_variant<XT, TM, TR, false, true>(p, L, stream, prep)
+               : launch_variant<XT, TM, TR, false, false>(p, L, stream, prep);
+}
 
-// ---------------------------------------------------------------------------
-// host side: geometry and dispatch
-// ---------------------------------------------------------------------------
+cudaError_t dispatch(int mode, int x_dtype, const MttkrpCCParams& p, const MttkrpCCLaunch& L,
+                     cudaStream_t stream, int prep) {
+  if (x_dtype == NTF_F32) {
+    if (L.TR == 16) return dispatch_kind<float, 4, 16>(mode, p, L, stream, prep);
+    return dispatch_kind<float, 4, 8>(mode, p, L, stream, prep);
+  }
+  if (L.TR == 16) return dispatch_kind<double, 2, 16>(mode, p, L, stream, prep);
+  if (L.TR == 8) return dispatch_kind<double, 2, 8>(mode, p, L, stream, prep);
+  return dispatch_kind<double, 2, 4>(mode, p, L, stream, prep);
+}
 
-static int sm_count_cached() {
+int sm_count_cached() {
   static int n = 0;
   if (n == 0) {
     int dev = 0;
@@ -311,48 +445,9 @@ static int sm_count_cached() {
   return n;
 }
 
-MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
-  MttkrpCCLaunch L{};
-  const bool f32 = x_dtype == NTF_F32;
-  L.TM = f32 ? 4 : 2;
-  L.TR = f32 ? (R > 64 ? 16 : 8) : (R > 32 ? 8 : 4);
-  const int BM = 32 * L.TM;
-  const int BQ = 32;
-  L.R_pad = ((R + L.TR - 1) / L.TR) * L.TR;
-  L.threads = (L.R_pad / L.TR) * 32;
-  if (L.threads < 64) L.threads = 64;  // keep loaders busy; extra warps skip math
-  const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
-  const int64_t Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
-  L.M = M;
-  L.Q = Q;
-  L.n_mtiles = static_cast<int>((M + BM - 1) / BM);
-  L.n_chunks = (Q + BQ - 1) / BQ;
-  const int esz = f32 ? 4 : 8;
-  const int tile = BM * (BQ + 1) > BQ * BM ? BM * (BQ + 1) : BQ * BM;
-  L.smem_bytes = 3 * tile * esz + 2 * BQ * L.R_pad * esz;
-  // Occupancy-driven split count: fill every SM ~4 CTAs deep.
-  int per_sm = static_cast<int>((227 * 1024) / (L.smem_bytes + 1024));
-  if (per_sm < 1) per_sm = 1;
-  if (per_sm > 4) per_sm = 4;
-  const int64_t target = static_cast<int64_t>(sm_count_cached()) * per_sm * 2;
-  int64_t splits = (target + L.n_mtiles - 1) / L.n_mtiles;
-  if (splits < 1) splits = 1;
-  if (splits > L.n_chunks) splits = L.n_chunks;
-  L.chunks_per_split = (L.n_chunks + splits - 1) / splits;
-  L.splits = static_cast<int>((L.n_chunks + L.chunks_per_split - 1) / L.chunks_per_split);
-  L.vec16 = (mode == 3) && f32 && (K % 4 == 0) && (M % 4 == 0);
-  return L;
-}
-
-size_t mttkrp_cc_workspace_bytes(const MttkrpCCLaunch& L, int R) {
-  return static_cast<size_t>(L.splits) * L.M * R * sizeof(double);
-}
-
-cudaError_t mttkrp_cc_launch(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
-                             const double* A, const double* B, const double* C, int R,
-                             const MttkrpCCLaunch& L, double* ws, const int* stop_flag,
-                             cudaStream_t stream) {
-  MttkrpCCParams p{};
+void fill_params(MttkrpCCParams& p, int mode, const void* X, int64_t I, int64_t J, int64_t K,
+                 const double* A, const double* B, const double* C, int R, const MttkrpCCLaunch& L,
+                 double* ws, const int* stop_flag) {
   p.X = X;
   p.R = R;
   p.R_pad = L.R_pad;
@@ -363,53 +458,114 @@ cudaError_t mttkrp_cc_launch(int mode, int x_dtype, const void* X, int64_t I, in
   p.chunks_per_split = L.chunks_per_split;
   p.ws = ws;
   p.stop_flag = stop_flag;
+  p.stage_bytes = L.stage_bytes;
+  p.max_hi = L.max_hi;
   if (mode == 1) {
     p.s_m = J * K;
     p.s_o = K;
     p.Fhi = B;
     p.Flo = C;
     p.lo_extent = static_cast<uint32_t>(K);
+    p.hi_extent = static_cast<uint32_t>(J);
   } else if (mode == 2) {
     p.s_m = K;
     p.s_o = J * K;
     p.Fhi = A;
     p.Flo = C;
     p.lo_extent = static_cast<uint32_t>(K);
+    p.hi_extent = static_cast<uint32_t>(I);
   } else {
     p.s_m = K;  // row pitch of the [P][K] view
     p.s_o = 0;
     p.Fhi = A;
     p.Flo = B;
     p.lo_extent = static_cast<uint32_t>(J);
+    p.hi_extent = static_cast<uint32_t>(I);
   }
-  const bool f32 = x_dtype == NTF_F32;
-  if (f32) {
-    if (L.TR == 16) {
-      if (mode == 3)
-        return L.vec16 ? launch_variant<float, 4, 16, true, 16>(p, L, stream)
-                       : launch_variant<float, 4, 16, true, 4>(p, L, stream);
-      return launch_variant<float, 4, 16, false, 4>(p, L, stream);
-    }
-    if (mode == 3)
-      return L.vec16 ? launch_variant<float, 4, 8, true, 16>(p, L, stream)
-                     : launch_variant<float, 4, 8, true, 4>(p, L, stream);
-    return launch_variant<float, 4, 8, false, 4>(p, L, stream);
-  }
-  if (L.TR == 8) {
-    if (mode == 3) return launch_variant<double, 2, 8, true, 8>(p, L, stream);
-    return launch_variant<double, 2, 8, false, 8>(p, L, stream);
-  }
-  if (mode == 3) return launch_variant<double, 2, 4, true, 8>(p, L, stream);
-  return launch_variant<double, 2, 4, false, 8>(p, L, stream);
 }
 
-cudaError_t mttkrp_reduce_launch(const double* ws, int splits, int64_t M, int R, double* out,
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side: geometry and dispatch
+// ---------------------------------------------------------------------------
+MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
+  MttkrpCCLaunch L{};
+  const bool f32 = x_dtype == NTF_F32;
+  const int esz = f32 ? 4 : 8;
+  const int VW = 16 / esz;
+  L.TM = f32 ? 4 : 2;
+  L.TR = (R > 64) ? 16 : (R > 32 || f32 ? 8 : 4);
+  const int BM = 32 * L.TM;
+  L.R_pad = ((R + L.TR - 1) / L.TR) * L.TR;
+  L.threads = (L.R_pad / L.TR) * 32;
+  if (L.threads < 64) L.threads = 64;  // keep loaders busy; extra warps skip the math
+  const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
+  const int64_t Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
+  const int64_t lo_ext = mode == 3 ? J : K;
+  L.M = M;
+  L.Q = Q;
+  L.n_mtiles = static_cast<int>((M + BM - 1) / BM);
+  L.n_chunks = (Q + kBQ - 1) / kBQ;
+  // 16-byte cp.async needs whole vectors that never straddle a row/o boundary
+  L.vec = (K % VW == 0) && (mode != 3 || M % VW == 0);
+  const int pitchQ = L.vec ? kBQ + VW : kBQ + 1;
+  const int tile = (mode == 3 ? kBQ * BM : BM * pitchQ) * esz;
+  L.max_hi = static_cast<int>(std::min<int64_t>(kBQ, (kBQ - 1) / lo_ext + 2));
+  const int R2 = (R + 1) & ~1;
+  int fac = (L.max_hi + kBQ) * R2 * 8;
+  L.stage_bytes = ((tile + fac) + 15) & ~15;
+  const int wbytes = kBQ * L.R_pad * esz;  // one KR buffer (rebuilt after a barrier)
+  L.smem_bytes = kStages * L.stage_bytes + wbytes;
+  const int part_bytes = BM * R * 8;  // cluster-reduction tile reuses the stage ring
+  if (part_bytes > kStages * L.stage_bytes) L.smem_bytes = part_bytes + wbytes;
+  L.cluster = kClusterSplits;
+  // One wave: as many clusters as can be co-resident (whole clusters per GPC),
+  // spread over the m-tiles; splits are whole clusters.
+  int active = 0;
+  {
+    MttkrpCCParams p{};
+    if (dispatch(mode, x_dtype, p, L, nullptr, kQueryClusters) == cudaSuccess)
+      active = g_active_clusters;
+    cudaGetLastError();
+  }
+  if (active <= 0) active = sm_count_cached() / L.cluster;
+  int64_t per_tile = active / L.n_mtiles;
+  if (per_tile < 1) per_tile = 1;
+  int64_t splits = per_tile * L.cluster;
+  const int64_t max_splits = ((L.n_chunks + L.cluster - 1) / L.cluster) * L.cluster;
+  if (splits > max_splits) splits = max_splits;
+  L.chunks_per_split = (L.n_chunks + splits - 1) / splits;
+  L.splits = static_cast<int>(splits);
+  L.groups = L.splits / L.cluster;
+  return L;
+}
+
+size_t mttkrp_cc_workspace_bytes(const MttkrpCCLaunch& L, int R) {
+  return static_cast<size_t>(L.groups) * L.M * R * sizeof(double);
+}
+
+cudaError_t mttkrp_cc_prepare(int mode, int x_dtype, const MttkrpCCLaunch& L) {
+  MttkrpCCParams p{};
+  return dispatch(mode, x_dtype, p, L, nullptr, kPrepare);
+}
+
+cudaError_t mttkrp_cc_launch(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
+                             const double* A, const double* B, const double* C, int R,
+                             const MttkrpCCLaunch& L, double* ws, const int* stop_flag,
+                             cudaStream_t stream) {
+  MttkrpCCParams p{};
+  fill_params(p, mode, X, I, J, K, A, B, C, R, L, ws, stop_flag);
+  return dispatch(mode, x_dtype, p, L, stream, kLaunch);
+}
+
+cudaError_t mttkrp_reduce_launch(const double* ws, int groups, int64_t M, int R, double* out,
                                  const int* stop_flag, cudaStream_t stream) {
   const int64_t n = M * R;
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 4 * sm_count_cached()) blocks = 4 * sm_count_cached();
   if (blocks < 1) blocks = 1;
-  mttkrp_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, splits, n, out, stop_flag);
+  mttkrp_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, groups, n, out, stop_flag);
   return cudaGetLastError();
 }
 

@@ -1,6 +1,8 @@
 // CUDA-core dense MTTKRP: parameter block and host dispatch declarations.
 #pragma once
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ntf {
@@ -13,28 +15,30 @@ struct MttkrpCCParams {
   int64_t s_m, s_o;     // element strides of m and o
   const double* Fhi;    // KR slow factor (indexed by q / lo_extent)
   const double* Flo;    // KR fast factor (indexed by q % lo_extent)
-  uint32_t lo_extent;
+  uint32_t lo_extent, hi_extent;
   int R, R_pad;
   int64_t n_chunks, chunks_per_split;
-  double* ws;           // [splits][M][R] fp64 partials
+  int stage_bytes, max_hi;
+  double* ws;           // [groups][M][R] fp64 partials (one per cluster)
   const int* stop_flag;
 };
 
 struct MttkrpCCLaunch {
   int TM, TR, R_pad, threads;
-  int n_mtiles, splits;
+  int n_mtiles, splits, cluster, groups;
   int64_t M, Q, n_chunks, chunks_per_split;
-  int smem_bytes;
-  bool vec16;
+  int stage_bytes, max_hi, smem_bytes;
+  bool vec;
 };
 
 MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R);
 size_t mttkrp_cc_workspace_bytes(const MttkrpCCLaunch& L, int R);
+cudaError_t mttkrp_cc_prepare(int mode, int x_dtype, const MttkrpCCLaunch& L);
 cudaError_t mttkrp_cc_launch(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
                              const double* A, const double* B, const double* C, int R,
                              const MttkrpCCLaunch& L, double* ws, const int* stop_flag,
                              cudaStream_t stream);
-cudaError_t mttkrp_reduce_launch(const double* ws, int splits, int64_t M, int R, double* out,
+cudaError_t mttkrp_reduce_launch(const double* ws, int groups, int64_t M, int R, double* out,
                                  const int* stop_flag, cudaStream_t stream);
 
 }  // namespace ntf

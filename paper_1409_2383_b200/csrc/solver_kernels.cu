@@ -40,15 +40,10 @@ __device__ void build_and_factor(double* L, int ldl, int R, const double* __rest
       return;
     }
     const double inv = 1.0 / piv;
-    const int n = R - j - 1;  // trailing order
-    // lower-triangular trailing elements (i >= k > j): n(n+1)/2
-    const int cnt = n * (n + 1) / 2;
-    for (int e = tid; e < cnt; e += blockDim.x) {
-      // map e -> (ii, kk) with 0 <= kk <= ii < n
-      int ii = static_cast<int>((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-      while (ii * (ii + 1) / 2 > e) --ii;
-      const int kk = e - ii * (ii + 1) / 2;
+    const int n = R - j - 1;  // trailing order; update the lower triangle i >= k > j
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int ii = e / n, kk = e - (e / n) * n;
+      if (kk > ii) continue;
       const int i = j + 1 + ii, k = j + 1 + kk;
       L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j] * inv;
     }
@@ -112,10 +107,28 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   const int ldl = R + 1;  // odd pitch: conflict-free row and column walks
   double* L = reinterpret_cast<double*>(smem_raw);
   double* xrows = L + R * ldl;                  // [kRowsPerBlock][R]
-  double* red = xrows + kRowsPerBlock * R;      // [8 warps][5]
+  double* msum = xrows + kRowsPerBlock * R;     // [kRowsPerBlock][R] reduced MTTKRP rows
+  double* red = msum + kRowsPerBlock * R;       // [8 warps][5]
   __shared__ bool bad;
   __shared__ bool is_last;
   if (threadIdx.x == 0) bad = false;
+
+  const int64_t row_base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
+  const int64_t n_rows = p.rows;
+  const int64_t nM = n_rows * R;
+  // Sum the MTTKRP split partials of this block's rows (fixed split order),
+  // all threads cooperating; rows are contiguous so the block's slice of each
+  // partial is one contiguous run.
+  {
+    const int64_t base = row_base * R;
+    int64_t cnt = nM - base;
+    if (cnt > static_cast<int64_t>(kRowsPerBlock) * R) cnt = static_cast<int64_t>(kRowsPerBlock) * R;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      double m = 0.0;
+      for (int s = 0; s < p.splits; ++s) m += p.mtt[s * nM + base + e];
+      msum[e] = m;
+    }
+  }
 
   const double rho = p.rho[p.mode - 1];
   build_and_factor(L, ldl, R, p.Ga, p.Gb, rho, p.status, &bad);
@@ -124,9 +137,6 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = kUpdThreads / 32;
-  const int64_t row_base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
-  const int64_t n_rows = p.rows;
-  const int64_t nM = n_rows * R;
   const double inv_rho = 1.0 / rho;
 
   double nrm[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -140,10 +150,8 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
         y[t] = 0.0;
         if (r < R) {
           const int64_t e = row * R + r;
-          double m = 0.0;
-          for (int s = 0; s < p.splits; ++s) m += p.mtt[s * nM + e];
           // ridge_rhs: mtt + rho*aux - dual (solver.py:178-179)
-          y[t] = (m + rho * p.aux[e]) - p.dual[e];
+          y[t] = (msum[lr * R + r] + rho * p.aux[e]) - p.dual[e];
         }
       }
       warp_chol_solve<RT>(y, L, ldl, R, lane);
@@ -293,7 +301,9 @@ __global__ void finalize_kernel(FinalizeParams p) {
   double rho_new[3];
   for (int m = 0; m < 3; ++m) {
     const double r = p.rho[m];
-    if (!p.adapt) {
+    if (p.rho_schedule && it < p.history_capacity) {
+      rho_new[m] = p.rho_schedule[it * 3 + m];
+    } else if (!p.adapt) {
       rho_new[m] = r;
     } else if (primal[m] > p.mu * dual[m]) {
       rho_new[m] = r * p.tau_incr;
@@ -430,7 +440,7 @@ int factor_update_blocks(int64_t rows) {
 }
 
 size_t factor_update_smem(int R) {
-  return (static_cast<size_t>(R) * (R + 1) + static_cast<size_t>(kRowsPerBlock) * R + 8 * 5) *
+  return (static_cast<size_t>(R) * (R + 1) + 2 * static_cast<size_t>(kRowsPerBlock) * R + 8 * 5) *
          sizeof(double);
 }
 

@@ -42,6 +42,7 @@ struct FinalizeParams {
   double* resid_history;    // [cap][6]
   double* rho_history;      // [cap][3]
   int* counters;            // [0] iteration, [1] stop flag
+  const double* rho_schedule;  // optional [cap][3] replayed penalties
 };
 
 int factor_update_blocks(int64_t rows);

@@ -49,7 +49,11 @@ def device_tensor(t, device=None):
     if cache is not None and cache.device == dev:
         return cache
     if isinstance(vals, np.ndarray):
-        host = torch.from_numpy(np.ascontiguousarray(vals))
+        import warnings
+
+        with warnings.catch_warnings():  # read-only source: we only read it
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.from_numpy(np.ascontiguousarray(vals))
         x = host.to(dev)
     else:
         x = vals.to(dev, non_blocking=bool(vals.is_pinned()) if vals.device.type == "cpu" else False)
@@ -146,7 +150,7 @@ class DeviceProblem:
     """HBM state of one fit and its C-ABI plan."""
 
     def __init__(self, x, dims, rank: int, config, history_capacity: int, engine: int = N.ENGINE_AUTO,
-                 slabs: Slabs | None = None, stream=None):
+                 slabs: Slabs | None = None, stream=None, rho_schedule=None):
         torch = _torch()
         self.torch = torch
         self.lib = N.load()
@@ -205,6 +209,13 @@ class DeviceProblem:
         d.resid_history = _ptr(self.resid_hist)
         d.rho_history = _ptr(self.rho_hist)
         d.counters = _ptr(self.counters)
+        self._rho_schedule = None
+        if rho_schedule is not None:
+            sched = np.zeros((cap, 3))
+            rs = np.asarray(rho_schedule, dtype=np.float64).reshape(-1, 3)[:cap]
+            sched[: len(rs)] = rs
+            self._rho_schedule = torch.from_numpy(sched).to(dev)
+            d.rho_schedule = _ptr(self._rho_schedule)
         self._desc = d
         handle = ctypes.c_void_p()
         N.check(self.lib.ntf_plan_create(ctypes.byref(d), ctypes.byref(handle)))

@@ -159,7 +159,8 @@ def mttkrp_factors(t, factors: Sequence[np.ndarray], mode: int, engine=None) -> 
 
 
 def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = None,
-        config: SolverConfig | None = None, *, engine=None, device=None) -> FitResult:
+        config: SolverConfig | None = None, *, engine=None, device=None,
+        rho_schedule=None) -> FitResult:
     """Constrained (non-negative) CP fit with restarts (reference solver.py:340-403).
 
     Same semantics as the reference: per outer iteration ``inner_sweeps``
@@ -167,6 +168,12 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
     projection, dual ascent, residuals, adaptation and the stop test; restarts
     from fresh seeds on non-convergence; the model is the auxiliary copies and
     ``rfe`` is computed by explicit reconstruction (fp64 accumulation).
+
+    ``rho_schedule`` (verification hook, not part of the reference API): an
+    ``[n_max, 3]`` penalty sequence to replay instead of adapting, so a
+    trajectory can be compared iteration by iteration with the reference's
+    even where the adaptation rule's branch is decided by rounding noise
+    (``p > 0`` at p ~ 1e-17, solver.py:286-291).
     """
     from .engine import DeviceProblem, device_tensor, sq_error
 
@@ -180,7 +187,7 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
     if x_norm == 0.0:
         raise ValueError("cannot factorize a zero tensor")
     prob = DeviceProblem(x, t.dims, rank, config, history_capacity=config.n_max,
-                         engine=_engine_code(engine))
+                         engine=_engine_code(engine), rho_schedule=rho_schedule)
     try:
         return _run_fit(prob, x, t.dims, rank, config, x_norm)
     finally:
