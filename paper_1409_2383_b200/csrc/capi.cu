@@ -97,6 +97,10 @@ struct ntf_plan {
   unsigned* done = nullptr;
   cudaStream_t capture_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
+  // ridge factorisation runs on a side stream concurrently with the MTTKRP
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  double* ridge = nullptr;  // [R*R + R]
   // per-launch timing events: 3 per mode update (before MTTKRP, after MTTKRP,
   // after the row update), inner_sweeps * 3 mode updates per iteration
   int timing = 0;
@@ -123,6 +127,22 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   const int m = mode - 1;
   const int R = d.rank;
   const int64_t* xd = d.x_dims[m];
+  // companions, highest mode first (solver.py:196-204)
+  static const int comp[3][2] = {{2, 1}, {2, 0}, {1, 0}};
+  // fork: ridge Cholesky (solver.py:167-175) on the side stream
+  ntf::RidgeParams rp{};
+  rp.mode = mode;
+  rp.R = R;
+  rp.Ga = d.grams[comp[m][0]];
+  rp.Gb = d.grams[comp[m][1]];
+  rp.rho = d.rho;
+  rp.L = pl->ridge;
+  rp.status = d.counters + 2;
+  rp.stop_flag = d.counters + 1;
+  NTF_CUDA_TRY(cudaEventRecord(pl->fork_ev, s));
+  NTF_CUDA_TRY(cudaStreamWaitEvent(pl->side, pl->fork_ev, 0));
+  NTF_CUDA_TRY(ntf::ridge_factor_launch(rp, pl->side));
+  NTF_CUDA_TRY(cudaEventRecord(pl->join_ev, pl->side));
   cudaEvent_t* ev = nullptr;
   if (pl->timing && pl->events) {
     ev = pl->events + 3 * pl->cursor;
@@ -132,8 +152,7 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2], d.factors[0],
                       d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s));
   if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
-  // companions, highest mode first (solver.py:196-204)
-  static const int comp[3][2] = {{2, 1}, {2, 0}, {1, 0}};
+  NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
   ntf::FactorUpdateParams fp{};
   fp.mode = mode;
   fp.R = R;
@@ -141,8 +160,7 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   fp.row_offset = d.row_offset[m];
   fp.mtt = pl->mtt_ws;
   fp.splits = pl->op[m].splits();
-  fp.Ga = d.grams[comp[m][0]];
-  fp.Gb = d.grams[comp[m][1]];
+  fp.Lg = pl->ridge;
   fp.rho = d.rho;
   fp.F = d.factors[m];
   fp.aux = d.aux[m];
@@ -294,7 +312,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     const int64_t* xd = d.x_dims[m];
     pl->op[m] = make_op(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R, d.engine);
     ws = std::max(ws, pl->op[m].ws_bytes(R));
-    pl->blocks[m] = ntf::factor_update_blocks(d.row_count[m]);
+    pl->blocks[m] = ntf::factor_update_blocks(d.row_count[m], R);
     maxb = std::max(maxb, pl->blocks[m]);
     max_rows = std::max(max_rows, d.dims[m]);
   }
@@ -310,6 +328,14 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaMalloc gram"));
   if ((e = cudaMalloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc gram ws"));
+  if ((e = cudaMalloc(&pl->ridge, sizeof(double) * (R * R + R))) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc ridge"));
+  if ((e = cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaStreamCreate"));
+  if ((e = cudaEventCreateWithFlags(&pl->fork_ev, cudaEventDisableTiming)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaEventCreate"));
+  if ((e = cudaEventCreateWithFlags(&pl->join_ev, cudaEventDisableTiming)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaEventCreate"));
   if ((e = cudaMalloc(&pl->done, sizeof(unsigned) * 4)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc counters"));
   if ((e = cudaMemset(pl->done, 0, sizeof(unsigned) * 4)) != cudaSuccess)
@@ -432,6 +458,10 @@ void ntf_plan_destroy(ntf_plan* pl) {
   free_events(pl);
   if (pl->graph) cudaGraphExecDestroy(pl->graph);
   if (pl->capture_stream) cudaStreamDestroy(pl->capture_stream);
+  if (pl->side) cudaStreamDestroy(pl->side);
+  if (pl->fork_ev) cudaEventDestroy(pl->fork_ev);
+  if (pl->join_ev) cudaEventDestroy(pl->join_ev);
+  cudaFree(pl->ridge);
   cudaFree(pl->mtt_ws);
   cudaFree(pl->norm_partials);
   cudaFree(pl->gram_partials);

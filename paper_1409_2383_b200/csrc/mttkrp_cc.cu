@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
         } else {
           const int e2 = e - nh;
           const int qq = e2 / vpr, v = e2 - (e2 / vpr) * vpr;
-          const uint32_t lo = (l0 + qq) % L;
+          uint32_t lo = l0 + qq;
+          lo = L >= kBQ ? (lo >= L ? lo - L : lo) : lo % L;
           cp_async_cg16(ls + qq * R2 + 2 * v, p.Flo + static_cast<int64_t>(lo) * R + 2 * v, true);
         }
       }
@@ -206,16 +207,24 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
     const uint32_t l0 = q0 - h0 * L;
     const double* hs = hi_rows(s);
     const double* ls = lo_rows(s);
-    for (int qq = warp; qq < kBQ; qq += nwarps) {
-      const uint32_t q = q0 + qq;
-      const bool qv = q < p.Q;
-      const int hoff = static_cast<int>((l0 + qq) / L);
-      const double* fh = hs + hoff * R2;
-      const double* fl = ls + qq * R2;
+    // batches of 4 q-rows per warp: all shared loads issued before the math
+    for (int qb = warp * 4; qb < kBQ; qb += nwarps * 4) {
       for (int r = lane; r < R_pad; r += 32) {
-        XT w = XT(0);
-        if (qv && r < R) w = static_cast<XT>(fh[r] * fl[r]);
-        dst[qq * R_pad + r] = w;
+        double a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = qb + u;
+          const uint32_t lsum = l0 + qq;
+          const int hoff = L >= kBQ ? (lsum >= L ? 1 : 0) : static_cast<int>(lsum / L);
+          const bool ok = qq < kBQ && r < R;
+          a[u] = ok ? hs[hoff * R2 + r] : 0.0;
+          b[u] = ok ? ls[qq * R2 + r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = qb + u;
+          if (qq < kBQ) dst[qq * R_pad + r] = (q0 + qq < p.Q) ? static_cast<XT>(a[u] * b[u]) : XT(0);
+        }
       }
     }
   };

@@ -9,7 +9,9 @@ namespace ntf {
 namespace {
 
 constexpr int kUpdThreads = 256;
-constexpr int kRowsPerBlock = 32;
+// rows per update block: enough rows that the per-block Gram partials stay
+// few, small enough that R x R + 2 x rows x R doubles fit in shared memory
+__host__ __device__ __forceinline__ int rows_per_block(int R) { return R <= 64 ? 64 : 32; }
 
 // ---------------------------------------------------------------------------
 // Ridge Cholesky in shared memory (solver.ridge_cholesky, solver.py:167-175):
@@ -59,19 +61,41 @@ __device__ void build_and_factor(double* L, int ldl, int R, const double* __rest
   __syncthreads();
 }
 
+// One block: H = G_a o G_b + rho I, Cholesky, then L (row-major R x R, lower)
+// and 1/diag(L) to global for the row-update kernel.  Runs concurrently with
+// the mode's MTTKRP (it only depends on the companion Grams and rho).
+__global__ void ridge_factor_kernel(RidgeParams p) {
+  if (p.stop_flag && *p.stop_flag) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int R = p.R;
+  const int ldl = R + 1;
+  double* L = reinterpret_cast<double*>(smem_raw);
+  __shared__ bool bad;
+  if (threadIdx.x == 0) bad = false;
+  __syncthreads();
+  build_and_factor(L, ldl, R, p.Ga, p.Gb, p.rho[p.mode - 1], p.status, &bad);
+  if (bad) return;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    p.L[e] = k <= i ? L[i * ldl + k] : 0.0;
+  }
+  for (int j = threadIdx.x; j < R; j += blockDim.x) p.L[R * R + j] = 1.0 / L[j * ldl + j];
+}
+
 // Row solve of X (L L^T) = rhs for one row held by a warp: lane owns entries
 // r = lane + 32*t, t < RT.  Column-oriented forward then backward
-// substitution (solver.solve_factor_rows / cho_solve, solver.py:182-188).
+// substitution (solver.solve_factor_rows / cho_solve, solver.py:182-188),
+// dividing by the diagonal through its precomputed reciprocal.
 template <int RT>
 __device__ __forceinline__ void warp_chol_solve(double (&y)[RT], const double* L, int ldl, int R,
-                                                int lane) {
+                                                const double* inv_diag, int lane) {
   // forward: L z = y
 #pragma unroll
   for (int s = 0; s < RT; ++s) {
     for (int kk = 0; kk < 32; ++kk) {
       const int k = s * 32 + kk;
       if (k >= R) break;
-      double zk = y[s] / L[k * ldl + k];
+      double zk = y[s] * inv_diag[k];
       zk = __shfl_sync(0xffffffffu, zk, kk);
       if (lane == kk) y[s] = zk;
 #pragma unroll
@@ -87,7 +111,7 @@ __device__ __forceinline__ void warp_chol_solve(double (&y)[RT], const double* L
     for (int kk = 31; kk >= 0; --kk) {
       const int k = s * 32 + kk;
       if (k >= R) continue;
-      double xk = y[s] / L[k * ldl + k];
+      double xk = y[s] * inv_diag[k];
       xk = __shfl_sync(0xffffffffu, xk, kk);
       if (lane == kk) y[s] = xk;
 #pragma unroll
@@ -106,12 +130,19 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   const int R = p.R;
   const int ldl = R + 1;  // odd pitch: conflict-free row and column walks
   double* L = reinterpret_cast<double*>(smem_raw);
-  double* xrows = L + R * ldl;                  // [kRowsPerBlock][R]
-  double* msum = xrows + kRowsPerBlock * R;     // [kRowsPerBlock][R] reduced MTTKRP rows
+  double* inv_diag = L + R * ldl;               // [R]
+  const int kRowsPerBlock = rows_per_block(R);
+  double* xrows = inv_diag + R;                 // [rows][R] new factor rows
+  double* msum = xrows + kRowsPerBlock * R;     // [rows][R] reduced MTTKRP rows
   double* red = msum + kRowsPerBlock * R;       // [8 warps][5]
-  __shared__ bool bad;
   __shared__ bool is_last;
-  if (threadIdx.x == 0) bad = false;
+  // Ridge factor from the concurrent ridge_factor_kernel (solver.py:167-175)
+  if (*p.status == kDevNotPD) return;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    L[i * ldl + k] = p.Lg[e];
+  }
+  for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
 
   const int64_t row_base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
   const int64_t n_rows = p.rows;
@@ -131,13 +162,11 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   }
 
   const double rho = p.rho[p.mode - 1];
-  build_and_factor(L, ldl, R, p.Ga, p.Gb, rho, p.status, &bad);
-  if (bad) return;
+  __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = kUpdThreads / 32;
-  const double inv_rho = 1.0 / rho;
 
   double nrm[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int lr = warp; lr < kRowsPerBlock; lr += nwarps) {
@@ -154,7 +183,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
           y[t] = (msum[lr * R + r] + rho * p.aux[e]) - p.dual[e];
         }
       }
-      warp_chol_solve<RT>(y, L, ldl, R, lane);
+      warp_chol_solve<RT>(y, L, ldl, R, inv_diag, lane);
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int r = lane + 32 * t;
@@ -168,7 +197,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
             // Y += rho (F - aux) (solver.py:315-317), residual partials (247-255)
             const double yd = p.dual[e];
             const double a_old = p.aux[e];
-            const double v = x + yd * inv_rho;
+            const double v = x + yd / rho;
             if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
             const double a = v > 0.0 ? v : 0.0;
             const double ynew = yd + rho * (x - a);
@@ -435,18 +464,30 @@ int sm_count() {
 // ---------------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------------
-int factor_update_blocks(int64_t rows) {
-  return static_cast<int>((rows + kRowsPerBlock - 1) / kRowsPerBlock);
+int factor_update_blocks(int64_t rows, int R) {
+  const int rpb = rows_per_block(R);
+  return static_cast<int>((rows + rpb - 1) / rpb);
 }
 
 size_t factor_update_smem(int R) {
-  return (static_cast<size_t>(R) * (R + 1) + 2 * static_cast<size_t>(kRowsPerBlock) * R + 8 * 5) *
+  const int rpb = rows_per_block(R);
+  return (static_cast<size_t>(R) * (R + 1) + R + 2 * static_cast<size_t>(rpb) * R + 8 * 5) *
          sizeof(double);
+}
+
+size_t ridge_factor_smem(int R) { return static_cast<size_t>(R) * (R + 1) * sizeof(double); }
+
+cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream) {
+  ridge_factor_kernel<<<1, 256, ridge_factor_smem(p.R), stream>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t factor_update_prepare(int R) {
   const int smem = static_cast<int>(factor_update_smem(R));
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(ridge_factor_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(ridge_factor_smem(R)));
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(factor_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(factor_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -458,7 +499,7 @@ cudaError_t factor_update_prepare(int R) {
 }
 
 cudaError_t factor_update_launch(const FactorUpdateParams& p, cudaStream_t stream) {
-  const int blocks = factor_update_blocks(p.rows);
+  const int blocks = factor_update_blocks(p.rows, p.R);
   const size_t smem = factor_update_smem(p.R);
   const int rt = (p.R + 31) / 32;
   switch (rt) {

@@ -14,8 +14,7 @@ struct FactorUpdateParams {
   int64_t row_offset;       // first owned row within the full factor
   const double* mtt;        // [splits][rows][R] MTTKRP partials
   int splits;
-  const double* Ga;         // companion Grams (highest mode first)
-  const double* Gb;
+  const double* Lg;         // ridge factor from ridge_factor_kernel
   const double* rho;        // device [3]
   double* F;                // full factor (rows written at row_offset)
   double* aux;              // owned rows
@@ -45,7 +44,19 @@ struct FinalizeParams {
   const double* rho_schedule;  // optional [cap][3] replayed penalties
 };
 
-int factor_update_blocks(int64_t rows);
+struct RidgeParams {
+  int mode, R;
+  const double* Ga;         // companion Grams (highest mode first)
+  const double* Gb;
+  const double* rho;        // device [3]
+  double* L;                // out: [R*R] lower factor + [R] 1/diag
+  int* status;
+  const int* stop_flag;
+};
+
+int factor_update_blocks(int64_t rows, int R);
+size_t ridge_factor_smem(int R);
+cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream);
 size_t factor_update_smem(int R);
 cudaError_t factor_update_prepare(int R);
 cudaError_t factor_update_launch(const FactorUpdateParams& p, cudaStream_t stream);
