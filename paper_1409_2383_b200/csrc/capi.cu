@@ -44,10 +44,14 @@ int check_dims(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
   return NTF_OK;
 }
 
-bool use_tc(int engine, int x_dtype, int R) {
+bool tc_ok(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
+  return ntf::mttkrp_tc_supported(x_dtype, R) && ntf::mttkrp_tc_shape_ok(mode, I, J, K);
+}
+
+bool use_tc(int engine, int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
   if (engine == NTF_ENGINE_CUDA_CORE) return false;
-  if (engine == NTF_ENGINE_TCGEN05) return true;
-  return ntf::mttkrp_tc_auto(x_dtype, R);
+  if (engine == NTF_ENGINE_TCGEN05) return tc_ok(mode, x_dtype, I, J, K, R);
+  return ntf::mttkrp_tc_auto(x_dtype, R) && tc_ok(mode, x_dtype, I, J, K, R);
 }
 
 // One MTTKRP engine instance for one (mode, shape): geometry + launcher.
@@ -55,6 +59,7 @@ struct MttkrpOp {
   bool tc = false;
   ntf::MttkrpCCLaunch cc{};
   ntf::MttkrpTCLaunch tcl{};
+  const ntf::TcTensor* tct = nullptr;  // fp16 split planes (tensor-core engine)
   int splits() const { return tc ? tcl.splits : cc.groups; }
   size_t ws_bytes(int R) const {
     return tc ? ntf::mttkrp_tc_workspace_bytes(tcl, R) : ntf::mttkrp_cc_workspace_bytes(cc, R);
@@ -63,7 +68,7 @@ struct MttkrpOp {
 
 MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, int engine) {
   MttkrpOp op;
-  op.tc = use_tc(engine, x_dtype, R);
+  op.tc = use_tc(engine, mode, x_dtype, I, J, K, R);
   if (op.tc)
     op.tcl = ntf::mttkrp_tc_plan(mode, x_dtype, I, J, K, R);
   else
@@ -74,7 +79,7 @@ MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, 
 cudaError_t run_op(const MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
                    const int* stop, cudaStream_t s) {
-  if (op.tc) return ntf::mttkrp_tc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.tcl, ws, stop, s);
+  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, ws, stop, s);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
 }
 
@@ -101,6 +106,9 @@ struct ntf_plan {
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   double* ridge = nullptr;  // [R*R + R]
+  // fp16 split planes for the tensor-core engine, one per distinct slab
+  ntf::TcTensor tct[3];
+  int n_tct = 0;
   // per-launch timing events: 3 per mode update (before MTTKRP, after MTTKRP,
   // after the row update), inner_sweeps * 3 mode updates per iteration
   int timing = 0;
@@ -234,15 +242,31 @@ int ntf_mttkrp(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64
   if (!X || !out || !workspace) return fail(NTF_ERR_INVALID, "null pointer");
   if ((mode != 1 && !A) || (mode != 2 && !B) || (mode != 3 && !C))
     return fail(NTF_ERR_INVALID, "missing companion factor");
-  if (engine == NTF_ENGINE_TCGEN05 && !ntf::mttkrp_tc_supported(x_dtype, R))
-    return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank");
-  const MttkrpOp op = make_op(mode, x_dtype, I, J, K, R, engine);
+  if (engine == NTF_ENGINE_TCGEN05 && !tc_ok(mode, x_dtype, I, J, K, R))
+    return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank/shape");
+  MttkrpOp op = make_op(mode, x_dtype, I, J, K, R, engine);
   if (workspace_bytes < op.ws_bytes(R)) return fail(NTF_ERR_INVALID, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* ws = static_cast<double*>(workspace);
   NTF_CUDA_TRY(prepare_op(op, mode, x_dtype));
-  NTF_CUDA_TRY(run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s));
   const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
+  if (op.tc) {
+    // one-shot call: split the tensor into its fp16 planes for this call only
+    // (a solver plan does this once); synchronises before releasing them.
+    ntf::TcTensor t;
+    const int64_t dims[3] = {I, J, K};
+    NTF_CUDA_TRY(ntf::tc_tensor_create(static_cast<const float*>(X), dims, &t, s));
+    cudaError_t e = ntf::mttkrp_tc_bind(op.tcl, t);
+    op.tct = &t;
+    if (e == cudaSuccess) e = run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s);
+    if (e == cudaSuccess) e = ntf::mttkrp_reduce_launch(ws, op.splits(), M, R, out, nullptr, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    ntf::mttkrp_tc_unbind(op.tcl);
+    ntf::tc_tensor_destroy(&t);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 mttkrp");
+    return NTF_OK;
+  }
+  NTF_CUDA_TRY(run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s));
   NTF_CUDA_TRY(ntf::mttkrp_reduce_launch(ws, op.splits(), M, R, out, nullptr, s));
   return NTF_OK;
 }
@@ -299,8 +323,10 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     for (int a = 0; a < 3; ++a)
       if (a != m && xd[a] != d.dims[a]) return fail(NTF_ERR_INVALID, "slab companion extent");
   }
-  if (d.engine == NTF_ENGINE_TCGEN05 && !ntf::mttkrp_tc_supported(d.x_dtype, R))
-    return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank");
+  for (int m = 0; m < 3; ++m)
+    if (d.engine == NTF_ENGINE_TCGEN05 &&
+        !tc_ok(m + 1, d.x_dtype, d.x_dims[m][0], d.x_dims[m][1], d.x_dims[m][2], R))
+      return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank/shape");
 
   ntf_plan* pl = new (std::nothrow) ntf_plan();
   if (!pl) return fail(NTF_ERR_INVALID, "out of host memory");
@@ -344,6 +370,33 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   for (int m = 0; m < 3; ++m) {
     if ((e = prepare_op(pl->op[m], m + 1, d.x_dtype)) != cudaSuccess)
       return cleanup(cuda_fail(e, "mttkrp prepare"));
+  }
+  // Tensor-core engine: split each distinct slab once into its fp16 planes
+  // (one-time setup; synchronous so the caller's upload stream is irrelevant).
+  bool any_tc = false;
+  for (int m = 0; m < 3; ++m) any_tc = any_tc || pl->op[m].tc;
+  if (any_tc) {
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
+    for (int m = 0; m < 3; ++m) {
+      if (!pl->op[m].tc) continue;
+      int found = -1;
+      for (int k = 0; k < m; ++k)
+        if (d.x_mode[k] == d.x_mode[m] && pl->op[k].tc) found = k;
+      const ntf::TcTensor* t = nullptr;
+      if (found >= 0) {
+        t = pl->op[found].tct;
+      } else {
+        ntf::TcTensor& slot = pl->tct[pl->n_tct++];
+        if ((e = ntf::tc_tensor_create(static_cast<const float*>(d.x_mode[m]), d.x_dims[m], &slot,
+                                       nullptr)) != cudaSuccess)
+          return cleanup(cuda_fail(e, "tc split"));
+        t = &slot;
+      }
+      pl->op[m].tct = t;
+      if ((e = ntf::mttkrp_tc_bind(pl->op[m].tcl, *t)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "tc tensor map"));
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
   }
   *out = pl;
   return NTF_OK;
@@ -462,6 +515,9 @@ void ntf_plan_destroy(ntf_plan* pl) {
   if (pl->fork_ev) cudaEventDestroy(pl->fork_ev);
   if (pl->join_ev) cudaEventDestroy(pl->join_ev);
   cudaFree(pl->ridge);
+  for (int m = 0; m < 3; ++m)
+    if (pl->op[m].tc) ntf::mttkrp_tc_unbind(pl->op[m].tcl);
+  for (int k = 0; k < pl->n_tct; ++k) ntf::tc_tensor_destroy(&pl->tct[k]);
   cudaFree(pl->mtt_ws);
   cudaFree(pl->norm_partials);
   cudaFree(pl->gram_partials);

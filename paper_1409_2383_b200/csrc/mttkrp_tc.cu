@@ -1,22 +1,747 @@
-// tcgen05 MTTKRP — not yet enabled in this build (the AUTO engine never
-// selects it; an explicit request returns NTF_ERR_UNSUPPORTED).
+// Dense MTTKRP on the 5th-generation tensor cores (tcgen05, sm_100a) for fp32
+// tensors.  Same contraction as mttkrp_cc.cu (reference tensors.py:254-262):
+//   out[m, n] = sum_q X(m, q) W(q, n),  W(q, n) = F_hi[q_hi, n] * F_lo[q_lo, n]
+//
+// Numerics: exact fixed-point slicing on kind::f16 MMAs.
+//   X  = xs * (S0 + S1)          S0 integers |S0| <= 2^11, S1 in 2^-11 units,
+//                                xs = 2^(e-11) global (computed once per tensor)
+//   W  = ws(n) * (T0 + T1 + T2)  T0 integers |T0| <= 2^7, T1 in 2^-7 and T2 in
+//                                2^-14 units, ws(n) = 2^(f(n)-7) per column
+// All slices are exact fp16 values.  Per 64-wide q chunk the tensor core forms
+//   ACC0 = sum S0*T0                          (integers < 2^24: EXACT in fp32)
+//   ACC1 = sum S0*T1 + S1*T0 + S0*T2 + S1*T1  (a 2^-7-scaled correction)
+// so the dominant term carries no accumulation rounding at all (whatever the
+// tensor core's rounding mode), and the correction's rounding is ~2^-29 of the
+// result.  The epilogue folds ACC0 into a double-float accumulator (Fast2Sum)
+// and ACC1 into its low word; dropped terms (S1*T2 ~ 2^-25, slice residues
+// ~2^-23 of the column/tensor maxima) are i.i.d. per element, never a
+// structured rounding of the factors (SURVEY 8(d) precision findings).
+//
+// Pipeline (one CTA per SM, warp-specialised, mbarrier handshakes):
+//   warp 0      TMA producer: S0/S1 tiles (128 rows x 64 q, 128B-swizzled)
+//   warp 1      TMEM allocator + single-thread MMA issuer (tcgen05.mma)
+//   warps 2..   KR formers: W slices of the chunk from the fp64 factors,
+//               written in the UMMA K-major SW128 layout
+//   last 4      epilogue: tcgen05.ld of the two accumulators (double-buffered
+//               in TMEM), double-float accumulation, fp64 partial per split.
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
 #include "mttkrp_tc.cuh"
 
 namespace ntf {
 
-bool mttkrp_tc_supported(int, int) { return false; }
-bool mttkrp_tc_auto(int, int) { return false; }
-MttkrpTCLaunch mttkrp_tc_plan(int mode, int, int64_t, int64_t, int64_t, int) {
+namespace {
+
+constexpr int kTM = 128;     // MMA M (rows per tile, TMEM lanes)
+constexpr int kBK = 64;      // q per chunk (fp16: 128 B rows, one SW128 atom)
+constexpr int kUK = 16;      // MMA K for kind::f16
+constexpr int kEpiWarps = 4;
+
+// ----------------------------------------------------------------------------
+// PTX wrappers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 32 bits, 16 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
+__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: F16 x F16 -> F32, M=128
+__host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
+  return (1u << 4)                                 // D format F32
+         | (0u << 7) | (0u << 10)                  // A, B format F16
+         | ((a_mn_major ? 1u : 0u) << 15)          // A major
+         | (0u << 16)                              // B K-major
+         | ((static_cast<uint32_t>(N) >> 3) << 17) // N >> 3
+         | ((static_cast<uint32_t>(kTM) >> 4) << 24);  // M >> 4
+}
+
+struct TcParams {
+  CUtensorMap tmap0;
+  CUtensorMap tmap1;
+  int mode, R, N;
+  int64_t M, P, K;           // P = I*J (mode 3 reduction length)
+  uint32_t lo_extent;        // mode 3: J
+  int64_t n_chunks, chunks_per_split, chunks_per_o;
+  int n_mtiles, splits;
+  int x_stages, w_stages, n_wf;
+  const double* Fhi;
+  const double* Flo;
+  const double* wscale;      // [N] 2^(7 - f(n)),  [N..2N) output scale (with xscale)
+  double* ws;                // [splits * n_mtiles][M][R] partials (split-major)
+  const int* stop_flag;
+};
+
+__device__ __forceinline__ void fast_two_sum(float& hi, float& lo, float a) {
+  const float s = hi + a;
+  const float err = a - (s - hi);
+  hi = s;
+  lo += err;
+}
+
+// W slices for one (n, 8-q octet): 3 x 16 bytes at the swizzled positions.
+__device__ __forceinline__ void emit_w_octet(unsigned char* t0, unsigned char* t1, unsigned char* t2,
+                                             int n, int oct, const double (&w)[8]) {
+  __align__(16) __half h0[8], h1[8], h2[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double t = w[u];
+    const double a0 = rint(t);
+    const float r1 = static_cast<float>((t - a0) * 128.0);  // |r1| <= 64, exact to 2^-18
+    const float a1 = rintf(r1);
+    const float a2 = rintf((r1 - a1) * 128.0f);
+    h0[u] = __float2half_rn(static_cast<float>(a0));        // integer <= 128: exact
+    h1[u] = __float2half_rn(a1 * 0.0078125f);               // 2^-7 units: exact
+    h2[u] = __float2half_rn(a2 * 6.103515625e-05f);         // 2^-14 units: exact
+  }
+  const int off = n * 128 + ((oct ^ (n & 7)) << 4);
+  *reinterpret_cast<uint4*>(t0 + off) = *reinterpret_cast<const uint4*>(h0);
+  *reinterpret_cast<uint4*>(t1 + off) = *reinterpret_cast<const uint4*>(h1);
+  *reinterpret_cast<uint4*>(t2 + off) = *reinterpret_cast<const uint4*>(h2);
+}
+
+template <int NT>  // N / 16
+__global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
+  constexpr int N = NT * 16;
+  if (p.stop_flag && *p.stop_flag) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // carve: [X stages: S0 16KB | S1 16KB] [W stages: T0 | T1 | T2 (N*128 each)] [barriers]
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int kXTile = kTM * kBK * 2;  // 16 KB
+  constexpr int kWTile = N * kBK * 2;    // N * 128 B
+  const int SX = p.x_stages, SW = p.w_stages;
+  unsigned char* xbase = base;
+  unsigned char* wbase = xbase + SX * 2 * kXTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + SW * 3 * kWTile);
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = x_full + SX;
+  uint64_t* w_full = x_empty + SX;
+  uint64_t* w_empty = w_full + SW;
+  uint64_t* acc_full = w_empty + SW;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_wf = p.n_wf;
+  const int wf_first = 2;
+  const int epi_first = 2 + n_wf;
+  const int n_wf_threads = n_wf * 32;
+
+  const int tile = blockIdx.x % p.n_mtiles;
+  const int split = blockIdx.x / p.n_mtiles;
+  const int64_t m0 = static_cast<int64_t>(tile) * kTM;
+  const int64_t c_begin = static_cast<int64_t>(split) * p.chunks_per_split;
+  int64_t c_end = c_begin + p.chunks_per_split;
+  if (c_end > p.n_chunks) c_end = p.n_chunks;
+  const int n_iter = c_begin < c_end ? static_cast<int>(c_end - c_begin) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SX; ++s) {
+      mbar_init(&x_full[s], 1);
+      mbar_init(&x_empty[s], 1);
+    }
+    for (int s = 0; s < SW; ++s) {
+      mbar_init(&w_full[s], n_wf_threads);
+      mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kEpiWarps * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    const uint32_t ncols = 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it % SX;
+        mbar_wait(&x_empty[s], ((it / SX) & 1) ^ 1);
+        unsigned char* d0 = xbase + s * 2 * kXTile;
+        unsigned char* d1 = d0 + kXTile;
+        mbar_arrive_expect_tx(&x_full[s], 2 * kXTile);
+        const int64_t c = c_begin + it;
+        if (p.mode == 3) {
+          const int p0 = static_cast<int>(c * kBK);
+          const int k0 = static_cast<int>(m0);
+          tma_load_2d(d0, &p.tmap0, &x_full[s], k0, p0);
+          tma_load_2d(d0 + kXTile / 2, &p.tmap0, &x_full[s], k0 + 64, p0);
+          tma_load_2d(d1, &p.tmap1, &x_full[s], k0, p0);
+          tma_load_2d(d1 + kXTile / 2, &p.tmap1, &x_full[s], k0 + 64, p0);
+        } else {
+          const int o = static_cast<int>(c / p.chunks_per_o);
+          const int k0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
+          if (p.mode == 1) {
+            tma_load_3d(d0, &p.tmap0, &x_full[s], k0, o, static_cast<int>(m0));
+            tma_load_3d(d1, &p.tmap1, &x_full[s], k0, o, static_cast<int>(m0));
+          } else {
+            tma_load_3d(d0, &p.tmap0, &x_full[s], k0, static_cast<int>(m0), o);
+            tma_load_3d(d1, &p.tmap1, &x_full[s], k0, static_cast<int>(m0), o);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer --------------------------------
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(N, p.mode == 3);
+      const bool mn = p.mode == 3;
+      for (int it = 0; it < n_iter; ++it) {
+        const int s = it % SX, sw = it % SW, ab = it & 1;
+        mbar_wait(&x_full[s], (it / SX) & 1);
+        mbar_wait(&w_full[sw], (it / SW) & 1);
+        mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const unsigned char* a0 = xbase + s * 2 * kXTile;
+        const unsigned char* a1 = a0 + kXTile;
+        const unsigned char* b0 = wbase + sw * 3 * kWTile;
+        const unsigned char* b1 = b0 + kWTile;
+        const unsigned char* b2 = b1 + kWTile;
+        const uint32_t d0 = tmem + ab * 2 * N;
+        const uint32_t d1 = d0 + N;
+#pragma unroll
+        for (int kk = 0; kk < kBK / kUK; ++kk) {
+          uint64_t da0, da1;
+          if (mn) {  // A = X^T: MN-major, atoms of 64 m (8 KB apart), 8 q-rows per 1 KB
+            da0 = smem_desc(a0 + kk * 2048, kXTile / 2, 1024);
+            da1 = smem_desc(a1 + kk * 2048, kXTile / 2, 1024);
+          } else {   // K-major: 128 B rows, 8-row groups 1 KB apart, +32 B per K step
+            da0 = smem_desc(a0 + kk * 32, 16, 1024);
+            da1 = smem_desc(a1 + kk * 32, 16, 1024);
+          }
+          const uint64_t db0 = smem_desc(b0 + kk * 32, 16, 1024);
+          const uint64_t db1 = smem_desc(b1 + kk * 32, 16, 1024);
+          const uint64_t db2 = smem_desc(b2 + kk * 32, 16, 1024);
+          const uint32_t acc = kk > 0 ? 1u : 0u;
+          tc_mma_f16(d0, da0, db0, idesc, acc);   // S0*T0   exact
+          tc_mma_f16(d1, da0, db1, idesc, acc);   // S0*T1
+          tc_mma_f16(d1, da1, db0, idesc, 1u);    // S1*T0
+          tc_mma_f16(d1, da0, db2, idesc, 1u);    // S0*T2
+          tc_mma_f16(d1, da1, db1, idesc, 1u);    // S1*T1
+        }
+        tc_commit(&x_empty[s]);
+        tc_commit(&w_empty[sw]);
+        tc_commit(&acc_full[ab]);
+      }
+    }
+  } else if (warp < epi_first) {
+    // ------------------------------ KR formers --------------------------------
+    const int t = threadIdx.x - wf_first * 32;
+    const int R = p.R;
+    const int items = N * (kBK / 8);  // (n, octet) pairs
+    for (int it = 0; it < n_iter; ++it) {
+      const int sw = it % SW;
+      mbar_wait(&w_empty[sw], ((it / SW) & 1) ^ 1);
+      unsigned char* t0 = wbase + sw * 3 * kWTile;
+      unsigned char* t1 = t0 + kWTile;
+      unsigned char* t2 = t1 + kWTile;
+      const int64_t c = c_begin + it;
+      for (int e = t; e < items; e += n_wf_threads) {
+        const int n = e / (kBK / 8);
+        const int oct = e - n * (kBK / 8);
+        double w[8];
+        const double sc = n < R ? p.wscale[n] : 0.0;
+        if (p.mode == 3) {
+          const int64_t q0 = c * kBK + oct * 8;
+          int64_t hi = q0 / p.lo_extent;
+          int64_t lo = q0 - hi * p.lo_extent;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const bool ok = n < R && q0 + u < p.P;
+            w[u] = ok ? p.Fhi[hi * R + n] * p.Flo[lo * R + n] * sc : 0.0;
+            if (++lo == p.lo_extent) {
+              lo = 0;
+              ++hi;
+            }
+          }
+        } else {
+          const int64_t o = c / p.chunks_per_o;
+          const int64_t k0 = (c - o * p.chunks_per_o) * kBK + oct * 8;
+          const double fo = n < R ? p.Fhi[o * R + n] * sc : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const bool ok = n < R && k0 + u < p.K;
+            w[u] = ok ? fo * p.Flo[(k0 + u) * R + n] : 0.0;
+          }
+        }
+        emit_w_octet(t0, t1, t2, n, oct, w);
+      }
+      fence_proxy_async();
+      mbar_arrive(&w_full[sw]);
+    }
+  } else {
+    // ------------------------------ epilogue ----------------------------------
+    const int q4 = warp & 3;          // TMEM lane quarter of this warp
+    const int row = q4 * 32 + lane;   // tile row == TMEM lane
+    float hi[N], lo[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      hi[n] = 0.f;
+      lo[n] = 0.f;
+    }
+    for (int it = 0; it < n_iter; ++it) {
+      const int ab = it & 1;
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ab * 2 * N;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        float a0[16], a1[16];
+        tmem_ld16(taddr + j * 16, a0);
+        tmem_ld16(taddr + N + j * 16, a1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          fast_two_sum(hi[j * 16 + u], lo[j * 16 + u], a0[u]);
+          lo[j * 16 + u] += a1[u];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
+    }
+    // fp64 partial of this split: out = (hi + lo) * xscale * ws(n)
+    const int64_t gm = m0 + row;
+    if (gm < p.M) {
+      double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * p.R;
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < p.R) out[n] = (static_cast<double>(hi[n]) + static_cast<double>(lo[n])) * p.wscale[N + n];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    const uint32_t ncols = 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// tensor split: max|X| then S0 / S1 planes
+// ----------------------------------------------------------------------------
+__global__ void absmax_kernel(const float* __restrict__ X, int64_t n, unsigned* out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(X[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // order-free: max is exact
+}
+
+__global__ void split_kernel(const float* __restrict__ X, int64_t n, const unsigned* amax,
+                             __half* __restrict__ s0, __half* __restrict__ s1, double* xscale) {
+  const float mx = __uint_as_float(*amax);
+  int e = 0;
+  if (mx > 0.f) frexpf(mx, &e);            // mx < 2^e
+  const float up = ldexpf(1.0f, 11 - e);   // X * 2^(11-e) in [-2048, 2048]
+  if (blockIdx.x == 0 && threadIdx.x == 0) *xscale = ldexp(1.0, e - 11);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float s = X[i] * up;              // exact (power-of-two scaling)
+    const float a0 = rintf(s);
+    const float r = (s - a0) * 2048.0f;     // exact
+    const float a1 = rintf(r);
+    s0[i] = __float2half_rn(a0);
+    s1[i] = __float2half_rn(a1 * 4.8828125e-04f);  // 2^-11 units
+  }
+}
+
+// per-column W scales: wscale[n] = 2^(7 - f(n)) with max|Fhi[:,n]| max|Flo[:,n]| <= 2^f(n);
+// wscale[N + n] = xscale * 2^(f(n) - 7)
+__global__ void wscale_kernel(const double* __restrict__ Fhi, int64_t hi_rows,
+                              const double* __restrict__ Flo, int64_t lo_rows, int R, int N,
+                              const double* xscale, double* wscale) {
+  const int n = blockIdx.x;
+  double mh = 0.0, ml = 0.0;
+  if (n < R) {
+    for (int64_t i = threadIdx.x; i < hi_rows; i += blockDim.x) mh = fmax(mh, fabs(Fhi[i * R + n]));
+    for (int64_t i = threadIdx.x; i < lo_rows; i += blockDim.x) ml = fmax(ml, fabs(Flo[i * R + n]));
+  }
+  __shared__ double sh[2][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    mh = fmax(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+    ml = fmax(ml, __shfl_xor_sync(0xffffffffu, ml, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = mh;
+    sh[1][threadIdx.x >> 5] = ml;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      mh = fmax(mh, sh[0][w]);
+      ml = fmax(ml, sh[1][w]);
+    }
+    const double prod = mh * ml;
+    int f = 0;
+    if (prod > 0.0) frexp(prod, &f);  // prod < 2^f
+    // A column that has decayed to ~1e-300 (large penalties shrink factor
+    // columns geometrically) must not overflow the 2^(7-f) slice scale: clamp,
+    // which represents it as zero (absolute error < 2^-990).
+    if (f < -1000) f = -1000;
+    wscale[n] = ldexp(1.0, 7 - f);
+    wscale[N + n] = *xscale * ldexp(1.0, f - 7);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int sm_count_tc() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int NT>
+cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
+  auto kern = mttkrp_tc_kernel<NT>;
+  if (prep) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
+  kern<<<L.n_mtiles * L.splits, L.threads, L.smem_bytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
+  switch (L.N / 16) {
+    case 1: return launch_nt<1>(p, L, stream, prep);
+    case 2: return launch_nt<2>(p, L, stream, prep);
+    case 3: return launch_nt<3>(p, L, stream, prep);
+    case 4: return launch_nt<4>(p, L, stream, prep);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// host API
+// ----------------------------------------------------------------------------
+bool mttkrp_tc_supported(int x_dtype, int R) { return x_dtype == NTF_F32 && R >= 1 && R <= 64; }
+
+bool mttkrp_tc_auto(int x_dtype, int R) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* env = getenv("NTF_B200_TC");
+    enabled = env ? (env[0] != '0') : 1;
+  }
+  return enabled && mttkrp_tc_supported(x_dtype, R);
+}
+
+bool mttkrp_tc_shape_ok(int mode, int64_t I, int64_t J, int64_t K) {
+  // TMA global strides are multiples of 16 B (K % 8 == 0 for fp16 planes);
+  // coordinates are int32.
+  if (K % 8 != 0) return false;
+  if (I > (1 << 30) || J > (1 << 30) || K > (1 << 30)) return false;
+  if (mode == 3 && I * J >= (int64_t(1) << 31)) return false;
+  return true;
+}
+
+MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
+  (void)x_dtype;
   MttkrpTCLaunch L{};
   L.mode = mode;
+  L.R = R;
+  L.N = ((R + 15) / 16) * 16;
+  L.M = mode == 1 ? I : (mode == 2 ? J : K);
+  L.Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
+  L.n_mtiles = static_cast<int>((L.M + kTM - 1) / kTM);
+  if (mode == 3) {
+    L.chunks_per_o = 0;
+    L.n_chunks = (I * J + kBK - 1) / kBK;
+  } else {
+    L.chunks_per_o = (K + kBK - 1) / kBK;
+    L.n_chunks = (mode == 1 ? J : I) * L.chunks_per_o;
+  }
+  L.n_wf_warps = 4;
+  L.threads = (2 + L.n_wf_warps + kEpiWarps) * 32;
+  L.x_stages = 4;
+  L.w_stages = 3;
+  const int xs = 2 * kTM * kBK * 2;
+  const int wsz = 3 * L.N * kBK * 2;
+  L.smem_bytes = 1024 + L.x_stages * xs + L.w_stages * wsz + 256;
+  if (L.smem_bytes > 227 * 1024) {
+    L.x_stages = 3;
+    L.smem_bytes = 1024 + L.x_stages * xs + L.w_stages * wsz + 256;
+  }
+  // one CTA per SM; split the chunk range so that the grid is one wave
+  const int sms = sm_count_tc();
+  int splits = sms / L.n_mtiles;
+  if (splits < 1) splits = 1;
+  if (splits > L.n_chunks) splits = static_cast<int>(L.n_chunks);
+  L.chunks_per_split = (L.n_chunks + splits - 1) / splits;
+  L.splits = static_cast<int>((L.n_chunks + L.chunks_per_split - 1) / L.chunks_per_split);
+  L.wscale = nullptr;
+  L.bound = false;
   return L;
 }
-size_t mttkrp_tc_workspace_bytes(const MttkrpTCLaunch&, int) { return 0; }
-cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch&) { return cudaErrorNotSupported; }
-cudaError_t mttkrp_tc_launch(int, int, const void*, int64_t, int64_t, int64_t, const double*,
-                             const double*, const double*, int, const MttkrpTCLaunch&, double*,
-                             const int*, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+size_t mttkrp_tc_workspace_bytes(const MttkrpTCLaunch& L, int R) {
+  return static_cast<size_t>(L.splits) * L.M * R * sizeof(double);
+}
+
+cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L) {
+  TcParams p{};
+  return dispatch_tc(p, L, nullptr, true);
+}
+
+cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* out,
+                             cudaStream_t stream) {
+  const int64_t n = dims[0] * dims[1] * dims[2];
+  TcTensor t;
+  for (int i = 0; i < 3; ++i) t.dims[i] = dims[i];
+  cudaError_t e;
+  if ((e = cudaMalloc(&t.s0, n * sizeof(__half))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.s1, n * sizeof(__half))) != cudaSuccess) {
+    tc_tensor_destroy(&t);
+    return e;
+  }
+  unsigned* amax = nullptr;
+  if ((e = cudaMalloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
+    tc_tensor_destroy(&t);
+    return e;
+  }
+  amax = reinterpret_cast<unsigned*>(t.xscale + 1);
+  cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
+  const int blocks = 4 * sm_count_tc();
+  absmax_kernel<<<blocks, 256, 0, stream>>>(X, n, amax);
+  split_kernel<<<blocks, 256, 0, stream>>>(X, n, amax, t.s0, t.s1, t.xscale);
+  if ((e = cudaGetLastError()) != cudaSuccess) {
+    tc_tensor_destroy(&t);
+    return e;
+  }
+  *out = t;
+  return cudaSuccess;
+}
+
+void tc_tensor_destroy(TcTensor* t) {
+  if (!t) return;
+  cudaFree(t->s0);
+  cudaFree(t->s1);
+  cudaFree(t->xscale);
+  t->s0 = t->s1 = nullptr;
+  t->xscale = nullptr;
+}
+
+cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
+  auto enc = get_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
+  CUresult r0, r1;
+  if (L.mode == 3) {
+    cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(I * J)};
+    cuuint64_t gstr[1] = {static_cast<cuuint64_t>(K * 2)};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, t.s0, gdim, gstr, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, t.s1, gdim, gstr, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t gdim[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(J),
+                          static_cast<cuuint64_t>(I)};
+    cuuint64_t gstr[2] = {static_cast<cuuint64_t>(K * 2), static_cast<cuuint64_t>(J * K * 2)};
+    cuuint32_t box[3];
+    if (L.mode == 1) {
+      box[0] = 64; box[1] = 1; box[2] = 128;
+    } else {
+      box[0] = 64; box[1] = 128; box[2] = 1;
+    }
+    cuuint32_t es[3] = {1, 1, 1};
+    r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s0, gdim, gstr, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s1, gdim, gstr, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  if (!L.wscale) {
+    cudaError_t e = cudaMalloc(&L.wscale, sizeof(double) * 2 * L.N);
+    if (e != cudaSuccess) return e;
+  }
+  L.bound = true;
+  return cudaSuccess;
+}
+
+void mttkrp_tc_unbind(MttkrpTCLaunch& L) {
+  cudaFree(L.wscale);
+  L.wscale = nullptr;
+  L.bound = false;
+}
+
+cudaError_t mttkrp_tc_launch(const MttkrpTCLaunch& L, const TcTensor& t, const double* A,
+                             const double* B, const double* C, double* ws, const int* stop_flag,
+                             cudaStream_t stream) {
+  if (!L.bound) return cudaErrorInvalidValue;
+  const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
+  TcParams p{};
+  p.tmap0 = L.tmap0;
+  p.tmap1 = L.tmap1;
+  p.mode = L.mode;
+  p.R = L.R;
+  p.N = L.N;
+  p.M = L.M;
+  p.P = I * J;
+  p.K = K;
+  p.n_chunks = L.n_chunks;
+  p.chunks_per_split = L.chunks_per_split;
+  p.chunks_per_o = L.chunks_per_o;
+  p.n_mtiles = L.n_mtiles;
+  p.splits = L.splits;
+  p.x_stages = L.x_stages;
+  p.w_stages = L.w_stages;
+  p.n_wf = L.n_wf_warps;
+  p.ws = ws;
+  p.stop_flag = stop_flag;
+  p.wscale = L.wscale;
+  int64_t hi_rows, lo_rows;
+  if (L.mode == 1) {
+    p.Fhi = B; p.Flo = C; p.lo_extent = static_cast<uint32_t>(K); hi_rows = J; lo_rows = K;
+  } else if (L.mode == 2) {
+    p.Fhi = A; p.Flo = C; p.lo_extent = static_cast<uint32_t>(K); hi_rows = I; lo_rows = K;
+  } else {
+    p.Fhi = A; p.Flo = B; p.lo_extent = static_cast<uint32_t>(J); hi_rows = I; lo_rows = J;
+  }
+  wscale_kernel<<<L.N, 256, 0, stream>>>(p.Fhi, hi_rows, p.Flo, lo_rows, L.R, L.N, t.xscale,
+                                         L.wscale);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return dispatch_tc(p, L, stream, false);
 }
 
 }  // namespace ntf

@@ -1,29 +1,53 @@
-// tcgen05 (5th-gen tensor core) dense MTTKRP with split-precision TF32 for
-// ranks where the CUDA-core contraction leaves the HBM roof.
+// tcgen05 (5th-gen tensor core) dense MTTKRP for fp32 tensors, exact
+// fixed-point slicing (see mttkrp_tc.cu for the numerics).
 #pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
 namespace ntf {
 
+// fp16 fixed-point split of an fp32 tensor: X ~= xscale * (S0 + S1),
+// S0 integers |S0| <= 2048, S1 multiples of 2^-11 with |S1| <= 0.5, xscale a
+// power of two (2^(e-11), e = ceil(log2 max|X|)).  Built once per tensor.
+struct TcTensor {
+  __half* s0 = nullptr;
+  __half* s1 = nullptr;
+  double* xscale = nullptr;  // device scalar
+  int64_t dims[3] = {0, 0, 0};
+};
+
+cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* out,
+                             cudaStream_t stream);
+void tc_tensor_destroy(TcTensor* t);
+
 struct MttkrpTCLaunch {
   int mode;
+  int R, N;                 // rank and MMA N (R rounded up to 16)
   int64_t M, Q;
-  int n_mtiles, splits;
-  int64_t n_chunks, chunks_per_split;
-  int n_pad;          // MMA N (rank padded)
-  int smem_bytes;
-  int threads;
+  int n_mtiles, splits;     // splits per m-tile
+  int64_t n_chunks, chunks_per_split, chunks_per_o;
+  int n_wf_warps, threads, smem_bytes;
+  int x_stages, w_stages;
+  int tmem_cols;
+  CUtensorMap tmap0, tmap1; // S0 / S1 planes (built by mttkrp_tc_bind)
+  double* wscale;           // [2 * N] device: 2^(7-f(n)), output scale
+  bool bound;
 };
 
 bool mttkrp_tc_supported(int x_dtype, int R);
 bool mttkrp_tc_auto(int x_dtype, int R);
+bool mttkrp_tc_shape_ok(int mode, int64_t I, int64_t J, int64_t K);
 MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R);
 size_t mttkrp_tc_workspace_bytes(const MttkrpTCLaunch& L, int R);
 cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L);
-cudaError_t mttkrp_tc_launch(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
-                             const double* A, const double* B, const double* C, int R,
-                             const MttkrpTCLaunch& L, double* ws, const int* stop_flag,
+// Encode the tensor maps of the split planes and allocate the scale buffer.
+cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t);
+void mttkrp_tc_unbind(MttkrpTCLaunch& L);
+cudaError_t mttkrp_tc_launch(const MttkrpTCLaunch& L, const TcTensor& t, const double* A,
+                             const double* B, const double* C, double* ws, const int* stop_flag,
                              cudaStream_t stream);
 
 }  // namespace ntf
