@@ -76,7 +76,7 @@ MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, 
   return op;
 }
 
-cudaError_t run_op(const MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
+cudaError_t run_op(MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
                    const int* stop, cudaStream_t s) {
   if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, ws, stop, s);

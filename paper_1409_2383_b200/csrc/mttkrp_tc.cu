@@ -1,6 +1,6 @@
 // Dense MTTKRP on the 5th-generation tensor cores (tcgen05, sm_100a) for fp32
 // tensors.  Same contraction as mttkrp_cc.cu (reference tensors.py:254-262):
-//   out[m, n] = sum_q X(m, q) W(q, n),  W(q, n) = F_hi[q_hi, n] * F_lo[q_lo, n]
+//   out[m, n] = sum_q X(m, q) W(q, n),  W(q, n) = F_hi[o, n] * F_lo[l, n]
 //
 // Numerics: exact fixed-point slicing on kind::f16 MMAs.
 //   X  = xs * (S0 + S1)          S0 integers |S0| <= 2^11, S1 in 2^-11 units,
@@ -17,15 +17,26 @@
 // ~2^-23 of the column/tensor maxima) are i.i.d. per element, never a
 // structured rounding of the factors (SURVEY 8(d) precision findings).
 //
+// Chunking.  All modes view X as 3-D (K, J, I) and walk chunks (o, l0): the
+// reduction index q = (o, l) with l in [l0, l0+64) along one tensor axis:
+//   mode 1: m = i, o = j, l = k   W = B[j] * C[k]   A tile K-major
+//   mode 2: m = j, o = i, l = k   W = A[i] * C[k]   A tile K-major
+//   mode 3: m = k, o = i, l = j   W = A[i] * B[j]   A tile MN-major (X^T)
+// TMA zero-fills the out-of-range tail of each (o, .) run, so no byte is
+// fetched twice.  The chunk's factor rows (F_lo[l0..l0+63], F_hi[o]) ride on
+// the same TMA stage as the X tiles.
+//
 // Pipeline (one CTA per SM, warp-specialised, mbarrier handshakes):
-//   warp 0      TMA producer: S0/S1 tiles (128 rows x 64 q, 128B-swizzled)
+//   warp 0      TMA producer: S0/S1 tiles (128B-swizzled) + factor rows
 //   warp 1      TMEM allocator + single-thread MMA issuer (tcgen05.mma)
-//   warps 2..   KR formers: W slices of the chunk from the fp64 factors,
+//   warps 2-5   KR formers: W slices of the chunk from the staged fp64 rows,
 //               written in the UMMA K-major SW128 layout
-//   last 4      epilogue: tcgen05.ld of the two accumulators (double-buffered
+//   warps 6-9   epilogue: tcgen05.ld of the two accumulators (double-buffered
 //               in TMEM), double-float accumulation, fp64 partial per split.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "mttkrp_tc.cuh"
 
@@ -37,6 +48,8 @@ constexpr int kTM = 128;     // MMA M (rows per tile, TMEM lanes)
 constexpr int kBK = 64;      // q per chunk (fp16: 128 B rows, one SW128 atom)
 constexpr int kUK = 16;      // MMA K for kind::f16
 constexpr int kEpiWarps = 4;
+constexpr int kWfWarps = 4;
+constexpr int kThreads = (2 + kWfWarps + kEpiWarps) * 32;
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
@@ -160,19 +173,24 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
          | ((static_cast<uint32_t>(kTM) >> 4) << 24);  // M >> 4
 }
 
+__host__ __device__ constexpr uint32_t tmem_cols(int N) {
+  return 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
+}
+
 struct TcParams {
-  CUtensorMap tmap0;
-  CUtensorMap tmap1;
-  int mode, R, N;
-  int64_t M, P, K;           // P = I*J (mode 3 reduction length)
-  uint32_t lo_extent;        // mode 3: J
+  CUtensorMap tmap0;         // S0 plane, 3-D (K, J, I)
+  CUtensorMap tmap1;         // S1 plane
+  CUtensorMap tmap_lo;       // F_lo rows, 2-D (R, rows), box (R, 64)
+  CUtensorMap tmap_hi;       // F_hi rows, 2-D (R, rows), box (R, 1)
+  int mode, R;
+  int64_t M;
+  int64_t l_extent;          // extent of the chunked axis (K or J)
   int64_t n_chunks, chunks_per_split, chunks_per_o;
   int n_mtiles, splits;
-  int x_stages, w_stages, n_wf;
-  const double* Fhi;
-  const double* Flo;
+  int x_stages, w_stages;
+  int stage_bytes;           // X tiles + factor rows
   const double* wscale;      // [N] 2^(7 - f(n)),  [N..2N) output scale (with xscale)
-  double* ws;                // [splits * n_mtiles][M][R] partials (split-major)
+  double* ws;                // [splits][M][R] partials
   const int* stop_flag;
 };
 
@@ -205,18 +223,21 @@ __device__ __forceinline__ void emit_w_octet(unsigned char* t0, unsigned char* t
 }
 
 template <int NT>  // N / 16
-__global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(kThreads, 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
   constexpr int N = NT * 16;
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // carve: [X stages: S0 16KB | S1 16KB] [W stages: T0 | T1 | T2 (N*128 each)] [barriers]
+  // carve: [X stages: S0 16KB | S1 16KB | lo rows 64*R*8 | hi row R*8]
+  //        [W stages: T0 | T1 | T2 (N*128 each)] [barriers]
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   constexpr int kXTile = kTM * kBK * 2;  // 16 KB
   constexpr int kWTile = N * kBK * 2;    // N * 128 B
   const int SX = p.x_stages, SW = p.w_stages;
+  const int R = p.R;
+  const int SB = p.stage_bytes;
   unsigned char* xbase = base;
-  unsigned char* wbase = xbase + SX * 2 * kXTile;
+  unsigned char* wbase = xbase + SX * SB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + SW * 3 * kWTile);
   uint64_t* x_full = bars;
   uint64_t* x_empty = x_full + SX;
@@ -228,10 +249,9 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n_wf = p.n_wf;
-  const int wf_first = 2;
-  const int epi_first = 2 + n_wf;
-  const int n_wf_threads = n_wf * 32;
+  constexpr int kWfFirst = 2;
+  constexpr int kEpiFirst = 2 + kWfWarps;
+  constexpr int kWfThreads = kWfWarps * 32;
 
   const int tile = blockIdx.x % p.n_mtiles;
   const int split = blockIdx.x / p.n_mtiles;
@@ -244,10 +264,10 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < SX; ++s) {
       mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1);
+      mbar_init(&x_empty[s], 1 + kWfThreads);  // MMA commit + KR formers (factor rows)
     }
     for (int s = 0; s < SW; ++s) {
-      mbar_init(&w_full[s], n_wf_threads);
+      mbar_init(&w_full[s], kWfThreads);
       mbar_init(&w_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -257,10 +277,9 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
-    const uint32_t ncols = 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(ncols));
+                 "r"(tmem_cols(N)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
@@ -271,45 +290,47 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
+      const uint32_t fac_bytes = static_cast<uint32_t>((kBK + 1) * R * 8);
       for (int it = 0; it < n_iter; ++it) {
         const int s = it % SX;
         mbar_wait(&x_empty[s], ((it / SX) & 1) ^ 1);
-        unsigned char* d0 = xbase + s * 2 * kXTile;
+        unsigned char* d0 = xbase + s * SB;
         unsigned char* d1 = d0 + kXTile;
-        mbar_arrive_expect_tx(&x_full[s], 2 * kXTile);
+        unsigned char* dlo = d1 + kXTile;
+        unsigned char* dhi = dlo + kBK * R * 8;
+        mbar_arrive_expect_tx(&x_full[s], 2 * kXTile + fac_bytes);
         const int64_t c = c_begin + it;
-        if (p.mode == 3) {
-          const int p0 = static_cast<int>(c * kBK);
-          const int k0 = static_cast<int>(m0);
-          tma_load_2d(d0, &p.tmap0, &x_full[s], k0, p0);
-          tma_load_2d(d0 + kXTile / 2, &p.tmap0, &x_full[s], k0 + 64, p0);
-          tma_load_2d(d1, &p.tmap1, &x_full[s], k0, p0);
-          tma_load_2d(d1 + kXTile / 2, &p.tmap1, &x_full[s], k0 + 64, p0);
-        } else {
-          const int o = static_cast<int>(c / p.chunks_per_o);
-          const int k0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
-          if (p.mode == 1) {
-            tma_load_3d(d0, &p.tmap0, &x_full[s], k0, o, static_cast<int>(m0));
-            tma_load_3d(d1, &p.tmap1, &x_full[s], k0, o, static_cast<int>(m0));
-          } else {
-            tma_load_3d(d0, &p.tmap0, &x_full[s], k0, static_cast<int>(m0), o);
-            tma_load_3d(d1, &p.tmap1, &x_full[s], k0, static_cast<int>(m0), o);
-          }
+        const int o = static_cast<int>(c / p.chunks_per_o);
+        const int l0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
+        const int mm = static_cast<int>(m0);
+        if (p.mode == 1) {
+          tma_load_3d(d0, &p.tmap0, &x_full[s], l0, o, mm);
+          tma_load_3d(d1, &p.tmap1, &x_full[s], l0, o, mm);
+        } else if (p.mode == 2) {
+          tma_load_3d(d0, &p.tmap0, &x_full[s], l0, mm, o);
+          tma_load_3d(d1, &p.tmap1, &x_full[s], l0, mm, o);
+        } else {  // two 64-m boxes per plane
+          tma_load_3d(d0, &p.tmap0, &x_full[s], mm, l0, o);
+          tma_load_3d(d0 + kXTile / 2, &p.tmap0, &x_full[s], mm + 64, l0, o);
+          tma_load_3d(d1, &p.tmap1, &x_full[s], mm, l0, o);
+          tma_load_3d(d1 + kXTile / 2, &p.tmap1, &x_full[s], mm + 64, l0, o);
         }
+        tma_load_2d(dlo, &p.tmap_lo, &x_full[s], 0, l0);
+        tma_load_2d(dhi, &p.tmap_hi, &x_full[s], 0, o);
       }
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
     if (lane == 0) {
-      const uint32_t idesc = make_idesc(N, p.mode == 3);
       const bool mn = p.mode == 3;
+      const uint32_t idesc = make_idesc(N, mn);
       for (int it = 0; it < n_iter; ++it) {
         const int s = it % SX, sw = it % SW, ab = it & 1;
         mbar_wait(&x_full[s], (it / SX) & 1);
         mbar_wait(&w_full[sw], (it / SW) & 1);
         mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const unsigned char* a0 = xbase + s * 2 * kXTile;
+        const unsigned char* a0 = xbase + s * SB;
         const unsigned char* a1 = a0 + kXTile;
         const unsigned char* b0 = wbase + sw * 3 * kWTile;
         const unsigned char* b1 = b0 + kWTile;
@@ -341,50 +362,38 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
         tc_commit(&acc_full[ab]);
       }
     }
-  } else if (warp < epi_first) {
+  } else if (warp < kEpiFirst) {
     // ------------------------------ KR formers --------------------------------
-    const int t = threadIdx.x - wf_first * 32;
-    const int R = p.R;
-    const int items = N * (kBK / 8);  // (n, octet) pairs
+    // thread t owns column n = t % N (lanes along n: conflict-free row reads)
+    // and octets t / N, t / N + kWfThreads / N, ...
+    const int t = threadIdx.x - kWfFirst * 32;
+    const int n = t % N;
+    const int oct0 = t / N;
+    constexpr int kOctStep = kWfThreads / N > 0 ? kWfThreads / N : 1;
+    const bool active = t < N * (kBK / 8) && (kWfThreads >= N || true);
+    const double sc = n < R ? p.wscale[n] : 0.0;
     for (int it = 0; it < n_iter; ++it) {
-      const int sw = it % SW;
+      const int s = it % SX, sw = it % SW;
+      mbar_wait(&x_full[s], (it / SX) & 1);
       mbar_wait(&w_empty[sw], ((it / SW) & 1) ^ 1);
+      const unsigned char* srow = xbase + s * SB + 2 * kXTile;
+      const double* lo_s = reinterpret_cast<const double*>(srow);
+      const double* hi_s = lo_s + kBK * R;
       unsigned char* t0 = wbase + sw * 3 * kWTile;
       unsigned char* t1 = t0 + kWTile;
       unsigned char* t2 = t1 + kWTile;
-      const int64_t c = c_begin + it;
-      for (int e = t; e < items; e += n_wf_threads) {
-        const int n = e / (kBK / 8);
-        const int oct = e - n * (kBK / 8);
-        double w[8];
-        const double sc = n < R ? p.wscale[n] : 0.0;
-        if (p.mode == 3) {
-          const int64_t q0 = c * kBK + oct * 8;
-          int64_t hi = q0 / p.lo_extent;
-          int64_t lo = q0 - hi * p.lo_extent;
+      if (active) {
+        const double hs = n < R ? hi_s[n] * sc : 0.0;
+        for (int oct = oct0; oct < kBK / 8; oct += kOctStep) {
+          double w[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const bool ok = n < R && q0 + u < p.P;
-            w[u] = ok ? p.Fhi[hi * R + n] * p.Flo[lo * R + n] * sc : 0.0;
-            if (++lo == p.lo_extent) {
-              lo = 0;
-              ++hi;
-            }
-          }
-        } else {
-          const int64_t o = c / p.chunks_per_o;
-          const int64_t k0 = (c - o * p.chunks_per_o) * kBK + oct * 8;
-          const double fo = n < R ? p.Fhi[o * R + n] * sc : 0.0;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const bool ok = n < R && k0 + u < p.K;
-            w[u] = ok ? fo * p.Flo[(k0 + u) * R + n] : 0.0;
-          }
+          for (int u = 0; u < 8; ++u) w[u] = n < R ? hs * lo_s[(oct * 8 + u) * R + n] : 0.0;
+          emit_w_octet(t0, t1, t2, n, oct, w);
         }
-        emit_w_octet(t0, t1, t2, n, oct, w);
       }
       fence_proxy_async();
       mbar_arrive(&w_full[sw]);
+      mbar_arrive(&x_empty[s]);  // factor rows consumed
     }
   } else {
     // ------------------------------ epilogue ----------------------------------
@@ -392,9 +401,9 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
     const int row = q4 * 32 + lane;   // tile row == TMEM lane
     float hi[N], lo[N];
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-      hi[n] = 0.f;
-      lo[n] = 0.f;
+    for (int j = 0; j < N; ++j) {
+      hi[j] = 0.f;
+      lo[j] = 0.f;
     }
     for (int it = 0; it < n_iter; ++it) {
       const int ab = it & 1;
@@ -419,18 +428,18 @@ __global__ void __launch_bounds__(320, 1) mttkrp_tc_kernel(const __grid_constant
     // fp64 partial of this split: out = (hi + lo) * xscale * ws(n)
     const int64_t gm = m0 + row;
     if (gm < p.M) {
-      double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * p.R;
+      double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * R;
 #pragma unroll
-      for (int n = 0; n < N; ++n)
-        if (n < p.R) out[n] = (static_cast<double>(hi[n]) + static_cast<double>(lo[n])) * p.wscale[N + n];
+      for (int j = 0; j < N; ++j)
+        if (j < R) out[j] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * p.wscale[N + j];
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    const uint32_t ncols = 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(tmem_cols(N)));
   }
 }
 
@@ -468,7 +477,8 @@ __global__ void split_kernel(const float* __restrict__ X, int64_t n, const unsig
 // wscale[N + n] = xscale * 2^(f(n) - 7)
 __global__ void wscale_kernel(const double* __restrict__ Fhi, int64_t hi_rows,
                               const double* __restrict__ Flo, int64_t lo_rows, int R, int N,
-                              const double* xscale, double* wscale) {
+                              const double* xscale, double* wscale, const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
   const int n = blockIdx.x;
   double mh = 0.0, ml = 0.0;
   if (n < R) {
@@ -526,6 +536,21 @@ int sm_count_tc() {
   return n;
 }
 
+// fp64 factor rows [rows][R] as a 2-D tensor map with box (R, box_rows)
+cudaError_t encode_factor_map(CUtensorMap* map, const double* F, int64_t rows, int R,
+                              int box_rows) {
+  auto enc = get_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstr[1] = {static_cast<cuuint64_t>(R) * 8};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(R), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(F), gdim, gstr, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int NT>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
   auto kern = mttkrp_tc_kernel<NT>;
@@ -549,7 +574,10 @@ cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
 // ----------------------------------------------------------------------------
 // host API
 // ----------------------------------------------------------------------------
-bool mttkrp_tc_supported(int x_dtype, int R) { return x_dtype == NTF_F32 && R >= 1 && R <= 64; }
+bool mttkrp_tc_supported(int x_dtype, int R) {
+  // even R: the fp64 factor rows are TMA boxes of R*8 bytes (multiple of 16)
+  return x_dtype == NTF_F32 && R >= 2 && R <= 64 && R % 2 == 0;
+}
 
 bool mttkrp_tc_auto(int x_dtype, int R) {
   static int enabled = -1;
@@ -561,11 +589,11 @@ bool mttkrp_tc_auto(int x_dtype, int R) {
 }
 
 bool mttkrp_tc_shape_ok(int mode, int64_t I, int64_t J, int64_t K) {
-  // TMA global strides are multiples of 16 B (K % 8 == 0 for fp16 planes);
+  // TMA global strides are multiples of 16 B (K % 8 == 0 for the fp16 planes);
   // coordinates are int32.
+  (void)mode;
   if (K % 8 != 0) return false;
-  if (I > (1 << 30) || J > (1 << 30) || K > (1 << 30)) return false;
-  if (mode == 3 && I * J >= (int64_t(1) << 31)) return false;
+  if (I >= (1 << 30) || J >= (1 << 30) || K >= (1 << 30)) return false;
   return true;
 }
 
@@ -578,24 +606,22 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.M = mode == 1 ? I : (mode == 2 ? J : K);
   L.Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
   L.n_mtiles = static_cast<int>((L.M + kTM - 1) / kTM);
-  if (mode == 3) {
-    L.chunks_per_o = 0;
-    L.n_chunks = (I * J + kBK - 1) / kBK;
-  } else {
-    L.chunks_per_o = (K + kBK - 1) / kBK;
-    L.n_chunks = (mode == 1 ? J : I) * L.chunks_per_o;
-  }
-  L.n_wf_warps = 4;
-  L.threads = (2 + L.n_wf_warps + kEpiWarps) * 32;
+  const int64_t l_ext = mode == 3 ? J : K;
+  const int64_t o_ext = mode == 1 ? J : I;
+  L.chunks_per_o = (l_ext + kBK - 1) / kBK;
+  L.n_chunks = o_ext * L.chunks_per_o;
+  L.n_wf_warps = kWfWarps;
+  L.threads = kThreads;
+  const int xs = 2 * kTM * kBK * 2 + (kBK + 1) * R * 8;
+  L.stage_bytes = (xs + 1023) & ~1023;
+  const int wsz = 3 * L.N * kBK * 2;
   L.x_stages = 4;
   L.w_stages = 3;
-  const int xs = 2 * kTM * kBK * 2;
-  const int wsz = 3 * L.N * kBK * 2;
-  L.smem_bytes = 1024 + L.x_stages * xs + L.w_stages * wsz + 256;
-  if (L.smem_bytes > 227 * 1024) {
-    L.x_stages = 3;
-    L.smem_bytes = 1024 + L.x_stages * xs + L.w_stages * wsz + 256;
-  }
+  auto total = [&]() { return 1024 + L.x_stages * L.stage_bytes + L.w_stages * wsz + 256; };
+  while (total() > 227 * 1024 && L.x_stages > 2) --L.x_stages;
+  while (total() > 227 * 1024 && L.w_stages > 2) --L.w_stages;
+  L.smem_bytes = total();
+  L.tmem_cols = static_cast<int>(tmem_cols(L.N));
   // one CTA per SM; split the chunk range so that the grid is one wave
   const int sms = sm_count_tc();
   int splits = sms / L.n_mtiles;
@@ -628,12 +654,11 @@ cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* ou
     tc_tensor_destroy(&t);
     return e;
   }
-  unsigned* amax = nullptr;
   if ((e = cudaMalloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
   }
-  amax = reinterpret_cast<unsigned*>(t.xscale + 1);
+  unsigned* amax = reinterpret_cast<unsigned*>(t.xscale + 1);
   cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
   const int blocks = 4 * sm_count_tc();
   absmax_kernel<<<blocks, 256, 0, stream>>>(X, n, amax);
@@ -659,41 +684,31 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
   auto enc = get_encoder();
   if (!enc) return cudaErrorNotSupported;
   const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
-  CUresult r0, r1;
-  if (L.mode == 3) {
-    cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(I * J)};
-    cuuint64_t gstr[1] = {static_cast<cuuint64_t>(K * 2)};
-    cuuint32_t box[2] = {64, 64};
-    cuuint32_t es[2] = {1, 1};
-    r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, t.s0, gdim, gstr, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, t.s1, gdim, gstr, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t gdim[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(J),
+                        static_cast<cuuint64_t>(I)};
+  cuuint64_t gstr[2] = {static_cast<cuuint64_t>(K * 2), static_cast<cuuint64_t>(J * K * 2)};
+  cuuint32_t box[3];
+  if (L.mode == 1) {
+    box[0] = 64; box[1] = 1; box[2] = 128;
+  } else if (L.mode == 2) {
+    box[0] = 64; box[1] = 128; box[2] = 1;
   } else {
-    cuuint64_t gdim[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(J),
-                          static_cast<cuuint64_t>(I)};
-    cuuint64_t gstr[2] = {static_cast<cuuint64_t>(K * 2), static_cast<cuuint64_t>(J * K * 2)};
-    cuuint32_t box[3];
-    if (L.mode == 1) {
-      box[0] = 64; box[1] = 1; box[2] = 128;
-    } else {
-      box[0] = 64; box[1] = 128; box[2] = 1;
-    }
-    cuuint32_t es[3] = {1, 1, 1};
-    r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s0, gdim, gstr, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s1, gdim, gstr, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    box[0] = 64; box[1] = 64; box[2] = 1;
   }
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s0, gdim, gstr, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s1, gdim, gstr, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) return cudaErrorInvalidValue;
   if (!L.wscale) {
     cudaError_t e = cudaMalloc(&L.wscale, sizeof(double) * 2 * L.N);
     if (e != cudaSuccess) return e;
   }
+  L.fac_lo = nullptr;
+  L.fac_hi = nullptr;
   L.bound = true;
   return cudaSuccess;
 }
@@ -704,20 +719,40 @@ void mttkrp_tc_unbind(MttkrpTCLaunch& L) {
   L.bound = false;
 }
 
-cudaError_t mttkrp_tc_launch(const MttkrpTCLaunch& L, const TcTensor& t, const double* A,
+cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
                              const double* B, const double* C, double* ws, const int* stop_flag,
                              cudaStream_t stream) {
   if (!L.bound) return cudaErrorInvalidValue;
   const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
+  const double *Fhi, *Flo;
+  int64_t hi_rows, lo_rows;
+  if (L.mode == 1) {
+    Fhi = B; Flo = C; hi_rows = J; lo_rows = K;
+  } else if (L.mode == 2) {
+    Fhi = A; Flo = C; hi_rows = I; lo_rows = K;
+  } else {
+    Fhi = A; Flo = B; hi_rows = I; lo_rows = J;
+  }
+  // factor tensor maps are cached per factor pointer (plan buffers are fixed)
+  if (Flo != L.fac_lo) {
+    cudaError_t e = encode_factor_map(&L.tmap_lo, Flo, lo_rows, L.R, kBK);
+    if (e != cudaSuccess) return e;
+    L.fac_lo = Flo;
+  }
+  if (Fhi != L.fac_hi) {
+    cudaError_t e = encode_factor_map(&L.tmap_hi, Fhi, hi_rows, L.R, 1);
+    if (e != cudaSuccess) return e;
+    L.fac_hi = Fhi;
+  }
   TcParams p{};
   p.tmap0 = L.tmap0;
   p.tmap1 = L.tmap1;
+  p.tmap_lo = L.tmap_lo;
+  p.tmap_hi = L.tmap_hi;
   p.mode = L.mode;
   p.R = L.R;
-  p.N = L.N;
   p.M = L.M;
-  p.P = I * J;
-  p.K = K;
+  p.l_extent = L.mode == 3 ? J : K;
   p.n_chunks = L.n_chunks;
   p.chunks_per_split = L.chunks_per_split;
   p.chunks_per_o = L.chunks_per_o;
@@ -725,20 +760,12 @@ cudaError_t mttkrp_tc_launch(const MttkrpTCLaunch& L, const TcTensor& t, const d
   p.splits = L.splits;
   p.x_stages = L.x_stages;
   p.w_stages = L.w_stages;
-  p.n_wf = L.n_wf_warps;
+  p.stage_bytes = L.stage_bytes;
   p.ws = ws;
   p.stop_flag = stop_flag;
   p.wscale = L.wscale;
-  int64_t hi_rows, lo_rows;
-  if (L.mode == 1) {
-    p.Fhi = B; p.Flo = C; p.lo_extent = static_cast<uint32_t>(K); hi_rows = J; lo_rows = K;
-  } else if (L.mode == 2) {
-    p.Fhi = A; p.Flo = C; p.lo_extent = static_cast<uint32_t>(K); hi_rows = I; lo_rows = K;
-  } else {
-    p.Fhi = A; p.Flo = B; p.lo_extent = static_cast<uint32_t>(J); hi_rows = I; lo_rows = J;
-  }
-  wscale_kernel<<<L.N, 256, 0, stream>>>(p.Fhi, hi_rows, p.Flo, lo_rows, L.R, L.N, t.xscale,
-                                         L.wscale);
+  wscale_kernel<<<L.N, 256, 0, stream>>>(Fhi, hi_rows, Flo, lo_rows, L.R, L.N, t.xscale, L.wscale,
+                                         stop_flag);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return dispatch_tc(p, L, stream, false);

@@ -30,9 +30,12 @@ struct MttkrpTCLaunch {
   int n_mtiles, splits;     // splits per m-tile
   int64_t n_chunks, chunks_per_split, chunks_per_o;
   int n_wf_warps, threads, smem_bytes;
-  int x_stages, w_stages;
+  int x_stages, w_stages, stage_bytes;
   int tmem_cols;
   CUtensorMap tmap0, tmap1; // S0 / S1 planes (built by mttkrp_tc_bind)
+  CUtensorMap tmap_lo, tmap_hi;      // factor rows (cached per factor pointer)
+  const double* fac_lo;
+  const double* fac_hi;
   double* wscale;           // [2 * N] device: 2^(7-f(n)), output scale
   bool bound;
 };
@@ -46,7 +49,7 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L);
 // Encode the tensor maps of the split planes and allocate the scale buffer.
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t);
 void mttkrp_tc_unbind(MttkrpTCLaunch& L);
-cudaError_t mttkrp_tc_launch(const MttkrpTCLaunch& L, const TcTensor& t, const double* A,
+cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
                              const double* B, const double* C, double* ws, const int* stop_flag,
                              cudaStream_t stream);
 
