@@ -48,8 +48,9 @@ constexpr int kTM = 128;     // MMA M (rows per tile, TMEM lanes)
 constexpr int kBK = 64;      // q per chunk (fp16: 128 B rows, one SW128 atom)
 constexpr int kUK = 16;      // MMA K for kind::f16
 constexpr int kEpiWarps = 4;
-constexpr int kWfWarps = 4;
-constexpr int kThreads = (2 + kWfWarps + kEpiWarps) * 32;
+// KR-former warps: more for small N (light epilogue, registers to spare)
+__host__ __device__ constexpr int wf_warps(int NT) { return NT <= 2 ? 8 : 4; }
+__host__ __device__ constexpr int tc_threads(int NT) { return (2 + wf_warps(NT) + kEpiWarps) * 32; }
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
@@ -202,19 +203,25 @@ __device__ __forceinline__ void fast_two_sum(float& hi, float& lo, float a) {
 }
 
 // W slices for one (n, 8-q octet): 3 x 16 bytes at the swizzled positions.
+// t (|t| <= 128) is converted to fp32 once: its rounding error (<= 2^-17) is
+// far below the T2 quantum (2^-14), so slicing in fp32 loses nothing.
 __device__ __forceinline__ void emit_w_octet(unsigned char* t0, unsigned char* t1, unsigned char* t2,
                                              int n, int oct, const double (&w)[8]) {
-  __align__(16) __half h0[8], h1[8], h2[8];
+  __align__(16) __half2 h0[4], h1[4], h2[4];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const double t = w[u];
-    const double a0 = rint(t);
-    const float r1 = static_cast<float>((t - a0) * 128.0);  // |r1| <= 64, exact to 2^-18
-    const float a1 = rintf(r1);
-    const float a2 = rintf((r1 - a1) * 128.0f);
-    h0[u] = __float2half_rn(static_cast<float>(a0));        // integer <= 128: exact
-    h1[u] = __float2half_rn(a1 * 0.0078125f);               // 2^-7 units: exact
-    h2[u] = __float2half_rn(a2 * 6.103515625e-05f);         // 2^-14 units: exact
+  for (int u = 0; u < 8; u += 2) {
+    float a0[2], a1[2], a2[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const float tf = static_cast<float>(w[u + v]);
+      a0[v] = rintf(tf);                                     // integer, |a0| <= 128
+      const float r1 = (tf - a0[v]) * 128.0f;                // exact, |r1| <= 64
+      a1[v] = rintf(r1);
+      a2[v] = rintf((r1 - a1[v]) * 128.0f);
+    }
+    h0[u / 2] = __floats2half2_rn(a0[0], a0[1]);                          // exact
+    h1[u / 2] = __floats2half2_rn(a1[0] * 0.0078125f, a1[1] * 0.0078125f);  // 2^-7 units
+    h2[u / 2] = __floats2half2_rn(a2[0] * 6.103515625e-05f, a2[1] * 6.103515625e-05f);  // 2^-14
   }
   const int off = n * 128 + ((oct ^ (n & 7)) << 4);
   *reinterpret_cast<uint4*>(t0 + off) = *reinterpret_cast<const uint4*>(h0);
@@ -223,7 +230,8 @@ __device__ __forceinline__ void emit_w_octet(unsigned char* t0, unsigned char* t
 }
 
 template <int NT>  // N / 16
-__global__ void __launch_bounds__(kThreads, 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
+  constexpr int kWfWarps = wf_warps(NT);
   constexpr int N = NT * 16;
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -610,8 +618,8 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   const int64_t o_ext = mode == 1 ? J : I;
   L.chunks_per_o = (l_ext + kBK - 1) / kBK;
   L.n_chunks = o_ext * L.chunks_per_o;
-  L.n_wf_warps = kWfWarps;
-  L.threads = kThreads;
+  L.n_wf_warps = wf_warps(L.N / 16);
+  L.threads = tc_threads(L.N / 16);
   const int xs = 2 * kTM * kBK * 2 + (kBK + 1) * R * 8;
   L.stage_bytes = (xs + 1023) & ~1023;
   const int wsz = 3 * L.N * kBK * 2;

@@ -9,9 +9,10 @@ namespace ntf {
 namespace {
 
 constexpr int kUpdThreads = 256;
-// rows per update block: enough rows that the per-block Gram partials stay
-// few, small enough that R x R + 2 x rows x R doubles fit in shared memory
-__host__ __device__ __forceinline__ int rows_per_block(int R) { return R <= 64 ? 64 : 32; }
+// rows per update block: two rows per warp keeps the dependent substitution
+// chains short and spreads a mode's rows over many SMs; the per-block Gram
+// partials are reduced by the last block
+__host__ __device__ __forceinline__ int rows_per_block(int R) { return R <= 64 ? 16 : 8; }
 
 // ---------------------------------------------------------------------------
 // Ridge Cholesky in shared memory (solver.ridge_cholesky, solver.py:167-175):
