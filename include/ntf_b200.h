@@ -123,10 +123,17 @@ typedef struct ntf_plan_desc {
   double* aux[3];           /* row_count[m] x R  auxiliary copies (owned)   */
   double* duals[3];         /* row_count[m] x R  scaled duals Y (owned)     */
   double* grams[3];         /* R x R        F_m^T F_m                       */
+  double* colmax;           /* [3][R]       max_i |F_m[i][r]| (W scales of the
+                               tensor-core MTTKRP), kept like the grams     */
   double* rho;              /* [3]          per-mode penalties              */
-  double* norm_acc;         /* [3][5]  per-mode sums of squares of the last
-                               sweep: F-aux, aux-aux_prev, F, aux, Y (all-
-                               reduced by the caller before finalize if P>1) */
+  double* norm_acc;         /* [3][5][2] per-mode scaled sums of squares of
+                               the last sweep, (scale, ssq) with value
+                               scale^2*ssq (nrm2-style, no under/overflow):
+                               F-aux, aux-aux_prev, F, aux, Y               */
+  const double* norm_all;   /* NULL, or [norm_parts][30]: every shard's
+                               norm_acc gathered in rank order (P>1); the
+                               finalize merges them instead of norm_acc     */
+  int norm_parts;           /* rows of norm_all (ignored when NULL)         */
   /* per-iteration outputs: row `it` written by iteration `it` */
   int64_t history_capacity; /* rows available in the history buffers        */
   double* resid_history;    /* [cap][6]  primal[3], dual[3]                 */
@@ -139,6 +146,9 @@ typedef struct ntf_plan_desc {
 } ntf_plan_desc;
 
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);
+/* Column maxima out[r] = max_i |F[i][r]| (sharded runs refresh colmax[m]
+ * with this after gathering a factor, as they refresh grams[m]). */
+int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t stream);
 /* Recompute grams[m] from factors[m] (after the caller (re)initialises state). */
 int ntf_plan_sync_grams(ntf_plan* plan, ntf_stream_t stream);
 /* Enqueue `n_iters` outer iterations.  Iterations after the stop flag is set

@@ -39,6 +39,7 @@ EXPORTED = (
     "ntf_sq_error_workspace_bytes",
     "ntf_sq_error",
     "ntf_plan_create",
+    "ntf_colmax",
     "ntf_plan_sync_grams",
     "ntf_plan_run",
     "ntf_plan_mode_update",
@@ -90,8 +91,11 @@ class PlanDesc(ctypes.Structure):
         ("aux", c_vp * 3),
         ("duals", c_vp * 3),
         ("grams", c_vp * 3),
+        ("colmax", c_vp),
         ("rho", c_vp),
         ("norm_acc", c_vp),
+        ("norm_all", c_vp),
+        ("norm_parts", ctypes.c_int),
         ("history_capacity", c_i64),
         ("resid_history", c_vp),
         ("rho_history", c_vp),
@@ -123,6 +127,8 @@ def _declare(lib):
                                  c_vp, ctypes.c_size_t, c_vp]
     lib.ntf_plan_create.restype = c_int
     lib.ntf_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(c_vp)]
+    lib.ntf_colmax.restype = c_int
+    lib.ntf_colmax.argtypes = [c_vp, c_i64, c_int, c_vp, c_vp]
     lib.ntf_plan_sync_grams.restype = c_int
     lib.ntf_plan_sync_grams.argtypes = [c_vp, c_vp]
     lib.ntf_plan_run.restype = c_int

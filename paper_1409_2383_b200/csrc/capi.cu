@@ -78,8 +78,8 @@ MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, 
 
 cudaError_t run_op(MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
-                   const int* stop, cudaStream_t s) {
-  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, ws, stop, s);
+                   const int* stop, cudaStream_t s, const double* colmax3 = nullptr) {
+  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
 }
 
@@ -106,6 +106,7 @@ struct ntf_plan {
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   double* ridge = nullptr;  // [R*R + R]
+  double* colmax_partials = nullptr;  // [blocks][R]
   // fp16 split planes for the tensor-core engine, one per distinct slab
   ntf::TcTensor tct[3];
   int n_tct = 0;
@@ -158,7 +159,7 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
     NTF_CUDA_TRY(record_event(ev[0], s));
   }
   NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2], d.factors[0],
-                      d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s));
+                      d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s, d.colmax));
   if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
   NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
   ntf::FactorUpdateParams fp{};
@@ -178,7 +179,9 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   fp.norm_partials = pl->norm_partials;
   fp.gram_partials = pl->gram_partials;
   fp.G_out = d.grams[m];
-  fp.norm_acc = d.norm_acc + 5 * m;
+  fp.colmax_partials = pl->colmax_partials;
+  fp.colmax_out = d.colmax + m * R;
+  fp.norm_acc = d.norm_acc + 10 * m;
   fp.done_counter = pl->done + m;
   fp.status = d.counters + 2;
   fp.stop_flag = d.counters + 1;
@@ -190,7 +193,8 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
 int enqueue_finalize(ntf_plan* pl, cudaStream_t s) {
   const ntf_plan_desc& d = pl->d;
   ntf::FinalizeParams fz{};
-  fz.norm_acc = d.norm_acc;
+  fz.norm_acc = d.norm_all ? d.norm_all : d.norm_acc;
+  fz.norm_parts = d.norm_all ? d.norm_parts : 1;
   fz.rho = d.rho;
   for (int m = 0; m < 3; ++m) fz.dims[m] = d.dims[m];
   fz.R = d.rank;
@@ -309,7 +313,8 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   const int R = d.rank;
   if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
   if (d.inner_sweeps < 1) return fail(NTF_ERR_INVALID, "inner_sweeps must be >= 1");
-  if (!d.rho || !d.norm_acc || !d.counters || !d.resid_history || !d.rho_history)
+  if (d.norm_all && d.norm_parts < 1) return fail(NTF_ERR_INVALID, "norm_parts must be >= 1");
+  if (!d.rho || !d.norm_acc || !d.counters || !d.resid_history || !d.rho_history || !d.colmax)
     return fail(NTF_ERR_INVALID, "null plan buffer");
   for (int m = 0; m < 3; ++m) {
     const int64_t* xd = d.x_dims[m];
@@ -348,13 +353,15 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return rc;
   };
   if ((e = cudaMalloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
-  if ((e = cudaMalloc(&pl->norm_partials, sizeof(double) * 5 * maxb)) != cudaSuccess)
+  if ((e = cudaMalloc(&pl->norm_partials, sizeof(double) * 10 * maxb)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc norm"));
+  if ((e = cudaMalloc(&pl->colmax_partials, sizeof(double) * R * maxb)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc colmax"));
   if ((e = cudaMalloc(&pl->gram_partials, sizeof(double) * R * R * maxb)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc gram"));
   if ((e = cudaMalloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc gram ws"));
-  if ((e = cudaMalloc(&pl->ridge, sizeof(double) * (R * R + R))) != cudaSuccess)
+  if ((e = cudaMalloc(&pl->ridge, sizeof(double) * ntf::ridge_buffer_doubles(R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc ridge"));
   if ((e = cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaStreamCreate"));
@@ -405,9 +412,19 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
 int ntf_plan_sync_grams(ntf_plan* pl, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int m = 0; m < 3; ++m)
+  for (int m = 0; m < 3; ++m) {
     NTF_CUDA_TRY(ntf::gram_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank, pl->d.grams[m],
                                   pl->gram_ws, s));
+    NTF_CUDA_TRY(ntf::colmax_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank,
+                                    pl->d.colmax + m * pl->d.rank, s));
+  }
+  return NTF_OK;
+}
+
+int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t stream) {
+  if (!F || !out) return fail(NTF_ERR_INVALID, "null pointer");
+  if (rows < 1 || R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_INVALID, "bad shape");
+  NTF_CUDA_TRY(ntf::colmax_launch(F, rows, R, out, static_cast<cudaStream_t>(stream)));
   return NTF_OK;
 }
 
@@ -521,6 +538,7 @@ void ntf_plan_destroy(ntf_plan* pl) {
   cudaFree(pl->mtt_ws);
   cudaFree(pl->norm_partials);
   cudaFree(pl->gram_partials);
+  cudaFree(pl->colmax_partials);
   cudaFree(pl->gram_ws);
   cudaFree(pl->done);
   delete pl;

@@ -44,6 +44,38 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Overflow/underflow-safe sum of squares, (scale, ssq) with value
+// scale^2 * ssq, as the reference's BLAS nrm2 under np.linalg.norm
+// (solver.py:247-255): factor columns driven to ~1e-200 by large penalties
+// must not square to zero and fake an exactly consistent split.
+struct ScaledSq {
+  double scale = 0.0, ssq = 0.0;
+  __device__ __forceinline__ void add(double v) {
+    const double a = fabs(v);
+    if (a == 0.0) return;
+    if (a > scale) {
+      const double r = scale / a;
+      ssq = 1.0 + ssq * r * r;
+      scale = a;
+    } else {
+      const double r = a / scale;
+      ssq += r * r;
+    }
+  }
+  __device__ __forceinline__ void merge(double s2, double q2) {
+    if (s2 == 0.0) return;
+    if (s2 > scale) {
+      const double r = scale / s2;
+      ssq = q2 + ssq * r * r;
+      scale = s2;
+    } else {
+      const double r = s2 / scale;
+      ssq += q2 * r * r;
+    }
+  }
+  __device__ __forceinline__ double norm() const { return scale * sqrt(ssq); }
+};
+
 // Error/status flags written by kernels (host reads them back once per run).
 enum DeviceStatus : int {
   kDevOk = 0,

@@ -50,7 +50,8 @@ constexpr int kUK = 16;      // MMA K for kind::f16
 constexpr int kEpiWarps = 4;
 // KR-former warps: more for small N (light epilogue, registers to spare)
 __host__ __device__ constexpr int wf_warps(int NT) { return NT <= 2 ? 8 : 4; }
-__host__ __device__ constexpr int tc_threads(int NT) { return (2 + wf_warps(NT) + kEpiWarps) * 32; }
+// warps: 0 X-tile TMA, 1 MMA, 2 factor-row TMA, KR formers, 4 epilogue
+__host__ __device__ constexpr int tc_threads(int NT) { return (3 + wf_warps(NT) + kEpiWarps) * 32; }
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
@@ -174,8 +175,16 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
          | ((static_cast<uint32_t>(kTM) >> 4) << 24);  // M >> 4
 }
 
+// accumulator sets (5N fp32 columns each) resident in TMEM: double-buffered
+// when two fit in the 512 columns, so the MMA never waits for the epilogue
+__host__ __device__ constexpr int acc_bufs(int N) { return 10 * N <= 512 ? 2 : 1; }
+
 __host__ __device__ constexpr uint32_t tmem_cols(int N) {
-  return 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
+  return acc_bufs(N) * 5 * N <= 32    ? 32
+         : acc_bufs(N) * 5 * N <= 64  ? 64
+         : acc_bufs(N) * 5 * N <= 128 ? 128
+         : acc_bufs(N) * 5 * N <= 256 ? 256
+                                      : 512;
 }
 
 struct TcParams {
@@ -188,11 +197,14 @@ struct TcParams {
   int64_t l_extent;          // extent of the chunked axis (K or J)
   int64_t n_chunks, chunks_per_split, chunks_per_o;
   int n_mtiles, splits;
-  int x_stages, w_stages;
+  int x_stages, w_stages, f_stages;
   int stage_bytes;           // X tiles + factor rows
-  const double* wscale;      // [N] 2^(7 - f(n)),  [N..2N) output scale (with xscale)
+  const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
+  const double* cm_lo;       // [R] max |F_lo[:, n]|
+  const double* xscale;      // tensor split scale (device scalar)
   double* ws;                // [splits][M][R] partials
   const int* stop_flag;
+  int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip KR, 2 skip MMA
 };
 
 __device__ __forceinline__ void fast_two_sum(float& hi, float& lo, float a) {
@@ -208,16 +220,20 @@ __device__ __forceinline__ void fast_two_sum(float& hi, float& lo, float a) {
 __device__ __forceinline__ void emit_w_octet(unsigned char* t0, unsigned char* t1, unsigned char* t2,
                                              int n, int oct, const double (&w)[8]) {
   __align__(16) __half2 h0[4], h1[4], h2[4];
+  // round-to-nearest-even via the 1.5*2^23 magic constant (two FADDs, exact
+  // for |x| < 2^22) instead of the slower FRND
+  constexpr float kMagic = 12582912.0f;
 #pragma unroll
   for (int u = 0; u < 8; u += 2) {
     float a0[2], a1[2], a2[2];
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const float tf = static_cast<float>(w[u + v]);
-      a0[v] = rintf(tf);                                     // integer, |a0| <= 128
+      a0[v] = __fsub_rn(__fadd_rn(tf, kMagic), kMagic);     // integer, |a0| <= 128
       const float r1 = (tf - a0[v]) * 128.0f;                // exact, |r1| <= 64
-      a1[v] = rintf(r1);
-      a2[v] = rintf((r1 - a1[v]) * 128.0f);
+      a1[v] = __fsub_rn(__fadd_rn(r1, kMagic), kMagic);
+      const float r2 = (r1 - a1[v]) * 128.0f;
+      a2[v] = __fsub_rn(__fadd_rn(r2, kMagic), kMagic);
     }
     h0[u / 2] = __floats2half2_rn(a0[0], a0[1]);                          // exact
     h1[u / 2] = __floats2half2_rn(a1[0] * 0.0078125f, a1[1] * 0.0078125f);  // 2^-7 units
@@ -233,32 +249,52 @@ template <int NT>  // N / 16
 __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
   constexpr int kWfWarps = wf_warps(NT);
   constexpr int N = NT * 16;
+  constexpr int kAccBufs = acc_bufs(N);
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // carve: [X stages: S0 16KB | S1 16KB | lo rows 64*R*8 | hi row R*8]
+  // carve: [X stages: S0 16KB | S1 16KB]  (released by the MMA)
+  //        [factor stages: lo rows 64*R*8 | hi row R*8]  (released by KR formers)
   //        [W stages: T0 | T1 | T2 (N*128 each)] [barriers]
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1 KB alignment by offset (keeps the pointer in the shared address space,
+  // so the compiler emits LDS/STS instead of generic loads/stores)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kXTile = kTM * kBK * 2;  // 16 KB
   constexpr int kWTile = N * kBK * 2;    // N * 128 B
-  const int SX = p.x_stages, SW = p.w_stages;
+  const int SX = p.x_stages, SW = p.w_stages, SF = p.f_stages;
   const int R = p.R;
-  const int SB = p.stage_bytes;
+  const int SB = p.stage_bytes;          // factor stage bytes (1 KB aligned)
   unsigned char* xbase = base;
-  unsigned char* wbase = xbase + SX * SB;
+  unsigned char* fbase = xbase + SX * 2 * kXTile;
+  unsigned char* wbase = fbase + SF * SB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + SW * 3 * kWTile);
   uint64_t* x_full = bars;
   uint64_t* x_empty = x_full + SX;
-  uint64_t* w_full = x_empty + SX;
+  uint64_t* f_full = x_empty + SX;
+  uint64_t* f_empty = f_full + SF;
+  uint64_t* w_full = f_empty + SF;
   uint64_t* w_empty = w_full + SW;
   uint64_t* acc_full = w_empty + SW;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // per-column W scales: wsc[n] = 2^(7 - f(n)) with max|F_hi[:,n]| max|F_lo[:,n]|
+  // <= 2^f(n), so |t| = |W| 2^(7-f) <= 128; wsc[N + n] = xscale * 2^(f(n) - 7)
+  double* wsc = reinterpret_cast<double*>(acc_empty + 4);
+  if (threadIdx.x < N) {
+    const int n = threadIdx.x;
+    const double prod = n < p.R ? p.cm_hi[n] * p.cm_lo[n] : 0.0;
+    int f = 0;
+    if (prod > 0.0) frexp(prod, &f);  // prod < 2^f
+    // a column that decayed to ~1e-300 (large penalties shrink factor columns
+    // geometrically) must not overflow the scale: clamp (represented as zero)
+    if (f < -1000) f = -1000;
+    wsc[n] = ldexp(1.0, 7 - f);
+    wsc[N + n] = *p.xscale * ldexp(1.0, f - 7);
+  }
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  constexpr int kWfFirst = 2;
-  constexpr int kEpiFirst = 2 + kWfWarps;
+  constexpr int kWfFirst = 3;
+  constexpr int kEpiFirst = 3 + kWfWarps;
   constexpr int kWfThreads = kWfWarps * 32;
 
   const int tile = blockIdx.x % p.n_mtiles;
@@ -272,7 +308,11 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   if (threadIdx.x == 0) {
     for (int s = 0; s < SX; ++s) {
       mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1 + kWfThreads);  // MMA commit + KR formers (factor rows)
+      mbar_init(&x_empty[s], 1);  // MMA commit
+    }
+    for (int s = 0; s < SF; ++s) {
+      mbar_init(&f_full[s], 1);
+      mbar_init(&f_empty[s], kWfThreads);  // KR formers consumed the rows
     }
     for (int s = 0; s < SW; ++s) {
       mbar_init(&w_full[s], kWfThreads);
@@ -295,18 +335,33 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------ TMA producer ------------------------------
+  if (warp == 2) {
+    // ---------------------------- factor-row producer -------------------------
     if (lane == 0) {
+      // factor rows of each chunk: F_lo[l0 .. l0+63] and F_hi[o]
       const uint32_t fac_bytes = static_cast<uint32_t>((kBK + 1) * R * 8);
+      for (int it = 0; it < n_iter; ++it) {
+        const int fs = it % SF;
+        mbar_wait(&f_empty[fs], ((it / SF) & 1) ^ 1);
+        unsigned char* dlo = fbase + fs * SB;
+        unsigned char* dhi = dlo + kBK * R * 8;
+        mbar_arrive_expect_tx(&f_full[fs], fac_bytes);
+        const int64_t c = c_begin + it;
+        const int o = static_cast<int>(c / p.chunks_per_o);
+        const int l0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
+        tma_load_2d(dlo, &p.tmap_lo, &f_full[fs], 0, l0);
+        tma_load_2d(dhi, &p.tmap_hi, &f_full[fs], 0, o);
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------ X-tile producer ---------------------------
+    if (lane == 0) {
       for (int it = 0; it < n_iter; ++it) {
         const int s = it % SX;
         mbar_wait(&x_empty[s], ((it / SX) & 1) ^ 1);
-        unsigned char* d0 = xbase + s * SB;
+        unsigned char* d0 = xbase + s * 2 * kXTile;
         unsigned char* d1 = d0 + kXTile;
-        unsigned char* dlo = d1 + kXTile;
-        unsigned char* dhi = dlo + kBK * R * 8;
-        mbar_arrive_expect_tx(&x_full[s], 2 * kXTile + fac_bytes);
+        mbar_arrive_expect_tx(&x_full[s], 2 * kXTile);
         const int64_t c = c_begin + it;
         const int o = static_cast<int>(c / p.chunks_per_o);
         const int l0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
@@ -323,30 +378,30 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
           tma_load_3d(d1, &p.tmap1, &x_full[s], mm, l0, o);
           tma_load_3d(d1 + kXTile / 2, &p.tmap1, &x_full[s], mm + 64, l0, o);
         }
-        tma_load_2d(dlo, &p.tmap_lo, &x_full[s], 0, l0);
-        tma_load_2d(dhi, &p.tmap_hi, &x_full[s], 0, o);
       }
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
     if (lane == 0) {
+      // Two wide MMAs per K step, each reading its A tile once: the W slices
+      // T0|T1|T2 are consecutive N-row blocks of one K-major B operand.
+      //   cols [0, 3N):  S0 * [T0 | T1 | T2]     cols [3N, 5N): S1 * [T0 | T1]
       const bool mn = p.mode == 3;
-      const uint32_t idesc = make_idesc(N, mn);
+      const uint32_t idesc3 = make_idesc(3 * N, mn);
+      const uint32_t idesc2 = make_idesc(2 * N, mn);
       for (int it = 0; it < n_iter; ++it) {
-        const int s = it % SX, sw = it % SW, ab = it & 1;
+        const int s = it % SX, sw = it % SW, ab = it % kAccBufs;
         mbar_wait(&x_full[s], (it / SX) & 1);
         mbar_wait(&w_full[sw], (it / SW) & 1);
-        mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&acc_empty[ab], ((it / kAccBufs) & 1) ^ 1);
         tc_fence_after();
-        const unsigned char* a0 = xbase + s * SB;
+        const unsigned char* a0 = xbase + s * 2 * kXTile;
         const unsigned char* a1 = a0 + kXTile;
         const unsigned char* b0 = wbase + sw * 3 * kWTile;
-        const unsigned char* b1 = b0 + kWTile;
-        const unsigned char* b2 = b1 + kWTile;
-        const uint32_t d0 = tmem + ab * 2 * N;
-        const uint32_t d1 = d0 + N;
+        const uint32_t d0 = tmem + ab * 5 * N;
+        const uint32_t d1 = d0 + 3 * N;
 #pragma unroll
-        for (int kk = 0; kk < kBK / kUK; ++kk) {
+        for (int kk = 0; kk < ((p.debug & 2) && it >= 2 ? 0 : kBK / kUK); ++kk) {
           uint64_t da0, da1;
           if (mn) {  // A = X^T: MN-major, atoms of 64 m (8 KB apart), 8 q-rows per 1 KB
             da0 = smem_desc(a0 + kk * 2048, kXTile / 2, 1024);
@@ -355,15 +410,10 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
             da0 = smem_desc(a0 + kk * 32, 16, 1024);
             da1 = smem_desc(a1 + kk * 32, 16, 1024);
           }
-          const uint64_t db0 = smem_desc(b0 + kk * 32, 16, 1024);
-          const uint64_t db1 = smem_desc(b1 + kk * 32, 16, 1024);
-          const uint64_t db2 = smem_desc(b2 + kk * 32, 16, 1024);
+          const uint64_t db = smem_desc(b0 + kk * 32, 16, 1024);
           const uint32_t acc = kk > 0 ? 1u : 0u;
-          tc_mma_f16(d0, da0, db0, idesc, acc);   // S0*T0   exact
-          tc_mma_f16(d1, da0, db1, idesc, acc);   // S0*T1
-          tc_mma_f16(d1, da1, db0, idesc, 1u);    // S1*T0
-          tc_mma_f16(d1, da0, db2, idesc, 1u);    // S0*T2
-          tc_mma_f16(d1, da1, db1, idesc, 1u);    // S1*T1
+          tc_mma_f16(d0, da0, db, idesc3, acc);   // S0*T0 (exact), S0*T1, S0*T2
+          tc_mma_f16(d1, da1, db, idesc2, acc);   // S1*T0, S1*T1
         }
         tc_commit(&x_empty[s]);
         tc_commit(&w_empty[sw]);
@@ -379,18 +429,18 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     const int oct0 = t / N;
     constexpr int kOctStep = kWfThreads / N > 0 ? kWfThreads / N : 1;
     const bool active = t < N * (kBK / 8) && (kWfThreads >= N || true);
-    const double sc = n < R ? p.wscale[n] : 0.0;
+    const double sc = n < R ? wsc[n] : 0.0;
     for (int it = 0; it < n_iter; ++it) {
-      const int s = it % SX, sw = it % SW;
-      mbar_wait(&x_full[s], (it / SX) & 1);
+      const int fs = it % SF, sw = it % SW;
+      mbar_wait(&f_full[fs], (it / SF) & 1);
       mbar_wait(&w_empty[sw], ((it / SW) & 1) ^ 1);
-      const unsigned char* srow = xbase + s * SB + 2 * kXTile;
+      const unsigned char* srow = fbase + fs * SB;
       const double* lo_s = reinterpret_cast<const double*>(srow);
       const double* hi_s = lo_s + kBK * R;
       unsigned char* t0 = wbase + sw * 3 * kWTile;
       unsigned char* t1 = t0 + kWTile;
       unsigned char* t2 = t1 + kWTile;
-      if (active) {
+      if (active && !((p.debug & 1) && it >= SW)) {
         const double hs = n < R ? hi_s[n] * sc : 0.0;
         for (int oct = oct0; oct < kBK / 8; oct += kOctStep) {
           double w[8];
@@ -401,7 +451,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       }
       fence_proxy_async();
       mbar_arrive(&w_full[sw]);
-      mbar_arrive(&x_empty[s]);  // factor rows consumed
+      mbar_arrive(&f_empty[fs]);  // factor rows consumed
     }
   } else {
     // ------------------------------ epilogue ----------------------------------
@@ -414,21 +464,27 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       lo[j] = 0.f;
     }
     for (int it = 0; it < n_iter; ++it) {
-      const int ab = it & 1;
-      mbar_wait(&acc_full[ab], (it >> 1) & 1);
+      const int ab = it % kAccBufs;
+      mbar_wait(&acc_full[ab], (it / kAccBufs) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ab * 2 * N;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ab * 5 * N;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        float a0[16], a1[16];
-        tmem_ld16(taddr + j * 16, a0);
-        tmem_ld16(taddr + N + j * 16, a1);
+      for (int j = 0; j < ((p.debug & 4) && it >= 2 ? 0 : NT); ++j) {
+        float a0[16], a1[16], a2[16];
+        tmem_ld16(taddr + j * 16, a0);           // S0*T0 (exact integers)
+        tmem_ld16(taddr + N + j * 16, a1);       // S0*T1
+        tmem_ld16(taddr + 2 * N + j * 16, a2);   // S0*T2
         tmem_wait_ld();
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           fast_two_sum(hi[j * 16 + u], lo[j * 16 + u], a0[u]);
-          lo[j * 16 + u] += a1[u];
+          a1[u] += a2[u];
         }
+        tmem_ld16(taddr + 3 * N + j * 16, a0);   // S1*T0
+        tmem_ld16(taddr + 4 * N + j * 16, a2);   // S1*T1
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) lo[j * 16 + u] += (a1[u] + a0[u]) + a2[u];
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
@@ -439,7 +495,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * R;
 #pragma unroll
       for (int j = 0; j < N; ++j)
-        if (j < R) out[j] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * p.wscale[N + j];
+        if (j < R) out[j] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * wsc[N + j];
     }
   }
   tc_fence_before();
@@ -481,42 +537,18 @@ __global__ void split_kernel(const float* __restrict__ X, int64_t n, const unsig
   }
 }
 
-// per-column W scales: wscale[n] = 2^(7 - f(n)) with max|Fhi[:,n]| max|Flo[:,n]| <= 2^f(n);
-// wscale[N + n] = xscale * 2^(f(n) - 7)
-__global__ void wscale_kernel(const double* __restrict__ Fhi, int64_t hi_rows,
-                              const double* __restrict__ Flo, int64_t lo_rows, int R, int N,
-                              const double* xscale, double* wscale, const int* stop_flag) {
-  if (stop_flag && *stop_flag) return;
-  const int n = blockIdx.x;
-  double mh = 0.0, ml = 0.0;
-  if (n < R) {
-    for (int64_t i = threadIdx.x; i < hi_rows; i += blockDim.x) mh = fmax(mh, fabs(Fhi[i * R + n]));
-    for (int64_t i = threadIdx.x; i < lo_rows; i += blockDim.x) ml = fmax(ml, fabs(Flo[i * R + n]));
-  }
-  __shared__ double sh[2][32];
-  for (int o = 16; o > 0; o >>= 1) {
-    mh = fmax(mh, __shfl_xor_sync(0xffffffffu, mh, o));
-    ml = fmax(ml, __shfl_xor_sync(0xffffffffu, ml, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    sh[0][threadIdx.x >> 5] = mh;
-    sh[1][threadIdx.x >> 5] = ml;
-  }
+// out[r] = max_i |F[i][r]| (one block per column; max is order-free)
+__global__ void colmax_kernel(const double* __restrict__ F, int64_t rows, int R, double* out) {
+  const int r = blockIdx.x;
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) m = fmax(m, fabs(F[i * R + r]));
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
-      mh = fmax(mh, sh[0][w]);
-      ml = fmax(ml, sh[1][w]);
-    }
-    const double prod = mh * ml;
-    int f = 0;
-    if (prod > 0.0) frexp(prod, &f);  // prod < 2^f
-    // A column that has decayed to ~1e-300 (large penalties shrink factor
-    // columns geometrically) must not overflow the 2^(7-f) slice scale: clamp,
-    // which represents it as zero (absolute error < 2^-990).
-    if (f < -1000) f = -1000;
-    wscale[n] = ldexp(1.0, 7 - f);
-    wscale[N + n] = *xscale * ldexp(1.0, f - 7);
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    out[r] = m;
   }
 }
 
@@ -620,19 +652,30 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.n_chunks = o_ext * L.chunks_per_o;
   L.n_wf_warps = wf_warps(L.N / 16);
   L.threads = tc_threads(L.N / 16);
-  const int xs = 2 * kTM * kBK * 2 + (kBK + 1) * R * 8;
-  L.stage_bytes = (xs + 1023) & ~1023;
+  // X ring as deep as shared memory allows (bytes in flight hide HBM latency);
+  // the factor-row and KR rings only need to stay a few chunks ahead.
+  const int xs = 2 * kTM * kBK * 2;
+  L.stage_bytes = ((kBK + 1) * R * 8 + 1023) & ~1023;  // factor stage
   const int wsz = 3 * L.N * kBK * 2;
   L.x_stages = 4;
+  L.f_stages = 3;
   L.w_stages = 3;
-  auto total = [&]() { return 1024 + L.x_stages * L.stage_bytes + L.w_stages * wsz + 256; };
+  if (const char* e2 = getenv("NTF_TC_WSTAGES")) L.w_stages = atoi(e2);
+  auto total = [&]() {
+    // + barriers, TMEM slot and the 2N per-column scales
+    return 1024 + L.x_stages * xs + L.f_stages * L.stage_bytes + L.w_stages * wsz + 512 + 16 * L.N;
+  };
+  const char* env = getenv("NTF_TC_XSTAGES");
+  if (env) L.x_stages = atoi(env);
   while (total() > 227 * 1024 && L.x_stages > 2) --L.x_stages;
-  while (total() > 227 * 1024 && L.w_stages > 2) --L.w_stages;
+  while (total() > 227 * 1024 && L.f_stages > 2) --L.f_stages;
   L.smem_bytes = total();
   L.tmem_cols = static_cast<int>(tmem_cols(L.N));
   // one CTA per SM; split the chunk range so that the grid is one wave
   const int sms = sm_count_tc();
-  int splits = sms / L.n_mtiles;
+  // one SM is left free so the mode's ridge Cholesky (side stream) runs
+  // concurrently instead of queueing behind the MTTKRP
+  int splits = (sms - 1) / L.n_mtiles;
   if (splits < 1) splits = 1;
   if (splits > L.n_chunks) splits = static_cast<int>(L.n_chunks);
   L.chunks_per_split = (L.n_chunks + splits - 1) / splits;
@@ -727,9 +770,14 @@ void mttkrp_tc_unbind(MttkrpTCLaunch& L) {
   L.bound = false;
 }
 
+cudaError_t colmax_launch(const double* F, int64_t rows, int R, double* out, cudaStream_t stream) {
+  colmax_kernel<<<R, 256, 0, stream>>>(F, rows, R, out);
+  return cudaGetLastError();
+}
+
 cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
-                             const double* B, const double* C, double* ws, const int* stop_flag,
-                             cudaStream_t stream) {
+                             const double* B, const double* C, const double* colmax3, double* ws,
+                             const int* stop_flag, cudaStream_t stream) {
   if (!L.bound) return cudaErrorInvalidValue;
   const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
   const double *Fhi, *Flo;
@@ -768,14 +816,31 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   p.splits = L.splits;
   p.x_stages = L.x_stages;
   p.w_stages = L.w_stages;
+  p.f_stages = L.f_stages;
   p.stage_bytes = L.stage_bytes;
   p.ws = ws;
   p.stop_flag = stop_flag;
-  p.wscale = L.wscale;
-  wscale_kernel<<<L.N, 256, 0, stream>>>(Fhi, hi_rows, Flo, lo_rows, L.R, L.N, t.xscale, L.wscale,
-                                         stop_flag);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* env = getenv("NTF_TC_DEBUG");
+      dbg = env ? atoi(env) : 0;
+    }
+    p.debug = dbg;
+  }
+  p.xscale = t.xscale;
+  if (colmax3) {  // plan: column maxima kept current by the row-update kernels
+    const int hm = L.mode == 1 ? 1 : 0, lm = L.mode == 3 ? 1 : 2;
+    p.cm_hi = colmax3 + hm * L.R;
+    p.cm_lo = colmax3 + lm * L.R;
+  } else {        // one-shot call: compute them here
+    colmax_kernel<<<L.R, 256, 0, stream>>>(Fhi, hi_rows, L.R, L.wscale);
+    colmax_kernel<<<L.R, 256, 0, stream>>>(Flo, lo_rows, L.R, L.wscale + L.R);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    p.cm_hi = L.wscale;
+    p.cm_lo = L.wscale + L.R;
+  }
   return dispatch_tc(p, L, stream, false);
 }
 

@@ -30,7 +30,7 @@ struct MttkrpTCLaunch {
   int n_mtiles, splits;     // splits per m-tile
   int64_t n_chunks, chunks_per_split, chunks_per_o;
   int n_wf_warps, threads, smem_bytes;
-  int x_stages, w_stages, stage_bytes;
+  int x_stages, w_stages, f_stages, stage_bytes;
   int tmem_cols;
   CUtensorMap tmap0, tmap1; // S0 / S1 planes (built by mttkrp_tc_bind)
   CUtensorMap tmap_lo, tmap_hi;      // factor rows (cached per factor pointer)
@@ -49,8 +49,11 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L);
 // Encode the tensor maps of the split planes and allocate the scale buffer.
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t);
 void mttkrp_tc_unbind(MttkrpTCLaunch& L);
+// colmax3: [3][R] per-factor column maxima of |F| (NULL: computed here)
 cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
-                             const double* B, const double* C, double* ws, const int* stop_flag,
-                             cudaStream_t stream);
+                             const double* B, const double* C, const double* colmax3, double* ws,
+                             const int* stop_flag, cudaStream_t stream);
+// out[r] = max_i |F[i][r]|
+cudaError_t colmax_launch(const double* F, int64_t rows, int R, double* out, cudaStream_t stream);
 
 }  // namespace ntf

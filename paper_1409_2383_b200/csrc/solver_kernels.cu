@@ -62,25 +62,73 @@ __device__ void build_and_factor(double* L, int ldl, int R, const double* __rest
   __syncthreads();
 }
 
+// Fixed-order sum of n strided values with 8 independent load/add chains
+// (latency-bound reductions over L2-resident partials).  The combination
+// order is fixed, so results are bitwise reproducible.
+__device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t n,
+                                              int64_t stride) {
+  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t s = 0; s < n; s += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)  // static indices: the chains stay in registers
+      if (s + u < n) a[u] += p[(s + u) * stride];
+  }
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // One block: H = G_a o G_b + rho I, Cholesky, then L (row-major R x R, lower)
 // and 1/diag(L) to global for the row-update kernel.  Runs concurrently with
 // the mode's MTTKRP (it only depends on the companion Grams and rho).
+// Output layout of the ridge buffer:
+//   [0, R*R)            L, row-major lower Cholesky factor of H
+//   [R*R, R*R+R)        1 / diag(L)
+//   [R*R+R, 2R*R+R)     H^-1 = L^-T L^-1  (R <= 64 only)
+//   [2R*R+R, 3R*R+R)    H = G_a o G_b + rho I
 __global__ void ridge_factor_kernel(RidgeParams p) {
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
   const int ldl = R + 1;
   double* L = reinterpret_cast<double*>(smem_raw);
+  double* Li = L + R * ldl;  // L^-1 (lower), R <= 64
   __shared__ bool bad;
   if (threadIdx.x == 0) bad = false;
   __syncthreads();
-  build_and_factor(L, ldl, R, p.Ga, p.Gb, p.rho[p.mode - 1], p.status, &bad);
+  const double rho = p.rho[p.mode - 1];
+  double* Hout = p.L + 2 * R * R + R;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    Hout[e] = p.Ga[e] * p.Gb[e] + (i == k ? rho : 0.0);
+  }
+  build_and_factor(L, ldl, R, p.Ga, p.Gb, rho, p.status, &bad);
   if (bad) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
     p.L[e] = k <= i ? L[i * ldl + k] : 0.0;
   }
   for (int j = threadIdx.x; j < R; j += blockDim.x) p.L[R * R + j] = 1.0 / L[j * ldl + j];
+  if (R > 64) return;
+  // L^-1 by forward substitution on the identity, one column per thread
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    for (int i = 0; i < R; ++i) {
+      double s = i == j ? 1.0 : 0.0;
+      if (i < j) {
+        Li[i * ldl + j] = 0.0;
+        continue;
+      }
+      for (int k = j; k < i; ++k) s -= L[i * ldl + k] * Li[k * ldl + j];
+      Li[i * ldl + j] = s / L[i * ldl + i];
+    }
+  }
+  __syncthreads();
+  // H^-1 = L^-T L^-1: (a, b) = sum_{i >= max(a,b)} Li[i][a] Li[i][b]
+  double* Hinv = p.L + R * R + R;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e - (e / R) * R;
+    double s = 0.0;
+    for (int i = a > b ? a : b; i < R; ++i) s += Li[i * ldl + a] * Li[i * ldl + b];
+    Hinv[e] = s;
+  }
 }
 
 // Row solve of X (L L^T) = rhs for one row held by a warp: lane owns entries
@@ -125,7 +173,7 @@ __device__ __forceinline__ void warp_chol_solve(double (&y)[RT], const double* L
 }
 
 template <int RT>
-__global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdateParams p) {
+__global__ void __launch_bounds__(kUpdThreads, 1) factor_update_kernel(FactorUpdateParams p) {
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
@@ -135,15 +183,25 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   const int kRowsPerBlock = rows_per_block(R);
   double* xrows = inv_diag + R;                 // [rows][R] new factor rows
   double* msum = xrows + kRowsPerBlock * R;     // [rows][R] reduced MTTKRP rows
-  double* red = msum + kRowsPerBlock * R;       // [8 warps][5]
+  // [8 warps][5][scale, ssq], after the GEMV path's H / rhs / x1 buffers when RT <= 2
+  double* red = msum + kRowsPerBlock * R + (RT <= 2 ? R * R + 2 * kRowsPerBlock * R : 0);
   __shared__ bool is_last;
   // Ridge factor from the concurrent ridge_factor_kernel (solver.py:167-175)
   if (*p.status == kDevNotPD) return;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, k = e - (e / R) * R;
-    L[i * ldl + k] = p.Lg[e];
+  if constexpr (RT <= 2) {
+    // H^-1 into L's slot (pitch R) and H after the MTTKRP row sums
+    double* Hm = msum + kRowsPerBlock * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      L[e] = p.Lg[R * R + R + e];
+      Hm[e] = p.Lg[2 * R * R + R + e];
+    }
+  } else {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, k = e - (e / R) * R;
+      L[i * ldl + k] = p.Lg[e];
+    }
+    for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
   }
-  for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
 
   const int64_t row_base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
   const int64_t n_rows = p.rows;
@@ -157,7 +215,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
     if (cnt > static_cast<int64_t>(kRowsPerBlock) * R) cnt = static_cast<int64_t>(kRowsPerBlock) * R;
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
       double m = 0.0;
-      for (int s = 0; s < p.splits; ++s) m += p.mtt[s * nM + base + e];
+      if (!(p.debug & 1)) m = strided_sum(p.mtt + base + e, p.splits, nM);
       msum[e] = m;
     }
   }
@@ -169,8 +227,88 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   const int warp = threadIdx.x >> 5;
   const int nwarps = kUpdThreads / 32;
 
-  double nrm[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int lr = warp; lr < kRowsPerBlock; lr += nwarps) {
+  ScaledSq nrm[5];
+  if constexpr (RT <= 2) {
+    // R <= 64: all rows of the block at once as small GEMMs against the
+    // ridge inverse, with one step of iterative refinement against H itself:
+    //   x1 = y H^-1,  x = x1 + (y - x1 H) H^-1
+    // Every (row, column) pair is independent: no sequential substitution
+    // chain on the critical path.  Agreement with cho_solve (solver.py:188)
+    // is at the backward-error level.
+    double* Hi = L;                          // reuse: [R][R] H^-1
+    double* Hm = msum + kRowsPerBlock * R;   // [R][R] H   (after msum)
+    double* yb = Hm + R * R;                 // [rows][R]  rhs, then residual
+    double* x1 = yb + kRowsPerBlock * R;     // [rows][R]
+    const int np = kRowsPerBlock * R;
+    for (int e = threadIdx.x; e < np; e += blockDim.x) {
+      const int lr = e / R, c = e - (e / R) * R;
+      const int64_t row = row_base + lr;
+      double y = 0.0;
+      if (row < n_rows) {
+        const int64_t g = row * R + c;
+        y = (msum[e] + rho * p.aux[g]) - p.dual[g];  // ridge_rhs (solver.py:178-179)
+      }
+      yb[e] = y;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < np; e += blockDim.x) {
+      const int lr = e / R, c = e - (e / R) * R;
+      double s = 0.0;
+      for (int k = 0; k < R; ++k) s = fma(yb[lr * R + k], Hi[k * R + c], s);
+      x1[e] = s;
+    }
+    __syncthreads();
+    double res[4];  // np / blockDim <= 4 (rows 16 x R <= 64 over 256 threads)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * kUpdThreads;
+      res[u] = 0.0;
+      if (e < np) {
+        const int lr = e / R, c = e - (e / R) * R;
+        double s = yb[e];
+        for (int k = 0; k < R; ++k) s = fma(-x1[lr * R + k], Hm[k * R + c], s);
+        res[u] = s;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * kUpdThreads;
+      if (e < np) yb[e] = res[u];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < np; e += blockDim.x) {
+      const int lr = e / R, c = e - (e / R) * R;
+      const int64_t row = row_base + lr;
+      double x = x1[e];
+      for (int k = 0; k < R; ++k) x = fma(yb[lr * R + k], Hi[k * R + c], x);
+      if (row >= n_rows) {
+        xrows[e] = 0.0;
+        continue;
+      }
+      const int64_t g = row * R + c;
+      p.F[(p.row_offset + row) * R + c] = x;
+      xrows[e] = x;
+      if (p.last_sweep) {
+        // aux = project(F + Y/rho), Y += rho (F - aux), residual partials
+        const double yd = p.dual[g];
+        const double a_old = p.aux[g];
+        const double v = x + yd / rho;
+        if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
+        const double a = v > 0.0 ? v : 0.0;
+        const double ynew = yd + rho * (x - a);
+        p.aux[g] = a;
+        p.dual[g] = ynew;
+        const double d0 = x - a, d1 = a - a_old;
+        nrm[0].add(d0);
+        nrm[1].add(d1);
+        nrm[2].add(x);
+        nrm[3].add(a);
+        nrm[4].add(ynew);
+      }
+    }
+  }
+  for (int lr = warp; RT > 2 && lr < kRowsPerBlock; lr += nwarps) {
     const int64_t row = row_base + lr;
     double y[RT];
     if (row < n_rows) {
@@ -184,7 +322,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
           y[t] = (msum[lr * R + r] + rho * p.aux[e]) - p.dual[e];
         }
       }
-      warp_chol_solve<RT>(y, L, ldl, R, inv_diag, lane);
+      if (!(p.debug & 2)) warp_chol_solve<RT>(y, L, ldl, R, inv_diag, lane);
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int r = lane + 32 * t;
@@ -205,11 +343,11 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
             p.aux[e] = a;
             p.dual[e] = ynew;
             const double d0 = x - a, d1 = a - a_old;
-            nrm[0] += d0 * d0;
-            nrm[1] += d1 * d1;
-            nrm[2] += x * x;
-            nrm[3] += a * a;
-            nrm[4] += ynew * ynew;
+            nrm[0].add(d0);
+            nrm[1].add(d1);
+            nrm[2].add(x);
+            nrm[3].add(a);
+            nrm[4].add(ynew);
           }
         }
       }
@@ -226,15 +364,26 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   if (p.last_sweep) {
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      const double v = warp_sum(nrm[c]);
-      if (lane == 0) red[warp * 5 + c] = v;
+      ScaledSq v = nrm[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double s2 = __shfl_xor_sync(0xffffffffu, v.scale, o);
+        const double q2 = __shfl_xor_sync(0xffffffffu, v.ssq, o);
+        v.merge(s2, q2);
+      }
+      if (lane == 0) {
+        red[(warp * 5 + c) * 2] = v.scale;
+        red[(warp * 5 + c) * 2 + 1] = v.ssq;
+      }
     }
   }
   __syncthreads();
   if (p.last_sweep && threadIdx.x < 5) {
-    double s = 0.0;
-    for (int w = 0; w < nwarps; ++w) s += red[w * 5 + threadIdx.x];
-    p.norm_partials[blockIdx.x * 5 + threadIdx.x] = s;
+    ScaledSq s;
+    for (int w = 0; w < nwarps; ++w)
+      s.merge(red[(w * 5 + threadIdx.x) * 2], red[(w * 5 + threadIdx.x) * 2 + 1]);
+    p.norm_partials[(blockIdx.x * 5 + threadIdx.x) * 2] = s.scale;
+    p.norm_partials[(blockIdx.x * 5 + threadIdx.x) * 2 + 1] = s.ssq;
   }
   if (p.fuse_gram) {
     // partial Gram of this block's new rows, fixed row order
@@ -244,6 +393,12 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
       double acc = 0.0;
       for (int lr = 0; lr < kRowsPerBlock; ++lr) acc += xrows[lr * R + r] * xrows[lr * R + s];
       gp[e] = acc;
+    }
+    // per-column max |F| of this block's rows (W scales of the next MTTKRPs)
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      double mx = 0.0;
+      for (int lr = 0; lr < kRowsPerBlock; ++lr) mx = fmax(mx, fabs(xrows[lr * R + r]));
+      p.colmax_partials[blockIdx.x * R + r] = mx;
     }
   }
   if (!p.fuse_gram && !p.last_sweep) return;
@@ -258,17 +413,37 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_kernel(FactorUpdate
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  if (p.fuse_gram) {
+  if (p.fuse_gram && !(p.debug & 4)) {
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
       double s = 0.0;
-      for (int b = 0; b < nblocks; ++b) s += p.gram_partials[static_cast<int64_t>(b) * R * R + e];
+      s = strided_sum(p.gram_partials + e, nblocks, static_cast<int64_t>(R) * R);
       p.G_out[e] = s;
     }
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      double mx = 0.0;  // max is order-independent: exact and deterministic
+      for (int b = 0; b < nblocks; ++b) mx = fmax(mx, p.colmax_partials[b * R + r]);
+      p.colmax_out[r] = mx;
+    }
   }
-  if (p.last_sweep && threadIdx.x < 5) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += p.norm_partials[b * 5 + threadIdx.x];
-    p.norm_acc[threadIdx.x] = s;
+  if (p.last_sweep) {
+    // 8 interleaved merge chains per norm (fixed order), then chain 0..7 merged
+    __syncthreads();
+    if (threadIdx.x < 40) {
+      const int c = threadIdx.x >> 3, ch = threadIdx.x & 7;
+      ScaledSq s;
+      for (int b = ch; b < nblocks; b += 8)
+        s.merge(p.norm_partials[(b * 5 + c) * 2], p.norm_partials[(b * 5 + c) * 2 + 1]);
+      red[threadIdx.x * 2] = s.scale;
+      red[threadIdx.x * 2 + 1] = s.ssq;
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+      ScaledSq s;
+      for (int ch = 0; ch < 8; ++ch)
+        s.merge(red[(threadIdx.x * 8 + ch) * 2], red[(threadIdx.x * 8 + ch) * 2 + 1]);
+      p.norm_acc[threadIdx.x * 2] = s.scale;
+      p.norm_acc[threadIdx.x * 2 + 1] = s.ssq;
+    }
   }
   if (threadIdx.x == 0) *p.done_counter = 0u;
 }
@@ -319,11 +494,17 @@ __global__ void finalize_kernel(FinalizeParams p) {
   double primal[3], dual[3];
   bool stop = true;
   for (int m = 0; m < 3; ++m) {
-    const double* a = p.norm_acc + 5 * m;
-    primal[m] = sqrt(a[0]);
-    dual[m] = p.rho[m] * sqrt(a[1]);
+    // merge the shards' (scale, ssq) pairs in rank order
+    ScaledSq a[5];
+    for (int q = 0; q < p.norm_parts; ++q)
+      for (int c = 0; c < 5; ++c) {
+        const double* s = p.norm_acc + ((q * 3 + m) * 5 + c) * 2;
+        a[c].merge(s[0], s[1]);
+      }
+    primal[m] = a[0].norm();
+    dual[m] = p.rho[m] * a[1].norm();
     const double base = sqrt(static_cast<double>(p.dims[m]) * p.R) * p.eps_abs;
-    const double fn = sqrt(a[2]), an = sqrt(a[3]), yn = sqrt(a[4]);
+    const double fn = a[2].norm(), an = a[3].norm(), yn = a[4].norm();
     const double pthr = base + p.eps_rel * (fn > an ? fn : an);
     const double dthr = base + p.eps_rel * yn;
     if (primal[m] > pthr || dual[m] > dthr) stop = false;
@@ -471,12 +652,17 @@ int factor_update_blocks(int64_t rows, int R) {
 }
 
 size_t factor_update_smem(int R) {
-  const int rpb = rows_per_block(R);
-  return (static_cast<size_t>(R) * (R + 1) + R + 2 * static_cast<size_t>(rpb) * R + 8 * 5) *
-         sizeof(double);
+  const size_t rpb = rows_per_block(R);
+  size_t n = static_cast<size_t>(R) * (R + 1) + R + 2 * rpb * R + 8 * 10;
+  if (R <= 64) n += static_cast<size_t>(R) * R + 2 * rpb * R;  // GEMV path buffers
+  return n * sizeof(double);
 }
 
-size_t ridge_factor_smem(int R) { return static_cast<size_t>(R) * (R + 1) * sizeof(double); }
+size_t ridge_factor_smem(int R) {
+  return static_cast<size_t>(R <= 64 ? 2 : 1) * R * (R + 1) * sizeof(double);
+}
+
+size_t ridge_buffer_doubles(int R) { return 3 * static_cast<size_t>(R) * R + R; }
 
 cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream) {
   ridge_factor_kernel<<<1, 256, ridge_factor_smem(p.R), stream>>>(p);
@@ -499,7 +685,14 @@ cudaError_t factor_update_prepare(int R) {
                               smem);
 }
 
-cudaError_t factor_update_launch(const FactorUpdateParams& p, cudaStream_t stream) {
+cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t stream) {
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* env = getenv("NTF_UPD_DEBUG");
+    dbg = env ? atoi(env) : 0;
+  }
+  FactorUpdateParams p = p_in;
+  p.debug = dbg;
   const int blocks = factor_update_blocks(p.rows, p.R);
   const size_t smem = factor_update_smem(p.R);
   const int rt = (p.R + 31) / 32;

@@ -21,17 +21,21 @@ struct FactorUpdateParams {
   double* dual;             // owned rows
   int last_sweep;
   int fuse_gram;
-  double* norm_partials;    // [blocks][5]
+  double* norm_partials;    // [blocks][5][scale, ssq]
   double* gram_partials;    // [blocks][R][R]
   double* G_out;            // R x R (fuse_gram)
-  double* norm_acc;         // [5] this mode
+  double* colmax_partials;  // [blocks][R]
+  double* colmax_out;       // [R] max |F[:, r]| (fuse_gram)
+  double* norm_acc;         // [5][scale, ssq] this mode
   unsigned* done_counter;
   int* status;
   const int* stop_flag;
+  int debug;                // profiling only (NTF_UPD_DEBUG)
 };
 
 struct FinalizeParams {
-  const double* norm_acc;   // [3][5]
+  const double* norm_acc;   // [parts][3][5][scale, ssq]
+  int norm_parts;           // shards whose norms are merged (1 unsharded)
   double* rho;              // [3] in/out
   int64_t dims[3];
   int R;
@@ -56,6 +60,7 @@ struct RidgeParams {
 
 int factor_update_blocks(int64_t rows, int R);
 size_t ridge_factor_smem(int R);
+size_t ridge_buffer_doubles(int R);
 cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream);
 size_t factor_update_smem(int R);
 cudaError_t factor_update_prepare(int R);

@@ -8,8 +8,10 @@ X[:,:,K_p].  A mode-n update is then entirely local (MTTKRP of the owned rows
 from the local slab, the shared ridge Cholesky, the row solves and the fused
 aux/dual step); the one exchange per mode update is an all-gather of the
 updated row block, after which every rank recomputes the same Gram locally.
-Once per outer iteration the 15 residual sums of squares are all-reduced so
-the stop test and the penalty adaptation are replicated bit-identically.
+Once per outer iteration the 15 scaled residual sums of squares
+((scale, ssq) pairs, nrm2-style) are all-gathered and merged in rank order by
+every rank's finalize, so the stop test and the penalty adaptation are
+replicated bit-identically.
 
 ``sharded_iteration`` is written against a small problem interface so the
 collective logic can be exercised on CPU with the gloo backend
@@ -82,6 +84,10 @@ class Comm:
     def all_reduce_(self, t) -> None:
         self.dist.all_reduce(t, group=self.group)
 
+    def all_gather_(self, out, t) -> None:
+        """out[q * t.numel():(q + 1) * t.numel()] = rank q's ``t``."""
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+
     def gather_rows(self, full, offsets: Sequence[int], counts: Sequence[int]) -> None:
         """In place: every rank's owned block of ``full`` (rows offsets[p] ..
         +counts[p]) is broadcast to all ranks.  Blocks are padded to the
@@ -104,7 +110,7 @@ class Comm:
 def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
     """One outer iteration of the sharded solver (reference solver.py:295-327
     semantics; mesh.py:149-237 data flow).  ``prob`` provides mode_update,
-    refresh_gram, finalize, factors, norm_acc, offsets/counts."""
+    refresh_gram, finalize, factors, norm_acc, norm_all, offsets/counts."""
     sweeps = config.inner_sweeps
     for sw in range(sweeps):
         for mode in (1, 2, 3):
@@ -112,7 +118,7 @@ def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
             prob.mode_update(mode, sw == sweeps - 1)
             comm.gather_rows(prob.factors[m], prob.offsets[m], prob.counts[m])
             prob.refresh_gram(m)
-    comm.all_reduce_(prob.norm_acc)
+    comm.all_gather_(prob.norm_all, prob.norm_acc)
     prob.finalize()
 
 
@@ -129,7 +135,7 @@ def _sharded_problem_class():
             own_off = tuple(self.offsets[m][p] for m in range(3))
             own_cnt = tuple(self.counts[m][p] for m in range(3))
             super().__init__(x_slabs[0], dims, rank, config, cap, engine,
-                             slabs=Slabs(list(x_slabs), own_off, own_cnt))
+                             slabs=Slabs(list(x_slabs), own_off, own_cnt), norm_parts=comm.size)
 
         def step(self) -> None:
             torch = self.torch

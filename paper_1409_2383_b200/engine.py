@@ -11,7 +11,7 @@ HBM layout (row-major, fp64 unless noted):
   factors[m]         I_m x R   working factors (replicated across ranks)
   aux[m], duals[m]   I_m x R   (owned rows only when sharded)
   grams[m]           R x R     F_m^T F_m, refreshed by each mode update
-  rho[3], norm_acc[15], counters int32[4]
+  rho[3], norm_acc[3][5][2] (scale, ssq), counters int32[4]
   resid_history      cap x 6,  rho_history cap x 3
 """
 
@@ -150,7 +150,8 @@ class DeviceProblem:
     """HBM state of one fit and its C-ABI plan."""
 
     def __init__(self, x, dims, rank: int, config, history_capacity: int, engine: int = N.ENGINE_AUTO,
-                 slabs: Slabs | None = None, stream=None, rho_schedule=None):
+                 slabs: Slabs | None = None, stream=None, rho_schedule=None,
+                 norm_parts: int = 1):
         torch = _torch()
         self.torch = torch
         self.lib = N.load()
@@ -172,8 +173,12 @@ class DeviceProblem:
             self.aux = [torch.zeros((c, R), dtype=f64, device=dev) for c in slabs.row_count]
             self.duals = [torch.zeros((c, R), dtype=f64, device=dev) for c in slabs.row_count]
             self.grams = [torch.zeros((R, R), dtype=f64, device=dev) for _ in range(3)]
+            self.colmax = torch.zeros((3, R), dtype=f64, device=dev)
             self.rho = torch.zeros(3, dtype=f64, device=dev)
-            self.norm_acc = torch.zeros(15, dtype=f64, device=dev)
+            self.norm_acc = torch.zeros(30, dtype=f64, device=dev)
+            # every shard's norm_acc, gathered before finalize (sharded runs)
+            self.norm_all = (torch.zeros(norm_parts * 30, dtype=f64, device=dev)
+                             if norm_parts > 1 else None)
             cap = max(1, int(history_capacity))
             self.cap = cap
             self.resid_hist = torch.zeros((cap, 6), dtype=f64, device=dev)
@@ -193,6 +198,7 @@ class DeviceProblem:
             d.aux[m] = _ptr(self.aux[m])
             d.duals[m] = _ptr(self.duals[m])
             d.grams[m] = _ptr(self.grams[m])
+        d.colmax = _ptr(self.colmax)
         d.rank = R
         d.engine = int(engine)
         d.fuse_gram = 0 if self.sharded else 1
@@ -205,6 +211,9 @@ class DeviceProblem:
         d.adapt = 1 if config.adapt else 0
         d.rho = _ptr(self.rho)
         d.norm_acc = _ptr(self.norm_acc)
+        if self.norm_all is not None:
+            d.norm_all = _ptr(self.norm_all)
+            d.norm_parts = int(norm_parts)
         d.history_capacity = cap
         d.resid_history = _ptr(self.resid_hist)
         d.rho_history = _ptr(self.rho_hist)
@@ -297,6 +306,8 @@ class DeviceProblem:
                 self._gram_ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=self.device)
         N.check(lib.ntf_gram(_ptr(self.factors[m]), rows, self.R, _ptr(self.grams[m]),
                              _ptr(self._gram_ws), self._gram_ws.numel() * 8, self._sh))
+        N.check(lib.ntf_colmax(_ptr(self.factors[m]), rows, self.R,
+                               self.colmax.data_ptr() + m * self.R * 8, self._sh))
 
     def counters_host(self) -> np.ndarray:
         self.stream.synchronize()

@@ -1,6 +1,7 @@
 """Multi-process (world_size 2 and 3, gloo, CPU) tests of the sharded
 iteration's host logic: slab extraction, padded all-gather of uneven row
-blocks, norm all-reduce and the per-mode ordering.  The per-rank compute is a
+blocks, the gather of the scaled (scale, ssq) residual norms and their
+rank-order merge, and the per-mode ordering.  The per-rank compute is a
 numpy stand-in built on the oracle (test-only), so the collective logic of
 ``paper_1409_2383_b200.distributed.sharded_iteration`` is checked against the
 centralized oracle trajectory to 1e-12 (the reference mesh's bar,
@@ -44,7 +45,8 @@ class CpuShardProblem:
         self.aux = [init.aux[m][own[m]].copy() for m in range(3)]
         self.duals = [init.duals[m][own[m]].copy() for m in range(3)]
         self.rho = list(init.rho)
-        self.norm_acc = torch.zeros(15, dtype=torch.float64)
+        self.norm_acc = torch.zeros(30, dtype=torch.float64)
+        self.norm_all = torch.zeros(30 * len(plan.extents[0]), dtype=torch.float64)
         self.history = []
 
     def mode_update(self, mode, last):
@@ -57,18 +59,32 @@ class CpuShardProblem:
         if last:
             a = np.maximum(x + self.duals[m] / self.rho[m], 0.0)
             y = self.duals[m] + self.rho[m] * (x - a)
-            acc = [np.sum((x - a) ** 2), np.sum((a - self.aux[m]) ** 2), np.sum(x ** 2),
-                   np.sum(a ** 2), np.sum(y ** 2)]
-            self.norm_acc[5 * m: 5 * m + 5] = torch.tensor(acc, dtype=torch.float64)
+            acc = []
+            for v in (x - a, a - self.aux[m], x, a, y):  # (scale, ssq) as the device
+                sc = float(np.max(np.abs(v))) if v.size else 0.0
+                acc += [sc, float(np.sum((v / sc) ** 2)) if sc > 0 else 0.0]
+            self.norm_acc[10 * m: 10 * m + 10] = torch.tensor(acc, dtype=torch.float64)
             self.aux[m], self.duals[m] = a, y
 
     def refresh_gram(self, m):
         pass
 
     def finalize(self):
-        acc = self.norm_acc.numpy().reshape(3, 5)
-        primal = tuple(float(np.sqrt(a[0])) for a in acc)
-        dual = tuple(r * float(np.sqrt(a[1])) for r, a in zip(self.rho, acc))
+        parts = self.norm_all.numpy().reshape(-1, 3, 5, 2)
+        nrm = np.zeros((3, 5))
+        for m in range(3):
+            for c in range(5):
+                sc, q = 0.0, 0.0
+                for s2, q2 in parts[:, m, c]:  # rank-order merge (finalize_kernel)
+                    if s2 == 0.0:
+                        continue
+                    if s2 > sc:
+                        sc, q = s2, q2 + q * (sc / s2) ** 2
+                    else:
+                        q += q2 * (s2 / sc) ** 2
+                nrm[m, c] = sc * np.sqrt(q)
+        primal = tuple(float(n[0]) for n in nrm)
+        dual = tuple(r * float(n[1]) for r, n in zip(self.rho, nrm))
         self.history.append((primal, dual))
         self.rho = O.adapt(self.rho, primal, dual, self.cfg)
 

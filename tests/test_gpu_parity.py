@@ -72,16 +72,18 @@ def test_mttkrp_fp32_accuracy(dims, R):
         assert rel(got, O.mttkrp(t, f, mode)) <= 2e-8
 
 
-def test_mttkrp_mode_consistency_c2_full_size():
+@pytest.mark.parametrize("engine,tol", [("cuda_core", 1e-9), ("tcgen05", 5e-9)])
+def test_mttkrp_mode_consistency_c2_full_size(engine, tol):
     """Size-independent property at BASELINE c2 size: for every column r,
-    sum_i M1[i,r] A[i,r] = sum_j M2[j,r] B[j,r] = sum_k M3[k,r] C[k,r]."""
+    sum_i M1[i,r] A[i,r] = sum_j M2[j,r] B[j,r] = sum_k M3[k,r] C[k,r].
+    (tcgen05: the i.i.d. 2^-22 KR-slice quantisation differs per mode.)"""
     w = synth.CONFIGS["c2"]
     rng = np.random.default_rng(1)
     x = rng.random(w.dims, dtype=np.float32)
     f = _factors(rng, w.dims, w.rank)
     t = P.DenseTensor(x)
-    v = [np.sum(P.mttkrp_factors(t, f, m) * f[m - 1], axis=0) for m in (1, 2, 3)]
-    assert rel(v[1], v[0]) <= 1e-9 and rel(v[2], v[0]) <= 1e-9
+    v = [np.sum(P.mttkrp_factors(t, f, m, engine=engine) * f[m - 1], axis=0) for m in (1, 2, 3)]
+    assert rel(v[1], v[0]) <= tol and rel(v[2], v[0]) <= tol
 
 
 def test_norm_and_rfe_kernel():
