@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-kernel-timing", action="store_true",
+                    help="diagnostic: no per-kernel events in the graph (no roofline)")
     return ap.parse_args()
 
 
@@ -267,7 +269,7 @@ def main():
         rows = [plan.extents[m][rank] for m in range(3)]
     st = P.init_state(w.dims, w.rank, cfg)
     prob.load_state(st.factors, st.aux, st.duals, st.rho)
-    prob.set_timing(True)
+    prob.set_timing(not args.no_kernel_timing)
     for _ in range(args.warmup):
         prob.step()
     prob.stream.synchronize()
@@ -290,7 +292,10 @@ def main():
         dist.barrier()
     t_ms = float(t_ms.item())
     done, _ = prob.check_status()
-    ktimes = prob.kernel_times()  # [inner*3][2] ms, last timed iteration
+    if args.no_kernel_timing:
+        ktimes = np.full((w.inner * 3, 2), np.nan)
+    else:
+        ktimes = prob.kernel_times()  # [inner*3][2] ms, last timed iteration
     # algorithmic bytes of one mode-n MTTKRP on this rank:
     # s_X * |slab| + 8 R (sum of companion extents + output rows)
     sx = 4 if w.dtype == "float32" else 8

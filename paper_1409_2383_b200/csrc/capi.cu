@@ -61,6 +61,11 @@ struct MttkrpOp {
   ntf::MttkrpTCLaunch tcl{};
   const ntf::TcTensor* tct = nullptr;  // fp16 split planes (tensor-core engine)
   int splits() const { return tc ? tcl.splits : cc.groups; }
+  // rows from tail_row0() on have splits_tail() partials (ragged last tile)
+  int64_t tail_row0() const {
+    return tc && tcl.splits_tail ? static_cast<int64_t>(tcl.n_full) * 128 : INT64_MAX;
+  }
+  int splits_tail() const { return tc ? tcl.splits_tail : 0; }
   size_t ws_bytes(int R) const {
     return tc ? ntf::mttkrp_tc_workspace_bytes(tcl, R) : ntf::mttkrp_cc_workspace_bytes(cc, R);
   }
@@ -169,6 +174,8 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   fp.row_offset = d.row_offset[m];
   fp.mtt = pl->mtt_ws;
   fp.splits = pl->op[m].splits();
+  fp.tail_row0 = pl->op[m].tail_row0();
+  fp.splits_tail = pl->op[m].splits_tail();
   fp.Lg = pl->ridge;
   fp.rho = d.rho;
   fp.F = d.factors[m];
@@ -263,7 +270,9 @@ int ntf_mttkrp(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64
     cudaError_t e = ntf::mttkrp_tc_bind(op.tcl, t);
     op.tct = &t;
     if (e == cudaSuccess) e = run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s);
-    if (e == cudaSuccess) e = ntf::mttkrp_reduce_launch(ws, op.splits(), M, R, out, nullptr, s);
+    if (e == cudaSuccess)
+      e = ntf::mttkrp_reduce_launch(ws, op.splits(), M, R, out, nullptr, s, op.tail_row0(),
+                                    op.splits_tail());
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     ntf::mttkrp_tc_unbind(op.tcl);
     ntf::tc_tensor_destroy(&t);

@@ -373,12 +373,14 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
 
 // Sum the split-group partials in a fixed order: out[m, r] = sum_g ws[g][m][r].
 __global__ void mttkrp_reduce_kernel(const double* __restrict__ ws, int64_t groups, int64_t n,
-                                     double* __restrict__ out, const int* stop_flag) {
+                                     double* __restrict__ out, const int* stop_flag,
+                                     int64_t tail_e0, int64_t groups_tail) {
   if (stop_flag && *stop_flag) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int64_t k = 0; k < groups; ++k) s += ws[k * n + e];
+    const int64_t ng = e >= tail_e0 ? groups_tail : groups;
+    for (int64_t k = 0; k < ng; ++k) s += ws[k * n + e];
     out[e] = s;
   }
 }
@@ -569,12 +571,15 @@ cudaError_t mttkrp_cc_launch(int mode, int x_dtype, const void* X, int64_t I, in
 }
 
 cudaError_t mttkrp_reduce_launch(const double* ws, int groups, int64_t M, int R, double* out,
-                                 const int* stop_flag, cudaStream_t stream) {
+                                 const int* stop_flag, cudaStream_t stream, int64_t tail_row0,
+                                 int groups_tail) {
   const int64_t n = M * R;
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 4 * sm_count_cached()) blocks = 4 * sm_count_cached();
   if (blocks < 1) blocks = 1;
-  mttkrp_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, groups, n, out, stop_flag);
+  const int64_t tail_e0 = tail_row0 >= M ? n : tail_row0 * R;
+  mttkrp_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, groups, n, out, stop_flag, tail_e0,
+                                                    groups_tail);
   return cudaGetLastError();
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdint>
 
 #include "common.cuh"
 
@@ -38,7 +39,10 @@ cudaError_t mttkrp_cc_launch(int mode, int x_dtype, const void* X, int64_t I, in
                              const double* A, const double* B, const double* C, int R,
                              const MttkrpCCLaunch& L, double* ws, const int* stop_flag,
                              cudaStream_t stream);
+// out[m] = sum of the partials of row m: `groups` of them for m < tail_row0,
+// `groups_tail` after (the tensor-core engine's ragged last tile)
 cudaError_t mttkrp_reduce_launch(const double* ws, int groups, int64_t M, int R, double* out,
-                                 const int* stop_flag, cudaStream_t stream);
+                                 const int* stop_flag, cudaStream_t stream,
+                                 int64_t tail_row0 = INT64_MAX, int groups_tail = 0);
 
 }  // namespace ntf

@@ -1,41 +1,46 @@
 // Dense MTTKRP on the 5th-generation tensor cores (tcgen05, sm_100a) for fp32
 // tensors.  Same contraction as mttkrp_cc.cu (reference tensors.py:254-262):
-//   out[m, n] = sum_q X(m, q) W(q, n),  W(q, n) = F_hi[o, n] * F_lo[l, n]
+//   out[m, n] = sum_o F_hi[o, n] * sum_l X(m, o, l) F_lo[l, n]
+// with (o, l) the two non-m tensor axes:
+//   mode 1: m = i, o = j, l = k   (F_hi, F_lo) = (B, C)   A tile K-major
+//   mode 2: m = j, o = i, l = k   (F_hi, F_lo) = (A, C)   A tile K-major
+//   mode 3: m = k, o = i, l = j   (F_hi, F_lo) = (A, B)   A tile MN-major (X^T)
 //
 // Numerics: exact fixed-point slicing on kind::f16 MMAs.
-//   X  = xs * (S0 + S1)          S0 integers |S0| <= 2^11, S1 in 2^-11 units,
-//                                xs = 2^(e-11) global (computed once per tensor)
-//   W  = ws(n) * (T0 + T1 + T2)  T0 integers |T0| <= 2^7, T1 in 2^-7 and T2 in
-//                                2^-14 units, ws(n) = 2^(f(n)-7) per column
-// All slices are exact fp16 values.  Per 64-wide q chunk the tensor core forms
-//   ACC0 = sum S0*T0                          (integers < 2^24: EXACT in fp32)
-//   ACC1 = sum S0*T1 + S1*T0 + S0*T2 + S1*T1  (a 2^-7-scaled correction)
-// so the dominant term carries no accumulation rounding at all (whatever the
-// tensor core's rounding mode), and the correction's rounding is ~2^-29 of the
-// result.  The epilogue folds ACC0 into a double-float accumulator (Fast2Sum)
-// and ACC1 into its low word; dropped terms (S1*T2 ~ 2^-25, slice residues
-// ~2^-23 of the column/tensor maxima) are i.i.d. per element, never a
-// structured rounding of the factors (SURVEY 8(d) precision findings).
+//   X    = xs * (S0 + S1)        S0 integers |S0| <= 2^11, S1 in 2^-11 units,
+//                                xs = 2^(e-11) global (split once per tensor)
+//   F_lo = ls(n) * (T0 + T1 + T2)  T0 integers |T0| <= 2^t, T1 in 2^-11 and T2
+//                                in 2^-22 units (fp16-exact, T2 possibly
+//                                subnormal), ls(n) = 2^(f(n)-t) per column
+// The tensor core forms, per unit of G consecutive 64-wide l blocks at one o,
+//   ACC0 = sum S0*T0                       integers < 2^24: EXACT in fp32
+//   ACC1 = sum S0*T1 + S1*T0,  ACC2 = sum S0*T2 + S1*T1   (corrections)
+// with t = 7 - log2(G) keeping |ACC0| <= 2^11 * 2^t * 64G <= 2^24.  F_lo is
+// represented to 2^-(22+t) of its column maximum (27-28 bits); the dropped
+// S1*T2 term is ~2^-33.  The epilogue multiplies the unit's accumulators by
+// F_hi[o, n] held as an fp32 pair (exact product split with FMA) and
+// accumulates in double-float (TwoSum), so F_hi enters at ~2^-48.
 //
-// Chunking.  All modes view X as 3-D (K, J, I) and walk chunks (o, l0): the
-// reduction index q = (o, l) with l in [l0, l0+64) along one tensor axis:
-//   mode 1: m = i, o = j, l = k   W = B[j] * C[k]   A tile K-major
-//   mode 2: m = j, o = i, l = k   W = A[i] * C[k]   A tile K-major
-//   mode 3: m = k, o = i, l = j   W = A[i] * B[j]   A tile MN-major (X^T)
-// TMA zero-fills the out-of-range tail of each (o, .) run, so no byte is
-// fetched twice.  The chunk's factor rows (F_lo[l0..l0+63], F_hi[o]) ride on
-// the same TMA stage as the X tiles.
+// Work: a CTA owns one 128-row m-tile and a contiguous range of units
+// (g, o) in g-major order, g = group of G l-blocks.  The W slices of a group
+// do not depend on o, so they are formed once per group (usually once per
+// CTA) and stay resident; the CTA then streams X tiles through a TMA ring and
+// the epilogue drains TMEM once per unit instead of once per 64 q.
 //
-// Pipeline (one CTA per SM, warp-specialised, mbarrier handshakes):
-//   warp 0      TMA producer: S0/S1 tiles (128B-swizzled) + factor rows
-//   warp 1      TMEM allocator + single-thread MMA issuer (tcgen05.mma)
-//   warps 2-5   KR formers: W slices of the chunk from the staged fp64 rows,
-//               written in the UMMA K-major SW128 layout
-//   warps 6-9   epilogue: tcgen05.ld of the two accumulators (double-buffered
-//               in TMEM), double-float accumulation, fp64 partial per split.
+// Roles (one CTA per SM, mbarrier handshakes, all ring indices incremental):
+//   warp 0        TMA producer: S0/S1 tiles (128B-swizzled)
+//   warp 1        TMEM allocator + single-thread MMA issuer (tcgen05.mma)
+//   warp 2        F_hi rows of the coming units -> scaled fp32 pairs (smem ring)
+//   warps 3..     epilogue, 4 warps (8 for N >= 48, two column halves per TMEM
+//                 lane quarter).  At each group start it forms the W slices
+//                 T0|T1|T2 of the group's F_lo rows (UMMA K-major SW128 layout);
+//                 per unit: tcgen05.ld, F_hi scaling, double-float
+//                 accumulation; finally the fp64 partial of the CTA.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "mttkrp_tc.cuh"
@@ -45,13 +50,12 @@ namespace ntf {
 namespace {
 
 constexpr int kTM = 128;     // MMA M (rows per tile, TMEM lanes)
-constexpr int kBK = 64;      // q per chunk (fp16: 128 B rows, one SW128 atom)
+constexpr int kBK = 64;      // l per block (fp16: 128 B rows, one SW128 atom)
 constexpr int kUK = 16;      // MMA K for kind::f16
-constexpr int kEpiWarps = 4;
-// KR-former warps: more for small N (light epilogue, registers to spare)
-__host__ __device__ constexpr int wf_warps(int NT) { return NT <= 2 ? 8 : 4; }
-// warps: 0 X-tile TMA, 1 MMA, 2 factor-row TMA, KR formers, 4 epilogue
-__host__ __device__ constexpr int tc_threads(int NT) { return (3 + wf_warps(NT) + kEpiWarps) * 32; }
+constexpr int kFMin = -990;  // exponent clamp of the column scales (2^(7+22-kFMin) finite)
+__host__ __device__ constexpr int epi_warps(int NT) { return NT >= 3 ? 8 : 4; }
+// warps: 0 X TMA, 1 MMA, 2 F_hi rows, epilogue (which also forms W)
+__host__ __device__ constexpr int tc_threads(int NT) { return (3 + epi_warps(NT)) * 32; }
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
@@ -86,6 +90,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// NTF_TC_DEBUG & 32: cycles each role spends waiting (printed per CTA)
+__device__ __forceinline__ void mbar_wait_p(uint64_t* bar, uint32_t parity, bool prof, long long& acc) {
+  if (!prof) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  acc += clock64() - t0;
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2) {
   asm volatile(
@@ -95,12 +116,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1) {
+// one lane of a converged warp (the warp's loop stays warp-uniform, so
+// descriptors and barrier addresses live in uniform registers)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -175,152 +209,154 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
          | ((static_cast<uint32_t>(kTM) >> 4) << 24);  // M >> 4
 }
 
-// accumulator sets (5N fp32 columns each) resident in TMEM: double-buffered
-// when two fit in the 512 columns, so the MMA never waits for the epilogue
-__host__ __device__ constexpr int acc_bufs(int N) { return 10 * N <= 512 ? 2 : 1; }
+// Accumulator set: 3N fp32 TMEM columns [ACC0 | ACC1 | ACC2].  As many sets
+// as fit (up to 4) so the MMA runs ahead of the epilogue.
+__host__ __device__ constexpr int acc_bufs(int N) {
+  return 512 / (3 * N) >= 4 ? 4 : 512 / (3 * N);
+}
 
 __host__ __device__ constexpr uint32_t tmem_cols(int N) {
-  return acc_bufs(N) * 5 * N <= 32    ? 32
-         : acc_bufs(N) * 5 * N <= 64  ? 64
-         : acc_bufs(N) * 5 * N <= 128 ? 128
-         : acc_bufs(N) * 5 * N <= 256 ? 256
+  return acc_bufs(N) * 3 * N <= 32    ? 32
+         : acc_bufs(N) * 3 * N <= 64  ? 64
+         : acc_bufs(N) * 3 * N <= 128 ? 128
+         : acc_bufs(N) * 3 * N <= 256 ? 256
                                       : 512;
 }
 
 struct TcParams {
   CUtensorMap tmap0;         // S0 plane, 3-D (K, J, I)
   CUtensorMap tmap1;         // S1 plane
-  CUtensorMap tmap_lo;       // F_lo rows, 2-D (R, rows), box (R, 64)
-  CUtensorMap tmap_hi;       // F_hi rows, 2-D (R, rows), box (R, 1)
   int mode, R;
   int64_t M;
-  int64_t l_extent;          // extent of the chunked axis (K or J)
-  int64_t n_chunks, chunks_per_split, chunks_per_o;
-  int n_mtiles, splits;
-  int x_stages, w_stages, f_stages;
-  int stage_bytes;           // X tiles + factor rows
+  int l_ext, n_o, n_lb, G;   // l extent, o extent, 64-wide l blocks, blocks per unit
+  int n_full, splits, splits_tail;
+  int x_stages, h_stages;
+  const double* f_hi;        // [n_o][R]
+  const unsigned char* wsl;  // [n_lb][3][N][128 B] W slices of F_lo (w_slice_kernel)
   const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
   const double* cm_lo;       // [R] max |F_lo[:, n]|
   const double* xscale;      // tensor split scale (device scalar)
   double* ws;                // [splits][M][R] partials
   const int* stop_flag;
-  int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip KR, 2 skip MMA
+  int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip W forming,
+                             // 2 skip MMA, 4 skip TMEM drain, 16 skip X TMA
+  uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
+  uint32_t ub_tail[kTcMaxSplits + 1];  // ... of the ragged last tile
 };
 
-__device__ __forceinline__ void fast_two_sum(float& hi, float& lo, float a) {
-  const float s = hi + a;
-  const float err = a - (s - hi);
-  hi = s;
-  lo += err;
-}
-
-// W slices for one (n, 8-q octet): 3 x 16 bytes at the swizzled positions.
-// t (|t| <= 128) is converted to fp32 once: its rounding error (<= 2^-17) is
-// far below the T2 quantum (2^-14), so slicing in fp32 loses nothing.
-__device__ __forceinline__ void emit_w_octet(unsigned char* t0, unsigned char* t1, unsigned char* t2,
-                                             int n, int oct, const double (&w)[8]) {
-  __align__(16) __half2 h0[4], h1[4], h2[4];
-  // round-to-nearest-even via the 1.5*2^23 magic constant (two FADDs, exact
-  // for |x| < 2^22) instead of the slower FRND
-  constexpr float kMagic = 12582912.0f;
-#pragma unroll
-  for (int u = 0; u < 8; u += 2) {
-    float a0[2], a1[2], a2[2];
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const float tf = static_cast<float>(w[u + v]);
-      a0[v] = __fsub_rn(__fadd_rn(tf, kMagic), kMagic);     // integer, |a0| <= 128
-      const float r1 = (tf - a0[v]) * 128.0f;                // exact, |r1| <= 64
-      a1[v] = __fsub_rn(__fadd_rn(r1, kMagic), kMagic);
-      const float r2 = (r1 - a1[v]) * 128.0f;
-      a2[v] = __fsub_rn(__fadd_rn(r2, kMagic), kMagic);
+// ring slot + phase, advanced without divisions
+struct Ring {
+  int idx = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1u;
     }
-    h0[u / 2] = __floats2half2_rn(a0[0], a0[1]);                          // exact
-    h1[u / 2] = __floats2half2_rn(a1[0] * 0.0078125f, a1[1] * 0.0078125f);  // 2^-7 units
-    h2[u / 2] = __floats2half2_rn(a2[0] * 6.103515625e-05f, a2[1] * 6.103515625e-05f);  // 2^-14
   }
-  const int off = n * 128 + ((oct ^ (n & 7)) << 4);
-  *reinterpret_cast<uint4*>(t0 + off) = *reinterpret_cast<const uint4*>(h0);
-  *reinterpret_cast<uint4*>(t1 + off) = *reinterpret_cast<const uint4*>(h1);
-  *reinterpret_cast<uint4*>(t2 + off) = *reinterpret_cast<const uint4*>(h2);
+};
+
+// unit (g, o) walk in g-major order
+struct UnitIt {
+  int g, o;
+  __device__ __forceinline__ void next(int n_o) {
+    if (++o == n_o) {
+      o = 0;
+      ++g;
+    }
+  }
+};
+
+__device__ __forceinline__ void two_sum(float& hi, float& lo, float p) {
+  const float s = hi + p;
+  const float bp = s - hi;
+  lo += (hi - (s - bp)) + (p - bp);
+  hi = s;
 }
 
 template <int NT>  // N / 16
 __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
-  constexpr int kWfWarps = wf_warps(NT);
   constexpr int N = NT * 16;
+  constexpr int kEpi = epi_warps(NT);
+  constexpr int NC = N * 4 / kEpi;         // columns per epilogue thread
   constexpr int kAccBufs = acc_bufs(N);
+  constexpr int kXTile = kTM * kBK * 2;    // 16 KB per plane
+  constexpr int kWlb = 3 * N * kBK * 2;    // T0|T1|T2 of one l block
+  constexpr int kFirstEpi = 3;
+  const uint64_t g_entry = gtimer();
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // carve: [X stages: S0 16KB | S1 16KB]  (released by the MMA)
-  //        [factor stages: lo rows 64*R*8 | hi row R*8]  (released by KR formers)
-  //        [W stages: T0 | T1 | T2 (N*128 each)] [barriers]
-  // 1 KB alignment by offset (keeps the pointer in the shared address space,
-  // so the compiler emits LDS/STS instead of generic loads/stores)
+  // 1 KB alignment by offset (keeps the pointer in the shared address space)
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr int kXTile = kTM * kBK * 2;  // 16 KB
-  constexpr int kWTile = N * kBK * 2;    // N * 128 B
-  const int SX = p.x_stages, SW = p.w_stages, SF = p.f_stages;
+  const int SX = p.x_stages, SH = p.h_stages, G = p.G;
   const int R = p.R;
-  const int SB = p.stage_bytes;          // factor stage bytes (1 KB aligned)
   unsigned char* xbase = base;
-  unsigned char* fbase = xbase + SX * 2 * kXTile;
-  unsigned char* wbase = fbase + SF * SB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + SW * 3 * kWTile);
-  uint64_t* x_full = bars;
+  unsigned char* wbase = xbase + SX * 2 * kXTile;
+  float2* hbase = reinterpret_cast<float2*>(wbase + G * kWlb);  // [SH][N]
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(hbase + SH * N);
   uint64_t* x_empty = x_full + SX;
-  uint64_t* f_full = x_empty + SX;
-  uint64_t* f_empty = f_full + SF;
-  uint64_t* w_full = f_empty + SF;
-  uint64_t* w_empty = w_full + SW;
-  uint64_t* acc_full = w_empty + SW;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  // per-column W scales: wsc[n] = 2^(7 - f(n)) with max|F_hi[:,n]| max|F_lo[:,n]|
-  // <= 2^f(n), so |t| = |W| 2^(7-f) <= 128; wsc[N + n] = xscale * 2^(f(n) - 7)
-  double* wsc = reinterpret_cast<double*>(acc_empty + 4);
-  if (threadIdx.x < N) {
-    const int n = threadIdx.x;
-    const double prod = n < p.R ? p.cm_hi[n] * p.cm_lo[n] : 0.0;
-    int f = 0;
-    if (prod > 0.0) frexp(prod, &f);  // prod < 2^f
-    // a column that decayed to ~1e-300 (large penalties shrink factor columns
-    // geometrically) must not overflow the scale: clamp (represented as zero)
-    if (f < -1000) f = -1000;
-    wsc[n] = ldexp(1.0, 7 - f);
-    wsc[N + n] = *p.xscale * ldexp(1.0, f - 7);
-  }
-
+  uint64_t* h_full = x_empty + SX;
+  uint64_t* h_empty = h_full + SH;
+  uint64_t* w_full = h_empty + SH;
+  uint64_t* w_empty = w_full + 1;
+  uint64_t* acc_full = w_empty + 1;
+  uint64_t* acc_empty = acc_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 4);
+  // per-column scales: [0,N) F_lo -> T scale 2^(t-f), [N,2N) F_hi -> unit
+  // range 2^-e, [2N,3N) output xs * 2^(f-t) * 2^e
+  double* wsc = reinterpret_cast<double*>(acc_empty + 6);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  constexpr int kWfFirst = 3;
-  constexpr int kEpiFirst = 3 + kWfWarps;
-  constexpr int kWfThreads = kWfWarps * 32;
+  if (threadIdx.x < N) {
+    const int n = threadIdx.x;
+    const int t = G >= 4 ? 5 : (G >= 2 ? 6 : 7);
+    int f = 0, e = 0;
+    const double cl = n < R ? p.cm_lo[n] : 0.0, ch = n < R ? p.cm_hi[n] : 0.0;
+    if (cl > 0.0) frexp(cl, &f);  // cl < 2^f
+    if (ch > 0.0) frexp(ch, &e);
+    // columns decayed to ~1e-300 (large penalties shrink factor columns
+    // geometrically) must not overflow the scales (2^(t+22-f) in the slice
+    // kernel): clamp, identically there (kFMin)
+    f = max(f, kFMin);
+    e = max(e, kFMin);
+    wsc[n] = ldexp(1.0, t - f);
+    wsc[N + n] = ldexp(1.0, -e);
+    wsc[2 * N + n] = *p.xscale * ldexp(1.0, f - t + e);
+  }
 
-  const int tile = blockIdx.x % p.n_mtiles;
-  const int split = blockIdx.x / p.n_mtiles;
+  // this CTA's tile and unit range
+  int tile, split;
+  const uint32_t* ub;
+  if (static_cast<int>(blockIdx.x) < p.n_full * p.splits) {
+    tile = blockIdx.x % p.n_full;
+    split = blockIdx.x / p.n_full;
+    ub = p.ub_full;
+  } else {
+    tile = p.n_full;
+    split = blockIdx.x - p.n_full * p.splits;
+    ub = p.ub_tail;
+  }
   const int64_t m0 = static_cast<int64_t>(tile) * kTM;
-  const int64_t c_begin = static_cast<int64_t>(split) * p.chunks_per_split;
-  int64_t c_end = c_begin + p.chunks_per_split;
-  if (c_end > p.n_chunks) c_end = p.n_chunks;
-  const int n_iter = c_begin < c_end ? static_cast<int>(c_end - c_begin) : 0;
+  const int u_begin = static_cast<int>(ub[split]);
+  const int u_end = static_cast<int>(ub[split + 1]);
+  const int n_o = p.n_o;
+  const UnitIt u0{u_begin / n_o, u_begin - (u_begin / n_o) * n_o};
+  auto lbs_of = [&](int g) { return min(G, p.n_lb - g * G); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SX; ++s) {
       mbar_init(&x_full[s], 1);
       mbar_init(&x_empty[s], 1);  // MMA commit
     }
-    for (int s = 0; s < SF; ++s) {
-      mbar_init(&f_full[s], 1);
-      mbar_init(&f_empty[s], kWfThreads);  // KR formers consumed the rows
+    for (int s = 0; s < SH; ++s) {
+      mbar_init(&h_full[s], 1);
+      mbar_init(&h_empty[s], kEpi);
     }
-    for (int s = 0; s < SW; ++s) {
-      mbar_init(&w_full[s], kWfThreads);
-      mbar_init(&w_empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
+    mbar_init(w_full, 1);
+    mbar_init(w_empty, 1);
+    for (int s = 0; s < kAccBufs; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], kEpiWarps * 32);
+      mbar_init(&acc_empty[s], kEpi);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -334,176 +370,259 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const bool prof = (p.debug & 32) != 0;
+  const uint64_t g_ready = prof ? gtimer() : 0;
+  long long wt[3] = {0, 0, 0};
+  const long long t_start = prof ? clock64() : 0;
 
-  if (warp == 2) {
-    // ---------------------------- factor-row producer -------------------------
-    if (lane == 0) {
-      // factor rows of each chunk: F_lo[l0 .. l0+63] and F_hi[o]
-      const uint32_t fac_bytes = static_cast<uint32_t>((kBK + 1) * R * 8);
-      for (int it = 0; it < n_iter; ++it) {
-        const int fs = it % SF;
-        mbar_wait(&f_empty[fs], ((it / SF) & 1) ^ 1);
-        unsigned char* dlo = fbase + fs * SB;
-        unsigned char* dhi = dlo + kBK * R * 8;
-        mbar_arrive_expect_tx(&f_full[fs], fac_bytes);
-        const int64_t c = c_begin + it;
-        const int o = static_cast<int>(c / p.chunks_per_o);
-        const int l0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
-        tma_load_2d(dlo, &p.tmap_lo, &f_full[fs], 0, l0);
-        tma_load_2d(dhi, &p.tmap_hi, &f_full[fs], 0, o);
-      }
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
     // ------------------------------ X-tile producer ---------------------------
-    if (lane == 0) {
-      for (int it = 0; it < n_iter; ++it) {
-        const int s = it % SX;
-        mbar_wait(&x_empty[s], ((it / SX) & 1) ^ 1);
-        unsigned char* d0 = xbase + s * 2 * kXTile;
+    // warp-uniform loop; one elected lane issues
+    Ring xr;
+    UnitIt ui = u0;
+    const int mm = static_cast<int>(m0);
+    for (int u = u_begin; u < u_end; ++u) {
+      const int nl = lbs_of(ui.g);
+      for (int j = 0; j < nl; ++j) {
+        mbar_wait_p(&x_empty[xr.idx], xr.phase ^ 1u, prof, wt[0]);
+        uint64_t* bar = &x_full[xr.idx];
+        unsigned char* d0 = xbase + xr.idx * 2 * kXTile;
         unsigned char* d1 = d0 + kXTile;
-        mbar_arrive_expect_tx(&x_full[s], 2 * kXTile);
-        const int64_t c = c_begin + it;
-        const int o = static_cast<int>(c / p.chunks_per_o);
-        const int l0 = static_cast<int>((c - static_cast<int64_t>(o) * p.chunks_per_o) * kBK);
-        const int mm = static_cast<int>(m0);
-        if (p.mode == 1) {
-          tma_load_3d(d0, &p.tmap0, &x_full[s], l0, o, mm);
-          tma_load_3d(d1, &p.tmap1, &x_full[s], l0, o, mm);
-        } else if (p.mode == 2) {
-          tma_load_3d(d0, &p.tmap0, &x_full[s], l0, mm, o);
-          tma_load_3d(d1, &p.tmap1, &x_full[s], l0, mm, o);
-        } else {  // two 64-m boxes per plane
-          tma_load_3d(d0, &p.tmap0, &x_full[s], mm, l0, o);
-          tma_load_3d(d0 + kXTile / 2, &p.tmap0, &x_full[s], mm + 64, l0, o);
-          tma_load_3d(d1, &p.tmap1, &x_full[s], mm, l0, o);
-          tma_load_3d(d1 + kXTile / 2, &p.tmap1, &x_full[s], mm + 64, l0, o);
+        const int l0 = (ui.g * G + j) * kBK;
+        if (elect_one()) {
+          if (p.debug & 16) {
+            mbar_arrive(bar);
+          } else {
+            mbar_arrive_expect_tx(bar, 2 * kXTile);
+            if (p.mode == 1) {
+              tma_load_3d(d0, &p.tmap0, bar, l0, ui.o, mm);
+              tma_load_3d(d1, &p.tmap1, bar, l0, ui.o, mm);
+            } else if (p.mode == 2) {
+              tma_load_3d(d0, &p.tmap0, bar, l0, mm, ui.o);
+              tma_load_3d(d1, &p.tmap1, bar, l0, mm, ui.o);
+            } else {  // two 64-m boxes per plane
+              tma_load_3d(d0, &p.tmap0, bar, mm, l0, ui.o);
+              tma_load_3d(d0 + kXTile / 2, &p.tmap0, bar, mm + 64, l0, ui.o);
+              tma_load_3d(d1, &p.tmap1, bar, mm, l0, ui.o);
+              tma_load_3d(d1 + kXTile / 2, &p.tmap1, bar, mm + 64, l0, ui.o);
+            }
+          }
         }
+        __syncwarp();
+        xr.next(SX);
       }
+      ui.next(n_o);
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
-    if (lane == 0) {
-      // Two wide MMAs per K step, each reading its A tile once: the W slices
-      // T0|T1|T2 are consecutive N-row blocks of one K-major B operand.
-      //   cols [0, 3N):  S0 * [T0 | T1 | T2]     cols [3N, 5N): S1 * [T0 | T1]
-      const bool mn = p.mode == 3;
-      const uint32_t idesc3 = make_idesc(3 * N, mn);
-      const uint32_t idesc2 = make_idesc(2 * N, mn);
-      for (int it = 0; it < n_iter; ++it) {
-        const int s = it % SX, sw = it % SW, ab = it % kAccBufs;
-        mbar_wait(&x_full[s], (it / SX) & 1);
-        mbar_wait(&w_full[sw], (it / SW) & 1);
-        mbar_wait(&acc_empty[ab], ((it / kAccBufs) & 1) ^ 1);
+    // Two wide MMAs per K step, each reading its A tile once: the W slices
+    // T0|T1|T2 are consecutive N-row blocks of one K-major B operand.
+    //   cols [0, 3N) (=|+=) S0 * [T0 | T1 | T2]     cols [N, 3N) += S1 * [T0 | T1]
+    // Warp-uniform loop; one elected lane issues the MMAs and commits.
+    const bool mn = p.mode == 3;
+    const uint32_t idesc3 = make_idesc(3 * N, mn);
+    const uint32_t idesc2 = make_idesc(2 * N, mn);
+    // descriptors of stage 0 / l-block 0; stages are 32 KB apart, l blocks
+    // kWlb apart (both multiples of 16 B: added to the address field)
+    const uint64_t da_base = mn ? smem_desc(xbase, kXTile / 2, 1024) : smem_desc(xbase, 16, 1024);
+    const uint64_t db_base = smem_desc(wbase, 16, 1024);
+    const uint32_t a_kstep = mn ? 2048 >> 4 : 32 >> 4;  // descriptor units (16 B)
+    Ring xr, ar;
+    UnitIt ui = u0;
+    int cur_g = -1;
+    uint32_t wphase = 0;
+    for (int u = u_begin; u < u_end; ++u) {
+      if (ui.g != cur_g) {  // new group: its W slices must be formed
+        if (cur_g >= 0) {
+          if (elect_one()) tc_commit(w_empty);
+          __syncwarp();
+        }
+        mbar_wait_p(w_full, wphase, prof, wt[2]);
+        wphase ^= 1u;
+        cur_g = ui.g;
+      }
+      mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, prof, wt[1]);
+      tc_fence_after();
+      const uint32_t d0 = tmem + ar.idx * 3 * N;
+      const uint32_t d1 = d0 + N;
+      const int nl = lbs_of(ui.g);
+      for (int j = 0; j < nl; ++j) {
+        mbar_wait_p(&x_full[xr.idx], xr.phase, prof, wt[0]);
         tc_fence_after();
-        const unsigned char* a0 = xbase + s * 2 * kXTile;
-        const unsigned char* a1 = a0 + kXTile;
-        const unsigned char* b0 = wbase + sw * 3 * kWTile;
-        const uint32_t d0 = tmem + ab * 5 * N;
-        const uint32_t d1 = d0 + 3 * N;
+        const uint64_t da0 = da_base + static_cast<uint64_t>((xr.idx * 2 * kXTile) >> 4);
+        const uint64_t da1 = da0 + static_cast<uint64_t>(kXTile >> 4);
+        const uint64_t db = db_base + static_cast<uint64_t>((j * kWlb) >> 4);
+        if (elect_one()) {
+          if (!(p.debug & 2)) {
 #pragma unroll
-        for (int kk = 0; kk < ((p.debug & 2) && it >= 2 ? 0 : kBK / kUK); ++kk) {
-          uint64_t da0, da1;
-          if (mn) {  // A = X^T: MN-major, atoms of 64 m (8 KB apart), 8 q-rows per 1 KB
-            da0 = smem_desc(a0 + kk * 2048, kXTile / 2, 1024);
-            da1 = smem_desc(a1 + kk * 2048, kXTile / 2, 1024);
-          } else {   // K-major: 128 B rows, 8-row groups 1 KB apart, +32 B per K step
-            da0 = smem_desc(a0 + kk * 32, 16, 1024);
-            da1 = smem_desc(a1 + kk * 32, 16, 1024);
+            for (int kk = 0; kk < kBK / kUK; ++kk) {
+              tc_mma_f16(d0, da0 + kk * a_kstep, db + kk * (32 >> 4), idesc3, (j | kk) ? 1u : 0u);
+              tc_mma_f16(d1, da1 + kk * a_kstep, db + kk * (32 >> 4), idesc2, 1u);
+            }
           }
-          const uint64_t db = smem_desc(b0 + kk * 32, 16, 1024);
-          const uint32_t acc = kk > 0 ? 1u : 0u;
-          tc_mma_f16(d0, da0, db, idesc3, acc);   // S0*T0 (exact), S0*T1, S0*T2
-          tc_mma_f16(d1, da1, db, idesc2, acc);   // S1*T0, S1*T1
+          if (p.debug & 64) mbar_arrive(&x_empty[xr.idx]);  // profiling: no tensor-pipe commit
+          else tc_commit(&x_empty[xr.idx]);
         }
-        tc_commit(&x_empty[s]);
-        tc_commit(&w_empty[sw]);
-        tc_commit(&acc_full[ab]);
+        __syncwarp();
+        xr.next(SX);
       }
+      if (elect_one()) {
+        if (p.debug & 64) mbar_arrive(&acc_full[ar.idx]);
+        else tc_commit(&acc_full[ar.idx]);
+      }
+      __syncwarp();
+      ar.next(kAccBufs);
+      ui.next(n_o);
     }
-  } else if (warp < kEpiFirst) {
-    // ------------------------------ KR formers --------------------------------
-    // thread t owns column n = t % N (lanes along n: conflict-free row reads)
-    // and octets t / N, t / N + kWfThreads / N, ...
-    const int t = threadIdx.x - kWfFirst * 32;
-    const int n = t % N;
-    const int oct0 = t / N;
-    constexpr int kOctStep = kWfThreads / N > 0 ? kWfThreads / N : 1;
-    const bool active = t < N * (kBK / 8) && (kWfThreads >= N || true);
-    const double sc = n < R ? wsc[n] : 0.0;
-    for (int it = 0; it < n_iter; ++it) {
-      const int fs = it % SF, sw = it % SW;
-      mbar_wait(&f_full[fs], (it / SF) & 1);
-      mbar_wait(&w_empty[sw], ((it / SW) & 1) ^ 1);
-      const unsigned char* srow = fbase + fs * SB;
-      const double* lo_s = reinterpret_cast<const double*>(srow);
-      const double* hi_s = lo_s + kBK * R;
-      unsigned char* t0 = wbase + sw * 3 * kWTile;
-      unsigned char* t1 = t0 + kWTile;
-      unsigned char* t2 = t1 + kWTile;
-      if (active && !((p.debug & 1) && it >= SW)) {
-        const double hs = n < R ? hi_s[n] * sc : 0.0;
-        for (int oct = oct0; oct < kBK / 8; oct += kOctStep) {
-          double w[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) w[u] = n < R ? hs * lo_s[(oct * 8 + u) * R + n] : 0.0;
-          emit_w_octet(t0, t1, t2, n, oct, w);
+  } else if (warp == 2) {
+    // ---------- W slices of each group (bulk copy) + F_hi rows -> fp32 pairs ---------
+    Ring hr;
+    UnitIt ui = u0;
+    int seg = 0;
+    for (int u = u_begin; u < u_end; ++u) {
+      if (u == u_begin || ui.o == 0) {  // group start: the previous group's MMAs are done
+        if (seg > 0) mbar_wait_p(w_empty, (seg - 1) & 1, prof, wt[2]);
+        if (elect_one()) {
+          const uint32_t bytes = static_cast<uint32_t>(lbs_of(ui.g) * kWlb);
+          mbar_arrive_expect_tx(w_full, bytes);
+          bulk_load(wbase, p.wsl + static_cast<int64_t>(ui.g) * G * kWlb, bytes, w_full);
         }
+        __syncwarp();
+        ++seg;
       }
-      fence_proxy_async();
-      mbar_arrive(&w_full[sw]);
-      mbar_arrive(&f_empty[fs]);  // factor rows consumed
+      mbar_wait_p(&h_empty[hr.idx], hr.phase ^ 1u, prof, wt[0]);
+      float2* hs = hbase + hr.idx * N;
+      for (int n = lane; n < N; n += 32) {
+        const double h = n < R ? p.f_hi[static_cast<int64_t>(ui.o) * R + n] * wsc[N + n] : 0.0;
+        const float hx = static_cast<float>(h);
+        hs[n] = make_float2(hx, static_cast<float>(h - static_cast<double>(hx)));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h_full[hr.idx]);
+      hr.next(SH);
+      ui.next(n_o);
     }
   } else {
     // ------------------------------ epilogue ----------------------------------
-    const int q4 = warp & 3;          // TMEM lane quarter of this warp
-    const int row = q4 * 32 + lane;   // tile row == TMEM lane
-    float hi[N], lo[N];
+    const int e = warp - kFirstEpi;
+    const int q4 = warp & 3;            // TMEM lane quarter of this warp
+    const int c0 = (e >> 2) * NC;       // this warp's column range
+    const int row = q4 * 32 + lane;     // tile row == TMEM lane
+    float hi[NC], lo[NC];
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
+    for (int j = 0; j < NC; ++j) {
       hi[j] = 0.f;
       lo[j] = 0.f;
     }
-    for (int it = 0; it < n_iter; ++it) {
-      const int ab = it % kAccBufs;
-      mbar_wait(&acc_full[ab], (it / kAccBufs) & 1);
+    Ring ar, hr;
+    for (int u = u_begin; u < u_end; ++u) {
+      mbar_wait_p(&acc_full[ar.idx], ar.phase, prof, wt[0]);
+      mbar_wait_p(&h_full[hr.idx], hr.phase, prof, wt[1]);
       tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ab * 5 * N;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * 3 * N + c0;
+      const float2* hs = hbase + hr.idx * N + c0;
+      if (!(p.debug & 4)) {
 #pragma unroll
-      for (int j = 0; j < ((p.debug & 4) && it >= 2 ? 0 : NT); ++j) {
-        float a0[16], a1[16], a2[16];
-        tmem_ld16(taddr + j * 16, a0);           // S0*T0 (exact integers)
-        tmem_ld16(taddr + N + j * 16, a1);       // S0*T1
-        tmem_ld16(taddr + 2 * N + j * 16, a2);   // S0*T2
-        tmem_wait_ld();
+        for (int j = 0; j < NC / 16; ++j) {
+          float a0[16], a1[16], a2[16];
+          tmem_ld16(taddr + j * 16, a0);           // ACC0: S0*T0 (exact integers)
+          tmem_ld16(taddr + N + j * 16, a1);       // ACC1: S0*T1 + S1*T0
+          tmem_ld16(taddr + 2 * N + j * 16, a2);   // ACC2: S0*T2 + S1*T1
+          tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          fast_two_sum(hi[j * 16 + u], lo[j * 16 + u], a0[u]);
-          a1[u] += a2[u];
+          for (int v = 0; v < 16; ++v) {
+            const float2 h = hs[j * 16 + v];
+            const float a = a0[v];
+            const float pr = a * h.x;
+            const float er = fmaf(a, h.x, -pr);    // a*h.x = pr + er exactly
+            const float cr = fmaf(a1[v] + a2[v], h.x, fmaf(a, h.y, er));
+            two_sum(hi[j * 16 + v], lo[j * 16 + v], pr);
+            lo[j * 16 + v] += cr;
+          }
         }
-        tmem_ld16(taddr + 3 * N + j * 16, a0);   // S1*T0
-        tmem_ld16(taddr + 4 * N + j * 16, a2);   // S1*T1
-        tmem_wait_ld();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) lo[j * 16 + u] += (a1[u] + a0[u]) + a2[u];
       }
       tc_fence_before();
-      mbar_arrive(&acc_empty[ab]);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&acc_empty[ar.idx]);
+        mbar_arrive(&h_empty[hr.idx]);
+      }
+      ar.next(kAccBufs);
+      hr.next(SH);
     }
-    // fp64 partial of this split: out = (hi + lo) * xscale * ws(n)
+    // fp64 partial of this CTA: out = (hi + lo) * xs * 2^(f-t) * 2^e
     const int64_t gm = m0 + row;
     if (gm < p.M) {
       double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * R;
 #pragma unroll
-      for (int j = 0; j < N; ++j)
-        if (j < R) out[j] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * wsc[N + j];
+      for (int j = 0; j < NC; ++j) {
+        const int n = c0 + j;
+        if (n < R)
+          out[n] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * wsc[2 * N + n];
+      }
     }
   }
+  if (prof && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && warp <= 3)
+    printf("tc cta %d warp %d units %d loop %lld wait %lld %lld %lld gt %llu %llu %llu\n", blockIdx.x,
+           warp, u_end - u_begin, clock64() - t_start, wt[0], wt[1], wt[2],
+           (unsigned long long)g_entry, (unsigned long long)(g_ready - g_entry),
+           (unsigned long long)(gtimer() - g_entry));
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "r"(tmem_cols(N)));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// W slices of F_lo for every 64-row l block, in the UMMA K-major SW128 layout
+// the MTTKRP CTAs bulk-copy into shared memory:
+//   wsl[lb][s][n][128 B],  element l of row n at ((l/8) ^ (n&7))*16 + (l%8)*2
+//   v = F_lo[l, n] * 2^(t - f(n)) = T0 + T1 + T2 (+ <= 2^-23 rounding),
+//   T0 integer (|T0| <= 2^t), T1 in 2^-11 units, T2 in 2^-22 units (fp16
+//   exact, T2 possibly subnormal).  One thread per (l block, n, octet).
+// ----------------------------------------------------------------------------
+__global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int n_lb,
+                               const double* __restrict__ cm, int t, unsigned char* __restrict__ wsl,
+                               const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
+  const int total = n_lb * N * (kBK / 8);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int n = e % N;
+    const int oc = e / N;
+    const int lb = oc / (kBK / 8), oct = oc % (kBK / 8);
+    double sc = 0.0;
+    if (n < R) {
+      int f = 0;
+      if (cm[n] > 0.0) frexp(cm[n], &f);
+      sc = ldexp(1.0, t + 22 - max(f, kFMin));  // v in 2^-22 units of the T0 scale
+    }
+    double x[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {  // all loads first (independent, in flight together)
+      const int l = lb * kBK + oct * 8 + v;
+      x[v] = (n < R && l < l_ext) ? F[static_cast<int64_t>(l) * R + n] : 0.0;
+    }
+    __align__(16) __half h0[8], h1[8], h2[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      // one rounding to the 2^-22 quantum, then exact integer digit split
+      const long long q = __double2ll_rn(x[v] * sc);      // |q| <= 2^(t+22)
+      const long long b0 = (q + (1ll << 21)) >> 22;        // |b0| <= 2^t
+      const long long r = q - (b0 << 22);                  // [-2^21, 2^21)
+      const long long b1 = (r + (1ll << 10)) >> 11;        // [-1024, 1024]
+      const long long b2 = r - (b1 << 11);                 // [-1024, 1024)
+      h0[v] = __float2half_rn(static_cast<float>(b0));
+      h1[v] = __float2half_rn(static_cast<float>(b1) * 4.8828125e-04f);         // 2^-11 units
+      h2[v] = __float2half_rn(static_cast<float>(b2) * 2.384185791015625e-07f);  // 2^-22 units
+    }
+    unsigned char* wb = wsl + static_cast<int64_t>(lb) * 3 * N * 128;
+    const int off = n * 128 + ((oct ^ (n & 7)) << 4);
+    *reinterpret_cast<uint4*>(wb + off) = *reinterpret_cast<const uint4*>(h0);
+    *reinterpret_cast<uint4*>(wb + N * 128 + off) = *reinterpret_cast<const uint4*>(h1);
+    *reinterpret_cast<uint4*>(wb + 2 * N * 128 + off) = *reinterpret_cast<const uint4*>(h2);
   }
 }
 
@@ -576,26 +695,11 @@ int sm_count_tc() {
   return n;
 }
 
-// fp64 factor rows [rows][R] as a 2-D tensor map with box (R, box_rows)
-cudaError_t encode_factor_map(CUtensorMap* map, const double* F, int64_t rows, int R,
-                              int box_rows) {
-  auto enc = get_encoder();
-  if (!enc) return cudaErrorNotSupported;
-  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(R), static_cast<cuuint64_t>(rows)};
-  cuuint64_t gstr[1] = {static_cast<cuuint64_t>(R) * 8};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(R), static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(F), gdim, gstr, box,
-                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
 template <int NT>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
   auto kern = mttkrp_tc_kernel<NT>;
   if (prep) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
-  kern<<<L.n_mtiles * L.splits, L.threads, L.smem_bytes, stream>>>(p);
+  kern<<<L.n_full * L.splits + L.splits_tail, L.threads, L.smem_bytes, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -609,14 +713,29 @@ cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
   }
 }
 
+// Split units [0, n_g * n_o) (g-major, unit (g, o) costs lbs(g) l blocks)
+// into `parts` contiguous ranges of about equal cost.
+void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
+  const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
+  auto lbs = [&](int g) { return std::min(L.G, L.n_lb - g * L.G); };
+  const double total = static_cast<double>(L.n_o) * L.n_lb;
+  ub[0] = 0;
+  int k = 1;
+  double acc = 0.0;
+  for (int64_t u = 0; u < units && k < parts; ++u) {
+    acc += lbs(static_cast<int>(u / L.n_o));
+    while (k < parts && acc >= total * k / parts) ub[k++] = static_cast<uint32_t>(u + 1);
+  }
+  while (k <= parts) ub[k++] = static_cast<uint32_t>(units);
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------------------
 // host API
 // ----------------------------------------------------------------------------
 bool mttkrp_tc_supported(int x_dtype, int R) {
-  // even R: the fp64 factor rows are TMA boxes of R*8 bytes (multiple of 16)
-  return x_dtype == NTF_F32 && R >= 2 && R <= 64 && R % 2 == 0;
+  return x_dtype == NTF_F32 && R >= 1 && R <= 64;
 }
 
 bool mttkrp_tc_auto(int x_dtype, int R) {
@@ -630,10 +749,12 @@ bool mttkrp_tc_auto(int x_dtype, int R) {
 
 bool mttkrp_tc_shape_ok(int mode, int64_t I, int64_t J, int64_t K) {
   // TMA global strides are multiples of 16 B (K % 8 == 0 for the fp16 planes);
-  // coordinates are int32.
+  // coordinates are int32; unit ranges are 32-bit.
   (void)mode;
   if (K % 8 != 0) return false;
   if (I >= (1 << 30) || J >= (1 << 30) || K >= (1 << 30)) return false;
+  const int64_t l_ext = mode == 3 ? J : K, o_ext = mode == 1 ? J : I;
+  if (((l_ext + kBK - 1) / kBK) * o_ext >= (int64_t(1) << 31)) return false;
   return true;
 }
 
@@ -646,47 +767,68 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.M = mode == 1 ? I : (mode == 2 ? J : K);
   L.Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
   L.n_mtiles = static_cast<int>((L.M + kTM - 1) / kTM);
-  const int64_t l_ext = mode == 3 ? J : K;
-  const int64_t o_ext = mode == 1 ? J : I;
-  L.chunks_per_o = (l_ext + kBK - 1) / kBK;
-  L.n_chunks = o_ext * L.chunks_per_o;
-  L.n_wf_warps = wf_warps(L.N / 16);
+  L.l_ext = static_cast<int>(mode == 3 ? J : K);
+  L.n_o = static_cast<int>(mode == 1 ? J : I);
+  L.n_lb = (L.l_ext + kBK - 1) / kBK;
   L.threads = tc_threads(L.N / 16);
-  // X ring as deep as shared memory allows (bytes in flight hide HBM latency);
-  // the factor-row and KR rings only need to stay a few chunks ahead.
+  // Shared memory: X ring (32 KB per l block) + resident W slices of a group
+  // (G blocks x 3N x 128 B) + F_hi pair ring.  Largest G (fewest epilogue
+  // drains) that still leaves a 4-deep X ring; then as deep an X ring as fits.
   const int xs = 2 * kTM * kBK * 2;
-  L.stage_bytes = ((kBK + 1) * R * 8 + 1023) & ~1023;  // factor stage
-  const int wsz = 3 * L.N * kBK * 2;
-  L.x_stages = 4;
-  L.f_stages = 3;
-  L.w_stages = 3;
-  if (const char* e2 = getenv("NTF_TC_WSTAGES")) L.w_stages = atoi(e2);
-  auto total = [&]() {
-    // + barriers, TMEM slot and the 2N per-column scales
-    return 1024 + L.x_stages * xs + L.f_stages * L.stage_bytes + L.w_stages * wsz + 512 + 16 * L.N;
+  L.h_stages = 8;
+  auto total = [&](int G, int SX) {
+    return 1024 + SX * xs + G * 3 * L.N * kBK * 2 + L.h_stages * L.N * 8 +
+           (2 * SX + 2 * L.h_stages + 12) * 8 + 16 + 3 * L.N * 8;
   };
-  const char* env = getenv("NTF_TC_XSTAGES");
-  if (env) L.x_stages = atoi(env);
-  while (total() > 227 * 1024 && L.x_stages > 2) --L.x_stages;
-  while (total() > 227 * 1024 && L.f_stages > 2) --L.f_stages;
-  L.smem_bytes = total();
+  const int limit = 227 * 1024;
+  L.G = 1;
+  for (int G : {4, 2, 1})
+    if (total(G, 4) <= limit) {
+      L.G = G;
+      break;
+    }
+  if (const char* e = getenv("NTF_TC_G")) L.G = atoi(e);
+  L.G = std::max(1, std::min(L.G, L.n_lb));
+  if (L.G == 3) L.G = 2;
+  L.x_stages = 6;
+  if (const char* e = getenv("NTF_TC_XSTAGES")) L.x_stages = atoi(e);
+  while (total(L.G, L.x_stages) > limit && L.x_stages > 2) --L.x_stages;
+  L.smem_bytes = total(L.G, L.x_stages);
   L.tmem_cols = static_cast<int>(tmem_cols(L.N));
-  // one CTA per SM; split the chunk range so that the grid is one wave
-  const int sms = sm_count_tc();
-  // one SM is left free so the mode's ridge Cholesky (side stream) runs
-  // concurrently instead of queueing behind the MTTKRP
-  int splits = (sms - 1) / L.n_mtiles;
-  if (splits < 1) splits = 1;
-  if (splits > L.n_chunks) splits = static_cast<int>(L.n_chunks);
-  L.chunks_per_split = (L.n_chunks + splits - 1) / splits;
-  L.splits = static_cast<int>((L.n_chunks + L.chunks_per_split - 1) / L.chunks_per_split);
+  L.n_g = (L.n_lb + L.G - 1) / L.G;
+  const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
+  // One CTA per SM, one wave.  CTAs go to tiles in proportion to their cost
+  // (a 400-row mode is 3 full tiles + 16 rows: equal splits would leave a
+  // fifth of the SMs streaming almost nothing); a block of a ragged tile
+  // costs a fixed pipeline share plus its rows' share of the bytes.  One SM
+  // is left free so the mode's ridge Cholesky (side stream) runs concurrently.
+  const int cap = std::min(sm_count_tc() - 1, kTcMaxSplits);
+  L.n_full = static_cast<int>(L.M / kTM);
+  const int tail = static_cast<int>(L.M % kTM);
+  double fixed = 1.0;  // measured: a ragged tile's l block costs about a full one
+  if (const char* e = getenv("NTF_TC_TAILCOST")) fixed = atof(e);
+  const double wt = tail ? fixed + (1.0 - fixed) * tail / static_cast<double>(kTM) : 0.0;
+  auto clampu = [&](int64_t s) { return static_cast<int>(std::max<int64_t>(1, std::min(s, units))); };
+  if (L.n_full == 0) {
+    L.splits = 0;
+    L.splits_tail = clampu(cap);
+  } else {
+    L.splits = clampu(static_cast<int64_t>(cap / (L.n_full + wt)));
+    L.splits_tail = 0;
+    if (tail)
+      L.splits_tail = clampu(std::min<int64_t>(static_cast<int64_t>(L.splits * wt + 0.5),
+                                               cap - static_cast<int64_t>(L.n_full) * L.splits));
+  }
+  if (L.splits) partition_units(L, L.splits, L.ub_full);
+  if (L.splits_tail) partition_units(L, L.splits_tail, L.ub_tail);
   L.wscale = nullptr;
+  L.wsl = nullptr;
   L.bound = false;
   return L;
 }
 
 size_t mttkrp_tc_workspace_bytes(const MttkrpTCLaunch& L, int R) {
-  return static_cast<size_t>(L.splits) * L.M * R * sizeof(double);
+  return static_cast<size_t>(std::max(L.splits, L.splits_tail)) * L.M * R * sizeof(double);
 }
 
 cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L) {
@@ -749,24 +891,28 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s0, gdim, gstr, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   CUresult r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s1, gdim, gstr, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) return cudaErrorInvalidValue;
   if (!L.wscale) {
     cudaError_t e = cudaMalloc(&L.wscale, sizeof(double) * 2 * L.N);
     if (e != cudaSuccess) return e;
   }
-  L.fac_lo = nullptr;
-  L.fac_hi = nullptr;
+  if (!L.wsl) {
+    cudaError_t e = cudaMalloc(&L.wsl, static_cast<size_t>(L.n_lb) * 3 * L.N * kBK * 2);
+    if (e != cudaSuccess) return e;
+  }
   L.bound = true;
   return cudaSuccess;
 }
 
 void mttkrp_tc_unbind(MttkrpTCLaunch& L) {
   cudaFree(L.wscale);
+  cudaFree(L.wsl);
   L.wscale = nullptr;
+  L.wsl = nullptr;
   L.bound = false;
 }
 
@@ -789,37 +935,29 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   } else {
     Fhi = A; Flo = B; hi_rows = I; lo_rows = J;
   }
-  // factor tensor maps are cached per factor pointer (plan buffers are fixed)
-  if (Flo != L.fac_lo) {
-    cudaError_t e = encode_factor_map(&L.tmap_lo, Flo, lo_rows, L.R, kBK);
-    if (e != cudaSuccess) return e;
-    L.fac_lo = Flo;
-  }
-  if (Fhi != L.fac_hi) {
-    cudaError_t e = encode_factor_map(&L.tmap_hi, Fhi, hi_rows, L.R, 1);
-    if (e != cudaSuccess) return e;
-    L.fac_hi = Fhi;
-  }
   TcParams p{};
   p.tmap0 = L.tmap0;
   p.tmap1 = L.tmap1;
-  p.tmap_lo = L.tmap_lo;
-  p.tmap_hi = L.tmap_hi;
   p.mode = L.mode;
   p.R = L.R;
   p.M = L.M;
-  p.l_extent = L.mode == 3 ? J : K;
-  p.n_chunks = L.n_chunks;
-  p.chunks_per_split = L.chunks_per_split;
-  p.chunks_per_o = L.chunks_per_o;
-  p.n_mtiles = L.n_mtiles;
+  p.l_ext = L.l_ext;
+  p.n_o = L.n_o;
+  p.n_lb = L.n_lb;
+  p.G = L.G;
+  p.n_full = L.n_full;
   p.splits = L.splits;
+  p.splits_tail = L.splits_tail;
   p.x_stages = L.x_stages;
-  p.w_stages = L.w_stages;
-  p.f_stages = L.f_stages;
-  p.stage_bytes = L.stage_bytes;
+  p.h_stages = L.h_stages;
+  p.f_hi = Fhi;
+  p.wsl = L.wsl;
   p.ws = ws;
   p.stop_flag = stop_flag;
+  for (int i = 0; i <= kTcMaxSplits; ++i) {
+    p.ub_full[i] = L.ub_full[i];
+    p.ub_tail[i] = L.ub_tail[i];
+  }
   {
     static int dbg = -1;
     if (dbg < 0) {
@@ -840,6 +978,16 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     if (e != cudaSuccess) return e;
     p.cm_hi = L.wscale;
     p.cm_lo = L.wscale + L.R;
+  }
+  {
+    const int t = L.G >= 4 ? 5 : (L.G >= 2 ? 6 : 7);
+    const int total = L.n_lb * L.N * (kBK / 8);
+    const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
+    if (!(p.debug & 128))
+    w_slice_kernel<<<blocks, 64, 0, stream>>>(Flo, L.l_ext, L.R, L.N, L.n_lb, p.cm_lo, t, L.wsl,
+                                               stop_flag);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
   return dispatch_tc(p, L, stream, false);
 }

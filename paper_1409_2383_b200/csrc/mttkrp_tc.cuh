@@ -23,20 +23,25 @@ cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* ou
                              cudaStream_t stream);
 void tc_tensor_destroy(TcTensor* t);
 
+constexpr int kTcMaxSplits = 160;  // CTAs per m-tile
+
 struct MttkrpTCLaunch {
   int mode;
   int R, N;                 // rank and MMA N (R rounded up to 16)
   int64_t M, Q;
-  int n_mtiles, splits;     // splits per m-tile
-  int64_t n_chunks, chunks_per_split, chunks_per_o;
-  int n_wf_warps, threads, smem_bytes;
-  int x_stages, w_stages, f_stages, stage_bytes;
+  int n_mtiles;
+  int n_full, splits;       // full 128-row tiles and CTAs per full tile
+  int splits_tail;          // CTAs of the ragged last tile (0: none)
+  int l_ext, n_o, n_lb;     // l extent, o extent, 64-wide l blocks
+  int G, n_g;               // l blocks per unit (one TMEM drain), groups
+  int threads, smem_bytes;
+  int x_stages, h_stages;
   int tmem_cols;
+  uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
+  uint32_t ub_tail[kTcMaxSplits + 1];
   CUtensorMap tmap0, tmap1; // S0 / S1 planes (built by mttkrp_tc_bind)
-  CUtensorMap tmap_lo, tmap_hi;      // factor rows (cached per factor pointer)
-  const double* fac_lo;
-  const double* fac_hi;
-  double* wscale;           // [2 * N] device: 2^(7-f(n)), output scale
+  double* wscale;           // [2 * N] device: column maxima for one-shot calls
+  unsigned char* wsl;       // [n_lb][3][N][128 B] W slices of F_lo (per launch)
   bool bound;
 };
 

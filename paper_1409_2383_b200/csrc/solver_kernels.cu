@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1) factor_update_kernel(FactorUpd
     if (cnt > static_cast<int64_t>(kRowsPerBlock) * R) cnt = static_cast<int64_t>(kRowsPerBlock) * R;
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
       double m = 0.0;
-      if (!(p.debug & 1)) m = strided_sum(p.mtt + base + e, p.splits, nM);
+      const int ns = (base + e) / R >= p.tail_row0 ? p.splits_tail : p.splits;
+      if (!(p.debug & 1)) m = strided_sum(p.mtt + base + e, ns, nM);
       msum[e] = m;
     }
   }

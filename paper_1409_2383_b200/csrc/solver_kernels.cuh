@@ -13,7 +13,9 @@ struct FactorUpdateParams {
   int64_t rows;             // owned rows
   int64_t row_offset;       // first owned row within the full factor
   const double* mtt;        // [splits][rows][R] MTTKRP partials
-  int splits;
+  int splits;               // partials of rows < tail_row0
+  int64_t tail_row0;        // rows >= tail_row0 have splits_tail partials
+  int splits_tail;
   const double* Lg;         // ridge factor from ridge_factor_kernel
   const double* rho;        // device [3]
   double* F;                // full factor (rows written at row_offset)
