@@ -101,17 +101,18 @@ struct ntf_plan {
   MttkrpOp op[3];
   int blocks[3];
   double* mtt_ws = nullptr;
-  double* norm_partials = nullptr;
-  double* gram_partials = nullptr;
+  double* norm_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][5][2] per mode
+  double* gram_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][R][R] per mode
   double* gram_ws = nullptr;
-  unsigned* done = nullptr;
+  bool any_tc = false;
   cudaStream_t capture_stream = nullptr;
   cudaGraphExec_t graph = nullptr;
   // ridge factorisation runs on a side stream concurrently with the MTTKRP
+  // Gram reductions (after each update) and the next mode's ridge run there:
+  // both only feed the ridge, so neither is on the critical path.
   cudaStream_t side = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-  double* ridge = nullptr;  // [R*R + R]
-  double* colmax_partials = nullptr;  // [blocks][R]
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, post_ev = nullptr;
+  double* ridge = nullptr;  // [3R*R + R], see ridge_factor_kernel
   // fp16 split planes for the tensor-core engine, one per distinct slab
   ntf::TcTensor tct[3];
   int n_tct = 0;
@@ -183,17 +184,31 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   fp.dual = d.duals[m];
   fp.last_sweep = last;
   fp.fuse_gram = d.fuse_gram;
-  fp.norm_partials = pl->norm_partials;
-  fp.gram_partials = pl->gram_partials;
-  fp.G_out = d.grams[m];
-  fp.colmax_partials = pl->colmax_partials;
-  fp.colmax_out = d.colmax + m * R;
-  fp.norm_acc = d.norm_acc + 10 * m;
-  fp.done_counter = pl->done + m;
+  fp.norm_partials = pl->norm_partials[m];
+  fp.gram_partials = pl->gram_partials[m];
+  // column maxima feed the tensor-core MTTKRPs only (zeroed by this mode's
+  // MTTKRP, re-accumulated here)
+  fp.colmax_bits = pl->any_tc ? reinterpret_cast<unsigned long long*>(d.colmax + m * R) : nullptr;
   fp.status = d.counters + 2;
   fp.stop_flag = d.counters + 1;
   NTF_CUDA_TRY(ntf::factor_update_launch(fp, s));
   if (ev) NTF_CUDA_TRY(record_event(ev[2], s));
+  if (d.fuse_gram) {  // G_m for the coming ridges, off the critical path
+    NTF_CUDA_TRY(cudaEventRecord(pl->post_ev, s));
+    NTF_CUDA_TRY(cudaStreamWaitEvent(pl->side, pl->post_ev, 0));
+    NTF_CUDA_TRY(ntf::gram_reduce_launch(pl->gram_partials[m], pl->blocks[m], R, d.grams[m],
+                                         d.counters + 1, pl->side));
+  }
+  if (last)
+    NTF_CUDA_TRY(ntf::norm_reduce_launch(pl->norm_partials[m], pl->blocks[m], d.norm_acc + 10 * m,
+                                         d.counters + 1, s));
+  return NTF_OK;
+}
+
+// main stream waits for the side stream's queued work (Gram reductions)
+int join_side(ntf_plan* pl, cudaStream_t s) {
+  NTF_CUDA_TRY(cudaEventRecord(pl->join_ev, pl->side));
+  NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
   return NTF_OK;
 }
 
@@ -227,6 +242,8 @@ int enqueue_iteration(ntf_plan* pl, cudaStream_t s) {
       const int rc = enqueue_mode_update(pl, mode, sw == sweeps - 1, s);
       if (rc != NTF_OK) return rc;
     }
+  const int rc = join_side(pl, s);
+  if (rc != NTF_OK) return rc;
   return enqueue_finalize(pl, s);
 }
 
@@ -362,12 +379,13 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return rc;
   };
   if ((e = cudaMalloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
-  if ((e = cudaMalloc(&pl->norm_partials, sizeof(double) * 10 * maxb)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMalloc norm"));
-  if ((e = cudaMalloc(&pl->colmax_partials, sizeof(double) * R * maxb)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMalloc colmax"));
-  if ((e = cudaMalloc(&pl->gram_partials, sizeof(double) * R * R * maxb)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMalloc gram"));
+  for (int m = 0; m < 3; ++m) {
+    const size_t nb = static_cast<size_t>(pl->blocks[m]);
+    if ((e = cudaMalloc(&pl->norm_partials[m], sizeof(double) * 10 * nb)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "cudaMalloc norm"));
+    if ((e = cudaMalloc(&pl->gram_partials[m], sizeof(double) * R * R * nb)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "cudaMalloc gram"));
+  }
   if ((e = cudaMalloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc gram ws"));
   if ((e = cudaMalloc(&pl->ridge, sizeof(double) * ntf::ridge_buffer_doubles(R))) != cudaSuccess)
@@ -378,10 +396,8 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaEventCreate"));
   if ((e = cudaEventCreateWithFlags(&pl->join_ev, cudaEventDisableTiming)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaEventCreate"));
-  if ((e = cudaMalloc(&pl->done, sizeof(unsigned) * 4)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMalloc counters"));
-  if ((e = cudaMemset(pl->done, 0, sizeof(unsigned) * 4)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMemset"));
+  if ((e = cudaEventCreateWithFlags(&pl->post_ev, cudaEventDisableTiming)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaEventCreate"));
   if ((e = ntf::factor_update_prepare(R)) != cudaSuccess) return cleanup(cuda_fail(e, "prepare"));
   for (int m = 0; m < 3; ++m) {
     if ((e = prepare_op(pl->op[m], m + 1, d.x_dtype)) != cudaSuccess)
@@ -389,9 +405,8 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   }
   // Tensor-core engine: split each distinct slab once into its fp16 planes
   // (one-time setup; synchronous so the caller's upload stream is irrelevant).
-  bool any_tc = false;
-  for (int m = 0; m < 3; ++m) any_tc = any_tc || pl->op[m].tc;
-  if (any_tc) {
+  for (int m = 0; m < 3; ++m) pl->any_tc = pl->any_tc || pl->op[m].tc;
+  if (pl->any_tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
     for (int m = 0; m < 3; ++m) {
       if (!pl->op[m].tc) continue;
@@ -440,7 +455,10 @@ int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t s
 int ntf_plan_mode_update(ntf_plan* pl, int mode, int last_sweep, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
-  return enqueue_mode_update(pl, mode, last_sweep ? 1 : 0, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int rc = enqueue_mode_update(pl, mode, last_sweep ? 1 : 0, s);
+  if (rc != NTF_OK) return rc;
+  return join_side(pl, s);  // grams[m] is current when the stream reaches here
 }
 
 int ntf_plan_finalize(ntf_plan* pl, ntf_stream_t stream) {
@@ -540,16 +558,17 @@ void ntf_plan_destroy(ntf_plan* pl) {
   if (pl->side) cudaStreamDestroy(pl->side);
   if (pl->fork_ev) cudaEventDestroy(pl->fork_ev);
   if (pl->join_ev) cudaEventDestroy(pl->join_ev);
+  if (pl->post_ev) cudaEventDestroy(pl->post_ev);
   cudaFree(pl->ridge);
   for (int m = 0; m < 3; ++m)
     if (pl->op[m].tc) ntf::mttkrp_tc_unbind(pl->op[m].tcl);
   for (int k = 0; k < pl->n_tct; ++k) ntf::tc_tensor_destroy(&pl->tct[k]);
   cudaFree(pl->mtt_ws);
-  cudaFree(pl->norm_partials);
-  cudaFree(pl->gram_partials);
-  cudaFree(pl->colmax_partials);
+  for (int m = 0; m < 3; ++m) {
+    cudaFree(pl->norm_partials[m]);
+    cudaFree(pl->gram_partials[m]);
+  }
   cudaFree(pl->gram_ws);
-  cudaFree(pl->done);
   delete pl;
 }
 

@@ -236,6 +236,8 @@ struct TcParams {
   const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
   const double* cm_lo;       // [R] max |F_lo[:, n]|
   const double* xscale;      // tensor split scale (device scalar)
+  double* cm_self;           // [R] this mode's column maxima: zeroed here, re-accumulated
+                             // by the row update that follows (NULL: untouched)
   double* ws;                // [splits][M][R] partials
   const int* stop_flag;
   int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip W forming,
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   double* wsc = reinterpret_cast<double*>(acc_empty + 6);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && p.cm_self && threadIdx.x < R) p.cm_self[threadIdx.x] = 0.0;
   if (threadIdx.x < N) {
     const int n = threadIdx.x;
     const int t = G >= 4 ? 5 : (G >= 2 ? 6 : 7);
@@ -971,6 +974,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     const int hm = L.mode == 1 ? 1 : 0, lm = L.mode == 3 ? 1 : 2;
     p.cm_hi = colmax3 + hm * L.R;
     p.cm_lo = colmax3 + lm * L.R;
+    p.cm_self = const_cast<double*>(colmax3) + (L.mode - 1) * L.R;
   } else {        // one-shot call: compute them here
     colmax_kernel<<<L.R, 256, 0, stream>>>(Fhi, hi_rows, L.R, L.wscale);
     colmax_kernel<<<L.R, 256, 0, stream>>>(Flo, lo_rows, L.R, L.wscale + L.R);

@@ -1,7 +1,8 @@
 // Per-mode ridge/ADMM update, Gram, iteration finalisation and residual-norm
-// kernels for the B200 NTF hot path (sm_100a).  All reductions run in a fixed
-// order (no float atomics), so a fit is bitwise run-to-run deterministic like
-// the reference (blocks.py:130-140).
+// kernels for the B200 NTF hot path (sm_100a).  All floating-point reductions
+// run in a fixed order (no float atomics; column maxima use an integer
+// atomicMax on IEEE bits, which is exact and order-free), so a fit is bitwise
+// run-to-run deterministic like the reference (blocks.py:130-140).
 #include "solver_kernels.cuh"
 
 namespace ntf {
@@ -9,10 +10,13 @@ namespace ntf {
 namespace {
 
 constexpr int kUpdThreads = 256;
-// rows per update block: two rows per warp keeps the dependent substitution
-// chains short and spreads a mode's rows over many SMs; the per-block Gram
-// partials are reduced by the last block
-__host__ __device__ __forceinline__ int rows_per_block(int R) { return R <= 64 ? 16 : 8; }
+// rows per update block.  R <= 64: the rows of a block are solved together as
+// small GEMMs against the ridge inverse; few rows per block spread a mode over
+// many SMs, so the latency-bound MTTKRP split reduction runs wide.  R > 64:
+// one row per warp (substitution against the Cholesky factor).
+__host__ __device__ __forceinline__ int rows_per_block(int R) {
+  return R <= 32 ? 4 : (R <= 64 ? 2 : 8);
+}
 
 // ---------------------------------------------------------------------------
 // Ridge Cholesky in shared memory (solver.ridge_cholesky, solver.py:167-175):
@@ -172,196 +176,75 @@ __device__ __forceinline__ void warp_chol_solve(double (&y)[RT], const double* L
   }
 }
 
-template <int RT>
-__global__ void __launch_bounds__(kUpdThreads, 1) factor_update_kernel(FactorUpdateParams p) {
-  if (p.stop_flag && *p.stop_flag) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// Sum of the MTTKRP split partials of the block's elements [base, base+cnt)
+// (rows * R contiguous values) into out[0, npm).  With npm < kUpdThreads,
+// kUpdThreads / npm threads share an element, each summing a fixed strided
+// subset of the splits with 8 independent loads in flight, then the subsets
+// are combined in fixed order; all orders are fixed, so the sum is
+// deterministic.  Ends with a barrier.
+__device__ void split_sum(const FactorUpdateParams& p, int64_t base, int cnt, int npm, double* out,
+                          double* scratch) {
   const int R = p.R;
-  const int ldl = R + 1;  // odd pitch: conflict-free row and column walks
-  double* L = reinterpret_cast<double*>(smem_raw);
-  double* inv_diag = L + R * ldl;               // [R]
-  const int kRowsPerBlock = rows_per_block(R);
-  double* xrows = inv_diag + R;                 // [rows][R] new factor rows
-  double* msum = xrows + kRowsPerBlock * R;     // [rows][R] reduced MTTKRP rows
-  // [8 warps][5][scale, ssq], after the GEMV path's H / rhs / x1 buffers when RT <= 2
-  double* red = msum + kRowsPerBlock * R + (RT <= 2 ? R * R + 2 * kRowsPerBlock * R : 0);
-  __shared__ bool is_last;
-  // Ridge factor from the concurrent ridge_factor_kernel (solver.py:167-175)
-  if (*p.status == kDevNotPD) return;
-  if constexpr (RT <= 2) {
-    // H^-1 into L's slot (pitch R) and H after the MTTKRP row sums
-    double* Hm = msum + kRowsPerBlock * R;
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      L[e] = p.Lg[R * R + R + e];
-      Hm[e] = p.Lg[2 * R * R + R + e];
+  const int64_t nM = p.rows * R;
+  const int K = npm >= kUpdThreads ? 1 : kUpdThreads / npm;
+  auto partial = [&](int e, int k) {
+    const int64_t g = base + e;
+    const int ns = g / R >= p.tail_row0 ? p.splits_tail : p.splits;
+    const double* src = p.mtt + g;
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int s0 = k; s0 < ns; s0 += 8 * K) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int sp = s0 + u * K;
+        if (sp < ns) a[u] += src[static_cast<int64_t>(sp) * nM];
+      }
     }
+    return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  };
+  if (K == 1) {
+    for (int e = threadIdx.x; e < npm; e += blockDim.x) out[e] = e < cnt ? partial(e, 0) : 0.0;
   } else {
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      const int i = e / R, k = e - (e / R) * R;
-      L[i * ldl + k] = p.Lg[e];
-    }
-    for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
-  }
-
-  const int64_t row_base = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;
-  const int64_t n_rows = p.rows;
-  const int64_t nM = n_rows * R;
-  // Sum the MTTKRP split partials of this block's rows (fixed split order),
-  // all threads cooperating; rows are contiguous so the block's slice of each
-  // partial is one contiguous run.
-  {
-    const int64_t base = row_base * R;
-    int64_t cnt = nM - base;
-    if (cnt > static_cast<int64_t>(kRowsPerBlock) * R) cnt = static_cast<int64_t>(kRowsPerBlock) * R;
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-      double m = 0.0;
-      const int ns = (base + e) / R >= p.tail_row0 ? p.splits_tail : p.splits;
-      if (!(p.debug & 1)) m = strided_sum(p.mtt + base + e, ns, nM);
-      msum[e] = m;
+    const int t = threadIdx.x, e = t % npm, k = t / npm;
+    double v = 0.0;
+    if (k < K && e < cnt && !(p.debug & 1)) v = partial(e, k);
+    scratch[t] = v;
+    __syncthreads();
+    if (t < npm) {
+      double acc = 0.0;
+      for (int kk = 0; kk < K; ++kk) acc += scratch[kk * npm + t];
+      out[t] = acc;
     }
   }
-
-  const double rho = p.rho[p.mode - 1];
   __syncthreads();
+}
 
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = kUpdThreads / 32;
+// aux = project(F + Y/rho) (solver.py:311-314, constraints.py:105-111),
+// Y += rho (F - aux) (solver.py:315-317); residual terms into the scaled norms
+__device__ __forceinline__ void admm_step(const FactorUpdateParams& p, int64_t g, double x,
+                                          double rho, ScaledSq (&nrm)[5]) {
+  const double yd = p.dual[g];
+  const double a_old = p.aux[g];
+  const double v = x + yd / rho;
+  if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
+  const double a = v > 0.0 ? v : 0.0;
+  const double ynew = yd + rho * (x - a);
+  p.aux[g] = a;
+  p.dual[g] = ynew;
+  nrm[0].add(x - a);
+  nrm[1].add(a - a_old);
+  nrm[2].add(x);
+  nrm[3].add(a);
+  nrm[4].add(ynew);
+}
 
-  ScaledSq nrm[5];
-  if constexpr (RT <= 2) {
-    // R <= 64: all rows of the block at once as small GEMMs against the
-    // ridge inverse, with one step of iterative refinement against H itself:
-    //   x1 = y H^-1,  x = x1 + (y - x1 H) H^-1
-    // Every (row, column) pair is independent: no sequential substitution
-    // chain on the critical path.  Agreement with cho_solve (solver.py:188)
-    // is at the backward-error level.
-    double* Hi = L;                          // reuse: [R][R] H^-1
-    double* Hm = msum + kRowsPerBlock * R;   // [R][R] H   (after msum)
-    double* yb = Hm + R * R;                 // [rows][R]  rhs, then residual
-    double* x1 = yb + kRowsPerBlock * R;     // [rows][R]
-    const int np = kRowsPerBlock * R;
-    for (int e = threadIdx.x; e < np; e += blockDim.x) {
-      const int lr = e / R, c = e - (e / R) * R;
-      const int64_t row = row_base + lr;
-      double y = 0.0;
-      if (row < n_rows) {
-        const int64_t g = row * R + c;
-        y = (msum[e] + rho * p.aux[g]) - p.dual[g];  // ridge_rhs (solver.py:178-179)
-      }
-      yb[e] = y;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < np; e += blockDim.x) {
-      const int lr = e / R, c = e - (e / R) * R;
-      double s = 0.0;
-      for (int k = 0; k < R; ++k) s = fma(yb[lr * R + k], Hi[k * R + c], s);
-      x1[e] = s;
-    }
-    __syncthreads();
-    double res[4];  // np / blockDim <= 4 (rows 16 x R <= 64 over 256 threads)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = threadIdx.x + u * kUpdThreads;
-      res[u] = 0.0;
-      if (e < np) {
-        const int lr = e / R, c = e - (e / R) * R;
-        double s = yb[e];
-        for (int k = 0; k < R; ++k) s = fma(-x1[lr * R + k], Hm[k * R + c], s);
-        res[u] = s;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = threadIdx.x + u * kUpdThreads;
-      if (e < np) yb[e] = res[u];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < np; e += blockDim.x) {
-      const int lr = e / R, c = e - (e / R) * R;
-      const int64_t row = row_base + lr;
-      double x = x1[e];
-      for (int k = 0; k < R; ++k) x = fma(yb[lr * R + k], Hi[k * R + c], x);
-      if (row >= n_rows) {
-        xrows[e] = 0.0;
-        continue;
-      }
-      const int64_t g = row * R + c;
-      p.F[(p.row_offset + row) * R + c] = x;
-      xrows[e] = x;
-      if (p.last_sweep) {
-        // aux = project(F + Y/rho), Y += rho (F - aux), residual partials
-        const double yd = p.dual[g];
-        const double a_old = p.aux[g];
-        const double v = x + yd / rho;
-        if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
-        const double a = v > 0.0 ? v : 0.0;
-        const double ynew = yd + rho * (x - a);
-        p.aux[g] = a;
-        p.dual[g] = ynew;
-        const double d0 = x - a, d1 = a - a_old;
-        nrm[0].add(d0);
-        nrm[1].add(d1);
-        nrm[2].add(x);
-        nrm[3].add(a);
-        nrm[4].add(ynew);
-      }
-    }
-  }
-  for (int lr = warp; RT > 2 && lr < kRowsPerBlock; lr += nwarps) {
-    const int64_t row = row_base + lr;
-    double y[RT];
-    if (row < n_rows) {
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int r = lane + 32 * t;
-        y[t] = 0.0;
-        if (r < R) {
-          const int64_t e = row * R + r;
-          // ridge_rhs: mtt + rho*aux - dual (solver.py:178-179)
-          y[t] = (msum[lr * R + r] + rho * p.aux[e]) - p.dual[e];
-        }
-      }
-      if (!(p.debug & 2)) warp_chol_solve<RT>(y, L, ldl, R, inv_diag, lane);
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int r = lane + 32 * t;
-        if (r < R) {
-          const int64_t e = row * R + r;
-          const double x = y[t];
-          p.F[(p.row_offset + row) * R + r] = x;
-          xrows[lr * R + r] = x;
-          if (p.last_sweep) {
-            // aux = project(F + Y/rho) (solver.py:311-314, constraints.py:105-111),
-            // Y += rho (F - aux) (solver.py:315-317), residual partials (247-255)
-            const double yd = p.dual[e];
-            const double a_old = p.aux[e];
-            const double v = x + yd / rho;
-            if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
-            const double a = v > 0.0 ? v : 0.0;
-            const double ynew = yd + rho * (x - a);
-            p.aux[e] = a;
-            p.dual[e] = ynew;
-            const double d0 = x - a, d1 = a - a_old;
-            nrm[0].add(d0);
-            nrm[1].add(d1);
-            nrm[2].add(x);
-            nrm[3].add(a);
-            nrm[4].add(ynew);
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int r = lane + 32 * t;
-        if (r < R) xrows[lr * R + r] = 0.0;
-      }
-    }
-  }
-
-  const int nblocks = gridDim.x;
+// Block epilogue: scaled-norm partial (last sweep), Gram partial of the
+// block's new rows and the column maxima (fuse_gram).  xr: [rpb][R] new rows
+// (zero for rows past the end).  red: >= 80 doubles of scratch.
+__device__ void block_partials(const FactorUpdateParams& p, ScaledSq (&nrm)[5], const double* xr,
+                               int rpb, double* red) {
+  const int R = p.R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nwarps = kUpdThreads / 32;
   if (p.last_sweep) {
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
@@ -377,76 +260,207 @@ __global__ void __launch_bounds__(kUpdThreads, 1) factor_update_kernel(FactorUpd
         red[(warp * 5 + c) * 2 + 1] = v.ssq;
       }
     }
-  }
-  __syncthreads();
-  if (p.last_sweep && threadIdx.x < 5) {
-    ScaledSq s;
-    for (int w = 0; w < nwarps; ++w)
-      s.merge(red[(w * 5 + threadIdx.x) * 2], red[(w * 5 + threadIdx.x) * 2 + 1]);
-    p.norm_partials[(blockIdx.x * 5 + threadIdx.x) * 2] = s.scale;
-    p.norm_partials[(blockIdx.x * 5 + threadIdx.x) * 2 + 1] = s.ssq;
-  }
-  if (p.fuse_gram) {
-    // partial Gram of this block's new rows, fixed row order
-    double* gp = p.gram_partials + static_cast<int64_t>(blockIdx.x) * R * R;
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      const int r = e / R, s = e - (e / R) * R;
-      double acc = 0.0;
-      for (int lr = 0; lr < kRowsPerBlock; ++lr) acc += xrows[lr * R + r] * xrows[lr * R + s];
-      gp[e] = acc;
-    }
-    // per-column max |F| of this block's rows (W scales of the next MTTKRPs)
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
-      double mx = 0.0;
-      for (int lr = 0; lr < kRowsPerBlock; ++lr) mx = fmax(mx, fabs(xrows[lr * R + r]));
-      p.colmax_partials[blockIdx.x * R + r] = mx;
-    }
-  }
-  if (!p.fuse_gram && !p.last_sweep) return;
-
-  // last block to finish reduces the per-block partials in block order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(p.done_counter, 1u);
-    is_last = (prev == static_cast<unsigned>(nblocks - 1));
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  if (p.fuse_gram && !(p.debug & 4)) {
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      double s = 0.0;
-      s = strided_sum(p.gram_partials + e, nblocks, static_cast<int64_t>(R) * R);
-      p.G_out[e] = s;
-    }
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
-      double mx = 0.0;  // max is order-independent: exact and deterministic
-      for (int b = 0; b < nblocks; ++b) mx = fmax(mx, p.colmax_partials[b * R + r]);
-      p.colmax_out[r] = mx;
-    }
-  }
-  if (p.last_sweep) {
-    // 8 interleaved merge chains per norm (fixed order), then chain 0..7 merged
-    __syncthreads();
-    if (threadIdx.x < 40) {
-      const int c = threadIdx.x >> 3, ch = threadIdx.x & 7;
-      ScaledSq s;
-      for (int b = ch; b < nblocks; b += 8)
-        s.merge(p.norm_partials[(b * 5 + c) * 2], p.norm_partials[(b * 5 + c) * 2 + 1]);
-      red[threadIdx.x * 2] = s.scale;
-      red[threadIdx.x * 2 + 1] = s.ssq;
-    }
     __syncthreads();
     if (threadIdx.x < 5) {
-      ScaledSq s;
-      for (int ch = 0; ch < 8; ++ch)
-        s.merge(red[(threadIdx.x * 8 + ch) * 2], red[(threadIdx.x * 8 + ch) * 2 + 1]);
-      p.norm_acc[threadIdx.x * 2] = s.scale;
-      p.norm_acc[threadIdx.x * 2 + 1] = s.ssq;
+      ScaledSq acc;
+      for (int w = 0; w < nwarps; ++w)
+        acc.merge(red[(w * 5 + threadIdx.x) * 2], red[(w * 5 + threadIdx.x) * 2 + 1]);
+      p.norm_partials[(blockIdx.x * 5 + threadIdx.x) * 2] = acc.scale;
+      p.norm_partials[(blockIdx.x * 5 + threadIdx.x) * 2 + 1] = acc.ssq;
     }
   }
-  if (threadIdx.x == 0) *p.done_counter = 0u;
+  if (p.fuse_gram) {
+    // partial Gram of this block's rows (fixed row order), reduced by
+    // gram_reduce_kernel off the critical path
+    double* gp = p.gram_partials + static_cast<int64_t>(blockIdx.x) * R * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int r = e / R, c = e - (e / R) * R;
+      double acc = 0.0;
+      for (int lr = 0; lr < rpb; ++lr) acc += xr[lr * R + r] * xr[lr * R + c];
+      gp[e] = acc;
+    }
+    // max |F[:, r]| (W scales of the next tensor-core MTTKRPs): non-negative
+    // doubles order like their IEEE bits, so an integer atomicMax is exact
+    if (p.colmax_bits)
+      for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        double mx = 0.0;
+        for (int lr = 0; lr < rpb; ++lr) mx = fmax(mx, fabs(xr[lr * R + r]));
+        if (mx > 0.0) atomicMax(p.colmax_bits + r, static_cast<unsigned long long>(__double_as_longlong(mx)));
+      }
+  }
+}
+
+// R <= 64: all rows of the block at once as small GEMMs against the ridge
+// inverse, with one step of iterative refinement against H itself:
+//   x1 = y H^-1,  x = x1 + (y - x1 H) H^-1
+// Every (row, column) pair is independent: no sequential substitution chain
+// on the critical path.  Agreement with cho_solve (solver.py:188) is at the
+// backward-error level.
+__global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorUpdateParams p) {
+  if (p.stop_flag && *p.stop_flag) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int R = p.R;
+  const int rpb = rows_per_block(R);
+  const int npm = rpb * R;
+  double* Hi = reinterpret_cast<double*>(smem_raw);  // [R][R] H^-1
+  double* Hm = Hi + R * R;                            // [R][R] H
+  double* yb = Hm + R * R;                            // [npm] rhs, then residual
+  double* x1 = yb + npm;
+  double* ms = x1 + npm;                              // MTTKRP row sums
+  double* ax = ms + npm;                              // aux rows
+  double* dl = ax + npm;                              // dual rows
+  double* xr = dl + npm;                              // new rows
+  double* scr = xr + npm;                             // [kUpdThreads] scratch
+  // Ridge factor from the concurrent ridge_factor_kernel (solver.py:167-175)
+  if (*p.status == kDevNotPD) return;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
+  const int64_t nM = p.rows * R;
+  const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
+  // loads that do not depend on the MTTKRP first (all in flight together)
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    Hi[e] = p.Lg[R * R + R + e];
+    Hm[e] = p.Lg[2 * R * R + R + e];
+  }
+  for (int e = threadIdx.x; e < npm; e += blockDim.x) {
+    ax[e] = e < cnt ? p.aux[base + e] : 0.0;
+    dl[e] = e < cnt ? p.dual[base + e] : 0.0;
+  }
+  const double rho = p.rho[p.mode - 1];
+  split_sum(p, base, cnt, npm, ms, scr);
+  for (int e = threadIdx.x; e < npm; e += blockDim.x)
+    yb[e] = e < cnt ? (ms[e] + rho * ax[e]) - dl[e] : 0.0;  // ridge_rhs (solver.py:178-179)
+  __syncthreads();
+  for (int e = threadIdx.x; e < npm; e += blockDim.x) {
+    const int lr = e / R, c = e - (e / R) * R;
+    double acc = 0.0;
+    for (int k = 0; k < R; ++k) acc = fma(yb[lr * R + k], Hi[k * R + c], acc);
+    x1[e] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < npm; e += blockDim.x) {  // residual y - x1 H
+    const int lr = e / R, c = e - (e / R) * R;
+    double acc = yb[e];
+    for (int k = 0; k < R; ++k) acc = fma(-x1[lr * R + k], Hm[k * R + c], acc);
+    xr[e] = acc;
+  }
+  __syncthreads();
+  ScaledSq nrm[5];
+  double xv[(64 * 2 + kUpdThreads - 1) / kUpdThreads];
+#pragma unroll
+  for (int u = 0; u < (64 * 2 + kUpdThreads - 1) / kUpdThreads; ++u) {
+    const int e = threadIdx.x + u * kUpdThreads;
+    xv[u] = 0.0;
+    if (e < npm) {
+      const int lr = e / R, c = e - (e / R) * R;
+      double acc = x1[e];
+      for (int k = 0; k < R; ++k) acc = fma(xr[lr * R + k], Hi[k * R + c], acc);
+      xv[u] = e < cnt ? acc : 0.0;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < (64 * 2 + kUpdThreads - 1) / kUpdThreads; ++u) {
+    const int e = threadIdx.x + u * kUpdThreads;
+    if (e < npm) {
+      xr[e] = xv[u];
+      if (e < cnt) {
+        const int64_t g = base + e;
+        p.F[p.row_offset * R + g] = xv[u];
+        if (p.last_sweep) admm_step(p, g, xv[u], rho, nrm);
+      }
+    }
+  }
+  __syncthreads();
+  block_partials(p, nrm, xr, rpb, scr);
+}
+
+// R > 64: one row per warp, forward/backward substitution against L.
+template <int RT>
+__global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorUpdateParams p) {
+  if (p.stop_flag && *p.stop_flag) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int R = p.R;
+  const int ldl = R + 1;  // odd pitch: conflict-free row and column walks
+  const int rpb = rows_per_block(R);
+  const int npm = rpb * R;
+  double* L = reinterpret_cast<double*>(smem_raw);
+  double* inv_diag = L + R * ldl;  // [R]
+  double* ms = inv_diag + R;       // [npm] MTTKRP row sums
+  double* xr = ms + npm;           // [npm] new rows
+  double* scr = xr + npm;          // [kUpdThreads]
+  if (*p.status == kDevNotPD) return;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    L[i * ldl + k] = p.Lg[e];
+  }
+  for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
+  const int64_t nM = p.rows * R;
+  const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
+  const double rho = p.rho[p.mode - 1];
+  split_sum(p, base, cnt, npm, ms, scr);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ScaledSq nrm[5];
+  for (int lr = warp; lr < rpb; lr += kUpdThreads / 32) {
+    const bool valid = lr * R < cnt;
+    double y[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int r = lane + 32 * t;
+      y[t] = 0.0;
+      if (valid && r < R) {
+        const int64_t g = base + lr * R + r;
+        y[t] = (ms[lr * R + r] + rho * p.aux[g]) - p.dual[g];  // ridge_rhs
+      }
+    }
+    if (valid) warp_chol_solve<RT>(y, L, ldl, R, inv_diag, lane);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int r = lane + 32 * t;
+      if (r < R) {
+        xr[lr * R + r] = valid ? y[t] : 0.0;
+        if (valid) {
+          const int64_t g = base + lr * R + r;
+          p.F[p.row_offset * R + g] = y[t];
+          if (p.last_sweep) admm_step(p, g, y[t], rho, nrm);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  block_partials(p, nrm, xr, rpb, scr);
+}
+
+// G[e] = sum_b part[b][e] (fixed block order; off the critical path on the
+// plan's side stream)
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int nb, int n,
+                                   double* __restrict__ G, const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) G[e] = strided_sum(part + e, nb, n);
+}
+
+// norm_acc[c] = merge_b part[b][c] (5 scaled norms; 8 interleaved chains of
+// fixed order, then the chains in order)
+__global__ void norm_reduce_kernel(const double* __restrict__ part, int nb, double* __restrict__ out,
+                                   const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
+  __shared__ double red[80];
+  if (threadIdx.x < 40) {
+    const int c = threadIdx.x >> 3, ch = threadIdx.x & 7;
+    ScaledSq acc;
+    for (int b = ch; b < nb; b += 8) acc.merge(part[(b * 5 + c) * 2], part[(b * 5 + c) * 2 + 1]);
+    red[threadIdx.x * 2] = acc.scale;
+    red[threadIdx.x * 2 + 1] = acc.ssq;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    ScaledSq acc;
+    for (int ch = 0; ch < 8; ++ch)
+      acc.merge(red[(threadIdx.x * 8 + ch) * 2], red[(threadIdx.x * 8 + ch) * 2 + 1]);
+    out[threadIdx.x * 2] = acc.scale;
+    out[threadIdx.x * 2 + 1] = acc.ssq;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -653,9 +667,12 @@ int factor_update_blocks(int64_t rows, int R) {
 }
 
 size_t factor_update_smem(int R) {
-  const size_t rpb = rows_per_block(R);
-  size_t n = static_cast<size_t>(R) * (R + 1) + R + 2 * rpb * R + 8 * 10;
-  if (R <= 64) n += static_cast<size_t>(R) * R + 2 * rpb * R;  // GEMV path buffers
+  const size_t npm = static_cast<size_t>(rows_per_block(R)) * R;
+  size_t n;
+  if (R <= 64)
+    n = 2 * static_cast<size_t>(R) * R + 6 * npm + kUpdThreads;
+  else
+    n = static_cast<size_t>(R) * (R + 1) + R + 2 * npm + kUpdThreads;
   return n * sizeof(double);
 }
 
@@ -676,13 +693,11 @@ cudaError_t factor_update_prepare(int R) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(ridge_factor_smem(R)));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(factor_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  e = cudaFuncSetAttribute(factor_update_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(factor_update_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  e = cudaFuncSetAttribute(factor_update_warp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(factor_update_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(factor_update_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(factor_update_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               smem);
 }
 
@@ -696,13 +711,25 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
   p.debug = dbg;
   const int blocks = factor_update_blocks(p.rows, p.R);
   const size_t smem = factor_update_smem(p.R);
-  const int rt = (p.R + 31) / 32;
-  switch (rt) {
-    case 1: factor_update_kernel<1><<<blocks, kUpdThreads, smem, stream>>>(p); break;
-    case 2: factor_update_kernel<2><<<blocks, kUpdThreads, smem, stream>>>(p); break;
-    case 3: factor_update_kernel<3><<<blocks, kUpdThreads, smem, stream>>>(p); break;
-    default: factor_update_kernel<4><<<blocks, kUpdThreads, smem, stream>>>(p); break;
-  }
+  if (p.R <= 64)
+    factor_update_gemv_kernel<<<blocks, kUpdThreads, smem, stream>>>(p);
+  else if (p.R <= 96)
+    factor_update_warp_kernel<3><<<blocks, kUpdThreads, smem, stream>>>(p);
+  else
+    factor_update_warp_kernel<4><<<blocks, kUpdThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t gram_reduce_launch(const double* part, int nb, int R, double* G, const int* stop_flag,
+                               cudaStream_t stream) {
+  const int n = R * R;
+  gram_reduce_kernel<<<(n + 127) / 128, 128, 0, stream>>>(part, nb, n, G, stop_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t norm_reduce_launch(const double* part, int nb, double* out, const int* stop_flag,
+                               cudaStream_t stream) {
+  norm_reduce_kernel<<<1, 64, 0, stream>>>(part, nb, out, stop_flag);
   return cudaGetLastError();
 }
 

@@ -23,13 +23,9 @@ struct FactorUpdateParams {
   double* dual;             // owned rows
   int last_sweep;
   int fuse_gram;
-  double* norm_partials;    // [blocks][5][scale, ssq]
-  double* gram_partials;    // [blocks][R][R]
-  double* G_out;            // R x R (fuse_gram)
-  double* colmax_partials;  // [blocks][R]
-  double* colmax_out;       // [R] max |F[:, r]| (fuse_gram)
-  double* norm_acc;         // [5][scale, ssq] this mode
-  unsigned* done_counter;
+  double* norm_partials;    // [blocks][5][scale, ssq] (last sweep)
+  double* gram_partials;    // [blocks][R][R] (fuse_gram)
+  unsigned long long* colmax_bits;  // [R] running max |F[:, r]| as IEEE bits (fuse_gram)
   int* status;
   const int* stop_flag;
   int debug;                // profiling only (NTF_UPD_DEBUG)
@@ -67,6 +63,11 @@ cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream);
 size_t factor_update_smem(int R);
 cudaError_t factor_update_prepare(int R);
 cudaError_t factor_update_launch(const FactorUpdateParams& p, cudaStream_t stream);
+// grams[m] = sum of the update blocks' Gram partials; norm_acc[m] likewise
+cudaError_t gram_reduce_launch(const double* part, int nb, int R, double* G, const int* stop_flag,
+                               cudaStream_t stream);
+cudaError_t norm_reduce_launch(const double* part, int nb, double* out, const int* stop_flag,
+                               cudaStream_t stream);
 
 size_t gram_workspace_bytes(int64_t rows, int R);
 cudaError_t gram_launch(const double* F, int64_t rows, int R, double* G, double* ws,
