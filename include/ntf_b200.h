@@ -162,9 +162,11 @@ int ntf_plan_mode_update(ntf_plan* plan, int mode, int last_sweep, ntf_stream_t 
 int ntf_plan_finalize(ntf_plan* plan, ntf_stream_t stream);
 /* Optional per-launch timing: when enabled, the plan records CUDA events
  * around every MTTKRP and every row-update launch of an outer iteration (also
- * inside the captured graph).  ntf_plan_kernel_times writes, for the most
- * recent iteration, 2 floats (MTTKRP ms, update ms) per mode update in sweep
- * order and returns how many floats were written (or a negative status). */
+ * inside the captured graph; the plain and the instrumented graph are cached
+ * separately, so toggling costs nothing after the first capture of each).
+ * ntf_plan_kernel_times writes, for the most recent instrumented iteration,
+ * 2 floats (MTTKRP ms, update ms) per mode update in sweep order and returns
+ * how many floats were written (or a negative status). */
 int ntf_plan_set_timing(ntf_plan* plan, int enable);
 int ntf_plan_kernel_times(ntf_plan* plan, float* ms_out, int capacity);
 void ntf_plan_destroy(ntf_plan* plan);

@@ -106,7 +106,7 @@ struct ntf_plan {
   double* gram_ws = nullptr;
   bool any_tc = false;
   cudaStream_t capture_stream = nullptr;
-  cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [timing]: plain / with timing events
   // ridge factorisation runs on a side stream concurrently with the MTTKRP
   // Gram reductions (after each update) and the next mode's ridge run there:
   // both only feed the ridge, so neither is on the critical path.
@@ -378,17 +378,17 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     ntf_plan_destroy(pl);
     return rc;
   };
-  if ((e = cudaMalloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
+  if ((e = ntf::dev_alloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
   for (int m = 0; m < 3; ++m) {
     const size_t nb = static_cast<size_t>(pl->blocks[m]);
-    if ((e = cudaMalloc(&pl->norm_partials[m], sizeof(double) * 10 * nb)) != cudaSuccess)
+    if ((e = ntf::dev_alloc(&pl->norm_partials[m], sizeof(double) * 10 * nb)) != cudaSuccess)
       return cleanup(cuda_fail(e, "cudaMalloc norm"));
-    if ((e = cudaMalloc(&pl->gram_partials[m], sizeof(double) * R * R * nb)) != cudaSuccess)
+    if ((e = ntf::dev_alloc(&pl->gram_partials[m], sizeof(double) * R * R * nb)) != cudaSuccess)
       return cleanup(cuda_fail(e, "cudaMalloc gram"));
   }
-  if ((e = cudaMalloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
+  if ((e = ntf::dev_alloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc gram ws"));
-  if ((e = cudaMalloc(&pl->ridge, sizeof(double) * ntf::ridge_buffer_doubles(R))) != cudaSuccess)
+  if ((e = ntf::dev_alloc(&pl->ridge, sizeof(double) * ntf::ridge_buffer_doubles(R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc ridge"));
   if ((e = cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaStreamCreate"));
@@ -477,7 +477,8 @@ int ntf_plan_run(ntf_plan* pl, int n_iters, int use_graph, ntf_stream_t stream) 
     }
     return NTF_OK;
   }
-  if (!pl->graph) {
+  cudaGraphExec_t& graph = pl->graph[pl->timing ? 1 : 0];
+  if (!graph) {
     if (!pl->capture_stream)
       NTF_CUDA_TRY(cudaStreamCreateWithFlags(&pl->capture_stream, cudaStreamNonBlocking));
     NTF_CUDA_TRY(cudaStreamBeginCapture(pl->capture_stream, cudaStreamCaptureModeThreadLocal));
@@ -489,11 +490,11 @@ int ntf_plan_run(ntf_plan* pl, int n_iters, int use_graph, ntf_stream_t stream) 
       return rc;
     }
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&pl->graph, g, 0);
+    e = cudaGraphInstantiate(&graph, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   }
-  for (int i = 0; i < n_iters; ++i) NTF_CUDA_TRY(cudaGraphLaunch(pl->graph, s));
+  for (int i = 0; i < n_iters; ++i) NTF_CUDA_TRY(cudaGraphLaunch(graph, s));
   return NTF_OK;
 }
 
@@ -509,13 +510,9 @@ static void free_events(ntf_plan* pl) {
 
 int ntf_plan_set_timing(ntf_plan* pl, int enable) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
-  if (pl->graph) {
-    cudaGraphExecDestroy(pl->graph);
-    pl->graph = nullptr;
-  }
-  free_events(pl);
+  // the two captured graphs stay cached: toggling is free once both exist
   pl->timing = enable ? 1 : 0;
-  if (!enable) return NTF_OK;
+  if (!enable || pl->events) return NTF_OK;
   const int n = 3 * 3 * pl->d.inner_sweeps;
   pl->events = new (std::nothrow) cudaEvent_t[n];
   if (!pl->events) return fail(NTF_ERR_INVALID, "out of host memory");
@@ -552,23 +549,25 @@ int ntf_plan_kernel_times(ntf_plan* pl, float* ms_out, int capacity) {
 
 void ntf_plan_destroy(ntf_plan* pl) {
   if (!pl) return;
+  if (pl->side) cudaStreamSynchronize(pl->side);  // pool releases are legacy-stream ordered
   free_events(pl);
-  if (pl->graph) cudaGraphExecDestroy(pl->graph);
+  for (int k = 0; k < 2; ++k)
+    if (pl->graph[k]) cudaGraphExecDestroy(pl->graph[k]);
   if (pl->capture_stream) cudaStreamDestroy(pl->capture_stream);
   if (pl->side) cudaStreamDestroy(pl->side);
   if (pl->fork_ev) cudaEventDestroy(pl->fork_ev);
   if (pl->join_ev) cudaEventDestroy(pl->join_ev);
   if (pl->post_ev) cudaEventDestroy(pl->post_ev);
-  cudaFree(pl->ridge);
+  ntf::dev_free(pl->ridge);
   for (int m = 0; m < 3; ++m)
     if (pl->op[m].tc) ntf::mttkrp_tc_unbind(pl->op[m].tcl);
   for (int k = 0; k < pl->n_tct; ++k) ntf::tc_tensor_destroy(&pl->tct[k]);
-  cudaFree(pl->mtt_ws);
+  ntf::dev_free(pl->mtt_ws);
   for (int m = 0; m < 3; ++m) {
-    cudaFree(pl->norm_partials[m]);
-    cudaFree(pl->gram_partials[m]);
+    ntf::dev_free(pl->norm_partials[m]);
+    ntf::dev_free(pl->gram_partials[m]);
   }
-  cudaFree(pl->gram_ws);
+  ntf::dev_free(pl->gram_ws);
   delete pl;
 }
 

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdint>
+#include <mutex>
+
 #include "../../include/ntf_b200.h"
 
 namespace ntf {
@@ -75,6 +78,37 @@ struct ScaledSq {
   }
   __device__ __forceinline__ double norm() const { return scale * sqrt(ssq); }
 };
+
+// Device memory of plans and tensor splits comes from the device's default
+// stream-ordered pool with a retained release threshold: repeated fit() calls
+// reuse already-mapped memory instead of paying cudaMalloc/cudaFree page
+// mapping each time.  Allocation and release are ordered on the legacy
+// stream; callers synchronise their own streams before release.
+inline void retain_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+}
+
+template <typename T>
+inline cudaError_t dev_alloc(T** p, size_t bytes) {
+  retain_pool();
+  void* v = nullptr;
+  cudaError_t e = cudaMallocAsync(&v, bytes, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  *p = static_cast<T*>(v);
+  return e;
+}
+
+inline void dev_free(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
 
 // Error/status flags written by kernels (host reads them back once per run).
 enum DeviceStatus : int {

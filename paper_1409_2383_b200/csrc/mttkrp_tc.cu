@@ -845,12 +845,12 @@ cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* ou
   TcTensor t;
   for (int i = 0; i < 3; ++i) t.dims[i] = dims[i];
   cudaError_t e;
-  if ((e = cudaMalloc(&t.s0, n * sizeof(__half))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.s1, n * sizeof(__half))) != cudaSuccess) {
+  if ((e = ntf::dev_alloc(&t.s0, n * sizeof(__half))) != cudaSuccess) return e;
+  if ((e = ntf::dev_alloc(&t.s1, n * sizeof(__half))) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
   }
-  if ((e = cudaMalloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
+  if ((e = ntf::dev_alloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
   }
@@ -869,9 +869,9 @@ cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* ou
 
 void tc_tensor_destroy(TcTensor* t) {
   if (!t) return;
-  cudaFree(t->s0);
-  cudaFree(t->s1);
-  cudaFree(t->xscale);
+  ntf::dev_free(t->s0);
+  ntf::dev_free(t->s1);
+  ntf::dev_free(t->xscale);
   t->s0 = t->s1 = nullptr;
   t->xscale = nullptr;
 }
@@ -900,11 +900,11 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) return cudaErrorInvalidValue;
   if (!L.wscale) {
-    cudaError_t e = cudaMalloc(&L.wscale, sizeof(double) * 2 * L.N);
+    cudaError_t e = ntf::dev_alloc(&L.wscale, sizeof(double) * 2 * L.N);
     if (e != cudaSuccess) return e;
   }
   if (!L.wsl) {
-    cudaError_t e = cudaMalloc(&L.wsl, static_cast<size_t>(L.n_lb) * 3 * L.N * kBK * 2);
+    cudaError_t e = ntf::dev_alloc(&L.wsl, static_cast<size_t>(L.n_lb) * 3 * L.N * kBK * 2);
     if (e != cudaSuccess) return e;
   }
   L.bound = true;
@@ -912,8 +912,8 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
 }
 
 void mttkrp_tc_unbind(MttkrpTCLaunch& L) {
-  cudaFree(L.wscale);
-  cudaFree(L.wsl);
+  ntf::dev_free(L.wscale);
+  ntf::dev_free(L.wsl);
   L.wscale = nullptr;
   L.wsl = nullptr;
   L.bound = false;
