@@ -431,33 +431,65 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   block_partials(p, nrm, xr, rpb, scr);
 }
 
-// G[e] = sum_b part[b][e] (fixed block order; off the critical path on the
-// plan's side stream)
+// G[e] = sum_b part[b][e]: kGramSub threads per element each sum a fixed
+// strided subset of the blocks (8 independent loads in flight), then the
+// subsets are added in fixed order.  On the plan's side stream, it only
+// feeds the next ridge factorisation.
+constexpr int kGramSub = 8;
+
 __global__ void gram_reduce_kernel(const double* __restrict__ part, int nb, int n,
                                    double* __restrict__ G, const int* stop_flag) {
   if (stop_flag && *stop_flag) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) G[e] = strided_sum(part + e, nb, n);
+  __shared__ double sub[kGramSub][32];
+  const int el = threadIdx.x & 31, k = threadIdx.x >> 5;  // 32 elements x kGramSub subsets
+  const int e = blockIdx.x * 32 + el;
+  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (e < n) {
+    for (int b0 = k; b0 < nb; b0 += 8 * kGramSub) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + u * kGramSub;
+        if (b < nb) a[u] += part[static_cast<int64_t>(b) * n + e];
+      }
+    }
+  }
+  sub[k][el] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  __syncthreads();
+  if (k == 0 && e < n) {
+    double acc = 0.0;
+    for (int kk = 0; kk < kGramSub; ++kk) acc += sub[kk][el];
+    G[e] = acc;
+  }
 }
 
-// norm_acc[c] = merge_b part[b][c] (5 scaled norms; 8 interleaved chains of
-// fixed order, then the chains in order)
+// norm_acc[c] = merge_b part[b][c] (5 scaled norms): 32 chains per norm, each
+// merging a fixed strided subset of the blocks (loads issued first), then
+// the chains merged in order.
 __global__ void norm_reduce_kernel(const double* __restrict__ part, int nb, double* __restrict__ out,
                                    const int* stop_flag) {
   if (stop_flag && *stop_flag) return;
-  __shared__ double red[80];
-  if (threadIdx.x < 40) {
-    const int c = threadIdx.x >> 3, ch = threadIdx.x & 7;
+  __shared__ double red[5][32][2];
+  const int c = threadIdx.x >> 5, ch = threadIdx.x & 31;  // 5 warps: norm c, chain ch
+  if (c < 5) {
     ScaledSq acc;
-    for (int b = ch; b < nb; b += 8) acc.merge(part[(b * 5 + c) * 2], part[(b * 5 + c) * 2 + 1]);
-    red[threadIdx.x * 2] = acc.scale;
-    red[threadIdx.x * 2 + 1] = acc.ssq;
+    for (int b0 = ch; b0 < nb; b0 += 4 * 32) {
+      double s2[4], q2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = b0 + u * 32;
+        s2[u] = b < nb ? part[(b * 5 + c) * 2] : 0.0;
+        q2[u] = b < nb ? part[(b * 5 + c) * 2 + 1] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc.merge(s2[u], q2[u]);
+    }
+    red[c][ch][0] = acc.scale;
+    red[c][ch][1] = acc.ssq;
   }
   __syncthreads();
   if (threadIdx.x < 5) {
     ScaledSq acc;
-    for (int ch = 0; ch < 8; ++ch)
-      acc.merge(red[(threadIdx.x * 8 + ch) * 2], red[(threadIdx.x * 8 + ch) * 2 + 1]);
+    for (int k = 0; k < 32; ++k) acc.merge(red[threadIdx.x][k][0], red[threadIdx.x][k][1]);
     out[threadIdx.x * 2] = acc.scale;
     out[threadIdx.x * 2 + 1] = acc.ssq;
   }
@@ -502,24 +534,30 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t npa
 // (solver.py:258-269), penalty adaptation (solver.py:272-292).
 // ---------------------------------------------------------------------------
 __global__ void finalize_kernel(FinalizeParams p) {
-  if (threadIdx.x != 0) return;
+  // thread (m, c) < 15 merges the shards' (scale, ssq) pairs of one norm in
+  // rank order; thread 0 then closes the iteration
+  __shared__ double nv[15];
   int* ctr = p.counters;
   if (ctr[1]) return;  // already stopped: iteration is a no-op
+  if (threadIdx.x < 15) {
+    ScaledSq a;
+    for (int q = 0; q < p.norm_parts; ++q) {
+      const double* s = p.norm_acc + (q * 15 + threadIdx.x) * 2;
+      a.merge(s[0], s[1]);
+    }
+    nv[threadIdx.x] = a.norm();
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   const int64_t it = ctr[0];
   double primal[3], dual[3];
   bool stop = true;
   for (int m = 0; m < 3; ++m) {
-    // merge the shards' (scale, ssq) pairs in rank order
-    ScaledSq a[5];
-    for (int q = 0; q < p.norm_parts; ++q)
-      for (int c = 0; c < 5; ++c) {
-        const double* s = p.norm_acc + ((q * 3 + m) * 5 + c) * 2;
-        a[c].merge(s[0], s[1]);
-      }
-    primal[m] = a[0].norm();
-    dual[m] = p.rho[m] * a[1].norm();
+    const double a[5] = {nv[m * 5], nv[m * 5 + 1], nv[m * 5 + 2], nv[m * 5 + 3], nv[m * 5 + 4]};
+    primal[m] = a[0];
+    dual[m] = p.rho[m] * a[1];
     const double base = sqrt(static_cast<double>(p.dims[m]) * p.R) * p.eps_abs;
-    const double fn = a[2].norm(), an = a[3].norm(), yn = a[4].norm();
+    const double fn = a[2], an = a[3], yn = a[4];
     const double pthr = base + p.eps_rel * (fn > an ? fn : an);
     const double dthr = base + p.eps_rel * yn;
     if (primal[m] > pthr || dual[m] > dthr) stop = false;
@@ -723,13 +761,13 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
 cudaError_t gram_reduce_launch(const double* part, int nb, int R, double* G, const int* stop_flag,
                                cudaStream_t stream) {
   const int n = R * R;
-  gram_reduce_kernel<<<(n + 127) / 128, 128, 0, stream>>>(part, nb, n, G, stop_flag);
+  gram_reduce_kernel<<<(n + 31) / 32, 32 * kGramSub, 0, stream>>>(part, nb, n, G, stop_flag);
   return cudaGetLastError();
 }
 
 cudaError_t norm_reduce_launch(const double* part, int nb, double* out, const int* stop_flag,
                                cudaStream_t stream) {
-  norm_reduce_kernel<<<1, 64, 0, stream>>>(part, nb, out, stop_flag);
+  norm_reduce_kernel<<<1, 160, 0, stream>>>(part, nb, out, stop_flag);
   return cudaGetLastError();
 }
 
