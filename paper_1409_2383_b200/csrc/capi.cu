@@ -63,7 +63,7 @@ struct MttkrpOp {
   int splits() const { return tc ? tcl.splits : cc.groups; }
   // rows from tail_row0() on have splits_tail() partials (ragged last tile)
   int64_t tail_row0() const {
-    return tc && tcl.splits_tail ? static_cast<int64_t>(tcl.n_full) * 128 : INT64_MAX;
+    return tc && tcl.splits_tail ? static_cast<int64_t>(tcl.n_full) * tcl.tm : INT64_MAX;
   }
   int splits_tail() const { return tc ? tcl.splits_tail : 0; }
   size_t ws_bytes(int R) const {

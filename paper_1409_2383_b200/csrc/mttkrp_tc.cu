@@ -230,6 +230,7 @@ struct TcParams {
   int64_t M;
   int l_ext, n_o, n_lb, G;   // l extent, o extent, 64-wide l blocks, blocks per unit
   int n_full, splits, splits_tail;
+  int tm;                    // rows per m-tile (<= 128; MMA M is 128, rows >= tm ignored)
   int x_stages, h_stages;
   const double* f_hi;        // [n_o][R]
   const unsigned char* wsl;  // [n_lb][3][N][128 B] W slices of F_lo (w_slice_kernel)
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     split = blockIdx.x - p.n_full * p.splits;
     ub = p.ub_tail;
   }
-  const int64_t m0 = static_cast<int64_t>(tile) * kTM;
+  const int64_t m0 = static_cast<int64_t>(tile) * p.tm;
   const int u_begin = static_cast<int>(ub[split]);
   const int u_end = static_cast<int>(ub[split + 1]);
   const int n_o = p.n_o;
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
           if (p.debug & 16) {
             mbar_arrive(bar);
           } else {
-            mbar_arrive_expect_tx(bar, 2 * kXTile);
+            mbar_arrive_expect_tx(bar, p.mode == 3 ? 2 * kXTile : 2 * p.tm * kBK * 2);
             if (p.mode == 1) {
               tma_load_3d(d0, &p.tmap0, bar, l0, ui.o, mm);
               tma_load_3d(d1, &p.tmap1, bar, l0, ui.o, mm);
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     }
     // fp64 partial of this CTA: out = (hi + lo) * xs * 2^(f-t) * 2^e
     const int64_t gm = m0 + row;
-    if (gm < p.M) {
+    if (row < p.tm && gm < p.M) {
       double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * R;
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
@@ -806,8 +807,17 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   // costs a fixed pipeline share plus its rows' share of the bytes.  One SM
   // is left free so the mode's ridge Cholesky (side stream) runs concurrently.
   const int cap = std::min(sm_count_tc() - 1, kTcMaxSplits);
-  L.n_full = static_cast<int>(L.M / kTM);
-  const int tail = static_cast<int>(L.M % kTM);
+  // Modes 1/2 (K-major A, box height free): equal tiles of tm <= 128 rows,
+  // so every CTA streams the same bytes.  Mode 3 (MN-major A, 64-row boxes):
+  // 128-row tiles plus a ragged last tile.
+  if (mode != 3) {
+    const int64_t nt = (L.M + kTM - 1) / kTM;
+    L.tm = static_cast<int>((L.M + nt - 1) / nt);
+  } else {
+    L.tm = kTM;
+  }
+  L.n_full = static_cast<int>(L.M / L.tm);
+  const int tail = static_cast<int>(L.M % L.tm);
   double fixed = 1.0;  // measured: a ragged tile's l block costs about a full one
   if (const char* e = getenv("NTF_TC_TAILCOST")) fixed = atof(e);
   const double wt = tail ? fixed + (1.0 - fixed) * tail / static_cast<double>(kTM) : 0.0;
@@ -885,9 +895,9 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
   cuuint64_t gstr[2] = {static_cast<cuuint64_t>(K * 2), static_cast<cuuint64_t>(J * K * 2)};
   cuuint32_t box[3];
   if (L.mode == 1) {
-    box[0] = 64; box[1] = 1; box[2] = 128;
+    box[0] = 64; box[1] = 1; box[2] = static_cast<cuuint32_t>(L.tm);
   } else if (L.mode == 2) {
-    box[0] = 64; box[1] = 128; box[2] = 1;
+    box[0] = 64; box[1] = static_cast<cuuint32_t>(L.tm); box[2] = 1;
   } else {
     box[0] = 64; box[1] = 64; box[2] = 1;
   }
@@ -951,6 +961,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   p.n_full = L.n_full;
   p.splits = L.splits;
   p.splits_tail = L.splits_tail;
+  p.tm = L.tm;
   p.x_stages = L.x_stages;
   p.h_stages = L.h_stages;
   p.f_hi = Fhi;

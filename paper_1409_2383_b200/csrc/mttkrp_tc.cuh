@@ -32,6 +32,7 @@ struct MttkrpTCLaunch {
   int n_mtiles;
   int n_full, splits;       // full 128-row tiles and CTAs per full tile
   int splits_tail;          // CTAs of the ragged last tile (0: none)
+  int tm;                   // rows per m-tile
   int l_ext, n_o, n_lb;     // l extent, o extent, 64-wide l blocks
   int G, n_g;               // l blocks per unit (one TMEM drain), groups
   int threads, smem_bytes;
