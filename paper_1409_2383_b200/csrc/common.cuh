@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <utility>
 
 #include "../../include/ntf_b200.h"
 
@@ -108,6 +109,35 @@ inline cudaError_t dev_alloc(T** p, size_t bytes) {
 
 inline void dev_free(void* p) {
   if (p) cudaFreeAsync(p, 0);
+}
+
+// Programmatic dependent launch (PDL).  The main-stream chain of a mode
+// update (W slices -> MTTKRP -> row update -> ...) is launched with the
+// programmatic-serialization attribute: every kernel lets its dependent be
+// scheduled at once (pdl_trigger), and each kernel waits for its predecessor
+// (pdl_wait: full completion and memory visibility) only before touching
+// data that predecessor produced.  Prologues, TMEM allocation and the
+// predecessor-independent X stream then overlap the previous kernel.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Error/status flags written by kernels (host reads them back once per run).

@@ -31,8 +31,8 @@
 //   warp 0        TMA producer: S0/S1 tiles (128B-swizzled)
 //   warp 1        TMEM allocator + single-thread MMA issuer (tcgen05.mma)
 //   warp 2        F_hi rows of the coming units -> scaled fp32 pairs (smem ring)
-//   warps 3..     epilogue, 4 warps (8 for N >= 48, two column halves per TMEM
-//                 lane quarter).  At each group start it forms the W slices
+//   warps 3..     epilogue, 4, 8 or 16 warps (1, 2 or 4 column groups per
+//                 TMEM lane quarter, by N).  At each group start it forms the W slices
 //                 T0|T1|T2 of the group's F_lo rows (UMMA K-major SW128 layout);
 //                 per unit: tcgen05.ld, F_hi scaling, double-float
 //                 accumulation; finally the fp64 partial of the CTA.
@@ -53,7 +53,12 @@ constexpr int kTM = 128;     // MMA M (rows per tile, TMEM lanes)
 constexpr int kBK = 64;      // l per block (fp16: 128 B rows, one SW128 atom)
 constexpr int kUK = 16;      // MMA K for kind::f16
 constexpr int kFMin = -990;  // exponent clamp of the column scales (2^(7+22-kFMin) finite)
-__host__ __device__ constexpr int epi_warps(int NT) { return NT >= 3 ? 8 : 4; }
+// epilogue warps: 1, 2 or 4 per TMEM lane quarter (column groups), keeping
+// the double-float accumulators (2 x N / groups per thread) in registers
+// (the per-thread column count N*4/warps must be a multiple of 8)
+__host__ __device__ constexpr int epi_warps(int NT) {
+  return NT <= 2 ? 4 : ((NT == 6 || NT == 8) ? 16 : 8);
+}
 // warps: 0 X TMA, 1 MMA, 2 F_hi rows, epilogue (which also forms W)
 __host__ __device__ constexpr int tc_threads(int NT) { return (3 + epi_warps(NT)) * 32; }
 
@@ -183,6 +188,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 bits, 8 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int W>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[W]) {
+  if constexpr (W == 16) tmem_ld16(taddr, v);
+  else tmem_ld8(taddr, v);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
@@ -282,11 +305,15 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   constexpr int N = NT * 16;
   constexpr int kEpi = epi_warps(NT);
   constexpr int NC = N * 4 / kEpi;         // columns per epilogue thread
+  // TMEM load width: 16 columns where it divides NC and registers allow
+  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : 8;
+  static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kXTile = kTM * kBK * 2;    // 16 KB per plane
   constexpr int kWlb = 3 * N * kBK * 2;    // T0|T1|T2 of one l block
   constexpr int kFirstEpi = 3;
   const uint64_t g_entry = gtimer();
+  pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1 KB alignment by offset (keeps the pointer in the shared address space)
@@ -305,29 +332,10 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   uint64_t* acc_full = w_empty + 1;
   uint64_t* acc_empty = acc_full + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 4);
-  // per-column scales: [0,N) F_lo -> T scale 2^(t-f), [N,2N) F_hi -> unit
-  // range 2^-e, [2N,3N) output xs * 2^(f-t) * 2^e
+  // per-column scales, written by warp 2 after pdl_wait (see there)
   double* wsc = reinterpret_cast<double*>(acc_empty + 6);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && p.cm_self && threadIdx.x < R) p.cm_self[threadIdx.x] = 0.0;
-  if (threadIdx.x < N) {
-    const int n = threadIdx.x;
-    const int t = G >= 4 ? 5 : (G >= 2 ? 6 : 7);
-    int f = 0, e = 0;
-    const double cl = n < R ? p.cm_lo[n] : 0.0, ch = n < R ? p.cm_hi[n] : 0.0;
-    if (cl > 0.0) frexp(cl, &f);  // cl < 2^f
-    if (ch > 0.0) frexp(ch, &e);
-    // columns decayed to ~1e-300 (large penalties shrink factor columns
-    // geometrically) must not overflow the scales (2^(t+22-f) in the slice
-    // kernel): clamp, identically there (kFMin)
-    f = max(f, kFMin);
-    e = max(e, kFMin);
-    wsc[n] = ldexp(1.0, t - f);
-    wsc[N + n] = ldexp(1.0, -e);
-    wsc[2 * N + n] = *p.xscale * ldexp(1.0, f - t + e);
-  }
-
   // this CTA's tile and unit range
   int tile, split;
   const uint32_t* ub;
@@ -424,8 +432,12 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     //   cols [0, 3N) (=|+=) S0 * [T0 | T1 | T2]     cols [N, 3N) += S1 * [T0 | T1]
     // Warp-uniform loop; one elected lane issues the MMAs and commits.
     const bool mn = p.mode == 3;
-    const uint32_t idesc3 = make_idesc(3 * N, mn);
+    // N' <= 256 per MMA: for N > 85 the first MMA is split into S0*[T0|T1]
+    // and S0*T2 (the S0 tile is then read twice)
+    constexpr bool kSplit = 3 * N > 256;
+    const uint32_t idesc3 = make_idesc(kSplit ? 2 * N : 3 * N, mn);
     const uint32_t idesc2 = make_idesc(2 * N, mn);
+    const uint32_t idesc1 = make_idesc(N, mn);
     // descriptors of stage 0 / l-block 0; stages are 32 KB apart, l blocks
     // kWlb apart (both multiples of 16 B: added to the address field)
     const uint64_t da_base = mn ? smem_desc(xbase, kXTile / 2, 1024) : smem_desc(xbase, 16, 1024);
@@ -460,7 +472,11 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
           if (!(p.debug & 2)) {
 #pragma unroll
             for (int kk = 0; kk < kBK / kUK; ++kk) {
-              tc_mma_f16(d0, da0 + kk * a_kstep, db + kk * (32 >> 4), idesc3, (j | kk) ? 1u : 0u);
+              const uint32_t first = (j | kk) ? 1u : 0u;
+              tc_mma_f16(d0, da0 + kk * a_kstep, db + kk * (32 >> 4), idesc3, first);
+              if constexpr (kSplit)  // S0*T2 into ACC2 (B rows [2N, 3N))
+                tc_mma_f16(d0 + 2 * N, da0 + kk * a_kstep,
+                           db + kk * (32 >> 4) + static_cast<uint64_t>((2 * N * 128) >> 4), idesc1, first);
               tc_mma_f16(d1, da1 + kk * a_kstep, db + kk * (32 >> 4), idesc2, 1u);
             }
           }
@@ -480,6 +496,28 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     }
   } else if (warp == 2) {
     // ---------- W slices of each group (bulk copy) + F_hi rows -> fp32 pairs ---------
+    // Everything from here on reads what the preceding kernels produced.
+    pdl_wait();
+    // per-column scales: [N,2N) F_hi -> unit range 2^-e, [2N,3N) output
+    // xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f, max|F_hi[:,n]| < 2^e
+    for (int n = lane; n < N; n += 32) {
+      const int t = G >= 4 ? 5 : (G >= 2 ? 6 : 7);
+      int f = 0, e = 0;
+      const double cl = n < R ? p.cm_lo[n] : 0.0, ch = n < R ? p.cm_hi[n] : 0.0;
+      if (cl > 0.0) frexp(cl, &f);
+      if (ch > 0.0) frexp(ch, &e);
+      // columns decayed to ~1e-300 (large penalties shrink factor columns
+      // geometrically) must not overflow the scales (2^(t+22-f) in the slice
+      // kernel): clamp, identically there (kFMin)
+      f = max(f, kFMin);
+      e = max(e, kFMin);
+      wsc[N + n] = ldexp(1.0, -e);
+      wsc[2 * N + n] = *p.xscale * ldexp(1.0, f - t + e);
+    }
+    // this mode's column maxima are re-accumulated by the row update that follows
+    if (blockIdx.x == 0 && p.cm_self)
+      for (int n = lane; n < R; n += 32) p.cm_self[n] = 0.0;
+    __syncwarp();
     Ring hr;
     UnitIt ui = u0;
     int seg = 0;
@@ -527,21 +565,21 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       const float2* hs = hbase + hr.idx * N + c0;
       if (!(p.debug & 4)) {
 #pragma unroll
-        for (int j = 0; j < NC / 16; ++j) {
-          float a0[16], a1[16], a2[16];
-          tmem_ld16(taddr + j * 16, a0);           // ACC0: S0*T0 (exact integers)
-          tmem_ld16(taddr + N + j * 16, a1);       // ACC1: S0*T1 + S1*T0
-          tmem_ld16(taddr + 2 * N + j * 16, a2);   // ACC2: S0*T2 + S1*T1
+        for (int j = 0; j < NC / LW; ++j) {
+          float a0[LW], a1[LW], a2[LW];
+          tmem_ld<LW>(taddr + j * LW, a0);           // ACC0: S0*T0 (exact integers)
+          tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*T0
+          tmem_ld<LW>(taddr + 2 * N + j * LW, a2);   // ACC2: S0*T2 + S1*T1
           tmem_wait_ld();
 #pragma unroll
-          for (int v = 0; v < 16; ++v) {
-            const float2 h = hs[j * 16 + v];
+          for (int v = 0; v < LW; ++v) {
+            const float2 h = hs[j * LW + v];
             const float a = a0[v];
             const float pr = a * h.x;
             const float er = fmaf(a, h.x, -pr);    // a*h.x = pr + er exactly
             const float cr = fmaf(a1[v] + a2[v], h.x, fmaf(a, h.y, er));
-            two_sum(hi[j * 16 + v], lo[j * 16 + v], pr);
-            lo[j * 16 + v] += cr;
+            two_sum(hi[j * LW + v], lo[j * LW + v], pr);
+            lo[j * LW + v] += cr;
           }
         }
       }
@@ -591,6 +629,8 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
 __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int n_lb,
                                const double* __restrict__ cm, int t, unsigned char* __restrict__ wsl,
                                const int* stop_flag) {
+  pdl_trigger();
+  pdl_wait();  // F_lo and its column maxima come from the preceding row update
   if (stop_flag && *stop_flag) return;
   const int total = n_lb * N * (kBK / 8);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -703,8 +743,8 @@ template <int NT>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
   auto kern = mttkrp_tc_kernel<NT>;
   if (prep) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
-  kern<<<L.n_full * L.splits + L.splits_tail, L.threads, L.smem_bytes, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(L.n_full * L.splits + L.splits_tail), dim3(L.threads), L.smem_bytes,
+                    stream, p);
 }
 
 cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
@@ -713,6 +753,10 @@ cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
     case 2: return launch_nt<2>(p, L, stream, prep);
     case 3: return launch_nt<3>(p, L, stream, prep);
     case 4: return launch_nt<4>(p, L, stream, prep);
+    case 5: return launch_nt<5>(p, L, stream, prep);
+    case 6: return launch_nt<6>(p, L, stream, prep);
+    case 7: return launch_nt<7>(p, L, stream, prep);
+    case 8: return launch_nt<8>(p, L, stream, prep);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -739,7 +783,7 @@ void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
 // host API
 // ----------------------------------------------------------------------------
 bool mttkrp_tc_supported(int x_dtype, int R) {
-  return x_dtype == NTF_F32 && R >= 1 && R <= 64;
+  return x_dtype == NTF_F32 && R >= 1 && R <= 128;
 }
 
 bool mttkrp_tc_auto(int x_dtype, int R) {
@@ -998,11 +1042,11 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     const int t = L.G >= 4 ? 5 : (L.G >= 2 ? 6 : 7);
     const int total = L.n_lb * L.N * (kBK / 8);
     const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
-    if (!(p.debug & 128))
-    w_slice_kernel<<<blocks, 64, 0, stream>>>(Flo, L.l_ext, L.R, L.N, L.n_lb, p.cm_lo, t, L.wsl,
-                                               stop_flag);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (!(p.debug & 128)) {
+      cudaError_t e = launch_pdl(w_slice_kernel, dim3(blocks), dim3(64), 0, stream, Flo, L.l_ext,
+                                 L.R, L.N, L.n_lb, p.cm_lo, t, L.wsl, stop_flag);
+      if (e != cudaSuccess) return e;
+    }
   }
   return dispatch_tc(p, L, stream, false);
 }

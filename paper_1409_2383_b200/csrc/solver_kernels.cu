@@ -297,6 +297,7 @@ __device__ void block_partials(const FactorUpdateParams& p, ScaledSq (&nrm)[5], 
 // on the critical path.  Agreement with cho_solve (solver.py:188) is at the
 // backward-error level.
 __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorUpdateParams p) {
+  pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
@@ -326,6 +327,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
     dl[e] = e < cnt ? p.dual[base + e] : 0.0;
   }
   const double rho = p.rho[p.mode - 1];
+  pdl_wait();  // the MTTKRP partials (and every later write) follow the preceding kernel
   split_sum(p, base, cnt, npm, ms, scr);
   for (int e = threadIdx.x; e < npm; e += blockDim.x)
     yb[e] = e < cnt ? (ms[e] + rho * ax[e]) - dl[e] : 0.0;  // ridge_rhs (solver.py:178-179)
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
 // R > 64: one row per warp, forward/backward substitution against L.
 template <int RT>
 __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorUpdateParams p) {
+  pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
@@ -398,6 +401,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
   const double rho = p.rho[p.mode - 1];
+  pdl_wait();
   split_sum(p, base, cnt, npm, ms, scr);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   ScaledSq nrm[5];
@@ -467,6 +471,8 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int nb, int 
 // the chains merged in order.
 __global__ void norm_reduce_kernel(const double* __restrict__ part, int nb, double* __restrict__ out,
                                    const int* stop_flag) {
+  pdl_trigger();
+  pdl_wait();
   if (stop_flag && *stop_flag) return;
   __shared__ double red[5][32][2];
   const int c = threadIdx.x >> 5, ch = threadIdx.x & 31;  // 5 warps: norm c, chain ch
@@ -749,13 +755,10 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
   p.debug = dbg;
   const int blocks = factor_update_blocks(p.rows, p.R);
   const size_t smem = factor_update_smem(p.R);
-  if (p.R <= 64)
-    factor_update_gemv_kernel<<<blocks, kUpdThreads, smem, stream>>>(p);
-  else if (p.R <= 96)
-    factor_update_warp_kernel<3><<<blocks, kUpdThreads, smem, stream>>>(p);
-  else
-    factor_update_warp_kernel<4><<<blocks, kUpdThreads, smem, stream>>>(p);
-  return cudaGetLastError();
+  if (p.R <= 64) return launch_pdl(factor_update_gemv_kernel, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
+  if (p.R <= 96)
+    return launch_pdl(factor_update_warp_kernel<3>, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
+  return launch_pdl(factor_update_warp_kernel<4>, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
 }
 
 cudaError_t gram_reduce_launch(const double* part, int nb, int R, double* G, const int* stop_flag,
@@ -767,8 +770,7 @@ cudaError_t gram_reduce_launch(const double* part, int nb, int R, double* G, con
 
 cudaError_t norm_reduce_launch(const double* part, int nb, double* out, const int* stop_flag,
                                cudaStream_t stream) {
-  norm_reduce_kernel<<<1, 160, 0, stream>>>(part, nb, out, stop_flag);
-  return cudaGetLastError();
+  return launch_pdl(norm_reduce_kernel, dim3(1), dim3(160), 0, stream, part, nb, out, stop_flag);
 }
 
 size_t gram_workspace_bytes(int64_t rows, int R) {

@@ -72,6 +72,23 @@ def test_mttkrp_fp32_accuracy(dims, R):
         assert rel(got, O.mttkrp(t, f, mode)) <= 2e-8
 
 
+@pytest.mark.parametrize("dims,R", [((96, 80, 72), 1), ((130, 40, 64), 7), ((260, 200, 136), 20),
+                                    ((70, 300, 48), 33), ((129, 129, 200), 50), ((64, 64, 64), 64),
+                                    ((150, 90, 112), 100), ((40, 50, 64), 128)])
+def test_mttkrp_tcgen05_accuracy(dims, R):
+    """Tensor-core engine (fp32 X, exact fixed-point slicing) against the fp64
+    oracle on the same fp32 values, every mode, all accumulator widths
+    (N = 16..128: single and split first MMA, 4/8/16 epilogue warps), equal
+    and ragged m-tiles (K % 8 == 0 is the engine's TMA stride requirement)."""
+    rng = np.random.default_rng(11)
+    x32 = rng.random(dims).astype(np.float32)
+    f = _factors(rng, dims, R)
+    t = O.OracleTensor(x32.astype(np.float64))
+    for mode in (1, 2, 3):
+        got = P.mttkrp_factors(P.DenseTensor(x32), f, mode, engine="tcgen05")
+        assert rel(got, O.mttkrp(t, f, mode)) <= 5e-9, (mode, rel(got, O.mttkrp(t, f, mode)))
+
+
 @pytest.mark.parametrize("engine,tol", [("cuda_core", 1e-9), ("tcgen05", 5e-9)])
 def test_mttkrp_mode_consistency_c2_full_size(engine, tol):
     """Size-independent property at BASELINE c2 size: for every column r,

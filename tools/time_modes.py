@@ -10,7 +10,11 @@ from paper_1409_2383_b200.engine import DeviceProblem
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 eng = sys.argv[2] if len(sys.argv) > 2 else "auto"
-w = synth.CONFIGS[cfgname]
+if cfgname == "custom":  # time_modes.py custom ENGINE I J K R INNER
+    I, J, K, R, inner = (int(v) for v in sys.argv[3:8])
+    w = synth.Workload("custom", (I, J, K), R, "float32", 20.0, inner, 1)
+else:
+    w = synth.CONFIGS[cfgname]
 dt = torch.float32 if w.dtype == "float32" else torch.float64
 x = torch.rand(w.dims, dtype=dt, device="cuda")
 cfg = P.SolverConfig(seed=1, eps_abs=0, eps_rel=0, n_max=4, max_restarts=0, inner_sweeps=w.inner)
