@@ -83,8 +83,9 @@ MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, 
 
 cudaError_t run_op(MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
-                   const int* stop, cudaStream_t s, const double* colmax3 = nullptr) {
-  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s);
+                   const int* stop, cudaStream_t s, const double* colmax3 = nullptr,
+                   const ntf::TcRidge* ridge = nullptr) {
+  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s, ridge);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
 }
 
@@ -105,6 +106,11 @@ struct ntf_plan {
   double* gram_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][R][R] per mode
   double* gram_ws = nullptr;
   bool any_tc = false;
+  // all three MTTKRPs on the tensor cores: the ridge factorisation (and the
+  // Gram reduction feeding it) runs in one extra CTA of each MTTKRP, so a
+  // mode update is a pure PDL chain on one stream
+  bool fused_ridge = false;
+  int* gram_pending = nullptr;  // [3] device flags
   cudaStream_t capture_stream = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [timing]: plain / with timing events
   // ridge factorisation runs on a side stream concurrently with the MTTKRP
@@ -137,6 +143,8 @@ cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
   return cudaEventRecord(ev, s);
 }
 
+int enqueue_row_update(ntf_plan* pl, int mode, int last, cudaStream_t s, cudaEvent_t* ev);
+
 int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   const ntf_plan_desc& d = pl->d;
   const int m = mode - 1;
@@ -144,6 +152,30 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   const int64_t* xd = d.x_dims[m];
   // companions, highest mode first (solver.py:196-204)
   static const int comp[3][2] = {{2, 1}, {2, 0}, {1, 0}};
+  if (pl->fused_ridge) {
+    const int prev = (m + 2) % 3;  // the factor updated just before this mode
+    ntf::TcRidge rg{};
+    rg.f_prev = d.factors[prev];
+    rg.rows_prev = d.dims[prev];
+    rg.gram_prev = d.grams[prev];
+    rg.gram_pending = pl->gram_pending + prev;
+    rg.Ga = d.grams[comp[m][0]];
+    rg.Gb = d.grams[comp[m][1]];
+    rg.rho = d.rho + m;
+    rg.out = pl->ridge;
+    rg.status = d.counters + 2;
+    cudaEvent_t* ev = nullptr;
+    if (pl->timing && pl->events) {
+      ev = pl->events + 3 * pl->cursor;
+      pl->cursor = (pl->cursor + 1) % (pl->n_events / 3);
+      NTF_CUDA_TRY(record_event(ev[0], s));
+    }
+    NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2],
+                        d.factors[0], d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s,
+                        d.colmax, &rg));
+    if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
+    return enqueue_row_update(pl, mode, last, s, ev);
+  }
   // fork: ridge Cholesky (solver.py:167-175) on the side stream
   ntf::RidgeParams rp{};
   rp.mode = mode;
@@ -168,6 +200,15 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
                       d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s, d.colmax));
   if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
   NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
+  return enqueue_row_update(pl, mode, last, s, ev);
+}
+
+// Row update of one mode (+ Gram reduction off the critical path, + norm
+// reduction in the last sweep), after its MTTKRP and ridge factor.
+int enqueue_row_update(ntf_plan* pl, int mode, int last, cudaStream_t s, cudaEvent_t* ev) {
+  const ntf_plan_desc& d = pl->d;
+  const int m = mode - 1;
+  const int R = d.rank;
   ntf::FactorUpdateParams fp{};
   fp.mode = mode;
   fp.R = R;
@@ -185,15 +226,17 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   fp.last_sweep = last;
   fp.fuse_gram = d.fuse_gram;
   fp.norm_partials = pl->norm_partials[m];
-  fp.gram_partials = pl->gram_partials[m];
+  fp.gram_partials = pl->fused_ridge ? nullptr : pl->gram_partials[m];
   // column maxima feed the tensor-core MTTKRPs only (zeroed by this mode's
   // MTTKRP, re-accumulated here)
   fp.colmax_bits = pl->any_tc ? reinterpret_cast<unsigned long long*>(d.colmax + m * R) : nullptr;
+  fp.gram_pending = pl->fused_ridge ? pl->gram_pending + m : nullptr;
+  fp.ridge_in_pred = pl->fused_ridge ? 1 : 0;
   fp.status = d.counters + 2;
   fp.stop_flag = d.counters + 1;
   NTF_CUDA_TRY(ntf::factor_update_launch(fp, s));
   if (ev) NTF_CUDA_TRY(record_event(ev[2], s));
-  if (d.fuse_gram) {  // G_m for the coming ridges, off the critical path
+  if (d.fuse_gram && !pl->fused_ridge) {  // G_m for the coming ridges, off the critical path
     NTF_CUDA_TRY(cudaEventRecord(pl->post_ev, s));
     NTF_CUDA_TRY(cudaStreamWaitEvent(pl->side, pl->post_ev, 0));
     NTF_CUDA_TRY(ntf::gram_reduce_launch(pl->gram_partials[m], pl->blocks[m], R, d.grams[m],
@@ -207,6 +250,7 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
 
 // main stream waits for the side stream's queued work (Gram reductions)
 int join_side(ntf_plan* pl, cudaStream_t s) {
+  if (pl->fused_ridge) return NTF_OK;  // nothing runs on the side stream
   NTF_CUDA_TRY(cudaEventRecord(pl->join_ev, pl->side));
   NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
   return NTF_OK;
@@ -406,6 +450,17 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   // Tensor-core engine: split each distinct slab once into its fp16 planes
   // (one-time setup; synchronous so the caller's upload stream is irrelevant).
   for (int m = 0; m < 3; ++m) pl->any_tc = pl->any_tc || pl->op[m].tc;
+  // Opt-in (NTF_B200_FUSED_RIDGE=1): measured slower at c2 today, where the
+  // single-CTA ridge (~30 us, serial fp64 divisions) outlasts the streaming
+  // CTAs; the side-stream ridge hides it on the 148th SM instead.
+  {
+    const char* env = getenv("NTF_B200_FUSED_RIDGE");
+    pl->fused_ridge = env && env[0] == '1' && pl->op[0].tc && pl->op[1].tc && pl->op[2].tc;
+  }
+  if ((e = ntf::dev_alloc(&pl->gram_pending, sizeof(int) * 3)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc flags"));
+  if ((e = cudaMemset(pl->gram_pending, 0, sizeof(int) * 3)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMemset flags"));
   if (pl->any_tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
     for (int m = 0; m < 3; ++m) {
@@ -436,6 +491,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
 int ntf_plan_sync_grams(ntf_plan* pl, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pl->gram_pending) NTF_CUDA_TRY(cudaMemsetAsync(pl->gram_pending, 0, sizeof(int) * 3, s));
   for (int m = 0; m < 3; ++m) {
     NTF_CUDA_TRY(ntf::gram_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank, pl->d.grams[m],
                                   pl->gram_ws, s));
@@ -568,6 +624,7 @@ void ntf_plan_destroy(ntf_plan* pl) {
     ntf::dev_free(pl->gram_partials[m]);
   }
   ntf::dev_free(pl->gram_ws);
+  ntf::dev_free(pl->gram_pending);
   delete pl;
 }
 

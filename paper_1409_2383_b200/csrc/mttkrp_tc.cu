@@ -44,6 +44,7 @@
 #include <cstdlib>
 
 #include "mttkrp_tc.cuh"
+#include "ridge.cuh"
 
 namespace ntf {
 
@@ -266,6 +267,7 @@ struct TcParams {
   const int* stop_flag;
   int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip W forming,
                              // 2 skip MMA, 4 skip TMEM drain, 16 skip X TMA
+  TcRidge ridge;              // extra CTA (gridDim.x - 1) when ridge.out != NULL
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
   uint32_t ub_tail[kTcMaxSplits + 1];  // ... of the ragged last tile
 };
@@ -316,6 +318,19 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (p.ridge.out && blockIdx.x == gridDim.x - 1) {
+    // ----------------- ridge CTA (concurrent with the streaming CTAs) -----------------
+    pdl_wait();  // the previous row update's Gram partials / grams / rho
+    if (*p.ridge.gram_pending) {  // G of the factor updated just before this mode
+      gram_from_rows_block(p.ridge.f_prev, p.ridge.rows_prev, p.R, p.ridge.gram_prev,
+                           reinterpret_cast<double*>(smem_raw));
+      __syncthreads();
+      if (threadIdx.x == 0) *p.ridge.gram_pending = 0;
+    }
+    ridge_factor_block(p.ridge.Ga, p.ridge.Gb, *p.ridge.rho, p.R, p.ridge.out, p.ridge.status,
+                       reinterpret_cast<double*>(smem_raw));
+    return;
+  }
   // 1 KB alignment by offset (keeps the pointer in the shared address space)
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int SX = p.x_stages, SH = p.h_stages, G = p.G;
@@ -743,8 +758,9 @@ template <int NT>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
   auto kern = mttkrp_tc_kernel<NT>;
   if (prep) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
-  return launch_pdl(kern, dim3(L.n_full * L.splits + L.splits_tail), dim3(L.threads), L.smem_bytes,
-                    stream, p);
+  const int extra = p.ridge.out ? 1 : 0;
+  return launch_pdl(kern, dim3(L.n_full * L.splits + L.splits_tail + extra), dim3(L.threads),
+                    L.smem_bytes, stream, p);
 }
 
 cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
@@ -841,7 +857,8 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.x_stages = 6;
   if (const char* e = getenv("NTF_TC_XSTAGES")) L.x_stages = atoi(e);
   while (total(L.G, L.x_stages) > limit && L.x_stages > 2) --L.x_stages;
-  L.smem_bytes = total(L.G, L.x_stages);
+  L.smem_bytes = std::max<int>(total(L.G, L.x_stages),
+                               1024 + ridge_smem_doubles(R) * static_cast<int>(sizeof(double)));
   L.tmem_cols = static_cast<int>(tmem_cols(L.N));
   L.n_g = (L.n_lb + L.G - 1) / L.G;
   const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
@@ -980,7 +997,7 @@ cudaError_t colmax_launch(const double* F, int64_t rows, int R, double* out, cud
 
 cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
                              const double* B, const double* C, const double* colmax3, double* ws,
-                             const int* stop_flag, cudaStream_t stream) {
+                             const int* stop_flag, cudaStream_t stream, const TcRidge* ridge) {
   if (!L.bound) return cudaErrorInvalidValue;
   const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
   const double *Fhi, *Flo;
@@ -1010,6 +1027,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   p.h_stages = L.h_stages;
   p.f_hi = Fhi;
   p.wsl = L.wsl;
+  if (ridge) p.ridge = *ridge;
   p.ws = ws;
   p.stop_flag = stop_flag;
   for (int i = 0; i <= kTcMaxSplits; ++i) {

@@ -55,10 +55,27 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L);
 // Encode the tensor maps of the split planes and allocate the scale buffer.
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t);
 void mttkrp_tc_unbind(MttkrpTCLaunch& L);
+// Optional ridge work done by one extra CTA of the MTTKRP grid, concurrently
+// with the streaming CTAs: recompute the Gram of the most recently updated
+// factor (when *gram_pending), then factor H = Ga o Gb + rho I into `out`
+// (ridge.cuh layout) for the row update that follows.
+struct TcRidge {
+  const double* f_prev;     // factor updated just before this mode (rows x R)
+  int64_t rows_prev;
+  double* gram_prev;        // its Gram (R x R), recomputed when pending
+  int* gram_pending;        // device flag, cleared after the reduction
+  const double* Ga;         // companion Grams (highest mode first)
+  const double* Gb;
+  const double* rho;        // device scalar rho[mode - 1]
+  double* out;              // ridge buffer
+  int* status;              // NOT_PD
+};
+
 // colmax3: [3][R] per-factor column maxima of |F| (NULL: computed here)
 cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
                              const double* B, const double* C, const double* colmax3, double* ws,
-                             const int* stop_flag, cudaStream_t stream);
+                             const int* stop_flag, cudaStream_t stream,
+                             const TcRidge* ridge = nullptr);
 // out[r] = max_i |F[i][r]|
 cudaError_t colmax_launch(const double* F, int64_t rows, int R, double* out, cudaStream_t stream);
 

@@ -1,0 +1,163 @@
+// Ridge factorisation shared by ridge_factor_kernel (side stream, CUDA-core
+// engine) and the extra CTA of the tensor-core MTTKRP.
+#pragma once
+
+#include "common.cuh"
+
+namespace ntf {
+
+// ---------------------------------------------------------------------------
+// Ridge Cholesky in shared memory (solver.ridge_cholesky, solver.py:167-175):
+// H = G_a o G_b + rho*I (companion Gram, solver.py:196-204), lower factor
+// L with L L^T = H.  Right-looking, one barrier per column: the trailing
+// update uses the unscaled column (L[i][j] L[k][j] / pivot) and columns are
+// scaled at the end.  A non-positive or non-finite pivot raises NOT_PD.
+// ---------------------------------------------------------------------------
+__device__ inline void build_and_factor(double* L, int ldl, int R, const double* __restrict__ Ga,
+                                        const double* __restrict__ Gb, double rho, int* status,
+                                        bool* bad) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    double h = Ga[e] * Gb[e];
+    if (i == k) h += rho;
+    L[i * ldl + k] = h;
+  }
+  __syncthreads();
+  for (int j = 0; j < R; ++j) {
+    const double piv = L[j * ldl + j];
+    if (!(piv > 0.0) || !isfinite(piv)) {
+      if (tid == 0) {
+        raise_status(status, kDevNotPD);
+        *bad = true;
+      }
+      __syncthreads();
+      return;
+    }
+    const double inv = 1.0 / piv;
+    const int n = R - j - 1;  // trailing order; update the lower triangle i >= k > j
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int ii = e / n, kk = e - (e / n) * n;
+      if (kk > ii) continue;
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j] * inv;
+    }
+    __syncthreads();
+  }
+  // scale: L[i][j] = U[i][j] / sqrt(U[j][j]) for i > j, L[j][j] = sqrt(U[j][j])
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    if (k < i) L[i * ldl + k] = L[i * ldl + k] / sqrt(L[k * ldl + k]);
+  }
+  __syncthreads();
+  for (int j = tid; j < R; j += blockDim.x) L[j * ldl + j] = sqrt(L[j * ldl + j]);
+  __syncthreads();
+}
+
+// Ridge buffer (out), written by one block with smem >= ridge_smem_doubles(R):
+//   [0, R*R)            L, row-major lower Cholesky factor of H
+//   [R*R, R*R+R)        1 / diag(L)
+//   [R*R+R, 2R*R+R)     H^-1 = L^-T L^-1  (R <= 64 only)
+//   [2R*R+R, 3R*R+R)    H = G_a o G_b + rho I
+__host__ __device__ inline int ridge_smem_doubles(int R) {
+  const int fact = (R <= 64 ? 2 : 1) * R * (R + 1) + R;
+  const int gram = R * R + 32 * R;  // gram_from_rows_block
+  return fact > gram ? fact : gram;
+}
+
+__device__ inline void ridge_factor_block(const double* Ga, const double* Gb, double rho, int R,
+                                          double* out, int* status, double* sm) {
+  const int ldl = R + 1;
+  double* L = sm;
+  double* Li = L + R * ldl;  // L^-1 (lower), R <= 64
+  __shared__ bool bad;
+  if (threadIdx.x == 0) bad = false;
+  __syncthreads();
+  double* Hout = out + 2 * R * R + R;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    Hout[e] = Ga[e] * Gb[e] + (i == k ? rho : 0.0);
+  }
+  build_and_factor(L, ldl, R, Ga, Gb, rho, status, &bad);
+  if (bad) return;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, k = e - (e / R) * R;
+    out[e] = k <= i ? L[i * ldl + k] : 0.0;
+  }
+  double* rdiag = Li + R * ldl;  // [R] 1/L[i][i] (R <= 64 path)
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    const double r = 1.0 / L[j * ldl + j];
+    out[R * R + j] = r;
+    if (R <= 64) rdiag[j] = r;
+  }
+  if (R > 64) return;
+  __syncthreads();
+  // L^-1 by forward substitution on the identity, one column per thread
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    for (int i = 0; i < R; ++i) {
+      double s = i == j ? 1.0 : 0.0;
+      if (i < j) {
+        Li[i * ldl + j] = 0.0;
+        continue;
+      }
+      for (int k = j; k < i; ++k) s -= L[i * ldl + k] * Li[k * ldl + j];
+      Li[i * ldl + j] = s * rdiag[i];
+    }
+  }
+  __syncthreads();
+  // H^-1 = L^-T L^-1: (a, b) = sum_{i >= max(a,b)} Li[i][a] Li[i][b]
+  double* Hinv = out + R * R + R;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e - (e / R) * R;
+    double s = 0.0;
+    for (int i = a > b ? a : b; i < R; ++i) s += Li[i * ldl + a] * Li[i * ldl + b];
+    Hinv[e] = s;
+  }
+}
+
+// G = F^T F (R x R) of a row-major factor by one block, rows streamed through
+// shared memory in chunks, fixed order (row-sequential sums; every element
+// has one owning thread), mirrored so G is exactly symmetric.  sm: >= R*R +
+// 32*R doubles.
+__device__ inline void gram_from_rows_block(const double* __restrict__ F, int64_t rows, int R,
+                                            double* __restrict__ G, double* sm) {
+  constexpr int kChunk = 32;
+  double* Gs = sm;                // [R][R] accumulators (upper triangle used)
+  double* Fs = sm + R * R;        // [kChunk][R]
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = 0.0;
+  for (int64_t r0 = 0; r0 < rows; r0 += kChunk) {
+    const int nr = static_cast<int>(rows - r0 < kChunk ? rows - r0 : kChunk);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * R; e += blockDim.x) Fs[e] = F[r0 * R + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int a = e / R, b = e - (e / R) * R;
+      if (b < a) continue;
+      double acc = Gs[e];
+      for (int i = 0; i < nr; ++i) acc = fma(Fs[i * R + a], Fs[i * R + b], acc);
+      Gs[e] = acc;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e - (e / R) * R;
+    G[e] = b >= a ? Gs[e] : Gs[b * R + a];
+  }
+}
+
+// G[e] = sum_b part[b][e] by one block, fixed order: each thread owns
+// elements e and sums all blocks with 8 independent loads in flight.
+__device__ inline void gram_reduce_block(const double* __restrict__ part, int nb, int n,
+                                         double* __restrict__ G) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b0 = 0; b0 < nb; b0 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + u < nb) a[u] += part[static_cast<int64_t>(b0 + u) * n + e];
+    }
+    G[e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  }
+}
+
+}  // namespace ntf

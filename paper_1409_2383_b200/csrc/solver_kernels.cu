@@ -4,6 +4,7 @@
 // atomicMax on IEEE bits, which is exact and order-free), so a fit is bitwise
 // run-to-run deterministic like the reference (blocks.py:130-140).
 #include "solver_kernels.cuh"
+#include "ridge.cuh"
 
 namespace ntf {
 
@@ -18,121 +19,15 @@ __host__ __device__ __forceinline__ int rows_per_block(int R) {
   return R <= 32 ? 4 : (R <= 64 ? 2 : 8);
 }
 
-// ---------------------------------------------------------------------------
-// Ridge Cholesky in shared memory (solver.ridge_cholesky, solver.py:167-175):
-// H = G_a o G_b + rho*I (companion Gram, solver.py:196-204), lower factor
-// L with L L^T = H.  Right-looking, one barrier per column: the trailing
-// update uses the unscaled column (L[i][j] L[k][j] / pivot) and columns are
-// scaled at the end.  A non-positive or non-finite pivot raises NOT_PD.
-// ---------------------------------------------------------------------------
-__device__ void build_and_factor(double* L, int ldl, int R, const double* __restrict__ Ga,
-                                 const double* __restrict__ Gb, double rho, int* status,
-                                 bool* bad) {
-  const int tid = threadIdx.x;
-  for (int e = tid; e < R * R; e += blockDim.x) {
-    const int i = e / R, k = e - (e / R) * R;
-    double h = Ga[e] * Gb[e];
-    if (i == k) h += rho;
-    L[i * ldl + k] = h;
-  }
-  __syncthreads();
-  for (int j = 0; j < R; ++j) {
-    const double piv = L[j * ldl + j];
-    if (!(piv > 0.0) || !isfinite(piv)) {
-      if (tid == 0) {
-        raise_status(status, kDevNotPD);
-        *bad = true;
-      }
-      __syncthreads();
-      return;
-    }
-    const double inv = 1.0 / piv;
-    const int n = R - j - 1;  // trailing order; update the lower triangle i >= k > j
-    for (int e = tid; e < n * n; e += blockDim.x) {
-      const int ii = e / n, kk = e - (e / n) * n;
-      if (kk > ii) continue;
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j] * inv;
-    }
-    __syncthreads();
-  }
-  // scale: L[i][j] = U[i][j] / sqrt(U[j][j]) for i > j, L[j][j] = sqrt(U[j][j])
-  for (int e = tid; e < R * R; e += blockDim.x) {
-    const int i = e / R, k = e - (e / R) * R;
-    if (k < i) L[i * ldl + k] = L[i * ldl + k] / sqrt(L[k * ldl + k]);
-  }
-  __syncthreads();
-  for (int j = tid; j < R; j += blockDim.x) L[j * ldl + j] = sqrt(L[j * ldl + j]);
-  __syncthreads();
-}
-
-// Fixed-order sum of n strided values with 8 independent load/add chains
-// (latency-bound reductions over L2-resident partials).  The combination
-// order is fixed, so results are bitwise reproducible.
-__device__ __forceinline__ double strided_sum(const double* __restrict__ p, int64_t n,
-                                              int64_t stride) {
-  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int64_t s = 0; s < n; s += 8) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)  // static indices: the chains stay in registers
-      if (s + u < n) a[u] += p[(s + u) * stride];
-  }
-  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-}
-
 // One block: H = G_a o G_b + rho I, Cholesky, then L (row-major R x R, lower)
-// and 1/diag(L) to global for the row-update kernel.  Runs concurrently with
-// the mode's MTTKRP (it only depends on the companion Grams and rho).
-// Output layout of the ridge buffer:
-//   [0, R*R)            L, row-major lower Cholesky factor of H
-//   [R*R, R*R+R)        1 / diag(L)
-//   [R*R+R, 2R*R+R)     H^-1 = L^-T L^-1  (R <= 64 only)
-//   [2R*R+R, 3R*R+R)    H = G_a o G_b + rho I
+// and 1/diag(L) to global for the row-update kernel (ridge.cuh).  Runs on the
+// plan's side stream concurrently with the mode's CUDA-core MTTKRP; the
+// tensor-core MTTKRP runs the same code in one extra CTA.
 __global__ void ridge_factor_kernel(RidgeParams p) {
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int R = p.R;
-  const int ldl = R + 1;
-  double* L = reinterpret_cast<double*>(smem_raw);
-  double* Li = L + R * ldl;  // L^-1 (lower), R <= 64
-  __shared__ bool bad;
-  if (threadIdx.x == 0) bad = false;
-  __syncthreads();
-  const double rho = p.rho[p.mode - 1];
-  double* Hout = p.L + 2 * R * R + R;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, k = e - (e / R) * R;
-    Hout[e] = p.Ga[e] * p.Gb[e] + (i == k ? rho : 0.0);
-  }
-  build_and_factor(L, ldl, R, p.Ga, p.Gb, rho, p.status, &bad);
-  if (bad) return;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, k = e - (e / R) * R;
-    p.L[e] = k <= i ? L[i * ldl + k] : 0.0;
-  }
-  for (int j = threadIdx.x; j < R; j += blockDim.x) p.L[R * R + j] = 1.0 / L[j * ldl + j];
-  if (R > 64) return;
-  // L^-1 by forward substitution on the identity, one column per thread
-  for (int j = threadIdx.x; j < R; j += blockDim.x) {
-    for (int i = 0; i < R; ++i) {
-      double s = i == j ? 1.0 : 0.0;
-      if (i < j) {
-        Li[i * ldl + j] = 0.0;
-        continue;
-      }
-      for (int k = j; k < i; ++k) s -= L[i * ldl + k] * Li[k * ldl + j];
-      Li[i * ldl + j] = s / L[i * ldl + i];
-    }
-  }
-  __syncthreads();
-  // H^-1 = L^-T L^-1: (a, b) = sum_{i >= max(a,b)} Li[i][a] Li[i][b]
-  double* Hinv = p.L + R * R + R;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int a = e / R, b = e - (e / R) * R;
-    double s = 0.0;
-    for (int i = a > b ? a : b; i < R; ++i) s += Li[i * ldl + a] * Li[i * ldl + b];
-    Hinv[e] = s;
-  }
+  ridge_factor_block(p.Ga, p.Gb, p.rho[p.mode - 1], p.R, p.L, p.status,
+                     reinterpret_cast<double*>(smem_raw));
 }
 
 // Row solve of X (L L^T) = rhs for one row held by a warp: lane owns entries
@@ -270,10 +165,11 @@ __device__ void block_partials(const FactorUpdateParams& p, ScaledSq (&nrm)[5], 
     }
   }
   if (p.fuse_gram) {
-    // partial Gram of this block's rows (fixed row order), reduced by
-    // gram_reduce_kernel off the critical path
-    double* gp = p.gram_partials + static_cast<int64_t>(blockIdx.x) * R * R;
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    // G_m: recomputed from the new rows by the next MTTKRP's ridge CTA
+    // (gram_pending), or from per-block partials reduced on the side stream
+    if (p.gram_pending && blockIdx.x == 0 && threadIdx.x == 0) *p.gram_pending = 1;
+    double* gp = p.gram_partials ? p.gram_partials + static_cast<int64_t>(blockIdx.x) * R * R : nullptr;
+    for (int e = threadIdx.x; gp && e < R * R; e += blockDim.x) {
       const int r = e / R, c = e - (e / R) * R;
       double acc = 0.0;
       for (int lr = 0; lr < rpb; ++lr) acc += xr[lr * R + r] * xr[lr * R + c];
@@ -312,22 +208,33 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
   double* dl = ax + npm;                              // dual rows
   double* xr = dl + npm;                              // new rows
   double* scr = xr + npm;                             // [kUpdThreads] scratch
-  // Ridge factor from the concurrent ridge_factor_kernel (solver.py:167-175)
-  if (*p.status == kDevNotPD) return;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
-  // loads that do not depend on the MTTKRP first (all in flight together)
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    Hi[e] = p.Lg[R * R + R + e];
-    Hm[e] = p.Lg[2 * R * R + R + e];
-  }
+  // loads that do not depend on the preceding kernel first
   for (int e = threadIdx.x; e < npm; e += blockDim.x) {
     ax[e] = e < cnt ? p.aux[base + e] : 0.0;
     dl[e] = e < cnt ? p.dual[base + e] : 0.0;
   }
   const double rho = p.rho[p.mode - 1];
-  pdl_wait();  // the MTTKRP partials (and every later write) follow the preceding kernel
+  auto load_ridge = [&]() {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      Hi[e] = p.Lg[R * R + R + e];
+      Hm[e] = p.Lg[2 * R * R + R + e];
+    }
+  };
+  // The side-stream ridge is event-joined (complete): prefetch it.  The
+  // MTTKRP partials, a ridge computed by the preceding kernel, and every
+  // write below follow the preceding kernel.
+  if (!p.ridge_in_pred) {
+    if (*p.status == kDevNotPD) return;
+    load_ridge();
+  }
+  pdl_wait();
+  if (p.ridge_in_pred) {
+    if (*p.status == kDevNotPD) return;
+    load_ridge();
+  }
   split_sum(p, base, cnt, npm, ms, scr);
   for (int e = threadIdx.x; e < npm; e += blockDim.x)
     yb[e] = e < cnt ? (ms[e] + rho * ax[e]) - dl[e] : 0.0;  // ridge_rhs (solver.py:178-179)
@@ -391,17 +298,17 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   double* ms = inv_diag + R;       // [npm] MTTKRP row sums
   double* xr = ms + npm;           // [npm] new rows
   double* scr = xr + npm;          // [kUpdThreads]
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
+  const int64_t nM = p.rows * R;
+  const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
+  const double rho = p.rho[p.mode - 1];
+  pdl_wait();  // MTTKRP partials and ridge factor
   if (*p.status == kDevNotPD) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
     L[i * ldl + k] = p.Lg[e];
   }
   for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
-  const int64_t nM = p.rows * R;
-  const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
-  const double rho = p.rho[p.mode - 1];
-  pdl_wait();
   split_sum(p, base, cnt, npm, ms, scr);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   ScaledSq nrm[5];
@@ -720,9 +627,7 @@ size_t factor_update_smem(int R) {
   return n * sizeof(double);
 }
 
-size_t ridge_factor_smem(int R) {
-  return static_cast<size_t>(R <= 64 ? 2 : 1) * R * (R + 1) * sizeof(double);
-}
+size_t ridge_factor_smem(int R) { return static_cast<size_t>(ridge_smem_doubles(R)) * sizeof(double); }
 
 size_t ridge_buffer_doubles(int R) { return 3 * static_cast<size_t>(R) * R + R; }
 

@@ -26,6 +26,8 @@ struct FactorUpdateParams {
   double* norm_partials;    // [blocks][5][scale, ssq] (last sweep)
   double* gram_partials;    // [blocks][R][R] (fuse_gram)
   unsigned long long* colmax_bits;  // [R] running max |F[:, r]| as IEEE bits (fuse_gram)
+  int* gram_pending;        // set to 1 (fuse_gram): partials await the next MTTKRP's ridge CTA
+  int ridge_in_pred;        // 1: Lg comes from the preceding kernel (read after pdl_wait)
   int* status;
   const int* stop_flag;
   int debug;                // profiling only (NTF_UPD_DEBUG)
