@@ -327,7 +327,7 @@ int ntf_mttkrp(int mode, int x_dtype, const void* X, int64_t I, int64_t J, int64
     // (a solver plan does this once); synchronises before releasing them.
     ntf::TcTensor t;
     const int64_t dims[3] = {I, J, K};
-    NTF_CUDA_TRY(ntf::tc_tensor_create(static_cast<const float*>(X), dims, &t, s));
+    NTF_CUDA_TRY(ntf::tc_tensor_create(op.tcl, static_cast<const float*>(X), dims, &t, s));
     cudaError_t e = ntf::mttkrp_tc_bind(op.tcl, t);
     op.tct = &t;
     if (e == cudaSuccess) e = run_op(op, mode, x_dtype, X, I, J, K, A, B, C, R, ws, nullptr, s);
@@ -463,24 +463,16 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaMemset flags"));
   if (pl->any_tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
+    // one block image per mode (each is laid out for its mode's stream)
     for (int m = 0; m < 3; ++m) {
       if (!pl->op[m].tc) continue;
-      int found = -1;
-      for (int k = 0; k < m; ++k)
-        if (d.x_mode[k] == d.x_mode[m] && pl->op[k].tc) found = k;
-      const ntf::TcTensor* t = nullptr;
-      if (found >= 0) {
-        t = pl->op[found].tct;
-      } else {
-        ntf::TcTensor& slot = pl->tct[pl->n_tct++];
-        if ((e = ntf::tc_tensor_create(static_cast<const float*>(d.x_mode[m]), d.x_dims[m], &slot,
-                                       nullptr)) != cudaSuccess)
-          return cleanup(cuda_fail(e, "tc split"));
-        t = &slot;
-      }
-      pl->op[m].tct = t;
-      if ((e = ntf::mttkrp_tc_bind(pl->op[m].tcl, *t)) != cudaSuccess)
-        return cleanup(cuda_fail(e, "tc tensor map"));
+      ntf::TcTensor& slot = pl->tct[pl->n_tct++];
+      if ((e = ntf::tc_tensor_create(pl->op[m].tcl, static_cast<const float*>(d.x_mode[m]),
+                                     d.x_dims[m], &slot, nullptr)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "tc split"));
+      pl->op[m].tct = &slot;
+      if ((e = ntf::mttkrp_tc_bind(pl->op[m].tcl, slot)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "tc bind"));
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
   }
@@ -626,6 +618,12 @@ void ntf_plan_destroy(ntf_plan* pl) {
   ntf::dev_free(pl->gram_ws);
   ntf::dev_free(pl->gram_pending);
   delete pl;
+}
+
+// Diagnostics only (not part of the reference-facing ABI): per-CTA globaltimer
+// stamps of the last tcgen05 MTTKRP launched with NTF_TC_DEBUG & 256 set.
+int ntf_debug_tc_times(unsigned long long* host, int ctas) {
+  return ntf::tc_debug_read_times(host, ctas);
 }
 
 }  // extern "C"

@@ -96,10 +96,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// try_wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or the hint expires) instead of re-polling the barrier
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!done);
+}
+
 // NTF_TC_DEBUG & 32: cycles each role spends waiting (printed per CTA)
-__device__ __forceinline__ void mbar_wait_p(uint64_t* bar, uint32_t parity, bool prof, long long& acc) {
-  if (!prof) {
-    mbar_wait(bar, parity);
+// wm: bit 0 profile (count the cycles), bit 1 wait with a suspend-time hint
+__device__ __forceinline__ void mbar_wait_p(uint64_t* bar, uint32_t parity, int wm, long long& acc) {
+  if (!(wm & 1)) {
+    if (wm & 2) mbar_wait_sleep(bar, parity);
+    else mbar_wait(bar, parity);
     return;
   }
   const long long t0 = clock64();
@@ -223,6 +243,19 @@ __device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo_bytes,
   return d;
 }
 
+// UMMA shared-memory descriptor, no swizzle (layout type 0): K-major core
+// matrices of 8 rows x 16 B; lbo = stride between K-adjacent core matrices,
+// sbo = stride between M-adjacent (8-row) core matrices.
+__device__ __forceinline__ uint64_t smem_desc_noswz(const void* p, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+
 // kind::f16 instruction descriptor: F16 x F16 -> F32, M=128
 __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
   return (1u << 4)                                 // D format F32
@@ -248,15 +281,17 @@ __host__ __device__ constexpr uint32_t tmem_cols(int N) {
 }
 
 struct TcParams {
-  CUtensorMap tmap0;         // S0 plane, 3-D (K, J, I)
-  CUtensorMap tmap1;         // S1 plane
+  const unsigned char* img;  // this mode's block image of the split tensor (see tc_tensor_create)
+  int64_t tile_bytes;        // bytes of one full m-tile in the image
+  int r8_full, r8_tail;      // stored rows (multiple of 8) of a full / the ragged last m-tile
+  int ct;                    // 8-element chunks of the last l block (8 when l_ext % 64 == 0)
   int mode, R;
   int64_t M;
   int l_ext, n_o, n_lb, G;   // l extent, o extent, 64-wide l blocks, blocks per unit
   int n_full, splits, splits_tail;
   int tm;                    // rows per m-tile (<= 128; MMA M is 128, rows >= tm ignored)
   int x_stages, h_stages;
-  const double* f_hi;        // [n_o][R]
+  const float2* hpair;       // [n_o][N] F_hi[o, n] * 2^-e(n) as fp32 (hi, lo) pairs (w_slice_kernel)
   const unsigned char* wsl;  // [n_lb][3][N][128 B] W slices of F_lo (w_slice_kernel)
   const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
   const double* cm_lo;       // [R] max |F_lo[:, n]|
@@ -267,6 +302,7 @@ struct TcParams {
   const int* stop_flag;
   int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip W forming,
                              // 2 skip MMA, 4 skip TMEM drain, 16 skip X TMA
+  unsigned long long* times;  // NTF_TC_DEBUG & 256: per-CTA globaltimer stamps [8]
   TcRidge ridge;              // extra CTA (gridDim.x - 1) when ridge.out != NULL
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
   uint32_t ub_tail[kTcMaxSplits + 1];  // ... of the ragged last tile
@@ -398,123 +434,139 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const bool prof = (p.debug & 32) != 0;
-  const uint64_t g_ready = prof ? gtimer() : 0;
+  const int wm = (prof ? 1 : 0) | ((p.debug & 2048) ? 2 : 0);
+  const uint64_t g_ready = (prof || (p.debug & 256)) ? gtimer() : 0;
   long long wt[3] = {0, 0, 0};
   const long long t_start = prof ? clock64() : 0;
+  uint64_t t_role = 0;  // NTF_TC_DEBUG & 256: end of this role's loop
 
+  // Roles 0-2: warp-uniform loops (descriptors and barrier addresses stay in
+  // uniform registers); one elected lane issues.
+  const int dbg = p.debug;
+  // This CTA's m-tile in the image: stored rows, block sizes and the byte
+  // offset of its first unit.  A CTA's units are consecutive (g-major) and
+  // the image stores them consecutively, so the CTA streams ONE contiguous
+  // byte range, block after block.
+  const int r8 = tile < p.n_full ? p.r8_full : p.r8_tail;
+  const uint32_t blk_full = 256u * static_cast<uint32_t>(r8);  // 2 planes x 8 chunks x r8 x 16 B
+  const uint32_t blk_tail = 32u * static_cast<uint32_t>(p.ct * r8);
   if (warp == 0) {
-    // ------------------------------ X-tile producer ---------------------------
-    // warp-uniform loop; one elected lane issues
+    // ------------------------------ X-block producer --------------------------
+    const bool no_x = (dbg & 16) != 0;
+    const int n_lb = p.n_lb;
+    int64_t off = static_cast<int64_t>(tile) * p.tile_bytes +
+                  static_cast<int64_t>(u0.g) * n_o * G * blk_full;
+    {  // units (u0.g, 0 .. u0.o - 1) of the first group precede this CTA's range
+      const int nl = lbs_of(u0.g);
+      const bool has_tail = u0.g * G + nl == n_lb;
+      const int64_t unit_bytes = has_tail ? (nl - 1) * int64_t(blk_full) + blk_tail : nl * int64_t(blk_full);
+      off += static_cast<int64_t>(u0.o) * unit_bytes;
+    }
     Ring xr;
     UnitIt ui = u0;
-    const int mm = static_cast<int>(m0);
     for (int u = u_begin; u < u_end; ++u) {
       const int nl = lbs_of(ui.g);
       for (int j = 0; j < nl; ++j) {
-        mbar_wait_p(&x_empty[xr.idx], xr.phase ^ 1u, prof, wt[0]);
+        mbar_wait_p(&x_empty[xr.idx], xr.phase ^ 1u, wm, wt[0]);
         uint64_t* bar = &x_full[xr.idx];
-        unsigned char* d0 = xbase + xr.idx * 2 * kXTile;
-        unsigned char* d1 = d0 + kXTile;
-        const int l0 = (ui.g * G + j) * kBK;
+        const uint32_t bytes = (ui.g * G + j == n_lb - 1) ? blk_tail : blk_full;
         if (elect_one()) {
-          if (p.debug & 16) {
+          if (no_x) {
             mbar_arrive(bar);
           } else {
-            mbar_arrive_expect_tx(bar, p.mode == 3 ? 2 * kXTile : 2 * p.tm * kBK * 2);
-            if (p.mode == 1) {
-              tma_load_3d(d0, &p.tmap0, bar, l0, ui.o, mm);
-              tma_load_3d(d1, &p.tmap1, bar, l0, ui.o, mm);
-            } else if (p.mode == 2) {
-              tma_load_3d(d0, &p.tmap0, bar, l0, mm, ui.o);
-              tma_load_3d(d1, &p.tmap1, bar, l0, mm, ui.o);
-            } else {  // two 64-m boxes per plane
-              tma_load_3d(d0, &p.tmap0, bar, mm, l0, ui.o);
-              tma_load_3d(d0 + kXTile / 2, &p.tmap0, bar, mm + 64, l0, ui.o);
-              tma_load_3d(d1, &p.tmap1, bar, mm, l0, ui.o);
-              tma_load_3d(d1 + kXTile / 2, &p.tmap1, bar, mm + 64, l0, ui.o);
-            }
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_load(xbase + xr.idx * 2 * kXTile, p.img + off, bytes, bar);
           }
         }
         __syncwarp();
+        off += bytes;
         xr.next(SX);
       }
       ui.next(n_o);
     }
+    t_role = gtimer();
   } else if (warp == 1) {
     // ------------------------------ MMA issuer --------------------------------
     // Two wide MMAs per K step, each reading its A tile once: the W slices
     // T0|T1|T2 are consecutive N-row blocks of one K-major B operand.
     //   cols [0, 3N) (=|+=) S0 * [T0 | T1 | T2]     cols [N, 3N) += S1 * [T0 | T1]
-    // Warp-uniform loop; one elected lane issues the MMAs and commits.
-    const bool mn = p.mode == 3;
+    // A (the X block) is a no-swizzle K-major image: 8-row x 16 B core
+    // matrices, row groups 128 B apart (SBO), 8-element chunks r8*16 B apart
+    // (LBO); plane S1 follows plane S0.
+    const bool no_mma = (dbg & 2) != 0, plain_arrive = (dbg & 64) != 0;
     // N' <= 256 per MMA: for N > 85 the first MMA is split into S0*[T0|T1]
     // and S0*T2 (the S0 tile is then read twice)
     constexpr bool kSplit = 3 * N > 256;
-    const uint32_t idesc3 = make_idesc(kSplit ? 2 * N : 3 * N, mn);
-    const uint32_t idesc2 = make_idesc(2 * N, mn);
-    const uint32_t idesc1 = make_idesc(N, mn);
-    // descriptors of stage 0 / l-block 0; stages are 32 KB apart, l blocks
-    // kWlb apart (both multiples of 16 B: added to the address field)
-    const uint64_t da_base = mn ? smem_desc(xbase, kXTile / 2, 1024) : smem_desc(xbase, 16, 1024);
+    const uint32_t idesc3 = make_idesc(kSplit ? 2 * N : 3 * N, false);
+    const uint32_t idesc2 = make_idesc(2 * N, false);
+    const uint32_t idesc1 = make_idesc(N, false);
+    const uint32_t lbo = static_cast<uint32_t>(r8) * 16u;
+    const uint64_t da_base = smem_desc_noswz(xbase, lbo, 128);
     const uint64_t db_base = smem_desc(wbase, 16, 1024);
-    const uint32_t a_kstep = mn ? 2048 >> 4 : 32 >> 4;  // descriptor units (16 B)
+    const uint32_t a_kstep = (2 * lbo) >> 4;  // descriptor units (16 B): two chunks per K=16
+    const int n_lb = p.n_lb, ct = p.ct;
     Ring xr, ar;
     UnitIt ui = u0;
     int cur_g = -1;
     uint32_t wphase = 0;
     for (int u = u_begin; u < u_end; ++u) {
-      if (ui.g != cur_g) {  // new group: its W slices must be formed
+      if (ui.g != cur_g) {  // new group: its W slices must be resident
         if (cur_g >= 0) {
           if (elect_one()) tc_commit(w_empty);
           __syncwarp();
         }
-        mbar_wait_p(w_full, wphase, prof, wt[2]);
+        mbar_wait_p(w_full, wphase, wm, wt[2]);
         wphase ^= 1u;
         cur_g = ui.g;
       }
-      mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, prof, wt[1]);
+      mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, wm, wt[1]);
       tc_fence_after();
       const uint32_t d0 = tmem + ar.idx * 3 * N;
       const uint32_t d1 = d0 + N;
       const int nl = lbs_of(ui.g);
       for (int j = 0; j < nl; ++j) {
-        mbar_wait_p(&x_full[xr.idx], xr.phase, prof, wt[0]);
+        mbar_wait_p(&x_full[xr.idx], xr.phase, wm, wt[0]);
         tc_fence_after();
+        const int chunks = (ui.g * G + j == n_lb - 1) ? ct : 8;
         const uint64_t da0 = da_base + static_cast<uint64_t>((xr.idx * 2 * kXTile) >> 4);
-        const uint64_t da1 = da0 + static_cast<uint64_t>(kXTile >> 4);
+        const uint64_t da1 = da0 + static_cast<uint64_t>((static_cast<uint32_t>(chunks) * lbo) >> 4);
         const uint64_t db = db_base + static_cast<uint64_t>((j * kWlb) >> 4);
         if (elect_one()) {
-          if (!(p.debug & 2)) {
+          if (!no_mma) {
 #pragma unroll
             for (int kk = 0; kk < kBK / kUK; ++kk) {
-              const uint32_t first = (j | kk) ? 1u : 0u;
-              tc_mma_f16(d0, da0 + kk * a_kstep, db + kk * (32 >> 4), idesc3, first);
-              if constexpr (kSplit)  // S0*T2 into ACC2 (B rows [2N, 3N))
-                tc_mma_f16(d0 + 2 * N, da0 + kk * a_kstep,
-                           db + kk * (32 >> 4) + static_cast<uint64_t>((2 * N * 128) >> 4), idesc1, first);
-              tc_mma_f16(d1, da1 + kk * a_kstep, db + kk * (32 >> 4), idesc2, 1u);
+              if (2 * kk < chunks) {
+                const uint32_t first = (j | kk) ? 1u : 0u;
+                tc_mma_f16(d0, da0 + kk * a_kstep, db + kk * (32 >> 4), idesc3, first);
+                if constexpr (kSplit)  // S0*T2 into ACC2 (B rows [2N, 3N))
+                  tc_mma_f16(d0 + 2 * N, da0 + kk * a_kstep,
+                             db + kk * (32 >> 4) + static_cast<uint64_t>((2 * N * 128) >> 4), idesc1, first);
+                tc_mma_f16(d1, da1 + kk * a_kstep, db + kk * (32 >> 4), idesc2, 1u);
+              }
             }
           }
-          if (p.debug & 64) mbar_arrive(&x_empty[xr.idx]);  // profiling: no tensor-pipe commit
+          if (plain_arrive) mbar_arrive(&x_empty[xr.idx]);  // profiling: no tensor-pipe commit
           else tc_commit(&x_empty[xr.idx]);
         }
         __syncwarp();
         xr.next(SX);
       }
       if (elect_one()) {
-        if (p.debug & 64) mbar_arrive(&acc_full[ar.idx]);
+        if (plain_arrive) mbar_arrive(&acc_full[ar.idx]);
         else tc_commit(&acc_full[ar.idx]);
       }
       __syncwarp();
       ar.next(kAccBufs);
       ui.next(n_o);
     }
+    t_role = gtimer();
   } else if (warp == 2) {
-    // ---------- W slices of each group (bulk copy) + F_hi rows -> fp32 pairs ---------
-    // Everything from here on reads what the preceding kernels produced.
+    // ------- W slices of each group + F_hi pair rows (bulk copies, many in flight) -------
+    // Everything from here on reads what the preceding kernels produced
+    // (w_slice_kernel formed both the W slices and the F_hi pair table).
     pdl_wait();
-    // per-column scales: [N,2N) F_hi -> unit range 2^-e, [2N,3N) output
-    // xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f, max|F_hi[:,n]| < 2^e
+    // per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
+    // max|F_hi[:,n]| < 2^e (the same clamps as w_slice_kernel)
     for (int n = lane; n < N; n += 32) {
       const int t = G >= 4 ? 5 : (G >= 2 ? 6 : 7);
       int f = 0, e = 0;
@@ -526,7 +578,6 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       // kernel): clamp, identically there (kFMin)
       f = max(f, kFMin);
       e = max(e, kFMin);
-      wsc[N + n] = ldexp(1.0, -e);
       wsc[2 * N + n] = *p.xscale * ldexp(1.0, f - t + e);
     }
     // this mode's column maxima are re-accumulated by the row update that follows
@@ -538,7 +589,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     int seg = 0;
     for (int u = u_begin; u < u_end; ++u) {
       if (u == u_begin || ui.o == 0) {  // group start: the previous group's MMAs are done
-        if (seg > 0) mbar_wait_p(w_empty, (seg - 1) & 1, prof, wt[2]);
+        if (seg > 0) mbar_wait_p(w_empty, (seg - 1) & 1, wm, wt[2]);
         if (elect_one()) {
           const uint32_t bytes = static_cast<uint32_t>(lbs_of(ui.g) * kWlb);
           mbar_arrive_expect_tx(w_full, bytes);
@@ -547,18 +598,16 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
         __syncwarp();
         ++seg;
       }
-      mbar_wait_p(&h_empty[hr.idx], hr.phase ^ 1u, prof, wt[0]);
-      float2* hs = hbase + hr.idx * N;
-      for (int n = lane; n < N; n += 32) {
-        const double h = n < R ? p.f_hi[static_cast<int64_t>(ui.o) * R + n] * wsc[N + n] : 0.0;
-        const float hx = static_cast<float>(h);
-        hs[n] = make_float2(hx, static_cast<float>(h - static_cast<double>(hx)));
+      mbar_wait_p(&h_empty[hr.idx], hr.phase ^ 1u, wm, wt[0]);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&h_full[hr.idx], N * 8);
+        bulk_load(hbase + hr.idx * N, p.hpair + static_cast<int64_t>(ui.o) * N, N * 8, &h_full[hr.idx]);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&h_full[hr.idx]);
       hr.next(SH);
       ui.next(n_o);
     }
+    t_role = gtimer();
   } else {
     // ------------------------------ epilogue ----------------------------------
     const int e = warp - kFirstEpi;
@@ -573,8 +622,11 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     }
     Ring ar, hr;
     for (int u = u_begin; u < u_end; ++u) {
-      mbar_wait_p(&acc_full[ar.idx], ar.phase, prof, wt[0]);
-      mbar_wait_p(&h_full[hr.idx], hr.phase, prof, wt[1]);
+      if (!(p.debug & 1024) || e == 0) {  // 1024: one polling warp, named barrier for the rest
+        mbar_wait_p(&acc_full[ar.idx], ar.phase, wm, wt[0]);
+        mbar_wait_p(&h_full[hr.idx], hr.phase, wm, wt[1]);
+      }
+      if (p.debug & 1024) asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * 3 * N + c0;
       const float2* hs = hbase + hr.idx * N + c0;
@@ -607,6 +659,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       ar.next(kAccBufs);
       hr.next(SH);
     }
+    t_role = gtimer();
     // fp64 partial of this CTA: out = (hi + lo) * xs * 2^(f-t) * 2^e
     const int64_t gm = m0 + row;
     if (row < p.tm && gm < p.M) {
@@ -624,12 +677,22 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
            warp, u_end - u_begin, clock64() - t_start, wt[0], wt[1], wt[2],
            (unsigned long long)g_entry, (unsigned long long)(g_ready - g_entry),
            (unsigned long long)(gtimer() - g_entry));
+  if ((p.debug & 256) && lane == 0 && warp <= 3) {
+    unsigned long long* ts = p.times + static_cast<int64_t>(blockIdx.x) * 8;
+    ts[2 + warp] = t_role;
+    if (warp == 0) {
+      ts[0] = g_entry;
+      ts[1] = g_ready;
+      ts[7] = static_cast<unsigned long long>(u_end - u_begin);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "r"(tmem_cols(N)));
+    if ((p.debug & 256) && lane == 0) p.times[static_cast<int64_t>(blockIdx.x) * 8 + 6] = gtimer();
   }
 }
 
@@ -643,10 +706,30 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
 // ----------------------------------------------------------------------------
 __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int n_lb,
                                const double* __restrict__ cm, int t, unsigned char* __restrict__ wsl,
+                               const double* __restrict__ Fhi, int n_o,
+                               const double* __restrict__ cm_hi, float2* __restrict__ hpair,
                                const int* stop_flag) {
   pdl_trigger();
   pdl_wait();  // F_lo and its column maxima come from the preceding row update
   if (stop_flag && *stop_flag) return;
+  // F_hi pair table: hpair[o][n] = F_hi[o, n] * 2^-e(n) as an fp32 (hi, lo)
+  // pair, max|F_hi[:, n]| < 2^e(n) (clamped like the MTTKRP's output scale)
+  {
+    const int64_t total_h = static_cast<int64_t>(n_o) * N;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total_h;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int n = static_cast<int>(e % N);
+      const int64_t o = e / N;
+      double h = 0.0;
+      if (n < R) {
+        int ex = 0;
+        if (cm_hi[n] > 0.0) frexp(cm_hi[n], &ex);
+        h = Fhi[o * R + n] * ldexp(1.0, -max(ex, kFMin));
+      }
+      const float hx = static_cast<float>(h);
+      hpair[e] = make_float2(hx, static_cast<float>(h - static_cast<double>(hx)));
+    }
+  }
   const int total = n_lb * N * (kBK / 8);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int n = e % N;
@@ -697,21 +780,70 @@ __global__ void absmax_kernel(const float* __restrict__ X, int64_t n, unsigned* 
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // order-free: max is exact
 }
 
-__global__ void split_kernel(const float* __restrict__ X, int64_t n, const unsigned* amax,
-                             __half* __restrict__ s0, __half* __restrict__ s1, double* xscale) {
+// One mode's block image of the split tensor.  For each m-tile t (r8
+// stored rows, a multiple of 8; rows >= M are zero), each unit (g, o) in
+// g-major order and each l block j of the unit, both planes back to back:
+//   [plane][chunk c < chunks(lb)][row < r8][8 fp16]      (chunk = 8 l values)
+// i.e. the no-swizzle K-major UMMA image of the block, so one bulk copy moves
+// it into shared memory and a CTA's units are one contiguous byte range.
+// The last l block stores only ct chunks (l_ext rounded up to 16).
+// Values: X * 2^(11-e) = S0 + S1, S0 = rint (|S0| <= 2^11), S1 = rint of the
+// remainder in 2^-11 units (both exact in fp16), xscale = 2^(e-11).
+struct ImgGeom {
+  int mode;
+  int64_t I, J, K, M;
+  int n_o, l_ext, n_lb, G, tm, n_full, n_tiles, r8_full, r8_tail, ct;
+  int64_t tile_bytes;
+};
+
+__global__ void image_split_kernel(const float* __restrict__ X, ImgGeom g, const unsigned* amax,
+                                   unsigned char* __restrict__ img, double* xscale) {
   const float mx = __uint_as_float(*amax);
-  int e = 0;
-  if (mx > 0.f) frexpf(mx, &e);            // mx < 2^e
-  const float up = ldexpf(1.0f, 11 - e);   // X * 2^(11-e) in [-2048, 2048]
-  if (blockIdx.x == 0 && threadIdx.x == 0) *xscale = ldexp(1.0, e - 11);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float s = X[i] * up;              // exact (power-of-two scaling)
-    const float a0 = rintf(s);
-    const float r = (s - a0) * 2048.0f;     // exact
-    const float a1 = rintf(r);
-    s0[i] = __float2half_rn(a0);
-    s1[i] = __float2half_rn(a1 * 4.8828125e-04f);  // 2^-11 units
+  int ex = 0;
+  if (mx > 0.f) frexpf(mx, &ex);            // mx < 2^ex
+  const float up = ldexpf(1.0f, 11 - ex);   // X * 2^(11-ex) in [-2048, 2048]
+  if (blockIdx.x == 0 && threadIdx.x == 0) *xscale = ldexp(1.0, ex - 11);
+  const int64_t total = static_cast<int64_t>(g.n_tiles) * g.n_o * g.n_lb * 1024;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(e & 127);
+    const int c = static_cast<int>((e >> 7) & 7);
+    int64_t rest = e >> 10;
+    const int lb = static_cast<int>(rest % g.n_lb);
+    rest /= g.n_lb;
+    const int o = static_cast<int>(rest % g.n_o);
+    const int t = static_cast<int>(rest / g.n_o);
+    const int r8 = t < g.n_full ? g.r8_full : g.r8_tail;
+    const int chunks = lb == g.n_lb - 1 ? g.ct : 8;
+    if (row >= r8 || c >= chunks) continue;
+    const int64_t bf = 256 * static_cast<int64_t>(r8), bt = 32 * static_cast<int64_t>(g.ct) * r8;
+    const int gi = lb / g.G, j = lb - gi * g.G;
+    const int nl = min(g.G, g.n_lb - gi * g.G);
+    const int64_t unit_bytes = (nl - 1) * bf + (gi * g.G + nl == g.n_lb ? bt : bf);
+    const int64_t off = t * g.tile_bytes + static_cast<int64_t>(gi) * g.n_o * g.G * bf +
+                        o * unit_bytes + j * bf + static_cast<int64_t>(c) * r8 * 16 + row * 16;
+    const int64_t m = static_cast<int64_t>(t) * g.tm + row;
+    const int l0 = lb * 64 + c * 8;
+    __align__(16) __half h0[8], h1[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int l = l0 + v;
+      float x = 0.f;
+      if (m < g.M && l < g.l_ext) {
+        const int64_t idx = g.mode == 1 ? (m * g.J + o) * g.K + l
+                            : g.mode == 2 ? (static_cast<int64_t>(o) * g.J + m) * g.K + l
+                                          : (static_cast<int64_t>(o) * g.J + l) * g.K + m;
+        x = X[idx];
+      }
+      const float sv = x * up;                // exact (power-of-two scaling)
+      const float a0 = rintf(sv);
+      const float a1 = rintf((sv - a0) * 2048.0f);  // exact
+      h0[v] = __float2half_rn(a0);
+      h1[v] = __float2half_rn(a1 * 4.8828125e-04f);  // 2^-11 units
+    }
+    *reinterpret_cast<uint4*>(img + off) = *reinterpret_cast<const uint4*>(h0);
+    *reinterpret_cast<uint4*>(img + off + static_cast<int64_t>(chunks) * r8 * 16) =
+        *reinterpret_cast<const uint4*>(h1);
   }
 }
 
@@ -728,6 +860,16 @@ __global__ void colmax_kernel(const double* __restrict__ F, int64_t rows, int R,
     for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
     out[r] = m;
   }
+}
+
+// NTF_TC_DEBUG & 256: per-CTA stamps of the last launch (diagnostics only)
+constexpr int kTcTimesCtas = 1024;
+__device__ unsigned long long g_tc_times[kTcTimesCtas * 8];
+
+unsigned long long* tc_debug_times() {
+  void* ptr = nullptr;
+  cudaGetSymbolAddress(&ptr, g_tc_times);
+  return static_cast<unsigned long long*>(ptr);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
@@ -794,6 +936,13 @@ void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
 }
 
 }  // namespace
+
+// diagnostics: copy the per-CTA stamps of the last NTF_TC_DEBUG&256 launch
+int tc_debug_read_times(unsigned long long* host, int ctas) {
+  ctas = std::min(ctas, kTcTimesCtas);
+  return cudaMemcpy(host, tc_debug_times(), sizeof(unsigned long long) * 8 * ctas,
+                    cudaMemcpyDeviceToHost) == cudaSuccess ? ctas : -1;
+}
 
 // ----------------------------------------------------------------------------
 // host API
@@ -868,17 +1017,24 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   // costs a fixed pipeline share plus its rows' share of the bytes.  One SM
   // is left free so the mode's ridge Cholesky (side stream) runs concurrently.
   const int cap = std::min(sm_count_tc() - 1, kTcMaxSplits);
-  // Modes 1/2 (K-major A, box height free): equal tiles of tm <= 128 rows,
-  // so every CTA streams the same bytes.  Mode 3 (MN-major A, 64-row boxes):
-  // 128-row tiles plus a ragged last tile.
-  if (mode != 3) {
+  // Equal m-tiles of tm <= 128 rows (a multiple of 8, the core-matrix
+  // height), so every CTA of a full tile streams the same bytes; the last
+  // tile may be shorter.
+  {
     const int64_t nt = (L.M + kTM - 1) / kTM;
-    L.tm = static_cast<int>((L.M + nt - 1) / nt);
-  } else {
-    L.tm = kTM;
+    L.tm = static_cast<int>(8 * ((L.M + 8 * nt - 1) / (8 * nt)));
   }
   L.n_full = static_cast<int>(L.M / L.tm);
   const int tail = static_cast<int>(L.M % L.tm);
+  L.r8_full = L.tm;
+  L.r8_tail = tail ? 8 * ((tail + 7) / 8) : 0;
+  {
+    const int rem = L.l_ext % kBK;
+    L.ct = rem == 0 ? 8 : 2 * ((rem + 15) / 16);
+  }
+  L.tile_bytes = static_cast<int64_t>(L.n_o) * 32 * L.tm * (8 * (L.n_lb - 1) + L.ct);
+  L.img_bytes = static_cast<size_t>(L.n_full) * L.tile_bytes +
+                (tail ? static_cast<size_t>(L.n_o) * 32 * L.r8_tail * (8 * (L.n_lb - 1) + L.ct) : 0);
   double fixed = 1.0;  // measured: a ragged tile's l block costs about a full one
   if (const char* e = getenv("NTF_TC_TAILCOST")) fixed = atof(e);
   const double wt = tail ? fixed + (1.0 - fixed) * tail / static_cast<double>(kTM) : 0.0;
@@ -897,6 +1053,7 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   if (L.splits_tail) partition_units(L, L.splits_tail, L.ub_tail);
   L.wscale = nullptr;
   L.wsl = nullptr;
+  L.hpair = nullptr;
   L.bound = false;
   return L;
 }
@@ -910,17 +1067,15 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L) {
   return dispatch_tc(p, L, nullptr, true);
 }
 
-cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* out,
-                             cudaStream_t stream) {
+cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
+                             TcTensor* out, cudaStream_t stream) {
   const int64_t n = dims[0] * dims[1] * dims[2];
   TcTensor t;
   for (int i = 0; i < 3; ++i) t.dims[i] = dims[i];
+  t.mode = L.mode;
+  t.img_bytes = L.img_bytes;
   cudaError_t e;
-  if ((e = ntf::dev_alloc(&t.s0, n * sizeof(__half))) != cudaSuccess) return e;
-  if ((e = ntf::dev_alloc(&t.s1, n * sizeof(__half))) != cudaSuccess) {
-    tc_tensor_destroy(&t);
-    return e;
-  }
+  if ((e = ntf::dev_alloc(&t.img, L.img_bytes)) != cudaSuccess) return e;
   if ((e = ntf::dev_alloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
@@ -929,7 +1084,24 @@ cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* ou
   cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
   const int blocks = 4 * sm_count_tc();
   absmax_kernel<<<blocks, 256, 0, stream>>>(X, n, amax);
-  split_kernel<<<blocks, 256, 0, stream>>>(X, n, amax, t.s0, t.s1, t.xscale);
+  ImgGeom g;
+  g.mode = L.mode;
+  g.I = dims[0];
+  g.J = dims[1];
+  g.K = dims[2];
+  g.M = L.M;
+  g.n_o = L.n_o;
+  g.l_ext = L.l_ext;
+  g.n_lb = L.n_lb;
+  g.G = L.G;
+  g.tm = L.tm;
+  g.n_full = L.n_full;
+  g.n_tiles = L.n_full + (L.r8_tail ? 1 : 0);
+  g.r8_full = L.r8_full;
+  g.r8_tail = L.r8_tail;
+  g.ct = L.ct;
+  g.tile_bytes = L.tile_bytes;
+  image_split_kernel<<<8 * sm_count_tc(), 256, 0, stream>>>(X, g, amax, t.img, t.xscale);
   if ((e = cudaGetLastError()) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
@@ -940,42 +1112,24 @@ cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* ou
 
 void tc_tensor_destroy(TcTensor* t) {
   if (!t) return;
-  ntf::dev_free(t->s0);
-  ntf::dev_free(t->s1);
+  ntf::dev_free(t->img);
   ntf::dev_free(t->xscale);
-  t->s0 = t->s1 = nullptr;
+  t->img = nullptr;
   t->xscale = nullptr;
 }
 
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
-  auto enc = get_encoder();
-  if (!enc) return cudaErrorNotSupported;
-  const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
-  cuuint64_t gdim[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(J),
-                        static_cast<cuuint64_t>(I)};
-  cuuint64_t gstr[2] = {static_cast<cuuint64_t>(K * 2), static_cast<cuuint64_t>(J * K * 2)};
-  cuuint32_t box[3];
-  if (L.mode == 1) {
-    box[0] = 64; box[1] = 1; box[2] = static_cast<cuuint32_t>(L.tm);
-  } else if (L.mode == 2) {
-    box[0] = 64; box[1] = static_cast<cuuint32_t>(L.tm); box[2] = 1;
-  } else {
-    box[0] = 64; box[1] = 64; box[2] = 1;
-  }
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r0 = enc(&L.tmap0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s0, gdim, gstr, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  CUresult r1 = enc(&L.tmap1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, t.s1, gdim, gstr, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  if (t.mode != L.mode || t.img_bytes != L.img_bytes) return cudaErrorInvalidValue;
   if (!L.wscale) {
     cudaError_t e = ntf::dev_alloc(&L.wscale, sizeof(double) * 2 * L.N);
     if (e != cudaSuccess) return e;
   }
   if (!L.wsl) {
     cudaError_t e = ntf::dev_alloc(&L.wsl, static_cast<size_t>(L.n_lb) * 3 * L.N * kBK * 2);
+    if (e != cudaSuccess) return e;
+  }
+  if (!L.hpair) {
+    cudaError_t e = ntf::dev_alloc(&L.hpair, static_cast<size_t>(L.n_o) * L.N * sizeof(float2));
     if (e != cudaSuccess) return e;
   }
   L.bound = true;
@@ -985,8 +1139,10 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
 void mttkrp_tc_unbind(MttkrpTCLaunch& L) {
   ntf::dev_free(L.wscale);
   ntf::dev_free(L.wsl);
+  ntf::dev_free(L.hpair);
   L.wscale = nullptr;
   L.wsl = nullptr;
+  L.hpair = nullptr;
   L.bound = false;
 }
 
@@ -1010,8 +1166,11 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     Fhi = A; Flo = B; hi_rows = I; lo_rows = J;
   }
   TcParams p{};
-  p.tmap0 = L.tmap0;
-  p.tmap1 = L.tmap1;
+  p.img = t.img;
+  p.tile_bytes = L.tile_bytes;
+  p.r8_full = L.r8_full;
+  p.r8_tail = L.r8_tail;
+  p.ct = L.ct;
   p.mode = L.mode;
   p.R = L.R;
   p.M = L.M;
@@ -1025,7 +1184,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   p.tm = L.tm;
   p.x_stages = L.x_stages;
   p.h_stages = L.h_stages;
-  p.f_hi = Fhi;
+  p.hpair = L.hpair;
   p.wsl = L.wsl;
   if (ridge) p.ridge = *ridge;
   p.ws = ws;
@@ -1041,6 +1200,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
       dbg = env ? atoi(env) : 0;
     }
     p.debug = dbg;
+    if (dbg & 256) p.times = tc_debug_times();
   }
   p.xscale = t.xscale;
   if (colmax3) {  // plan: column maxima kept current by the row-update kernels
@@ -1058,11 +1218,12 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   }
   {
     const int t = L.G >= 4 ? 5 : (L.G >= 2 ? 6 : 7);
-    const int total = L.n_lb * L.N * (kBK / 8);
+    const int total = std::max(L.n_lb * L.N * (kBK / 8), L.n_o * L.N);
     const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
     if (!(p.debug & 128)) {
       cudaError_t e = launch_pdl(w_slice_kernel, dim3(blocks), dim3(64), 0, stream, Flo, L.l_ext,
-                                 L.R, L.N, L.n_lb, p.cm_lo, t, L.wsl, stop_flag);
+                                 L.R, L.N, L.n_lb, p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
+                                 L.hpair, stop_flag);
       if (e != cudaSuccess) return e;
     }
   }

@@ -11,16 +11,21 @@ namespace ntf {
 
 // fp16 fixed-point split of an fp32 tensor: X ~= xscale * (S0 + S1),
 // S0 integers |S0| <= 2048, S1 multiples of 2^-11 with |S1| <= 0.5, xscale a
-// power of two (2^(e-11), e = ceil(log2 max|X|)).  Built once per tensor.
+// power of two (2^(e-11), e = ceil(log2 max|X|)), stored as ONE mode's block
+// image (mttkrp_tc.cu: image_split_kernel): every X block a CTA streams is a
+// contiguous no-swizzle UMMA image, and a CTA's blocks are consecutive.
+// Built once per (tensor, mode plan).
 struct TcTensor {
-  __half* s0 = nullptr;
-  __half* s1 = nullptr;
+  unsigned char* img = nullptr;
+  size_t img_bytes = 0;
   double* xscale = nullptr;  // device scalar
+  int mode = 0;
   int64_t dims[3] = {0, 0, 0};
 };
 
-cudaError_t tc_tensor_create(const float* X, const int64_t dims[3], TcTensor* out,
-                             cudaStream_t stream);
+struct MttkrpTCLaunch;
+cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
+                             TcTensor* out, cudaStream_t stream);
 void tc_tensor_destroy(TcTensor* t);
 
 constexpr int kTcMaxSplits = 160;  // CTAs per m-tile
@@ -32,7 +37,11 @@ struct MttkrpTCLaunch {
   int n_mtiles;
   int n_full, splits;       // full 128-row tiles and CTAs per full tile
   int splits_tail;          // CTAs of the ragged last tile (0: none)
-  int tm;                   // rows per m-tile
+  int tm;                   // rows per m-tile (a multiple of 8)
+  int r8_full, r8_tail;     // stored rows of a full / the ragged last tile (multiples of 8)
+  int ct;                   // 8-element chunks stored for the last l block
+  int64_t tile_bytes;       // image bytes of one full m-tile
+  size_t img_bytes;         // image bytes of the whole mode
   int l_ext, n_o, n_lb;     // l extent, o extent, 64-wide l blocks
   int G, n_g;               // l blocks per unit (one TMEM drain), groups
   int threads, smem_bytes;
@@ -40,9 +49,9 @@ struct MttkrpTCLaunch {
   int tmem_cols;
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
   uint32_t ub_tail[kTcMaxSplits + 1];
-  CUtensorMap tmap0, tmap1; // S0 / S1 planes (built by mttkrp_tc_bind)
   double* wscale;           // [2 * N] device: column maxima for one-shot calls
   unsigned char* wsl;       // [n_lb][3][N][128 B] W slices of F_lo (per launch)
+  float2* hpair;            // [n_o][N] F_hi rows as scaled fp32 pairs (per launch)
   bool bound;
 };
 
@@ -52,7 +61,7 @@ bool mttkrp_tc_shape_ok(int mode, int64_t I, int64_t J, int64_t K);
 MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R);
 size_t mttkrp_tc_workspace_bytes(const MttkrpTCLaunch& L, int R);
 cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L);
-// Encode the tensor maps of the split planes and allocate the scale buffer.
+// Check the image matches the plan and allocate the per-launch buffers.
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t);
 void mttkrp_tc_unbind(MttkrpTCLaunch& L);
 // Optional ridge work done by one extra CTA of the MTTKRP grid, concurrently
@@ -76,6 +85,8 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
                              const double* B, const double* C, const double* colmax3, double* ws,
                              const int* stop_flag, cudaStream_t stream,
                              const TcRidge* ridge = nullptr);
+// diagnostics (NTF_TC_DEBUG & 256): per-CTA globaltimer stamps of the last launch
+int tc_debug_read_times(unsigned long long* host, int ctas);
 // out[r] = max_i |F[i][r]|
 cudaError_t colmax_launch(const double* F, int64_t rows, int R, double* out, cudaStream_t stream);
 
