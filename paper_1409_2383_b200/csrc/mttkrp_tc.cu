@@ -61,7 +61,10 @@ __host__ __device__ constexpr int epi_warps(int NT) {
   return NT <= 2 ? 4 : ((NT == 6 || NT == 8) ? 16 : 8);
 }
 // warps: 0 X TMA, 1 MMA, 2 F_hi rows, epilogue (which also forms W)
-__host__ __device__ constexpr int tc_threads(int NT) { return (3 + epi_warps(NT)) * 32; }
+// warps: 0 X producer, 1 and 3 MMA issuers (alternate units; warp 3 idle
+// when only one accumulator set fits), 2 W slices + F_hi rows, 4.. epilogue
+// (warp & 3 = its TMEM lane quarter)
+__host__ __device__ constexpr int tc_threads(int NT) { return (4 + epi_warps(NT)) * 32; }
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
@@ -268,8 +271,14 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
 
 // Accumulator set: 3N fp32 TMEM columns [ACC0 | ACC1 | ACC2].  As many sets
 // as fit (up to 4) so the MMA runs ahead of the epilogue.
-__host__ __device__ constexpr int acc_bufs(int N) {
+__host__ __device__ constexpr int acc_bufs_fit(int N) {
   return 512 / (3 * N) >= 4 ? 4 : 512 / (3 * N);
+}
+// MMA issuer warps: two (alternate units, each with its own X ring and its
+// own accumulator sets) whenever two or more sets fit; an even set count then.
+__host__ __device__ constexpr int mma_issuers(int N) { return acc_bufs_fit(N) >= 2 ? 2 : 1; }
+__host__ __device__ constexpr int acc_bufs(int N) {
+  return mma_issuers(N) == 2 ? (acc_bufs_fit(N) & ~1) : 1;
 }
 
 __host__ __device__ constexpr uint32_t tmem_cols(int N) {
@@ -347,9 +356,10 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : 8;
   static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
+  constexpr int kIssuers = mma_issuers(N);
   constexpr int kXTile = kTM * kBK * 2;    // 16 KB per plane
   constexpr int kWlb = 3 * N * kBK * 2;    // T0|T1|T2 of one l block
-  constexpr int kFirstEpi = 3;
+  constexpr int kFirstEpi = 4;
   const uint64_t g_entry = gtimer();
   pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
@@ -409,14 +419,14 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   if (threadIdx.x == 0) {
     for (int s = 0; s < SX; ++s) {
       mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1);  // MMA commit
+      mbar_init(&x_empty[s], kIssuers);  // owner's MMA commit (+ the other issuer's arrive)
     }
     for (int s = 0; s < SH; ++s) {
       mbar_init(&h_full[s], 1);
       mbar_init(&h_empty[s], kEpi);
     }
     mbar_init(w_full, 1);
-    mbar_init(w_empty, 1);
+    mbar_init(w_empty, kIssuers);  // one commit per MMA issuer
     for (int s = 0; s < kAccBufs; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], kEpi);
@@ -462,6 +472,10 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       const int64_t unit_bytes = has_tail ? (nl - 1) * int64_t(blk_full) + blk_tail : nl * int64_t(blk_full);
       off += static_cast<int64_t>(u0.o) * unit_bytes;
     }
+    // One X ring in stream order.  With two issuers a slot is released
+    // when BOTH have passed it (x_empty counts 2: the owner's commit after its
+    // MMAs, the other issuer's arrive after observing the load), so neither
+    // can fall a full ring behind and every parity wait stays unambiguous.
     Ring xr;
     UnitIt ui = u0;
     for (int u = u_begin; u < u_end; ++u) {
@@ -485,8 +499,9 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       ui.next(n_o);
     }
     t_role = gtimer();
-  } else if (warp == 1) {
-    // ------------------------------ MMA issuer --------------------------------
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------ MMA issuers --------------------------------
+   if (warp == 1 || kIssuers == 2) {  // warp 3 idles when one accumulator set fits
     // Two wide MMAs per K step, each reading its A tile once: the W slices
     // T0|T1|T2 are consecutive N-row blocks of one K-major B operand.
     //   cols [0, 3N) (=|+=) S0 * [T0 | T1 | T2]     cols [N, 3N) += S1 * [T0 | T1]
@@ -505,6 +520,11 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     const uint64_t db_base = smem_desc(wbase, 16, 1024);
     const uint32_t a_kstep = (2 * lbo) >> 4;  // descriptor units (16 B): two chunks per K=16
     const int n_lb = p.n_lb, ct = p.ct;
+    // Issuer warps take alternate units, each with its own accumulator sets
+    // (set b serves units u with u % kAccBufs == b, an even count), and both
+    // walk the shared X ring in order (see the producer).  A single issuing thread is bound by the per-
+    // instruction issue latency of small-N MMAs, not by the tensor pipe.
+    const int mine = warp == 1 ? 0 : 1;
     Ring xr, ar;
     UnitIt ui = u0;
     int cur_g = -1;
@@ -519,16 +539,29 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
         wphase ^= 1u;
         cur_g = ui.g;
       }
+      const int nl = lbs_of(ui.g);
+      const int owner = kIssuers == 2 ? ((u - u_begin) & 1) : 0;
+      if (owner != mine) {  // the other issuer's unit: observe and release its X slots
+        for (int j = 0; j < nl; ++j) {
+          mbar_wait_p(&x_full[xr.idx], xr.phase, wm, wt[0]);
+          if (elect_one()) mbar_arrive(&x_empty[xr.idx]);
+          __syncwarp();
+          xr.next(SX);
+        }
+        ar.next(kAccBufs);
+        ui.next(n_o);
+        continue;
+      }
       mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, wm, wt[1]);
       tc_fence_after();
       const uint32_t d0 = tmem + ar.idx * 3 * N;
       const uint32_t d1 = d0 + N;
-      const int nl = lbs_of(ui.g);
       for (int j = 0; j < nl; ++j) {
-        mbar_wait_p(&x_full[xr.idx], xr.phase, wm, wt[0]);
+        const int slot = xr.idx;
+        mbar_wait_p(&x_full[slot], xr.phase, wm, wt[0]);
         tc_fence_after();
         const int chunks = (ui.g * G + j == n_lb - 1) ? ct : 8;
-        const uint64_t da0 = da_base + static_cast<uint64_t>((xr.idx * 2 * kXTile) >> 4);
+        const uint64_t da0 = da_base + static_cast<uint64_t>((slot * 2 * kXTile) >> 4);
         const uint64_t da1 = da0 + static_cast<uint64_t>((static_cast<uint32_t>(chunks) * lbo) >> 4);
         const uint64_t db = db_base + static_cast<uint64_t>((j * kWlb) >> 4);
         if (elect_one()) {
@@ -545,8 +578,8 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
               }
             }
           }
-          if (plain_arrive) mbar_arrive(&x_empty[xr.idx]);  // profiling: no tensor-pipe commit
-          else tc_commit(&x_empty[xr.idx]);
+          if (plain_arrive) mbar_arrive(&x_empty[slot]);  // profiling: no tensor-pipe commit
+          else tc_commit(&x_empty[slot]);
         }
         __syncwarp();
         xr.next(SX);
@@ -560,6 +593,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       ui.next(n_o);
     }
     t_role = gtimer();
+   }
   } else if (warp == 2) {
     // ------- W slices of each group + F_hi pair rows (bulk copies, many in flight) -------
     // Everything from here on reads what the preceding kernels produced
@@ -672,7 +706,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       }
     }
   }
-  if (prof && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && warp <= 3)
+  if (prof && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && warp <= 4)
     printf("tc cta %d warp %d units %d loop %lld wait %lld %lld %lld gt %llu %llu %llu\n", blockIdx.x,
            warp, u_end - u_begin, clock64() - t_start, wt[0], wt[1], wt[2],
            (unsigned long long)g_entry, (unsigned long long)(g_ready - g_entry),

@@ -37,4 +37,4 @@ for mode in map(int, modes):
     q = lambda v: f"{np.median(v):6.1f}/{v.max():6.1f}"
     print(f"{cfg} mode {mode}: ctas {len(t)} units {units.min()}-{units.max()} | entry {q(rel[:,0])} "
           f"ready {q(rel[:,1])} | loop end (med/max) X {q(rel[:,2])} MMA {q(rel[:,3])} "
-          f"Fhi {q(rel[:,4])} epi {q(rel[:,5])} | exit {q(rel[:,6])} us", flush=True)
+          f"Fhi {q(rel[:,4])} MMA2 {q(rel[:,5])} | exit {q(rel[:,6])} us", flush=True)
