@@ -271,8 +271,14 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
 
 // Accumulator set: 3N fp32 TMEM columns [ACC0 | ACC1 | ACC2].  As many sets
 // as fit (up to 4) so the MMA runs ahead of the epilogue.
+// Accumulator set per unit: [ACC0 | ACC1 | ACC2] (3N fp32 columns), or for
+// N > 85 (3N > 256, the MMA N limit) the merged [ACC0 | ACC12] (2N columns):
+// ACC2's terms (2^-11 below ACC1's) are accumulated into ACC1 directly, which
+// loses nothing (ACC1's own fp32 rounding dominates) and lets two sets fit.
+__host__ __device__ constexpr bool merged_acc(int N) { return 3 * N > 256; }
+__host__ __device__ constexpr int set_cols(int N) { return merged_acc(N) ? 2 * N : 3 * N; }
 __host__ __device__ constexpr int acc_bufs_fit(int N) {
-  return 512 / (3 * N) >= 4 ? 4 : 512 / (3 * N);
+  return 512 / set_cols(N) >= 4 ? 4 : 512 / set_cols(N);
 }
 // MMA issuer warps: two (alternate units, each with its own X ring and its
 // own accumulator sets) whenever two or more sets fit; an even set count then.
@@ -282,10 +288,10 @@ __host__ __device__ constexpr int acc_bufs(int N) {
 }
 
 __host__ __device__ constexpr uint32_t tmem_cols(int N) {
-  return acc_bufs(N) * 3 * N <= 32    ? 32
-         : acc_bufs(N) * 3 * N <= 64  ? 64
-         : acc_bufs(N) * 3 * N <= 128 ? 128
-         : acc_bufs(N) * 3 * N <= 256 ? 256
+  return acc_bufs(N) * set_cols(N) <= 32    ? 32
+         : acc_bufs(N) * set_cols(N) <= 64  ? 64
+         : acc_bufs(N) * set_cols(N) <= 128 ? 128
+         : acc_bufs(N) * set_cols(N) <= 256 ? 256
                                       : 512;
 }
 
@@ -511,8 +517,8 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     const bool no_mma = (dbg & 2) != 0, plain_arrive = (dbg & 64) != 0;
     // N' <= 256 per MMA: for N > 85 the first MMA is split into S0*[T0|T1]
     // and S0*T2 (the S0 tile is then read twice)
-    constexpr bool kSplit = 3 * N > 256;
-    const uint32_t idesc3 = make_idesc(kSplit ? 2 * N : 3 * N, false);
+    constexpr bool kMerged = merged_acc(N);
+    const uint32_t idesc3 = make_idesc(kMerged ? 2 * N : 3 * N, false);
     const uint32_t idesc2 = make_idesc(2 * N, false);
     const uint32_t idesc1 = make_idesc(N, false);
     const uint32_t lbo = static_cast<uint32_t>(r8) * 16u;
@@ -554,7 +560,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       }
       mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, wm, wt[1]);
       tc_fence_after();
-      const uint32_t d0 = tmem + ar.idx * 3 * N;
+      const uint32_t d0 = tmem + ar.idx * set_cols(N);
       const uint32_t d1 = d0 + N;
       for (int j = 0; j < nl; ++j) {
         const int slot = xr.idx;
@@ -570,11 +576,19 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
             for (int kk = 0; kk < kBK / kUK; ++kk) {
               if (2 * kk < chunks) {
                 const uint32_t first = (j | kk) ? 1u : 0u;
-                tc_mma_f16(d0, da0 + kk * a_kstep, db + kk * (32 >> 4), idesc3, first);
-                if constexpr (kSplit)  // S0*T2 into ACC2 (B rows [2N, 3N))
-                  tc_mma_f16(d0 + 2 * N, da0 + kk * a_kstep,
-                             db + kk * (32 >> 4) + static_cast<uint64_t>((2 * N * 128) >> 4), idesc1, first);
-                tc_mma_f16(d1, da1 + kk * a_kstep, db + kk * (32 >> 4), idesc2, 1u);
+                const uint64_t b = db + kk * (32 >> 4);
+                if constexpr (kMerged) {
+                  // [ACC0|ACC12] = S0*[T0|T1]; ACC12 += S0*T2 + S1*T0 + S1*T1
+                  constexpr uint64_t kT1 = (N * 128) >> 4, kT2 = (2 * N * 128) >> 4;
+                  tc_mma_f16(d0, da0 + kk * a_kstep, b, idesc3, first);
+                  tc_mma_f16(d1, da0 + kk * a_kstep, b + kT2, idesc1, 1u);
+                  tc_mma_f16(d1, da1 + kk * a_kstep, b, idesc1, 1u);
+                  tc_mma_f16(d1, da1 + kk * a_kstep, b + kT1, idesc1, 1u);
+                } else {
+                  // [ACC0|ACC1|ACC2] = S0*[T0|T1|T2]; [ACC1|ACC2] += S1*[T0|T1]
+                  tc_mma_f16(d0, da0 + kk * a_kstep, b, idesc3, first);
+                  tc_mma_f16(d1, da1 + kk * a_kstep, b, idesc2, 1u);
+                }
               }
             }
           }
@@ -662,16 +676,20 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       }
       if (p.debug & 1024) asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
       tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * 3 * N + c0;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * set_cols(N) + c0;
       const float2* hs = hbase + hr.idx * N + c0;
       if (!(p.debug & 4)) {
 #pragma unroll
         for (int j = 0; j < NC / LW; ++j) {
           float a0[LW], a1[LW], a2[LW];
           tmem_ld<LW>(taddr + j * LW, a0);           // ACC0: S0*T0 (exact integers)
-          tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*T0
-          tmem_ld<LW>(taddr + 2 * N + j * LW, a2);   // ACC2: S0*T2 + S1*T1
+          tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*T0 (+ ACC2 when merged)
+          if constexpr (!merged_acc(N)) tmem_ld<LW>(taddr + 2 * N + j * LW, a2);  // ACC2: S0*T2 + S1*T1
           tmem_wait_ld();
+          if constexpr (merged_acc(N)) {
+#pragma unroll
+            for (int v = 0; v < LW; ++v) a2[v] = 0.f;
+          }
 #pragma unroll
           for (int v = 0; v < LW; ++v) {
             const float2 h = hs[j * LW + v];
@@ -953,17 +971,26 @@ cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
   }
 }
 
-// Split units [0, n_g * n_o) (g-major, unit (g, o) costs lbs(g) l blocks)
-// into `parts` contiguous ranges of about equal cost.
+// Split units [0, n_g * n_o) (g-major) into `parts` contiguous ranges of
+// about equal cost.  A unit costs its streamed bytes (in full-block units:
+// the last l block stores only ct of 8 chunks) plus a fixed per-unit share
+// for its accumulator drain and handshakes, which grows with N.
 void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
   const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
-  auto lbs = [&](int g) { return std::min(L.G, L.n_lb - g * L.G); };
-  const double total = static_cast<double>(L.n_o) * L.n_lb;
+  double unit_fixed = 2.0 + L.N / 32.0;  // measured: c2 best near 3, R = 64..100 near 4..6
+  if (const char* e = getenv("NTF_TC_UNITCOST")) unit_fixed = atof(e);
+  auto cost = [&](int g) {
+    const int nl = std::min(L.G, L.n_lb - g * L.G);
+    const bool tail = g * L.G + nl == L.n_lb;
+    return (tail ? (nl - 1) + L.ct / 8.0 : nl) + unit_fixed;
+  };
+  double total = 0.0;
+  for (int g = 0; g < L.n_g; ++g) total += cost(g) * L.n_o;
   ub[0] = 0;
   int k = 1;
   double acc = 0.0;
   for (int64_t u = 0; u < units && k < parts; ++u) {
-    acc += lbs(static_cast<int>(u / L.n_o));
+    acc += cost(static_cast<int>(u / L.n_o));
     while (k < parts && acc >= total * k / parts) ub[k++] = static_cast<uint32_t>(u + 1);
   }
   while (k <= parts) ub[k++] = static_cast<uint32_t>(units);
@@ -995,10 +1022,9 @@ bool mttkrp_tc_auto(int x_dtype, int R) {
 }
 
 bool mttkrp_tc_shape_ok(int mode, int64_t I, int64_t J, int64_t K) {
-  // TMA global strides are multiples of 16 B (K % 8 == 0 for the fp16 planes);
-  // coordinates are int32; unit ranges are 32-bit.
-  (void)mode;
-  if (K % 8 != 0) return false;
+  // The block image is written element-wise (no stride constraints); l/o
+  // coordinates and unit ranges are 32-bit.
+  if (I < 1 || J < 1 || K < 1) return false;
   if (I >= (1 << 30) || J >= (1 << 30) || K >= (1 << 30)) return false;
   const int64_t l_ext = mode == 3 ? J : K, o_ext = mode == 1 ? J : I;
   if (((l_ext + kBK - 1) / kBK) * o_ext >= (int64_t(1) << 31)) return false;

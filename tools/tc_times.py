@@ -13,8 +13,13 @@ from paper_1409_2383_b200.engine import mttkrp_device
 
 assert int(os.environ.get("NTF_TC_DEBUG", "0")) & 256
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-modes = sys.argv[2] if len(sys.argv) > 2 else "123"
-w = synth.CONFIGS[cfg]
+if cfg == "custom":  # tc_times.py custom I J K R [modes]
+    I, J, K, R = (int(v) for v in sys.argv[2:6])
+    w = synth.Workload("custom", (I, J, K), R, "float32", 20.0, 1, 1)
+    modes = sys.argv[6] if len(sys.argv) > 6 else "123"
+else:
+    modes = sys.argv[2] if len(sys.argv) > 2 else "123"
+    w = synth.CONFIGS[cfg]
 x = torch.rand(w.dims, dtype=torch.float32, device="cuda")
 f = [torch.rand((d, w.rank), dtype=torch.float64, device="cuda") for d in w.dims]
 lib = _native.load()
