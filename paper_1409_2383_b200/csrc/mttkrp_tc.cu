@@ -2,9 +2,9 @@
 // tensors.  Same contraction as mttkrp_cc.cu (reference tensors.py:254-262):
 //   out[m, n] = sum_o F_hi[o, n] * sum_l X(m, o, l) F_lo[l, n]
 // with (o, l) the two non-m tensor axes:
-//   mode 1: m = i, o = j, l = k   (F_hi, F_lo) = (B, C)   A tile K-major
-//   mode 2: m = j, o = i, l = k   (F_hi, F_lo) = (A, C)   A tile K-major
-//   mode 3: m = k, o = i, l = j   (F_hi, F_lo) = (A, B)   A tile MN-major (X^T)
+//   mode 1: m = i, o = j, l = k   (F_hi, F_lo) = (B, C)
+//   mode 2: m = j, o = i, l = k   (F_hi, F_lo) = (A, C)
+//   mode 3: m = k, o = i, l = j   (F_hi, F_lo) = (A, B)
 //
 // Numerics: exact fixed-point slicing on kind::f16 MMAs.
 //   X    = xs * (S0 + S1)        S0 integers |S0| <= 2^11, S1 in 2^-11 units,
@@ -14,28 +14,33 @@
 //                                subnormal), ls(n) = 2^(f(n)-t) per column
 // The tensor core forms, per unit of G consecutive 64-wide l blocks at one o,
 //   ACC0 = sum S0*T0                       integers < 2^24: EXACT in fp32
-//   ACC1 = sum S0*T1 + S1*T0,  ACC2 = sum S0*T2 + S1*T1   (corrections)
+//   ACC1 = sum S0*T1 + S1*T0,  ACC2 = sum S0*T2 + S1*T1   (corrections;
+//   for N > 85 ACC2's terms go straight into ACC1: two sets of 2N columns fit)
 // with t = 7 - log2(G) keeping |ACC0| <= 2^11 * 2^t * 64G <= 2^24.  F_lo is
 // represented to 2^-(22+t) of its column maximum (27-28 bits); the dropped
 // S1*T2 term is ~2^-33.  The epilogue multiplies the unit's accumulators by
 // F_hi[o, n] held as an fp32 pair (exact product split with FMA) and
 // accumulates in double-float (TwoSum), so F_hi enters at ~2^-48.
 //
-// Work: a CTA owns one 128-row m-tile and a contiguous range of units
-// (g, o) in g-major order, g = group of G l-blocks.  The W slices of a group
-// do not depend on o, so they are formed once per group (usually once per
-// CTA) and stay resident; the CTA then streams X tiles through a TMA ring and
-// the epilogue drains TMEM once per unit instead of once per 64 q.
+// Data layout: the split tensor is stored once per mode as a BLOCK IMAGE
+// (image_split_kernel): for each m-tile and unit (g, o) in g-major order, each
+// l block is the no-swizzle K-major UMMA image of both planes.  A CTA owns one
+// m-tile and a contiguous range of units, so it streams ONE contiguous byte
+// range with 1-D bulk copies (long sequential DRAM runs; the natural layout's
+// 128-byte row pieces ran at 4.4-4.8 TB/s, the image at 6.7).  The W slices of
+// a group do not depend on o: formed once per MTTKRP (w_slice_kernel) and
+// bulk-copied into shared memory once per group; the epilogue drains TMEM
+// once per unit.
 //
 // Roles (one CTA per SM, mbarrier handshakes, all ring indices incremental):
-//   warp 0        TMA producer: S0/S1 tiles (128B-swizzled)
-//   warp 1        TMEM allocator + single-thread MMA issuer (tcgen05.mma)
-//   warp 2        F_hi rows of the coming units -> scaled fp32 pairs (smem ring)
-//   warps 3..     epilogue, 4, 8 or 16 warps (1, 2 or 4 column groups per
-//                 TMEM lane quarter, by N).  At each group start it forms the W slices
-//                 T0|T1|T2 of the group's F_lo rows (UMMA K-major SW128 layout);
-//                 per unit: tcgen05.ld, F_hi scaling, double-float
-//                 accumulation; finally the fp64 partial of the CTA.
+//   warp 0        producer: one bulk copy per X block into an SX-stage ring
+//   warps 1, 3    MMA issuers on alternate units (a single issuing thread is
+//                 bound by per-instruction issue latency for small-N MMAs);
+//                 each owns its accumulator sets, both release X slots
+//   warp 2        W slices of each group + F_hi pair rows (bulk copies)
+//   warps 4..     epilogue, 4, 8 or 16 warps (1, 2 or 4 column groups per
+//                 TMEM lane quarter, by N): per unit tcgen05.ld, F_hi scaling,
+//                 double-float accumulation; finally the fp64 partial of the CTA.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
