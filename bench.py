@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sharded", action="store_true",
+                    help="one GPU: run the sharded engine on a one-rank NCCL group")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="diagnostic: no per-kernel events in the graph (no roofline)")
     return ap.parse_args()
@@ -118,14 +120,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload_config(w, world, engine, rho0):
+def workload_config(w, world, engine, rho0, sharded=False):
     return {
         "workload": f"{w.name}: {w.dims[0]}x{w.dims[1]}x{w.dims[2]} {w.dtype}, R={w.rank}, "
                     f"{w.inner} inner sweeps/outer, {w.snr_db:g} dB, stopping off",
         "dims": list(w.dims), "rank": w.rank, "inner_sweeps": w.inner,
         "outer_iterations_in_config": w.outer, "rho_init": "trace((C0^T C0)*(B0^T B0))/R",
         "rho_init_value": rho0, "engine": engine,
-        "parallelism": "single-gpu" if world == 1 else f"slab-sharded x{world} (NCCL all-gather)",
+        "parallelism": (f"slab-sharded x{world} (NCCL all-gather, graph-captured iteration)"
+                        if sharded else "single-gpu"),
         "l2": "inputs larger than L2: every MTTKRP streams the whole tensor "
               f"({math.prod(w.dims) * (4 if w.dtype == 'float32' else 8) / 2**20:.0f} MiB)",
         "data": "synthetic seeded (SURVEY 8(d) generator), data seed derive_seed(0,101,0)",
@@ -240,8 +243,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    sharded = world > 1 or args.sharded
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+    elif args.sharded:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+                                device_id=device)
     w = synth.CONFIGS[args.config]
     engine = P.solver._engine_code(args.engine)
     dseed, fseed = synth.seeds()
@@ -253,7 +260,7 @@ def main():
     cap = args.warmup + args.steps + 1
     cfg = P.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=cap, max_restarts=0,
                          inner_sweeps=w.inner, rho_init=rho0)
-    if world == 1:
+    if not sharded:
         x = x_host.to(device)
         prob = DeviceProblem(x, w.dims, w.rank, cfg, history_capacity=cap, engine=engine)
         slab_elems = [math.prod(w.dims)] * 3
@@ -279,7 +286,7 @@ def main():
         prob.set_timing(timed_last and i == args.warmup - 1)
         prob.step()
     prob.stream.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -294,7 +301,7 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     t_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
-    if world > 1:
+    if sharded:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
         dist.barrier()
     t_ms = float(t_ms.item())
@@ -330,7 +337,7 @@ def main():
     prob.set_timing(False)
     prob.close()  # the e2e leg below is a fresh user call: release this plan first
     del prob
-    if world == 1:
+    if not sharded:
         del x
     torch.cuda.synchronize()
 
@@ -339,10 +346,14 @@ def main():
     if not args.no_e2e:
         cfg_e = P.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=w.outer,
                                max_restarts=0, inner_sweeps=w.inner, rho_init=rho0)
-        fitfn = P.fit if world == 1 else P.distributed_fit
+        if sharded:
+            def fitfn(t, r, s_, c):
+                return P.distributed_fit(t, r, s_, c, sharded=True)
+        else:
+            fitfn = P.fit
         fitfn(P.DenseTensor(x_host), w.rank, None, cfg_e)  # warm-up
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
         t0 = time.perf_counter()
         res = None
@@ -350,7 +361,7 @@ def main():
             res = fitfn(P.DenseTensor(x_host), w.rank, None, cfg_e)
         torch.cuda.synchronize()
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=device)
-        if world > 1:
+        if sharded:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         el = float(el.item())
         h2d = x_host.numel() * x_host.element_size() + 8 * w.rank * sum(w.dims) * 3 + 24
@@ -374,12 +385,14 @@ def main():
         # Gram reduction (side stream); per step: 3 norm reductions + finalize
         tc = w.dtype == "float32" and w.rank <= 64 and args.engine != "cuda_core"
         launches_per_step = w.inner * 3 * (4 + (1 if tc else 0)) + 3 + 1
+        if sharded:  # + Gram refresh (partial + reduce) and column maxima per mode update
+            launches_per_step += w.inner * 3 * 3
         out = {
             "metric": "ntf_outer_iters_per_sec", "value": value, "unit": "outer_it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if w.dtype == "float32" else "f64", "data": "synthetic",
-            "config": workload_config(w, world, args.engine, rho0),
+            "config": workload_config(w, world, args.engine, rho0, sharded),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "MTTKRP op (fp32: W-slice + tcgen05 kernels; fp64: CUDA-core kernel), all modes: "
@@ -395,7 +408,7 @@ def main():
             "iterations_run": done,
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

@@ -91,20 +91,26 @@ class Comm:
     def gather_rows(self, full, offsets: Sequence[int], counts: Sequence[int]) -> None:
         """In place: every rank's owned block of ``full`` (rows offsets[p] ..
         +counts[p]) is broadcast to all ranks.  Blocks are padded to the
-        largest count because the uniform plan is uneven (SURVEY 7.3 #7)."""
-        import torch
-
+        largest count because the uniform plan is uneven.
+        The staging buffers are allocated once per target tensor, so the call
+        can be captured in a CUDA graph."""
         maxc = max(counts)
         p = self.rank
-        send = full.new_zeros((maxc,) + tuple(full.shape[1:]))
+        key = (full.data_ptr(), tuple(full.shape), maxc)
+        bufs = self._bufs.get(key) if hasattr(self, "_bufs") else None
+        if bufs is None:
+            if not hasattr(self, "_bufs"):
+                self._bufs = {}
+            send = full.new_zeros((maxc,) + tuple(full.shape[1:]))
+            recv = full.new_empty((self.size * maxc,) + tuple(full.shape[1:]))
+            bufs = self._bufs[key] = (send, recv)
+        send, recv = bufs
         send[: counts[p]].copy_(full[offsets[p]: offsets[p] + counts[p]])
-        recv = full.new_empty((self.size * maxc,) + tuple(full.shape[1:]))
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
         for q in range(self.size):
             if q == p:
                 continue
             full[offsets[q]: offsets[q] + counts[q]].copy_(recv[q * maxc: q * maxc + counts[q]])
-        del torch
 
 
 def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
@@ -123,7 +129,7 @@ def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
 
 
 def _sharded_problem_class():
-    from .engine import DeviceProblem, Slabs, gram_device, mttkrp_device, sq_error
+    from .engine import DeviceProblem, Slabs, gram_device, mttkrp_device, sq_error  # noqa: F401
 
     class ShardedProblem(DeviceProblem):
         def __init__(self, x_slabs, dims, rank, config, cap, engine, plan: PartitionPlan, comm: Comm):
@@ -136,11 +142,52 @@ def _sharded_problem_class():
             own_cnt = tuple(self.counts[m][p] for m in range(3))
             super().__init__(x_slabs[0], dims, rank, config, cap, engine,
                              slabs=Slabs(list(x_slabs), own_off, own_cnt), norm_parts=comm.size)
+            import os
+
+            self._graph = None
+            self._eager_steps = 0
+            self._graph_ok = os.environ.get("NTF_B200_SHARDED_GRAPH", "1") != "0"
+            for m in range(3):  # capture-safe: Gram workspace allocated up front
+                self._ensure_gram_ws(m)
+            # per-launch timing events stay on (they are captured into the
+            # graph), so kernel_times() always reflects the latest iteration
+            super().set_timing(True)
+
+        def set_timing(self, enable: bool) -> None:
+            """Timing events are always recorded on the sharded path."""
 
         def step(self) -> None:
+            """One outer iteration.  After two eager iterations (NCCL
+            communicators and staging buffers exist by then) the iteration --
+            mode updates, row all-gathers, Gram refreshes, norm gather and
+            finalize -- is captured once as a CUDA graph and replayed, so the
+            host issues one launch per outer iteration instead of ~10 per mode
+            update.  NTF_B200_SHARDED_GRAPH=0 keeps the eager loop."""
             torch = self.torch
+            if self._graph is None and self._graph_ok and self._eager_steps >= 2:
+                self._capture()
+            if self._graph is not None:
+                with torch.cuda.stream(self.stream):
+                    self._graph.replay()
+                return
             with torch.cuda.stream(self.stream):
                 sharded_iteration(self, self.comm, self.config)
+            self._eager_steps += 1
+
+        def _capture(self) -> None:
+            import warnings
+
+            torch = self.torch
+            g = torch.cuda.CUDAGraph()
+            self.stream.synchronize()
+            try:
+                with torch.cuda.graph(g, stream=self.stream):
+                    sharded_iteration(self, self.comm, self.config)
+            except Exception as exc:  # capture unsupported: stay eager (same results)
+                self._graph_ok = False
+                warnings.warn(f"sharded iteration not captured as a CUDA graph ({exc}); running eagerly")
+                return
+            self._graph = g
 
         def final_sq_error(self, aux):
             torch = self.torch
@@ -203,11 +250,13 @@ def make_slabs(values, plan: PartitionPlan, rank_id: int, device):
 
 def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None,
                     plan: PartitionPlan | int | None = None, trace_path: str | None = None,
-                    *, engine=None, group=None) -> FitResult:
+                    *, engine=None, group=None, sharded: bool | None = None) -> FitResult:
     """Block-parallel fit over the ranks of ``torch.distributed`` (reference
     mesh.distributed_fit, mesh.py:331-350).  Without an initialised process
-    group (or with one rank) this is exactly ``fit``.  ``trace_path`` (the
-    simulator's message trace) has no NCCL equivalent and is ignored."""
+    group (or with one rank) this is exactly ``fit``, unless ``sharded=True``
+    forces the sharded engine (a one-rank group exercises its collectives and
+    graph capture on a single GPU).  ``trace_path`` (the simulator's message
+    trace) has no NCCL equivalent and is ignored."""
     import torch
     import torch.distributed as dist
 
@@ -218,7 +267,8 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     normalize_specs(specs, t.order)
     if rank < 1:
         raise ValueError("rank must be >= 1")
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not (dist.is_available() and dist.is_initialized()) or (
+            dist.get_world_size(group) == 1 and not sharded):
         return fit(t, rank, specs, config, engine=engine)
     comm = Comm(group)
     if plan is None or isinstance(plan, int):

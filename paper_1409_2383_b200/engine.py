@@ -178,7 +178,7 @@ class DeviceProblem:
             self.norm_acc = torch.zeros(30, dtype=f64, device=dev)
             # every shard's norm_acc, gathered before finalize (sharded runs)
             self.norm_all = (torch.zeros(norm_parts * 30, dtype=f64, device=dev)
-                             if norm_parts > 1 else None)
+                             if norm_parts > 1 or self.sharded else None)
             cap = max(1, int(history_capacity))
             self.cap = cap
             self.resid_hist = torch.zeros((cap, 6), dtype=f64, device=dev)
@@ -296,14 +296,17 @@ class DeviceProblem:
     def finalize(self) -> None:
         N.check(self.lib.ntf_plan_finalize(self._plan, self._sh))
 
+    def _ensure_gram_ws(self, m: int) -> None:
+        wsb = self.lib.ntf_gram_workspace_bytes(self.dims[m], self.R)
+        if not hasattr(self, "_gram_ws") or self._gram_ws.numel() * 8 < wsb:
+            torch = self.torch
+            with torch.cuda.stream(self.stream):
+                self._gram_ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=self.device)
+
     def refresh_gram(self, m: int) -> None:
         lib = self.lib
         rows = self.dims[m]
-        torch = self.torch
-        wsb = lib.ntf_gram_workspace_bytes(rows, self.R)
-        if not hasattr(self, "_gram_ws") or self._gram_ws.numel() * 8 < wsb:
-            with torch.cuda.stream(self.stream):
-                self._gram_ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=self.device)
+        self._ensure_gram_ws(m)
         N.check(lib.ntf_gram(_ptr(self.factors[m]), rows, self.R, _ptr(self.grams[m]),
                              _ptr(self._gram_ws), self._gram_ws.numel() * 8, self._sh))
         N.check(lib.ntf_colmax(_ptr(self.factors[m]), rows, self.R,

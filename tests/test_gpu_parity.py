@@ -296,3 +296,36 @@ def test_library_is_the_one_loaded():
 
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libntf_b200.so" in maps
+
+
+def test_sharded_engine_one_rank_nccl_graph(golden_small, tmp_path, monkeypatch):
+    """The sharded engine (slab images, row all-gathers, norm gather, the
+    graph-captured outer iteration) on a one-rank NCCL group: per-iteration
+    factors within 1e-9 of the oracle, and the captured iteration bitwise equal
+    to the eager one (NTF_B200_SHARDED_GRAPH=0)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        g = golden_small
+        kw = dict(MESH2_CFG)
+        kw["n_max"] = max(int(kw.get("n_max", 0)), 8)
+        want = O.fit(g["mesh2_x"], 3, O.Config(**kw))
+        import warnings
+
+        with warnings.catch_warnings():  # the graph capture must succeed (no eager fallback)
+            warnings.filterwarnings("error", message="sharded iteration not captured")
+            got = P.distributed_fit(g["mesh2_x"], 3, None, P.SolverConfig(**kw), plan=1,
+                                    sharded=True)
+        monkeypatch.setenv("NTF_B200_SHARDED_GRAPH", "0")
+        eager = P.distributed_fit(g["mesh2_x"], 3, None, P.SolverConfig(**kw), plan=1, sharded=True)
+        assert len(got.factor_history) == len(want.factor_history) >= 4
+        for it in range(len(want.factor_history)):
+            for m in range(3):
+                assert rel(got.factor_history[it][m], want.factor_history[it][m]) <= 1e-9
+                assert np.array_equal(got.factor_history[it][m], eager.factor_history[it][m])
+        assert got.residual_history == eager.residual_history
+    finally:
+        dist.destroy_process_group()
