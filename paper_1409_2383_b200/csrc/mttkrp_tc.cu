@@ -16,7 +16,7 @@
 //   ACC0 = sum S0*T0                       integers < 2^24: EXACT in fp32
 //   ACC1 = sum S0*T1 + S1*T0,  ACC2 = sum S0*T2 + S1*T1   (corrections;
 //   for N > 85 ACC2's terms go straight into ACC1: two sets of 2N columns fit)
-// with t = 7 - log2(G) keeping |ACC0| <= 2^11 * 2^t * 64G <= 2^24.  F_lo is
+// with t = 7, 6, 5 for G = 1, 2, 3..4 keeping |ACC0| <= 2^11 * 2^t * 64G <= 2^24.  F_lo is
 // represented to 2^-(22+t) of its column maximum (27-28 bits); the dropped
 // S1*T2 term is ~2^-33.  The epilogue multiplies the unit's accumulators by
 // F_hi[o, n] held as an fp32 pair (exact product split with FMA) and
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
     // max|F_hi[:,n]| < 2^e (the same clamps as w_slice_kernel)
     for (int n = lane; n < N; n += 32) {
-      const int t = G >= 4 ? 5 : (G >= 2 ? 6 : 7);
+      const int t = G >= 3 ? 5 : (G >= 2 ? 6 : 7);
       int f = 0, e = 0;
       const double cl = n < R ? p.cm_lo[n] : 0.0, ch = n < R ? p.cm_hi[n] : 0.0;
       if (cl > 0.0) frexp(cl, &f);
@@ -1050,8 +1050,7 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.n_lb = (L.l_ext + kBK - 1) / kBK;
   L.threads = tc_threads(L.N / 16);
   // Shared memory: X ring (32 KB per l block) + resident W slices of a group
-  // (G blocks x 3N x 128 B) + F_hi pair ring.  Largest G (fewest epilogue
-  // drains) that still leaves a 4-deep X ring; then as deep an X ring as fits.
+  // (G blocks x 3N x 128 B) + F_hi pair ring; then as deep an X ring as fits.
   const int xs = 2 * kTM * kBK * 2;
   L.h_stages = 8;
   auto total = [&](int G, int SX) {
@@ -1059,15 +1058,19 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
            (2 * SX + 2 * L.h_stages + 12) * 8 + 16 + 3 * L.N * 8;
   };
   const int limit = 227 * 1024;
+  // Largest G (fewest drains) with a 3-deep X ring (2-deep for N >= 96,
+  // whose epilogue, not the stream, is the bound); measured: c3 G=4/3
+  // stages 668 us vs G=2/4 stages 757 us, 1000^3 R=100 G=3/2 stages 1016 vs 1083.
+  int min_stages = L.N >= 96 ? 2 : 3;
+  if (const char* e = getenv("NTF_TC_MINSTAGES")) min_stages = atoi(e);
   L.G = 1;
-  for (int G : {4, 2, 1})
-    if (total(G, 4) <= limit) {
+  for (int G : {4, 3, 2, 1})
+    if (total(G, min_stages) <= limit) {
       L.G = G;
       break;
     }
   if (const char* e = getenv("NTF_TC_G")) L.G = atoi(e);
   L.G = std::max(1, std::min(L.G, L.n_lb));
-  if (L.G == 3) L.G = 2;
   L.x_stages = 6;
   if (const char* e = getenv("NTF_TC_XSTAGES")) L.x_stages = atoi(e);
   while (total(L.G, L.x_stages) > limit && L.x_stages > 2) --L.x_stages;
@@ -1282,7 +1285,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     p.cm_lo = L.wscale + L.R;
   }
   {
-    const int t = L.G >= 4 ? 5 : (L.G >= 2 ? 6 : 7);
+    const int t = L.G >= 3 ? 5 : (L.G >= 2 ? 6 : 7);
     const int total = std::max(L.n_lb * L.N * (kBK / 8), L.n_o * L.N);
     const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
     if (!(p.debug & 128)) {

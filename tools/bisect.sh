@@ -1,2 +1,5 @@
-for d in 0 16 22 6 18 20; do NTF_TC_DEBUG=$d timeout 60 python tools/time_modes.py c2 2>&1 | tail -1 | cut -c1-100; done
-for d in 32 48; do NTF_TC_DEBUG=$d timeout 120 python tools/time_modes.py c2 > gpurun_out/w_$d.log 2>&1; done
+run() { echo "== $C $*"; env "$@" timeout 60 python tools/time_modes.py $C 2>&1 | tail -1 | cut -c1-110; }
+C=c2; run NTF_TC_MINSTAGES=4; run NTF_TC_MINSTAGES=3
+C=c3; run NTF_TC_MINSTAGES=4; run NTF_TC_MINSTAGES=3; run NTF_TC_G=4 NTF_TC_XSTAGES=3; run NTF_TC_G=2
+C="custom auto 1000 1000 1000 100 1"; run NTF_TC_MINSTAGES=4; run NTF_TC_G=3 NTF_TC_XSTAGES=2; run NTF_TC_MINSTAGES=2
+C=c4; run NTF_TC_MINSTAGES=4; run NTF_TC_MINSTAGES=3
