@@ -320,8 +320,10 @@ struct TcParams {
                              // by the row update that follows (NULL: untouched)
   double* ws;                // [splits][M][R] partials
   const int* stop_flag;
-  int debug;                 // profiling only (NTF_TC_DEBUG): 1 skip W forming,
-                             // 2 skip MMA, 4 skip TMEM drain, 16 skip X TMA
+  int debug;                 // profiling only (NTF_TC_DEBUG): 2 skip MMA, 4 skip TMEM
+                             // drain, 16 skip X loads, 32 per-role wait cycles,
+                             // 64 plain arrives for commits, 128 skip W slicing,
+                             // 256 per-CTA globaltimer stamps, 2048 sleeping waits
   unsigned long long* times;  // NTF_TC_DEBUG & 256: per-CTA globaltimer stamps [8]
   TcRidge ridge;              // extra CTA (gridDim.x - 1) when ridge.out != NULL
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
@@ -675,11 +677,8 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     }
     Ring ar, hr;
     for (int u = u_begin; u < u_end; ++u) {
-      if (!(p.debug & 1024) || e == 0) {  // 1024: one polling warp, named barrier for the rest
-        mbar_wait_p(&acc_full[ar.idx], ar.phase, wm, wt[0]);
-        mbar_wait_p(&h_full[hr.idx], hr.phase, wm, wt[1]);
-      }
-      if (p.debug & 1024) asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
+      mbar_wait_p(&acc_full[ar.idx], ar.phase, wm, wt[0]);
+      mbar_wait_p(&h_full[hr.idx], hr.phase, wm, wt[1]);
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * set_cols(N) + c0;
       const float2* hs = hbase + hr.idx * N + c0;
