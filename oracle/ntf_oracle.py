@@ -227,12 +227,21 @@ def ridge_factor(gram: np.ndarray, rho: float):
         raise InvalidPenalty(str(exc)) from exc
 
 
-def factor_update(t: OracleTensor, factors, aux, dual, rho: float, mode: int) -> np.ndarray:
-    """solver.py:207-219 + 178-188 — MTTKRP, ridge Cholesky, rhs, row solve."""
+def factor_update(t: OracleTensor, factors, aux, dual, rho: float, mode: int,
+                  row_sum_one: bool = False) -> np.ndarray:
+    """solver.py:207-219 + 178-193 — MTTKRP, ridge Cholesky, rhs, row solve;
+    with ``row_sum_one`` (row_stochastic modes) the per-row Lagrange
+    correction m = sol + lam g1, g1 = (G+rho I)^-1 1, lam = (1 - sol 1)/sum(g1)."""
     m = mttkrp(t, factors, mode)
     cho = ridge_factor(companion_gram(factors, mode), rho)
     rhs = m + rho * aux - dual
-    return cho_solve(cho, rhs.T).T
+    sol = cho_solve(cho, rhs.T).T
+    if not row_sum_one:
+        return sol
+    ones = np.ones(rhs.shape[1])
+    g1 = cho_solve(cho, ones)
+    lam = (1.0 - sol @ ones) / float(g1.sum())
+    return sol + lam[:, None] * g1[None, :]
 
 
 def project_nonneg(x: np.ndarray) -> np.ndarray:
@@ -240,6 +249,64 @@ def project_nonneg(x: np.ndarray) -> np.ndarray:
     if not np.all(np.isfinite(x)):
         raise ValueError("cannot project a matrix with non-finite entries")
     return np.maximum(x, 0.0)
+
+
+_EPS = float(np.finfo(np.float64).eps)
+
+
+def simplex_rows(m: np.ndarray) -> np.ndarray:
+    """constraints.py:72-92 — per-row projection onto the probability simplex
+    (sort-and-threshold); rows already feasible (min >= 0, |sum - 1| <= 8 eps n)
+    are returned unchanged."""
+    m = np.asarray(m, dtype=np.float64)
+    n = m.shape[1]
+    u = -np.sort(-m, axis=1)
+    css = np.cumsum(u, axis=1)
+    j = np.arange(1, n + 1)
+    k = np.count_nonzero(u * j > css - 1.0, axis=1)
+    theta = (css[np.arange(m.shape[0]), k - 1] - 1.0) / k
+    out = np.maximum(m - theta[:, None], 0.0)
+    feasible = (m.min(axis=1) >= 0.0) & (np.abs(m.sum(axis=1) - 1.0) <= 8.0 * _EPS * n)
+    out[feasible] = m[feasible]
+    return out
+
+
+def card_keep(m: np.ndarray, c: int) -> np.ndarray:
+    """constraints.py:95-102 — clamp, then keep the c largest entries of the
+    whole matrix; ties keep the smaller row-major index."""
+    clamped = np.maximum(m, 0.0)
+    if c >= clamped.size:
+        return clamped
+    flat = clamped.reshape(-1)
+    order = np.lexsort((np.arange(flat.size), -flat))[:c]
+    out = np.zeros_like(flat)
+    out[order] = flat[order]
+    return out.reshape(m.shape)
+
+
+def spec_of(spec) -> tuple:
+    """(kind, card) from a ConstraintSpec-like object, a config-file name or a tuple."""
+    if spec is None:
+        return ("nonneg", None)
+    if isinstance(spec, tuple):
+        return spec
+    if isinstance(spec, str):
+        if spec.startswith("nonneg_card:"):
+            return ("nonneg_card", int(spec.split(":", 1)[1]))
+        return (spec, None)
+    return (spec.kind, getattr(spec, "card", None))
+
+
+def project(x: np.ndarray, spec) -> np.ndarray:
+    """constraints.py:105-115 — projection onto the spec's constraint set."""
+    kind, card = spec_of(spec)
+    if not np.all(np.isfinite(x)):
+        raise ValueError("cannot project a matrix with non-finite entries")
+    if kind == "nonneg":
+        return np.maximum(x, 0.0)
+    if kind == "nonneg_card":
+        return card_keep(x, int(card))
+    return simplex_rows(x)
 
 
 def adapt(rho, primal, dual, cfg: Config) -> list:
@@ -267,15 +334,17 @@ def stop_test(primal, dual, st: State, cfg: Config) -> bool:
     return True
 
 
-def iterate(st: State, t: OracleTensor, cfg: Config):
+def iterate(st: State, t: OracleTensor, cfg: Config, specs=None):
     """solver.py:295-327 — sweeps, then aux/dual/residuals/adaptation."""
     n = len(st.factors)
+    specs = [spec_of(s) for s in (specs or [None] * n)]
     f = list(st.factors)
     for _ in range(cfg.inner_sweeps):
         for mode in range(1, n + 1):
             f[mode - 1] = factor_update(t, f, st.aux[mode - 1], st.duals[mode - 1],
-                                        st.rho[mode - 1], mode)
-    aux = [project_nonneg(x + y / r) for x, y, r in zip(f, st.duals, st.rho)]
+                                        st.rho[mode - 1], mode,
+                                        specs[mode - 1][0] == "row_stochastic")
+    aux = [project(x + y / r, sp) for x, y, r, sp in zip(f, st.duals, st.rho, specs)]
     duals = [y + r * (x - a) for y, r, x, a in zip(st.duals, st.rho, f, aux)]
     primal = tuple(float(np.linalg.norm(x - a)) for x, a in zip(f, aux))
     dual = tuple(r * float(np.linalg.norm(a - p)) for r, a, p in zip(st.rho, aux, st.aux))
@@ -294,14 +363,18 @@ def aux_model_rfe(t: OracleTensor, st: State) -> float:
     return math.sqrt(max(sq, 0.0)) / t.norm()
 
 
-def fit(t, rank: int, cfg: Config | None = None) -> Result:
-    """solver.py:340-403 — nonneg specs on every mode (the §8 scope)."""
+def fit(t, rank: int, cfg: Config | None = None, specs=None) -> Result:
+    """solver.py:340-403 — one constraint spec per mode (nonneg by default)."""
     cfg = cfg or Config()
     t = as_oracle_tensor(t)
+    specs = [spec_of(s) for s in (specs or [None] * len(t.dims))]
     if rank < 1:
         raise ValueError("rank must be >= 1")
     if t.norm() == 0.0:
         raise ValueError("cannot factorize a zero tensor")
+    for d, (kind, card) in zip(t.dims, specs):
+        if kind == "nonneg_card" and card > d * rank:
+            raise ValueError(f"cardinality budget {card} exceeds factor size {d}x{rank}")
     total = 0
     converged = False
     attempt = 0
@@ -311,7 +384,7 @@ def fit(t, rank: int, cfg: Config | None = None) -> Result:
         st = init_state(t.dims, rank, cfg, attempt)
         hist, rfes, fhist, rhos = [], [], [], []
         for _ in range(cfg.n_max):
-            st, res = iterate(st, t, cfg)
+            st, res = iterate(st, t, cfg, specs)
             total += 1
             hist.append(res)
             rhos.append(list(st.rho))

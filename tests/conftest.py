@@ -32,6 +32,11 @@ def golden_small():
 
 
 @pytest.fixture(scope="session")
+def golden_constraints():
+    return load_golden("constraints.npz")
+
+
+@pytest.fixture(scope="session")
 def golden_c1():
     return load_golden("c1.npz")
 
@@ -48,6 +53,14 @@ SMALL_CASES = {
     "ragged": dict(seed=2, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, track_factors=True),
     "bigrho": dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=15, max_restarts=0, rho_init=300.0,
                    inner_sweeps=4, track_factors=True),
+}
+# cases of make_golden.constraint_fits (specs are stored in the fixture)
+CONSTRAINT_CASES = {
+    "rowstoch": dict(seed=5, eps_abs=0.0, eps_rel=0.0, n_max=12, max_restarts=0, track_factors=True),
+    "card": dict(seed=6, eps_abs=0.0, eps_rel=0.0, n_max=12, max_restarts=0, track_factors=True),
+    "mixed": dict(seed=7, eps_abs=0.0, eps_rel=0.0, n_max=10, max_restarts=0, inner_sweeps=2,
+                  track_factors=True),
+    "cardall": dict(seed=8, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, track_factors=True),
 }
 MESH2_CFG = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=20, max_restarts=0, track_factors=True,
                  inner_sweeps=2)

@@ -137,10 +137,54 @@ def c1_fixture():
     np.savez_compressed(os.path.join(HERE, "c1.npz"), **st)
 
 
+CONSTRAINT_CASES = [
+    # name, dims, rank, sigma2, data_seed, spec names, cfg kwargs
+    ("rowstoch", (10, 9, 8), 3, 1e-2, 51, ("row_stochastic", "nonneg", "nonneg"),
+     dict(seed=5, eps_abs=0.0, eps_rel=0.0, n_max=12, max_restarts=0, track_factors=True)),
+    ("card", (9, 10, 7), 3, 1e-2, 52, ("nonneg", "nonneg_card:12", "nonneg"),
+     dict(seed=6, eps_abs=0.0, eps_rel=0.0, n_max=12, max_restarts=0, track_factors=True)),
+    ("mixed", (12, 10, 8), 4, 1e-3, 53, ("row_stochastic", "nonneg_card:20", "nonneg_card:5"),
+     dict(seed=7, eps_abs=0.0, eps_rel=0.0, n_max=10, max_restarts=0, inner_sweeps=2,
+          track_factors=True)),
+    ("cardall", (6, 7, 5), 2, 1e-2, 54, ("nonneg_card:12", "nonneg_card:3", "row_stochastic"),
+     dict(seed=8, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, track_factors=True)),
+]
+
+
+def constraint_fits():
+    """Fits with the cardinality and row-stochastic constraints (reference
+    constraints.py:72-111, solver.py:182-193) and projection goldens."""
+    from cpadmm.constraints import ConstraintSpec, project
+
+    st = {}
+    for name, dims, rank, s2, dseed, specs, kw in CONSTRAINT_CASES:
+        t, _ = bench.generate(dims, rank, s2, seed=dseed)
+        cfg = solver.SolverConfig(**kw)
+        res = cpadmm.fit(t, rank, [ConstraintSpec.parse(sp) for sp in specs], cfg)
+        st[f"{name}_x"] = np.asarray(t.values)
+        st[f"{name}_rank"] = np.array(rank)
+        st[f"{name}_specs"] = np.array(specs)
+        pack_fit(name, res, cfg, st)
+    rng = np.random.default_rng(77)
+    for k in range(4):
+        m = rng.normal(size=(7, 5)) * (0.3 + k)
+        m[1] = np.array([0.1, 0.2, 0.3, 0.4, 0.0])       # already on the simplex
+        m[2, :3] = m[2, 3]                                # ties
+        st[f"proj{k}_m"] = m
+        st[f"proj{k}_simplex"] = project(m, ConstraintSpec.row_stochastic())
+        for c in (1, 4, 9, 40):
+            st[f"proj{k}_card{c}"] = project(m, ConstraintSpec.nonneg_card(c))
+    np.savez_compressed(os.path.join(HERE, "constraints.npz"), **st)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["constraints"]:
+        constraint_fits()
+        sys.exit(0)
     algebra()
     small_fits()
     c1_fixture()
+    constraint_fits()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

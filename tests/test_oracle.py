@@ -11,7 +11,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import MESH2_CFG, SMALL_CASES, rel
+from conftest import CONSTRAINT_CASES, MESH2_CFG, SMALL_CASES, rel
 from oracle import ntf_oracle as O
 
 
@@ -140,3 +140,31 @@ def test_c1_generator_and_trajectory(golden_c1):
         for m in range(3):
             assert np.array_equal(res.factor_history[it][m], g[f"rho1_hist{m}"][n])
     assert res.rfe == float(g["rho1_rfe"])
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_constraint_projections_match_reference(golden_constraints, k):
+    """constraints.py:72-111 goldens: simplex rows (an already-feasible row
+    unchanged, ties) and the global top-c cardinality keep (stable ties)."""
+    g = golden_constraints
+    m = g[f"proj{k}_m"]
+    assert np.array_equal(O.project(m, "row_stochastic"), g[f"proj{k}_simplex"])
+    for c in (1, 4, 9, 40):
+        assert np.array_equal(O.project(m, f"nonneg_card:{c}"), g[f"proj{k}_card{c}"])
+
+
+@pytest.mark.parametrize("name", sorted(CONSTRAINT_CASES))
+def test_constraint_fit_trajectories_match_reference(golden_constraints, name):
+    """Fits with row-stochastic / cardinality modes (solver.py:182-193 equality
+    constrained solve) reproduce the reference bit for bit."""
+    g = golden_constraints
+    specs = [str(s) for s in g[f"{name}_specs"]]
+    res = O.fit(g[f"{name}_x"], int(g[f"{name}_rank"]), O.Config(**CONSTRAINT_CASES[name]), specs)
+    assert np.array_equal(np.array([p for p, _ in res.residual_history]), g[f"{name}_primal"])
+    assert np.array_equal(np.array([d for _, d in res.residual_history]), g[f"{name}_dual"])
+    assert res.rfe == float(g[f"{name}_rfe"])
+    for m in range(3):
+        assert np.array_equal(res.factors[m], g[f"{name}_aux{m}"])
+    for n, it in enumerate(g[f"{name}_hist_idx"]):
+        for m in range(3):
+            assert np.array_equal(res.factor_history[it][m], g[f"{name}_hist{m}"][n])
