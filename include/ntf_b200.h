@@ -99,6 +99,12 @@ int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, co
  * ------------------------------------------------------------------------- */
 typedef struct ntf_plan ntf_plan;
 
+enum ntf_constraint {
+  NTF_CONSTRAINT_NONNEG = 0,
+  NTF_CONSTRAINT_CARD = 1,
+  NTF_CONSTRAINT_ROW_STOCHASTIC = 2
+};
+
 typedef struct ntf_plan_desc {
   /* problem: the tensor as seen by each mode's MTTKRP.  Single GPU: all
    * three entries are the whole tensor.  Sharded (P GPUs): entry
@@ -143,6 +149,13 @@ typedef struct ntf_plan_desc {
    * of this [cap][3] device array instead of applying adapt_penalties, so a
    * trajectory can be replayed under the reference's penalty sequence. */
   const double* rho_schedule;
+  /* Constraint of each mode (reference constraints.py, solver.py:182-193):
+   * NTF_CONSTRAINT_NONNEG (0, the default of a zero-initialised desc),
+   * NTF_CONSTRAINT_CARD with card[m] the global nonzero budget (single-GPU
+   * plans only), NTF_CONSTRAINT_ROW_STOCHASTIC (rows on the simplex, the
+   * equality-constrained row solve). */
+  int constraint[3];
+  int64_t card[3];
 } ntf_plan_desc;
 
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);

@@ -101,6 +101,8 @@ class PlanDesc(ctypes.Structure):
         ("rho_history", c_vp),
         ("counters", c_vp),
         ("rho_schedule", c_vp),
+        ("constraint", ctypes.c_int * 3),
+        ("card", c_i64 * 3),
     ]
 
 

@@ -1,9 +1,11 @@
 """Constraint specifications of the drop-in API (reference constraints.py:27-69).
 
 The B200 path implements the non-negative projection (constraints.py:105-111),
-fused into the per-mode update kernel.  The cardinality and row-stochastic
-kinds are accepted by ``ConstraintSpec`` for API compatibility but ``fit``
-raises NotImplementedError for them.
+fused into the per-mode update kernel; row-stochastic rows (equality-
+constrained solve + simplex projection) likewise; the global cardinality
+projection (constraints.py:95-102) runs as a select + apply kernel pair
+after the last-sweep update.  The cardinality constraint
+needs the whole factor on one GPU, so the sharded path rejects it.
 """
 
 from __future__ import annotations
@@ -54,8 +56,7 @@ class ConstraintSpec:
 
 
 def normalize_specs(specs, order: int) -> list[ConstraintSpec]:
-    """solver.normalize_specs (reference solver.py:154-164), plus the B200
-    envelope check (nonneg only)."""
+    """solver.normalize_specs (reference solver.py:154-164)."""
     if specs is None:
         specs = ConstraintSpec.nonneg()
     if isinstance(specs, ConstraintSpec):
@@ -65,7 +66,22 @@ def normalize_specs(specs, order: int) -> list[ConstraintSpec]:
         if len(specs) != order:
             raise ValueError(f"need one constraint per mode ({order}), got {len(specs)}")
     for s in specs:
-        if getattr(s, "kind", None) != "nonneg":
-            raise NotImplementedError(
-                f"constraint {getattr(s, 'kind', s)!r} is outside the B200 path (nonneg only)")
+        if getattr(s, "kind", None) not in _KINDS:
+            raise ValueError(f"unknown constraint {s!r}")
     return specs
+
+
+# plan codes (include/ntf_b200.h: ntf_constraint)
+_CODES = {"nonneg": 0, "nonneg_card": 1, "row_stochastic": 2}
+
+
+def plan_codes(specs, dims, rank: int) -> tuple[list[int], list[int]]:
+    """Per-mode (constraint code, cardinality budget) for the plan descriptor,
+    with the reference's budget check (solver.py:359-363)."""
+    codes, cards = [], []
+    for d, s in zip(dims, specs):
+        if s.kind == "nonneg_card" and s.card > d * rank:
+            raise ValueError(f"cardinality budget {s.card} exceeds factor size {d}x{rank}")
+        codes.append(_CODES[s.kind])
+        cards.append(int(s.card) if s.kind == "nonneg_card" else 0)
+    return codes, cards

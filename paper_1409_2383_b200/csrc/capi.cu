@@ -104,6 +104,8 @@ struct ntf_plan {
   double* mtt_ws = nullptr;
   double* norm_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][5][2] per mode
   double* gram_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][R][R] per mode
+  double* card_cand[3] = {nullptr, nullptr, nullptr};      // [rows][R] (cardinality modes)
+  unsigned long long* card_sel[3] = {nullptr, nullptr, nullptr};  // [2] threshold, index cut
   double* gram_ws = nullptr;
   bool any_tc = false;
   // all three MTTKRPs on the tensor cores: the ridge factorisation (and the
@@ -234,7 +236,14 @@ int enqueue_row_update(ntf_plan* pl, int mode, int last, cudaStream_t s, cudaEve
   fp.ridge_in_pred = pl->fused_ridge ? 1 : 0;
   fp.status = d.counters + 2;
   fp.stop_flag = d.counters + 1;
+  fp.kind = d.constraint[m];
+  fp.cand = pl->card_cand[m];
   NTF_CUDA_TRY(ntf::factor_update_launch(fp, s));
+  if (last && fp.kind == NTF_CONSTRAINT_CARD) {  // global top-c projection (constraints.py:95-102)
+    NTF_CUDA_TRY(ntf::card_select_launch(pl->card_cand[m], d.row_count[m] * R, d.card[m],
+                                         pl->card_sel[m], d.counters + 1, s));
+    NTF_CUDA_TRY(ntf::card_apply_launch(fp, pl->card_sel[m], s));
+  }
   if (ev) NTF_CUDA_TRY(record_event(ev[2], s));
   if (d.fuse_gram && !pl->fused_ridge) {  // G_m for the coming ridges, off the critical path
     NTF_CUDA_TRY(cudaEventRecord(pl->post_ev, s));
@@ -398,6 +407,16 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     for (int a = 0; a < 3; ++a)
       if (a != m && xd[a] != d.dims[a]) return fail(NTF_ERR_INVALID, "slab companion extent");
   }
+  for (int m = 0; m < 3; ++m) {
+    if (d.constraint[m] < NTF_CONSTRAINT_NONNEG || d.constraint[m] > NTF_CONSTRAINT_ROW_STOCHASTIC)
+      return fail(NTF_ERR_INVALID, "unknown constraint kind");
+    if (d.constraint[m] == NTF_CONSTRAINT_CARD) {
+      if (d.card[m] < 1 || d.card[m] > d.dims[m] * R)
+        return fail(NTF_ERR_INVALID, "cardinality budget out of range");
+      if (d.row_count[m] != d.dims[m])
+        return fail(NTF_ERR_UNSUPPORTED, "cardinality constraint needs the whole factor on one GPU");
+    }
+  }
   for (int m = 0; m < 3; ++m)
     if (d.engine == NTF_ENGINE_TCGEN05 &&
         !tc_ok(m + 1, d.x_dtype, d.x_dims[m][0], d.x_dims[m][1], d.x_dims[m][2], R))
@@ -429,6 +448,11 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
       return cleanup(cuda_fail(e, "cudaMalloc norm"));
     if ((e = ntf::dev_alloc(&pl->gram_partials[m], sizeof(double) * R * R * nb)) != cudaSuccess)
       return cleanup(cuda_fail(e, "cudaMalloc gram"));
+    if (d.constraint[m] == NTF_CONSTRAINT_CARD) {
+      if ((e = ntf::dev_alloc(&pl->card_cand[m], sizeof(double) * R * d.row_count[m])) != cudaSuccess ||
+          (e = ntf::dev_alloc(&pl->card_sel[m], 2 * sizeof(unsigned long long))) != cudaSuccess)
+        return cleanup(cuda_fail(e, "cudaMalloc card"));
+    }
   }
   if ((e = ntf::dev_alloc(&pl->gram_ws, ntf::gram_workspace_bytes(max_rows, R))) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc gram ws"));
@@ -614,6 +638,8 @@ void ntf_plan_destroy(ntf_plan* pl) {
   for (int m = 0; m < 3; ++m) {
     ntf::dev_free(pl->norm_partials[m]);
     ntf::dev_free(pl->gram_partials[m]);
+    ntf::dev_free(pl->card_cand[m]);
+    ntf::dev_free(pl->card_sel[m]);
   }
   ntf::dev_free(pl->gram_ws);
   ntf::dev_free(pl->gram_pending);

@@ -115,13 +115,10 @@ __device__ void split_sum(const FactorUpdateParams& p, int64_t base, int cnt, in
 
 // aux = project(F + Y/rho) (solver.py:311-314, constraints.py:105-111),
 // Y += rho (F - aux) (solver.py:315-317); residual terms into the scaled norms
-__device__ __forceinline__ void admm_step(const FactorUpdateParams& p, int64_t g, double x,
-                                          double rho, ScaledSq (&nrm)[5]) {
+__device__ __forceinline__ void admm_apply(const FactorUpdateParams& p, int64_t g, double x,
+                                           double a, double rho, ScaledSq (&nrm)[5]) {
   const double yd = p.dual[g];
   const double a_old = p.aux[g];
-  const double v = x + yd / rho;
-  if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
-  const double a = v > 0.0 ? v : 0.0;
   const double ynew = yd + rho * (x - a);
   p.aux[g] = a;
   p.dual[g] = ynew;
@@ -132,6 +129,69 @@ __device__ __forceinline__ void admm_step(const FactorUpdateParams& p, int64_t g
   nrm[4].add(ynew);
 }
 
+__device__ __forceinline__ void admm_step(const FactorUpdateParams& p, int64_t g, double x,
+                                          double rho, ScaledSq (&nrm)[5]) {
+  const double v = x + p.dual[g] / rho;
+  if (!isfinite(v)) raise_status(p.status, kDevNonFinite);
+  if (p.kind == kConstraintCard) {  // projection needs the whole matrix: card_apply
+    p.cand[g] = v;
+    return;
+  }
+  admm_apply(p, g, x, v > 0.0 ? v : 0.0, rho, nrm);
+}
+
+// Row-stochastic projection of one row (constraints.py:72-92) by one warp:
+// v[0..R) in shared memory (u: R doubles of scratch) -> a[c] for the lane's
+// columns c = lane + 32 t.  Sort-and-threshold: u = v sorted descending
+// (rank by value, ties by index), css = running sums (in order, as
+// np.cumsum), k = #{j: u_j (j+1) > css_j - 1}, theta = (css_{k-1} - 1)/k,
+// a = max(v - theta, 0); a row already on the simplex (min >= 0,
+// |sum - 1| <= 8 eps R) is returned unchanged.
+template <int RT>
+__device__ void simplex_row(const double* v, double* u, int R, int lane, double (&a)[RT]) {
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    const int c = lane + 32 * t;
+    if (c < R) {
+      const double vc = v[c];
+      int rank = 0;
+      for (int j = 0; j < R; ++j) {
+        const double vj = v[j];
+        rank += (vj > vc || (vj == vc && j < c)) ? 1 : 0;
+      }
+      u[rank] = vc;
+    }
+  }
+  __syncwarp();
+  double theta = 0.0;
+  int feasible = 0;
+  if (lane == 0) {
+    double css = 0.0, mn = v[0], sum = 0.0;
+    int k = 0;
+    for (int j = 0; j < R; ++j) {
+      css += u[j];
+      k += (u[j] * (j + 1) > css - 1.0) ? 1 : 0;  // count, as np.count_nonzero
+      u[j] = css;                                 // u now holds the running sums
+      mn = fmin(mn, v[j]);
+      sum += v[j];
+    }
+    theta = (u[k - 1] - 1.0) / k;
+    feasible = (mn >= 0.0 && fabs(sum - 1.0) <= 8.0 * 2.220446049250313e-16 * R) ? 1 : 0;
+  }
+  theta = __shfl_sync(0xffffffffu, theta, 0);
+  feasible = __shfl_sync(0xffffffffu, feasible, 0);
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    const int c = lane + 32 * t;
+    a[t] = 0.0;
+    if (c < R) {
+      const double d = v[c] - theta;
+      a[t] = feasible ? v[c] : (d > 0.0 ? d : 0.0);
+    }
+  }
+  __syncwarp();
+}
+
 // Block epilogue: scaled-norm partial (last sweep), Gram partial of the
 // block's new rows and the column maxima (fuse_gram).  xr: [rpb][R] new rows
 // (zero for rows past the end).  red: >= 80 doubles of scratch.
@@ -140,7 +200,7 @@ __device__ void block_partials(const FactorUpdateParams& p, ScaledSq (&nrm)[5], 
   const int R = p.R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int nwarps = kUpdThreads / 32;
-  if (p.last_sweep) {
+  if (p.last_sweep && p.kind != kConstraintCard) {
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
       ScaledSq v = nrm[c];
@@ -208,9 +268,11 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
   double* dl = ax + npm;                              // dual rows
   double* xr = dl + npm;                              // new rows
   double* scr = xr + npm;                             // [kUpdThreads] scratch
+  double* gs = scr + kUpdThreads;                     // [R + 8]: g1 = H^-1 1, sum(g1), lambdas
   const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
+  const bool rowstoch = p.kind == kConstraintRowStochastic;
   // loads that do not depend on the preceding kernel first
   for (int e = threadIdx.x; e < npm; e += blockDim.x) {
     ax[e] = e < cnt ? p.aux[base + e] : 0.0;
@@ -236,6 +298,34 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
     load_ridge();
   }
   split_sum(p, base, cnt, npm, ms, scr);
+  if (rowstoch) {  // g1 = (G + rho I)^-1 1 (solver.py:190), refined like the rows
+    for (int c = threadIdx.x; c < R; c += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < R; ++k) acc += Hi[k * R + c];
+      gs[c] = acc;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < R; c += blockDim.x) {
+      double acc = 1.0;
+      for (int k = 0; k < R; ++k) acc = fma(-gs[k], Hm[k * R + c], acc);
+      x1[c] = acc;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < R; c += blockDim.x) {
+      double acc = gs[c];
+      for (int k = 0; k < R; ++k) acc = fma(x1[k], Hi[k * R + c], acc);
+      scr[c] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sg = 0.0;
+      for (int c = 0; c < R; ++c) {
+        gs[c] = scr[c];
+        sg += scr[c];
+      }
+      gs[R] = sg;
+    }
+  }
   for (int e = threadIdx.x; e < npm; e += blockDim.x)
     yb[e] = e < cnt ? (ms[e] + rho * ax[e]) - dl[e] : 0.0;  // ridge_rhs (solver.py:178-179)
   __syncthreads();
@@ -270,12 +360,45 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
 #pragma unroll
   for (int u = 0; u < (64 * 2 + kUpdThreads - 1) / kUpdThreads; ++u) {
     const int e = threadIdx.x + u * kUpdThreads;
-    if (e < npm) {
-      xr[e] = xv[u];
-      if (e < cnt) {
-        const int64_t g = base + e;
-        p.F[p.row_offset * R + g] = xv[u];
-        if (p.last_sweep) admm_step(p, g, xv[u], rho, nrm);
+    if (e < npm) xr[e] = xv[u];
+  }
+  __syncthreads();
+  if (rowstoch) {
+    // rows summing to one (solver.py:189-193): x += lam g1, lam = (1 - x 1)/sum(g1)
+    if (threadIdx.x < rpb) {
+      double sx = 0.0;
+      for (int c = 0; c < R; ++c) sx += xr[threadIdx.x * R + c];
+      gs[R + 1 + threadIdx.x] = (1.0 - sx) / gs[R];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < npm; e += blockDim.x) {
+      const int lr = e / R, c = e - (e / R) * R;
+      if (e < cnt) xr[e] = fma(gs[R + 1 + lr], gs[c], xr[e]);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+    const int64_t g = base + e;
+    p.F[p.row_offset * R + g] = xr[e];
+    if (p.last_sweep && !rowstoch) admm_step(p, g, xr[e], rho, nrm);
+  }
+  if (p.last_sweep && rowstoch) {  // per-row simplex projection, one warp per row
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int lr = warp; lr < rpb && lr * R < cnt; lr += kUpdThreads / 32) {
+      double* v = x1 + lr * R;
+      double* u = yb + lr * R;
+      for (int c = lane; c < R; c += 32) {
+        const double vc = xr[lr * R + c] + dl[lr * R + c] / rho;
+        if (!isfinite(vc)) raise_status(p.status, kDevNonFinite);
+        v[c] = vc;
+      }
+      __syncwarp();
+      double a[2];
+      simplex_row<2>(v, u, R, lane, a);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int c = lane + 32 * t;
+        if (c < R) admm_apply(p, base + lr * R + c, xr[lr * R + c], a[t], rho, nrm);
       }
     }
   }
@@ -298,10 +421,14 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   double* ms = inv_diag + R;       // [npm] MTTKRP row sums
   double* xr = ms + npm;           // [npm] new rows
   double* scr = xr + npm;          // [kUpdThreads]
+  double* gs = scr + kUpdThreads;  // [R + 8] g1 = (G + rho I)^-1 1 and its sum
+  double* vb = gs + R + 8;         // [warps][R] projection input rows
+  double* ub = vb + (kUpdThreads / 32) * R;  // [warps][R] projection scratch
   const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
   const double rho = p.rho[p.mode - 1];
+  const bool rowstoch = p.kind == kConstraintRowStochastic;
   pdl_wait();  // MTTKRP partials and ridge factor
   if (*p.status == kDevNotPD) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -311,6 +438,24 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
   split_sum(p, base, cnt, npm, ms, scr);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (rowstoch) {  // g1 = cho_solve(ones) (solver.py:190) by warp 0
+    if (warp == 0) {
+      double y1[RT];
+#pragma unroll
+      for (int t = 0; t < RT; ++t) y1[t] = (lane + 32 * t) < R ? 1.0 : 0.0;
+      warp_chol_solve<RT>(y1, L, ldl, R, inv_diag, lane);
+#pragma unroll
+      for (int t = 0; t < RT; ++t)
+        if (lane + 32 * t < R) gs[lane + 32 * t] = y1[t];
+      __syncwarp();
+      if (lane == 0) {
+        double sg = 0.0;
+        for (int c = 0; c < R; ++c) sg += gs[c];
+        gs[R] = sg;
+      }
+    }
+    __syncthreads();
+  }
   ScaledSq nrm[5];
   for (int lr = warp; lr < rpb; lr += kUpdThreads / 32) {
     const bool valid = lr * R < cnt;
@@ -325,6 +470,17 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
       }
     }
     if (valid) warp_chol_solve<RT>(y, L, ldl, R, inv_diag, lane);
+    if (rowstoch && valid) {  // rows summing to one (solver.py:189-193)
+      double sx = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) sx += y[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      const double lam = (1.0 - sx) / gs[R];
+#pragma unroll
+      for (int t = 0; t < RT; ++t)
+        if (lane + 32 * t < R) y[t] = fma(lam, gs[lane + 32 * t], y[t]);
+    }
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
       const int r = lane + 32 * t;
@@ -333,8 +489,29 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
         if (valid) {
           const int64_t g = base + lr * R + r;
           p.F[p.row_offset * R + g] = y[t];
-          if (p.last_sweep) admm_step(p, g, y[t], rho, nrm);
+          if (p.last_sweep && !rowstoch) admm_step(p, g, y[t], rho, nrm);
         }
+      }
+    }
+    if (p.last_sweep && rowstoch && valid) {  // per-row simplex projection
+      double* v = vb + warp * R;
+      double* u = ub + warp * R;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int r = lane + 32 * t;
+        if (r < R) {
+          const double vc = y[t] + p.dual[base + lr * R + r] / rho;
+          if (!isfinite(vc)) raise_status(p.status, kDevNonFinite);
+          v[r] = vc;
+        }
+      }
+      __syncwarp();
+      double a[RT];
+      simplex_row<RT>(v, u, R, lane, a);
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int r = lane + 32 * t;
+        if (r < R) admm_apply(p, base + lr * R + r, y[t], a[t], rho, nrm);
       }
     }
   }
@@ -607,6 +784,124 @@ int sm_count() {
   return n;
 }
 
+
+// ---------------------------------------------------------------------------
+// Cardinality projection (constraints.py:95-102): keep the c largest clamped
+// entries of the mode's matrix, ties by smaller row-major index.  Clamped
+// values are non-negative, so their IEEE bits order like the values.
+// ---------------------------------------------------------------------------
+constexpr int kSelThreads = 1024;
+
+__device__ __forceinline__ unsigned long long card_key(double v) {
+  return v > 0.0 ? static_cast<unsigned long long>(__double_as_longlong(v)) : 0ull;
+}
+
+// One block: MSB-first radix select (8 passes of 8 bits, shared histograms)
+// of the c-th largest key T, then an ordered scan for the index cut among
+// the keys equal to T.  Integer counts only: deterministic.
+__global__ void __launch_bounds__(kSelThreads) card_select_kernel(const double* __restrict__ cand,
+                                                                  int64_t n, int64_t c,
+                                                                  unsigned long long* sel,
+                                                                  const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ long long s_remaining;
+  __shared__ long long scan[kSelThreads];
+  if (c >= n) {  // every clamped entry is kept
+    if (threadIdx.x == 0) {
+      sel[0] = 0ull;
+      sel[1] = static_cast<unsigned long long>(n);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    s_prefix = 0ull;
+    s_remaining = c;
+  }
+  unsigned long long mask = 0ull;
+  for (int pass = 7; pass >= 0; --pass) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    const int sh = pass * 8;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long k = card_key(cand[i]);
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh) & 255ull], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long rem = s_remaining;
+      int b = 255;
+      for (; b > 0; --b) {
+        if (static_cast<long long>(hist[b]) >= rem) break;
+        rem -= hist[b];
+      }
+      s_remaining = rem;
+      s_prefix = prefix | (static_cast<unsigned long long>(b) << sh);
+    }
+    mask |= 255ull << sh;
+    __syncthreads();
+  }
+  const unsigned long long T = s_prefix;
+  const long long want = s_remaining;  // ties with key T to keep, in index order
+  // ordered scan: thread t owns the contiguous index range [t*chunk, ...)
+  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t i0 = threadIdx.x * chunk, i1 = i0 + chunk < n ? i0 + chunk : n;
+  long long ties = 0;
+  for (int64_t i = i0; i < i1; ++i) ties += card_key(cand[i]) == T ? 1 : 0;
+  scan[threadIdx.x] = ties;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive prefix, in order
+    long long acc = 0;
+    for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {
+      const long long v = scan[t];
+      scan[t] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  const long long before = scan[threadIdx.x];
+  if (before < want && before + ties >= want) {
+    long long k = before;
+    for (int64_t i = i0; i < i1; ++i) {
+      if (card_key(cand[i]) == T && ++k == want) {
+        sel[0] = T;
+        sel[1] = static_cast<unsigned long long>(i + 1);
+        break;
+      }
+    }
+  }
+}
+
+// aux / dual / norms with the cardinality projection, same grid and element
+// ranges as the row update (its norm partials feed norm_reduce unchanged).
+__global__ void __launch_bounds__(kUpdThreads) card_apply_kernel(FactorUpdateParams p,
+                                                                 const unsigned long long* sel) {
+  if (p.stop_flag && *p.stop_flag) return;
+  __shared__ double red[kUpdThreads / 32 * 10];
+  const int R = p.R;
+  const int npm = rows_per_block(R) * R;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
+  const int64_t nM = p.rows * R;
+  const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
+  const double rho = p.rho[p.mode - 1];
+  const unsigned long long T = sel[0];
+  const int64_t cut = static_cast<int64_t>(sel[1]);
+  ScaledSq nrm[5];
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+    const int64_t g = base + e;
+    const double v = p.cand[g];
+    const unsigned long long k = card_key(v);
+    const bool keep = k > T || (k == T && p.row_offset * R + g < cut);
+    admm_apply(p, g, p.F[p.row_offset * R + g], keep ? (v > 0.0 ? v : 0.0) : 0.0, rho, nrm);
+  }
+  FactorUpdateParams q = p;
+  q.kind = kConstraintNonneg;  // write the norm partials
+  q.fuse_gram = 0;
+  q.last_sweep = 1;
+  block_partials(q, nrm, nullptr, 0, red);
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -621,9 +916,10 @@ size_t factor_update_smem(int R) {
   const size_t npm = static_cast<size_t>(rows_per_block(R)) * R;
   size_t n;
   if (R <= 64)
-    n = 2 * static_cast<size_t>(R) * R + 6 * npm + kUpdThreads;
+    n = 2 * static_cast<size_t>(R) * R + 6 * npm + kUpdThreads + R + 8;
   else
-    n = static_cast<size_t>(R) * (R + 1) + R + 2 * npm + kUpdThreads;
+    n = static_cast<size_t>(R) * (R + 1) + R + 2 * npm + kUpdThreads + R + 8 +
+        2 * (kUpdThreads / 32) * static_cast<size_t>(R);
   return n * sizeof(double);
 }
 
@@ -664,6 +960,18 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
   if (p.R <= 96)
     return launch_pdl(factor_update_warp_kernel<3>, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
   return launch_pdl(factor_update_warp_kernel<4>, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
+}
+
+cudaError_t card_select_launch(const double* cand, int64_t n, int64_t card, unsigned long long* sel,
+                               const int* stop_flag, cudaStream_t stream) {
+  card_select_kernel<<<1, kSelThreads, 0, stream>>>(cand, n, card, sel, stop_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t card_apply_launch(const FactorUpdateParams& p, const unsigned long long* sel,
+                              cudaStream_t stream) {
+  card_apply_kernel<<<factor_update_blocks(p.rows, p.R), kUpdThreads, 0, stream>>>(p, sel);
+  return cudaGetLastError();
 }
 
 cudaError_t gram_reduce_launch(const double* part, int nb, int R, double* G, const int* stop_flag,

@@ -31,7 +31,25 @@ struct FactorUpdateParams {
   int* status;
   const int* stop_flag;
   int debug;                // profiling only (NTF_UPD_DEBUG)
+  // constraint of this mode (reference constraints.py): 0 nonneg, 1 nonneg
+  // with a global cardinality budget (last sweep writes v = F + Y/rho to
+  // cand; card_select/card_apply finish the projection), 2 row-stochastic
+  // (equality-constrained row solve, per-row simplex projection)
+  int kind;
+  double* cand;             // [rows][R] (kind 1)
 };
+
+constexpr int kConstraintNonneg = 0, kConstraintCard = 1, kConstraintRowStochastic = 2;
+
+// Cardinality projection (constraints.py:95-102) of a mode's owned rows:
+// card_select finds the c-th largest clamped value T and the index cut among
+// its ties (stable, row-major order); card_apply then does the aux / dual
+// step (solver.py:311-317) with that projection and the norm partials.
+// sel: [2] uint64 {T bits, idx_cut}.
+cudaError_t card_select_launch(const double* cand, int64_t n, int64_t card, unsigned long long* sel,
+                               const int* stop_flag, cudaStream_t stream);
+cudaError_t card_apply_launch(const FactorUpdateParams& p, const unsigned long long* sel,
+                              cudaStream_t stream);
 
 struct FinalizeParams {
   const double* norm_acc;   // [parts][3][5][scale, ssq]

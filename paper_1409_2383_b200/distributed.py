@@ -132,7 +132,8 @@ def _sharded_problem_class():
     from .engine import DeviceProblem, Slabs, gram_device, mttkrp_device, sq_error  # noqa: F401
 
     class ShardedProblem(DeviceProblem):
-        def __init__(self, x_slabs, dims, rank, config, cap, engine, plan: PartitionPlan, comm: Comm):
+        def __init__(self, x_slabs, dims, rank, config, cap, engine, plan: PartitionPlan, comm: Comm,
+                     constraints=None):
             p = comm.rank
             self.comm = comm
             self.plan = plan
@@ -141,7 +142,8 @@ def _sharded_problem_class():
             own_off = tuple(self.offsets[m][p] for m in range(3))
             own_cnt = tuple(self.counts[m][p] for m in range(3))
             super().__init__(x_slabs[0], dims, rank, config, cap, engine,
-                             slabs=Slabs(list(x_slabs), own_off, own_cnt), norm_parts=comm.size)
+                             slabs=Slabs(list(x_slabs), own_off, own_cnt), norm_parts=comm.size,
+                             constraints=constraints)
             import os
 
             self._graph = None
@@ -264,12 +266,15 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
 
     config = config or SolverConfig()
     t = as_dense(t)
-    normalize_specs(specs, t.order)
+    specs = normalize_specs(specs, t.order)
     if rank < 1:
         raise ValueError("rank must be >= 1")
     if not (dist.is_available() and dist.is_initialized()) or (
             dist.get_world_size(group) == 1 and not sharded):
         return fit(t, rank, specs, config, engine=engine)
+    if any(s.kind == "nonneg_card" for s in specs):
+        raise NotImplementedError("the cardinality constraint needs the whole factor on one GPU "
+                                  "(a global top-c selection); use fit()")
     comm = Comm(group)
     if plan is None or isinstance(plan, int):
         plan = PartitionPlan.uniform(t.dims, comm.size)
@@ -287,7 +292,10 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     if x_norm == 0.0:
         raise ValueError("cannot factorize a zero tensor")
     cls = _sharded_problem_class()
-    prob = cls(slabs, t.dims, rank, config, config.n_max, _engine_code(engine), plan, comm)
+    from .constraints import plan_codes
+
+    prob = cls(slabs, t.dims, rank, config, config.n_max, _engine_code(engine), plan, comm,
+               constraints=plan_codes(specs, t.dims, rank))
     try:
         return _run_fit(prob, slabs[0], t.dims, rank, config, x_norm, gather=prob.gather_state)
     finally:

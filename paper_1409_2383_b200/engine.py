@@ -151,7 +151,7 @@ class DeviceProblem:
 
     def __init__(self, x, dims, rank: int, config, history_capacity: int, engine: int = N.ENGINE_AUTO,
                  slabs: Slabs | None = None, stream=None, rho_schedule=None,
-                 norm_parts: int = 1):
+                 norm_parts: int = 1, constraints=None):
         torch = _torch()
         self.torch = torch
         self.lib = N.load()
@@ -214,6 +214,10 @@ class DeviceProblem:
         if self.norm_all is not None:
             d.norm_all = _ptr(self.norm_all)
             d.norm_parts = int(norm_parts)
+        if constraints is not None:  # (codes, cards), constraints.plan_codes
+            for m in range(3):
+                d.constraint[m] = int(constraints[0][m])
+                d.card[m] = int(constraints[1][m])
         d.history_capacity = cap
         d.resid_history = _ptr(self.resid_hist)
         d.rho_history = _ptr(self.rho_hist)

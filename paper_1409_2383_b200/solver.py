@@ -18,7 +18,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _native as N
-from .constraints import ConstraintSpec, normalize_specs
+from .constraints import ConstraintSpec, normalize_specs, plan_codes
 from .tensors import DenseTensor, KruskalModel, as_dense
 
 
@@ -161,7 +161,8 @@ def mttkrp_factors(t, factors: Sequence[np.ndarray], mode: int, engine=None) -> 
 def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = None,
         config: SolverConfig | None = None, *, engine=None, device=None,
         rho_schedule=None) -> FitResult:
-    """Constrained (non-negative) CP fit with restarts (reference solver.py:340-403).
+    """Constrained CP fit with restarts (reference solver.py:340-403): nonneg,
+    nonneg_card:<c> or row_stochastic per mode.
 
     Same semantics as the reference: per outer iteration ``inner_sweeps``
     Gauss-Seidel sweeps of the ridge update over modes 1..3, then the aux
@@ -186,8 +187,9 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
     x_norm = math.sqrt(float(sq_error(x)[0].item()))
     if x_norm == 0.0:
         raise ValueError("cannot factorize a zero tensor")
+    codes = plan_codes(specs, t.dims, rank)
     prob = DeviceProblem(x, t.dims, rank, config, history_capacity=config.n_max,
-                         engine=_engine_code(engine), rho_schedule=rho_schedule)
+                         engine=_engine_code(engine), rho_schedule=rho_schedule, constraints=codes)
     try:
         return _run_fit(prob, x, t.dims, rank, config, x_norm)
     finally:
@@ -265,15 +267,18 @@ def iterate(state: SolverState, t, specs=None, config: SolverConfig | None = Non
 
     config = config or SolverConfig()
     t = as_dense(t)
-    normalize_specs(specs, t.order)
+    specs = normalize_specs(specs, t.order)
     rank = state.factors[0].shape[1]
+    codes = plan_codes(specs, t.dims, rank)
     x = device_tensor(t)
     key = (id(t), rank, config.inner_sweeps, config.adapt, config.mu, config.tau_incr,
-           config.tau_decr, config.eps_abs, config.eps_rel, _engine_code(engine))
+           config.tau_decr, config.eps_abs, config.eps_rel, _engine_code(engine),
+           tuple(codes[0]), tuple(codes[1]))
     prob = _ITER_CACHE.get(key)
     if prob is None or prob.x is not x:
         _ITER_CACHE.clear()
-        prob = DeviceProblem(x, t.dims, rank, config, history_capacity=1, engine=_engine_code(engine))
+        prob = DeviceProblem(x, t.dims, rank, config, history_capacity=1, engine=_engine_code(engine),
+                             constraints=codes)
         _ITER_CACHE[key] = prob
     prob.load_state(state.factors, state.aux, state.duals, state.rho)
     prob.run(1, use_graph=False)

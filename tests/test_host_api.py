@@ -24,10 +24,17 @@ def test_specs():
     assert [s.kind for s in normalize_specs(None, 3)] == ["nonneg"] * 3
     with pytest.raises(ValueError):
         normalize_specs([P.ConstraintSpec.nonneg()] * 2, 3)
-    with pytest.raises(NotImplementedError):
-        normalize_specs(P.ConstraintSpec.nonneg_card(3), 3)
+    assert [s.name() for s in normalize_specs(P.ConstraintSpec.nonneg_card(3), 3)] == \
+        ["nonneg_card:3"] * 3
     with pytest.raises(ValueError):
         P.ConstraintSpec("bogus")
+    from paper_1409_2383_b200.constraints import plan_codes
+
+    specs = [P.ConstraintSpec.row_stochastic(), P.ConstraintSpec.nonneg_card(7),
+             P.ConstraintSpec.nonneg()]
+    assert plan_codes(specs, (4, 5, 6), 2) == ([2, 1, 0], [0, 7, 0])
+    with pytest.raises(ValueError, match="exceeds factor size"):  # solver.py:359-363
+        plan_codes([P.ConstraintSpec.nonneg_card(11)] * 3, (5, 5, 5), 2)
 
 
 def test_seeds_and_init_state_match_oracle():
