@@ -120,16 +120,64 @@ class OracleTensor:
         return u
 
 
-def as_oracle_tensor(t) -> OracleTensor:
-    if isinstance(t, OracleTensor):
+class OracleSparse:
+    """Sparse COO tensor (tensors.py:84-132): entries sorted lexicographically,
+    indices int64 [nnz][order], values fp64; duplicates rejected."""
+
+    def __init__(self, dims, indices, vals):
+        self.dims = tuple(int(d) for d in dims)
+        idx = np.asarray(indices, dtype=np.int64).reshape(-1, len(self.dims))
+        v = np.asarray(vals, dtype=np.float64).reshape(-1)
+        if idx.shape[0] != v.shape[0]:
+            raise ValueError("index rows and value count differ")
+        if idx.size:
+            if idx.min() < 0 or np.any(idx >= np.array(self.dims)):
+                raise ValueError("entry index out of bounds")
+            order = np.lexsort(tuple(idx[:, m] for m in reversed(range(len(self.dims)))))
+            idx, v = idx[order], v[order]
+            if np.any(np.all(np.diff(idx, axis=0) == 0, axis=1)):
+                raise ValueError("duplicate entry indices")
+        self.indices, self.vals = idx, v
+
+    @property
+    def order(self) -> int:
+        return len(self.dims)
+
+    @property
+    def nnz(self) -> int:
+        return self.vals.shape[0]
+
+    def norm(self) -> float:
+        """tensors.py:114-115."""
+        return float(np.linalg.norm(self.vals))
+
+
+def as_oracle_tensor(t):
+    if isinstance(t, (OracleTensor, OracleSparse)):
         return t
+    if hasattr(t, "indices") and hasattr(t, "vals"):
+        return OracleSparse(t.dims, t.indices, t.vals)
     vals = getattr(t, "values", t)
     return OracleTensor(np.asarray(vals, dtype=np.float64))
 
 
-def mttkrp(t: OracleTensor, factors: Sequence[np.ndarray], mode: int) -> np.ndarray:
-    """tensors.py:254-262 (dense branch) — unfolding times materialised KR."""
-    kr = khatri_rao([factors[m - 1] for m in companion_modes(mode, t.order)])
+def mttkrp(t, factors: Sequence[np.ndarray], mode: int) -> np.ndarray:
+    """tensors.py:254-273 — dense: unfolding times materialised KR; sparse:
+    per-entry products (highest companion mode first, then the value),
+    accumulated with np.add.at in entry order."""
+    comp = companion_modes(mode, t.order)
+    if isinstance(t, OracleSparse):
+        rank = factors[0].shape[1]
+        out = np.zeros((t.dims[mode - 1], rank))
+        if t.nnz == 0:
+            return out
+        contrib = factors[comp[0] - 1][t.indices[:, comp[0] - 1], :].copy()
+        for m in comp[1:]:
+            contrib *= factors[m - 1][t.indices[:, m - 1], :]
+        contrib *= t.vals[:, None]
+        np.add.at(out, t.indices[:, mode - 1], contrib)
+        return out
+    kr = khatri_rao([factors[m - 1] for m in comp])
     return t.unfolding(mode) @ kr
 
 
@@ -140,8 +188,21 @@ def reconstruct(factors: Sequence[np.ndarray]) -> np.ndarray:
     return np.einsum("if,jf,kf,lf->ijkl", *factors, optimize=True)
 
 
-def rfe(t: OracleTensor, factors: Sequence[np.ndarray]) -> float:
-    """tensors.py:282-290 (dense) — explicit reconstruction."""
+def rfe(t, factors: Sequence[np.ndarray]) -> float:
+    """tensors.py:282-301 — dense: explicit reconstruction; sparse: the Gram
+    identity ||X||^2 - 2<X, W> + sum(Hadamard of the factor Grams)."""
+    if isinstance(t, OracleSparse):
+        tn = t.norm()
+        rows = factors[0][t.indices[:, 0], :].copy()
+        for m in range(1, t.order):
+            rows *= factors[m][t.indices[:, m], :]
+        cross = float(np.dot(t.vals, rows.sum(axis=1)))
+        gram = None
+        for f in factors:
+            g = f.T @ f
+            gram = g if gram is None else gram * g
+        sq = max(tn ** 2 - 2.0 * cross + float(gram.sum()), 0.0)
+        return math.sqrt(sq) / tn
     return float(np.linalg.norm(t.values - reconstruct(factors))) / t.norm()
 
 

@@ -62,6 +62,13 @@ CONSTRAINT_CASES = {
                   track_factors=True),
     "cardall": dict(seed=8, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, track_factors=True),
 }
+# cases of make_golden.sparse_fits (COO tensors)
+SPARSE_CASES = {
+    "sp1": dict(seed=1, eps_abs=0.0, eps_rel=0.0, n_max=10, max_restarts=0, track_factors=True),
+    "sp2": dict(seed=2, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, inner_sweeps=2,
+                track_factors=True, track_rfe=True),
+    "sp3": dict(seed=3),
+}
 MESH2_CFG = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=20, max_restarts=0, track_factors=True,
                  inner_sweeps=2)
 

@@ -177,14 +177,58 @@ def constraint_fits():
     np.savez_compressed(os.path.join(HERE, "constraints.npz"), **st)
 
 
+def sparse_fits():
+    """Sparse COO tensors (tensors.py:84-132, 263-273, 291-301): MTTKRP
+    goldens and fits (trajectories, sparse Gram-identity RFE)."""
+    from cpadmm.constraints import ConstraintSpec
+    from cpadmm.tensors import CooTensor, DenseTensor, mttkrp_factors
+
+    st = {}
+    rng = np.random.default_rng(91)
+    for k, (dims, density) in enumerate((((6, 7, 5), 0.3), ((9, 4, 8), 0.15), ((5, 5, 5), 1.0))):
+        vals = rng.normal(size=dims) * (rng.random(dims) < density)
+        t = CooTensor.from_dense(DenseTensor(vals))
+        fac = [rng.random((d, 3)) for d in dims]
+        st[f"m{k}_idx"] = np.asarray(t.indices)
+        st[f"m{k}_vals"] = np.asarray(t.vals)
+        st[f"m{k}_dims"] = np.array(dims)
+        for m in range(3):
+            st[f"m{k}_f{m}"] = fac[m]
+            st[f"m{k}_mttkrp{m + 1}"] = mttkrp_factors(t, fac, m + 1)
+    cases = [("sp1", (12, 10, 9), 3, 0.2, 61, None,
+              dict(seed=1, eps_abs=0.0, eps_rel=0.0, n_max=10, max_restarts=0, track_factors=True)),
+             ("sp2", (15, 8, 11), 4, 0.35, 62, ("nonneg", "row_stochastic", "nonneg_card:20"),
+              dict(seed=2, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, inner_sweeps=2,
+                   track_factors=True, track_rfe=True)),
+             ("sp3", (7, 6, 9), 2, 0.5, 63, None, dict(seed=3))]
+    for name, dims, rank, density, dseed, specs, kw in cases:
+        dense, _ = bench.generate(dims, rank, 1e-2, seed=dseed)
+        mask = np.random.default_rng(dseed + 1000).random(dims) < density
+        t = CooTensor.from_dense(DenseTensor(np.where(mask, dense.values, 0.0)))
+        cfg = solver.SolverConfig(**kw)
+        sp = None if specs is None else [ConstraintSpec.parse(s) for s in specs]
+        res = cpadmm.fit(t, rank, sp, cfg)
+        st[f"{name}_idx"] = np.asarray(t.indices)
+        st[f"{name}_vals"] = np.asarray(t.vals)
+        st[f"{name}_dims"] = np.array(dims)
+        st[f"{name}_rank"] = np.array(rank)
+        st[f"{name}_specs"] = np.array(specs if specs else ("nonneg",) * 3)
+        pack_fit(name, res, cfg, st)
+    np.savez_compressed(os.path.join(HERE, "sparse.npz"), **st)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["constraints"]:
         constraint_fits()
+        sys.exit(0)
+    if sys.argv[1:] == ["sparse"]:
+        sparse_fits()
         sys.exit(0)
     algebra()
     small_fits()
     c1_fixture()
     constraint_fits()
+    sparse_fits()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

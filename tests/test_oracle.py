@@ -11,7 +11,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import CONSTRAINT_CASES, MESH2_CFG, SMALL_CASES, rel
+from conftest import CONSTRAINT_CASES, MESH2_CFG, SMALL_CASES, SPARSE_CASES, rel
 from oracle import ntf_oracle as O
 
 
@@ -168,3 +168,25 @@ def test_constraint_fit_trajectories_match_reference(golden_constraints, name):
     for n, it in enumerate(g[f"{name}_hist_idx"]):
         for m in range(3):
             assert np.array_equal(res.factor_history[it][m], g[f"{name}_hist{m}"][n])
+
+
+def test_sparse_mttkrp_and_fits_match_reference():
+    """COO tensors (tensors.py:84-132, 263-273, 291-301): per-entry MTTKRP
+    accumulated in entry order, Gram-identity RFE, fits bit for bit."""
+    from conftest import load_golden
+
+    g = load_golden("sparse.npz")
+    for k in range(3):
+        t = O.OracleSparse(g[f"m{k}_dims"], g[f"m{k}_idx"], g[f"m{k}_vals"])
+        f = [g[f"m{k}_f{m}"] for m in range(3)]
+        for m in range(3):
+            assert np.array_equal(O.mttkrp(t, f, m + 1), g[f"m{k}_mttkrp{m + 1}"])
+    for name, kw in SPARSE_CASES.items():
+        t = O.OracleSparse(g[f"{name}_dims"], g[f"{name}_idx"], g[f"{name}_vals"])
+        specs = [str(s) for s in g[f"{name}_specs"]]
+        res = O.fit(t, int(g[f"{name}_rank"]), O.Config(**kw), specs)
+        assert res.iterations == int(g[f"{name}_iterations"])
+        assert res.rfe == float(g[f"{name}_rfe"])
+        assert np.array_equal(np.array([p for p, _ in res.residual_history]), g[f"{name}_primal"])
+        for m in range(3):
+            assert np.array_equal(res.factors[m], g[f"{name}_aux{m}"])
