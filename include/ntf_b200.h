@@ -87,9 +87,27 @@ int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, co
                  const double* B, const double* C, int R, double* out2, void* workspace,
                  size_t workspace_bytes, ntf_stream_t stream);
 
+/* Sparse COO MTTKRP, one mode: replaces tensors.mttkrp_factors' sparse branch
+ * (tensors.py:263-273).  Entries sorted lexicographically (idx [nnz][3]);
+ * perm: the entries ordered by index `mode` (stable; NULL for mode 1),
+ * rowptr: its row segments [dims[mode-1]+1].  Per (row, column) the
+ * products F_c0 * F_c1 * val are summed in entry order, as np.add.at:
+ * bitwise equal to the reference.  out: M x R fp64. */
+int ntf_mttkrp_coo(int mode, int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
+                   const double* vals, const int64_t* perm, const int64_t* rowptr, const double* A,
+                   const double* B, const double* C, int R, double* out, ntf_stream_t stream);
+
+/* COO sum of squares and model residual by the Gram identity
+ * (CooTensor.norm tensors.py:114-115, tensors.rfe sparse tensors.py:291-301):
+ * out2[0] = sum vals^2, out2[1] = ||X||^2 - 2<X, W> + sum((A'A)*(B'B)*(C'C)). */
+size_t ntf_sq_error_coo_workspace_bytes(int64_t nnz);
+int ntf_sq_error_coo(int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
+                     const double* vals, const double* A, const double* B, const double* C, int R,
+                     double* out2, void* workspace, size_t workspace_bytes, ntf_stream_t stream);
+
 /* ---------------------------------------------------------------------------
- * Solver plan: device-resident ADMoM outer iterations for one order-3 dense
- * tensor and nonneg constraints on every mode.  Replaces solver.iterate
+ * Solver plan: device-resident ADMoM outer iterations for one order-3 tensor
+ * (dense, or sparse COO on one GPU) and a constraint per mode.  Replaces solver.iterate
  * (solver.py:295-327) and the per-iteration part of solver.fit
  * (solver.py:375-387): Gauss-Seidel sweeps of _factor_update_core
  * (solver.py:207-219), aux/dual updates fused into each mode's last sweep
@@ -98,6 +116,8 @@ int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, co
  * penalties, histories and stop flag kept on the device.
  * ------------------------------------------------------------------------- */
 typedef struct ntf_plan ntf_plan;
+
+enum ntf_format { NTF_FORMAT_DENSE = 0, NTF_FORMAT_COO = 1 };
 
 enum ntf_constraint {
   NTF_CONSTRAINT_NONNEG = 0,
@@ -156,6 +176,19 @@ typedef struct ntf_plan_desc {
    * equality-constrained row solve). */
   int constraint[3];
   int64_t card[3];
+  /* Tensor format: NTF_FORMAT_DENSE (x_mode/x_dims as above), or
+   * NTF_FORMAT_COO (reference CooTensor, tensors.py:84-132; single GPU, fp64
+   * values, x_dtype = NTF_F64, x_mode[m] = coo_vals, x_dims[m] = dims):
+   * nnz entries sorted lexicographically, coo_idx [nnz][3] int64, and per
+   * mode m a stable order of the entries by index m (coo_perm[m], NULL for
+   * mode 1 = the entry order) with its row segments coo_rowptr[m]
+   * [dims[m]+1]. */
+  int x_format;
+  int64_t nnz;
+  const int64_t* coo_idx;
+  const double* coo_vals;
+  const int64_t* coo_perm[3];
+  const int64_t* coo_rowptr[3];
 } ntf_plan_desc;
 
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);

@@ -23,12 +23,13 @@ from .solver import (
     iterate,
     mttkrp_factors,
 )
-from .tensors import DenseTensor, KruskalModel
+from .tensors import CooTensor, DenseTensor, KruskalModel
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ConstraintSpec",
+    "CooTensor",
     "DenseTensor",
     "FitResult",
     "InvalidPenaltyError",

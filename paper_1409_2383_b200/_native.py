@@ -24,6 +24,9 @@ NTF_ERR_UNSUPPORTED = 5
 NTF_F32 = 0
 NTF_F64 = 1
 
+NTF_FORMAT_DENSE = 0
+NTF_FORMAT_COO = 1
+
 ENGINE_AUTO = 0
 ENGINE_CUDA_CORE = 1
 ENGINE_TCGEN05 = 2
@@ -38,6 +41,9 @@ EXPORTED = (
     "ntf_gram",
     "ntf_sq_error_workspace_bytes",
     "ntf_sq_error",
+    "ntf_mttkrp_coo",
+    "ntf_sq_error_coo_workspace_bytes",
+    "ntf_sq_error_coo",
     "ntf_plan_create",
     "ntf_colmax",
     "ntf_plan_sync_grams",
@@ -103,6 +109,12 @@ class PlanDesc(ctypes.Structure):
         ("rho_schedule", c_vp),
         ("constraint", ctypes.c_int * 3),
         ("card", c_i64 * 3),
+        ("x_format", ctypes.c_int),
+        ("nnz", c_i64),
+        ("coo_idx", c_vp),
+        ("coo_vals", c_vp),
+        ("coo_perm", c_vp * 3),
+        ("coo_rowptr", c_vp * 3),
     ]
 
 
@@ -127,6 +139,14 @@ def _declare(lib):
     lib.ntf_sq_error.restype = c_int
     lib.ntf_sq_error.argtypes = [c_int, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp,
                                  c_vp, ctypes.c_size_t, c_vp]
+    lib.ntf_mttkrp_coo.restype = c_int
+    lib.ntf_mttkrp_coo.argtypes = [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                   c_vp, c_vp, c_int, c_vp, c_vp]
+    lib.ntf_sq_error_coo_workspace_bytes.restype = ctypes.c_size_t
+    lib.ntf_sq_error_coo_workspace_bytes.argtypes = [c_i64]
+    lib.ntf_sq_error_coo.restype = c_int
+    lib.ntf_sq_error_coo.argtypes = [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
+                                     c_vp, c_vp, ctypes.c_size_t, c_vp]
     lib.ntf_plan_create.restype = c_int
     lib.ntf_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(c_vp)]
     lib.ntf_colmax.restype = c_int

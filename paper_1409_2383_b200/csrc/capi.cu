@@ -11,6 +11,7 @@
 #include <string>
 
 #include "mttkrp_cc.cuh"
+#include "mttkrp_coo.cuh"
 #include "mttkrp_tc.cuh"
 #include "solver_kernels.cuh"
 
@@ -57,16 +58,19 @@ bool use_tc(int engine, int mode, int x_dtype, int64_t I, int64_t J, int64_t K, 
 // One MTTKRP engine instance for one (mode, shape): geometry + launcher.
 struct MttkrpOp {
   bool tc = false;
+  bool coo = false;          // sparse COO tensor (mttkrp_coo.cu): one fp64 "split", the whole output
+  ntf::CooView cv{};
   ntf::MttkrpCCLaunch cc{};
   ntf::MttkrpTCLaunch tcl{};
   const ntf::TcTensor* tct = nullptr;  // fp16 split planes (tensor-core engine)
-  int splits() const { return tc ? tcl.splits : cc.groups; }
+  int splits() const { return coo ? 1 : (tc ? tcl.splits : cc.groups); }
   // rows from tail_row0() on have splits_tail() partials (ragged last tile)
   int64_t tail_row0() const {
-    return tc && tcl.splits_tail ? static_cast<int64_t>(tcl.n_full) * tcl.tm : INT64_MAX;
+    return !coo && tc && tcl.splits_tail ? static_cast<int64_t>(tcl.n_full) * tcl.tm : INT64_MAX;
   }
-  int splits_tail() const { return tc ? tcl.splits_tail : 0; }
+  int splits_tail() const { return !coo && tc ? tcl.splits_tail : 0; }
   size_t ws_bytes(int R) const {
+    if (coo) return 0;  // sized by the caller from the mode's row count
     return tc ? ntf::mttkrp_tc_workspace_bytes(tcl, R) : ntf::mttkrp_cc_workspace_bytes(cc, R);
   }
 };
@@ -85,12 +89,14 @@ cudaError_t run_op(MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
                    const int* stop, cudaStream_t s, const double* colmax3 = nullptr,
                    const ntf::TcRidge* ridge = nullptr) {
+  if (op.coo) return ntf::mttkrp_coo_launch(op.cv, mode, A, B, C, R, ws, stop, s);
   if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s, ridge);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
 }
 
 // Function attributes (dynamic smem opt-in) are set once, outside any capture.
 cudaError_t prepare_op(const MttkrpOp& op, int mode, int x_dtype) {
+  if (op.coo) return cudaSuccess;
   if (op.tc) return ntf::mttkrp_tc_prepare(op.tcl);
   return ntf::mttkrp_cc_prepare(mode, x_dtype, op.cc);
 }
@@ -385,6 +391,52 @@ int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, co
   return NTF_OK;
 }
 
+int ntf_mttkrp_coo(int mode, int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
+                   const double* vals, const int64_t* perm, const int64_t* rowptr, const double* A,
+                   const double* B, const double* C, int R, double* out, ntf_stream_t stream) {
+  if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
+  if (I < 1 || J < 1 || K < 1 || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
+  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
+  if (!out || !rowptr || (nnz > 0 && (!idx || !vals || (mode > 1 && !perm))))
+    return fail(NTF_ERR_INVALID, "null pointer");
+  if ((mode != 1 && !A) || (mode != 2 && !B) || (mode != 3 && !C))
+    return fail(NTF_ERR_INVALID, "missing companion factor");
+  ntf::CooView v{};
+  v.dims[0] = I;
+  v.dims[1] = J;
+  v.dims[2] = K;
+  v.nnz = nnz;
+  v.idx = idx;
+  v.vals = vals;
+  v.perm[mode - 1] = mode > 1 ? perm : nullptr;
+  v.rowptr[mode - 1] = rowptr;
+  NTF_CUDA_TRY(ntf::mttkrp_coo_launch(v, mode, A, B, C, R, out, nullptr,
+                                      static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
+size_t ntf_sq_error_coo_workspace_bytes(int64_t nnz) { return ntf::coo_sq_error_workspace_bytes(nnz, 0); }
+
+int ntf_sq_error_coo(int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
+                     const double* vals, const double* A, const double* B, const double* C, int R,
+                     double* out2, void* workspace, size_t workspace_bytes, ntf_stream_t stream) {
+  if (I < 1 || J < 1 || K < 1 || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
+  if (!out2 || !workspace || (nnz > 0 && (!idx || !vals))) return fail(NTF_ERR_INVALID, "null pointer");
+  if (A && (!B || !C || R < 1 || R > NTF_MAX_RANK)) return fail(NTF_ERR_INVALID, "bad model");
+  if (workspace_bytes < ntf::coo_sq_error_workspace_bytes(nnz, R))
+    return fail(NTF_ERR_INVALID, "workspace too small");
+  ntf::CooView v{};
+  v.dims[0] = I;
+  v.dims[1] = J;
+  v.dims[2] = K;
+  v.nnz = nnz;
+  v.idx = idx;
+  v.vals = vals;
+  NTF_CUDA_TRY(ntf::coo_sq_error_launch(v, A, B, C, A ? R : 0, out2, workspace,
+                                        static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if (!desc || !out) return fail(NTF_ERR_INVALID, "null pointer");
   *out = nullptr;
@@ -395,6 +447,19 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if (d.norm_all && d.norm_parts < 1) return fail(NTF_ERR_INVALID, "norm_parts must be >= 1");
   if (!d.rho || !d.norm_acc || !d.counters || !d.resid_history || !d.rho_history || !d.colmax)
     return fail(NTF_ERR_INVALID, "null plan buffer");
+  if (d.x_format != NTF_FORMAT_DENSE && d.x_format != NTF_FORMAT_COO)
+    return fail(NTF_ERR_INVALID, "unknown tensor format");
+  if (d.x_format == NTF_FORMAT_COO) {
+    if (d.x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "COO values are fp64");
+    if (d.nnz < 0 || (d.nnz > 0 && (!d.coo_idx || !d.coo_vals)))
+      return fail(NTF_ERR_INVALID, "null COO buffer");
+    for (int m = 0; m < 3; ++m) {
+      if (!d.coo_rowptr[m] || (m > 0 && d.nnz > 0 && !d.coo_perm[m]))
+        return fail(NTF_ERR_INVALID, "null COO mode order");
+      if (d.row_count[m] != d.dims[m] || d.row_offset[m] != 0)
+        return fail(NTF_ERR_UNSUPPORTED, "COO tensors are single-GPU");
+    }
+  }
   for (int m = 0; m < 3; ++m) {
     const int64_t* xd = d.x_dims[m];
     int rc = check_dims(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R);
@@ -428,9 +493,25 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   size_t ws = 0;
   int maxb = 1;
   int64_t max_rows = 1;
+  const bool coo = d.x_format == NTF_FORMAT_COO;
   for (int m = 0; m < 3; ++m) {
     const int64_t* xd = d.x_dims[m];
-    pl->op[m] = make_op(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R, d.engine);
+    if (coo) {
+      MttkrpOp op;
+      op.coo = true;
+      for (int a = 0; a < 3; ++a) op.cv.dims[a] = d.dims[a];
+      op.cv.nnz = d.nnz;
+      op.cv.idx = d.coo_idx;
+      op.cv.vals = d.coo_vals;
+      for (int a = 0; a < 3; ++a) {
+        op.cv.perm[a] = d.coo_perm[a];
+        op.cv.rowptr[a] = d.coo_rowptr[a];
+      }
+      pl->op[m] = op;
+      ws = std::max(ws, static_cast<size_t>(d.dims[m]) * R * sizeof(double));
+    } else {
+      pl->op[m] = make_op(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R, d.engine);
+    }
     ws = std::max(ws, pl->op[m].ws_bytes(R));
     pl->blocks[m] = ntf::factor_update_blocks(d.row_count[m], R);
     maxb = std::max(maxb, pl->blocks[m]);

@@ -265,6 +265,12 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     from .solver import fit
 
     config = config or SolverConfig()
+    from .tensors import is_sparse
+
+    if is_sparse(t):  # COO tensors run on one GPU
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            raise NotImplementedError("sparse COO tensors are single-GPU (no sharded COO engine)")
+        return fit(t, rank, specs, config, engine=engine)
     t = as_dense(t)
     specs = normalize_specs(specs, t.order)
     if rank < 1:

@@ -100,6 +100,97 @@ def sq_error(x, factors=None, stream=None):
     return out
 
 
+class DeviceCoo:
+    """HBM copy of a CooTensor for the COO engine (include/ntf_b200.h
+    NTF_FORMAT_COO): lexicographic entries, and per mode a stable order of
+    the entries by that mode's index with its row segments (built on the
+    host once per tensor, then uploaded)."""
+
+    def __init__(self, t, device=None):
+        torch = _torch()
+        dev = torch.device(device or "cuda")
+        self.dims = tuple(int(d) for d in t.dims)
+        self.shape = self.dims
+        self.nnz = int(t.vals.shape[0])
+        self.device = dev
+        self.dtype = torch.float64
+        idx = np.ascontiguousarray(t.indices, dtype=np.int64).reshape(-1, 3)
+        self.idx = torch.from_numpy(idx.copy()).to(dev)
+        self.vals = torch.from_numpy(np.ascontiguousarray(t.vals, dtype=np.float64).copy()).to(dev)
+        self.perm, self.rowptr = [], []
+        for m in range(3):
+            key = idx[:, m]
+            if m == 0:  # lexicographic order is already sorted by the first index
+                self.perm.append(None)
+                sk = key
+            else:
+                order = np.argsort(key, kind="stable")
+                self.perm.append(torch.from_numpy(order.astype(np.int64)).to(dev))
+                sk = key[order]
+            rp = np.searchsorted(sk, np.arange(self.dims[m] + 1), side="left").astype(np.int64)
+            self.rowptr.append(torch.from_numpy(rp).to(dev))
+
+    def data_ptr(self) -> int:
+        return self.vals.data_ptr() if self.nnz else self.rowptr[0].data_ptr()
+
+    def ptr_idx(self):
+        return self.idx.data_ptr() if self.nnz else None
+
+    def ptr_perm(self, m):
+        p = self.perm[m]
+        return p.data_ptr() if (p is not None and self.nnz) else None
+
+
+def device_coo(t, device=None) -> DeviceCoo:
+    """The DeviceCoo of CooTensor ``t`` (built once and cached on it)."""
+    torch = _torch()
+    dev = torch.device(device or "cuda")
+    cache = getattr(t, "_device_cache", None)
+    if isinstance(cache, DeviceCoo) and cache.device == dev:
+        return cache
+    d = DeviceCoo(t, dev)
+    try:
+        t._device_cache = d
+    except AttributeError:
+        pass
+    return d
+
+
+def mttkrp_coo_device(x: DeviceCoo, factors, mode: int, stream=None):
+    torch = _torch()
+    lib = N.load()
+    R = int(factors[0].shape[1])
+    out = torch.empty((x.dims[mode - 1], R), dtype=torch.float64, device=x.device)
+    s = stream or torch.cuda.current_stream(x.device)
+    a, b, c = (_ptr(f) for f in factors)
+    N.check(lib.ntf_mttkrp_coo(mode, x.dims[0], x.dims[1], x.dims[2], x.nnz, x.ptr_idx(),
+                               x.vals.data_ptr() if x.nnz else None, x.ptr_perm(mode - 1),
+                               _ptr(x.rowptr[mode - 1]), a, b, c, R, _ptr(out), _stream_handle(s)))
+    return out
+
+
+def coo_sq_error(x: DeviceCoo, factors=None, stream=None):
+    """(sum x^2, ||X - [[A,B,C]]||^2 by the Gram identity) on the device."""
+    torch = _torch()
+    lib = N.load()
+    wsb = lib.ntf_sq_error_coo_workspace_bytes(x.nnz)
+    ws = torch.empty(max(1, wsb // 8 + 1), dtype=torch.float64, device=x.device)
+    out = torch.zeros(2, dtype=torch.float64, device=x.device)
+    s = stream or torch.cuda.current_stream(x.device)
+    if factors is None:
+        a = b = c = None
+        R = 0
+    else:
+        f = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).to(x.device)
+             if isinstance(v, np.ndarray) else v.contiguous() for v in factors]
+        a, b, c = (_ptr(v) for v in f)
+        R = int(f[0].shape[1])
+    N.check(lib.ntf_sq_error_coo(x.dims[0], x.dims[1], x.dims[2], x.nnz, x.ptr_idx(),
+                                 x.vals.data_ptr() if x.nnz else None, a, b, c, R, _ptr(out),
+                                 _ptr(ws), ws.numel() * 8, _stream_handle(s)))
+    return out
+
+
 def tensor_norm(t) -> float:
     x = device_tensor(t)
     return float(np.sqrt(sq_error(x)[0].item()))
@@ -214,6 +305,14 @@ class DeviceProblem:
         if self.norm_all is not None:
             d.norm_all = _ptr(self.norm_all)
             d.norm_parts = int(norm_parts)
+        if isinstance(x, DeviceCoo):
+            d.x_format = N.NTF_FORMAT_COO
+            d.nnz = x.nnz
+            d.coo_idx = x.ptr_idx()
+            d.coo_vals = x.vals.data_ptr() if x.nnz else None
+            for m in range(3):
+                d.coo_perm[m] = x.ptr_perm(m)
+                d.coo_rowptr[m] = _ptr(x.rowptr[m])
         if constraints is not None:  # (codes, cards), constraints.plan_codes
             for m in range(3):
                 d.constraint[m] = int(constraints[0][m])
@@ -275,9 +374,13 @@ class DeviceProblem:
         self.run(1)
 
     def final_sq_error(self, aux):
-        """(sum x^2, sum (x - [[aux]])^2) over the whole tensor, on the device."""
+        """(sum x^2, sum (x - [[aux]])^2) over the whole tensor, on the device
+        (sparse: the Gram identity of tensors.py:291-301)."""
         with self.torch.cuda.stream(self.stream):
-            out = sq_error(self.x, aux, stream=self.stream)
+            if isinstance(self.x, DeviceCoo):
+                out = coo_sq_error(self.x, aux, stream=self.stream)
+            else:
+                out = sq_error(self.x, aux, stream=self.stream)
             return float(out[0].item()), float(out[1].item())
 
     def aux_model_rfe(self, x_norm: float) -> float:
@@ -286,7 +389,10 @@ class DeviceProblem:
         torch = self.torch
         with torch.cuda.stream(self.stream):
             aux = self.aux
-            m = mttkrp_device(self.x, aux, 1, self._desc.engine, stream=self.stream)
+            if isinstance(self.x, DeviceCoo):
+                m = mttkrp_coo_device(self.x, aux, 1, stream=self.stream)
+            else:
+                m = mttkrp_device(self.x, aux, 1, self._desc.engine, stream=self.stream)
             g = gram_device(aux[2], stream=self.stream) * gram_device(aux[1], stream=self.stream)
             ga = gram_device(aux[0], stream=self.stream)
             cross = float(torch.sum(aux[0] * m).item())

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _native as N
 from .constraints import ConstraintSpec, normalize_specs, plan_codes
-from .tensors import DenseTensor, KruskalModel, as_dense
+from .tensors import CooTensor, DenseTensor, KruskalModel, as_coo, as_dense, is_sparse  # noqa: F401
 
 
 class InvalidPenaltyError(RuntimeError):
@@ -141,13 +141,24 @@ def _engine_code(engine) -> int:
 
 
 def mttkrp_factors(t, factors: Sequence[np.ndarray], mode: int, engine=None) -> np.ndarray:
-    """Device MTTKRP (replaces tensors.mttkrp_factors, tensors.py:254-262)."""
-    from .engine import _torch, device_tensor, mttkrp_device
+    """Device MTTKRP (replaces tensors.mttkrp_factors, tensors.py:254-273):
+    dense (tensor-core / CUDA-core engines) or sparse COO."""
+    from .engine import _torch, device_coo, device_tensor, mttkrp_coo_device, mttkrp_device
 
     torch = _torch()
-    t = as_dense(t)
     if not 1 <= mode <= 3:
         raise ValueError(f"mode must be in 1..3, got {mode}")
+    if is_sparse(t):
+        t = as_coo(t)
+        x = device_coo(t)
+        f = [torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(x.device) for v in factors]
+        for m, v in enumerate(f):
+            if v.shape[0] != t.dims[m]:
+                raise ValueError("factor dims do not match tensor dims")
+        out = mttkrp_coo_device(x, f, mode)
+        torch.cuda.current_stream(x.device).synchronize()
+        return out.cpu().numpy()
+    t = as_dense(t)
     x = device_tensor(t)
     f = [torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(x.device) for v in factors]
     for m, v in enumerate(f):
@@ -176,17 +187,27 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
     even where the adaptation rule's branch is decided by rounding noise
     (``p > 0`` at p ~ 1e-17, solver.py:286-291).
     """
-    from .engine import DeviceProblem, device_tensor, sq_error
+    from .engine import DeviceProblem, device_coo, device_tensor, sq_error
 
     config = config or SolverConfig()
-    t = as_dense(t)
-    specs = normalize_specs(specs, t.order)
-    if rank < 1:
-        raise ValueError("rank must be >= 1")
-    x = device_tensor(t, device)
-    x_norm = math.sqrt(float(sq_error(x)[0].item()))
-    if x_norm == 0.0:
-        raise ValueError("cannot factorize a zero tensor")
+    if is_sparse(t):
+        t = as_coo(t)
+        specs = normalize_specs(specs, t.order)
+        if rank < 1:
+            raise ValueError("rank must be >= 1")
+        x_norm = t.norm()  # tensors.py:114-115
+        if x_norm == 0.0:
+            raise ValueError("cannot factorize a zero tensor")
+        x = device_coo(t, device)
+    else:
+        t = as_dense(t)
+        specs = normalize_specs(specs, t.order)
+        if rank < 1:
+            raise ValueError("rank must be >= 1")
+        x = device_tensor(t, device)
+        x_norm = math.sqrt(float(sq_error(x)[0].item()))
+        if x_norm == 0.0:
+            raise ValueError("cannot factorize a zero tensor")
     codes = plan_codes(specs, t.dims, rank)
     prob = DeviceProblem(x, t.dims, rank, config, history_capacity=config.n_max,
                          engine=_engine_code(engine), rho_schedule=rho_schedule, constraints=codes)
@@ -263,14 +284,18 @@ _ITER_CACHE: dict = {}
 def iterate(state: SolverState, t, specs=None, config: SolverConfig | None = None,
             *, engine=None) -> tuple[SolverState, Residuals]:
     """One outer iteration from ``state`` (reference solver.py:295-327)."""
-    from .engine import DeviceProblem, device_tensor
+    from .engine import DeviceProblem, device_coo, device_tensor
 
     config = config or SolverConfig()
-    t = as_dense(t)
+    if is_sparse(t):
+        t = as_coo(t)
+        x = device_coo(t)
+    else:
+        t = as_dense(t)
+        x = device_tensor(t)
     specs = normalize_specs(specs, t.order)
     rank = state.factors[0].shape[1]
     codes = plan_codes(specs, t.dims, rank)
-    x = device_tensor(t)
     key = (id(t), rank, config.inner_sweeps, config.adapt, config.mu, config.tau_incr,
            config.tau_decr, config.eps_abs, config.eps_rel, _engine_code(engine),
            tuple(codes[0]), tuple(codes[1]))

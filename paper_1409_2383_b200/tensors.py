@@ -4,8 +4,10 @@
 only) and additionally keeps fp32 storage when given fp32 values — the B200
 path streams fp32 tensors for BASELINE configs 2-5.  Values may
 also be a ``torch.Tensor`` (host or device), so a tensor generated on the GPU
-is never copied to the host.  Order-4 and sparse (``CooTensor``) inputs are
-outside the B200 path and are rejected by ``fit``.
+is never copied to the host.  ``CooTensor`` mirrors the reference's sparse
+container (tensors.py:84-132; order 3, fp64); ``fit`` runs it with the COO
+MTTKRP engine on one GPU.  Order-4 inputs are outside the B200 path (SURVEY
+8(f) #4) and are rejected by ``fit``.
 """
 
 from __future__ import annotations
@@ -120,13 +122,82 @@ class KruskalModel:
         return f"KruskalModel(dims={self.dims}, rank={self.rank})"
 
 
+class CooTensor:
+    """Sparse order-3 tensor in coordinate form, entries sorted
+    lexicographically, duplicates rejected (reference tensors.py:84-132)."""
+
+    __slots__ = ("dims", "indices", "vals", "_device_cache", "__weakref__")
+
+    def __init__(self, dims: Sequence[int], indices, vals):
+        self.dims = tuple(int(d) for d in dims)
+        if len(self.dims) != 3:
+            raise ValueError(f"tensor order must be 3, got {len(self.dims)}")
+        if any(d < 1 for d in self.dims):
+            raise ValueError(f"all extents must be >= 1, got {self.dims}")
+        idx = np.asarray(indices, dtype=np.int64).reshape(-1, 3)
+        v = np.asarray(vals, dtype=np.float64).reshape(-1)
+        if idx.shape[0] != v.shape[0]:
+            raise ValueError("index rows and value count differ")
+        if idx.size:
+            if idx.min() < 0 or np.any(idx >= np.array(self.dims)):
+                raise ValueError("entry index out of bounds")
+            order = np.lexsort((idx[:, 2], idx[:, 1], idx[:, 0]))
+            idx, v = idx[order], v[order]
+            if np.any(np.all(np.diff(idx, axis=0) == 0, axis=1)):
+                raise ValueError("duplicate entry indices")
+        idx.flags.writeable = False
+        v.flags.writeable = False
+        self.indices = idx
+        self.vals = v
+        self._device_cache = None
+
+    @property
+    def order(self) -> int:
+        return 3
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals.shape[0])
+
+    def norm(self) -> float:
+        """tensors.py:114-115 (host numpy over the stored values, as the reference)."""
+        return float(np.linalg.norm(self.vals))
+
+    def to_dense(self) -> DenseTensor:
+        out = np.zeros(self.dims)
+        out[tuple(self.indices[:, m] for m in range(3))] = self.vals
+        return DenseTensor(out)
+
+    @classmethod
+    def from_dense(cls, t, tol: float = 0.0) -> "CooTensor":
+        vals = np.asarray(getattr(t, "values", t), dtype=np.float64)
+        mask = np.abs(vals) > tol
+        return cls(vals.shape, np.argwhere(mask), vals[mask])
+
+    def __repr__(self) -> str:
+        return f"CooTensor(dims={self.dims}, nnz={self.nnz})"
+
+
+def is_sparse(t) -> bool:
+    return isinstance(t, CooTensor) or (hasattr(t, "indices") and hasattr(t, "vals"))
+
+
+def as_coo(t) -> CooTensor:
+    """Our CooTensor, or the reference's (duck-typed on dims/indices/vals)."""
+    if isinstance(t, CooTensor):
+        return t
+    if len(t.dims) != 3:
+        raise NotImplementedError("order-4 tensors are outside the B200 path (SURVEY 8(f) #4)")
+    return CooTensor(t.dims, t.indices, t.vals)
+
+
 def as_dense(t) -> DenseTensor:
     """Accept our DenseTensor, the reference's DenseTensor (duck-typed on
     ``.values``/``.dims``), a numpy array or a torch tensor."""
     if isinstance(t, DenseTensor):
         return t
-    if hasattr(t, "indices") and hasattr(t, "vals"):
-        raise NotImplementedError("sparse COO tensors are outside the B200 path (SURVEY 8(f) #4)")
+    if is_sparse(t):
+        raise TypeError("a sparse COO tensor is not dense (use as_coo)")
     vals = getattr(t, "values", t)
     if _is_torch(vals) or isinstance(vals, np.ndarray):
         if getattr(vals, "ndim", 3) == 4:
