@@ -252,6 +252,7 @@ __device__ void block_partials(const FactorUpdateParams& p, ScaledSq (&nrm)[5], 
 // Every (row, column) pair is independent: no sequential substitution chain
 // on the critical path.  Agreement with cho_solve (solver.py:188) is at the
 // backward-error level.
+template <int KIND>
 __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorUpdateParams p) {
   pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
   const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
-  const bool rowstoch = p.kind == kConstraintRowStochastic;
+  constexpr bool rowstoch = KIND == kConstraintRowStochastic;
   // loads that do not depend on the preceding kernel first
   for (int e = threadIdx.x; e < npm; e += blockDim.x) {
     ax[e] = e < cnt ? p.aux[base + e] : 0.0;
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
 }
 
 // R > 64: one row per warp, forward/backward substitution against L.
-template <int RT>
+template <int RT, int KIND>
 __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorUpdateParams p) {
   pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
   const double rho = p.rho[p.mode - 1];
-  const bool rowstoch = p.kind == kConstraintRowStochastic;
+  constexpr bool rowstoch = KIND == kConstraintRowStochastic;
   pdl_wait();  // MTTKRP partials and ridge factor
   if (*p.status == kDevNotPD) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -938,12 +939,18 @@ cudaError_t factor_update_prepare(int R) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(ridge_factor_smem(R)));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(factor_update_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(factor_update_warp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(factor_update_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem);
+  const void* kerns[] = {
+      reinterpret_cast<const void*>(factor_update_gemv_kernel<kConstraintNonneg>),
+      reinterpret_cast<const void*>(factor_update_gemv_kernel<kConstraintRowStochastic>),
+      reinterpret_cast<const void*>(factor_update_warp_kernel<3, kConstraintNonneg>),
+      reinterpret_cast<const void*>(factor_update_warp_kernel<3, kConstraintRowStochastic>),
+      reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintNonneg>),
+      reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintRowStochastic>)};
+  for (const void* k : kerns) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t stream) {
@@ -956,10 +963,18 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
   p.debug = dbg;
   const int blocks = factor_update_blocks(p.rows, p.R);
   const size_t smem = factor_update_smem(p.R);
-  if (p.R <= 64) return launch_pdl(factor_update_gemv_kernel, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
+  // the constraint kind is a template parameter: the nonneg kernels carry
+  // no row-stochastic code
+  auto launch = [&](auto kern) { return launch_pdl(kern, dim3(blocks), dim3(kUpdThreads), smem, stream, p); };
+  const bool rs = p.kind == kConstraintRowStochastic;
+  if (p.R <= 64)
+    return rs ? launch(factor_update_gemv_kernel<kConstraintRowStochastic>)
+              : launch(factor_update_gemv_kernel<kConstraintNonneg>);
   if (p.R <= 96)
-    return launch_pdl(factor_update_warp_kernel<3>, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
-  return launch_pdl(factor_update_warp_kernel<4>, dim3(blocks), dim3(kUpdThreads), smem, stream, p);
+    return rs ? launch(factor_update_warp_kernel<3, kConstraintRowStochastic>)
+              : launch(factor_update_warp_kernel<3, kConstraintNonneg>);
+  return rs ? launch(factor_update_warp_kernel<4, kConstraintRowStochastic>)
+            : launch(factor_update_warp_kernel<4, kConstraintNonneg>);
 }
 
 cudaError_t card_select_launch(const double* cand, int64_t n, int64_t card, unsigned long long* sel,
