@@ -229,10 +229,21 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 bits, 4 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 template <int W>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[W]) {
   if constexpr (W == 16) tmem_ld16(taddr, v);
-  else tmem_ld8(taddr, v);
+  else if constexpr (W == 8) tmem_ld8(taddr, v);
+  else tmem_ld4(taddr, v);
 }
 
 __device__ __forceinline__ void tmem_wait_ld() {
@@ -366,7 +377,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   constexpr int kEpi = epi_warps(NT);
   constexpr int NC = N * 4 / kEpi;         // columns per epilogue thread
   // TMEM load width: 16 columns where it divides NC and registers allow
-  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : 8;
+  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : (NC > 48 ? 4 : 8);
   static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kIssuers = mma_issuers(N);
@@ -690,17 +701,14 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
           tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*T0 (+ ACC2 when merged)
           if constexpr (!merged_acc(N)) tmem_ld<LW>(taddr + 2 * N + j * LW, a2);  // ACC2: S0*T2 + S1*T1
           tmem_wait_ld();
-          if constexpr (merged_acc(N)) {
-#pragma unroll
-            for (int v = 0; v < LW; ++v) a2[v] = 0.f;
-          }
 #pragma unroll
           for (int v = 0; v < LW; ++v) {
             const float2 h = hs[j * LW + v];
             const float a = a0[v];
             const float pr = a * h.x;
             const float er = fmaf(a, h.x, -pr);    // a*h.x = pr + er exactly
-            const float cr = fmaf(a1[v] + a2[v], h.x, fmaf(a, h.y, er));
+            const float a12 = merged_acc(N) ? a1[v] : a1[v] + a2[v];
+            const float cr = fmaf(a12, h.x, fmaf(a, h.y, er));
             two_sum(hi[j * LW + v], lo[j * LW + v], pr);
             lo[j * LW + v] += cr;
           }
