@@ -35,7 +35,8 @@
 extern "C" {
 #endif
 
-#define NTF_ABI_VERSION 1
+#define NTF_ABI_VERSION 2
+#define NTF_MAX_ORDER 4
 #define NTF_MAX_RANK 128
 
 typedef void* ntf_stream_t;
@@ -105,9 +106,16 @@ int ntf_sq_error_coo(int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t
                      const double* vals, const double* A, const double* B, const double* C, int R,
                      double* out2, void* workspace, size_t workspace_bytes, ntf_stream_t stream);
 
+/* Khatri-Rao pair out[a*nb + b][r] = Fa[a][r] * Fb[b][r] (tensors.khatri_rao,
+ * tensors.py:203-220, for two factors): the merged factor of an order-4
+ * tensor's reshaped views (e.g. the model [A, B, C o D] of X as I x J x KL). */
+int ntf_khatri_rao_pair(const double* Fa, int64_t na, const double* Fb, int64_t nb, int R, double* out,
+                        ntf_stream_t stream);
+
 /* ---------------------------------------------------------------------------
- * Solver plan: device-resident ADMoM outer iterations for one order-3 tensor
- * (dense, or sparse COO on one GPU) and a constraint per mode.  Replaces solver.iterate
+ * Solver plan: device-resident ADMoM outer iterations for one order-3 or
+ * order-4 tensor (order 3: dense or sparse COO, sharded or not; order 4:
+ * dense on one GPU) and a constraint per mode.  Replaces solver.iterate
  * (solver.py:295-327) and the per-iteration part of solver.fit
  * (solver.py:375-387): Gauss-Seidel sweeps of _factor_update_core
  * (solver.py:207-219), aux/dual updates fused into each mode's last sweep
@@ -126,17 +134,23 @@ enum ntf_constraint {
 };
 
 typedef struct ntf_plan_desc {
+  /* tensor order: 3, or 4 (dense, single GPU: each order-4 MTTKRP runs as an
+   * order-3 one on a reshaped view, I x J x (K L) for modes 1-2 and
+   * (I J) x K x L for modes 3-4, with the Khatri-Rao pair of the merged
+   * modes formed on the device); 0 means 3.  Arrays below hold `order`
+   * entries. */
+  int order;
   /* problem: the tensor as seen by each mode's MTTKRP.  Single GPU: all
-   * three entries are the whole tensor.  Sharded (P GPUs): entry
-   * m is this rank's mode-m slab (X[I_p,:,:], X[:,J_p,:], X[:,:,K_p]) and
-   * x_dims[m] its extents; mode-m rows [row_offset[m], +row_count[m]) of the
-   * factor are owned here (blocks.PartitionPlan.uniform, blocks.py:47-61). */
+   * entries are the whole tensor.  Sharded (P GPUs, order 3):
+   * entry m is this rank's mode-m slab (X[I_p,:,:], X[:,J_p,:], X[:,:,K_p])
+   * and x_dims[m] its extents; mode-m rows [row_offset[m], +row_count[m]) of
+   * the factor are owned here (blocks.PartitionPlan.uniform, blocks.py:47-61). */
   int x_dtype;
-  const void* x_mode[3];
-  int64_t x_dims[3][3];
-  int64_t dims[3];          /* full extents (factor row counts)             */
-  int64_t row_offset[3];
-  int64_t row_count[3];
+  const void* x_mode[4];
+  int64_t x_dims[4][4];
+  int64_t dims[4];          /* full extents (factor row counts)             */
+  int64_t row_offset[4];
+  int64_t row_count[4];
   int rank;
   int engine;               /* ntf_engine                                   */
   int fuse_gram;            /* 1: refresh grams[m] inside the mode update   */
@@ -145,28 +159,28 @@ typedef struct ntf_plan_desc {
   int inner_sweeps;
   int adapt;
   /* state, caller-owned device buffers (fp64 row-major) */
-  double* factors[3];       /* dims[m] x R  working factors (replicated)    */
-  double* aux[3];           /* row_count[m] x R  auxiliary copies (owned)   */
-  double* duals[3];         /* row_count[m] x R  scaled duals Y (owned)     */
-  double* grams[3];         /* R x R        F_m^T F_m                       */
-  double* colmax;           /* [3][R]       max_i |F_m[i][r]| (W scales of the
+  double* factors[4];       /* dims[m] x R  working factors (replicated)    */
+  double* aux[4];           /* row_count[m] x R  auxiliary copies (owned)   */
+  double* duals[4];         /* row_count[m] x R  scaled duals Y (owned)     */
+  double* grams[4];         /* R x R        F_m^T F_m                       */
+  double* colmax;           /* [order][R]   max_i |F_m[i][r]| (W scales of the
                                tensor-core MTTKRP), kept like the grams     */
-  double* rho;              /* [3]          per-mode penalties              */
-  double* norm_acc;         /* [3][5][2] per-mode scaled sums of squares of
+  double* rho;              /* [order]      per-mode penalties              */
+  double* norm_acc;         /* [order][5][2] per-mode scaled sums of squares of
                                the last sweep, (scale, ssq) with value
                                scale^2*ssq (nrm2-style, no under/overflow):
                                F-aux, aux-aux_prev, F, aux, Y               */
-  const double* norm_all;   /* NULL, or [norm_parts][30]: every shard's
+  const double* norm_all;   /* NULL, or [norm_parts][10 order]: every shard's
                                norm_acc gathered in rank order (P>1); the
                                finalize merges them instead of norm_acc     */
   int norm_parts;           /* rows of norm_all (ignored when NULL)         */
   /* per-iteration outputs: row `it` written by iteration `it` */
   int64_t history_capacity; /* rows available in the history buffers        */
-  double* resid_history;    /* [cap][6]  primal[3], dual[3]                 */
-  double* rho_history;      /* [cap][3]  rho after adaptation               */
+  double* resid_history;    /* [cap][2 order]  primal[order], dual[order]   */
+  double* rho_history;      /* [cap][order]  rho after adaptation           */
   int* counters;            /* [4]: iteration, stop flag, status, spare     */
   /* Verification hook: when non-NULL, iteration `it` sets rho to row `it`
-   * of this [cap][3] device array instead of applying adapt_penalties, so a
+   * of this [cap][order] device array instead of applying adapt_penalties, so a
    * trajectory can be replayed under the reference's penalty sequence. */
   const double* rho_schedule;
   /* Constraint of each mode (reference constraints.py, solver.py:182-193):
@@ -174,8 +188,8 @@ typedef struct ntf_plan_desc {
    * NTF_CONSTRAINT_CARD with card[m] the global nonzero budget (single-GPU
    * plans only), NTF_CONSTRAINT_ROW_STOCHASTIC (rows on the simplex, the
    * equality-constrained row solve). */
-  int constraint[3];
-  int64_t card[3];
+  int constraint[4];
+  int64_t card[4];
   /* Tensor format: NTF_FORMAT_DENSE (x_mode/x_dims as above), or
    * NTF_FORMAT_COO (reference CooTensor, tensors.py:84-132; single GPU, fp64
    * values, x_dtype = NTF_F64, x_mode[m] = coo_vals, x_dims[m] = dims):
@@ -187,8 +201,8 @@ typedef struct ntf_plan_desc {
   int64_t nnz;
   const int64_t* coo_idx;
   const double* coo_vals;
-  const int64_t* coo_perm[3];
-  const int64_t* coo_rowptr[3];
+  const int64_t* coo_perm[4];
+  const int64_t* coo_rowptr[4];
 } ntf_plan_desc;
 
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);

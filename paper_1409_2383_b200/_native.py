@@ -14,6 +14,8 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libntf_b200.so")
 
+ABI_VERSION = 2  # include/ntf_b200.h NTF_ABI_VERSION
+
 NTF_OK = 0
 NTF_ERR_INVALID = 1
 NTF_ERR_NOT_PD = 2
@@ -44,6 +46,7 @@ EXPORTED = (
     "ntf_mttkrp_coo",
     "ntf_sq_error_coo_workspace_bytes",
     "ntf_sq_error_coo",
+    "ntf_khatri_rao_pair",
     "ntf_plan_create",
     "ntf_colmax",
     "ntf_plan_sync_grams",
@@ -77,12 +80,13 @@ class PlanDesc(ctypes.Structure):
     """Mirror of ``ntf_plan_desc`` (include/ntf_b200.h)."""
 
     _fields_ = [
+        ("order", c_int),
         ("x_dtype", c_int),
-        ("x_mode", c_vp * 3),
-        ("x_dims", (c_i64 * 3) * 3),
-        ("dims", c_i64 * 3),
-        ("row_offset", c_i64 * 3),
-        ("row_count", c_i64 * 3),
+        ("x_mode", c_vp * 4),
+        ("x_dims", (c_i64 * 4) * 4),
+        ("dims", c_i64 * 4),
+        ("row_offset", c_i64 * 4),
+        ("row_count", c_i64 * 4),
         ("rank", c_int),
         ("engine", c_int),
         ("fuse_gram", c_int),
@@ -93,10 +97,10 @@ class PlanDesc(ctypes.Structure):
         ("tau_decr", c_dbl),
         ("inner_sweeps", c_int),
         ("adapt", c_int),
-        ("factors", c_vp * 3),
-        ("aux", c_vp * 3),
-        ("duals", c_vp * 3),
-        ("grams", c_vp * 3),
+        ("factors", c_vp * 4),
+        ("aux", c_vp * 4),
+        ("duals", c_vp * 4),
+        ("grams", c_vp * 4),
         ("colmax", c_vp),
         ("rho", c_vp),
         ("norm_acc", c_vp),
@@ -107,14 +111,14 @@ class PlanDesc(ctypes.Structure):
         ("rho_history", c_vp),
         ("counters", c_vp),
         ("rho_schedule", c_vp),
-        ("constraint", ctypes.c_int * 3),
-        ("card", c_i64 * 3),
+        ("constraint", ctypes.c_int * 4),
+        ("card", c_i64 * 4),
         ("x_format", ctypes.c_int),
         ("nnz", c_i64),
         ("coo_idx", c_vp),
         ("coo_vals", c_vp),
-        ("coo_perm", c_vp * 3),
-        ("coo_rowptr", c_vp * 3),
+        ("coo_perm", c_vp * 4),
+        ("coo_rowptr", c_vp * 4),
     ]
 
 
@@ -147,6 +151,8 @@ def _declare(lib):
     lib.ntf_sq_error_coo.restype = c_int
     lib.ntf_sq_error_coo.argtypes = [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
                                      c_vp, c_vp, ctypes.c_size_t, c_vp]
+    lib.ntf_khatri_rao_pair.restype = c_int
+    lib.ntf_khatri_rao_pair.argtypes = [c_vp, c_i64, c_vp, c_i64, c_int, c_vp, c_vp]
     lib.ntf_plan_create.restype = c_int
     lib.ntf_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(c_vp)]
     lib.ntf_colmax.restype = c_int
@@ -185,7 +191,7 @@ def load(build_if_missing: bool = True):
         except OSError as exc:
             raise NativeUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
         _lib = _declare(lib)
-        if _lib.ntf_abi_version() != 1:
+        if _lib.ntf_abi_version() != ABI_VERSION:
             raise NativeUnavailable("ABI version mismatch")
         return _lib
 

@@ -105,13 +105,20 @@ cudaError_t prepare_op(const MttkrpOp& op, int mode, int x_dtype) {
 
 struct ntf_plan {
   ntf_plan_desc d;
-  MttkrpOp op[3];
-  int blocks[3];
+  int order = 3;
+  MttkrpOp op[4];
+  int blocks[4];
   double* mtt_ws = nullptr;
-  double* norm_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][5][2] per mode
-  double* gram_partials[3] = {nullptr, nullptr, nullptr};  // [blocks][R][R] per mode
-  double* card_cand[3] = {nullptr, nullptr, nullptr};      // [rows][R] (cardinality modes)
-  unsigned long long* card_sel[3] = {nullptr, nullptr, nullptr};  // [2] threshold, index cut
+  double* norm_partials[4] = {};  // [blocks][5][2] per mode
+  double* gram_partials[4] = {};  // [blocks][R][R] per mode
+  double* card_cand[4] = {};      // [rows][R] (cardinality modes)
+  unsigned long long* card_sel[4] = {};  // [2] threshold, index cut
+  // order 4: each MTTKRP is an order-3 one on a reshaped view (view 0:
+  // I x J x KL for modes 1-2, view 1: IJ x K x L for modes 3-4) with the
+  // Khatri-Rao pair of the merged modes (C o D, A o B) formed per update
+  int64_t vdims[2][3] = {};
+  double* kr[2] = {};   // view 0: KL x R, view 1: IJ x R
+  double* vcm[2] = {};  // [3][R] column maxima of each view's factors
   double* gram_ws = nullptr;
   bool any_tc = false;
   // all three MTTKRPs on the tensor cores: the ridge factorisation (and the
@@ -128,7 +135,7 @@ struct ntf_plan {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, post_ev = nullptr;
   double* ridge = nullptr;  // [3R*R + R], see ridge_factor_kernel
   // fp16 split planes for the tensor-core engine, one per distinct slab
-  ntf::TcTensor tct[3];
+  ntf::TcTensor tct[4];
   int n_tct = 0;
   // per-launch timing events: 3 per mode update (before MTTKRP, after MTTKRP,
   // after the row update), inner_sweeps * 3 mode updates per iteration
@@ -157,9 +164,12 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   const ntf_plan_desc& d = pl->d;
   const int m = mode - 1;
   const int R = d.rank;
+  const int N = pl->order;
   const int64_t* xd = d.x_dims[m];
   // companions, highest mode first (solver.py:196-204)
-  static const int comp[3][2] = {{2, 1}, {2, 0}, {1, 0}};
+  int comp[3] = {-1, -1, -1};
+  for (int q = N - 1, k = 0; q >= 0; --q)
+    if (q != m) comp[k++] = q;
   if (pl->fused_ridge) {
     const int prev = (m + 2) % 3;  // the factor updated just before this mode
     ntf::TcRidge rg{};
@@ -167,8 +177,8 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
     rg.rows_prev = d.dims[prev];
     rg.gram_prev = d.grams[prev];
     rg.gram_pending = pl->gram_pending + prev;
-    rg.Ga = d.grams[comp[m][0]];
-    rg.Gb = d.grams[comp[m][1]];
+    rg.Ga = d.grams[comp[0]];
+    rg.Gb = d.grams[comp[1]];
     rg.rho = d.rho + m;
     rg.out = pl->ridge;
     rg.status = d.counters + 2;
@@ -188,8 +198,9 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   ntf::RidgeParams rp{};
   rp.mode = mode;
   rp.R = R;
-  rp.Ga = d.grams[comp[m][0]];
-  rp.Gb = d.grams[comp[m][1]];
+  rp.Ga = d.grams[comp[0]];
+  rp.Gb = d.grams[comp[1]];
+  rp.Gc = N == 4 ? d.grams[comp[2]] : nullptr;
   rp.rho = d.rho;
   rp.L = pl->ridge;
   rp.status = d.counters + 2;
@@ -204,8 +215,38 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
     pl->cursor = (pl->cursor + 1) % (pl->n_events / 3);
     NTF_CUDA_TRY(record_event(ev[0], s));
   }
-  NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2], d.factors[0],
-                      d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s, d.colmax));
+  if (N == 4) {
+    // order 4: Khatri-Rao pair of the merged modes, then the order-3 MTTKRP
+    // of the view (modes 1, 2: I x J x KL with C o D; 3, 4: IJ x K x L with A o B)
+    const int v = m < 2 ? 0 : 1;
+    const int vmode = m == 0 ? 1 : (m == 3 ? 3 : 2);
+    const double* cm = d.colmax;
+    ntf::KrMergeParams kp{};
+    kp.R = R;
+    kp.out = pl->kr[v];
+    kp.cm_view = pl->vcm[v];
+    kp.cm_zero = pl->any_tc ? d.colmax + m * R : nullptr;
+    kp.stop_flag = d.counters + 1;
+    if (v == 0) {
+      kp.Fa = d.factors[2], kp.na = d.dims[2], kp.Fb = d.factors[3], kp.nb = d.dims[3];
+      kp.merged_mode = 2;
+      kp.cm_src[0] = cm, kp.cm_src[1] = cm + R, kp.cm_src[2] = cm + 2 * R, kp.cm_src2 = cm + 3 * R;
+    } else {
+      kp.Fa = d.factors[0], kp.na = d.dims[0], kp.Fb = d.factors[1], kp.nb = d.dims[1];
+      kp.merged_mode = 0;
+      kp.cm_src[0] = cm, kp.cm_src[1] = cm + 2 * R, kp.cm_src[2] = cm + 3 * R, kp.cm_src2 = cm + R;
+    }
+    NTF_CUDA_TRY(ntf::kr_merge_launch(kp, s));
+    const int64_t* vd = pl->vdims[v];
+    const double* F0 = v == 0 ? d.factors[0] : pl->kr[1];
+    const double* F1 = v == 0 ? d.factors[1] : d.factors[2];
+    const double* F2 = v == 0 ? pl->kr[0] : d.factors[3];
+    NTF_CUDA_TRY(run_op(pl->op[m], vmode, d.x_dtype, d.x_mode[m], vd[0], vd[1], vd[2], F0, F1, F2, R,
+                        pl->mtt_ws, d.counters + 1, s, pl->vcm[v]));
+  } else {
+    NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2], d.factors[0],
+                        d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s, d.colmax));
+  }
   if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
   NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
   return enqueue_row_update(pl, mode, last, s, ev);
@@ -277,7 +318,8 @@ int enqueue_finalize(ntf_plan* pl, cudaStream_t s) {
   fz.norm_acc = d.norm_all ? d.norm_all : d.norm_acc;
   fz.norm_parts = d.norm_all ? d.norm_parts : 1;
   fz.rho = d.rho;
-  for (int m = 0; m < 3; ++m) fz.dims[m] = d.dims[m];
+  fz.order = pl->order;
+  for (int m = 0; m < pl->order; ++m) fz.dims[m] = d.dims[m];
   fz.R = d.rank;
   fz.eps_abs = d.eps_abs;
   fz.eps_rel = d.eps_rel;
@@ -297,7 +339,7 @@ int enqueue_finalize(ntf_plan* pl, cudaStream_t s) {
 int enqueue_iteration(ntf_plan* pl, cudaStream_t s) {
   const int sweeps = pl->d.inner_sweeps;
   for (int sw = 0; sw < sweeps; ++sw)
-    for (int mode = 1; mode <= 3; ++mode) {
+    for (int mode = 1; mode <= pl->order; ++mode) {
       const int rc = enqueue_mode_update(pl, mode, sw == sweeps - 1, s);
       if (rc != NTF_OK) return rc;
     }
@@ -447,9 +489,12 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if (d.norm_all && d.norm_parts < 1) return fail(NTF_ERR_INVALID, "norm_parts must be >= 1");
   if (!d.rho || !d.norm_acc || !d.counters || !d.resid_history || !d.rho_history || !d.colmax)
     return fail(NTF_ERR_INVALID, "null plan buffer");
+  const int N = d.order == 0 ? 3 : d.order;
+  if (N != 3 && N != 4) return fail(NTF_ERR_UNSUPPORTED, "tensor order must be 3 or 4");
   if (d.x_format != NTF_FORMAT_DENSE && d.x_format != NTF_FORMAT_COO)
     return fail(NTF_ERR_INVALID, "unknown tensor format");
   if (d.x_format == NTF_FORMAT_COO) {
+    if (N != 3) return fail(NTF_ERR_UNSUPPORTED, "COO tensors are order 3");
     if (d.x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "COO values are fp64");
     if (d.nnz < 0 || (d.nnz > 0 && (!d.coo_idx || !d.coo_vals)))
       return fail(NTF_ERR_INVALID, "null COO buffer");
@@ -460,19 +505,36 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
         return fail(NTF_ERR_UNSUPPORTED, "COO tensors are single-GPU");
     }
   }
-  for (int m = 0; m < 3; ++m) {
-    const int64_t* xd = d.x_dims[m];
-    int rc = check_dims(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R);
-    if (rc != NTF_OK) return rc;
+  // order-4 views: I x J x KL (modes 1, 2) and IJ x K x L (modes 3, 4)
+  int64_t vdims[2][3] = {};
+  if (N == 4) {
+    vdims[0][0] = d.dims[0], vdims[0][1] = d.dims[1], vdims[0][2] = d.dims[2] * d.dims[3];
+    vdims[1][0] = d.dims[0] * d.dims[1], vdims[1][1] = d.dims[2], vdims[1][2] = d.dims[3];
+  }
+  auto vmode_of = [](int m) { return m == 0 ? 1 : (m == 3 ? 3 : 2); };
+  for (int m = 0; m < N; ++m) {
     if (!d.x_mode[m] || !d.factors[m] || !d.aux[m] || !d.duals[m] || !d.grams[m])
       return fail(NTF_ERR_INVALID, "null state buffer");
-    if (xd[m] != d.row_count[m]) return fail(NTF_ERR_INVALID, "slab extent != owned row count");
     if (d.row_offset[m] < 0 || d.row_offset[m] + d.row_count[m] > d.dims[m])
       return fail(NTF_ERR_INVALID, "owned rows out of range");
+    const int64_t* xd = d.x_dims[m];
+    if (N == 4) {
+      if (d.row_count[m] != d.dims[m] || d.x_mode[m] != d.x_mode[0])
+        return fail(NTF_ERR_UNSUPPORTED, "order-4 tensors are single-GPU");
+      for (int a = 0; a < 4; ++a)
+        if (xd[a] != d.dims[a]) return fail(NTF_ERR_INVALID, "order-4 extents");
+      const int64_t* vd = vdims[m < 2 ? 0 : 1];
+      int rc = check_dims(vmode_of(m), d.x_dtype, vd[0], vd[1], vd[2], R);
+      if (rc != NTF_OK) return rc;
+      continue;
+    }
+    int rc = check_dims(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R);
+    if (rc != NTF_OK) return rc;
+    if (xd[m] != d.row_count[m]) return fail(NTF_ERR_INVALID, "slab extent != owned row count");
     for (int a = 0; a < 3; ++a)
       if (a != m && xd[a] != d.dims[a]) return fail(NTF_ERR_INVALID, "slab companion extent");
   }
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < N; ++m) {
     if (d.constraint[m] < NTF_CONSTRAINT_NONNEG || d.constraint[m] > NTF_CONSTRAINT_ROW_STOCHASTIC)
       return fail(NTF_ERR_INVALID, "unknown constraint kind");
     if (d.constraint[m] == NTF_CONSTRAINT_CARD) {
@@ -482,21 +544,29 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
         return fail(NTF_ERR_UNSUPPORTED, "cardinality constraint needs the whole factor on one GPU");
     }
   }
-  for (int m = 0; m < 3; ++m)
-    if (d.engine == NTF_ENGINE_TCGEN05 &&
-        !tc_ok(m + 1, d.x_dtype, d.x_dims[m][0], d.x_dims[m][1], d.x_dims[m][2], R))
+  for (int m = 0; m < N; ++m) {
+    const int64_t* xd = N == 4 ? vdims[m < 2 ? 0 : 1] : d.x_dims[m];
+    const int vm = N == 4 ? vmode_of(m) : m + 1;
+    if (d.engine == NTF_ENGINE_TCGEN05 && !tc_ok(vm, d.x_dtype, xd[0], xd[1], xd[2], R))
       return fail(NTF_ERR_UNSUPPORTED, "tcgen05 engine unsupported for this dtype/rank/shape");
+  }
 
   ntf_plan* pl = new (std::nothrow) ntf_plan();
   if (!pl) return fail(NTF_ERR_INVALID, "out of host memory");
   pl->d = d;
+  pl->order = N;
+  for (int v = 0; v < 2; ++v)
+    for (int a = 0; a < 3; ++a) pl->vdims[v][a] = vdims[v][a];
   size_t ws = 0;
   int maxb = 1;
   int64_t max_rows = 1;
   const bool coo = d.x_format == NTF_FORMAT_COO;
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < N; ++m) {
     const int64_t* xd = d.x_dims[m];
-    if (coo) {
+    if (N == 4) {
+      const int64_t* vd = vdims[m < 2 ? 0 : 1];
+      pl->op[m] = make_op(vmode_of(m), d.x_dtype, vd[0], vd[1], vd[2], R, d.engine);
+    } else if (coo) {
       MttkrpOp op;
       op.coo = true;
       for (int a = 0; a < 3; ++a) op.cv.dims[a] = d.dims[a];
@@ -523,7 +593,14 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return rc;
   };
   if ((e = ntf::dev_alloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
-  for (int m = 0; m < 3; ++m) {
+  if (N == 4) {
+    if ((e = ntf::dev_alloc(&pl->kr[0], sizeof(double) * R * vdims[0][2])) != cudaSuccess ||
+        (e = ntf::dev_alloc(&pl->kr[1], sizeof(double) * R * vdims[1][0])) != cudaSuccess ||
+        (e = ntf::dev_alloc(&pl->vcm[0], sizeof(double) * 3 * R)) != cudaSuccess ||
+        (e = ntf::dev_alloc(&pl->vcm[1], sizeof(double) * 3 * R)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "cudaMalloc views"));
+  }
+  for (int m = 0; m < N; ++m) {
     const size_t nb = static_cast<size_t>(pl->blocks[m]);
     if ((e = ntf::dev_alloc(&pl->norm_partials[m], sizeof(double) * 10 * nb)) != cudaSuccess)
       return cleanup(cuda_fail(e, "cudaMalloc norm"));
@@ -548,19 +625,19 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if ((e = cudaEventCreateWithFlags(&pl->post_ev, cudaEventDisableTiming)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaEventCreate"));
   if ((e = ntf::factor_update_prepare(R)) != cudaSuccess) return cleanup(cuda_fail(e, "prepare"));
-  for (int m = 0; m < 3; ++m) {
-    if ((e = prepare_op(pl->op[m], m + 1, d.x_dtype)) != cudaSuccess)
+  for (int m = 0; m < N; ++m) {
+    if ((e = prepare_op(pl->op[m], N == 4 ? vmode_of(m) : m + 1, d.x_dtype)) != cudaSuccess)
       return cleanup(cuda_fail(e, "mttkrp prepare"));
   }
   // Tensor-core engine: split each distinct slab once into its fp16 planes
   // (one-time setup; synchronous so the caller's upload stream is irrelevant).
-  for (int m = 0; m < 3; ++m) pl->any_tc = pl->any_tc || pl->op[m].tc;
+  for (int m = 0; m < N; ++m) pl->any_tc = pl->any_tc || pl->op[m].tc;
   // Opt-in (NTF_B200_FUSED_RIDGE=1): measured slower at c2 today, where the
   // single-CTA ridge (~30 us, serial fp64 divisions) outlasts the streaming
   // CTAs; the side-stream ridge hides it on the 148th SM instead.
   {
     const char* env = getenv("NTF_B200_FUSED_RIDGE");
-    pl->fused_ridge = env && env[0] == '1' && pl->op[0].tc && pl->op[1].tc && pl->op[2].tc;
+    pl->fused_ridge = env && env[0] == '1' && N == 3 && pl->op[0].tc && pl->op[1].tc && pl->op[2].tc;
   }
   if ((e = ntf::dev_alloc(&pl->gram_pending, sizeof(int) * 3)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMalloc flags"));
@@ -568,12 +645,14 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaMemset flags"));
   if (pl->any_tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
-    // one block image per mode (each is laid out for its mode's stream)
-    for (int m = 0; m < 3; ++m) {
+    // one block image per mode (each is laid out for its mode's stream;
+    // order 4: of the mode's reshaped view)
+    for (int m = 0; m < N; ++m) {
       if (!pl->op[m].tc) continue;
       ntf::TcTensor& slot = pl->tct[pl->n_tct++];
-      if ((e = ntf::tc_tensor_create(pl->op[m].tcl, static_cast<const float*>(d.x_mode[m]),
-                                     d.x_dims[m], &slot, nullptr)) != cudaSuccess)
+      const int64_t* xd = N == 4 ? vdims[m < 2 ? 0 : 1] : d.x_dims[m];
+      if ((e = ntf::tc_tensor_create(pl->op[m].tcl, static_cast<const float*>(d.x_mode[m]), xd,
+                                     &slot, nullptr)) != cudaSuccess)
         return cleanup(cuda_fail(e, "tc split"));
       pl->op[m].tct = &slot;
       if ((e = ntf::mttkrp_tc_bind(pl->op[m].tcl, slot)) != cudaSuccess)
@@ -589,12 +668,22 @@ int ntf_plan_sync_grams(ntf_plan* pl, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (pl->gram_pending) NTF_CUDA_TRY(cudaMemsetAsync(pl->gram_pending, 0, sizeof(int) * 3, s));
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < pl->order; ++m) {
     NTF_CUDA_TRY(ntf::gram_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank, pl->d.grams[m],
                                   pl->gram_ws, s));
     NTF_CUDA_TRY(ntf::colmax_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank,
                                     pl->d.colmax + m * pl->d.rank, s));
   }
+  return NTF_OK;
+}
+
+int ntf_khatri_rao_pair(const double* Fa, int64_t na, const double* Fb, int64_t nb, int R, double* out,
+                        ntf_stream_t stream) {
+  if (!Fa || !Fb || !out) return fail(NTF_ERR_INVALID, "null pointer");
+  if (na < 1 || nb < 1 || R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_INVALID, "bad shape");
+  ntf::KrMergeParams kp{};
+  kp.Fa = Fa, kp.na = na, kp.Fb = Fb, kp.nb = nb, kp.R = R, kp.out = out;
+  NTF_CUDA_TRY(ntf::kr_merge_launch(kp, static_cast<cudaStream_t>(stream)));
   return NTF_OK;
 }
 
@@ -607,7 +696,7 @@ int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t s
 
 int ntf_plan_mode_update(ntf_plan* pl, int mode, int last_sweep, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
-  if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
+  if (mode < 1 || mode > pl->order) return fail(NTF_ERR_INVALID, "mode out of range");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int rc = enqueue_mode_update(pl, mode, last_sweep ? 1 : 0, s);
   if (rc != NTF_OK) return rc;
@@ -666,7 +755,7 @@ int ntf_plan_set_timing(ntf_plan* pl, int enable) {
   // the two captured graphs stay cached: toggling is free once both exist
   pl->timing = enable ? 1 : 0;
   if (!enable || pl->events) return NTF_OK;
-  const int n = 3 * 3 * pl->d.inner_sweeps;
+  const int n = 3 * pl->order * pl->d.inner_sweeps;
   pl->events = new (std::nothrow) cudaEvent_t[n];
   if (!pl->events) return fail(NTF_ERR_INVALID, "out of host memory");
   for (int i = 0; i < n; ++i) {
@@ -712,11 +801,15 @@ void ntf_plan_destroy(ntf_plan* pl) {
   if (pl->join_ev) cudaEventDestroy(pl->join_ev);
   if (pl->post_ev) cudaEventDestroy(pl->post_ev);
   ntf::dev_free(pl->ridge);
-  for (int m = 0; m < 3; ++m)
+  for (int m = 0; m < 4; ++m)
     if (pl->op[m].tc) ntf::mttkrp_tc_unbind(pl->op[m].tcl);
   for (int k = 0; k < pl->n_tct; ++k) ntf::tc_tensor_destroy(&pl->tct[k]);
   ntf::dev_free(pl->mtt_ws);
-  for (int m = 0; m < 3; ++m) {
+  for (int v = 0; v < 2; ++v) {
+    ntf::dev_free(pl->kr[v]);
+    ntf::dev_free(pl->vcm[v]);
+  }
+  for (int m = 0; m < 4; ++m) {
     ntf::dev_free(pl->norm_partials[m]);
     ntf::dev_free(pl->gram_partials[m]);
     ntf::dev_free(pl->card_cand[m]);

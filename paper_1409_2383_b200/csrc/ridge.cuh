@@ -8,18 +8,19 @@ namespace ntf {
 
 // ---------------------------------------------------------------------------
 // Ridge Cholesky in shared memory (solver.ridge_cholesky, solver.py:167-175):
-// H = G_a o G_b + rho*I (companion Gram, solver.py:196-204), lower factor
+// H = G_a o G_b (o G_c for order 4) + rho*I (companion Gram, solver.py:196-204), lower factor
 // L with L L^T = H.  Right-looking, one barrier per column: the trailing
 // update uses the unscaled column (L[i][j] L[k][j] / pivot) and columns are
 // scaled at the end.  A non-positive or non-finite pivot raises NOT_PD.
 // ---------------------------------------------------------------------------
 __device__ inline void build_and_factor(double* L, int ldl, int R, const double* __restrict__ Ga,
                                         const double* __restrict__ Gb, double rho, int* status,
-                                        bool* bad) {
+                                        bool* bad, const double* __restrict__ Gc = nullptr) {
   const int tid = threadIdx.x;
   for (int e = tid; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
     double h = Ga[e] * Gb[e];
+    if (Gc) h *= Gc[e];  // order 4: ((G_a o G_b) o G_c), highest mode first
     if (i == k) h += rho;
     L[i * ldl + k] = h;
   }
@@ -66,7 +67,8 @@ __host__ __device__ inline int ridge_smem_doubles(int R) {
 }
 
 __device__ inline void ridge_factor_block(const double* Ga, const double* Gb, double rho, int R,
-                                          double* out, int* status, double* sm) {
+                                          double* out, int* status, double* sm,
+                                          const double* Gc = nullptr) {
   const int ldl = R + 1;
   double* L = sm;
   double* Li = L + R * ldl;  // L^-1 (lower), R <= 64
@@ -76,9 +78,11 @@ __device__ inline void ridge_factor_block(const double* Ga, const double* Gb, do
   double* Hout = out + 2 * R * R + R;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
-    Hout[e] = Ga[e] * Gb[e] + (i == k ? rho : 0.0);
+    double h = Ga[e] * Gb[e];
+    if (Gc) h *= Gc[e];
+    Hout[e] = h + (i == k ? rho : 0.0);
   }
-  build_and_factor(L, ldl, R, Ga, Gb, rho, status, &bad);
+  build_and_factor(L, ldl, R, Ga, Gb, rho, status, &bad, Gc);
   if (bad) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;

@@ -27,7 +27,7 @@ __global__ void ridge_factor_kernel(RidgeParams p) {
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ridge_factor_block(p.Ga, p.Gb, p.rho[p.mode - 1], p.R, p.L, p.status,
-                     reinterpret_cast<double*>(smem_raw));
+                     reinterpret_cast<double*>(smem_raw), p.Gc);
 }
 
 // Row solve of X (L L^T) = rhs for one row held by a warp: lane owns entries
@@ -625,15 +625,16 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int64_t npa
 // (solver.py:258-269), penalty adaptation (solver.py:272-292).
 // ---------------------------------------------------------------------------
 __global__ void finalize_kernel(FinalizeParams p) {
-  // thread (m, c) < 15 merges the shards' (scale, ssq) pairs of one norm in
-  // rank order; thread 0 then closes the iteration
-  __shared__ double nv[15];
+  // thread (m, c) < 5*order merges the shards' (scale, ssq) pairs of one norm
+  // in rank order; thread 0 then closes the iteration
+  __shared__ double nv[20];
+  const int N = p.order;
   int* ctr = p.counters;
   if (ctr[1]) return;  // already stopped: iteration is a no-op
-  if (threadIdx.x < 15) {
+  if (threadIdx.x < 5 * N) {
     ScaledSq a;
     for (int q = 0; q < p.norm_parts; ++q) {
-      const double* s = p.norm_acc + (q * 15 + threadIdx.x) * 2;
+      const double* s = p.norm_acc + (q * 5 * N + threadIdx.x) * 2;
       a.merge(s[0], s[1]);
     }
     nv[threadIdx.x] = a.norm();
@@ -641,9 +642,9 @@ __global__ void finalize_kernel(FinalizeParams p) {
   __syncthreads();
   if (threadIdx.x != 0) return;
   const int64_t it = ctr[0];
-  double primal[3], dual[3];
+  double primal[4], dual[4];
   bool stop = true;
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < N; ++m) {
     const double a[5] = {nv[m * 5], nv[m * 5 + 1], nv[m * 5 + 2], nv[m * 5 + 3], nv[m * 5 + 4]};
     primal[m] = a[0];
     dual[m] = p.rho[m] * a[1];
@@ -653,11 +654,11 @@ __global__ void finalize_kernel(FinalizeParams p) {
     const double dthr = base + p.eps_rel * yn;
     if (primal[m] > pthr || dual[m] > dthr) stop = false;
   }
-  double rho_new[3];
-  for (int m = 0; m < 3; ++m) {
+  double rho_new[4];
+  for (int m = 0; m < N; ++m) {
     const double r = p.rho[m];
     if (p.rho_schedule && it < p.history_capacity) {
-      rho_new[m] = p.rho_schedule[it * 3 + m];
+      rho_new[m] = p.rho_schedule[it * N + m];
     } else if (!p.adapt) {
       rho_new[m] = r;
     } else if (primal[m] > p.mu * dual[m]) {
@@ -669,13 +670,13 @@ __global__ void finalize_kernel(FinalizeParams p) {
     }
   }
   if (it < p.history_capacity) {
-    for (int m = 0; m < 3; ++m) {
-      p.resid_history[it * 6 + m] = primal[m];
-      p.resid_history[it * 6 + 3 + m] = dual[m];
-      p.rho_history[it * 3 + m] = rho_new[m];
+    for (int m = 0; m < N; ++m) {
+      p.resid_history[it * 2 * N + m] = primal[m];
+      p.resid_history[it * 2 * N + N + m] = dual[m];
+      p.rho_history[it * N + m] = rho_new[m];
     }
   }
-  for (int m = 0; m < 3; ++m) p.rho[m] = rho_new[m];
+  for (int m = 0; m < N; ++m) p.rho[m] = rho_new[m];
   ctr[0] = static_cast<int>(it + 1);
   if (stop) ctr[1] = 1;
 }
@@ -903,6 +904,35 @@ __global__ void __launch_bounds__(kUpdThreads) card_apply_kernel(FactorUpdatePar
   q.last_sweep = 1;
   block_partials(q, nrm, nullptr, 0, red);
 }
+
+// Khatri-Rao pair for the order-4 views (tensors.py:203-220 restated for two
+// factors, rows a*nb + b); block 0 also refreshes the view's column maxima.
+__global__ void kr_merge_kernel(KrMergeParams p) {
+  pdl_trigger();
+  pdl_wait();  // the factors come from the preceding row updates
+  if (p.stop_flag && *p.stop_flag) return;
+  const int R = p.R;
+  const int64_t n = p.na * p.nb * R;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e % R);
+    const int64_t row = e / R;
+    const int64_t a = row / p.nb, b = row - (row / p.nb) * p.nb;
+    p.out[e] = p.Fa[a * R + r] * p.Fb[b * R + r];
+  }
+  if (blockIdx.x == 0 && p.cm_view) {
+    // max over (a, b) of |Fa Fb| is the rounded product of the maxima
+    for (int e = threadIdx.x; e < 3 * R; e += blockDim.x) {
+      const int vm = e / R, r = e - (e / R) * R;
+      double v = p.cm_src[vm] ? p.cm_src[vm][r] : 0.0;
+      if (vm == p.merged_mode) v *= p.cm_src2[r];
+      p.cm_view[e] = v;
+    }
+    __syncthreads();
+    if (p.cm_zero)
+      for (int r = threadIdx.x; r < R; r += blockDim.x) p.cm_zero[r] = 0.0;
+  }
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -975,6 +1005,12 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
               : launch(factor_update_warp_kernel<3, kConstraintNonneg>);
   return rs ? launch(factor_update_warp_kernel<4, kConstraintRowStochastic>)
             : launch(factor_update_warp_kernel<4, kConstraintNonneg>);
+}
+
+cudaError_t kr_merge_launch(const KrMergeParams& p, cudaStream_t stream) {
+  const int64_t n = p.na * p.nb * p.R;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4 * 148));
+  return launch_pdl(kr_merge_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, stream, p);
 }
 
 cudaError_t card_select_launch(const double* cand, int64_t n, int64_t card, unsigned long long* sel,

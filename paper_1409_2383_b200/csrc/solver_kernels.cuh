@@ -46,31 +46,53 @@ constexpr int kConstraintNonneg = 0, kConstraintCard = 1, kConstraintRowStochast
 // its ties (stable, row-major order); card_apply then does the aux / dual
 // step (solver.py:311-317) with that projection and the norm partials.
 // sel: [2] uint64 {T bits, idx_cut}.
+// Khatri-Rao pair of two factors for the order-4 views (rows a*nb + b =
+// Fa[a] * Fb[b]); cm: view column maxima [3][R] filled from the factors'
+// maxima (cm_src[3] pointers, the merged view mode as the product of two),
+// and cm_zero ([R], may be NULL) zeroed for the row update that follows.
+struct KrMergeParams {
+  const double* Fa;
+  int64_t na;
+  const double* Fb;
+  int64_t nb;
+  int R;
+  double* out;
+  int merged_mode;          // view mode (0..2) whose factor is out
+  const double* cm_src[3];  // per view mode: factor maxima (merged: cm_src[mm] x cm_src2)
+  const double* cm_src2;
+  double* cm_view;          // [3][R]
+  double* cm_zero;
+  const int* stop_flag;
+};
+cudaError_t kr_merge_launch(const KrMergeParams& p, cudaStream_t stream);
+
 cudaError_t card_select_launch(const double* cand, int64_t n, int64_t card, unsigned long long* sel,
                                const int* stop_flag, cudaStream_t stream);
 cudaError_t card_apply_launch(const FactorUpdateParams& p, const unsigned long long* sel,
                               cudaStream_t stream);
 
 struct FinalizeParams {
-  const double* norm_acc;   // [parts][3][5][scale, ssq]
+  const double* norm_acc;   // [parts][order][5][scale, ssq]
   int norm_parts;           // shards whose norms are merged (1 unsharded)
-  double* rho;              // [3] in/out
-  int64_t dims[3];
+  int order;                // 3 or 4
+  double* rho;              // [order] in/out
+  int64_t dims[4];
   int R;
   double eps_abs, eps_rel, mu, tau_incr, tau_decr;
   int adapt;
   int64_t history_capacity;
-  double* resid_history;    // [cap][6]
-  double* rho_history;      // [cap][3]
+  double* resid_history;    // [cap][2 * order]
+  double* rho_history;      // [cap][order]
   int* counters;            // [0] iteration, [1] stop flag
-  const double* rho_schedule;  // optional [cap][3] replayed penalties
+  const double* rho_schedule;  // optional [cap][order] replayed penalties
 };
 
 struct RidgeParams {
   int mode, R;
   const double* Ga;         // companion Grams (highest mode first)
   const double* Gb;
-  const double* rho;        // device [3]
+  const double* Gc;         // third companion (order-4 tensors), else NULL
+  const double* rho;        // device [order]
   double* L;                // out: [R*R] lower factor + [R] 1/diag
   int* status;
   const int* stop_flag;

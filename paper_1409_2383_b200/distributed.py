@@ -275,6 +275,9 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     specs = normalize_specs(specs, t.order)
     if rank < 1:
         raise ValueError("rank must be >= 1")
+    if t.order != 3 and dist.is_available() and dist.is_initialized() and (
+            dist.get_world_size(group) > 1 or sharded):
+        raise NotImplementedError("order-4 tensors are single-GPU (no sharded order-4 engine)")
     if not (dist.is_available() and dist.is_initialized()) or (
             dist.get_world_size(group) == 1 and not sharded):
         return fit(t, rank, specs, config, engine=engine)

@@ -191,8 +191,36 @@ def coo_sq_error(x: DeviceCoo, factors=None, stream=None):
     return out
 
 
+def kr_pair_device(Fa, Fb, stream=None):
+    """Khatri-Rao pair rows a*nb + b = Fa[a] * Fb[b] (ntf_khatri_rao_pair)."""
+    torch = _torch()
+    lib = N.load()
+    na, R = (int(v) for v in Fa.shape)
+    nb = int(Fb.shape[0])
+    out = torch.empty((na * nb, R), dtype=torch.float64, device=Fa.device)
+    s = stream or torch.cuda.current_stream(Fa.device)
+    N.check(lib.ntf_khatri_rao_pair(_ptr(Fa), na, _ptr(Fb), nb, R, _ptr(out), _stream_handle(s)))
+    return out
+
+
+def order3_view(x, factors=None, stream=None):
+    """An order-4 tensor as the order-3 view I x J x (K L) and its model
+    [A, B, C o D] (the merged mode's Khatri-Rao pair formed on the device);
+    order-3 inputs are returned unchanged."""
+    if x.dim() == 3:
+        return x, factors
+    I, J, K, L = (int(d) for d in x.shape)
+    xv = x.view(I, J, K * L)
+    if factors is None:
+        return xv, None
+    torch = _torch()
+    f = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).to(x.device)
+         if isinstance(v, np.ndarray) else v.contiguous() for v in factors]
+    return xv, [f[0], f[1], kr_pair_device(f[2], f[3], stream)]
+
+
 def tensor_norm(t) -> float:
-    x = device_tensor(t)
+    x, _ = order3_view(device_tensor(t))
     return float(np.sqrt(sq_error(x)[0].item()))
 
 
@@ -254,8 +282,9 @@ class DeviceProblem:
         self.stream = stream or torch.cuda.Stream(device=self.device)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.sharded = slabs is not None
+        self.order = Nm = len(self.dims)
         if slabs is None:
-            slabs = Slabs([x, x, x], (0, 0, 0), self.dims)
+            slabs = Slabs([x] * Nm, (0,) * Nm, self.dims)
         self.slabs = slabs
         dev, f64 = self.device, torch.float64
         R = self.R
@@ -263,24 +292,25 @@ class DeviceProblem:
             self.factors = [torch.zeros((d, R), dtype=f64, device=dev) for d in self.dims]
             self.aux = [torch.zeros((c, R), dtype=f64, device=dev) for c in slabs.row_count]
             self.duals = [torch.zeros((c, R), dtype=f64, device=dev) for c in slabs.row_count]
-            self.grams = [torch.zeros((R, R), dtype=f64, device=dev) for _ in range(3)]
-            self.colmax = torch.zeros((3, R), dtype=f64, device=dev)
-            self.rho = torch.zeros(3, dtype=f64, device=dev)
-            self.norm_acc = torch.zeros(30, dtype=f64, device=dev)
+            self.grams = [torch.zeros((R, R), dtype=f64, device=dev) for _ in range(Nm)]
+            self.colmax = torch.zeros((Nm, R), dtype=f64, device=dev)
+            self.rho = torch.zeros(Nm, dtype=f64, device=dev)
+            self.norm_acc = torch.zeros(10 * Nm, dtype=f64, device=dev)
             # every shard's norm_acc, gathered before finalize (sharded runs)
-            self.norm_all = (torch.zeros(norm_parts * 30, dtype=f64, device=dev)
+            self.norm_all = (torch.zeros(norm_parts * 10 * Nm, dtype=f64, device=dev)
                              if norm_parts > 1 or self.sharded else None)
             cap = max(1, int(history_capacity))
             self.cap = cap
-            self.resid_hist = torch.zeros((cap, 6), dtype=f64, device=dev)
-            self.rho_hist = torch.zeros((cap, 3), dtype=f64, device=dev)
+            self.resid_hist = torch.zeros((cap, 2 * Nm), dtype=f64, device=dev)
+            self.rho_hist = torch.zeros((cap, Nm), dtype=f64, device=dev)
             self.counters = torch.zeros(4, dtype=torch.int32, device=dev)
         d = N.PlanDesc()
+        d.order = Nm
         d.x_dtype = dtype_code(x)
-        for m in range(3):
+        for m in range(Nm):
             xs = slabs.x_mode[m]
             d.x_mode[m] = _ptr(xs)
-            for a in range(3):
+            for a in range(len(xs.shape)):
                 d.x_dims[m][a] = int(xs.shape[a])
             d.dims[m] = self.dims[m]
             d.row_offset[m] = int(slabs.row_offset[m])
@@ -289,6 +319,8 @@ class DeviceProblem:
             d.aux[m] = _ptr(self.aux[m])
             d.duals[m] = _ptr(self.duals[m])
             d.grams[m] = _ptr(self.grams[m])
+        for m in range(Nm, 4):  # unused entries of the fixed-size descriptor
+            d.dims[m] = 0
         d.colmax = _ptr(self.colmax)
         d.rank = R
         d.engine = int(engine)
@@ -314,7 +346,7 @@ class DeviceProblem:
                 d.coo_perm[m] = x.ptr_perm(m)
                 d.coo_rowptr[m] = _ptr(x.rowptr[m])
         if constraints is not None:  # (codes, cards), constraints.plan_codes
-            for m in range(3):
+            for m in range(Nm):
                 d.constraint[m] = int(constraints[0][m])
                 d.card[m] = int(constraints[1][m])
         d.history_capacity = cap
@@ -323,8 +355,8 @@ class DeviceProblem:
         d.counters = _ptr(self.counters)
         self._rho_schedule = None
         if rho_schedule is not None:
-            sched = np.zeros((cap, 3))
-            rs = np.asarray(rho_schedule, dtype=np.float64).reshape(-1, 3)[:cap]
+            sched = np.zeros((cap, Nm))
+            rs = np.asarray(rho_schedule, dtype=np.float64).reshape(-1, Nm)[:cap]
             sched[: len(rs)] = rs
             self._rho_schedule = torch.from_numpy(sched).to(dev)
             d.rho_schedule = _ptr(self._rho_schedule)
@@ -340,7 +372,7 @@ class DeviceProblem:
         torch = self.torch
         off, cnt = self.slabs.row_offset, self.slabs.row_count
         with torch.cuda.stream(self.stream):
-            for m in range(3):
+            for m in range(self.order):
                 self.factors[m].copy_(torch.from_numpy(np.ascontiguousarray(factors[m], dtype=np.float64)))
                 a = np.ascontiguousarray(aux[m], dtype=np.float64)
                 y = np.ascontiguousarray(duals[m], dtype=np.float64)
@@ -362,7 +394,7 @@ class DeviceProblem:
 
     def kernel_times(self) -> np.ndarray:
         """[n_mode_updates][2] ms (MTTKRP, row update) of the latest iteration."""
-        n = 2 * 3 * int(self.config.inner_sweeps)
+        n = 2 * self.order * int(self.config.inner_sweeps)
         buf = (ctypes.c_float * n)()
         got = self.lib.ntf_plan_kernel_times(self._plan, buf, n)
         if got < 0:
@@ -380,7 +412,8 @@ class DeviceProblem:
             if isinstance(self.x, DeviceCoo):
                 out = coo_sq_error(self.x, aux, stream=self.stream)
             else:
-                out = sq_error(self.x, aux, stream=self.stream)
+                xv, fv = order3_view(self.x, aux, stream=self.stream)
+                out = sq_error(xv, fv, stream=self.stream)
             return float(out[0].item()), float(out[1].item())
 
     def aux_model_rfe(self, x_norm: float) -> float:
@@ -392,8 +425,12 @@ class DeviceProblem:
             if isinstance(self.x, DeviceCoo):
                 m = mttkrp_coo_device(self.x, aux, 1, stream=self.stream)
             else:
-                m = mttkrp_device(self.x, aux, 1, self._desc.engine, stream=self.stream)
-            g = gram_device(aux[2], stream=self.stream) * gram_device(aux[1], stream=self.stream)
+                xv, fv = order3_view(self.x, aux, stream=self.stream)
+                m = mttkrp_device(xv, fv, 1, self._desc.engine, stream=self.stream)
+            g = None
+            for f in reversed(aux[1:]):  # companions of mode 1, highest mode first
+                gf = gram_device(f, stream=self.stream)
+                g = gf if g is None else g * gf
             ga = gram_device(aux[0], stream=self.stream)
             cross = float(torch.sum(aux[0] * m).item())
             quad = float(torch.sum(ga * g).item())

@@ -142,12 +142,12 @@ def _engine_code(engine) -> int:
 
 def mttkrp_factors(t, factors: Sequence[np.ndarray], mode: int, engine=None) -> np.ndarray:
     """Device MTTKRP (replaces tensors.mttkrp_factors, tensors.py:254-273):
-    dense (tensor-core / CUDA-core engines) or sparse COO."""
+    dense order 3 or 4 (tensor-core / CUDA-core engines) or sparse COO."""
     from .engine import _torch, device_coo, device_tensor, mttkrp_coo_device, mttkrp_device
 
     torch = _torch()
-    if not 1 <= mode <= 3:
-        raise ValueError(f"mode must be in 1..3, got {mode}")
+    if not 1 <= mode <= 4:
+        raise ValueError(f"mode must be in 1..4, got {mode}")
     if is_sparse(t):
         t = as_coo(t)
         x = device_coo(t)
@@ -159,12 +159,26 @@ def mttkrp_factors(t, factors: Sequence[np.ndarray], mode: int, engine=None) -> 
         torch.cuda.current_stream(x.device).synchronize()
         return out.cpu().numpy()
     t = as_dense(t)
+    if not 1 <= mode <= t.order:
+        raise ValueError(f"mode must be in 1..{t.order}, got {mode}")
     x = device_tensor(t)
     f = [torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(x.device) for v in factors]
+    if len(f) != t.order:
+        raise ValueError("need one factor per mode")
     for m, v in enumerate(f):
         if v.shape[0] != t.dims[m]:
             raise ValueError("factor dims do not match tensor dims")
-    out = mttkrp_device(x, f, mode, _engine_code(engine))
+    if t.order == 4:  # order-3 view with the merged modes' Khatri-Rao pair
+        from .engine import kr_pair_device
+
+        I, J, K, L = t.dims
+        if mode <= 2:
+            xv, fv, vm = x.view(I, J, K * L), [f[0], f[1], kr_pair_device(f[2], f[3])], mode
+        else:
+            xv, fv, vm = x.view(I * J, K, L), [kr_pair_device(f[0], f[1]), f[2], f[3]], mode - 1
+        out = mttkrp_device(xv, fv, vm, _engine_code(engine))
+    else:
+        out = mttkrp_device(x, f, mode, _engine_code(engine))
     torch.cuda.current_stream(x.device).synchronize()
     return out.cpu().numpy()
 
@@ -187,7 +201,7 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
     even where the adaptation rule's branch is decided by rounding noise
     (``p > 0`` at p ~ 1e-17, solver.py:286-291).
     """
-    from .engine import DeviceProblem, device_coo, device_tensor, sq_error
+    from .engine import DeviceProblem, device_coo, device_tensor, order3_view, sq_error
 
     config = config or SolverConfig()
     if is_sparse(t):
@@ -205,7 +219,7 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
         if rank < 1:
             raise ValueError("rank must be >= 1")
         x = device_tensor(t, device)
-        x_norm = math.sqrt(float(sq_error(x)[0].item()))
+        x_norm = math.sqrt(float(sq_error(order3_view(x)[0])[0].item()))
         if x_norm == 0.0:
             raise ValueError("cannot factorize a zero tensor")
     codes = plan_codes(specs, t.dims, rank)
@@ -252,7 +266,8 @@ def _run_fit(prob, x, dims, rank: int, config: SolverConfig, x_norm: float,
                 done, stopped = prob.check_status()
         total += done
         r, rh = prob.histories(done)
-        res_hist = [Residuals(tuple(float(v) for v in row[:3]), tuple(float(v) for v in row[3:]))
+        n = len(dims)
+        res_hist = [Residuals(tuple(float(v) for v in row[:n]), tuple(float(v) for v in row[n:]))
                     for row in r]
         rho_hist = [list(map(float, row)) for row in rh]
         if stopped:
@@ -310,5 +325,6 @@ def iterate(state: SolverState, t, specs=None, config: SolverConfig | None = Non
     prob.check_status()
     r, _ = prob.histories(1)
     factors, aux, duals, rho = prob.read_state()
-    res = Residuals(tuple(float(v) for v in r[0][:3]), tuple(float(v) for v in r[0][3:]))
+    n = len(t.dims)
+    res = Residuals(tuple(float(v) for v in r[0][:n]), tuple(float(v) for v in r[0][n:]))
     return SolverState(factors, aux, duals, rho, state.iteration + 1), res

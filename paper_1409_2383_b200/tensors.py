@@ -4,10 +4,10 @@
 only) and additionally keeps fp32 storage when given fp32 values — the B200
 path streams fp32 tensors for BASELINE configs 2-5.  Values may
 also be a ``torch.Tensor`` (host or device), so a tensor generated on the GPU
-is never copied to the host.  ``CooTensor`` mirrors the reference's sparse
-container (tensors.py:84-132; order 3, fp64); ``fit`` runs it with the COO
-MTTKRP engine on one GPU.  Order-4 inputs are outside the B200 path (SURVEY
-8(f) #4) and are rejected by ``fit``.
+is never copied to the host.  Order-4 dense tensors run on one GPU as
+order-3 views (include/ntf_b200.h).  ``CooTensor`` mirrors the reference's
+sparse container (tensors.py:84-132; order 3, fp64); ``fit`` runs it with the
+COO MTTKRP engine on one GPU.
 """
 
 from __future__ import annotations
@@ -16,7 +16,7 @@ from typing import Sequence
 
 import numpy as np
 
-SUPPORTED_ORDERS = (3,)
+SUPPORTED_ORDERS = (3, 4)
 
 
 def _is_torch(x) -> bool:
@@ -25,7 +25,8 @@ def _is_torch(x) -> bool:
 
 
 class DenseTensor:
-    """Immutable dense order-3 tensor, row-major in (i, j, k)."""
+    """Immutable dense order-3 or order-4 tensor, row-major (reference
+    tensors.py:40-81)."""
 
     __slots__ = ("dims", "values", "_norm", "_device_cache", "__weakref__")
 
@@ -33,8 +34,8 @@ class DenseTensor:
         if _is_torch(values):
             import torch
 
-            if values.dim() != 3:
-                raise ValueError(f"tensor order must be 3, got {values.dim()}")
+            if values.dim() not in SUPPORTED_ORDERS:
+                raise ValueError(f"tensor order must be 3 or 4, got {values.dim()}")
             want = dtype or (torch.float32 if values.dtype == torch.float32 else torch.float64)
             if isinstance(want, type) or isinstance(want, np.dtype):
                 want = torch.float32 if np.dtype(want) == np.float32 else torch.float64
@@ -47,8 +48,8 @@ class DenseTensor:
             if want not in (np.dtype(np.float32), np.dtype(np.float64)):
                 raise ValueError("dtype must be float32 or float64")
             arr = np.array(arr, dtype=want, order="C", copy=arr.dtype != want or not arr.flags.c_contiguous)
-            if arr.ndim != 3:
-                raise ValueError(f"tensor order must be 3, got {arr.ndim}")
+            if arr.ndim not in SUPPORTED_ORDERS:
+                raise ValueError(f"tensor order must be 3 or 4, got {arr.ndim}")
             arr.flags.writeable = False
             self.values = arr
             self.dims = tuple(int(d) for d in arr.shape)
@@ -59,7 +60,7 @@ class DenseTensor:
 
     @property
     def order(self) -> int:
-        return 3
+        return len(self.dims)
 
     @property
     def dtype(self):
@@ -200,7 +201,5 @@ def as_dense(t) -> DenseTensor:
         raise TypeError("a sparse COO tensor is not dense (use as_coo)")
     vals = getattr(t, "values", t)
     if _is_torch(vals) or isinstance(vals, np.ndarray):
-        if getattr(vals, "ndim", 3) == 4:
-            raise NotImplementedError("order-4 tensors are outside the B200 path (SURVEY 8(f) #4)")
         return DenseTensor(vals)
     raise TypeError(f"unsupported tensor type {type(t).__name__}")

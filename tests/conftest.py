@@ -69,6 +69,13 @@ SPARSE_CASES = {
                 track_factors=True, track_rfe=True),
     "sp3": dict(seed=3),
 }
+# cases of make_golden.order4_fits (order-4 dense tensors)
+ORDER4_CASES = {
+    "o4a": dict(seed=1, eps_abs=0.0, eps_rel=0.0, n_max=10, max_restarts=0, track_factors=True),
+    "o4b": dict(seed=2, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, inner_sweeps=2,
+                track_factors=True, track_rfe=True),
+    "o4c": dict(seed=3),
+}
 MESH2_CFG = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=20, max_restarts=0, track_factors=True,
                  inner_sweeps=2)
 

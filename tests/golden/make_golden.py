@@ -217,7 +217,62 @@ def sparse_fits():
     np.savez_compressed(os.path.join(HERE, "sparse.npz"), **st)
 
 
+def order4_fits():
+    """Order-4 dense tensors (tensors.py:40-81, unfold/khatri_rao for N = 4,
+    solver over four modes): MTTKRP goldens and fits."""
+    from cpadmm.constraints import ConstraintSpec
+    from cpadmm.tensors import DenseTensor, mttkrp_factors
+
+    st = {}
+    rng = np.random.default_rng(44)
+    for k, dims in enumerate(((4, 5, 3, 6), (7, 3, 5, 4))):
+        vals = rng.normal(size=dims)
+        t = DenseTensor(vals)
+        fac = [rng.random((d, 3)) for d in dims]
+        st[f"m{k}_x"] = vals
+        for m in range(4):
+            st[f"m{k}_f{m}"] = fac[m]
+            st[f"m{k}_mttkrp{m + 1}"] = mttkrp_factors(t, fac, m + 1)
+    cases = [("o4a", (8, 6, 5, 7), 3, 1e-2, 71, None,
+              dict(seed=1, eps_abs=0.0, eps_rel=0.0, n_max=10, max_restarts=0, track_factors=True)),
+             ("o4b", (6, 9, 4, 5), 2, 1e-3, 72, ("nonneg", "row_stochastic", "nonneg", "nonneg_card:6"),
+              dict(seed=2, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0, inner_sweeps=2,
+                   track_factors=True, track_rfe=True)),
+             ("o4c", (5, 6, 7, 4), 2, 1e-2, 73, None, dict(seed=3))]
+    for name, dims, rank, s2, dseed, specs, kw in cases:
+        t, _ = bench.generate(dims, rank, s2, seed=dseed)
+        cfg = solver.SolverConfig(**kw)
+        sp = None if specs is None else [ConstraintSpec.parse(x) for x in specs]
+        res = cpadmm.fit(t, rank, sp, cfg)
+        st[f"{name}_x"] = np.asarray(t.values)
+        st[f"{name}_rank"] = np.array(rank)
+        st[f"{name}_specs"] = np.array(specs if specs else ("nonneg",) * 4)
+        st[f"{name}_rfe"] = np.array(res.rfe)
+        st[f"{name}_iterations"] = np.array(res.iterations)
+        st[f"{name}_converged"] = np.array(res.converged)
+        st[f"{name}_primal"] = np.array([r.primal for r in res.residual_history])
+        st[f"{name}_dual"] = np.array([r.dual for r in res.residual_history])
+        rho = [cfg.rho_init] * 4
+        rh = []
+        for r in res.residual_history:
+            if cfg.adapt:
+                rho = solver.adapt_penalties(rho, r, cfg)
+            rh.append(list(rho))
+        st[f"{name}_rho"] = np.array(rh)
+        for m, a in enumerate(res.model.factors):
+            st[f"{name}_aux{m}"] = np.asarray(a)
+        if res.factor_history is not None:
+            for m in range(4):
+                st[f"{name}_hist{m}"] = np.stack([h[m] for h in res.factor_history])
+        if res.rfe_history:
+            st[f"{name}_rfe_hist"] = np.array(res.rfe_history)
+    np.savez_compressed(os.path.join(HERE, "order4.npz"), **st)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["order4"]:
+        order4_fits()
+        sys.exit(0)
     if sys.argv[1:] == ["constraints"]:
         constraint_fits()
         sys.exit(0)
@@ -229,6 +284,7 @@ if __name__ == "__main__":
     c1_fixture()
     constraint_fits()
     sparse_fits()
+    order4_fits()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -39,7 +39,7 @@ def test_every_declared_symbol_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.ntf_abi_version() == 1
+    assert lib.ntf_abi_version() == 2
 
 
 def test_plan_desc_layout_matches_c(tmp_path):

@@ -291,7 +291,7 @@ def test_distributed_fit_single_rank_is_fit(golden_small):
 
 def test_library_is_the_one_loaded():
     lib = _native.load()
-    assert lib.ntf_abi_version() == 1
+    assert lib.ntf_abi_version() == 2
     import os
 
     maps = open(f"/proc/{os.getpid()}/maps").read()
@@ -415,3 +415,43 @@ def test_sparse_mttkrp_bitwise_and_fits_match_reference():
             assert np.allclose(res.rfe_history, g[f"{name}_rfe_hist"], rtol=1e-9, atol=0)
     with pytest.raises(ValueError):
         P.CooTensor((3, 3, 3), [[0, 0, 0], [0, 0, 0]], [1.0, 2.0])  # duplicates (tensors.py:103-104)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_order4_mttkrp_and_fits_match_reference(dtype):
+    """Order-4 dense tensors on the device: each MTTKRP runs as an order-3 one
+    on the reshaped view (I x J x KL or IJ x K x L) with the merged modes'
+    Khatri-Rao pair; fp64 MTTKRPs within 1e-12 of the reference (fp32 input:
+    within 5e-8 of the oracle on the same fp32 values); fits within 1e-9 per iteration
+    (penalty sequence replayed), RFE and track_rfe likewise."""
+    from conftest import ORDER4_CASES, load_golden
+
+    g = load_golden("order4.npz")
+    for k in range(2):
+        x = g[f"m{k}_x"].astype(dtype)
+        if dtype == np.float32:  # fixed-point split: 22 bits of max|X| (U[0,1) data, as the fp32 tests)
+            x = np.random.default_rng(k).random(x.shape).astype(np.float32)
+        f = [g[f"m{k}_f{m}"] for m in range(4)]
+        t = P.DenseTensor(x)
+        for m in range(4):
+            want = g[f"m{k}_mttkrp{m + 1}"] if dtype == np.float64 else O.mttkrp(
+                O.OracleTensor(x.astype(np.float64)), f, m + 1)
+            # fp32: the split's 2^-22 (of max|X|) rounding averages over only
+            # 60-90 terms at these tiny shapes
+            assert rel(P.mttkrp_factors(t, f, m + 1), want) <= (1e-12 if dtype == np.float64 else 5e-8)
+    if dtype == np.float32:
+        return
+    for name, kw in ORDER4_CASES.items():
+        specs = [P.ConstraintSpec.parse(str(s)) for s in g[f"{name}_specs"]]
+        res = P.fit(g[f"{name}_x"], int(g[f"{name}_rank"]), specs, P.SolverConfig(**kw),
+                    rho_schedule=g[f"{name}_rho"] if kw.get("eps_abs", 1) == 0.0 else None)
+        assert res.iterations == int(g[f"{name}_iterations"])
+        assert abs(res.rfe - float(g[f"{name}_rfe"])) <= 1e-9 * float(g[f"{name}_rfe"])
+        for m in range(4):
+            assert rel(res.model.factors[m], g[f"{name}_aux{m}"]) <= 1e-9
+        if f"{name}_hist0" in g:
+            for it in range(len(res.factor_history)):
+                for m in range(4):
+                    assert rel(res.factor_history[it][m], g[f"{name}_hist{m}"][it]) <= 1e-9
+        if f"{name}_rfe_hist" in g:
+            assert np.allclose(res.rfe_history, g[f"{name}_rfe_hist"], rtol=1e-9, atol=0)

@@ -190,3 +190,23 @@ def test_sparse_mttkrp_and_fits_match_reference():
         assert np.array_equal(np.array([p for p, _ in res.residual_history]), g[f"{name}_primal"])
         for m in range(3):
             assert np.array_equal(res.factors[m], g[f"{name}_aux{m}"])
+
+
+def test_order4_mttkrp_and_fits_match_reference():
+    """Order-4 dense tensors (unfold / khatri_rao for N = 4, four-mode
+    solver): the oracle reproduces the reference bit for bit."""
+    from conftest import ORDER4_CASES, load_golden
+
+    g = load_golden("order4.npz")
+    for k in range(2):
+        t = O.OracleTensor(g[f"m{k}_x"])
+        f = [g[f"m{k}_f{m}"] for m in range(4)]
+        for m in range(4):
+            assert np.array_equal(O.mttkrp(t, f, m + 1), g[f"m{k}_mttkrp{m + 1}"])
+    for name, kw in ORDER4_CASES.items():
+        specs = [str(s) for s in g[f"{name}_specs"]]
+        res = O.fit(g[f"{name}_x"], int(g[f"{name}_rank"]), O.Config(**kw), specs)
+        assert res.iterations == int(g[f"{name}_iterations"])
+        assert res.rfe == float(g[f"{name}_rfe"])
+        for m in range(4):
+            assert np.array_equal(res.factors[m], g[f"{name}_aux{m}"])
