@@ -89,22 +89,24 @@ int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, co
                  size_t workspace_bytes, ntf_stream_t stream);
 
 /* Sparse COO MTTKRP, one mode: replaces tensors.mttkrp_factors' sparse branch
- * (tensors.py:263-273).  Entries sorted lexicographically (idx [nnz][3]);
- * perm: the entries ordered by index `mode` (stable; NULL for mode 1),
- * rowptr: its row segments [dims[mode-1]+1].  Per (row, column) the
- * products F_c0 * F_c1 * val are summed in entry order, as np.add.at:
- * bitwise equal to the reference.  out: M x R fp64. */
-int ntf_mttkrp_coo(int mode, int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
-                   const double* vals, const int64_t* perm, const int64_t* rowptr, const double* A,
-                   const double* B, const double* C, int R, double* out, ntf_stream_t stream);
+ * (tensors.py:263-273) for order 3 or 4.  Entries sorted lexicographically
+ * (idx [nnz][order]); perm: the entries ordered by index `mode` (stable; NULL
+ * for mode 1), rowptr: its row segments [dims[mode-1]+1]; factors[order]
+ * (the mode's own entry unused).  Per (row, column) the products of the
+ * companion rows (highest mode first) times val are summed in entry order,
+ * as np.add.at: bitwise equal to the reference.  out: dims[mode-1] x R fp64. */
+int ntf_mttkrp_coo(int order, const int64_t* dims, int mode, int64_t nnz, const int64_t* idx,
+                   const double* vals, const int64_t* perm, const int64_t* rowptr,
+                   const double* const* factors, int R, double* out, ntf_stream_t stream);
 
 /* COO sum of squares and model residual by the Gram identity
  * (CooTensor.norm tensors.py:114-115, tensors.rfe sparse tensors.py:291-301):
- * out2[0] = sum vals^2, out2[1] = ||X||^2 - 2<X, W> + sum((A'A)*(B'B)*(C'C)). */
+ * out2[0] = sum vals^2, out2[1] = ||X||^2 - 2<X, W> + sum(Hadamard of the
+ * factor Grams); factors may be NULL (only out2[0]). */
 size_t ntf_sq_error_coo_workspace_bytes(int64_t nnz);
-int ntf_sq_error_coo(int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
-                     const double* vals, const double* A, const double* B, const double* C, int R,
-                     double* out2, void* workspace, size_t workspace_bytes, ntf_stream_t stream);
+int ntf_sq_error_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* idx,
+                     const double* vals, const double* const* factors, int R, double* out2,
+                     void* workspace, size_t workspace_bytes, ntf_stream_t stream);
 
 /* Khatri-Rao pair out[a*nb + b][r] = Fa[a][r] * Fb[b][r] (tensors.khatri_rao,
  * tensors.py:203-220, for two factors): the merged factor of an order-4
@@ -114,8 +116,8 @@ int ntf_khatri_rao_pair(const double* Fa, int64_t na, const double* Fb, int64_t 
 
 /* ---------------------------------------------------------------------------
  * Solver plan: device-resident ADMoM outer iterations for one order-3 or
- * order-4 tensor (order 3: dense or sparse COO, sharded or not; order 4:
- * dense on one GPU) and a constraint per mode.  Replaces solver.iterate
+ * order-4 tensor (dense order 3 sharded or not; dense order 4 and sparse
+ * COO of either order on one GPU) and a constraint per mode.  Replaces solver.iterate
  * (solver.py:295-327) and the per-iteration part of solver.fit
  * (solver.py:375-387): Gauss-Seidel sweeps of _factor_update_core
  * (solver.py:207-219), aux/dual updates fused into each mode's last sweep
@@ -193,7 +195,7 @@ typedef struct ntf_plan_desc {
   /* Tensor format: NTF_FORMAT_DENSE (x_mode/x_dims as above), or
    * NTF_FORMAT_COO (reference CooTensor, tensors.py:84-132; single GPU, fp64
    * values, x_dtype = NTF_F64, x_mode[m] = coo_vals, x_dims[m] = dims):
-   * nnz entries sorted lexicographically, coo_idx [nnz][3] int64, and per
+   * nnz entries sorted lexicographically, coo_idx [nnz][order] int64, and per
    * mode m a stable order of the entries by index m (coo_perm[m], NULL for
    * mode 1 = the entry order) with its row segments coo_rowptr[m]
    * [dims[m]+1]. */

@@ -144,13 +144,13 @@ def _declare(lib):
     lib.ntf_sq_error.argtypes = [c_int, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp,
                                  c_vp, ctypes.c_size_t, c_vp]
     lib.ntf_mttkrp_coo.restype = c_int
-    lib.ntf_mttkrp_coo.argtypes = [c_int, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                   c_vp, c_vp, c_int, c_vp, c_vp]
+    lib.ntf_mttkrp_coo.argtypes = [c_int, c_vp, c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
+                                   c_vp, c_vp]
     lib.ntf_sq_error_coo_workspace_bytes.restype = ctypes.c_size_t
     lib.ntf_sq_error_coo_workspace_bytes.argtypes = [c_i64]
     lib.ntf_sq_error_coo.restype = c_int
-    lib.ntf_sq_error_coo.argtypes = [c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_int,
-                                     c_vp, c_vp, ctypes.c_size_t, c_vp]
+    lib.ntf_sq_error_coo.argtypes = [c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp,
+                                     ctypes.c_size_t, c_vp]
     lib.ntf_khatri_rao_pair.restype = c_int
     lib.ntf_khatri_rao_pair.argtypes = [c_vp, c_i64, c_vp, c_i64, c_int, c_vp, c_vp]
     lib.ntf_plan_create.restype = c_int

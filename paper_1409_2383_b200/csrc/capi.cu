@@ -60,6 +60,7 @@ struct MttkrpOp {
   bool tc = false;
   bool coo = false;          // sparse COO tensor (mttkrp_coo.cu): one fp64 "split", the whole output
   ntf::CooView cv{};
+  const double* f3 = nullptr;  // order-4 COO: the fourth factor
   ntf::MttkrpCCLaunch cc{};
   ntf::MttkrpTCLaunch tcl{};
   const ntf::TcTensor* tct = nullptr;  // fp16 split planes (tensor-core engine)
@@ -89,7 +90,10 @@ cudaError_t run_op(MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
                    const int* stop, cudaStream_t s, const double* colmax3 = nullptr,
                    const ntf::TcRidge* ridge = nullptr) {
-  if (op.coo) return ntf::mttkrp_coo_launch(op.cv, mode, A, B, C, R, ws, stop, s);
+  if (op.coo) {  // the order's factors follow A, B, C in the plan (D: op.f3)
+    const double* F[4] = {A, B, C, op.f3};
+    return ntf::mttkrp_coo_launch(op.cv, mode, F, R, ws, stop, s);
+  }
   if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s, ridge);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
 }
@@ -215,7 +219,7 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
     pl->cursor = (pl->cursor + 1) % (pl->n_events / 3);
     NTF_CUDA_TRY(record_event(ev[0], s));
   }
-  if (N == 4) {
+  if (N == 4 && !pl->op[m].coo) {
     // order 4: Khatri-Rao pair of the merged modes, then the order-3 MTTKRP
     // of the view (modes 1, 2: I x J x KL with C o D; 3, 4: IJ x K x L with A o B)
     const int v = m < 2 ? 0 : 1;
@@ -433,48 +437,59 @@ int ntf_sq_error(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K, co
   return NTF_OK;
 }
 
-int ntf_mttkrp_coo(int mode, int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
-                   const double* vals, const int64_t* perm, const int64_t* rowptr, const double* A,
-                   const double* B, const double* C, int R, double* out, ntf_stream_t stream) {
-  if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
-  if (I < 1 || J < 1 || K < 1 || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
+int ntf_mttkrp_coo(int order, const int64_t* dims, int mode, int64_t nnz, const int64_t* idx,
+                   const double* vals, const int64_t* perm, const int64_t* rowptr,
+                   const double* const* factors, int R, double* out, ntf_stream_t stream) {
+  if (order != 3 && order != 4) return fail(NTF_ERR_UNSUPPORTED, "tensor order must be 3 or 4");
+  if (mode < 1 || mode > order) return fail(NTF_ERR_INVALID, "mode out of range");
+  if (!dims || !factors || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
+  for (int m = 0; m < order; ++m)
+    if (dims[m] < 1) return fail(NTF_ERR_INVALID, "bad shape");
   if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
   if (!out || !rowptr || (nnz > 0 && (!idx || !vals || (mode > 1 && !perm))))
     return fail(NTF_ERR_INVALID, "null pointer");
-  if ((mode != 1 && !A) || (mode != 2 && !B) || (mode != 3 && !C))
-    return fail(NTF_ERR_INVALID, "missing companion factor");
+  for (int m = 0; m < order; ++m)
+    if (m != mode - 1 && !factors[m]) return fail(NTF_ERR_INVALID, "missing companion factor");
   ntf::CooView v{};
-  v.dims[0] = I;
-  v.dims[1] = J;
-  v.dims[2] = K;
+  v.order = order;
+  for (int m = 0; m < order; ++m) v.dims[m] = dims[m];
   v.nnz = nnz;
   v.idx = idx;
   v.vals = vals;
   v.perm[mode - 1] = mode > 1 ? perm : nullptr;
   v.rowptr[mode - 1] = rowptr;
-  NTF_CUDA_TRY(ntf::mttkrp_coo_launch(v, mode, A, B, C, R, out, nullptr,
-                                      static_cast<cudaStream_t>(stream)));
+  const double* F[4] = {factors[0], factors[1], factors[2], order == 4 ? factors[3] : nullptr};
+  NTF_CUDA_TRY(ntf::mttkrp_coo_launch(v, mode, F, R, out, nullptr, static_cast<cudaStream_t>(stream)));
   return NTF_OK;
 }
 
 size_t ntf_sq_error_coo_workspace_bytes(int64_t nnz) { return ntf::coo_sq_error_workspace_bytes(nnz, 0); }
 
-int ntf_sq_error_coo(int64_t I, int64_t J, int64_t K, int64_t nnz, const int64_t* idx,
-                     const double* vals, const double* A, const double* B, const double* C, int R,
-                     double* out2, void* workspace, size_t workspace_bytes, ntf_stream_t stream) {
-  if (I < 1 || J < 1 || K < 1 || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
+int ntf_sq_error_coo(int order, const int64_t* dims, int64_t nnz, const int64_t* idx,
+                     const double* vals, const double* const* factors, int R, double* out2,
+                     void* workspace, size_t workspace_bytes, ntf_stream_t stream) {
+  if (order != 3 && order != 4) return fail(NTF_ERR_UNSUPPORTED, "tensor order must be 3 or 4");
+  if (!dims || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
+  for (int m = 0; m < order; ++m)
+    if (dims[m] < 1) return fail(NTF_ERR_INVALID, "bad shape");
   if (!out2 || !workspace || (nnz > 0 && (!idx || !vals))) return fail(NTF_ERR_INVALID, "null pointer");
-  if (A && (!B || !C || R < 1 || R > NTF_MAX_RANK)) return fail(NTF_ERR_INVALID, "bad model");
+  if (factors) {
+    if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_INVALID, "bad model");
+    for (int m = 0; m < order; ++m)
+      if (!factors[m]) return fail(NTF_ERR_INVALID, "bad model");
+  }
   if (workspace_bytes < ntf::coo_sq_error_workspace_bytes(nnz, R))
     return fail(NTF_ERR_INVALID, "workspace too small");
   ntf::CooView v{};
-  v.dims[0] = I;
-  v.dims[1] = J;
-  v.dims[2] = K;
+  v.order = order;
+  for (int m = 0; m < order; ++m) v.dims[m] = dims[m];
   v.nnz = nnz;
   v.idx = idx;
   v.vals = vals;
-  NTF_CUDA_TRY(ntf::coo_sq_error_launch(v, A, B, C, A ? R : 0, out2, workspace,
+  const double* F[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (factors)
+    for (int m = 0; m < order; ++m) F[m] = factors[m];
+  NTF_CUDA_TRY(ntf::coo_sq_error_launch(v, factors ? F : nullptr, factors ? R : 0, out2, workspace,
                                         static_cast<cudaStream_t>(stream)));
   return NTF_OK;
 }
@@ -493,12 +508,12 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if (N != 3 && N != 4) return fail(NTF_ERR_UNSUPPORTED, "tensor order must be 3 or 4");
   if (d.x_format != NTF_FORMAT_DENSE && d.x_format != NTF_FORMAT_COO)
     return fail(NTF_ERR_INVALID, "unknown tensor format");
-  if (d.x_format == NTF_FORMAT_COO) {
-    if (N != 3) return fail(NTF_ERR_UNSUPPORTED, "COO tensors are order 3");
+  const bool coo = d.x_format == NTF_FORMAT_COO;
+  if (coo) {
     if (d.x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "COO values are fp64");
     if (d.nnz < 0 || (d.nnz > 0 && (!d.coo_idx || !d.coo_vals)))
       return fail(NTF_ERR_INVALID, "null COO buffer");
-    for (int m = 0; m < 3; ++m) {
+    for (int m = 0; m < N; ++m) {
       if (!d.coo_rowptr[m] || (m > 0 && d.nnz > 0 && !d.coo_perm[m]))
         return fail(NTF_ERR_INVALID, "null COO mode order");
       if (d.row_count[m] != d.dims[m] || d.row_offset[m] != 0)
@@ -507,7 +522,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   }
   // order-4 views: I x J x KL (modes 1, 2) and IJ x K x L (modes 3, 4)
   int64_t vdims[2][3] = {};
-  if (N == 4) {
+  if (N == 4 && !coo) {
     vdims[0][0] = d.dims[0], vdims[0][1] = d.dims[1], vdims[0][2] = d.dims[2] * d.dims[3];
     vdims[1][0] = d.dims[0] * d.dims[1], vdims[1][1] = d.dims[2], vdims[1][2] = d.dims[3];
   }
@@ -518,6 +533,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     if (d.row_offset[m] < 0 || d.row_offset[m] + d.row_count[m] > d.dims[m])
       return fail(NTF_ERR_INVALID, "owned rows out of range");
     const int64_t* xd = d.x_dims[m];
+    if (coo) continue;  // the COO engine reads the entries directly
     if (N == 4) {
       if (d.row_count[m] != d.dims[m] || d.x_mode[m] != d.x_mode[0])
         return fail(NTF_ERR_UNSUPPORTED, "order-4 tensors are single-GPU");
@@ -544,7 +560,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
         return fail(NTF_ERR_UNSUPPORTED, "cardinality constraint needs the whole factor on one GPU");
     }
   }
-  for (int m = 0; m < N; ++m) {
+  for (int m = 0; m < N && !coo; ++m) {
     const int64_t* xd = N == 4 ? vdims[m < 2 ? 0 : 1] : d.x_dims[m];
     const int vm = N == 4 ? vmode_of(m) : m + 1;
     if (d.engine == NTF_ENGINE_TCGEN05 && !tc_ok(vm, d.x_dtype, xd[0], xd[1], xd[2], R))
@@ -560,25 +576,26 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   size_t ws = 0;
   int maxb = 1;
   int64_t max_rows = 1;
-  const bool coo = d.x_format == NTF_FORMAT_COO;
   for (int m = 0; m < N; ++m) {
     const int64_t* xd = d.x_dims[m];
-    if (N == 4) {
-      const int64_t* vd = vdims[m < 2 ? 0 : 1];
-      pl->op[m] = make_op(vmode_of(m), d.x_dtype, vd[0], vd[1], vd[2], R, d.engine);
-    } else if (coo) {
+    if (coo) {
       MttkrpOp op;
       op.coo = true;
-      for (int a = 0; a < 3; ++a) op.cv.dims[a] = d.dims[a];
+      op.cv.order = N;
+      for (int a = 0; a < N; ++a) op.cv.dims[a] = d.dims[a];
       op.cv.nnz = d.nnz;
       op.cv.idx = d.coo_idx;
       op.cv.vals = d.coo_vals;
-      for (int a = 0; a < 3; ++a) {
+      for (int a = 0; a < N; ++a) {
         op.cv.perm[a] = d.coo_perm[a];
         op.cv.rowptr[a] = d.coo_rowptr[a];
       }
+      op.f3 = N == 4 ? d.factors[3] : nullptr;
       pl->op[m] = op;
       ws = std::max(ws, static_cast<size_t>(d.dims[m]) * R * sizeof(double));
+    } else if (N == 4) {
+      const int64_t* vd = vdims[m < 2 ? 0 : 1];
+      pl->op[m] = make_op(vmode_of(m), d.x_dtype, vd[0], vd[1], vd[2], R, d.engine);
     } else {
       pl->op[m] = make_op(m + 1, d.x_dtype, xd[0], xd[1], xd[2], R, d.engine);
     }
@@ -593,7 +610,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return rc;
   };
   if ((e = ntf::dev_alloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
-  if (N == 4) {
+  if (N == 4 && !coo) {
     if ((e = ntf::dev_alloc(&pl->kr[0], sizeof(double) * R * vdims[0][2])) != cudaSuccess ||
         (e = ntf::dev_alloc(&pl->kr[1], sizeof(double) * R * vdims[1][0])) != cudaSuccess ||
         (e = ntf::dev_alloc(&pl->vcm[0], sizeof(double) * 3 * R)) != cudaSuccess ||

@@ -110,15 +110,17 @@ class DeviceCoo:
         torch = _torch()
         dev = torch.device(device or "cuda")
         self.dims = tuple(int(d) for d in t.dims)
+        self.order = len(self.dims)
         self.shape = self.dims
         self.nnz = int(t.vals.shape[0])
         self.device = dev
         self.dtype = torch.float64
-        idx = np.ascontiguousarray(t.indices, dtype=np.int64).reshape(-1, 3)
+        idx = np.ascontiguousarray(t.indices, dtype=np.int64).reshape(-1, self.order)
         self.idx = torch.from_numpy(idx.copy()).to(dev)
         self.vals = torch.from_numpy(np.ascontiguousarray(t.vals, dtype=np.float64).copy()).to(dev)
+        self._dims_arr = (ctypes.c_int64 * 4)(*(list(self.dims) + [0] * (4 - self.order)))
         self.perm, self.rowptr = [], []
-        for m in range(3):
+        for m in range(self.order):
             key = idx[:, m]
             if m == 0:  # lexicographic order is already sorted by the first index
                 self.perm.append(None)
@@ -156,16 +158,24 @@ def device_coo(t, device=None) -> DeviceCoo:
     return d
 
 
+def _ptr_array(tensors):
+    arr = (ctypes.c_void_p * 4)()
+    for i, t in enumerate(tensors):
+        arr[i] = _ptr(t)
+    return arr
+
+
 def mttkrp_coo_device(x: DeviceCoo, factors, mode: int, stream=None):
     torch = _torch()
     lib = N.load()
     R = int(factors[0].shape[1])
     out = torch.empty((x.dims[mode - 1], R), dtype=torch.float64, device=x.device)
     s = stream or torch.cuda.current_stream(x.device)
-    a, b, c = (_ptr(f) for f in factors)
-    N.check(lib.ntf_mttkrp_coo(mode, x.dims[0], x.dims[1], x.dims[2], x.nnz, x.ptr_idx(),
+    fa = _ptr_array(factors)
+    N.check(lib.ntf_mttkrp_coo(x.order, ctypes.addressof(x._dims_arr), mode, x.nnz, x.ptr_idx(),
                                x.vals.data_ptr() if x.nnz else None, x.ptr_perm(mode - 1),
-                               _ptr(x.rowptr[mode - 1]), a, b, c, R, _ptr(out), _stream_handle(s)))
+                               _ptr(x.rowptr[mode - 1]), ctypes.addressof(fa), R, _ptr(out),
+                               _stream_handle(s)))
     return out
 
 
@@ -177,16 +187,16 @@ def coo_sq_error(x: DeviceCoo, factors=None, stream=None):
     ws = torch.empty(max(1, wsb // 8 + 1), dtype=torch.float64, device=x.device)
     out = torch.zeros(2, dtype=torch.float64, device=x.device)
     s = stream or torch.cuda.current_stream(x.device)
-    if factors is None:
-        a = b = c = None
-        R = 0
-    else:
+    fa = None
+    R = 0
+    if factors is not None:
         f = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).to(x.device)
              if isinstance(v, np.ndarray) else v.contiguous() for v in factors]
-        a, b, c = (_ptr(v) for v in f)
+        fa = _ptr_array(f)
         R = int(f[0].shape[1])
-    N.check(lib.ntf_sq_error_coo(x.dims[0], x.dims[1], x.dims[2], x.nnz, x.ptr_idx(),
-                                 x.vals.data_ptr() if x.nnz else None, a, b, c, R, _ptr(out),
+    N.check(lib.ntf_sq_error_coo(x.order, ctypes.addressof(x._dims_arr), x.nnz, x.ptr_idx(),
+                                 x.vals.data_ptr() if x.nnz else None,
+                                 ctypes.addressof(fa) if fa is not None else None, R, _ptr(out),
                                  _ptr(ws), ws.numel() * 8, _stream_handle(s)))
     return out
 
@@ -342,7 +352,7 @@ class DeviceProblem:
             d.nnz = x.nnz
             d.coo_idx = x.ptr_idx()
             d.coo_vals = x.vals.data_ptr() if x.nnz else None
-            for m in range(3):
+            for m in range(x.order):
                 d.coo_perm[m] = x.ptr_perm(m)
                 d.coo_rowptr[m] = _ptr(x.rowptr[m])
         if constraints is not None:  # (codes, cards), constraints.plan_codes

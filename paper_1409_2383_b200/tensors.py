@@ -124,25 +124,26 @@ class KruskalModel:
 
 
 class CooTensor:
-    """Sparse order-3 tensor in coordinate form, entries sorted
+    """Sparse order-3 or order-4 tensor in coordinate form, entries sorted
     lexicographically, duplicates rejected (reference tensors.py:84-132)."""
 
     __slots__ = ("dims", "indices", "vals", "_device_cache", "__weakref__")
 
     def __init__(self, dims: Sequence[int], indices, vals):
         self.dims = tuple(int(d) for d in dims)
-        if len(self.dims) != 3:
-            raise ValueError(f"tensor order must be 3, got {len(self.dims)}")
+        if len(self.dims) not in SUPPORTED_ORDERS:
+            raise ValueError(f"tensor order must be 3 or 4, got {len(self.dims)}")
         if any(d < 1 for d in self.dims):
             raise ValueError(f"all extents must be >= 1, got {self.dims}")
-        idx = np.asarray(indices, dtype=np.int64).reshape(-1, 3)
+        n = len(self.dims)
+        idx = np.asarray(indices, dtype=np.int64).reshape(-1, n)
         v = np.asarray(vals, dtype=np.float64).reshape(-1)
         if idx.shape[0] != v.shape[0]:
             raise ValueError("index rows and value count differ")
         if idx.size:
             if idx.min() < 0 or np.any(idx >= np.array(self.dims)):
                 raise ValueError("entry index out of bounds")
-            order = np.lexsort((idx[:, 2], idx[:, 1], idx[:, 0]))
+            order = np.lexsort(tuple(idx[:, m] for m in reversed(range(n))))
             idx, v = idx[order], v[order]
             if np.any(np.all(np.diff(idx, axis=0) == 0, axis=1)):
                 raise ValueError("duplicate entry indices")
@@ -154,7 +155,7 @@ class CooTensor:
 
     @property
     def order(self) -> int:
-        return 3
+        return len(self.dims)
 
     @property
     def nnz(self) -> int:
@@ -166,7 +167,7 @@ class CooTensor:
 
     def to_dense(self) -> DenseTensor:
         out = np.zeros(self.dims)
-        out[tuple(self.indices[:, m] for m in range(3))] = self.vals
+        out[tuple(self.indices[:, m] for m in range(self.order))] = self.vals
         return DenseTensor(out)
 
     @classmethod
@@ -187,8 +188,6 @@ def as_coo(t) -> CooTensor:
     """Our CooTensor, or the reference's (duck-typed on dims/indices/vals)."""
     if isinstance(t, CooTensor):
         return t
-    if len(t.dims) != 3:
-        raise NotImplementedError("order-4 tensors are outside the B200 path (SURVEY 8(f) #4)")
     return CooTensor(t.dims, t.indices, t.vals)
 
 

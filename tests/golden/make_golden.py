@@ -266,7 +266,44 @@ def order4_fits():
                 st[f"{name}_hist{m}"] = np.stack([h[m] for h in res.factor_history])
         if res.rfe_history:
             st[f"{name}_rfe_hist"] = np.array(res.rfe_history)
+    # sparse order-4 (COO with four indices)
+    from cpadmm.tensors import CooTensor
+
+    for k, (dims, density) in enumerate((((4, 5, 3, 6), 0.3), ((6, 3, 4, 5), 0.5))):
+        vals = rng.normal(size=dims) * (rng.random(dims) < density)
+        t = CooTensor.from_dense(DenseTensor(vals))
+        fac = [rng.random((d, 3)) for d in dims]
+        st[f"s{k}_idx"] = np.asarray(t.indices)
+        st[f"s{k}_vals"] = np.asarray(t.vals)
+        st[f"s{k}_dims"] = np.array(dims)
+        for m in range(4):
+            st[f"s{k}_f{m}"] = fac[m]
+            st[f"s{k}_mttkrp{m + 1}"] = mttkrp_factors(t, fac, m + 1)
+    dense, _ = bench.generate((7, 6, 5, 6), 2, 1e-2, seed=74)
+    mask = np.random.default_rng(1074).random((7, 6, 5, 6)) < 0.4
+    t = CooTensor.from_dense(DenseTensor(np.where(mask, dense.values, 0.0)))
+    cfg = solver.SolverConfig(seed=4, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0,
+                              track_factors=True)
+    res = cpadmm.fit(t, 2, None, cfg)
+    st["sp4_idx"], st["sp4_vals"] = np.asarray(t.indices), np.asarray(t.vals)
+    st["sp4_dims"] = np.array((7, 6, 5, 6))
+    st["sp4_rfe"] = np.array(res.rfe)
+    st["sp4_rho"] = np.array(_rebuild_rho4(res.residual_history, cfg))
+    for m, a in enumerate(res.model.factors):
+        st[f"sp4_aux{m}"] = np.asarray(a)
+    for m in range(4):
+        st[f"sp4_hist{m}"] = np.stack([h[m] for h in res.factor_history])
     np.savez_compressed(os.path.join(HERE, "order4.npz"), **st)
+
+
+def _rebuild_rho4(res_hist, cfg):
+    rho = [cfg.rho_init] * 4
+    out = []
+    for r in res_hist:
+        if cfg.adapt:
+            rho = solver.adapt_penalties(rho, r, cfg)
+        out.append(list(rho))
+    return out
 
 
 if __name__ == "__main__":

@@ -455,3 +455,24 @@ def test_order4_mttkrp_and_fits_match_reference(dtype):
                     assert rel(res.factor_history[it][m], g[f"{name}_hist{m}"][it]) <= 1e-9
         if f"{name}_rfe_hist" in g:
             assert np.allclose(res.rfe_history, g[f"{name}_rfe_hist"], rtol=1e-9, atol=0)
+
+
+def test_sparse_order4_mttkrp_bitwise_and_fit():
+    """Order-4 COO tensors: MTTKRP bit for bit (np.add.at order, three
+    companion rows highest mode first), fit within 1e-9 per iteration."""
+    from conftest import load_golden
+
+    g = load_golden("order4.npz")
+    for k in range(2):
+        t = P.CooTensor(g[f"s{k}_dims"], g[f"s{k}_idx"], g[f"s{k}_vals"])
+        f = [g[f"s{k}_f{m}"] for m in range(4)]
+        for m in range(4):
+            assert np.array_equal(P.mttkrp_factors(t, f, m + 1), g[f"s{k}_mttkrp{m + 1}"])
+    t = P.CooTensor(g["sp4_dims"], g["sp4_idx"], g["sp4_vals"])
+    res = P.fit(t, 2, None, P.SolverConfig(seed=4, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0,
+                                           track_factors=True), rho_schedule=g["sp4_rho"])
+    assert abs(res.rfe - float(g["sp4_rfe"])) <= 1e-9 * float(g["sp4_rfe"])
+    for m in range(4):
+        assert rel(res.model.factors[m], g[f"sp4_aux{m}"]) <= 1e-9
+        for it in range(len(res.factor_history)):
+            assert rel(res.factor_history[it][m], g[f"sp4_hist{m}"][it]) <= 1e-9

@@ -210,3 +210,20 @@ def test_order4_mttkrp_and_fits_match_reference():
         assert res.rfe == float(g[f"{name}_rfe"])
         for m in range(4):
             assert np.array_equal(res.factors[m], g[f"{name}_aux{m}"])
+
+
+def test_sparse_order4_matches_reference():
+    from conftest import load_golden
+
+    g = load_golden("order4.npz")
+    for k in range(2):
+        t = O.OracleSparse(g[f"s{k}_dims"], g[f"s{k}_idx"], g[f"s{k}_vals"])
+        f = [g[f"s{k}_f{m}"] for m in range(4)]
+        for m in range(4):
+            assert np.array_equal(O.mttkrp(t, f, m + 1), g[f"s{k}_mttkrp{m + 1}"])
+    t = O.OracleSparse(g["sp4_dims"], g["sp4_idx"], g["sp4_vals"])
+    res = O.fit(t, 2, O.Config(seed=4, eps_abs=0.0, eps_rel=0.0, n_max=8, max_restarts=0,
+                               track_factors=True))
+    assert res.rfe == float(g["sp4_rfe"])
+    for m in range(4):
+        assert np.array_equal(res.factors[m], g[f"sp4_aux{m}"])
