@@ -42,7 +42,6 @@
 //                 TMEM lane quarter, by N): per unit tcgen05.ld, F_hi scaling,
 //                 double-float accumulation; finally the fp64 partial of the CTA.
 #include <cuda_fp16.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -139,15 +138,6 @@ __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
 }
 
 // one lane of a converged warp (the warp's loop stays warp-uniform, so
@@ -934,19 +924,6 @@ unsigned long long* tc_debug_times() {
   void* ptr = nullptr;
   cudaGetSymbolAddress(&ptr, g_tc_times);
   return static_cast<unsigned long long*>(ptr);
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
 }
 
 int sm_count_tc() {
