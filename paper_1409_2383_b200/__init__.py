@@ -23,6 +23,7 @@ from .solver import (
     iterate,
     mttkrp_factors,
 )
+from . import tensor_io  # noqa: F401
 from .tensors import CooTensor, DenseTensor, KruskalModel
 
 __version__ = "0.1.0"

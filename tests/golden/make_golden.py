@@ -306,7 +306,24 @@ def _rebuild_rho4(res_hist, cfg):
     return out
 
 
+def io_fixtures():
+    """Files written by the reference's own writers (tensor_io.py:27-93)."""
+    from cpadmm import tensor_io
+
+    rng = np.random.default_rng(3)
+    t = tensors.DenseTensor(rng.random((3, 4, 5)))
+    tensor_io.write_binary(t, os.path.join(HERE, "small.cpdt"))
+    vals = rng.normal(size=(3, 2, 4, 2)) * (rng.random((3, 2, 4, 2)) < 0.4)
+    c = tensors.CooTensor.from_dense(tensors.DenseTensor(vals))
+    tensor_io.write_coo(c, os.path.join(HERE, "small4.coo"))
+    np.savez_compressed(os.path.join(HERE, "io.npz"), dense=t.values, coo_idx=c.indices,
+                        coo_vals=c.vals, coo_dims=np.array(c.dims))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["io"]:
+        io_fixtures()
+        sys.exit(0)
     if sys.argv[1:] == ["order4"]:
         order4_fits()
         sys.exit(0)
@@ -322,6 +339,7 @@ if __name__ == "__main__":
     constraint_fits()
     sparse_fits()
     order4_fits()
+    io_fixtures()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
