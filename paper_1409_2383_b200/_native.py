@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libntf_b200.so")
+LIB_PATH = os.environ.get("NTF_B200_LIB") or os.path.join(HERE, "libntf_b200.so")  # env: dev variants
 
 ABI_VERSION = 2  # include/ntf_b200.h NTF_ABI_VERSION
 

@@ -15,8 +15,11 @@ constexpr int kUpdThreads = 256;
 // small GEMMs against the ridge inverse; few rows per block spread a mode over
 // many SMs, so the latency-bound MTTKRP split reduction runs wide.  R > 64:
 // one row per warp (substitution against the Cholesky factor).
+#ifndef NTF_RPB32
+#define NTF_RPB32 2
+#endif
 __host__ __device__ __forceinline__ int rows_per_block(int R) {
-  return R <= 32 ? 4 : (R <= 64 ? 2 : 8);
+  return R <= 32 ? NTF_RPB32 : (R <= 64 ? 2 : 8);
 }
 
 // One block: H = G_a o G_b + rho I, Cholesky, then L (row-major R x R, lower)
@@ -775,16 +778,6 @@ __global__ void sum_pairs_kernel(const double* __restrict__ part, int64_t n,
   }
 }
 
-int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 
 // ---------------------------------------------------------------------------
