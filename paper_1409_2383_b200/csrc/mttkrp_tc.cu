@@ -38,7 +38,7 @@
 //                 bound by per-instruction issue latency for small-N MMAs);
 //                 each owns its accumulator sets, both release X slots
 //   warp 2        W slices of each group + F_hi pair rows (bulk copies)
-//   warps 4..     epilogue, 4, 8 or 16 warps (1, 2 or 4 column groups per
+//   warps 4..     epilogue, 8 or 16 warps (2 or 4 column groups per
 //                 TMEM lane quarter, by N): per unit tcgen05.ld, F_hi scaling,
 //                 double-float accumulation; finally the fp64 partial of the CTA.
 #include <cuda_fp16.h>
@@ -58,13 +58,17 @@ constexpr int kTM = 128;     // MMA M (rows per tile, TMEM lanes)
 constexpr int kBK = 64;      // l per block (fp16: 128 B rows, one SW128 atom)
 constexpr int kUK = 16;      // MMA K for kind::f16
 constexpr int kFMin = -990;  // exponent clamp of the column scales (2^(7+22-kFMin) finite)
-// epilogue warps: 1, 2 or 4 per TMEM lane quarter (column groups), keeping
+// epilogue warps: 2 or 4 per TMEM lane quarter (column groups), keeping
 // the double-float accumulators (2 x N / groups per thread) in registers
-// (the per-thread column count N*4/warps must be a multiple of 8)
+// (the per-thread column count N*4/warps must be a multiple of 8).  N <= 32
+// runs 8 warps too: the last unit's drain is on the kernel's critical tail
+// (c2: 599 vs 594 it/s with 4 warps)
+#ifndef NTF_EPI_SMALL
+#define NTF_EPI_SMALL 8
+#endif
 __host__ __device__ constexpr int epi_warps(int NT) {
-  return NT <= 2 ? 4 : ((NT == 6 || NT == 8) ? 16 : 8);
+  return NT <= 2 ? NTF_EPI_SMALL : ((NT == 6 || NT == 8) ? 16 : 8);
 }
-// warps: 0 X TMA, 1 MMA, 2 F_hi rows, epilogue (which also forms W)
 // warps: 0 X producer, 1 and 3 MMA issuers (alternate units; warp 3 idle
 // when only one accumulator set fits), 2 W slices + F_hi rows, 4.. epilogue
 // (warp & 3 = its TMEM lane quarter)
@@ -459,6 +463,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   long long wt[3] = {0, 0, 0};
   const long long t_start = prof ? clock64() : 0;
   uint64_t t_role = 0;  // NTF_TC_DEBUG & 256: end of this role's loop
+  uint32_t x_kb = 0;     // ... and the bytes this CTA streamed (KiB)
 
   // Roles 0-2: warp-uniform loops (descriptors and barrier addresses stay in
   // uniform registers); one elected lane issues.
@@ -488,6 +493,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // can fall a full ring behind and every parity wait stays unambiguous.
     Ring xr;
     UnitIt ui = u0;
+    const int64_t off0 = off;
     for (int u = u_begin; u < u_end; ++u) {
       const int nl = lbs_of(ui.g);
       for (int j = 0; j < nl; ++j) {
@@ -509,6 +515,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       ui.next(n_o);
     }
     t_role = gtimer();
+    x_kb = static_cast<uint32_t>((off - off0) >> 10);
   } else if (warp == 1 || warp == 3) {
     // ------------------------------ MMA issuers --------------------------------
    if (warp == 1 || kIssuers == 2) {  // warp 3 idles when one accumulator set fits
@@ -710,10 +717,27 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       hr.next(SH);
     }
     t_role = gtimer();
-    // fp64 partial of this CTA: out = (hi + lo) * xs * 2^(f-t) * 2^e
-    const int64_t gm = m0 + row;
-    if (row < p.tm && gm < p.M) {
-      double* out = p.ws + (static_cast<int64_t>(split) * p.M + gm) * R;
+    // fp64 partial of this CTA: out = (hi + lo) * xs * 2^(f-t) * 2^e.  The
+    // tile's rows are one contiguous range of the partial buffer: staged
+    // row-major in the (now idle) X ring, then written with coalesced stores
+    // (a thread's own row is R doubles apart from its neighbours').
+    const int rows_valid = static_cast<int>(p.M - m0 < p.tm ? p.M - m0 : p.tm);
+    double* out0 = p.ws + (static_cast<int64_t>(split) * p.M + m0) * R;
+    if (p.tm * R * 8 <= SX * 2 * kXTile) {
+      double* stage = reinterpret_cast<double*>(xbase);
+      if (row < rows_valid) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const int n = c0 + j;
+          if (n < R)
+            stage[row * R + n] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * wsc[2 * N + n];
+        }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
+      const int total = rows_valid * R;
+      for (int i = threadIdx.x - kFirstEpi * 32; i < total; i += kEpi * 32) out0[i] = stage[i];
+    } else if (row < rows_valid) {
+      double* out = out0 + static_cast<int64_t>(row) * R;
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
         const int n = c0 + j;
@@ -733,7 +757,10 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     if (warp == 0) {
       ts[0] = g_entry;
       ts[1] = g_ready;
-      ts[7] = static_cast<unsigned long long>(u_end - u_begin);
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+      ts[7] = static_cast<unsigned long long>(u_end - u_begin) | (static_cast<unsigned long long>(smid) << 16) |
+              (static_cast<unsigned long long>(x_kb) << 32);
     }
   }
   tc_fence_before();
