@@ -119,6 +119,33 @@ def test_mttkrp_mode_consistency_c2_full_size(engine, tol):
     assert rel(v[1], v[0]) <= tol and rel(v[2], v[0]) <= tol
 
 
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_mttkrp_mode_consistency_large_configs(name):
+    """The same property at the other BASELINE configs' full sizes (c3 1000^3
+    R=50, c4 5000x500x200 R=32, c5 2000^3 R=100: 4, 2 and 32 GB fp32
+    tensors), i.e. the tcgen05 engine's N = 64, 32 and 112 instances with
+    many m-tiles, on a device-resident tensor."""
+    w = synth.CONFIGS[name]
+    need = 4 * int(np.prod(w.dims)) * 2 + (1 << 30)  # tensor + one mode's block image
+    free, _ = torch.cuda.mem_get_info()
+    if free < need:  # pragma: no cover
+        pytest.skip(f"{name} needs {need >> 30} GiB")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(w.dims, dtype=torch.float32, device="cuda", generator=g)
+    rng = np.random.default_rng(4)
+    f = _factors(rng, w.dims, w.rank)
+    t = P.DenseTensor(x)
+    v = []
+    for m in (1, 2, 3):
+        got = P.mttkrp_factors(t, f, m)
+        got = got.cpu().numpy() if hasattr(got, "cpu") else np.asarray(got)
+        v.append(np.sum(got * f[m - 1], axis=0))
+        torch.cuda.empty_cache()
+    assert rel(v[1], v[0]) <= 5e-9 and rel(v[2], v[0]) <= 5e-9, (rel(v[1], v[0]), rel(v[2], v[0]))
+    del x, t
+    torch.cuda.empty_cache()
+
+
 def test_norm_and_rfe_kernel():
     rng = np.random.default_rng(2)
     dims = (13, 9, 21)
