@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   constexpr int kEpi = epi_warps(NT);
   constexpr int NC = N * 4 / kEpi;         // columns per epilogue thread
   // TMEM load width: 16 columns where it divides NC and registers allow
-  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : (NC > 48 ? 4 : 8);
+  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : ((NC > 48 || NC % 8) ? 4 : 8);
   static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kIssuers = mma_issuers(N);
