@@ -57,4 +57,15 @@ for mode in (1, 2, 3):
     print(f"   xend spread {np.percentile(r[:,3],50)/1e3:.1f}/{r[:,3].max()/1e3:.1f} us; "
           f"corr(kib, xend) {np.corrcoef(r[:,1], r[:,3])[0,1]:.2f}", flush=True)
 os.makedirs("gpurun_out", exist_ok=True)
-np.save(f"gpurun_out/tc_smid_{cfg}.npy", np.array(out, dtype=object), allow_pickle=True)
+nsm = torch.cuda.get_device_properties(0).multi_processor_count
+acc = {}
+for rows in out:
+    for r in rows:
+        for sm, kb, rd, xe in r:
+            acc.setdefault(int(sm), []).append(kb * 1024 / max(xe - rd, 1))
+med = float(np.median([np.mean(v) for v in acc.values()]))
+with open(f"gpurun_out/smw_{cfg}.txt", "w") as fh:
+    for s_ in range(nsm):
+        fh.write(f"{(np.mean(acc[s_]) if s_ in acc else med) / med:.4f}\n")
+print(f"wrote gpurun_out/smw_{cfg}.txt ({len(acc)} SMs measured of {nsm})")
+np.save(f"gpurun_out/tc_smid_{cfg}.npy", np.array([np.asarray(o, dtype=np.int64) for o in out] + [None], dtype=object)[:-1], allow_pickle=True)
