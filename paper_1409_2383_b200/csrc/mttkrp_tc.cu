@@ -787,61 +787,70 @@ __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, i
                                const double* __restrict__ cm_hi, float2* __restrict__ hpair,
                                const int* stop_flag) {
   pdl_trigger();
-  pdl_wait();  // F_lo and its column maxima come from the preceding row update
-  if (stop_flag && *stop_flag) return;
-  // F_hi pair table: hpair[o][n] = F_hi[o, n] * 2^-e(n) as an fp32 (hi, lo)
-  // pair, max|F_hi[:, n]| < 2^e(n) (clamped like the MTTKRP's output scale)
-  {
-    const int64_t total_h = static_cast<int64_t>(n_o) * N;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total_h;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-      const int n = static_cast<int>(e % N);
-      const int64_t o = e / N;
+  pdl_wait();  // F_lo, F_hi and their column maxima come from the preceding row updates
+  // (no stop-flag read here: it would add a dependent round trip to every
+  // mode update, and slicing after a stop is harmless — the MTTKRP checks it)
+  (void)stop_flag;
+  // Work item e: the F_hi pair entry e (hpair[o][n] = F_hi[o, n] * 2^-e(n) as
+  // an fp32 (hi, lo) pair, max|F_hi[:, n]| < 2^e(n)) and the 8-value W slice
+  // chunk e of F_lo.  Every global load of a thread is issued before any
+  // result is used, so the kernel costs one L2 round trip after the wait.
+  const int64_t total_h = static_cast<int64_t>(n_o) * N;
+  const int total_w = n_lb * N * (kBK / 8);
+  const int64_t total = total_h > total_w ? total_h : total_w;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool do_h = e < total_h, do_w = e < total_w;
+    const int n = static_cast<int>(e % N);  // column of both items
+    const int64_t o = e / N;
+    const int oc = static_cast<int>(o);
+    const int lb = oc / (kBK / 8), oct = oc % (kBK / 8);
+    const bool vh = do_h && n < R, vw = do_w && n < R;
+    const double cmh = vh ? cm_hi[n] : 0.0;
+    const double fh = vh ? Fhi[o * R + n] : 0.0;
+    const double cml = vw ? cm[n] : 0.0;
+    double x[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int l = lb * kBK + oct * 8 + v;
+      x[v] = (vw && l < l_ext) ? F[static_cast<int64_t>(l) * R + n] : 0.0;
+    }
+    if (do_h) {
       double h = 0.0;
-      if (n < R) {
+      if (vh) {
         int ex = 0;
-        if (cm_hi[n] > 0.0) frexp(cm_hi[n], &ex);
-        h = Fhi[o * R + n] * ldexp(1.0, -max(ex, kFMin));
+        if (cmh > 0.0) frexp(cmh, &ex);
+        h = fh * ldexp(1.0, -max(ex, kFMin));
       }
       const float hx = static_cast<float>(h);
       hpair[e] = make_float2(hx, static_cast<float>(h - static_cast<double>(hx)));
     }
-  }
-  const int total = n_lb * N * (kBK / 8);
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int n = e % N;
-    const int oc = e / N;
-    const int lb = oc / (kBK / 8), oct = oc % (kBK / 8);
-    double sc = 0.0;
-    if (n < R) {
-      int f = 0;
-      if (cm[n] > 0.0) frexp(cm[n], &f);
-      sc = ldexp(1.0, t + 22 - max(f, kFMin));  // v in 2^-22 units of the T0 scale
-    }
-    double x[8];
+    if (do_w) {
+      double sc = 0.0;
+      if (vw) {
+        int f = 0;
+        if (cml > 0.0) frexp(cml, &f);
+        sc = ldexp(1.0, t + 22 - max(f, kFMin));  // v in 2^-22 units of the T0 scale
+      }
+      __align__(16) __half h0[8], h1[8], h2[8];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {  // all loads first (independent, in flight together)
-      const int l = lb * kBK + oct * 8 + v;
-      x[v] = (n < R && l < l_ext) ? F[static_cast<int64_t>(l) * R + n] : 0.0;
+      for (int v = 0; v < 8; ++v) {
+        // one rounding to the 2^-22 quantum, then exact integer digit split
+        const long long q = __double2ll_rn(x[v] * sc);      // |q| <= 2^(t+22)
+        const long long b0 = (q + (1ll << 21)) >> 22;        // |b0| <= 2^t
+        const long long r = q - (b0 << 22);                  // [-2^21, 2^21)
+        const long long b1 = (r + (1ll << 10)) >> 11;        // [-1024, 1024]
+        const long long b2 = r - (b1 << 11);                 // [-1024, 1024)
+        h0[v] = __float2half_rn(static_cast<float>(b0));
+        h1[v] = __float2half_rn(static_cast<float>(b1) * 4.8828125e-04f);         // 2^-11 units
+        h2[v] = __float2half_rn(static_cast<float>(b2) * 2.384185791015625e-07f);  // 2^-22 units
+      }
+      unsigned char* wb = wsl + static_cast<int64_t>(lb) * 3 * N * 128;
+      const int off = n * 128 + ((oct ^ (n & 7)) << 4);
+      *reinterpret_cast<uint4*>(wb + off) = *reinterpret_cast<const uint4*>(h0);
+      *reinterpret_cast<uint4*>(wb + N * 128 + off) = *reinterpret_cast<const uint4*>(h1);
+      *reinterpret_cast<uint4*>(wb + 2 * N * 128 + off) = *reinterpret_cast<const uint4*>(h2);
     }
-    __align__(16) __half h0[8], h1[8], h2[8];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      // one rounding to the 2^-22 quantum, then exact integer digit split
-      const long long q = __double2ll_rn(x[v] * sc);      // |q| <= 2^(t+22)
-      const long long b0 = (q + (1ll << 21)) >> 22;        // |b0| <= 2^t
-      const long long r = q - (b0 << 22);                  // [-2^21, 2^21)
-      const long long b1 = (r + (1ll << 10)) >> 11;        // [-1024, 1024]
-      const long long b2 = r - (b1 << 11);                 // [-1024, 1024)
-      h0[v] = __float2half_rn(static_cast<float>(b0));
-      h1[v] = __float2half_rn(static_cast<float>(b1) * 4.8828125e-04f);         // 2^-11 units
-      h2[v] = __float2half_rn(static_cast<float>(b2) * 2.384185791015625e-07f);  // 2^-22 units
-    }
-    unsigned char* wb = wsl + static_cast<int64_t>(lb) * 3 * N * 128;
-    const int off = n * 128 + ((oct ^ (n & 7)) << 4);
-    *reinterpret_cast<uint4*>(wb + off) = *reinterpret_cast<const uint4*>(h0);
-    *reinterpret_cast<uint4*>(wb + N * 128 + off) = *reinterpret_cast<const uint4*>(h1);
-    *reinterpret_cast<uint4*>(wb + 2 * N * 128 + off) = *reinterpret_cast<const uint4*>(h2);
   }
 }
 

@@ -297,11 +297,16 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
     load_ridge();
   }
   pdl_wait();
+  // The early stop-flag read above can precede the kernel that sets the flag
+  // (eager launches overlap through PDL); re-read it here, in flight with the
+  // partials, and skip every write if the fit has stopped.
+  const int stopped = p.stop_flag ? *reinterpret_cast<const volatile int*>(p.stop_flag) : 0;
   if (p.ridge_in_pred) {
     if (*p.status == kDevNotPD) return;
     load_ridge();
   }
   split_sum(p, base, cnt, npm, ms, scr);
+  if (stopped) return;
   if (rowstoch) {  // g1 = (G + rho I)^-1 1 (solver.py:190), refined like the rows
     for (int c = threadIdx.x; c < R; c += blockDim.x) {
       double acc = 0.0;
@@ -434,7 +439,8 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   const double rho = p.rho[p.mode - 1];
   constexpr bool rowstoch = KIND == kConstraintRowStochastic;
   pdl_wait();  // MTTKRP partials and ridge factor
-  if (*p.status == kDevNotPD) return;
+  const int stopped = p.stop_flag ? *reinterpret_cast<const volatile int*>(p.stop_flag) : 0;
+  if (*p.status == kDevNotPD || stopped) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
     L[i * ldl + k] = p.Lg[e];
