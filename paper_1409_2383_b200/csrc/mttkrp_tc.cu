@@ -312,6 +312,7 @@ struct TcParams {
   int n_full, splits, splits_tail;
   int tm;                    // rows per m-tile (<= 128; MMA M is 128, rows >= tm ignored)
   int x_stages, h_stages;
+  int stage_bytes;           // X ring slot stride (>= one full block, multiple of 1 KB)
   const float2* hpair;       // [n_o][N] F_hi[o, n] * 2^-e(n) as fp32 (hi, lo) pairs (w_slice_kernel)
   const unsigned char* wsl;  // [n_lb][3][N][128 B] W slices of F_lo (w_slice_kernel)
   const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kIssuers = mma_issuers(N);
-  constexpr int kXTile = kTM * kBK * 2;    // 16 KB per plane
+  const int kXStage = p.stage_bytes;       // one X block (both planes of r8_full rows), 1 KB aligned
   constexpr int kWlb = 3 * N * kBK * 2;    // T0|T1|T2 of one l block
   constexpr int kFirstEpi = 4;
   const uint64_t g_entry = gtimer();
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   const int SX = p.x_stages, SH = p.h_stages, G = p.G;
   const int R = p.R;
   unsigned char* xbase = base;
-  unsigned char* wbase = xbase + SX * 2 * kXTile;
+  unsigned char* wbase = xbase + SX * kXStage;
   float2* hbase = reinterpret_cast<float2*>(wbase + G * kWlb);  // [SH][N]
   uint64_t* x_full = reinterpret_cast<uint64_t*>(hbase + SH * N);
   uint64_t* x_empty = x_full + SX;
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
             mbar_arrive(bar);
           } else {
             mbar_arrive_expect_tx(bar, bytes);
-            bulk_load(xbase + xr.idx * 2 * kXTile, p.img + off, bytes, bar);
+            bulk_load(xbase + xr.idx * kXStage, p.img + off, bytes, bar);
           }
         }
         __syncwarp();
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
         mbar_wait_p(&x_full[slot], xr.phase, wm, wt[0]);
         tc_fence_after();
         const int chunks = (ui.g * G + j == n_lb - 1) ? ct : 8;
-        const uint64_t da0 = da_base + static_cast<uint64_t>((slot * 2 * kXTile) >> 4);
+        const uint64_t da0 = da_base + static_cast<uint64_t>((slot * kXStage) >> 4);
         const uint64_t da1 = da0 + static_cast<uint64_t>((static_cast<uint32_t>(chunks) * lbo) >> 4);
         const uint64_t db = db_base + static_cast<uint64_t>((j * kWlb) >> 4);
         if (elect_one()) {
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // (a thread's own row is R doubles apart from its neighbours').
     const int rows_valid = static_cast<int>(p.M - m0 < p.tm ? p.M - m0 : p.tm);
     double* out0 = p.ws + (static_cast<int64_t>(split) * p.M + m0) * R;
-    if (p.tm * R * 8 <= SX * 2 * kXTile) {
+    if (p.tm * R * 8 <= SX * kXStage) {
       double* stage = reinterpret_cast<double*>(xbase);
       if (row < rows_valid) {
 #pragma unroll
@@ -972,7 +973,19 @@ int sm_count_tc() {
 template <int NT>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
   auto kern = mttkrp_tc_kernel<NT>;
-  if (prep) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
+  // the opt-in limit, not this plan's size: plans of different modes share the
+  // instance and the last attribute set would otherwise win
+  if (prep) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    const int cap = optin - static_cast<int>(fa.sharedSizeBytes);
+    if (L.smem_bytes > cap) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+  }
   const int extra = p.ridge.out ? 1 : 0;
   return launch_pdl(kern, dim3(L.n_full * L.splits + L.splits_tail + extra), dim3(L.threads),
                     L.smem_bytes, stream, p);
@@ -1065,15 +1078,25 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.n_o = static_cast<int>(mode == 1 ? J : I);
   L.n_lb = (L.l_ext + kBK - 1) / kBK;
   L.threads = tc_threads(L.N / 16);
-  // Shared memory: X ring (32 KB per l block) + resident W slices of a group
-  // (G blocks x 3N x 128 B) + F_hi pair ring; then as deep an X ring as fits.
-  const int xs = 2 * kTM * kBK * 2;
+  // Equal m-tiles of tm <= 128 rows (a multiple of 8, the core-matrix
+  // height), so every CTA of a full tile streams the same bytes; the last
+  // tile may be shorter.
+  {
+    const int64_t nt = (L.M + kTM - 1) / kTM;
+    L.tm = static_cast<int>(8 * ((L.M + 8 * nt - 1) / (8 * nt)));
+  }
+  // Shared memory: X ring (one block of tm rows per slot: 26 KB at tm = 104,
+  // 32 KB at 128) + resident W slices of a group (G blocks x 3N x 128 B) +
+  // F_hi pair ring; then as deep an X ring as fits (the stream is
+  // latency-bound per SM: c2 548 / 596 / 609 it/s at 3 / 4 / 5 slots).
+  const int xs = ((2 * L.tm * kBK * 2 + 1023) / 1024) * 1024;
+  L.stage_bytes = xs;
   L.h_stages = 8;
   auto total = [&](int G, int SX) {
     return 1024 + SX * xs + G * 3 * L.N * kBK * 2 + L.h_stages * L.N * 8 +
            (2 * SX + 2 * L.h_stages + 12) * 8 + 16 + 3 * L.N * 8;
   };
-  const int limit = 227 * 1024;
+  const int limit = 226 * 1024;  // the opt-in 227 KB less the kernel's 1 KB of static shared memory
   // Largest G (fewest drains) with a 3-deep X ring (2-deep for N >= 96,
   // whose epilogue, not the stream, is the bound); measured: c3 G=4/3
   // stages 668 us vs G=2/4 stages 757 us, 1000^3 R=100 G=3/2 stages 1016 vs 1083.
@@ -1087,7 +1110,7 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
     }
   if (const char* e = getenv("NTF_TC_G")) L.G = atoi(e);
   L.G = std::max(1, std::min(L.G, L.n_lb));
-  L.x_stages = 6;
+  L.x_stages = 8;
   if (const char* e = getenv("NTF_TC_XSTAGES")) L.x_stages = atoi(e);
   while (total(L.G, L.x_stages) > limit && L.x_stages > 2) --L.x_stages;
   L.smem_bytes = std::max<int>(total(L.G, L.x_stages),
@@ -1101,13 +1124,6 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   // costs a fixed pipeline share plus its rows' share of the bytes.  One SM
   // is left free so the mode's ridge Cholesky (side stream) runs concurrently.
   const int cap = std::min(sm_count_tc() - 1, kTcMaxSplits);
-  // Equal m-tiles of tm <= 128 rows (a multiple of 8, the core-matrix
-  // height), so every CTA of a full tile streams the same bytes; the last
-  // tile may be shorter.
-  {
-    const int64_t nt = (L.M + kTM - 1) / kTM;
-    L.tm = static_cast<int>(8 * ((L.M + 8 * nt - 1) / (8 * nt)));
-  }
   L.n_full = static_cast<int>(L.M / L.tm);
   const int tail = static_cast<int>(L.M % L.tm);
   L.r8_full = L.tm;
@@ -1267,6 +1283,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   p.splits_tail = L.splits_tail;
   p.tm = L.tm;
   p.x_stages = L.x_stages;
+  p.stage_bytes = L.stage_bytes;
   p.h_stages = L.h_stages;
   p.hpair = L.hpair;
   p.wsl = L.wsl;

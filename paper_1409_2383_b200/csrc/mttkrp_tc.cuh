@@ -46,6 +46,7 @@ struct MttkrpTCLaunch {
   int G, n_g;               // l blocks per unit (one TMEM drain), groups
   int threads, smem_bytes;
   int x_stages, h_stages;
+  int stage_bytes;          // X ring slot stride: one block of tm rows, 1 KB aligned
   int tmem_cols;
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
   uint32_t ub_tail[kTcMaxSplits + 1];

@@ -277,6 +277,20 @@ def test_fp32_final_rfe_parity():
     assert d <= 1e-4
 
 
+def test_fp32_fit_modes_with_different_kernel_geometry():
+    """A plan whose three tcgen05 MTTKRPs need different shared-memory sizes
+    (m-tiles of 128, 104 and 112 rows; l extents of 1, 2 and 5 blocks share
+    one kernel instance): the fit runs and matches the oracle's final RFE."""
+    rng = np.random.default_rng(8)
+    dims, R = (512, 400, 300), 20
+    x = (O.reconstruct([rng.random((d, R)) for d in dims])
+         + 0.1 * rng.standard_normal(dims)).astype(np.float32)
+    cfg = P.SolverConfig(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=3, max_restarts=0, inner_sweeps=2)
+    got = P.fit(P.DenseTensor(x), R, None, cfg)
+    want = O.fit(x.astype(np.float64), R, O.Config(**vars(cfg)))
+    assert abs(got.rfe - want.rfe) <= 1e-4 * want.rfe, (got.rfe, want.rfe)
+
+
 def test_iterate_matches_oracle(golden_small):
     g = golden_small
     x = g["sweeps3_x"]
