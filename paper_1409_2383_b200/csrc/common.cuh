@@ -124,6 +124,23 @@ __device__ __forceinline__ void pdl_trigger() {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// Allow a kernel the device's whole opt-in dynamic shared memory (less its
+// static shared memory) and check `need` fits.  The attribute is a per-kernel
+// cap, not a reservation: setting it to the maximum once means plans of
+// different sizes that share a kernel instance never undercut each other
+// (setting it to each plan's own size let the last plan created win).
+inline cudaError_t allow_dyn_smem(const void* kern, size_t need) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  const int cap = optin - static_cast<int>(fa.sharedSizeBytes);
+  if (need > static_cast<size_t>(cap)) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, Args&&... args) {

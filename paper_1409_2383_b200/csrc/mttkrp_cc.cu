@@ -393,8 +393,7 @@ cudaError_t launch_variant(const MttkrpCCParams& p, const MttkrpCCLaunch& L, cud
                            int op) {
   auto kern = mttkrp_cc_kernel<XT, TM, TR, KIND_M, VEC>;
   if (op != kLaunch) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
+    cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(kern), L.smem_bytes);
     if (e != cudaSuccess || op == kPrepare) return e;
     cudaLaunchConfig_t q{};
     q.gridDim = dim3(1, L.cluster, 1);

@@ -973,19 +973,7 @@ int sm_count_tc() {
 template <int NT>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
   auto kern = mttkrp_tc_kernel<NT>;
-  // the opt-in limit, not this plan's size: plans of different modes share the
-  // instance and the last attribute set would otherwise win
-  if (prep) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa{};
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    const int cap = optin - static_cast<int>(fa.sharedSizeBytes);
-    if (L.smem_bytes > cap) return cudaErrorInvalidValue;
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-  }
+  if (prep) return allow_dyn_smem(reinterpret_cast<const void*>(kern), L.smem_bytes);
   const int extra = p.ridge.out ? 1 : 0;
   return launch_pdl(kern, dim3(L.n_full * L.splits + L.splits_tail + extra), dim3(L.threads),
                     L.smem_bytes, stream, p);

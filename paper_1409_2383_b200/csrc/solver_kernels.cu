@@ -963,10 +963,8 @@ cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream) {
 }
 
 cudaError_t factor_update_prepare(int R) {
-  const int smem = static_cast<int>(factor_update_smem(R));
-  cudaError_t e = cudaFuncSetAttribute(ridge_factor_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(ridge_factor_smem(R)));
+  const size_t smem = factor_update_smem(R);
+  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(ridge_factor_kernel), ridge_factor_smem(R));
   if (e != cudaSuccess) return e;
   const void* kerns[] = {
       reinterpret_cast<const void*>(factor_update_gemv_kernel<kConstraintNonneg>),
@@ -976,7 +974,7 @@ cudaError_t factor_update_prepare(int R) {
       reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintNonneg>),
       reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintRowStochastic>)};
   for (const void* k : kerns) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = allow_dyn_smem(k, smem);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1045,9 +1043,7 @@ cudaError_t gram_launch(const double* F, int64_t rows, int R, double* G, double*
                         cudaStream_t stream) {
   const int64_t nb = (rows + kGramRows - 1) / kGramRows;
   const size_t smem = static_cast<size_t>(kGramRows) * R * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(gram_partial_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(gram_partial_kernel), smem);
   if (e != cudaSuccess) return e;
   gram_partial_kernel<<<static_cast<unsigned>(nb), 256, smem, stream>>>(F, rows, R, ws);
   e = cudaGetLastError();

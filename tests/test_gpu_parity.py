@@ -291,6 +291,46 @@ def test_fp32_fit_modes_with_different_kernel_geometry():
     assert abs(got.rfe - want.rfe) <= 1e-4 * want.rfe, (got.rfe, want.rfe)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_interleaved_plans_with_different_ranks(dtype):
+    """Two live plans whose kernels need different shared memory (R = 3 and
+    R = 100 share the row-update, ridge and MTTKRP kernel instances): running
+    them interleaved gives bitwise the results each gives alone."""
+    from paper_1409_2383_b200.engine import DeviceProblem
+
+    rng = np.random.default_rng(12)
+    dims = (40, 30, 24)
+    x = torch.from_numpy(rng.random(dims).astype(dtype)).cuda()
+    cfg = P.SolverConfig(seed=4, eps_abs=0.0, eps_rel=0.0, n_max=4, max_restarts=0, inner_sweeps=2)
+
+    def make(R):
+        prob = DeviceProblem(x, dims, R, cfg, history_capacity=4)
+        st = P.init_state(dims, R, cfg)
+        prob.load_state(st.factors, st.aux, st.duals, st.rho)
+        return prob
+
+    def state(prob):
+        torch.cuda.synchronize()
+        return [np.array(f, copy=True) for f in prob.read_state()[0]]
+
+    alone = {}
+    for R in (3, 100):
+        prob = make(R)
+        prob.run(2)
+        alone[R] = state(prob)
+        prob.close()
+    b = make(100)
+    a = make(3)  # prepared last, with the smaller shared-memory needs
+    b.run(1)
+    a.run(1)
+    b.run(1)
+    a.run(1)
+    for R, prob in ((3, a), (100, b)):
+        for got, want in zip(state(prob), alone[R]):
+            assert np.array_equal(got, want), R
+        prob.close()
+
+
 def test_iterate_matches_oracle(golden_small):
     g = golden_small
     x = g["sweeps3_x"]
