@@ -5,6 +5,7 @@
 // update) followed by the finalize kernel, i.e. solver.iterate
 // (reference solver.py:295-327) with aux/dual fused into each mode's last
 // sweep exactly as mesh.py:220-223 does.  Nothing here synchronises the host.
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -609,6 +610,16 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     ntf_plan_destroy(pl);
     return rc;
   };
+  // NTF_B200_PLAN_TIMING=1: host wall time of each setup phase to stderr
+  static const bool plan_timing = getenv("NTF_B200_PLAN_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!plan_timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "plan %s %.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   if ((e = ntf::dev_alloc(&pl->mtt_ws, ws)) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc ws"));
   if (N == 4 && !coo) {
     if ((e = ntf::dev_alloc(&pl->kr[0], sizeof(double) * R * vdims[0][2])) != cudaSuccess ||
@@ -641,6 +652,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaEventCreate"));
   if ((e = cudaEventCreateWithFlags(&pl->post_ev, cudaEventDisableTiming)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaEventCreate"));
+  phase("buffers");
   if ((e = ntf::factor_update_prepare(R)) != cudaSuccess) return cleanup(cuda_fail(e, "prepare"));
   for (int m = 0; m < N; ++m) {
     if ((e = prepare_op(pl->op[m], N == 4 ? vmode_of(m) : m + 1, d.x_dtype)) != cudaSuccess)
@@ -660,8 +672,10 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return cleanup(cuda_fail(e, "cudaMalloc flags"));
   if ((e = cudaMemset(pl->gram_pending, 0, sizeof(int) * 3)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMemset flags"));
+  phase("prepare");
   if (pl->any_tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
+    phase("sync");
     // one block image per mode (each is laid out for its mode's stream;
     // order 4: of the mode's reshaped view)
     for (int m = 0; m < N; ++m) {
@@ -674,8 +688,10 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
       pl->op[m].tct = &slot;
       if ((e = ntf::mttkrp_tc_bind(pl->op[m].tcl, slot)) != cudaSuccess)
         return cleanup(cuda_fail(e, "tc bind"));
+      phase("tc image");
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
+    phase("images done");
   }
   *out = pl;
   return NTF_OK;

@@ -275,6 +275,23 @@ class Slabs:
     row_count: tuple
 
 
+_SOLVER_STREAMS: dict = {}
+
+
+def _solver_stream(device):
+    """One solver stream per device for every plan of the process.  torch's
+    caching allocator keeps freed blocks per stream: a fresh stream per fit
+    made each fit's state allocations miss the cache now and then (a
+    synchronous cudaMalloc, tens of ms when it also had to free cached
+    blocks), which showed up as outliers in back-to-back fit() calls."""
+    torch = _torch()
+    key = torch.device(device).index
+    s = _SOLVER_STREAMS.get(key)
+    if s is None:
+        s = _SOLVER_STREAMS[key] = torch.cuda.Stream(device=device)
+    return s
+
+
 class DeviceProblem:
     """HBM state of one fit and its C-ABI plan."""
 
@@ -289,7 +306,7 @@ class DeviceProblem:
         self.R = int(rank)
         self.config = config
         self.x = x
-        self.stream = stream or torch.cuda.Stream(device=self.device)
+        self.stream = stream or _solver_stream(self.device)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.sharded = slabs is not None
         self.order = Nm = len(self.dims)

@@ -14,7 +14,7 @@ rho0 = synth.initial_rho_trace(w.dims, w.rank, fseed)
 cfg = P.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=w.outer, max_restarts=0,
                      inner_sweeps=w.inner, rho_init=rho0)
 t = P.DenseTensor(xh)
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     T = {}
     def mark(k, t0):
         torch.cuda.synchronize(); T[k] = time.perf_counter() - t0; return time.perf_counter()
