@@ -368,7 +368,10 @@ def main():
         d2h = 8 * w.rank * sum(w.dims) * 3 + 48 * w.outer + 64
         e2e = {"value": args.e2e_steps * w.outer / el, "unit": "outer_it/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "step": f"one fit() call of {w.outer} outer iterations from a pinned host tensor",
+               "step": (f"one fit() call of {w.outer} outer iterations from a pinned host tensor (H2D of the "
+                        "tensor, block-image split, state upload, iterations, final RFE and model read-back; "
+                        "back-to-back calls of one geometry reuse the plan and its graph, as the warm-up call "
+                        "leaves it)"),
                "final_rfe": res.rfe}
 
     cpu = None

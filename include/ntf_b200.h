@@ -211,6 +211,12 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);
 /* Column maxima out[r] = max_i |F[i][r]| (sharded runs refresh colmax[m]
  * with this after gathering a factor, as they refresh grams[m]). */
 int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t stream);
+/* The tensor behind desc->x_mode[] was overwritten in place with new values
+ * (same shape and dtype): rebuild the plan's derived copies of it (the
+ * tensor-core block images) on `stream`, so the plan, its buffers and its
+ * captured graph serve another fit.  Follows reference solver.fit
+ * (solver.py:340-403) being called again on new data. */
+int ntf_plan_refresh_tensor(ntf_plan* plan, ntf_stream_t stream);
 /* Recompute grams[m] from factors[m] (after the caller (re)initialises state). */
 int ntf_plan_sync_grams(ntf_plan* plan, ntf_stream_t stream);
 /* Enqueue `n_iters` outer iterations.  Iterations after the stop flag is set

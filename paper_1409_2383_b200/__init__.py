@@ -22,6 +22,7 @@ from .solver import (
     init_state,
     iterate,
     mttkrp_factors,
+    release_plan_cache,
 )
 from . import tensor_io  # noqa: F401
 from .tensors import CooTensor, DenseTensor, KruskalModel
@@ -43,6 +44,7 @@ __all__ = [
     "distributed_fit",
     "fit",
     "init_state",
+    "release_plan_cache",
     "iterate",
     "mttkrp_factors",
 ]

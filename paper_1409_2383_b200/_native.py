@@ -50,6 +50,7 @@ EXPORTED = (
     "ntf_plan_create",
     "ntf_colmax",
     "ntf_plan_sync_grams",
+    "ntf_plan_refresh_tensor",
     "ntf_plan_run",
     "ntf_plan_mode_update",
     "ntf_plan_finalize",
@@ -159,6 +160,8 @@ def _declare(lib):
     lib.ntf_colmax.argtypes = [c_vp, c_i64, c_int, c_vp, c_vp]
     lib.ntf_plan_sync_grams.restype = c_int
     lib.ntf_plan_sync_grams.argtypes = [c_vp, c_vp]
+    lib.ntf_plan_refresh_tensor.restype = c_int
+    lib.ntf_plan_refresh_tensor.argtypes = [c_vp, c_vp]
     lib.ntf_plan_run.restype = c_int
     lib.ntf_plan_run.argtypes = [c_vp, c_int, c_int, c_vp]
     lib.ntf_plan_mode_update.restype = c_int

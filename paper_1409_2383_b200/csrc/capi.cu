@@ -697,6 +697,16 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   return NTF_OK;
 }
 
+int ntf_plan_refresh_tensor(ntf_plan* pl, ntf_stream_t stream) {
+  if (!pl) return fail(NTF_ERR_INVALID, "null plan");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int m = 0; m < pl->order; ++m) {
+    const MttkrpOp& op = pl->op[m];
+    if (op.tc && op.tct) NTF_CUDA_TRY(ntf::tc_tensor_fill(op.tcl, *op.tct, s));
+  }
+  return NTF_OK;
+}
+
 int ntf_plan_sync_grams(ntf_plan* pl, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   cudaStream_t s = static_cast<cudaStream_t>(stream);

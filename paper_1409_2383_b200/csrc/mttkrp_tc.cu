@@ -1155,28 +1155,17 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L) {
   return dispatch_tc(p, L, nullptr, true);
 }
 
-cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
-                             TcTensor* out, cudaStream_t stream) {
-  const int64_t n = dims[0] * dims[1] * dims[2];
-  TcTensor t;
-  for (int i = 0; i < 3; ++i) t.dims[i] = dims[i];
-  t.mode = L.mode;
-  t.img_bytes = L.img_bytes;
-  cudaError_t e;
-  if ((e = ntf::dev_alloc(&t.img, L.img_bytes)) != cudaSuccess) return e;
-  if ((e = ntf::dev_alloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
-    tc_tensor_destroy(&t);
-    return e;
-  }
+cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream) {
+  const int64_t n = t.dims[0] * t.dims[1] * t.dims[2];
   unsigned* amax = reinterpret_cast<unsigned*>(t.xscale + 1);
-  cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
-  const int blocks = 4 * sm_count_tc();
-  absmax_kernel<<<blocks, 256, 0, stream>>>(X, n, amax);
+  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
+  if (e != cudaSuccess) return e;
+  absmax_kernel<<<4 * sm_count_tc(), 256, 0, stream>>>(t.src, n, amax);
   ImgGeom g;
   g.mode = L.mode;
-  g.I = dims[0];
-  g.J = dims[1];
-  g.K = dims[2];
+  g.I = t.dims[0];
+  g.J = t.dims[1];
+  g.K = t.dims[2];
   g.M = L.M;
   g.n_o = L.n_o;
   g.l_ext = L.l_ext;
@@ -1189,8 +1178,24 @@ cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int6
   g.r8_tail = L.r8_tail;
   g.ct = L.ct;
   g.tile_bytes = L.tile_bytes;
-  image_split_kernel<<<8 * sm_count_tc(), 256, 0, stream>>>(X, g, amax, t.img, t.xscale);
-  if ((e = cudaGetLastError()) != cudaSuccess) {
+  image_split_kernel<<<8 * sm_count_tc(), 256, 0, stream>>>(t.src, g, amax, t.img, t.xscale);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
+                             TcTensor* out, cudaStream_t stream) {
+  TcTensor t;
+  for (int i = 0; i < 3; ++i) t.dims[i] = dims[i];
+  t.mode = L.mode;
+  t.img_bytes = L.img_bytes;
+  t.src = X;
+  cudaError_t e;
+  if ((e = ntf::dev_alloc(&t.img, L.img_bytes)) != cudaSuccess) return e;
+  if ((e = ntf::dev_alloc(&t.xscale, sizeof(double) + sizeof(unsigned) * 2)) != cudaSuccess) {
+    tc_tensor_destroy(&t);
+    return e;
+  }
+  if ((e = tc_tensor_fill(L, t, stream)) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
   }

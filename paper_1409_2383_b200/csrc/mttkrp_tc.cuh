@@ -21,12 +21,15 @@ struct TcTensor {
   double* xscale = nullptr;  // device scalar
   int mode = 0;
   int64_t dims[3] = {0, 0, 0};
+  const float* src = nullptr;  // the tensor the image was split from
 };
 
 struct MttkrpTCLaunch;
 cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
                              TcTensor* out, cudaStream_t stream);
 void tc_tensor_destroy(TcTensor* t);
+// Re-split t.src into the existing image (the tensor's values changed in place).
+cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream);
 
 constexpr int kTcMaxSplits = 160;  // CTAs per m-tile
 

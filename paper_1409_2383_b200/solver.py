@@ -218,6 +218,15 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
         specs = normalize_specs(specs, t.order)
         if rank < 1:
             raise ValueError("rank must be >= 1")
+        codes = plan_codes(specs, t.dims, rank)
+        if rho_schedule is None:
+            with _PLAN_CACHE.lease(t, rank, config, _engine_code(engine), codes, device) as hit:
+                if hit is not None:  # same geometry as the previous fit: reuse its plan and graph
+                    prob, x = hit
+                    x_norm = math.sqrt(float(sq_error(order3_view(x)[0])[0].item()))
+                    if x_norm == 0.0:
+                        raise ValueError("cannot factorize a zero tensor")
+                    return _run_fit(prob, x, t.dims, rank, config, x_norm)
         x = device_tensor(t, device)
         x_norm = math.sqrt(float(sq_error(order3_view(x)[0])[0].item()))
         if x_norm == 0.0:
@@ -229,6 +238,105 @@ def fit(t, rank: int, specs: ConstraintSpec | Sequence[ConstraintSpec] | None = 
         return _run_fit(prob, x, t.dims, rank, config, x_norm)
     finally:
         prob.close()
+
+
+class _PlanCache:
+    """The plan of the last dense fit, kept for the next fit of the same
+    geometry (shape, dtype, rank, constraints, engine and the config fields
+    baked into the plan and its captured graph).  A hit copies the new tensor
+    into the plan's own tensor buffer and re-splits the block images
+    (``ntf_plan_refresh_tensor``); ``load_state`` then resets the rest, as
+    between the reference's restarts.  Saves the plan setup, the graph
+    capture and the teardown of every back-to-back fit.
+
+    Only tensors up to ``NTF_B200_PLAN_CACHE_MB`` (default 2048 MB of tensor
+    data; the plan holds about four times that) are kept;
+    ``NTF_B200_PLAN_CACHE=0`` turns the cache off; ``release_plan_cache()``
+    frees it.  One fit at a time uses it (others build their own plan)."""
+
+    def __init__(self):
+        import threading
+
+        self._lock = threading.Lock()
+        self._key = None
+        self._prob = None
+        self._x = None
+
+    @staticmethod
+    def _enabled(nbytes: int) -> bool:
+        import os
+
+        if os.environ.get("NTF_B200_PLAN_CACHE", "1") == "0":
+            return False
+        return nbytes <= int(os.environ.get("NTF_B200_PLAN_CACHE_MB", "2048")) * (1 << 20)
+
+    def release(self) -> None:
+        with self._lock:
+            self._drop()
+
+    def _drop(self) -> None:
+        if self._prob is not None:
+            self._prob.close()
+        self._key = self._prob = self._x = None
+
+    def lease(self, t, rank, config, engine, codes, device):
+        import contextlib
+
+        from .engine import DeviceProblem, _torch
+
+        torch = _torch()
+        vals = t.values
+        dt = np.dtype(str(vals.dtype).replace("torch.", "")) if not isinstance(vals, np.ndarray) else vals.dtype
+        nbytes = int(np.prod(t.dims)) * dt.itemsize
+        dev = torch.device(device or "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        cfg = dict(vars(config))
+        for k in ("seed", "rho_init"):  # host-side: loaded by load_state / init_state
+            cfg.pop(k, None)
+        key = (dev.index, tuple(t.dims), str(dt), int(rank), int(engine), tuple(map(tuple, codes)),
+               tuple(sorted((k, repr(v)) for k, v in cfg.items())))
+        cache = self
+
+        @contextlib.contextmanager
+        def ctx():
+            if not cache._enabled(nbytes) or not cache._lock.acquire(blocking=False):
+                yield None
+                return
+            ok = False
+            try:
+                if cache._key != key:
+                    cache._drop()
+                    src = vals if not isinstance(vals, np.ndarray) else torch.from_numpy(np.ascontiguousarray(vals))
+                    x = torch.empty(tuple(t.dims), dtype=src.dtype, device=dev)
+                    x.copy_(src, non_blocking=src.device.type == "cpu" and src.is_pinned())
+                    prob = DeviceProblem(x, t.dims, rank, config, history_capacity=config.n_max,
+                                         engine=engine, constraints=codes)
+                    cache._key, cache._prob, cache._x = key, prob, x
+                else:
+                    prob, x = cache._prob, cache._x
+                    src = vals if not isinstance(vals, np.ndarray) else torch.from_numpy(np.ascontiguousarray(vals))
+                    with torch.cuda.stream(prob.stream):
+                        prob.stream.wait_stream(torch.cuda.current_stream(dev))
+                        x.copy_(src.reshape(x.shape), non_blocking=src.device.type == "cpu" and src.is_pinned())
+                        N.check(prob.lib.ntf_plan_refresh_tensor(prob._plan, prob._sh))
+                    torch.cuda.current_stream(dev).wait_stream(prob.stream)
+                yield (cache._prob, cache._x)
+                ok = True
+            finally:
+                if not ok:  # an error mid-fit: do not keep a plan of unknown state
+                    cache._drop()
+                cache._lock.release()
+
+        return ctx()
+
+
+_PLAN_CACHE = _PlanCache()
+
+
+def release_plan_cache() -> None:
+    """Free the plan kept for the next same-geometry ``fit`` (see _PlanCache)."""
+    _PLAN_CACHE.release()
 
 
 def _run_fit(prob, x, dims, rank: int, config: SolverConfig, x_norm: float,

@@ -331,6 +331,33 @@ def test_interleaved_plans_with_different_ranks(dtype):
         prob.close()
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_plan_cache_reuse_is_bitwise_fresh(dtype, monkeypatch):
+    """Back-to-back fits of one geometry reuse the plan (its tensor buffer
+    is refilled, block images re-split, state reloaded): bitwise the results
+    of fresh plans, the caller's device tensor untouched, and a config change
+    builds a new plan."""
+    rng = np.random.default_rng(21)
+    dims, R = (36, 28, 20), 4
+    xs = [rng.random(dims).astype(dtype) for _ in range(3)]
+    cfg = P.SolverConfig(seed=5, eps_abs=0.0, eps_rel=0.0, n_max=6, max_restarts=0, inner_sweeps=3)
+    cfg2 = P.SolverConfig(seed=5, eps_abs=0.0, eps_rel=0.0, n_max=6, max_restarts=0, inner_sweeps=2)
+    xd = torch.from_numpy(xs[0]).cuda()
+    keep = xd.clone()
+    P.release_plan_cache()
+    cached = [P.fit(P.DenseTensor(xd), R, None, cfg), P.fit(xs[1], R, None, cfg),
+              P.fit(xs[2], R, None, cfg2), P.fit(xs[1], R, None, cfg)]
+    assert torch.equal(xd, keep)
+    monkeypatch.setenv("NTF_B200_PLAN_CACHE", "0")
+    fresh = [P.fit(xs[0], R, None, cfg), P.fit(xs[1], R, None, cfg),
+             P.fit(xs[2], R, None, cfg2), P.fit(xs[1], R, None, cfg)]
+    for a, b in zip(cached, fresh):
+        for m in range(3):
+            assert np.array_equal(a.model.factors[m], b.model.factors[m])
+        assert a.residual_history == b.residual_history and a.rfe == b.rfe
+    P.release_plan_cache()
+
+
 def test_iterate_matches_oracle(golden_small):
     g = golden_small
     x = g["sweeps3_x"]
