@@ -1137,6 +1137,10 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
       L.splits_tail = clampu(std::min<int64_t>(static_cast<int64_t>(L.splits * wt + 0.5),
                                                cap - static_cast<int64_t>(L.n_full) * L.splits));
   }
+  if (const char* e = getenv("NTF_TC_SPLITS")) {  // tuning: CTAs per full tile, the rest to the tail
+    L.splits = std::max(1, std::min(atoi(e), static_cast<int>(cap / std::max(1, L.n_full))));
+    if (tail) L.splits_tail = clampu(cap - static_cast<int64_t>(L.n_full) * L.splits);
+  }
   if (L.splits) partition_units(L, L.splits, L.ub_full);
   if (L.splits_tail) partition_units(L, L.splits_tail, L.ub_tail);
   L.wscale = nullptr;
