@@ -15,11 +15,18 @@ constexpr int kUpdThreads = 256;
 // small GEMMs against the ridge inverse; few rows per block spread a mode over
 // many SMs, so the latency-bound MTTKRP split reduction runs wide.  R > 64:
 // one row per warp (substitution against the Cholesky factor).
-#ifndef NTF_RPB32
-#define NTF_RPB32 2
+#ifndef NTF_RPB_ROWS
+#define NTF_RPB_ROWS 1024
 #endif
-__host__ __device__ __forceinline__ int rows_per_block(int R) {
-  return R <= 32 ? NTF_RPB32 : (R <= 64 ? 2 : 8);
+#ifndef NTF_RPB_R2MAX
+#define NTF_RPB_R2MAX 32
+#endif
+__host__ __device__ __forceinline__ int rows_per_block(int R, int64_t rows) {
+  // R <= 32: two rows per block for short factors (c2's 400 rows: 200
+  // blocks, 605 vs 592 it/s with four), four for long ones, which bounds the
+  // Gram partials (one R x R block per CTA, reduced on the side stream) of
+  // factors like c4's 5000 rows (c4 within noise, 92-93 it/s, either way)
+  return R <= 32 ? ((rows > NTF_RPB_ROWS || R > NTF_RPB_R2MAX) ? 4 : 2) : (R <= 64 ? 2 : 8);
 }
 
 // One block: H = G_a o G_b + rho I, Cholesky, then L (row-major R x R, lower)
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
-  const int rpb = rows_per_block(R);
+  const int rpb = rows_per_block(R, p.rows);
   const int npm = rpb * R;
   double* Hi = reinterpret_cast<double*>(smem_raw);  // [R][R] H^-1
   double* Hm = Hi + R * R;                            // [R][R] H
@@ -423,7 +430,7 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
   const int ldl = R + 1;  // odd pitch: conflict-free row and column walks
-  const int rpb = rows_per_block(R);
+  const int rpb = rows_per_block(R, p.rows);
   const int npm = rpb * R;
   double* L = reinterpret_cast<double*>(smem_raw);
   double* inv_diag = L + R * ldl;  // [R]
@@ -882,7 +889,7 @@ __global__ void __launch_bounds__(kUpdThreads) card_apply_kernel(FactorUpdatePar
   if (p.stop_flag && *p.stop_flag) return;
   __shared__ double red[kUpdThreads / 32 * 10];
   const int R = p.R;
-  const int npm = rows_per_block(R) * R;
+  const int npm = rows_per_block(R, p.rows) * R;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * npm;
   const int64_t nM = p.rows * R;
   const int cnt = static_cast<int>(nM - base < npm ? nM - base : npm);
@@ -938,12 +945,12 @@ __global__ void kr_merge_kernel(KrMergeParams p) {
 // host-side launchers
 // ---------------------------------------------------------------------------
 int factor_update_blocks(int64_t rows, int R) {
-  const int rpb = rows_per_block(R);
+  const int rpb = rows_per_block(R, rows);
   return static_cast<int>((rows + rpb - 1) / rpb);
 }
 
 size_t factor_update_smem(int R) {
-  const size_t npm = static_cast<size_t>(rows_per_block(R)) * R;
+  const size_t npm = static_cast<size_t>(rows_per_block(R, INT64_MAX)) * R;  // the largest block
   size_t n;
   if (R <= 64)
     n = 2 * static_cast<size_t>(R) * R + 6 * npm + kUpdThreads + R + 8;
