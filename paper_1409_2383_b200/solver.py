@@ -11,6 +11,7 @@ reads the counters and copies the histories back.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import atexit
 import math
 from dataclasses import dataclass, field
 from typing import Sequence
@@ -307,7 +308,7 @@ class _PlanCache:
             try:
                 if cache._key != key:
                     cache._drop()
-                    src = vals if not isinstance(vals, np.ndarray) else torch.from_numpy(np.ascontiguousarray(vals))
+                    src = _as_torch(torch, vals)
                     x = torch.empty(tuple(t.dims), dtype=src.dtype, device=dev)
                     x.copy_(src, non_blocking=src.device.type == "cpu" and src.is_pinned())
                     prob = DeviceProblem(x, t.dims, rank, config, history_capacity=config.n_max,
@@ -315,7 +316,7 @@ class _PlanCache:
                     cache._key, cache._prob, cache._x = key, prob, x
                 else:
                     prob, x = cache._prob, cache._x
-                    src = vals if not isinstance(vals, np.ndarray) else torch.from_numpy(np.ascontiguousarray(vals))
+                    src = _as_torch(torch, vals)
                     with torch.cuda.stream(prob.stream):
                         prob.stream.wait_stream(torch.cuda.current_stream(dev))
                         x.copy_(src.reshape(x.shape), non_blocking=src.device.type == "cpu" and src.is_pinned())
@@ -331,7 +332,28 @@ class _PlanCache:
         return ctx()
 
 
+def _as_torch(torch, vals):
+    """Host numpy values as a torch view (read only: we only copy from it)."""
+    if not isinstance(vals, np.ndarray):
+        return vals
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(np.ascontiguousarray(vals))
+
+
 _PLAN_CACHE = _PlanCache()
+
+
+def _release_at_exit() -> None:  # free the plan while CUDA and torch are still up
+    try:
+        _PLAN_CACHE.release()
+    except Exception:  # pragma: no cover - best effort at interpreter exit
+        pass
+
+
+atexit.register(_release_at_exit)
 
 
 def release_plan_cache() -> None:
