@@ -239,6 +239,39 @@ int ntf_plan_set_timing(ntf_plan* plan, int enable);
 int ntf_plan_kernel_times(ntf_plan* plan, float* ms_out, int capacity);
 void ntf_plan_destroy(ntf_plan* plan);
 
+/* ---- Row all-gather over NVLink peer memory (sharded engine) -------------
+ * Replaces the broadcast of updated row blocks after every block-row mode
+ * update (reference blocks.py:171-196, mesh.py:149-237; the centralized
+ * equivalent is the factor assignment in solver.iterate, solver.py:305-310).
+ * Every rank allocates one peer buffer per factor (ntf_peer_alloc), exchanges
+ * the 64-byte IPC handles out of band and maps the peers' buffers
+ * (ntf_peer_open).  ntf_peer_gather then pushes the caller's owned rows of
+ * `full` into every peer's buffer with P2P stores, waits (at most timeout_ns,
+ * then writes NTF_PEER_TIMEOUT to *status) for every rank's rows to arrive in
+ * its own buffer and copies them into `full`.  One kernel, graph-capturable;
+ * every rank must issue the same sequence of gathers per buffer with the
+ * same `ctas`. */
+#define NTF_MAX_PEERS 8
+#define NTF_PEER_TIMEOUT 6
+typedef struct ntf_peer_gather_desc {
+  int nranks;                            /* 1..NTF_MAX_PEERS                   */
+  int me;                                /* caller's rank                      */
+  int R;
+  int ctas;                              /* CTAs per rank, same on all ranks   */
+  int64_t row_offset[NTF_MAX_PEERS + 1]; /* rank q owns rows [off[q], off[q+1]) */
+  double* full;                          /* local factor, off[nranks] x R fp64 */
+  void* peer_base[NTF_MAX_PEERS];        /* rank q's peer buffer, mapped here  */
+  int* status;                           /* device int, may be NULL            */
+  int64_t timeout_ns;
+} ntf_peer_gather_desc;
+size_t ntf_peer_buffer_bytes(int64_t rows, int R);
+/* cudaMalloc'd, zeroed; handle_out receives 64 bytes (cudaIpcMemHandle_t). */
+int ntf_peer_alloc(size_t bytes, void** base_out, void* handle_out);
+int ntf_peer_open(const void* handle, void** base_out);
+int ntf_peer_close(void* base);
+int ntf_peer_free(void* base);
+int ntf_peer_gather(const ntf_peer_gather_desc* desc, ntf_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

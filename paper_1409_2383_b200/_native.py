@@ -57,7 +57,16 @@ EXPORTED = (
     "ntf_plan_set_timing",
     "ntf_plan_kernel_times",
     "ntf_plan_destroy",
+    "ntf_peer_buffer_bytes",
+    "ntf_peer_alloc",
+    "ntf_peer_open",
+    "ntf_peer_close",
+    "ntf_peer_free",
+    "ntf_peer_gather",
 )
+
+NTF_MAX_PEERS = 8
+NTF_PEER_TIMEOUT = 6
 
 
 class NativeUnavailable(RuntimeError):
@@ -123,6 +132,22 @@ class PlanDesc(ctypes.Structure):
     ]
 
 
+class PeerGatherDesc(ctypes.Structure):
+    """Mirror of ``ntf_peer_gather_desc`` (include/ntf_b200.h)."""
+
+    _fields_ = [
+        ("nranks", c_int),
+        ("me", c_int),
+        ("R", c_int),
+        ("ctas", c_int),
+        ("row_offset", c_i64 * (NTF_MAX_PEERS + 1)),
+        ("full", c_vp),
+        ("peer_base", c_vp * NTF_MAX_PEERS),
+        ("status", c_vp),
+        ("timeout_ns", c_i64),
+    ]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -174,6 +199,18 @@ def _declare(lib):
     lib.ntf_plan_kernel_times.argtypes = [c_vp, ctypes.POINTER(ctypes.c_float), c_int]
     lib.ntf_plan_destroy.restype = None
     lib.ntf_plan_destroy.argtypes = [c_vp]
+    lib.ntf_peer_buffer_bytes.restype = ctypes.c_size_t
+    lib.ntf_peer_buffer_bytes.argtypes = [c_i64, c_int]
+    lib.ntf_peer_alloc.restype = c_int
+    lib.ntf_peer_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(c_vp), c_vp]
+    lib.ntf_peer_open.restype = c_int
+    lib.ntf_peer_open.argtypes = [c_vp, ctypes.POINTER(c_vp)]
+    lib.ntf_peer_close.restype = c_int
+    lib.ntf_peer_close.argtypes = [c_vp]
+    lib.ntf_peer_free.restype = c_int
+    lib.ntf_peer_free.argtypes = [c_vp]
+    lib.ntf_peer_gather.restype = c_int
+    lib.ntf_peer_gather.argtypes = [ctypes.POINTER(PeerGatherDesc), c_vp]
     return lib
 
 

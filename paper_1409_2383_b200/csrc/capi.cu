@@ -14,6 +14,7 @@
 #include "mttkrp_cc.cuh"
 #include "mttkrp_coo.cuh"
 #include "mttkrp_tc.cuh"
+#include "peer_gather.cuh"
 #include "solver_kernels.cuh"
 
 namespace {
@@ -727,6 +728,75 @@ int ntf_khatri_rao_pair(const double* Fa, int64_t na, const double* Fb, int64_t 
   ntf::KrMergeParams kp{};
   kp.Fa = Fa, kp.na = na, kp.Fb = Fb, kp.nb = nb, kp.R = R, kp.out = out;
   NTF_CUDA_TRY(ntf::kr_merge_launch(kp, static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
+size_t ntf_peer_buffer_bytes(int64_t rows, int R) {
+  if (rows < 1 || R < 1) return 0;
+  return ntf::kPeerHeaderBytes + 2 * static_cast<size_t>(rows) * R * sizeof(double);
+}
+
+int ntf_peer_alloc(size_t bytes, void** base_out, void* handle_out) {
+  if (!base_out || !handle_out) return fail(NTF_ERR_INVALID, "null pointer");
+  if (bytes < ntf::kPeerHeaderBytes) return fail(NTF_ERR_INVALID, "peer buffer too small");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  void* p = nullptr;
+  NTF_CUDA_TRY(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any peer can map it
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "ntf_peer_alloc");
+  }
+  std::memcpy(handle_out, &h, sizeof(h));
+  *base_out = p;
+  return NTF_OK;
+}
+
+int ntf_peer_open(const void* handle, void** base_out) {
+  if (!handle || !base_out) return fail(NTF_ERR_INVALID, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  NTF_CUDA_TRY(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return NTF_OK;
+}
+
+int ntf_peer_close(void* base) {
+  if (!base) return NTF_OK;
+  NTF_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return NTF_OK;
+}
+
+int ntf_peer_free(void* base) {
+  if (!base) return NTF_OK;
+  NTF_CUDA_TRY(cudaFree(base));
+  return NTF_OK;
+}
+
+int ntf_peer_gather(const ntf_peer_gather_desc* d, ntf_stream_t stream) {
+  static_assert(NTF_MAX_PEERS == ntf::kPeerMaxRanks, "peer limits");
+  static_assert(NTF_PEER_TIMEOUT == ntf::kPeerGatherTimeout, "timeout status");
+  if (!d || !d->full) return fail(NTF_ERR_INVALID, "null pointer");
+  if (d->nranks < 1 || d->nranks > NTF_MAX_PEERS || d->me < 0 || d->me >= d->nranks)
+    return fail(NTF_ERR_INVALID, "bad rank geometry");
+  if (d->R < 1 || d->R > NTF_MAX_RANK) return fail(NTF_ERR_INVALID, "bad rank R");
+  if (d->ctas < 1 || d->ctas > 148) return fail(NTF_ERR_INVALID, "ctas must be in 1..148");
+  if (d->timeout_ns <= 0) return fail(NTF_ERR_INVALID, "timeout_ns must be > 0");
+  ntf::PeerGatherArgs a{};
+  a.nranks = d->nranks, a.me = d->me, a.R = d->R, a.ctas = d->ctas;
+  for (int q = 0; q <= d->nranks; ++q) {
+    a.row_offset[q] = d->row_offset[q];
+    if (q > 0 && d->row_offset[q] < d->row_offset[q - 1]) return fail(NTF_ERR_INVALID, "row offsets decrease");
+  }
+  if (d->row_offset[0] != 0 || d->row_offset[d->nranks] < 1) return fail(NTF_ERR_INVALID, "bad row offsets");
+  for (int q = 0; q < d->nranks; ++q) {
+    if (!d->peer_base[q]) return fail(NTF_ERR_INVALID, "null peer buffer");
+    a.base[q] = d->peer_base[q];
+  }
+  a.full = d->full, a.status = d->status, a.timeout_ns = d->timeout_ns;
+  NTF_CUDA_TRY(ntf::peer_gather_launch(a, static_cast<cudaStream_t>(stream)));
   return NTF_OK;
 }
 

@@ -1,0 +1,122 @@
+// Row all-gather of a factor over NVLink peer memory: one kernel per mode
+// update of the sharded engine, replacing pack -> ncclAllGather -> unpack.
+//
+// Reference semantics: after the block-row updates of mode n every node holds
+// the whole updated factor (blocks.py:171-196, mesh.py:149-237: the wave's
+// broadcast of the updated row blocks).  Here each rank pushes its owned rows
+// straight into every peer's staging buffer with P2P stores, signals one
+// arrival per CTA on every peer's counter (release at system scope), waits
+// for all ranks' arrivals on its own counter (acquire), and copies the other
+// ranks' rows from its staging buffer into its factor.
+//
+// Staging is double-buffered by the parity of the per-buffer gather sequence
+// number: a rank can only start gather t+1 after its gather t saw every
+// peer's arrival for t, which each peer signalled after finishing gather t-1,
+// so nobody overwrites a parity a peer is still reading.  The staging buffer
+// (not the peer's factor) is the target because a peer may still be reading
+// its factor (as an MTTKRP companion) when the pushes of the next update land.
+#include <cstdint>
+
+#include "peer_gather.cuh"
+
+namespace ntf {
+namespace {
+
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_sys_add(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Copy doubles [lo, hi) of src to dst with CTA c of `ctas` taking one
+// contiguous, 16-byte-aligned share (double2 body, scalar tail).
+__device__ __forceinline__ void copy_share(double* __restrict__ dst, const double* __restrict__ src,
+                                           int64_t lo, int64_t hi, int c, int ctas) {
+  const int64_t n = hi - lo;
+  if (n <= 0) return;
+  const int64_t per = ((n + ctas - 1) / ctas + 1) & ~int64_t(1);  // even share
+  const int64_t a = lo + per * c;
+  const int64_t b = min(hi, a + per);
+  if (a >= b) return;
+  int64_t i = a + threadIdx.x * 2;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst + a) | reinterpret_cast<uintptr_t>(src + a)) & 15) == 0;
+  if (aligned) {
+    for (; i + 1 < b; i += 2 * blockDim.x)
+      *reinterpret_cast<double2*>(dst + i) = *reinterpret_cast<const double2*>(src + i);
+    if (i < b) dst[i] = src[i];  // odd tail: only the thread that reaches it
+  } else {
+    for (int64_t j = a + threadIdx.x; j < b; j += blockDim.x) dst[j] = src[j];
+  }
+}
+
+__global__ void __launch_bounds__(kPeerGatherThreads)
+peer_gather_kernel(PeerGatherArgs a) {
+  __shared__ unsigned int s_seq;
+  __shared__ int s_ok;
+  const int c = blockIdx.x;
+  const int R = a.R;
+  const int64_t rows = a.row_offset[a.nranks];
+  const int64_t plane = rows * R;  // doubles per staging parity
+  if (threadIdx.x == 0) {
+    s_seq = *reinterpret_cast<volatile unsigned int*>(peer_seq(a.base[a.me]));
+    s_ok = 1;
+  }
+  __syncthreads();
+  const unsigned int seq = s_seq;
+  const int64_t par = seq & 1u;
+
+  // 1. push the owned rows into every peer's staging (same row positions)
+  const int64_t lo = a.row_offset[a.me] * R, hi = a.row_offset[a.me + 1] * R;
+  for (int q = 0; q < a.nranks; ++q) {
+    if (q == a.me) continue;
+    copy_share(peer_staging(a.base[q]) + par * plane, a.full, lo, hi, c, gridDim.x);
+  }
+  __syncthreads();
+  // 2. one arrival per CTA on every rank's counter (own included), then wait
+  //    until all ranks' CTAs have arrived for this sequence number
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < a.nranks; ++q) red_release_sys_add(peer_arrivals(a.base[q]), 1u);
+    const unsigned int target = (seq + 1u) * static_cast<unsigned int>(a.nranks) * gridDim.x;
+    const unsigned int* mine = peer_arrivals(a.base[a.me]);
+    const uint64_t t0 = now_ns();
+    while (static_cast<int>(ld_acquire_sys(mine) - target) < 0) {
+      if (now_ns() - t0 > static_cast<uint64_t>(a.timeout_ns)) {
+        s_ok = 0;
+        if (a.status) atomicExch(a.status, kPeerGatherTimeout);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  // 3. the other ranks' rows: own staging -> factor
+  const double* st = peer_staging(a.base[a.me]) + par * plane;
+  for (int q = 0; q < a.nranks; ++q) {
+    if (q == a.me) continue;
+    copy_share(a.full, st, a.row_offset[q] * R, a.row_offset[q + 1] * R, c, gridDim.x);
+  }
+  // every CTA of this launch read seq before arriving, and CTA 0 is past the
+  // wait, so all of them have read it: advance for the next launch
+  if (c == 0 && threadIdx.x == 0) *peer_seq(a.base[a.me]) = seq + 1u;
+}
+
+}  // namespace
+
+cudaError_t peer_gather_launch(const PeerGatherArgs& a, cudaStream_t stream) {
+  peer_gather_kernel<<<a.ctas, kPeerGatherThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ntf

@@ -88,12 +88,58 @@ class Comm:
         """out[q * t.numel():(q + 1) * t.numel()] = rank q's ``t``."""
         self.dist.all_gather_into_tensor(out, t, group=self.group)
 
+    def peer_ok(self, device) -> bool:
+        """Whether rows can be gathered over NVLink peer memory (one fused
+        kernel, ``_PeerRows``) instead of ncclAllGather: CUDA tensors, at most
+        NTF_MAX_PEERS ranks on one node, each on its own GPU, every pair
+        P2P-reachable, and NTF_B200_P2P not "0".  Decided once, collectively
+        (every rank takes the same path)."""
+        if getattr(self, "_peer_state", None) is not None:
+            return self._peer_state
+        if device.type != "cuda":  # CPU (gloo) runs: all ranks alike, no exchange needed
+            self._peer_state = False
+            return False
+        import os
+        import socket
+
+        import torch
+
+        from ._native import NTF_MAX_PEERS
+
+        want = os.environ.get("NTF_B200_P2P", "1") != "0" and self.size <= NTF_MAX_PEERS
+        uuid = str(torch.cuda.get_device_properties(device).uuid)
+        infos = [None] * self.size
+        self.dist.all_gather_object(infos, (socket.gethostname(), uuid, want), group=self.group)
+        ok = all(w for _, _, w in infos) and len({h for h, _, _ in infos}) == 1 \
+            and len({u for _, u, _ in infos}) == self.size
+        if ok:  # map peer uuids to local ordinals (CUDA_VISIBLE_DEVICES may differ per rank)
+            local = {str(torch.cuda.get_device_properties(d).uuid): d for d in range(torch.cuda.device_count())}
+            me = device.index if device.index is not None else torch.cuda.current_device()
+            ok = all(u in local and (u == uuid or torch.cuda.can_device_access_peer(me, local[u]))
+                     for _, u, _ in infos)
+            flags = [None] * self.size
+            self.dist.all_gather_object(flags, ok, group=self.group)
+            ok = all(flags)
+        self._peer_state = ok
+        return ok
+
     def gather_rows(self, full, offsets: Sequence[int], counts: Sequence[int]) -> None:
         """In place: every rank's owned block of ``full`` (rows offsets[p] ..
-        +counts[p]) is broadcast to all ranks.  Blocks are padded to the
-        largest count because the uniform plan is uneven.
-        The staging buffers are allocated once per target tensor, so the call
-        can be captured in a CUDA graph."""
+        +counts[p]) is broadcast to all ranks.  On one NVLink node this is one
+        kernel that pushes the rows into the peers' buffers (``_PeerRows``);
+        otherwise ncclAllGather with blocks padded to the largest count
+        because the uniform plan is uneven.  Buffers are
+        allocated once per target tensor, so the call can be captured in a
+        CUDA graph."""
+        if self.peer_ok(full.device):
+            key = (full.data_ptr(), tuple(full.shape))
+            if not hasattr(self, "_peers"):
+                self._peers = {}
+            pr = self._peers.get(key)
+            if pr is None:
+                pr = self._peers[key] = _PeerRows(self, full, offsets, counts)
+            pr.gather()
+            return
         maxc = max(counts)
         p = self.rank
         key = (full.data_ptr(), tuple(full.shape), maxc)
@@ -111,6 +157,103 @@ class Comm:
             if q == p:
                 continue
             full[offsets[q]: offsets[q] + counts[q]].copy_(recv[q * maxc: q * maxc + counts[q]])
+
+
+    def check_peers(self) -> None:
+        """Raise if a peer gather timed out waiting for another rank."""
+        for pr in getattr(self, "_peers", {}).values():
+            pr.check()
+
+    def close_peers(self) -> None:
+        """Unmap the peers' buffers, wait for every rank to do the same, free
+        our own (a buffer is freed only after no peer maps it)."""
+        peers = getattr(self, "_peers", {})
+        if not peers:
+            return
+        import torch
+
+        torch.cuda.synchronize()
+        for pr in peers.values():
+            pr.unmap()
+        self.dist.barrier(group=self.group)
+        for pr in peers.values():
+            pr.free()
+        self._peers = {}
+
+
+class _PeerRows:
+    """One factor's row all-gather over NVLink peer memory: a peer buffer
+    (counters + double-buffered staging, ``ntf_peer_alloc``) per rank, mapped
+    by every other rank through CUDA IPC, and the ``ntf_peer_gather`` kernel
+    (csrc/peer_gather.cu).  Replaces pack + ncclAllGather + unpack of the
+    updated row blocks (reference blocks.py:171-196, mesh.py:149-237)."""
+
+    def __init__(self, comm: Comm, full, offsets: Sequence[int], counts: Sequence[int]):
+        import ctypes
+        import os
+
+        import torch
+
+        from . import _native
+
+        lib = self.lib = _native.load()
+        self.check_rc = _native.check
+        rows, R = int(full.shape[0]), int(full.shape[1])
+        P, me = comm.size, comm.rank
+        for q in range(P - 1):
+            if offsets[q] + counts[q] != offsets[q + 1]:
+                raise ValueError("row blocks must be contiguous")
+        if offsets[0] != 0 or offsets[-1] + counts[-1] != rows:
+            raise ValueError("row blocks must cover the factor")
+        base = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        self.check_rc(lib.ntf_peer_alloc(lib.ntf_peer_buffer_bytes(rows, R), ctypes.byref(base), handle))
+        self.own = base.value
+        handles = [None] * P
+        comm.dist.all_gather_object(handles, bytes(handle), group=comm.group)
+        self.mapped = []
+        bases = []
+        for q in range(P):
+            if q == me:
+                bases.append(self.own)
+                continue
+            pb = ctypes.c_void_p()
+            buf = ctypes.create_string_buffer(handles[q], 64)
+            self.check_rc(lib.ntf_peer_open(buf, ctypes.byref(pb)))
+            self.mapped.append(pb.value)
+            bases.append(pb.value)
+        self.status = torch.zeros(1, dtype=torch.int32, device=full.device)
+        d = self.desc = _native.PeerGatherDesc()
+        d.nranks, d.me, d.R = P, me, R
+        # same on every rank: derived from the global geometry only
+        d.ctas = int(min(32, max(1, -(-max(counts) * R // 8192))))
+        for q in range(P):
+            d.row_offset[q] = int(offsets[q])
+            d.peer_base[q] = bases[q]
+        d.row_offset[P] = rows
+        d.full = full.data_ptr()
+        d.status = self.status.data_ptr()
+        d.timeout_ns = int(float(os.environ.get("NTF_B200_P2P_TIMEOUT_S", "60")) * 1e9)
+        self._torch = torch
+
+    def gather(self) -> None:
+        stream = self._torch.cuda.current_stream().cuda_stream
+        self.check_rc(self.lib.ntf_peer_gather(self.desc, stream))
+
+    def check(self) -> None:
+        if int(self.status.item()) != 0:
+            raise RuntimeError("peer row gather timed out waiting for another rank "
+                               "(NTF_B200_P2P_TIMEOUT_S; NTF_B200_P2P=0 selects NCCL)")
+
+    def unmap(self) -> None:
+        for pb in self.mapped:
+            self.lib.ntf_peer_close(pb)
+        self.mapped = []
+
+    def free(self) -> None:
+        if self.own:
+            self.lib.ntf_peer_free(self.own)
+            self.own = None
 
 
 def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
@@ -243,7 +386,14 @@ def make_slabs(values, plan: PartitionPlan, rank_id: int, device):
     """This rank's three slabs of a host tensor, uploaded to ``device``."""
     import torch
 
-    x = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values))
+    if isinstance(values, torch.Tensor):
+        x = values
+    else:
+        import warnings
+
+        with warnings.catch_warnings():  # read-only source: we only read it
+            warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+            x = torch.from_numpy(np.ascontiguousarray(values))
     s1 = x[plan.row_slice(1, rank_id)]
     s2 = x[:, plan.row_slice(2, rank_id)]
     s3 = x[:, :, plan.row_slice(3, rank_id)]
@@ -306,6 +456,9 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     prob = cls(slabs, t.dims, rank, config, config.n_max, _engine_code(engine), plan, comm,
                constraints=plan_codes(specs, t.dims, rank))
     try:
-        return _run_fit(prob, slabs[0], t.dims, rank, config, x_norm, gather=prob.gather_state)
+        res = _run_fit(prob, slabs[0], t.dims, rank, config, x_norm, gather=prob.gather_state)
+        comm.check_peers()
+        return res
     finally:
         prob.close()
+        comm.close_peers()
