@@ -85,7 +85,7 @@ peer_gather_kernel(PeerGatherArgs a) {
   // 2. one arrival per CTA on every rank's counter (own included), then wait
   //    until all ranks' CTAs have arrived for this sequence number
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    __threadfence_system();  // the CTA's P2P stores (ordered by bar.sync) before the arrivals
     for (int q = 0; q < a.nranks; ++q) red_release_sys_add(peer_arrivals(a.base[q]), 1u);
     const unsigned int target = (seq + 1u) * static_cast<unsigned int>(a.nranks) * gridDim.x;
     const unsigned int* mine = peer_arrivals(a.base[a.me]);

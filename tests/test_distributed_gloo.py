@@ -142,7 +142,11 @@ def _gather_worker(rank, world, port, out_path):
         full = torch.full((11, 3), -1.0, dtype=torch.float64)
         o, c = offs[rank], cnts[rank]
         full[o:o + c] = torch.arange(o * 3, (o + c) * 3, dtype=torch.float64).reshape(c, 3)
-        Comm().gather_rows(full, offs, cnts)
+        comm = Comm()
+        comm.gather_rows(full, offs, cnts)
+        # CPU tensors: the NVLink peer-memory path is never selected (every
+        # rank decides alike, without a collective)
+        assert comm.peer_ok(full.device) is False and not getattr(comm, "_peers", {})
         if rank == 0:
             np.save(out_path, full.numpy())
     finally:

@@ -125,6 +125,7 @@ def test_sharded_fit_peer_path_equals_nccl_path(golden_small, tmp_path, monkeypa
 
     dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
+    monkeypatch.setenv("NTF_B200_P2P", "force")  # one rank: gather anyway
     try:
         assert Comm().peer_ok(torch.device("cuda", 0))
         g = golden_small
@@ -135,6 +136,9 @@ def test_sharded_fit_peer_path_equals_nccl_path(golden_small, tmp_path, monkeypa
         monkeypatch.setenv("NTF_B200_P2P", "0")
         assert not Comm().peer_ok(torch.device("cuda", 0))
         nccl = P.distributed_fit(g["mesh2_x"], 3, None, P.SolverConfig(**kw), plan=1, sharded=True)
+        monkeypatch.delenv("NTF_B200_P2P")  # one rank: no exchange at all
+        none = P.distributed_fit(g["mesh2_x"], 3, None, P.SolverConfig(**kw), plan=1, sharded=True)
+        assert none.residual_history == nccl.residual_history
         for it in range(len(want.factor_history)):
             for m in range(3):
                 assert rel(p2p.factor_history[it][m], want.factor_history[it][m]) <= 1e-9
