@@ -42,14 +42,17 @@ def test_abi_version(lib):
     assert lib.ntf_abi_version() == 2
 
 
-def test_plan_desc_layout_matches_c(tmp_path):
-    from paper_1409_2383_b200._native import PlanDesc
+@pytest.mark.parametrize("struct,cname", [("PlanDesc", "ntf_plan_desc"),
+                                          ("PeerGatherDesc", "ntf_peer_gather_desc")])
+def test_desc_layout_matches_c(tmp_path, struct, cname):
+    from paper_1409_2383_b200 import _native
 
+    PlanDesc = getattr(_native, struct)
     fields = [f[0] for f in PlanDesc._fields_]
     prog = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){",
-            'printf("%zu\\n", sizeof(ntf_plan_desc));']
+            f'printf("%zu\\n", sizeof({cname}));']
     for f in fields:
-        prog.append(f'printf("%zu\\n", offsetof(ntf_plan_desc, {f}));')
+        prog.append(f'printf("%zu\\n", offsetof({cname}, {f}));')
     prog.append("return 0;}")
     c = tmp_path / "layout.c"
     c.write_text("\n".join(prog))
@@ -70,3 +73,7 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     assert rc == 1 and b"mode" in lib.ntf_last_error()
     rc = lib.ntf_gram(None, 2, 2, None, None, 0, None)
     assert rc == 1
+    assert lib.ntf_peer_buffer_bytes(0, 4) == 0
+    assert lib.ntf_peer_buffer_bytes(10, 4) == 256 + 2 * 10 * 4 * 8
+    assert lib.ntf_peer_gather(None, None) == 1
+    assert lib.ntf_peer_alloc(8, None, None) == 1
