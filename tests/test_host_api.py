@@ -105,3 +105,20 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
+
+
+def test_peer_rows_validates_blocks_before_any_cuda_call():
+    """distributed._PeerRows (NVLink row all-gather) rejects row blocks that
+    are not contiguous or do not cover the factor before allocating."""
+    import types
+
+    import torch
+
+    from paper_1409_2383_b200.distributed import _PeerRows
+
+    comm = types.SimpleNamespace(size=2, rank=0)
+    full = torch.zeros(10, 3, dtype=torch.float64)
+    with pytest.raises(ValueError, match="contiguous"):
+        _PeerRows(comm, full, [0, 6], [5, 4])
+    with pytest.raises(ValueError, match="cover"):
+        _PeerRows(comm, full, [0, 5], [5, 4])
