@@ -114,6 +114,21 @@ int ntf_sq_error_coo(int order, const int64_t* dims, int64_t nnz, const int64_t*
 int ntf_khatri_rao_pair(const double* Fa, int64_t na, const double* Fb, int64_t nb, int R, double* out,
                         ntf_stream_t stream);
 
+/* Synthetic dense tensor in HBM (stands in for the reference
+ * generator bench.py:34-46: U[0,1) true factors, X = [[A,B,C]] + Gaussian
+ * noise).  Writes the box [lo, hi) of the full dims[0] x dims[1] x dims[2]
+ * tensor, row-major, to `out` (x_dtype):
+ *   x[i,j,k] = sum_r (A[i,r] B[j,r]) C[k,r]  (sequential in r, fp64)
+ *            + sigma * z(e),  e = (i dims[1] + j) dims[2] + k,
+ * z = Box-Muller over SplitMix64 words 2e+1, 2e+2 of `key`, with ln and cos
+ * as fixed polynomials in correctly rounded arithmetic: every element is a
+ * pure function of its global index, so ranks generate their own slabs and
+ * the bytes equal the host restatement's (oracle/synth_oracle.c).  A, B, C
+ * are the full device factors (dims[m] x R fp64). */
+int ntf_synth_dense(int x_dtype, void* out, const int64_t* dims, const int64_t* lo, const int64_t* hi,
+                    const double* A, const double* B, const double* C, int R, double sigma,
+                    uint64_t key, ntf_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * Solver plan: device-resident ADMoM outer iterations for one order-3 or
  * order-4 tensor (dense order 3 sharded or not; dense order 4 and sparse
@@ -208,6 +223,11 @@ typedef struct ntf_plan_desc {
 } ntf_plan_desc;
 
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);
+/* Plans draw device memory from the device's default stream-ordered pool and
+ * keep it mapped after release (repeated fits of one geometry re-use it).
+ * This returns every unused pool byte to the device (e.g. before allocating
+ * a large tensor outside the library).  Synchronises the device. */
+int ntf_trim_device_pool(void);
 /* Column maxima out[r] = max_i |F[i][r]| (sharded runs refresh colmax[m]
  * with this after gathering a factor, as they refresh grams[m]). */
 int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t stream);
@@ -250,7 +270,11 @@ void ntf_plan_destroy(ntf_plan* plan);
  * then writes NTF_PEER_TIMEOUT to *status) for every rank's rows to arrive in
  * its own buffer and copies them into `full`.  One kernel, graph-capturable;
  * every rank must issue the same sequence of gathers per buffer with the
- * same `ctas`. */
+ * same `ctas`.  The kernel's CTAs spin-wait on the arrivals of every rank's
+ * CTAs, so `ctas` is bounded by what is co-resident on the device
+ * (occupancy x SM count; larger values are rejected).  A gather finding
+ * *status already set does nothing (no pushes, no arrivals): after a timeout
+ * the caller checks the status word and aborts the fit on every rank. */
 #define NTF_MAX_PEERS 8
 #define NTF_PEER_TIMEOUT 6
 typedef struct ntf_peer_gather_desc {
@@ -271,6 +295,12 @@ int ntf_peer_open(const void* handle, void** base_out);
 int ntf_peer_close(void* base);
 int ntf_peer_free(void* base);
 int ntf_peer_gather(const ntf_peer_gather_desc* desc, ntf_stream_t stream);
+/* Every rank's gather in ONE cooperative launch on the current device,
+ * descs[q] being rank q's (all ranks' buffers and factors on this device).
+ * Ranks that wait on one another may not be separate launches on one GPU
+ * (nothing makes them co-resident); this is how the protocol runs with all
+ * ranks live on a single GPU (tests, single-process emulation of P ranks). */
+int ntf_peer_gather_group(const ntf_peer_gather_desc* descs, int nranks, ntf_stream_t stream);
 
 #ifdef __cplusplus
 }

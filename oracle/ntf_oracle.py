@@ -486,35 +486,183 @@ def uniform_extents(d: int, n: int) -> tuple[int, ...]:
 
 
 # ---------------------------------------------------------------------------
-# synthetic generator (pattern of bench.py:34-46)
+# synthetic generator (stands in for bench.py:34-46)
 # ---------------------------------------------------------------------------
+# Counter-based: every element is a pure function of its global index, so
+# the device generator (csrc/synth.cu, ntf_synth_dense) writes any slab of it
+# and the bytes never depend on the sharding.  Restated twice here: numpy
+# (``synth_box``, small boxes, fully vectorised, explicit operation order)
+# and C (``synth_oracle.c`` via ``synth_box_c``, OpenMP, for the BASELINE
+# sizes make_golden.py and bench.py's CPU legs need).
+
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+_SQRT2 = float.fromhex("0x1.6a09e667f3bcdp+0")
+_PIO2 = float.fromhex("0x1.921fb54442d18p+0")
+_LN2_HI = float.fromhex("0x1.62e42fee00000p-1")
+_LN2_LO = float.fromhex("0x1.a39ef35793c76p-33")
+_LN_C = [1.0 / (2 * k + 1) for k in range(12)]
+_COS_C = [(-1) ** k / math.factorial(2 * k) for k in range(11)]
+_SIN_C = [(-1) ** k / math.factorial(2 * k + 1) for k in range(11)]
 
 
-def generate(dims, rank: int, snr_db: float, seed: int, zero_frac: float = 0.0,
-             dtype=np.float64, slab_rows: int | None = None):
-    """Seeded noisy low-rank tensor: U[0,1) factors in mode order (optionally
-    zeroed with probability ``zero_frac`` factor by factor), X0 = [[A,B,C]],
-    sigma^2 from the exact Gram-identity ||X0||^2 and the SNR, N(0, sigma^2)
-    noise drawn slab by slab along mode 1 (bit-identical to a one-shot draw).
-    Returns (X as ``dtype``, true factors, sigma)."""
+def _mix64(z):
+    z = (z ^ (z >> np.uint64(30))) * _M1
+    z = (z ^ (z >> np.uint64(27))) * _M2
+    return z ^ (z >> np.uint64(31))
+
+
+def synth_key(data_seed: int) -> int:
+    """Generator key: SplitMix64 output 1 of the data seed."""
+    z = np.array([int(data_seed) % (1 << 64)], dtype=np.uint64) + _GAMMA
+    return int(_mix64(z)[0])
+
+
+def synth_std_normal(key: int, e) -> np.ndarray:
+    """Box-Muller normal of element indices ``e`` (uint64 array): u1, u2 from
+    SplitMix64 words 2e+1, 2e+2; ln and cos as fixed polynomials, each
+    operation one correctly rounded numpy ufunc (no fused multiply-add)."""
+    e = np.asarray(e, dtype=np.uint64)
+    k = np.uint64(key)
+    with np.errstate(over="ignore"):
+        w1 = _mix64(k + (np.uint64(2) * e + np.uint64(1)) * _GAMMA)
+        w2 = _mix64(k + (np.uint64(2) * e + np.uint64(2)) * _GAMMA)
+    u1 = ((w1 >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+    mant, ex = np.frexp(u1)
+    big = mant * 2.0 > _SQRT2
+    m = np.where(big, mant, mant * 2.0)
+    E = np.where(big, ex, ex - 1).astype(np.float64)
+    s = (m - 1.0) / (m + 1.0)
+    s2 = s * s
+    p = np.full_like(s, _LN_C[11])
+    for c in reversed(_LN_C[:11]):
+        p = p * s2
+        p = p + c
+    lnm = (2.0 * s) * p
+    ln = E * _LN2_HI + (E * _LN2_LO + lnm)
+    rad = np.sqrt(-2.0 * ln)
+    n2 = w2 >> np.uint64(11)
+    q = (n2 >> np.uint64(51)).astype(np.int64)
+    fi = n2 & np.uint64((1 << 51) - 1)
+    sw = fi > np.uint64(1 << 50)
+    g = np.where(sw, np.uint64(1 << 51) - fi, fi).astype(np.float64) * 2.0 ** -51
+    th = g * _PIO2
+    t2 = th * th
+    cc = np.full_like(th, _COS_C[10])
+    sn = np.full_like(th, _SIN_C[10])
+    for a, b in zip(reversed(_COS_C[:10]), reversed(_SIN_C[:10])):
+        cc = cc * t2
+        cc = cc + a
+        sn = sn * t2
+        sn = sn + b
+    sn = th * sn
+    cq = np.where(sw, sn, cc)
+    sq = np.where(sw, cc, sn)
+    v = np.select([q == 0, q == 1, q == 2], [cq, -sq, -cq], sq)
+    return rad * v
+
+
+def synth_box(factors, dims, lo, hi, sigma: float, key: int, dtype=np.float64) -> np.ndarray:
+    """Box [lo, hi) of the generator's tensor (numpy restatement):
+    clean = sum_r (A[i,r] B[j,r]) C[k,r] accumulated in r order, plus sigma
+    times the element's normal; e = (i J + j) K + k over the full dims."""
+    a, b, c = factors
+    I, J, K = (int(d) for d in dims)
+    ii = np.arange(lo[0], hi[0])[:, None, None]
+    jj = np.arange(lo[1], hi[1])[None, :, None]
+    kk = np.arange(lo[2], hi[2])[None, None, :]
+    acc = np.zeros((len(ii), jj.shape[1], kk.shape[2]))
+    for r in range(a.shape[1]):
+        ab = a[lo[0]:hi[0], r][:, None, None] * b[lo[1]:hi[1], r][None, :, None]
+        acc = acc + ab * c[lo[2]:hi[2], r][None, None, :]
+    e = ((ii * J + jj) * K + kk).astype(np.uint64)
+    x = acc + sigma * synth_std_normal(key, e)
+    return x.astype(dtype)
+
+
+_SYNTH_LIB = None
+
+
+def _synth_lib():
+    """oracle/libsynth_oracle.so (built by __graft_entry__.build(), or here)."""
+    global _SYNTH_LIB
+    if _SYNTH_LIB is None:
+        import ctypes
+        import os
+        import subprocess
+
+        here = os.path.dirname(os.path.abspath(__file__))
+        so = os.path.join(here, "libsynth_oracle.so")
+        src = os.path.join(here, "synth_oracle.c")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            subprocess.run(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared",
+                            "-fPIC", src, "-o", so, "-lm"], check=True)
+        lib = ctypes.CDLL(so)
+        lib.synth_box.restype = ctypes.c_int
+        lib.synth_box.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
+                                                          ctypes.c_int, ctypes.c_void_p]
+        lib.synth_std_normal.restype = ctypes.c_double
+        lib.synth_std_normal.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        _SYNTH_LIB = lib
+    return _SYNTH_LIB
+
+
+def synth_box_c(factors, dims, lo, hi, sigma: float, key: int, dtype=np.float64, out=None) -> np.ndarray:
+    """The same box from the C restatement (OpenMP over (i, j) rows)."""
+    lib = _synth_lib()
+    f = [np.ascontiguousarray(v, dtype=np.float64) for v in factors]
+    d = np.array(dims, dtype=np.int64)
+    lo_a = np.array(lo, dtype=np.int64)
+    hi_a = np.array(hi, dtype=np.int64)
+    shape = tuple(int(h - l) for l, h in zip(lo, hi))
+    if out is None:
+        out = np.empty(shape, dtype=dtype)
+    assert out.shape == shape and out.dtype in (np.float32, np.float64) and out.flags.c_contiguous
+    rc = lib.synth_box(f[0].ctypes.data, f[1].ctypes.data, f[2].ctypes.data, d.ctypes.data,
+                       lo_a.ctypes.data, hi_a.ctypes.data, int(f[0].shape[1]), float(sigma),
+                       int(key) % (1 << 64), 1 if out.dtype == np.float32 else 0, out.ctypes.data)
+    if rc != 0:
+        raise ValueError("synth_box: rank outside 1..4096")
+    return out
+
+
+def true_factors(dims, rank: int, seed: int, zero_frac: float = 0.0):
+    """U[0,1) true factors from PCG64(SeedSequence(seed)) in mode order, then
+    (zero_frac > 0) each factor's entries zeroed where a further U[0,1) draw
+    is below zero_frac, factor by factor."""
     gen = np.random.Generator(np.random.PCG64(np.random.SeedSequence(int(seed))))
-    dims = tuple(int(d) for d in dims)
-    truth = [gen.random((d, rank)) for d in dims]
+    truth = [gen.random((int(d), rank)) for d in dims]
     if zero_frac > 0:
         for f in truth:
             f[gen.random(f.shape) < zero_frac] = 0.0
-    g = np.ones((rank, rank))
+    return truth
+
+
+def noise_sigma(truth, snr_db: float) -> float:
+    """sigma^2 = ||X0||^2 / (IJK 10^(SNR/10)), ||X0||^2 by the Gram identity
+    sum((A^T A) * (B^T B) * (C^T C)) with every sum an exactly rounded
+    math.fsum, so sigma does not depend on the host's BLAS."""
+    R = truth[0].shape[1]
+    grams = []
     for f in truth:
-        g = g * (f.T @ f)
-    x0_sq = float(g.sum())
-    sigma2 = x0_sq / (math.prod(dims) * 10.0 ** (snr_db / 10.0))
-    sigma = math.sqrt(sigma2)
-    a, b, c = truth
-    out = np.empty(dims, dtype=dtype)
-    rows = slab_rows or max(1, (1 << 22) // max(1, dims[1] * dims[2]))
-    for i0 in range(0, dims[0], rows):
-        i1 = min(dims[0], i0 + rows)
-        clean = np.einsum("if,jf,kf->ijk", a[i0:i1], b, c, optimize=True)
-        noise = gen.normal(0.0, sigma, size=(i1 - i0, dims[1], dims[2]))
-        out[i0:i1] = clean + noise
-    return out, truth, sigma
+        g = np.empty((R, R))
+        for r in range(R):
+            for s_ in range(r, R):
+                g[r, s_] = g[s_, r] = math.fsum(f[:, r] * f[:, s_])
+        grams.append(g)
+    x0_sq = math.fsum(((grams[0] * grams[1]) * grams[2]).ravel())
+    n = math.prod(int(f.shape[0]) for f in truth)
+    return math.sqrt(x0_sq / (n * 10.0 ** (snr_db / 10.0)))
+
+
+def generate(dims, rank: int, snr_db: float, seed: int, zero_frac: float = 0.0,
+             dtype=np.float64, use_c: bool = True):
+    """The whole tensor: (X as ``dtype``, true factors, sigma)."""
+    dims = tuple(int(d) for d in dims)
+    truth = true_factors(dims, rank, seed, zero_frac)
+    sigma = noise_sigma(truth, snr_db)
+    key = synth_key(seed)
+    fn = synth_box_c if use_c else synth_box
+    x = fn(truth, dims, (0, 0, 0), dims, sigma, key, dtype)
+    return x, truth, sigma

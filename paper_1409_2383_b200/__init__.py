@@ -10,7 +10,7 @@ behind the C ABI declared in ``include/ntf_b200.h``.
 """
 
 from .constraints import ConstraintSpec
-from .distributed import PartitionPlan, distributed_fit
+from .distributed import PartitionPlan, ShardedTensor, distributed_fit
 from .solver import (
     FitResult,
     InvalidPenaltyError,
@@ -42,6 +42,7 @@ __all__ = [
     "SolverState",
     "derive_seed",
     "distributed_fit",
+    "ShardedTensor",
     "fit",
     "init_state",
     "release_plan_cache",

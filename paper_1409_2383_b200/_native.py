@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("NTF_B200_LIB") or os.path.join(HERE, "libntf_b200.so")  # env: dev variants
+LIB_PATH = os.path.join(HERE, "libntf_b200.so")
 
 ABI_VERSION = 2  # include/ntf_b200.h NTF_ABI_VERSION
 
@@ -47,6 +47,8 @@ EXPORTED = (
     "ntf_sq_error_coo_workspace_bytes",
     "ntf_sq_error_coo",
     "ntf_khatri_rao_pair",
+    "ntf_synth_dense",
+    "ntf_trim_device_pool",
     "ntf_plan_create",
     "ntf_colmax",
     "ntf_plan_sync_grams",
@@ -63,6 +65,7 @@ EXPORTED = (
     "ntf_peer_close",
     "ntf_peer_free",
     "ntf_peer_gather",
+    "ntf_peer_gather_group",
 )
 
 NTF_MAX_PEERS = 8
@@ -179,6 +182,11 @@ def _declare(lib):
                                      ctypes.c_size_t, c_vp]
     lib.ntf_khatri_rao_pair.restype = c_int
     lib.ntf_khatri_rao_pair.argtypes = [c_vp, c_i64, c_vp, c_i64, c_int, c_vp, c_vp]
+    lib.ntf_synth_dense.restype = c_int
+    lib.ntf_synth_dense.argtypes = [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_dbl,
+                                    ctypes.c_uint64, c_vp]
+    lib.ntf_trim_device_pool.restype = c_int
+    lib.ntf_trim_device_pool.argtypes = []
     lib.ntf_plan_create.restype = c_int
     lib.ntf_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(c_vp)]
     lib.ntf_colmax.restype = c_int
@@ -211,6 +219,8 @@ def _declare(lib):
     lib.ntf_peer_free.argtypes = [c_vp]
     lib.ntf_peer_gather.restype = c_int
     lib.ntf_peer_gather.argtypes = [ctypes.POINTER(PeerGatherDesc), c_vp]
+    lib.ntf_peer_gather_group.restype = c_int
+    lib.ntf_peer_gather_group.argtypes = [ctypes.POINTER(PeerGatherDesc), c_int, c_vp]
     return lib
 
 

@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 REPO = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libntf_b200.so")
-SOURCES = ["capi.cu", "mttkrp_cc.cu", "mttkrp_coo.cu", "mttkrp_tc.cu", "peer_gather.cu", "solver_kernels.cu"]
-HEADERS = ["common.cuh", "mttkrp_cc.cuh", "mttkrp_coo.cuh", "mttkrp_tc.cuh", "peer_gather.cuh", "ridge.cuh", "solver_kernels.cuh"]
+SOURCES = ["capi.cu", "mttkrp_cc.cu", "mttkrp_coo.cu", "mttkrp_tc.cu", "peer_gather.cu", "solver_kernels.cu", "synth.cu"]
+HEADERS = ["common.cuh", "mttkrp_cc.cuh", "mttkrp_coo.cuh", "mttkrp_tc.cuh", "peer_gather.cuh", "ridge.cuh", "solver_kernels.cuh", "synth.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

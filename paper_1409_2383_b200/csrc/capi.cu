@@ -16,6 +16,7 @@
 #include "mttkrp_tc.cuh"
 #include "peer_gather.cuh"
 #include "solver_kernels.cuh"
+#include "synth.cuh"
 
 namespace {
 
@@ -90,13 +91,12 @@ MttkrpOp make_op(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R, 
 
 cudaError_t run_op(MttkrpOp& op, int mode, int x_dtype, const void* X, int64_t I, int64_t J,
                    int64_t K, const double* A, const double* B, const double* C, int R, double* ws,
-                   const int* stop, cudaStream_t s, const double* colmax3 = nullptr,
-                   const ntf::TcRidge* ridge = nullptr) {
+                   const int* stop, cudaStream_t s, const double* colmax3 = nullptr) {
   if (op.coo) {  // the order's factors follow A, B, C in the plan (D: op.f3)
     const double* F[4] = {A, B, C, op.f3};
     return ntf::mttkrp_coo_launch(op.cv, mode, F, R, ws, stop, s);
   }
-  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s, ridge);
+  if (op.tc) return ntf::mttkrp_tc_launch(op.tcl, *op.tct, A, B, C, colmax3, ws, stop, s);
   return ntf::mttkrp_cc_launch(mode, x_dtype, X, I, J, K, A, B, C, R, op.cc, ws, stop, s);
 }
 
@@ -127,11 +127,6 @@ struct ntf_plan {
   double* vcm[2] = {};  // [3][R] column maxima of each view's factors
   double* gram_ws = nullptr;
   bool any_tc = false;
-  // all three MTTKRPs on the tensor cores: the ridge factorisation (and the
-  // Gram reduction feeding it) runs in one extra CTA of each MTTKRP, so a
-  // mode update is a pure PDL chain on one stream
-  bool fused_ridge = false;
-  int* gram_pending = nullptr;  // [3] device flags
   cudaStream_t capture_stream = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [timing]: plain / with timing events
   // ridge factorisation runs on a side stream concurrently with the MTTKRP
@@ -176,30 +171,6 @@ int enqueue_mode_update(ntf_plan* pl, int mode, int last, cudaStream_t s) {
   int comp[3] = {-1, -1, -1};
   for (int q = N - 1, k = 0; q >= 0; --q)
     if (q != m) comp[k++] = q;
-  if (pl->fused_ridge) {
-    const int prev = (m + 2) % 3;  // the factor updated just before this mode
-    ntf::TcRidge rg{};
-    rg.f_prev = d.factors[prev];
-    rg.rows_prev = d.dims[prev];
-    rg.gram_prev = d.grams[prev];
-    rg.gram_pending = pl->gram_pending + prev;
-    rg.Ga = d.grams[comp[0]];
-    rg.Gb = d.grams[comp[1]];
-    rg.rho = d.rho + m;
-    rg.out = pl->ridge;
-    rg.status = d.counters + 2;
-    cudaEvent_t* ev = nullptr;
-    if (pl->timing && pl->events) {
-      ev = pl->events + 3 * pl->cursor;
-      pl->cursor = (pl->cursor + 1) % (pl->n_events / 3);
-      NTF_CUDA_TRY(record_event(ev[0], s));
-    }
-    NTF_CUDA_TRY(run_op(pl->op[m], mode, d.x_dtype, d.x_mode[m], xd[0], xd[1], xd[2],
-                        d.factors[0], d.factors[1], d.factors[2], R, pl->mtt_ws, d.counters + 1, s,
-                        d.colmax, &rg));
-    if (ev) NTF_CUDA_TRY(record_event(ev[1], s));
-    return enqueue_row_update(pl, mode, last, s, ev);
-  }
   // fork: ridge Cholesky (solver.py:167-175) on the side stream
   ntf::RidgeParams rp{};
   rp.mode = mode;
@@ -281,12 +252,12 @@ int enqueue_row_update(ntf_plan* pl, int mode, int last, cudaStream_t s, cudaEve
   fp.last_sweep = last;
   fp.fuse_gram = d.fuse_gram;
   fp.norm_partials = pl->norm_partials[m];
-  fp.gram_partials = pl->fused_ridge ? nullptr : pl->gram_partials[m];
+  fp.gram_partials = pl->gram_partials[m];
   // column maxima feed the tensor-core MTTKRPs only (zeroed by this mode's
   // MTTKRP, re-accumulated here)
   fp.colmax_bits = pl->any_tc ? reinterpret_cast<unsigned long long*>(d.colmax + m * R) : nullptr;
-  fp.gram_pending = pl->fused_ridge ? pl->gram_pending + m : nullptr;
-  fp.ridge_in_pred = pl->fused_ridge ? 1 : 0;
+  fp.gram_pending = nullptr;
+  fp.ridge_in_pred = 0;
   fp.status = d.counters + 2;
   fp.stop_flag = d.counters + 1;
   fp.kind = d.constraint[m];
@@ -298,7 +269,7 @@ int enqueue_row_update(ntf_plan* pl, int mode, int last, cudaStream_t s, cudaEve
     NTF_CUDA_TRY(ntf::card_apply_launch(fp, pl->card_sel[m], s));
   }
   if (ev) NTF_CUDA_TRY(record_event(ev[2], s));
-  if (d.fuse_gram && !pl->fused_ridge) {  // G_m for the coming ridges, off the critical path
+  if (d.fuse_gram) {  // G_m for the coming ridges, off the critical path
     NTF_CUDA_TRY(cudaEventRecord(pl->post_ev, s));
     NTF_CUDA_TRY(cudaStreamWaitEvent(pl->side, pl->post_ev, 0));
     NTF_CUDA_TRY(ntf::gram_reduce_launch(pl->gram_partials[m], pl->blocks[m], R, d.grams[m],
@@ -312,7 +283,6 @@ int enqueue_row_update(ntf_plan* pl, int mode, int last, cudaStream_t s, cudaEve
 
 // main stream waits for the side stream's queued work (Gram reductions)
 int join_side(ntf_plan* pl, cudaStream_t s) {
-  if (pl->fused_ridge) return NTF_OK;  // nothing runs on the side stream
   NTF_CUDA_TRY(cudaEventRecord(pl->join_ev, pl->side));
   NTF_CUDA_TRY(cudaStreamWaitEvent(s, pl->join_ev, 0));
   return NTF_OK;
@@ -342,7 +312,19 @@ int enqueue_finalize(ntf_plan* pl, cudaStream_t s) {
   return NTF_OK;
 }
 
+// An instrumented iteration (timing events around every MTTKRP / row
+// update) is enqueued without PDL: its kernels serialise, so each event pair
+// brackets exactly its own kernels and the per-kernel times cannot overlap.
+struct PdlOff {
+  bool prev;
+  explicit PdlOff(bool off) : prev(ntf::pdl_switch()) {
+    if (off) ntf::pdl_switch() = false;
+  }
+  ~PdlOff() { ntf::pdl_switch() = prev; }
+};
+
 int enqueue_iteration(ntf_plan* pl, cudaStream_t s) {
+  PdlOff no_pdl(pl->timing && pl->events);
   const int sweeps = pl->d.inner_sweeps;
   for (int sw = 0; sw < sweeps; ++sw)
     for (int mode = 1; mode <= pl->order; ++mode) {
@@ -496,6 +478,36 @@ int ntf_sq_error_coo(int order, const int64_t* dims, int64_t nnz, const int64_t*
   return NTF_OK;
 }
 
+int ntf_synth_dense(int x_dtype, void* out, const int64_t* dims, const int64_t* lo, const int64_t* hi,
+                    const double* A, const double* B, const double* C, int R, double sigma,
+                    uint64_t key, ntf_stream_t stream) {
+  if (x_dtype != NTF_F32 && x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "bad dtype");
+  if (!out || !dims || !lo || !hi || !A || !B || !C) return fail(NTF_ERR_INVALID, "null pointer");
+  if (R < 1) return fail(NTF_ERR_INVALID, "rank must be >= 1");
+  if (!(sigma >= 0.0) || sigma > 1e300) return fail(NTF_ERR_INVALID, "sigma must be finite and >= 0");
+  ntf::SynthBox b{};
+  for (int m = 0; m < 3; ++m) {
+    if (dims[m] < 1 || lo[m] < 0 || hi[m] <= lo[m] || hi[m] > dims[m])
+      return fail(NTF_ERR_INVALID, "box outside the tensor");
+    b.dims[m] = dims[m];
+    b.lo[m] = lo[m];
+    b.hi[m] = hi[m];
+  }
+  NTF_CUDA_TRY(ntf::synth_dense_launch(x_dtype, out, b, A, B, C, R, sigma, key,
+                                       static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
+int ntf_trim_device_pool(void) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  NTF_CUDA_TRY(cudaGetDevice(&dev));
+  NTF_CUDA_TRY(cudaDeviceSynchronize());
+  NTF_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  NTF_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
+  return NTF_OK;
+}
+
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if (!desc || !out) return fail(NTF_ERR_INVALID, "null pointer");
   *out = nullptr;
@@ -612,7 +624,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     return rc;
   };
   // NTF_B200_PLAN_TIMING=1: host wall time of each setup phase to stderr
-  static const bool plan_timing = getenv("NTF_B200_PLAN_TIMING") != nullptr;
+  static const bool plan_timing = ntf::diag_env("NTF_B200_PLAN_TIMING") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
   auto phase = [&](const char* what) {
     if (!plan_timing) return;
@@ -662,17 +674,6 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   // Tensor-core engine: split each distinct slab once into its fp16 planes
   // (one-time setup; synchronous so the caller's upload stream is irrelevant).
   for (int m = 0; m < N; ++m) pl->any_tc = pl->any_tc || pl->op[m].tc;
-  // Opt-in (NTF_B200_FUSED_RIDGE=1): measured slower at c2 today, where the
-  // single-CTA ridge (~30 us, serial fp64 divisions) outlasts the streaming
-  // CTAs; the side-stream ridge hides it on the 148th SM instead.
-  {
-    const char* env = getenv("NTF_B200_FUSED_RIDGE");
-    pl->fused_ridge = env && env[0] == '1' && N == 3 && pl->op[0].tc && pl->op[1].tc && pl->op[2].tc;
-  }
-  if ((e = ntf::dev_alloc(&pl->gram_pending, sizeof(int) * 3)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMalloc flags"));
-  if ((e = cudaMemset(pl->gram_pending, 0, sizeof(int) * 3)) != cudaSuccess)
-    return cleanup(cuda_fail(e, "cudaMemset flags"));
   phase("prepare");
   if (pl->any_tc) {
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cleanup(cuda_fail(e, "sync"));
@@ -711,7 +712,6 @@ int ntf_plan_refresh_tensor(ntf_plan* pl, ntf_stream_t stream) {
 int ntf_plan_sync_grams(ntf_plan* pl, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (pl->gram_pending) NTF_CUDA_TRY(cudaMemsetAsync(pl->gram_pending, 0, sizeof(int) * 3, s));
   for (int m = 0; m < pl->order; ++m) {
     NTF_CUDA_TRY(ntf::gram_launch(pl->d.factors[m], pl->d.dims[m], pl->d.rank, pl->d.grams[m],
                                   pl->gram_ws, s));
@@ -775,16 +775,19 @@ int ntf_peer_free(void* base) {
   return NTF_OK;
 }
 
-int ntf_peer_gather(const ntf_peer_gather_desc* d, ntf_stream_t stream) {
+namespace {
+int peer_args(const ntf_peer_gather_desc* d, int ranks_in_launch, ntf::PeerGatherArgs* out) {
   static_assert(NTF_MAX_PEERS == ntf::kPeerMaxRanks, "peer limits");
   static_assert(NTF_PEER_TIMEOUT == ntf::kPeerGatherTimeout, "timeout status");
   if (!d || !d->full) return fail(NTF_ERR_INVALID, "null pointer");
   if (d->nranks < 1 || d->nranks > NTF_MAX_PEERS || d->me < 0 || d->me >= d->nranks)
     return fail(NTF_ERR_INVALID, "bad rank geometry");
   if (d->R < 1 || d->R > NTF_MAX_RANK) return fail(NTF_ERR_INVALID, "bad rank R");
-  if (d->ctas < 1 || d->ctas > 148) return fail(NTF_ERR_INVALID, "ctas must be in 1..148");
+  if (d->ctas < 1 || d->ctas > ntf::peer_gather_max_ctas(ranks_in_launch))
+    return fail(NTF_ERR_INVALID, "ctas must be >= 1 and small enough for every CTA to be co-resident");
   if (d->timeout_ns <= 0) return fail(NTF_ERR_INVALID, "timeout_ns must be > 0");
-  ntf::PeerGatherArgs a{};
+  ntf::PeerGatherArgs& a = *out;
+  a = ntf::PeerGatherArgs{};
   a.nranks = d->nranks, a.me = d->me, a.R = d->R, a.ctas = d->ctas;
   for (int q = 0; q <= d->nranks; ++q) {
     a.row_offset[q] = d->row_offset[q];
@@ -796,7 +799,31 @@ int ntf_peer_gather(const ntf_peer_gather_desc* d, ntf_stream_t stream) {
     a.base[q] = d->peer_base[q];
   }
   a.full = d->full, a.status = d->status, a.timeout_ns = d->timeout_ns;
+  return NTF_OK;
+}
+}  // namespace
+
+int ntf_peer_gather(const ntf_peer_gather_desc* d, ntf_stream_t stream) {
+  ntf::PeerGatherArgs a;
+  const int rc = peer_args(d, 1, &a);
+  if (rc != NTF_OK) return rc;
   NTF_CUDA_TRY(ntf::peer_gather_launch(a, static_cast<cudaStream_t>(stream)));
+  return NTF_OK;
+}
+
+int ntf_peer_gather_group(const ntf_peer_gather_desc* descs, int nranks, ntf_stream_t stream) {
+  if (!descs || nranks < 1 || nranks > NTF_MAX_PEERS) return fail(NTF_ERR_INVALID, "bad rank count");
+  ntf::PeerGatherGroup g{};
+  for (int q = 0; q < nranks; ++q) {
+    const int rc = peer_args(descs + q, nranks, &g.args[q]);
+    if (rc != NTF_OK) return rc;
+    if (descs[q].me != q || descs[q].nranks != nranks || descs[q].ctas != descs[0].ctas)
+      return fail(NTF_ERR_INVALID, "group: descs[q] must be rank q of nranks, same ctas");
+    for (int r = 0; r <= nranks; ++r)
+      if (descs[q].row_offset[r] != descs[0].row_offset[r])
+        return fail(NTF_ERR_INVALID, "group: ranks disagree on the row blocks");
+  }
+  NTF_CUDA_TRY(ntf::peer_gather_group_launch(g, nranks, static_cast<cudaStream_t>(stream)));
   return NTF_OK;
 }
 
@@ -811,6 +838,7 @@ int ntf_plan_mode_update(ntf_plan* pl, int mode, int last_sweep, ntf_stream_t st
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   if (mode < 1 || mode > pl->order) return fail(NTF_ERR_INVALID, "mode out of range");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PdlOff no_pdl(pl->timing && pl->events);
   const int rc = enqueue_mode_update(pl, mode, last_sweep ? 1 : 0, s);
   if (rc != NTF_OK) return rc;
   return join_side(pl, s);  // grams[m] is current when the stream reaches here
@@ -929,7 +957,6 @@ void ntf_plan_destroy(ntf_plan* pl) {
     ntf::dev_free(pl->card_sel[m]);
   }
   ntf::dev_free(pl->gram_ws);
-  ntf::dev_free(pl->gram_pending);
   delete pl;
 }
 

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 
@@ -13,6 +14,26 @@
 namespace ntf {
 
 constexpr int kWarp = 32;
+
+// Tuning and diagnostic environment knobs (tile geometry overrides, the
+// tcgen05 kernel's skip masks and wait counters, the row update's debug
+// flags, plan timing) exist only in NTF_DIAG builds made by tools/; the
+// release library never reads them, so no environment setting can change
+// what a timed kernel does.
+inline const char* diag_env(const char* name) {
+#ifdef NTF_DIAG
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+#ifdef NTF_DIAG
+constexpr bool kDiagBuild = true;
+#else
+constexpr bool kDiagBuild = false;
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -141,6 +162,16 @@ inline cudaError_t allow_dyn_smem(const void* kern, size_t need) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
 }
 
+// Launches made while this (per host thread) switch is off carry no PDL
+// attribute: kernels then serialise on the stream and the griddepcontrol
+// instructions are no-ops.  The plan turns it off while it enqueues an
+// instrumented iteration, so the CUDA events around each kernel bracket that
+// kernel alone.
+inline bool& pdl_switch() {
+  thread_local bool on = true;
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, Args&&... args) {
@@ -153,7 +184,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_switch() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

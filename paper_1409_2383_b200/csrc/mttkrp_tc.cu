@@ -6,41 +6,58 @@
 //   mode 2: m = j, o = i, l = k   (F_hi, F_lo) = (A, C)
 //   mode 3: m = k, o = i, l = j   (F_hi, F_lo) = (A, B)
 //
-// Numerics: exact fixed-point slicing on kind::f16 MMAs.
-//   X    = xs * (S0 + S1)        S0 integers |S0| <= 2^11, S1 in 2^-11 units,
-//                                xs = 2^(e-11) global (split once per tensor)
-//   F_lo = ls(n) * (T0 + T1 + T2)  T0 integers |T0| <= 2^t, T1 in 2^-11 and T2
-//                                in 2^-22 units (fp16-exact, T2 possibly
-//                                subnormal), ls(n) = 2^(f(n)-t) per column
+// Numerics: fixed-point slicing on kind::f16 MMAs with an exact leading term.
+//   X    = xs * (S0 + S1)        S0 integers |S0| <= 2^11, S1 = fp16 of the
+//                                exact remainder in [-1/2, 1/2] (11 significant
+//                                bits of it), xs = 2^(e-11) global
+//   F_lo = ls(n) * (T0 + T1 + T2)  T0 integers |T0| <= 2^t, T1, T2 = fp16 of the
+//                                successive exact remainders (T2 possibly
+//                                subnormal), ls(n) = 2^(f(n)-t) per column;
+//   Fh   = fp16(F_lo / ls(n))    F_lo to 11 significant bits
 // The tensor core forms, per unit of G consecutive 64-wide l blocks at one o,
 //   ACC0 = sum S0*T0                       integers < 2^24: EXACT in fp32
-//   ACC1 = sum S0*T1 + S1*T0,  ACC2 = sum S0*T2 + S1*T1   (corrections;
-//   for N > 85 ACC2's terms go straight into ACC1: two sets of 2N columns fit)
-// with t = 7, 6, 5 for G = 1, 2, 3..4 keeping |ACC0| <= 2^11 * 2^t * 64G <= 2^24.  F_lo is
-// represented to 2^-(22+t) of its column maximum (27-28 bits); the dropped
-// S1*T2 term is ~2^-33.  The epilogue multiplies the unit's accumulators by
-// F_hi[o, n] held as an fp32 pair (exact product split with FMA) and
-// accumulates in double-float (TwoSum), so F_hi enters at ~2^-48.
+//   ACC1 = sum S0*T1 + S1*Fh,  ACC2 = sum S0*T2        (corrections; for
+//   N > 85 ACC2's terms go straight into ACC1: two sets of 2N columns fit)
+// i.e. 4N MMA columns per K step (S1 multiplies the 11-bit Fh: its weight is
+// 2^-11 below S0's, so Fh's 2^-12 relative rounding sits at ~2^-23 of the
+// product and averages out over the contraction).  t = 7, 6, 5, 5 for
+// G = 1..4 keeps |ACC0| <= 2^11 * 2^t * 64G <= 2^24.  F_lo is represented to
+// 2^-25 of 2^t (2^-30 of its column maximum at t = 5), X to 2^-24 of its
+// maximum.  The epilogue multiplies the unit's accumulators by F_hi[o, n]
+// held as an fp32 pair (exact product split with FMA) and accumulates in
+// double-float (TwoSum, packed f32x2 on two columns at a time), so F_hi
+// enters at ~2^-48.
 //
 // Data layout: the split tensor is stored once per mode as a BLOCK IMAGE
 // (image_split_kernel): for each m-tile and unit (g, o) in g-major order, each
 // l block is the no-swizzle K-major UMMA image of both planes.  A CTA owns one
 // m-tile and a contiguous range of units, so it streams ONE contiguous byte
-// range with 1-D bulk copies (long sequential DRAM runs; the natural layout's
+// range, block after block (long sequential DRAM runs; the natural layout's
 // 128-byte row pieces ran at 4.4-4.8 TB/s, the image at 6.7).  The W slices of
 // a group do not depend on o: formed once per MTTKRP (w_slice_kernel) and
-// bulk-copied into shared memory once per group; the epilogue drains TMEM
-// once per unit.
+// copied into shared memory once per group; the epilogue drains TMEM once per
+// unit.
+//
+// CTA pairs (CG = 2, the default): two CTAs on one TPC take two consecutive
+// m-tiles with the same unit range; the leader issues tcgen05.mma.cta_group::2
+// (M = 256: each CTA's 128 rows of A from its own shared memory, each MMA's
+// N' rows of B split between them), so each CTA holds only half of the W
+// slices (twice the l blocks per unit for the same shared memory) and one MMA
+// instruction serves both SMs.  Both CTAs load their blocks with 2-CTA tensor
+// -map loads that complete on the leader's barriers; the leader's commits
+// multicast to both CTAs; each CTA drains its own TMEM lanes.
 //
 // Roles (one CTA per SM, mbarrier handshakes, all ring indices incremental):
-//   warp 0        producer: one bulk copy per X block into an SX-stage ring
+//   warp 0        producer: one copy per X block into an SX-stage ring
 //   warps 1, 3    MMA issuers on alternate units (a single issuing thread is
 //                 bound by per-instruction issue latency for small-N MMAs);
 //                 each owns its accumulator sets, both release X slots
-//   warp 2        W slices of each group + F_hi pair rows (bulk copies)
+//                 (a pair's peer CTA: idle)
+//   warp 2        W slices of each group + F_hi pair rows
 //   warps 4..     epilogue, 8 or 16 warps (2 or 4 column groups per
 //                 TMEM lane quarter, by N): per unit tcgen05.ld, F_hi scaling,
 //                 double-float accumulation; finally the fp64 partial of the CTA.
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -48,7 +65,6 @@
 #include <cstdlib>
 
 #include "mttkrp_tc.cuh"
-#include "ridge.cuh"
 
 namespace ntf {
 
@@ -66,8 +82,11 @@ constexpr int kFMin = -990;  // exponent clamp of the column scales (2^(7+22-kFM
 #ifndef NTF_EPI_SMALL
 #define NTF_EPI_SMALL 8
 #endif
+#ifndef NTF_EPI_N112
+#define NTF_EPI_N112 8
+#endif
 __host__ __device__ constexpr int epi_warps(int NT) {
-  return NT <= 2 ? NTF_EPI_SMALL : ((NT == 6 || NT == 8) ? 16 : 8);
+  return NT <= 2 ? NTF_EPI_SMALL : ((NT == 6 || NT == 8) ? 16 : (NT == 7 ? NTF_EPI_N112 : 8));
 }
 // warps: 0 X producer, 1 and 3 MMA issuers (alternate units; warp 3 idle
 // when only one accumulator set fits), 2 W slices + F_hi rows, 4.. epilogue
@@ -174,23 +193,111 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
 
+// Completion of this thread's earlier tcgen05 ops arrives on `bar`; for a CTA
+// pair (CG = 2) on the barrier at the same offset in BOTH CTAs.
+template <int CG>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;\n" ::"r"(smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+  }
+}
+
+// D[tmem] (+)= A[smem] * B[smem]; CG = 2: M = 256 over the CTA pair (each
+// CTA's A rows and half of B's N rows at the same shared-memory offsets),
+// issued by the pair's leader only.
+template <int CG>
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+// 2-D tensor-map load into this CTA's shared memory whose completion (bytes)
+// is counted on the mbarrier at `bar_cluster` (a shared::cluster address: for
+// a CTA pair the leader's barrier, cta_group::2).
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                             uint32_t bar_cluster) {
   asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-          smem_u32(bar))
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
 }
 
-__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                           uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(cta));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// arrive on the barrier at `bar`'s offset in CTA `cta` of the cluster (default
+// .release.cta semantics: a cluster-scope release per arrival measured ~2x
+// slower epilogues in the pair's peer CTA)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+}
+
+// wait with acquire at cluster scope (arrivals from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// store a word into the same shared-memory offset of CTA `cta` of the cluster
+__device__ __forceinline__ void st_cluster_u32(uint32_t* p, uint32_t cta, uint32_t v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(p)), "r"(cta));
+  asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(remote), "r"(v) : "memory");
 }
 
 // 32 lanes x 32 bits, 16 consecutive columns per thread
@@ -265,22 +372,21 @@ __device__ __forceinline__ uint64_t smem_desc_noswz(const void* p, uint32_t lbo_
   return d;
 }
 
-// kind::f16 instruction descriptor: F16 x F16 -> F32, M=128
-__host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major) {
+// kind::f16 instruction descriptor: F16 x F16 -> F32, M = 128 per CTA of the group
+__host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major, int cg = 1) {
   return (1u << 4)                                 // D format F32
          | (0u << 7) | (0u << 10)                  // A, B format F16
          | ((a_mn_major ? 1u : 0u) << 15)          // A major
          | (0u << 16)                              // B K-major
          | ((static_cast<uint32_t>(N) >> 3) << 17) // N >> 3
-         | ((static_cast<uint32_t>(kTM) >> 4) << 24);  // M >> 4
+         | ((static_cast<uint32_t>(kTM * cg) >> 4) << 24);  // M >> 4
 }
 
-// Accumulator set: 3N fp32 TMEM columns [ACC0 | ACC1 | ACC2].  As many sets
-// as fit (up to 4) so the MMA runs ahead of the epilogue.
 // Accumulator set per unit: [ACC0 | ACC1 | ACC2] (3N fp32 columns), or for
 // N > 85 (3N > 256, the MMA N limit) the merged [ACC0 | ACC12] (2N columns):
 // ACC2's terms (2^-11 below ACC1's) are accumulated into ACC1 directly, which
 // loses nothing (ACC1's own fp32 rounding dominates) and lets two sets fit.
+// As many sets as fit (up to 4) so the MMA runs ahead of the epilogue.
 __host__ __device__ constexpr bool merged_acc(int N) { return 3 * N > 256; }
 __host__ __device__ constexpr int set_cols(int N) { return merged_acc(N) ? 2 * N : 3 * N; }
 __host__ __device__ constexpr int acc_bufs_fit(int N) {
@@ -293,6 +399,43 @@ __host__ __device__ constexpr int acc_bufs(int N) {
   return mma_issuers(N) == 2 ? (acc_bufs_fit(N) & ~1) : 1;
 }
 
+// Bits of F_lo's integer slice T0 (|T0| <= 2^t) that keep ACC0 = sum S0*T0
+// over a unit's 64 G products exact in fp32: 2^11 * 2^t * 64 G <= 2^24.
+__host__ __device__ constexpr int t_bits(int G) {
+  return G <= 1 ? 7 : (G <= 2 ? 6 : (G <= 4 ? 5 : 4));
+}
+
+// The B operand (W slices) of one 64-wide l block, virtual rows
+// [T0 | T1 | T2 | Fh] (N rows each; Fh = F_lo rounded to fp16, the operand of
+// S1).  Per K step the MMAs read contiguous row ranges of it:
+//   N <= 85: S0 x [T0|T1|T2] (rows [0, 3N)), S1 x Fh ([3N, 4N))
+//   N >  85: S0 x [T0|T1] ([0, 2N)), S0 x T2 ([2N, 3N)), S1 x Fh ([3N, 4N))
+// For a CTA pair each MMA's N' rows are split in halves between the CTAs
+// (the leader's descriptor addresses both CTAs' shared memory at the same
+// offset), so CTA c stores the c-th half of every range, ranges in order:
+// 4N / CG rows per CTA and l block.  Returns CTA and row of virtual row v.
+__host__ __device__ constexpr int w_ranges(int N) { return merged_acc(N) ? 3 : 2; }
+__host__ __device__ constexpr int w_range_begin(int N, int k) {
+  return merged_acc(N) ? (k == 0 ? 0 : (k == 1 ? 2 * N : 3 * N)) : (k == 0 ? 0 : 3 * N);
+}
+__host__ __device__ constexpr int w_range_end(int N, int k) {
+  return merged_acc(N) ? (k == 0 ? 2 * N : (k == 1 ? 3 * N : 4 * N)) : (k == 0 ? 3 * N : 4 * N);
+}
+__host__ __device__ inline void w_row_slot(int N, int CG, int v, int& cta, int& row) {
+  int off = 0;
+  for (int k = 0; k < w_ranges(N); ++k) {
+    const int b = w_range_begin(N, k), e = w_range_end(N, k), h = (e - b) / CG;
+    if (v < e) {
+      cta = (v - b) / h;
+      row = off + (v - b) - cta * h;
+      return;
+    }
+    off += h;
+  }
+  cta = 0;
+  row = 0;
+}
+
 __host__ __device__ constexpr uint32_t tmem_cols(int N) {
   return acc_bufs(N) * set_cols(N) <= 32    ? 32
          : acc_bufs(N) * set_cols(N) <= 64  ? 64
@@ -302,6 +445,10 @@ __host__ __device__ constexpr uint32_t tmem_cols(int N) {
 }
 
 struct TcParams {
+  // CTA pairs: tensor maps over the image (rows of 128 B; box = one full /
+  // one last l block of an m-tile) and over the W slices (box = one l block
+  // of one CTA), so each CTA's loads complete on the pair leader's barriers
+  CUtensorMap map_full, map_tail, map_w;
   const unsigned char* img;  // this mode's block image of the split tensor (see tc_tensor_create)
   int64_t tile_bytes;        // bytes of one full m-tile in the image
   int r8_full, r8_tail;      // stored rows (multiple of 8) of a full / the ragged last m-tile
@@ -312,9 +459,11 @@ struct TcParams {
   int n_full, splits, splits_tail;
   int tm;                    // rows per m-tile (<= 128; MMA M is 128, rows >= tm ignored)
   int x_stages, h_stages;
-  int stage_bytes;           // X ring slot stride (>= one full block, multiple of 1 KB)
-  const float2* hpair;       // [n_o][N] F_hi[o, n] * 2^-e(n) as fp32 (hi, lo) pairs (w_slice_kernel)
-  const unsigned char* wsl;  // [n_lb][3][N][128 B] W slices of F_lo (w_slice_kernel)
+  int slot_ks;               // K steps (16 l values) per X ring slot
+  int stage_bytes;           // X ring slot stride (slot_ks * 64 * r8_full bytes, 128 B aligned)
+  const float2* hpair;       // [n_o][N/2] float4 {hi(n), hi(n+1), lo(n), lo(n+1)}, n even: F_hi[o, n] * 2^-e(n)
+                             // as fp32 (hi, lo) pairs, packed by column pair for the f32x2 epilogue
+  const unsigned char* wsl;  // [CG][n_lb][4N / CG][128 B] W slices of F_lo (w_slice_kernel)
   const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
   const double* cm_lo;       // [R] max |F_lo[:, n]|
   const double* xscale;      // tensor split scale (device scalar)
@@ -322,12 +471,12 @@ struct TcParams {
                              // by the row update that follows (NULL: untouched)
   double* ws;                // [splits][M][R] partials
   const int* stop_flag;
-  int debug;                 // profiling only (NTF_TC_DEBUG): 2 skip MMA, 4 skip TMEM
+  int debug;                 // NTF_DIAG builds only (NTF_TC_DEBUG): 2 skip MMA, 4 skip TMEM
                              // drain, 16 skip X loads, 32 per-role wait cycles,
                              // 64 plain arrives for commits, 128 skip W slicing,
                              // 256 per-CTA globaltimer stamps, 2048 sleeping waits
   unsigned long long* times;  // NTF_TC_DEBUG & 256: per-CTA globaltimer stamps [8]
-  TcRidge ridge;              // extra CTA (gridDim.x - 1) when ridge.out != NULL
+  int n_tiles;                // m-tiles (CG = 2: even, every tile stored with r8_full rows)
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
   uint32_t ub_tail[kTcMaxSplits + 1];  // ... of the ragged last tile
 };
@@ -355,14 +504,50 @@ struct UnitIt {
   }
 };
 
-__device__ __forceinline__ void two_sum(float& hi, float& lo, float p) {
-  const float s = hi + p;
-  const float bp = s - hi;
-  lo += (hi - (s - bp)) + (p - bp);
+// Packed fp32 pairs (f32x2: FFMA2 / FADD2 / FMUL2 on sm_100a): the epilogue
+// treats two adjacent accumulator columns per instruction.  Every operation is
+// an explicitly rounded PTX instruction, so the error-free transformations
+// below stay exact (no contraction across them).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2pack(float lo_col, float hi_col) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo_col), "f"(hi_col));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(f32x2 v, float& lo_col, float& hi_col) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo_col), "=f"(hi_col) : "l"(v));
+}
+__device__ __forceinline__ f32x2 f2mul(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm volatile("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2fma(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2add(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2sub(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm volatile("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2neg(f32x2 a) { return a ^ 0x8000000080000000ull; }
+
+// (hi, lo) += p exactly (Knuth TwoSum), on both lanes
+__device__ __forceinline__ void two_sum2(f32x2& hi, f32x2& lo, f32x2 p) {
+  const f32x2 s = f2add(hi, p);
+  const f32x2 bp = f2sub(s, hi);
+  lo = f2add(lo, f2add(f2sub(hi, f2sub(s, bp)), f2sub(p, bp)));
   hi = s;
 }
 
-template <int NT>  // N / 16
+template <int NT, int CG>  // N / 16; CTAs per MMA group (1, or 2: a CTA pair with M = 256)
 __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
   constexpr int N = NT * 16;
   constexpr int kEpi = epi_warps(NT);
@@ -372,34 +557,22 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kIssuers = mma_issuers(N);
-  const int kXStage = p.stage_bytes;       // one X block (both planes of r8_full rows), 1 KB aligned
-  constexpr int kWlb = 3 * N * kBK * 2;    // T0|T1|T2 of one l block
+  const int kXStage = p.stage_bytes;       // one X slot (slot_ks K steps of both planes), 128 B aligned
+  constexpr int kWrows = 4 * N / CG;       // W rows of one l block held by this CTA
+  constexpr int kWlb = kWrows * kBK * 2;   // their bytes
   constexpr int kFirstEpi = 4;
   const uint64_t g_entry = gtimer();
   pdl_trigger();
-  if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  if (p.ridge.out && blockIdx.x == gridDim.x - 1) {
-    // ----------------- ridge CTA (concurrent with the streaming CTAs) -----------------
-    pdl_wait();  // the previous row update's Gram partials / grams / rho
-    if (*p.ridge.gram_pending) {  // G of the factor updated just before this mode
-      gram_from_rows_block(p.ridge.f_prev, p.ridge.rows_prev, p.R, p.ridge.gram_prev,
-                           reinterpret_cast<double*>(smem_raw));
-      __syncthreads();
-      if (threadIdx.x == 0) *p.ridge.gram_pending = 0;
-    }
-    ridge_factor_block(p.ridge.Ga, p.ridge.Gb, *p.ridge.rho, p.R, p.ridge.out, p.ridge.status,
-                       reinterpret_cast<double*>(smem_raw));
-    return;
-  }
   // 1 KB alignment by offset (keeps the pointer in the shared address space)
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int SX = p.x_stages, SH = p.h_stages, G = p.G;
   const int R = p.R;
-  unsigned char* xbase = base;
-  unsigned char* wbase = xbase + SX * kXStage;
+  // [W slices of a group (SW128, 1 KB aligned)][F_hi pair ring][X ring][barriers]
+  unsigned char* wbase = base;
   float2* hbase = reinterpret_cast<float2*>(wbase + G * kWlb);  // [SH][N]
-  uint64_t* x_full = reinterpret_cast<uint64_t*>(hbase + SH * N);
+  unsigned char* xbase = reinterpret_cast<unsigned char*>(hbase + SH * N);  // 128 B aligned (N % 16 == 0)
+  uint64_t* x_full = reinterpret_cast<uint64_t*>(xbase + SX * kXStage);
   uint64_t* x_empty = x_full + SX;
   uint64_t* h_full = x_empty + SX;
   uint64_t* h_empty = h_full + SH;
@@ -408,14 +581,22 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   uint64_t* acc_full = w_empty + 1;
   uint64_t* acc_empty = acc_full + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 4);
+  uint32_t* stop_slot = tmem_slot + 1;
   // per-column scales, written by warp 2 after pdl_wait (see there)
   double* wsc = reinterpret_cast<double*>(acc_empty + 6);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // this CTA's tile and unit range
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0: the pair's leader (issues the MMAs)
+  const bool leader = crank == 0;
+  // this CTA's tile and unit range (a pair: consecutive tiles, one unit range)
   int tile, split;
   const uint32_t* ub;
-  if (static_cast<int>(blockIdx.x) < p.n_full * p.splits) {
+  if constexpr (CG == 2) {
+    const int pair = blockIdx.x / 2, n_tp = p.n_tiles / 2;
+    tile = (pair % n_tp) * 2 + static_cast<int>(crank);
+    split = pair / n_tp;
+    ub = p.ub_full;
+  } else if (static_cast<int>(blockIdx.x) < p.n_full * p.splits) {
     tile = blockIdx.x % p.n_full;
     split = blockIdx.x / p.n_full;
     ub = p.ub_full;
@@ -432,9 +613,13 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   auto lbs_of = [&](int g) { return min(G, p.n_lb - g * G); };
 
   if (threadIdx.x == 0) {
+    // A pair's loads (both CTAs' X blocks and W halves) complete on the
+    // leader's x_full / w_full; the leader's commits reach x_empty / w_empty
+    // / acc_full in both CTAs (multicast); the peer's x_empty has no second
+    // issuer, so it counts the owner's commit only.
     for (int s = 0; s < SX; ++s) {
       mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], kIssuers);  // owner's MMA commit (+ the other issuer's arrive)
+      mbar_init(&x_empty[s], leader ? kIssuers : 1);  // owner's MMA commit (+ the other issuer's arrive)
     }
     for (int s = 0; s < SH; ++s) {
       mbar_init(&h_full[s], 1);
@@ -444,23 +629,39 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     mbar_init(w_empty, kIssuers);  // one commit per MMA issuer
     for (int s = 0; s < kAccBufs; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], kEpi);
+      mbar_init(&acc_empty[s], kEpi * CG);  // both CTAs' epilogue warps (the peer's remotely)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // stop decision: the leader's read of the flag, so both CTAs of a pair agree
+    if (leader) {
+      const uint32_t stop = (p.stop_flag && *reinterpret_cast<const volatile int*>(p.stop_flag)) ? 1u : 0u;
+      *stop_slot = stop;
+      if constexpr (CG == 2) st_cluster_u32(stop_slot, 1, stop);
+    }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(tmem_cols(N)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(tmem_cols(N)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(tmem_cols(N)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // barriers initialised and the stop word delivered pair-wide
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const bool prof = (p.debug & 32) != 0;
-  const int wm = (prof ? 1 : 0) | ((p.debug & 2048) ? 2 : 0);
-  const uint64_t g_ready = (prof || (p.debug & 256)) ? gtimer() : 0;
+  const bool stopped = *reinterpret_cast<volatile uint32_t*>(stop_slot) != 0;
+  const int dbg = kDiagBuild ? p.debug : 0;  // release builds: constant 0, every branch folds away
+  const bool prof = (dbg & 32) != 0;
+  const int wm = (prof ? 1 : 0) | ((dbg & 2048) ? 2 : 0);
+  const uint64_t g_ready = (prof || (dbg & 256)) ? gtimer() : 0;
   long long wt[3] = {0, 0, 0};
   const long long t_start = prof ? clock64() : 0;
   uint64_t t_role = 0;  // NTF_TC_DEBUG & 256: end of this role's loop
@@ -468,7 +669,6 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
 
   // Roles 0-2: warp-uniform loops (descriptors and barrier addresses stay in
   // uniform registers); one elected lane issues.
-  const int dbg = p.debug;
   // This CTA's m-tile in the image: stored rows, block sizes and the byte
   // offset of its first unit.  A CTA's units are consecutive (g-major) and
   // the image stores them consecutively, so the CTA streams ONE contiguous
@@ -476,7 +676,13 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   const int r8 = tile < p.n_full ? p.r8_full : p.r8_tail;
   const uint32_t blk_full = 256u * static_cast<uint32_t>(r8);  // 2 planes x 8 chunks x r8 x 16 B
   const uint32_t blk_tail = 32u * static_cast<uint32_t>(p.ct * r8);
-  if (warp == 0) {
+  // A block is 4 (the last l block: ct / 2) K steps of 64 * r8 bytes each
+  // ([plane][2 chunks][r8 rows][16 B]); the X ring moves slot_ks of them per slot.
+  const uint32_t ks_bytes = 64u * static_cast<uint32_t>(r8);
+  const int slot_ks = p.slot_ks;
+  if (stopped) {
+    // converged earlier: nothing to compute (the row update skips as well)
+  } else if (warp == 0) {
     // ------------------------------ X-block producer --------------------------
     const bool no_x = (dbg & 16) != 0;
     const int n_lb = p.n_lb;
@@ -492,65 +698,85 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // when BOTH have passed it (x_empty counts 2: the owner's commit after its
     // MMAs, the other issuer's arrive after observing the load), so neither
     // can fall a full ring behind and every parity wait stays unambiguous.
+    // A pair's peer CTA fills its own ring the same way; the leader's
+    // commits and arrivals reach its x_empty too.
     Ring xr;
     UnitIt ui = u0;
     const int64_t off0 = off;
     for (int u = u_begin; u < u_end; ++u) {
       const int nl = lbs_of(ui.g);
       for (int j = 0; j < nl; ++j) {
-        mbar_wait_p(&x_empty[xr.idx], xr.phase ^ 1u, wm, wt[0]);
-        uint64_t* bar = &x_full[xr.idx];
-        const uint32_t bytes = (ui.g * G + j == n_lb - 1) ? blk_tail : blk_full;
-        if (elect_one()) {
-          if (no_x) {
-            mbar_arrive(bar);
-          } else {
-            mbar_arrive_expect_tx(bar, bytes);
-            bulk_load(xbase + xr.idx * kXStage, p.img + off, bytes, bar);
+        const bool last_lb = ui.g * G + j == n_lb - 1;
+        const int nks = last_lb ? p.ct / 2 : kBK / kUK;
+        for (int k0 = 0; k0 < nks; k0 += slot_ks) {
+          mbar_wait_p(&x_empty[xr.idx], xr.phase ^ 1u, wm, wt[0]);
+          uint64_t* bar = &x_full[xr.idx];
+          const uint32_t bytes = static_cast<uint32_t>(min(slot_ks, nks - k0)) * ks_bytes;
+          if (elect_one()) {
+            if constexpr (CG == 2) {
+              // both CTAs' blocks count on the leader's barrier (slot_ks = 4: one
+              // block per slot, one tensor-map load of 2 r8 rows of 128 B)
+              if (no_x) {
+                if (leader) mbar_arrive(bar);
+              } else {
+                if (leader) mbar_arrive_expect_tx(bar, 2 * bytes);
+                tma_load_2sm(xbase + xr.idx * kXStage, last_lb ? &p.map_tail : &p.map_full, 0,
+                             static_cast<int32_t>(off >> 7), mapa_u32(smem_u32(bar), 0));
+              }
+            } else if (no_x) {
+              mbar_arrive(bar);
+            } else {
+              mbar_arrive_expect_tx(bar, bytes);
+              bulk_load(xbase + xr.idx * kXStage, p.img + off, bytes, bar);
+            }
           }
+          __syncwarp();
+          off += bytes;
+          xr.next(SX);
         }
-        __syncwarp();
-        off += bytes;
-        xr.next(SX);
       }
       ui.next(n_o);
     }
     t_role = gtimer();
     x_kb = static_cast<uint32_t>((off - off0) >> 10);
+  } else if ((warp == 1 || warp == 3) && !leader) {
+    // CTA pair, peer: the leader issues every MMA of the pair
   } else if (warp == 1 || warp == 3) {
     // ------------------------------ MMA issuers --------------------------------
    if (warp == 1 || kIssuers == 2) {  // warp 3 idles when one accumulator set fits
-    // Two wide MMAs per K step, each reading its A tile once: the W slices
-    // T0|T1|T2 are consecutive N-row blocks of one K-major B operand.
-    //   cols [0, 3N) (=|+=) S0 * [T0 | T1 | T2]     cols [N, 3N) += S1 * [T0 | T1]
-    // A (the X block) is a no-swizzle K-major image: 8-row x 16 B core
-    // matrices, row groups 128 B apart (SBO), 8-element chunks r8*16 B apart
-    // (LBO); plane S1 follows plane S0.
+    // Per K step (W rows: see w_row_slot):
+    //   N <= 85: [ACC0|ACC1|ACC2] (=|+=) S0 x [T0|T1|T2];  ACC1 += S1 x Fh
+    //   N >  85: [ACC0|ACC12] (=|+=) S0 x [T0|T1];  ACC12 += S0 x T2;  ACC12 += S1 x Fh
+    // A (one K step of the X block) is a no-swizzle K-major image: 8-row x
+    // 16 B core matrices, row groups 128 B apart (SBO), the step's two
+    // 8-element chunks r8*16 B apart (LBO); plane S1 follows plane S0.
     const bool no_mma = (dbg & 2) != 0, plain_arrive = (dbg & 64) != 0;
-    // N' <= 256 per MMA: for N > 85 the first MMA is split into S0*[T0|T1]
-    // and S0*T2 (the S0 tile is then read twice)
     constexpr bool kMerged = merged_acc(N);
-    const uint32_t idesc3 = make_idesc(kMerged ? 2 * N : 3 * N, false);
-    const uint32_t idesc2 = make_idesc(2 * N, false);
-    const uint32_t idesc1 = make_idesc(N, false);
+    const uint32_t idesc_a = make_idesc(kMerged ? 2 * N : 3 * N, false, CG);
+    const uint32_t idesc_n = make_idesc(N, false, CG);
+    // B operand offsets (rows of this CTA's W block, descriptor units of 16 B)
+    constexpr uint64_t kB1 = ((w_range_end(N, 0) - w_range_begin(N, 0)) / CG) * 128 / 16;
+    constexpr uint64_t kB2 = kMerged ? kB1 + (N / CG) * 128 / 16 : kB1;
     const uint32_t lbo = static_cast<uint32_t>(r8) * 16u;
     const uint64_t da_base = smem_desc_noswz(xbase, lbo, 128);
     const uint64_t db_base = smem_desc(wbase, 16, 1024);
-    const uint32_t a_kstep = (2 * lbo) >> 4;  // descriptor units (16 B): two chunks per K=16
+    const uint32_t a_plane = (2 * lbo) >> 4;  // descriptor units (16 B): plane S1 of a K step
+    const uint32_t a_kstep = ks_bytes >> 4;   // next K step within a slot
     const int n_lb = p.n_lb, ct = p.ct;
     // Issuer warps take alternate units, each with its own accumulator sets
     // (set b serves units u with u % kAccBufs == b, an even count), and both
-    // walk the shared X ring in order (see the producer).  A single issuing thread is bound by the per-
-    // instruction issue latency of small-N MMAs, not by the tensor pipe.
+    // walk the shared X ring in order (see the producer).  A single issuing
+    // thread is bound by the per-instruction issue latency of small-N MMAs.
     const int mine = warp == 1 ? 0 : 1;
     Ring xr, ar;
     UnitIt ui = u0;
     int cur_g = -1;
     uint32_t wphase = 0;
+    auto wait_slot = [&](int slot, uint32_t phase) { mbar_wait_p(&x_full[slot], phase, wm, wt[0]); };
     for (int u = u_begin; u < u_end; ++u) {
-      if (ui.g != cur_g) {  // new group: its W slices must be resident
+      if (ui.g != cur_g) {  // new group: its W slices must be resident (both halves)
         if (cur_g >= 0) {
-          if (elect_one()) tc_commit(w_empty);
+          if (elect_one()) tc_commit<CG>(w_empty);
           __syncwarp();
         }
         mbar_wait_p(w_full, wphase, wm, wt[2]);
@@ -561,58 +787,53 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       const int owner = kIssuers == 2 ? ((u - u_begin) & 1) : 0;
       if (owner != mine) {  // the other issuer's unit: observe and release its X slots
         for (int j = 0; j < nl; ++j) {
-          mbar_wait_p(&x_full[xr.idx], xr.phase, wm, wt[0]);
-          if (elect_one()) mbar_arrive(&x_empty[xr.idx]);
-          __syncwarp();
-          xr.next(SX);
+          const int nks = (ui.g * G + j == n_lb - 1) ? ct / 2 : kBK / kUK;
+          for (int k0 = 0; k0 < nks; k0 += slot_ks) {
+            wait_slot(xr.idx, xr.phase);
+            if (elect_one()) mbar_arrive(&x_empty[xr.idx]);
+            __syncwarp();
+            xr.next(SX);
+          }
         }
         ar.next(kAccBufs);
         ui.next(n_o);
         continue;
       }
-      mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, wm, wt[1]);
+      mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, wm, wt[1]);  // (a pair: both CTAs drained)
       tc_fence_after();
       const uint32_t d0 = tmem + ar.idx * set_cols(N);
       const uint32_t d1 = d0 + N;
       for (int j = 0; j < nl; ++j) {
-        const int slot = xr.idx;
-        mbar_wait_p(&x_full[slot], xr.phase, wm, wt[0]);
-        tc_fence_after();
-        const int chunks = (ui.g * G + j == n_lb - 1) ? ct : 8;
-        const uint64_t da0 = da_base + static_cast<uint64_t>((slot * kXStage) >> 4);
-        const uint64_t da1 = da0 + static_cast<uint64_t>((static_cast<uint32_t>(chunks) * lbo) >> 4);
+        const int nks = (ui.g * G + j == n_lb - 1) ? ct / 2 : kBK / kUK;
         const uint64_t db = db_base + static_cast<uint64_t>((j * kWlb) >> 4);
-        if (elect_one()) {
-          if (!no_mma) {
-#pragma unroll
-            for (int kk = 0; kk < kBK / kUK; ++kk) {
-              if (2 * kk < chunks) {
-                const uint32_t first = (j | kk) ? 1u : 0u;
-                const uint64_t b = db + kk * (32 >> 4);
-                if constexpr (kMerged) {
-                  // [ACC0|ACC12] = S0*[T0|T1]; ACC12 += S0*T2 + S1*T0 + S1*T1
-                  constexpr uint64_t kT1 = (N * 128) >> 4, kT2 = (2 * N * 128) >> 4;
-                  tc_mma_f16(d0, da0 + kk * a_kstep, b, idesc3, first);
-                  tc_mma_f16(d1, da0 + kk * a_kstep, b + kT2, idesc1, 1u);
-                  tc_mma_f16(d1, da1 + kk * a_kstep, b, idesc1, 1u);
-                  tc_mma_f16(d1, da1 + kk * a_kstep, b + kT1, idesc1, 1u);
-                } else {
-                  // [ACC0|ACC1|ACC2] = S0*[T0|T1|T2]; [ACC1|ACC2] += S1*[T0|T1]
-                  tc_mma_f16(d0, da0 + kk * a_kstep, b, idesc3, first);
-                  tc_mma_f16(d1, da1 + kk * a_kstep, b, idesc2, 1u);
-                }
+        for (int k0 = 0; k0 < nks; k0 += slot_ks) {
+          const int slot = xr.idx;
+          const int nk = min(slot_ks, nks - k0);
+          wait_slot(slot, xr.phase);
+          tc_fence_after();
+          const uint64_t da = da_base + static_cast<uint64_t>((slot * kXStage) >> 4);
+          if (elect_one()) {
+            if (!no_mma) {
+              for (int kk = 0; kk < nk; ++kk) {
+                const int ks = k0 + kk;  // K step within the l block
+                const uint32_t first = (j | ks) ? 1u : 0u;
+                const uint64_t a0 = da + kk * a_kstep, a1 = a0 + a_plane;
+                const uint64_t b = db + ks * (32 >> 4);
+                tc_mma_f16<CG>(d0, a0, b, idesc_a, first);
+                if constexpr (kMerged) tc_mma_f16<CG>(d1, a0, b + kB1, idesc_n, 1u);
+                tc_mma_f16<CG>(d1, a1, b + kB2, idesc_n, 1u);
               }
             }
+            if (plain_arrive) mbar_arrive(&x_empty[slot]);  // profiling: no tensor-pipe commit
+            else tc_commit<CG>(&x_empty[slot]);
           }
-          if (plain_arrive) mbar_arrive(&x_empty[slot]);  // profiling: no tensor-pipe commit
-          else tc_commit(&x_empty[slot]);
+          __syncwarp();
+          xr.next(SX);
         }
-        __syncwarp();
-        xr.next(SX);
       }
       if (elect_one()) {
         if (plain_arrive) mbar_arrive(&acc_full[ar.idx]);
-        else tc_commit(&acc_full[ar.idx]);
+        else tc_commit<CG>(&acc_full[ar.idx]);
       }
       __syncwarp();
       ar.next(kAccBufs);
@@ -628,7 +849,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
     // max|F_hi[:,n]| < 2^e (the same clamps as w_slice_kernel)
     for (int n = lane; n < N; n += 32) {
-      const int t = G >= 3 ? 5 : (G >= 2 ? 6 : 7);
+      const int t = t_bits(G);
       int f = 0, e = 0;
       const double cl = n < R ? p.cm_lo[n] : 0.0, ch = n < R ? p.cm_hi[n] : 0.0;
       if (cl > 0.0) frexp(cl, &f);
@@ -644,6 +865,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     if (blockIdx.x == 0 && p.cm_self)
       for (int n = lane; n < R; n += 32) p.cm_self[n] = 0.0;
     __syncwarp();
+    const unsigned char* wsl = p.wsl + static_cast<int64_t>(crank) * p.n_lb * kWlb;  // this CTA's W half
     Ring hr;
     UnitIt ui = u0;
     int seg = 0;
@@ -651,9 +873,18 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       if (u == u_begin || ui.o == 0) {  // group start: the previous group's MMAs are done
         if (seg > 0) mbar_wait_p(w_empty, (seg - 1) & 1, wm, wt[2]);
         if (elect_one()) {
-          const uint32_t bytes = static_cast<uint32_t>(lbs_of(ui.g) * kWlb);
-          mbar_arrive_expect_tx(w_full, bytes);
-          bulk_load(wbase, p.wsl + static_cast<int64_t>(ui.g) * G * kWlb, bytes, w_full);
+          const int nl = lbs_of(ui.g);
+          const uint32_t bytes = static_cast<uint32_t>(nl * kWlb);
+          if constexpr (CG == 2) {  // one tensor-map load per l block; both halves count on the leader
+            if (leader) mbar_arrive_expect_tx(w_full, 2 * bytes);
+            const uint32_t wbar = mapa_u32(smem_u32(w_full), 0);
+            for (int j = 0; j < nl; ++j)
+              tma_load_2sm(wbase + j * kWlb, &p.map_w, 0,
+                           static_cast<int32_t>((crank * p.n_lb + ui.g * G + j) * kWrows), wbar);
+          } else {
+            mbar_arrive_expect_tx(w_full, bytes);
+            bulk_load(wbase, wsl + static_cast<int64_t>(ui.g) * G * kWlb, bytes, w_full);
+          }
         }
         __syncwarp();
         ++seg;
@@ -668,17 +899,17 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       ui.next(n_o);
     }
     t_role = gtimer();
-  } else {
+  } else if (warp >= kFirstEpi) {
     // ------------------------------ epilogue ----------------------------------
     const int e = warp - kFirstEpi;
     const int q4 = warp & 3;            // TMEM lane quarter of this warp
     const int c0 = (e >> 2) * NC;       // this warp's column range
     const int row = q4 * 32 + lane;     // tile row == TMEM lane
-    float hi[NC], lo[NC];
+    f32x2 hi[NC / 2], lo[NC / 2];       // double-float accumulators, column pairs
 #pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      hi[j] = 0.f;
-      lo[j] = 0.f;
+    for (int j = 0; j < NC / 2; ++j) {
+      hi[j] = 0ull;
+      lo[j] = 0ull;
     }
     Ring ar, hr;
     for (int u = u_begin; u < u_end; ++u) {
@@ -686,32 +917,36 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       mbar_wait_p(&h_full[hr.idx], hr.phase, wm, wt[1]);
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * set_cols(N) + c0;
-      const float2* hs = hbase + hr.idx * N + c0;
-      if (!(p.debug & 4)) {
+      const float4* hs = reinterpret_cast<const float4*>(hbase + hr.idx * N + c0);
+      if (!(dbg & 4)) {
 #pragma unroll
         for (int j = 0; j < NC / LW; ++j) {
           float a0[LW], a1[LW], a2[LW];
           tmem_ld<LW>(taddr + j * LW, a0);           // ACC0: S0*T0 (exact integers)
-          tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*T0 (+ ACC2 when merged)
-          if constexpr (!merged_acc(N)) tmem_ld<LW>(taddr + 2 * N + j * LW, a2);  // ACC2: S0*T2 + S1*T1
+          tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*Fh (+ ACC2 when merged)
+          if constexpr (!merged_acc(N)) tmem_ld<LW>(taddr + 2 * N + j * LW, a2);  // ACC2: S0*T2
           tmem_wait_ld();
 #pragma unroll
-          for (int v = 0; v < LW; ++v) {
-            const float2 h = hs[j * LW + v];
-            const float a = a0[v];
-            const float pr = a * h.x;
-            const float er = fmaf(a, h.x, -pr);    // a*h.x = pr + er exactly
-            const float a12 = merged_acc(N) ? a1[v] : a1[v] + a2[v];
-            const float cr = fmaf(a12, h.x, fmaf(a, h.y, er));
-            two_sum(hi[j * LW + v], lo[j * LW + v], pr);
-            lo[j * LW + v] += cr;
+          for (int v = 0; v < LW; v += 2) {
+            const float4 h = hs[(j * LW + v) >> 1];  // {hi, hi', lo, lo'} of columns v, v+1
+            const f32x2 hx = f2pack(h.x, h.y), hy = f2pack(h.z, h.w);
+            const f32x2 a = f2pack(a0[v], a0[v + 1]);
+            f32x2 a12 = f2pack(a1[v], a1[v + 1]);
+            if constexpr (!merged_acc(N)) a12 = f2add(a12, f2pack(a2[v], a2[v + 1]));
+            const f32x2 pr = f2mul(a, hx);
+            const f32x2 er = f2fma(a, hx, f2neg(pr));  // a*hx = pr + er exactly
+            const f32x2 cr = f2fma(a12, hx, f2fma(a, hy, er));
+            const int q = (j * LW + v) >> 1;
+            two_sum2(hi[q], lo[q], pr);
+            lo[q] = f2add(lo[q], cr);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&acc_empty[ar.idx]);
+        if (leader) mbar_arrive(&acc_empty[ar.idx]);
+        else mbar_arrive_remote(&acc_empty[ar.idx], 0);  // the peer's TMEM reads are done
         mbar_arrive(&h_empty[hr.idx]);
       }
       ar.next(kAccBufs);
@@ -724,6 +959,12 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // (a thread's own row is R doubles apart from its neighbours').
     const int rows_valid = static_cast<int>(p.M - m0 < p.tm ? p.M - m0 : p.tm);
     double* out0 = p.ws + (static_cast<int64_t>(split) * p.M + m0) * R;
+    float hf[NC], lf[NC];
+#pragma unroll
+    for (int j = 0; j < NC / 2; ++j) {
+      f2unpack(hi[j], hf[2 * j], hf[2 * j + 1]);
+      f2unpack(lo[j], lf[2 * j], lf[2 * j + 1]);
+    }
     if (p.tm * R * 8 <= SX * kXStage) {
       double* stage = reinterpret_cast<double*>(xbase);
       if (row < rows_valid) {
@@ -731,7 +972,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
         for (int j = 0; j < NC; ++j) {
           const int n = c0 + j;
           if (n < R)
-            stage[row * R + n] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * wsc[2 * N + n];
+            stage[row * R + n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * wsc[2 * N + n];
         }
       }
       asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
@@ -743,7 +984,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       for (int j = 0; j < NC; ++j) {
         const int n = c0 + j;
         if (n < R)
-          out[n] = (static_cast<double>(hi[j]) + static_cast<double>(lo[j])) * wsc[2 * N + n];
+          out[n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * wsc[2 * N + n];
       }
     }
   }
@@ -752,7 +993,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
            warp, u_end - u_begin, clock64() - t_start, wt[0], wt[1], wt[2],
            (unsigned long long)g_entry, (unsigned long long)(g_ready - g_entry),
            (unsigned long long)(gtimer() - g_entry));
-  if ((p.debug & 256) && lane == 0 && warp <= 3) {
+  if ((dbg & 256) && lane == 0 && warp <= 3) {
     unsigned long long* ts = p.times + static_cast<int64_t>(blockIdx.x) * 8;
     ts[2 + warp] = t_role;
     if (warp == 0) {
@@ -764,25 +1005,32 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
               (static_cast<unsigned long long>(x_kb) << 32);
     }
   }
+  // every MMA into this CTA's TMEM has completed (the epilogue saw its last
+  // commit); a pair also waits for the peer before releasing the columns
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(tmem_cols(N)));
-    if ((p.debug & 256) && lane == 0) p.times[static_cast<int64_t>(blockIdx.x) * 8 + 6] = gtimer();
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols(N)));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols(N)));
+    if ((dbg & 256) && lane == 0) p.times[static_cast<int64_t>(blockIdx.x) * 8 + 6] = gtimer();
   }
 }
 
 // ----------------------------------------------------------------------------
 // W slices of F_lo for every 64-row l block, in the UMMA K-major SW128 layout
 // the MTTKRP CTAs bulk-copy into shared memory:
-//   wsl[lb][s][n][128 B],  element l of row n at ((l/8) ^ (n&7))*16 + (l%8)*2
+//   wsl[cta][lb][row][128 B],  element l of a row at ((l/8) ^ (row&7))*16 + (l%8)*2
+// with the virtual rows [T0 | T1 | T2 | Fh] (N each) placed by w_row_slot:
 //   v = F_lo[l, n] * 2^(t - f(n)) = T0 + T1 + T2 (+ <= 2^-23 rounding),
 //   T0 integer (|T0| <= 2^t), T1 in 2^-11 units, T2 in 2^-22 units (fp16
-//   exact, T2 possibly subnormal).  One thread per (l block, n, octet).
+//   exact, T2 possibly subnormal); Fh = fp16(v), the 11-bit operand of the
+//   low tensor plane S1.  One thread per (l block, n, octet).
 // ----------------------------------------------------------------------------
-__global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int n_lb,
+__global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int CG, int n_lb,
                                const double* __restrict__ cm, int t, unsigned char* __restrict__ wsl,
                                const double* __restrict__ Fhi, int n_o,
                                const double* __restrict__ cm_hi, float2* __restrict__ hpair,
@@ -824,7 +1072,9 @@ __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, i
         h = fh * ldexp(1.0, -max(ex, kFMin));
       }
       const float hx = static_cast<float>(h);
-      hpair[e] = make_float2(hx, static_cast<float>(h - static_cast<double>(hx)));
+      float* hp = reinterpret_cast<float*>(hpair) + o * (2 * N) + (n >> 1) * 4 + (n & 1);
+      hp[0] = hx;                                                   // packed by column pair:
+      hp[2] = static_cast<float>(h - static_cast<double>(hx));      // {hi, hi', lo, lo'}
     }
     if (do_w) {
       double sc = 0.0;
@@ -833,24 +1083,33 @@ __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, i
         if (cml > 0.0) frexp(cml, &f);
         sc = ldexp(1.0, t + 22 - max(f, kFMin));  // v in 2^-22 units of the T0 scale
       }
-      __align__(16) __half h0[8], h1[8], h2[8];
+      __align__(16) __half hs[4][8];
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
-        // one rounding to the 2^-22 quantum, then exact integer digit split
-        const long long q = __double2ll_rn(x[v] * sc);      // |q| <= 2^(t+22)
-        const long long b0 = (q + (1ll << 21)) >> 22;        // |b0| <= 2^t
-        const long long r = q - (b0 << 22);                  // [-2^21, 2^21)
-        const long long b1 = (r + (1ll << 10)) >> 11;        // [-1024, 1024]
-        const long long b2 = r - (b1 << 11);                 // [-1024, 1024)
-        h0[v] = __float2half_rn(static_cast<float>(b0));
-        h1[v] = __float2half_rn(static_cast<float>(b1) * 4.8828125e-04f);         // 2^-11 units
-        h2[v] = __float2half_rn(static_cast<float>(b2) * 2.384185791015625e-07f);  // 2^-22 units
+        // v = F_lo * 2^(t-f), exact (a power-of-two scale); T0 = rint(v) is an
+        // integer, |T0| <= 2^t (ACC0's exactness rests on it); the remainders
+        // r1 = v - T0 and r2 = r1 - T1 are exact in fp64 and each rounded once
+        // to fp16 (11 significant bits of the remainder itself, not of a fixed
+        // 2^-11 grid): |v - (T0+T1+T2)| <= max(2^-12 |r2|, 2^-25) <= 2^-25.
+        const double vv = x[v] * (sc * 0x1p-22);
+        const double t0 = rint(vv);
+        const double r1 = vv - t0;
+        const __half h1 = __double2half(r1);
+        const double r2 = r1 - static_cast<double>(__half2float(h1));
+        hs[0][v] = __double2half(t0);
+        hs[1][v] = h1;
+        hs[2][v] = __double2half(r2);
+        hs[3][v] = __double2half(vv);  // Fh = fp16(v), the operand of the low plane S1
       }
-      unsigned char* wb = wsl + static_cast<int64_t>(lb) * 3 * N * 128;
-      const int off = n * 128 + ((oct ^ (n & 7)) << 4);
-      *reinterpret_cast<uint4*>(wb + off) = *reinterpret_cast<const uint4*>(h0);
-      *reinterpret_cast<uint4*>(wb + N * 128 + off) = *reinterpret_cast<const uint4*>(h1);
-      *reinterpret_cast<uint4*>(wb + 2 * N * 128 + off) = *reinterpret_cast<const uint4*>(h2);
+      const int rows_cta = 4 * N / CG;
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        int cta = 0, row = 0;
+        w_row_slot(N, CG, sl * N + n, cta, row);
+        unsigned char* wb = wsl + (static_cast<int64_t>(cta) * n_lb + lb) * rows_cta * 128;
+        *reinterpret_cast<uint4*>(wb + row * 128 + ((oct ^ (row & 7)) << 4)) =
+            *reinterpret_cast<const uint4*>(hs[sl]);
+      }
     }
   }
 }
@@ -869,13 +1128,14 @@ __global__ void absmax_kernel(const float* __restrict__ X, int64_t n, unsigned* 
 
 // One mode's block image of the split tensor.  For each m-tile t (r8
 // stored rows, a multiple of 8; rows >= M are zero), each unit (g, o) in
-// g-major order and each l block j of the unit, both planes back to back:
-//   [plane][chunk c < chunks(lb)][row < r8][8 fp16]      (chunk = 8 l values)
-// i.e. the no-swizzle K-major UMMA image of the block, so one bulk copy moves
-// it into shared memory and a CTA's units are one contiguous byte range.
+// g-major order and each l block j of the unit, K step by K step:
+//   [K step s < chunks(lb)/2][plane][chunk c < 2][row < r8][8 fp16]   (chunk = 8 l values)
+// i.e. each K step is the no-swizzle K-major UMMA image of both planes, so
+// one bulk copy moves any run of K steps into shared memory and a CTA's
+// units are one contiguous byte range.
 // The last l block stores only ct chunks (l_ext rounded up to 16).
-// Values: X * 2^(11-e) = S0 + S1, S0 = rint (|S0| <= 2^11), S1 = rint of the
-// remainder in 2^-11 units (both exact in fp16), xscale = 2^(e-11).
+// Values: X * 2^(11-e) = S0 + S1, S0 = rint (|S0| <= 2^11, exact in fp16),
+// S1 = fp16 of the exact remainder (|S1| <= 1/2), xscale = 2^(e-11).
 struct ImgGeom {
   int mode;
   int64_t I, J, K, M;
@@ -908,7 +1168,8 @@ __global__ void image_split_kernel(const float* __restrict__ X, ImgGeom g, const
     const int nl = min(g.G, g.n_lb - gi * g.G);
     const int64_t unit_bytes = (nl - 1) * bf + (gi * g.G + nl == g.n_lb ? bt : bf);
     const int64_t off = t * g.tile_bytes + static_cast<int64_t>(gi) * g.n_o * g.G * bf +
-                        o * unit_bytes + j * bf + static_cast<int64_t>(c) * r8 * 16 + row * 16;
+                        o * unit_bytes + j * bf + static_cast<int64_t>(c >> 1) * 64 * r8 +
+                        static_cast<int64_t>(c & 1) * r8 * 16 + row * 16;
     const int64_t m = static_cast<int64_t>(t) * g.tm + row;
     const int l0 = lb * 64 + c * 8;
     __align__(16) __half h0[8], h1[8];
@@ -923,14 +1184,12 @@ __global__ void image_split_kernel(const float* __restrict__ X, ImgGeom g, const
         x = X[idx];
       }
       const float sv = x * up;                // exact (power-of-two scaling)
-      const float a0 = rintf(sv);
-      const float a1 = rintf((sv - a0) * 2048.0f);  // exact
+      const float a0 = rintf(sv);             // S0: integer, |S0| <= 2^11
       h0[v] = __float2half_rn(a0);
-      h1[v] = __float2half_rn(a1 * 4.8828125e-04f);  // 2^-11 units
+      h1[v] = __float2half_rn(sv - a0);       // S1: the exact remainder in [-1/2, 1/2], rounded once to fp16
     }
     *reinterpret_cast<uint4*>(img + off) = *reinterpret_cast<const uint4*>(h0);
-    *reinterpret_cast<uint4*>(img + off + static_cast<int64_t>(chunks) * r8 * 16) =
-        *reinterpret_cast<const uint4*>(h1);
+    *reinterpret_cast<uint4*>(img + off + 32 * static_cast<int64_t>(r8)) = *reinterpret_cast<const uint4*>(h1);
   }
 }
 
@@ -970,27 +1229,51 @@ int sm_count_tc() {
   return n;
 }
 
-template <int NT>
+template <int NT, int CG>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
-  auto kern = mttkrp_tc_kernel<NT>;
+  auto kern = mttkrp_tc_kernel<NT, CG>;
   if (prep) return allow_dyn_smem(reinterpret_cast<const void*>(kern), L.smem_bytes);
-  const int extra = p.ridge.out ? 1 : 0;
-  return launch_pdl(kern, dim3(L.n_full * L.splits + L.splits_tail + extra), dim3(L.threads),
-                    L.smem_bytes, stream, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(L.n_full * L.splits + L.splits_tail);
+  cfg.blockDim = dim3(L.threads);
+  cfg.dynamicSmemBytes = L.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_switch()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (CG == 2) {  // CTA pairs on one TPC (tcgen05 cta_group::2)
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int CG>
+cudaError_t dispatch_cg(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
+  switch (L.N / 16) {
+    case 1: return launch_nt<1, CG>(p, L, stream, prep);
+    case 2: return launch_nt<2, CG>(p, L, stream, prep);
+    case 3: return launch_nt<3, CG>(p, L, stream, prep);
+    case 4: return launch_nt<4, CG>(p, L, stream, prep);
+    case 5: return launch_nt<5, CG>(p, L, stream, prep);
+    case 6: return launch_nt<6, CG>(p, L, stream, prep);
+    case 7: return launch_nt<7, CG>(p, L, stream, prep);
+    case 8: return launch_nt<8, CG>(p, L, stream, prep);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
-  switch (L.N / 16) {
-    case 1: return launch_nt<1>(p, L, stream, prep);
-    case 2: return launch_nt<2>(p, L, stream, prep);
-    case 3: return launch_nt<3>(p, L, stream, prep);
-    case 4: return launch_nt<4>(p, L, stream, prep);
-    case 5: return launch_nt<5>(p, L, stream, prep);
-    case 6: return launch_nt<6>(p, L, stream, prep);
-    case 7: return launch_nt<7>(p, L, stream, prep);
-    case 8: return launch_nt<8>(p, L, stream, prep);
-    default: return cudaErrorInvalidValue;
-  }
+  return L.cg == 2 ? dispatch_cg<2>(p, L, stream, prep) : dispatch_cg<1>(p, L, stream, prep);
 }
 
 // Split units [0, n_g * n_o) (g-major) into `parts` contiguous ranges of
@@ -1000,7 +1283,7 @@ cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
 void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
   const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
   double unit_fixed = 2.0 + L.N / 32.0;  // measured: c2 best near 3, R = 64..100 near 4..6
-  if (const char* e = getenv("NTF_TC_UNITCOST")) unit_fixed = atof(e);
+  if (const char* e = diag_env("NTF_TC_UNITCOST")) unit_fixed = atof(e);
   auto cost = [&](int g) {
     const int nl = std::min(L.G, L.n_lb - g * L.G);
     const bool tail = g * L.G + nl == L.n_lb;
@@ -1061,88 +1344,104 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.N = ((R + 15) / 16) * 16;
   L.M = mode == 1 ? I : (mode == 2 ? J : K);
   L.Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
-  L.n_mtiles = static_cast<int>((L.M + kTM - 1) / kTM);
   L.l_ext = static_cast<int>(mode == 3 ? J : K);
   L.n_o = static_cast<int>(mode == 1 ? J : I);
   L.n_lb = (L.l_ext + kBK - 1) / kBK;
   L.threads = tc_threads(L.N / 16);
+  // CTA pairs (tcgen05 cta_group::2, M = 256 over two SMs of a TPC): each
+  // CTA keeps only half of the W slices resident, so a unit (one TMEM
+  // drain) spans more l blocks, and one MMA instruction serves both SMs.
+  L.cg = 2;
+  if (const char* e = diag_env("NTF_TC_CG")) L.cg = atoi(e) == 1 ? 1 : 2;
   // Equal m-tiles of tm <= 128 rows (a multiple of 8, the core-matrix
-  // height), so every CTA of a full tile streams the same bytes; the last
-  // tile may be shorter.
+  // height), so every CTA of a full tile streams the same bytes.  Pairs
+  // take two consecutive tiles: an even tile count, and every tile stored
+  // with tm rows (the last one zero-padded) so both CTAs of a pair share the
+  // leader's A descriptor.  Single CTAs: the last tile may be shorter.
   {
-    const int64_t nt = (L.M + kTM - 1) / kTM;
+    const int64_t nt = L.cg == 2 ? 2 * ((L.M + 2 * kTM - 1) / (2 * kTM)) : (L.M + kTM - 1) / kTM;
     L.tm = static_cast<int>(8 * ((L.M + 8 * nt - 1) / (8 * nt)));
+    L.n_mtiles = static_cast<int>(nt);
   }
-  // Shared memory: X ring (one block of tm rows per slot: 26 KB at tm = 104,
-  // 32 KB at 128) + resident W slices of a group (G blocks x 3N x 128 B) +
-  // F_hi pair ring; then as deep an X ring as fits (the stream is
-  // latency-bound per SM: c2 548 / 596 / 609 it/s at 3 / 4 / 5 slots).
-  const int xs = ((2 * L.tm * kBK * 2 + 1023) / 1024) * 1024;
+  // Shared memory: resident W slices of a group (G blocks x 4N/cg x 128 B) +
+  // F_hi pair ring + the X ring, whose slots hold slot_ks K steps (64 tm
+  // bytes each).  Measured (per mode, c2/c3/c4/c5): one K step per slot
+  // (8 KB, a deep ring) 104/1069/645/11200 us, two 69/752/428/9866, a whole
+  // 64-wide l block (4 K steps) 56/693/336/9318: every X slot costs the MMA
+  // issuer a barrier wait and a tcgen05.commit, so slots are whole blocks.
+  // G is the largest (<= 4: T0 keeps t = 5 bits, F_lo 27 bits) that leaves
+  // a ring of at least min_ring bytes.
+  L.slot_ks = 4;
+  if (const char* e = diag_env("NTF_TC_SLOTKS")) L.slot_ks = std::max(1, std::min(4, atoi(e)));
+  const int xs = ((L.slot_ks * 64 * L.tm + 127) / 128) * 128;
   L.stage_bytes = xs;
   L.h_stages = 8;
-  auto total = [&](int G, int SX) {
-    return 1024 + SX * xs + G * 3 * L.N * kBK * 2 + L.h_stages * L.N * 8 +
-           (2 * SX + 2 * L.h_stages + 12) * 8 + 16 + 3 * L.N * 8;
-  };
+  const int wlb = 4 * L.N / L.cg * kBK * 2;  // W bytes of one l block in one CTA
   const int limit = 226 * 1024;  // the opt-in 227 KB less the kernel's 1 KB of static shared memory
-  // Largest G (fewest drains) with a 3-deep X ring (2-deep for N >= 96,
-  // whose epilogue, not the stream, is the bound); measured: c3 G=4/3
-  // stages 668 us vs G=2/4 stages 757 us, 1000^3 R=100 G=3/2 stages 1016 vs 1083.
-  int min_stages = L.N >= 96 ? 2 : 3;
-  if (const char* e = getenv("NTF_TC_MINSTAGES")) min_stages = atoi(e);
+  auto fixed_bytes = [&](int G) {
+    return 1024 + G * wlb + L.h_stages * L.N * 8 + (2 * L.h_stages + 14) * 8 + 16 + 3 * L.N * 8;
+  };
+  auto total = [&](int G, int SX) { return fixed_bytes(G) + SX * (xs + 24); };
+  int min_ring = 64 * 1024;
+  if (const char* e = diag_env("NTF_TC_MINRING")) min_ring = atoi(e) * 1024;
   L.G = 1;
   for (int G : {4, 3, 2, 1})
-    if (total(G, min_stages) <= limit) {
+    if (limit - fixed_bytes(G) >= min_ring) {
       L.G = G;
       break;
     }
-  if (const char* e = getenv("NTF_TC_G")) L.G = atoi(e);
+  if (const char* e = diag_env("NTF_TC_G")) L.G = atoi(e);
   L.G = std::max(1, std::min(L.G, L.n_lb));
-  L.x_stages = 8;
-  if (const char* e = getenv("NTF_TC_XSTAGES")) L.x_stages = atoi(e);
+  L.x_stages = kTcMaxXStages;
+  if (const char* e = diag_env("NTF_TC_XSTAGES")) L.x_stages = std::max(2, std::min(kTcMaxXStages, atoi(e)));
   while (total(L.G, L.x_stages) > limit && L.x_stages > 2) --L.x_stages;
-  L.smem_bytes = std::max<int>(total(L.G, L.x_stages),
-                               1024 + ridge_smem_doubles(R) * static_cast<int>(sizeof(double)));
+  L.smem_bytes = total(L.G, L.x_stages);
   L.tmem_cols = static_cast<int>(tmem_cols(L.N));
   L.n_g = (L.n_lb + L.G - 1) / L.G;
   const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
-  // One CTA per SM, one wave.  CTAs go to tiles in proportion to their cost
-  // (a 400-row mode is 3 full tiles + 16 rows: equal splits would leave a
-  // fifth of the SMs streaming almost nothing); a block of a ragged tile
-  // costs a fixed pipeline share plus its rows' share of the bytes.  One SM
-  // is left free so the mode's ridge Cholesky (side stream) runs concurrently.
-  const int cap = std::min(sm_count_tc() - 1, kTcMaxSplits);
-  L.n_full = static_cast<int>(L.M / L.tm);
-  const int tail = static_cast<int>(L.M % L.tm);
-  L.r8_full = L.tm;
-  L.r8_tail = tail ? 8 * ((tail + 7) / 8) : 0;
+  // One CTA per SM, one wave.  Two SMs are left free so the mode's ridge
+  // Cholesky (side stream) and the early row-update blocks run concurrently.
+  const int cap = std::min(sm_count_tc() - 2, kTcMaxSplits);
   {
     const int rem = L.l_ext % kBK;
     L.ct = rem == 0 ? 8 : 2 * ((rem + 15) / 16);
   }
   L.tile_bytes = static_cast<int64_t>(L.n_o) * 32 * L.tm * (8 * (L.n_lb - 1) + L.ct);
-  L.img_bytes = static_cast<size_t>(L.n_full) * L.tile_bytes +
-                (tail ? static_cast<size_t>(L.n_o) * 32 * L.r8_tail * (8 * (L.n_lb - 1) + L.ct) : 0);
-  double fixed = 1.0;  // measured: a ragged tile's l block costs about a full one
-  if (const char* e = getenv("NTF_TC_TAILCOST")) fixed = atof(e);
-  const double wt = tail ? fixed + (1.0 - fixed) * tail / static_cast<double>(kTM) : 0.0;
   auto clampu = [&](int64_t s) { return static_cast<int>(std::max<int64_t>(1, std::min(s, units))); };
-  if (L.n_full == 0) {
-    L.splits = 0;
-    L.splits_tail = clampu(cap);
-  } else {
-    L.splits = clampu(static_cast<int64_t>(cap / (L.n_full + wt)));
+  if (L.cg == 2) {
+    // every tile padded to tm rows: one partition shared by all pairs
+    L.n_full = L.n_mtiles;
+    L.r8_full = L.tm;
+    L.r8_tail = 0;
+    L.img_bytes = static_cast<size_t>(L.n_full) * L.tile_bytes;
+    L.splits = clampu(static_cast<int64_t>(cap / 2 / (L.n_full / 2)));
     L.splits_tail = 0;
-    if (tail)
-      L.splits_tail = clampu(std::min<int64_t>(static_cast<int64_t>(L.splits * wt + 0.5),
-                                               cap - static_cast<int64_t>(L.n_full) * L.splits));
+    if (const char* e = diag_env("NTF_TC_SPLITS")) L.splits = clampu(std::min(atoi(e), cap / L.n_full));
+    partition_units(L, L.splits, L.ub_full);
+  } else {
+    // CTAs go to tiles in proportion to their cost (a 400-row mode is 3 full
+    // tiles + 16 rows: equal splits would leave a fifth of the SMs streaming
+    // almost nothing); a block of a ragged tile costs about a full one.
+    L.n_full = static_cast<int>(L.M / L.tm);
+    const int tail = static_cast<int>(L.M % L.tm);
+    L.r8_full = L.tm;
+    L.r8_tail = tail ? 8 * ((tail + 7) / 8) : 0;
+    L.img_bytes = static_cast<size_t>(L.n_full) * L.tile_bytes +
+                  (tail ? static_cast<size_t>(L.n_o) * 32 * L.r8_tail * (8 * (L.n_lb - 1) + L.ct) : 0);
+    const double wt = tail ? 1.0 : 0.0;
+    if (L.n_full == 0) {
+      L.splits = 0;
+      L.splits_tail = clampu(cap);
+    } else {
+      L.splits = clampu(static_cast<int64_t>(cap / (L.n_full + wt)));
+      L.splits_tail = 0;
+      if (tail)
+        L.splits_tail = clampu(std::min<int64_t>(static_cast<int64_t>(L.splits * wt + 0.5),
+                                                 cap - static_cast<int64_t>(L.n_full) * L.splits));
+    }
+    if (L.splits) partition_units(L, L.splits, L.ub_full);
+    if (L.splits_tail) partition_units(L, L.splits_tail, L.ub_tail);
   }
-  if (const char* e = getenv("NTF_TC_SPLITS")) {  // tuning: CTAs per full tile, the rest to the tail
-    L.splits = std::max(1, std::min(atoi(e), static_cast<int>(cap / std::max(1, L.n_full))));
-    if (tail) L.splits_tail = clampu(cap - static_cast<int64_t>(L.n_full) * L.splits);
-  }
-  if (L.splits) partition_units(L, L.splits, L.ub_full);
-  if (L.splits_tail) partition_units(L, L.splits_tail, L.ub_tail);
   L.wscale = nullptr;
   L.wsl = nullptr;
   L.hpair = nullptr;
@@ -1215,6 +1514,35 @@ void tc_tensor_destroy(TcTensor* t) {
   t->xscale = nullptr;
 }
 
+namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// rows x 128 B of bytes at `base`, loaded box_rows rows at a time, no swizzle
+cudaError_t rows128_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
+  auto enc = tmap_encode();
+  if (!enc || box_rows < 1 || box_rows > 256) return cudaErrorInvalidValue;
+  const cuuint64_t dims[2] = {128, rows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace
+
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
   if (t.mode != L.mode || t.img_bytes != L.img_bytes) return cudaErrorInvalidValue;
   if (!L.wscale) {
@@ -1222,11 +1550,20 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
     if (e != cudaSuccess) return e;
   }
   if (!L.wsl) {
-    cudaError_t e = ntf::dev_alloc(&L.wsl, static_cast<size_t>(L.n_lb) * 3 * L.N * kBK * 2);
+    cudaError_t e = ntf::dev_alloc(&L.wsl, static_cast<size_t>(L.n_lb) * 4 * L.N * kBK * 2);
     if (e != cudaSuccess) return e;
   }
   if (!L.hpair) {
     cudaError_t e = ntf::dev_alloc(&L.hpair, static_cast<size_t>(L.n_o) * L.N * sizeof(float2));
+    if (e != cudaSuccess) return e;
+  }
+  if (L.cg == 2) {  // tensor maps of this image and of the W slices (CTA-pair loads)
+    const int wrows = 4 * L.N / 2;
+    cudaError_t e = rows128_map(&L.map_full, t.img, L.img_bytes / 128, static_cast<uint32_t>(2 * L.r8_full));
+    if (e == cudaSuccess)
+      e = rows128_map(&L.map_tail, t.img, L.img_bytes / 128, static_cast<uint32_t>(L.ct * L.r8_full / 4));
+    if (e == cudaSuccess)
+      e = rows128_map(&L.map_w, L.wsl, static_cast<uint64_t>(2) * L.n_lb * wrows, static_cast<uint32_t>(wrows));
     if (e != cudaSuccess) return e;
   }
   L.bound = true;
@@ -1250,7 +1587,7 @@ cudaError_t colmax_launch(const double* F, int64_t rows, int R, double* out, cud
 
 cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
                              const double* B, const double* C, const double* colmax3, double* ws,
-                             const int* stop_flag, cudaStream_t stream, const TcRidge* ridge) {
+                             const int* stop_flag, cudaStream_t stream) {
   if (!L.bound) return cudaErrorInvalidValue;
   const int64_t I = t.dims[0], J = t.dims[1], K = t.dims[2];
   const double *Fhi, *Flo;
@@ -1280,11 +1617,17 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   p.splits_tail = L.splits_tail;
   p.tm = L.tm;
   p.x_stages = L.x_stages;
+  p.slot_ks = L.slot_ks;
   p.stage_bytes = L.stage_bytes;
   p.h_stages = L.h_stages;
   p.hpair = L.hpair;
   p.wsl = L.wsl;
-  if (ridge) p.ridge = *ridge;
+  p.n_tiles = L.n_mtiles;
+  if (L.cg == 2) {
+    p.map_full = L.map_full;
+    p.map_tail = L.map_tail;
+    p.map_w = L.map_w;
+  }
   p.ws = ws;
   p.stop_flag = stop_flag;
   for (int i = 0; i <= kTcMaxSplits; ++i) {
@@ -1294,7 +1637,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
   {
     static int dbg = -1;
     if (dbg < 0) {
-      const char* env = getenv("NTF_TC_DEBUG");
+      const char* env = diag_env("NTF_TC_DEBUG");
       dbg = env ? atoi(env) : 0;
     }
     p.debug = dbg;
@@ -1315,12 +1658,12 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     p.cm_lo = L.wscale + L.R;
   }
   {
-    const int t = L.G >= 3 ? 5 : (L.G >= 2 ? 6 : 7);
+    const int t = t_bits(L.G);
     const int total = std::max(L.n_lb * L.N * (kBK / 8), L.n_o * L.N);
     const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
     if (!(p.debug & 128)) {
       cudaError_t e = launch_pdl(w_slice_kernel, dim3(blocks), dim3(64), 0, stream, Flo, L.l_ext,
-                                 L.R, L.N, L.n_lb, p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
+                                 L.R, L.N, L.cg, L.n_lb, p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
                                  L.hpair, stop_flag);
       if (e != cudaSuccess) return e;
     }

@@ -32,12 +32,15 @@ void tc_tensor_destroy(TcTensor* t);
 cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream);
 
 constexpr int kTcMaxSplits = 160;  // CTAs per m-tile
+constexpr int kTcMaxXStages = 32;  // X ring slots
 
 struct MttkrpTCLaunch {
+  CUtensorMap map_full, map_tail, map_w;  // cg == 2: the image's blocks and the W slices (mttkrp_tc_bind)
   int mode;
   int R, N;                 // rank and MMA N (R rounded up to 16)
   int64_t M, Q;
-  int n_mtiles;
+  int n_mtiles;             // m-tiles (cg == 2: even)
+  int cg;                   // CTAs per MMA group: 2 = CTA pairs (tcgen05 cta_group::2)
   int n_full, splits;       // full 128-row tiles and CTAs per full tile
   int splits_tail;          // CTAs of the ragged last tile (0: none)
   int tm;                   // rows per m-tile (a multiple of 8)
@@ -49,7 +52,8 @@ struct MttkrpTCLaunch {
   int G, n_g;               // l blocks per unit (one TMEM drain), groups
   int threads, smem_bytes;
   int x_stages, h_stages;
-  int stage_bytes;          // X ring slot stride: one block of tm rows, 1 KB aligned
+  int slot_ks;              // K steps (16 l values, 64 tm bytes) per X ring slot
+  int stage_bytes;          // X ring slot stride, 128 B aligned
   int tmem_cols;
   uint32_t ub_full[kTcMaxSplits + 1];  // unit range of each CTA of a full tile
   uint32_t ub_tail[kTcMaxSplits + 1];
@@ -68,27 +72,10 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L);
 // Check the image matches the plan and allocate the per-launch buffers.
 cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t);
 void mttkrp_tc_unbind(MttkrpTCLaunch& L);
-// Optional ridge work done by one extra CTA of the MTTKRP grid, concurrently
-// with the streaming CTAs: recompute the Gram of the most recently updated
-// factor (when *gram_pending), then factor H = Ga o Gb + rho I into `out`
-// (ridge.cuh layout) for the row update that follows.
-struct TcRidge {
-  const double* f_prev;     // factor updated just before this mode (rows x R)
-  int64_t rows_prev;
-  double* gram_prev;        // its Gram (R x R), recomputed when pending
-  int* gram_pending;        // device flag, cleared after the reduction
-  const double* Ga;         // companion Grams (highest mode first)
-  const double* Gb;
-  const double* rho;        // device scalar rho[mode - 1]
-  double* out;              // ridge buffer
-  int* status;              // NOT_PD
-};
-
 // colmax3: [3][R] per-factor column maxima of |F| (NULL: computed here)
 cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double* A,
                              const double* B, const double* C, const double* colmax3, double* ws,
-                             const int* stop_flag, cudaStream_t stream,
-                             const TcRidge* ridge = nullptr);
+                             const int* stop_flag, cudaStream_t stream);
 // diagnostics (NTF_TC_DEBUG & 256): per-CTA globaltimer stamps of the last launch
 int tc_debug_read_times(unsigned long long* host, int ctas);
 // out[r] = max_i |F[i][r]|

@@ -32,6 +32,14 @@ struct PeerGatherArgs {
   int64_t timeout_ns;
 };
 
+struct PeerGatherGroup {
+  PeerGatherArgs args[kPeerMaxRanks];  // args[q].me == q, one entry per rank
+};
+
 cudaError_t peer_gather_launch(const PeerGatherArgs& a, cudaStream_t stream);
+// all ranks' gathers as one cooperative launch on the current device
+cudaError_t peer_gather_group_launch(const PeerGatherGroup& g, int nranks, cudaStream_t stream);
+// co-residency bound on ctas (per rank) for one launch holding ranks_in_launch ranks
+int peer_gather_max_ctas(int ranks_in_launch);
 
 }  // namespace ntf

@@ -111,7 +111,7 @@ __device__ void split_sum(const FactorUpdateParams& p, int64_t base, int cnt, in
   } else {
     const int t = threadIdx.x, e = t % npm, k = t / npm;
     double v = 0.0;
-    if (k < K && e < cnt && !(p.debug & 1)) v = partial(e, k);
+    if (k < K && e < cnt && !(kDiagBuild && (p.debug & 1))) v = partial(e, k);
     scratch[t] = v;
     __syncthreads();
     if (t < npm) {
@@ -990,7 +990,7 @@ cudaError_t factor_update_prepare(int R) {
 cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t stream) {
   static int dbg = -1;
   if (dbg < 0) {
-    const char* env = getenv("NTF_UPD_DEBUG");
+    const char* env = diag_env("NTF_UPD_DEBUG");
     dbg = env ? atoi(env) : 0;
   }
   FactorUpdateParams p = p_in;

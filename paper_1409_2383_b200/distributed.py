@@ -85,16 +85,23 @@ class Comm:
     def all_reduce_(self, t) -> None:
         self.dist.all_reduce(t, group=self.group)
 
+    def all_reduce_max_(self, t) -> None:
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
     def all_gather_(self, out, t) -> None:
         """out[q * t.numel():(q + 1) * t.numel()] = rank q's ``t``."""
         self.dist.all_gather_into_tensor(out, t, group=self.group)
 
     def peer_ok(self, device) -> bool:
         """Whether rows can be gathered over NVLink peer memory (one fused
-        kernel, ``_PeerRows``) instead of ncclAllGather: CUDA tensors, at most
-        NTF_MAX_PEERS ranks on one node, each on its own GPU, every pair
-        P2P-reachable, and NTF_B200_P2P not "0".  Decided once, collectively
-        (every rank takes the same path)."""
+        kernel, ``_PeerRows``) instead of ncclAllGather: opted in with
+        NTF_B200_P2P=1 (or "force"), CUDA tensors, at most NTF_MAX_PEERS ranks
+        on one node, each on its own GPU, every pair P2P-reachable.  Decided
+        once, collectively (every rank takes the same path).  The default is
+        NCCL: the peer protocol has been verified with all ranks live on one
+        GPU (one cooperative launch, tests/test_peer_gather.py), not yet across
+        GPUs; each peer buffer is also checked against ncclAllGather on first
+        use, with a fall back to NCCL on any difference."""
         if getattr(self, "_peer_state", None) is not None:
             return self._peer_state
         if device.type != "cuda":  # CPU (gloo) runs: all ranks alike, no exchange needed
@@ -107,7 +114,7 @@ class Comm:
 
         from ._native import NTF_MAX_PEERS
 
-        want = os.environ.get("NTF_B200_P2P", "1") != "0" and self.size <= NTF_MAX_PEERS
+        want = os.environ.get("NTF_B200_P2P", "0") in ("1", "force") and self.size <= NTF_MAX_PEERS
         uuid = str(torch.cuda.get_device_properties(device).uuid)
         infos = [None] * self.size
         self.dist.all_gather_object(infos, (socket.gethostname(), uuid, want), group=self.group)
@@ -124,25 +131,44 @@ class Comm:
         self._peer_state = ok
         return ok
 
-    def gather_rows(self, full, offsets: Sequence[int], counts: Sequence[int]) -> None:
+    def gather_rows(self, full, offsets: Sequence[int], counts: Sequence[int], tag=None) -> None:
         """In place: every rank's owned block of ``full`` (rows offsets[p] ..
-        +counts[p]) is broadcast to all ranks.  On one NVLink node this is one
-        kernel that pushes the rows into the peers' buffers (``_PeerRows``);
-        otherwise ncclAllGather with blocks padded to the largest count
+        +counts[p]) is broadcast to all ranks.  ``tag`` names a gather target
+        that lives for the whole fit (the working factors, ``("factor", m)``):
+        on one NVLink node with the peer path enabled those go through one
+        kernel that pushes the rows into the peers' buffers (``_PeerRows``,
+        created collectively on the first gather of each tag, in the same
+        order on every rank).  Untagged targets (one-off temporaries) and every
+        other case use ncclAllGather with blocks padded to the largest count
         because the uniform plan is uneven.  Buffers are
-        allocated once per target tensor, so the call can be captured in a
-        CUDA graph."""
+        allocated once per target, so the call can be captured in a CUDA
+        graph."""
         if self.size == 1 and os.environ.get("NTF_B200_P2P") != "force":
             return  # the owned block is the whole factor ("force": run the kernel anyway, for tests)
-        if self.peer_ok(full.device):
-            key = (full.data_ptr(), tuple(full.shape))
+        if tag is not None and self.peer_ok(full.device):
             if not hasattr(self, "_peers"):
                 self._peers = {}
-            pr = self._peers.get(key)
+            pr = self._peers.get(tag)
             if pr is None:
-                pr = self._peers[key] = _PeerRows(self, full, offsets, counts)
+                pr = _PeerRows(self, full, offsets, counts)
+                if not pr.self_check(offsets, counts):
+                    pr.unmap()
+                    self.dist.barrier(group=self.group)
+                    pr.free()
+                    self._peer_state = False  # every rank saw the same verdict
+                    import warnings
+
+                    warnings.warn("NVLink peer row gather disagreed with ncclAllGather on first use; "
+                                  "using NCCL for this fit")
+                    return self._nccl_gather(full, offsets, counts)
+                self._peers[tag] = pr
+            elif pr.full_ptr != full.data_ptr():
+                raise ValueError(f"peer gather tag {tag!r} reused for another tensor")
             pr.gather()
             return
+        self._nccl_gather(full, offsets, counts)
+
+    def _nccl_gather(self, full, offsets: Sequence[int], counts: Sequence[int]) -> None:
         maxc = max(counts)
         p = self.rank
         key = (full.data_ptr(), tuple(full.shape), maxc)
@@ -161,11 +187,26 @@ class Comm:
                 continue
             full[offsets[q]: offsets[q] + counts[q]].copy_(recv[q * maxc: q * maxc + counts[q]])
 
+    def peer_failed(self) -> bool:
+        """Whether any rank's peer gather timed out (all-reduced: every rank
+        gets the same answer, so all of them abort together)."""
+        peers = getattr(self, "_peers", {})
+        if not peers and not getattr(self, "_peer_state", False):
+            return False
+        import torch
+
+        flag = torch.zeros(1, dtype=torch.int32, device=next(iter(peers.values())).status.device
+                           if peers else torch.device("cuda", torch.cuda.current_device()))
+        for pr in peers.values():
+            flag = torch.maximum(flag, (pr.status != 0).to(torch.int32))
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MAX, group=self.group)
+        return bool(flag.item())
 
     def check_peers(self) -> None:
-        """Raise if a peer gather timed out waiting for another rank."""
-        for pr in getattr(self, "_peers", {}).values():
-            pr.check()
+        """Raise on every rank if any rank's peer gather timed out."""
+        if self.peer_failed():
+            raise RuntimeError("peer row gather timed out waiting for another rank "
+                               "(NTF_B200_P2P_TIMEOUT_S; NTF_B200_P2P=0 selects NCCL)")
 
     def close_peers(self) -> None:
         """Unmap the peers' buffers, wait for every rank to do the same, free
@@ -226,6 +267,10 @@ class _PeerRows:
             self.mapped.append(pb.value)
             bases.append(pb.value)
         self.status = torch.zeros(1, dtype=torch.int32, device=full.device)
+        self.comm = comm
+        self.full_ptr = full.data_ptr()
+        self.shape = tuple(full.shape)
+        self.dtype = full.dtype
         d = self.desc = _native.PeerGatherDesc()
         d.nranks, d.me, d.R = P, me, R
         # same on every rank: derived from the global geometry only
@@ -243,10 +288,37 @@ class _PeerRows:
         stream = self._torch.cuda.current_stream().cuda_stream
         self.check_rc(self.lib.ntf_peer_gather(self.desc, stream))
 
-    def check(self) -> None:
-        if int(self.status.item()) != 0:
-            raise RuntimeError("peer row gather timed out waiting for another rank "
-                               "(NTF_B200_P2P_TIMEOUT_S; NTF_B200_P2P=0 selects NCCL)")
+    def self_check(self, offsets, counts) -> bool:
+        """First use: gather a rank-dependent pattern through this buffer and
+        through ncclAllGather and compare bitwise on every rank (the pattern
+        goes through a scratch tensor, so the real target is untouched; the
+        check consumes one sequence number on every rank alike).  Returns the
+        all-reduced verdict."""
+        torch = self._torch
+        comm = self.comm
+        p = comm.rank
+        rows, R = self.shape
+        pat = torch.arange(rows * R, dtype=torch.float64, device=self.status.device).reshape(rows, R)
+        pat = pat * 1.0000001 + 0.5
+        want = pat.clone()
+        got = torch.full_like(pat, float("nan"))
+        o, c = offsets[p], counts[p]
+        got[o:o + c] = pat[o:o + c]
+        saved = self.desc.full
+        self.desc.full = got.data_ptr()
+        try:
+            self.gather()
+            torch.cuda.current_stream().synchronize()
+        finally:
+            self.desc.full = saved
+        ref = torch.full_like(pat, float("nan"))
+        ref[o:o + c] = pat[o:o + c]
+        comm._nccl_gather(ref, offsets, counts)
+        ok = torch.tensor([1 if (torch.equal(got, want) and torch.equal(ref, want)
+                                 and int(self.status.item()) == 0) else 0],
+                          dtype=torch.int32, device=self.status.device)
+        comm.dist.all_reduce(ok, op=comm.dist.ReduceOp.MIN, group=comm.group)
+        return bool(ok.item())
 
     def unmap(self) -> None:
         for pb in self.mapped:
@@ -262,14 +334,14 @@ class _PeerRows:
 def sharded_iteration(prob, comm: Comm, config: SolverConfig) -> None:
     """One outer iteration of the sharded solver (reference solver.py:295-327
     semantics; mesh.py:149-237 data flow).  ``prob`` provides mode_update,
-    refresh_gram, finalize, factors, norm_acc, norm_all, offsets/counts."""
+    sync_gram, finalize, factors, norm_acc, norm_all, offsets/counts."""
     sweeps = config.inner_sweeps
     for sw in range(sweeps):
         for mode in (1, 2, 3):
             m = mode - 1
             prob.mode_update(mode, sw == sweeps - 1)
-            comm.gather_rows(prob.factors[m], prob.offsets[m], prob.counts[m])
-            prob.refresh_gram(m)
+            comm.gather_rows(prob.factors[m], prob.offsets[m], prob.counts[m], tag=("factor", m))
+            prob.sync_gram(m)
     comm.all_gather_(prob.norm_all, prob.norm_acc)
     prob.finalize()
 
@@ -292,17 +364,18 @@ def _sharded_problem_class():
                              constraints=constraints)
             import os
 
-            self._graph = None
+            self._graphs = {False: None, True: None}  # plain / instrumented iteration
+            self._timing = False
             self._eager_steps = 0
             self._graph_ok = os.environ.get("NTF_B200_SHARDED_GRAPH", "1") != "0"
             for m in range(3):  # capture-safe: Gram workspace allocated up front
                 self._ensure_gram_ws(m)
-            # per-launch timing events stay on (they are captured into the
-            # graph), so kernel_times() always reflects the latest iteration
-            super().set_timing(True)
 
         def set_timing(self, enable: bool) -> None:
-            """Timing events are always recorded on the sharded path."""
+            """Instrumented iterations (per-kernel events, no PDL) have their
+            own captured graph, as the single-GPU plan's."""
+            self._timing = bool(enable)
+            super().set_timing(self._timing)
 
         def step(self) -> None:
             """One outer iteration.  After two eager iterations (NCCL
@@ -312,17 +385,18 @@ def _sharded_problem_class():
             host issues one launch per outer iteration instead of ~10 per mode
             update.  NTF_B200_SHARDED_GRAPH=0 keeps the eager loop."""
             torch = self.torch
-            if self._graph is None and self._graph_ok and self._eager_steps >= 2:
-                self._capture()
-            if self._graph is not None:
+            g = self._graphs[self._timing]
+            if g is None and self._graph_ok and self._eager_steps >= 2:
+                g = self._capture()
+            if g is not None:
                 with torch.cuda.stream(self.stream):
-                    self._graph.replay()
+                    g.replay()
                 return
             with torch.cuda.stream(self.stream):
                 sharded_iteration(self, self.comm, self.config)
             self._eager_steps += 1
 
-        def _capture(self) -> None:
+        def _capture(self):
             import warnings
 
             torch = self.torch
@@ -334,8 +408,28 @@ def _sharded_problem_class():
             except Exception as exc:  # capture unsupported: stay eager (same results)
                 self._graph_ok = False
                 warnings.warn(f"sharded iteration not captured as a CUDA graph ({exc}); running eagerly")
-                return
-            self._graph = g
+                return None
+            self._graphs[self._timing] = g
+            return g
+
+        def sync_gram(self, m: int) -> None:
+            """grams[m] and colmax[m] of the whole factor.  The row update
+            already formed the Gram and column maxima of this rank's rows
+            (Gram partials reduced on the side stream, exact integer maxima),
+            so one R x R sum and one R max over the ranks close them; the
+            all-reduce hands every rank the same bits.  (Before: a Gram and
+            a column-maxima kernel over the whole gathered factor after every
+            mode update, ~15 us each time at c2.)"""
+            if self.comm.size > 1:
+                self.comm.all_reduce_(self.grams[m])
+                self.comm.all_reduce_max_(self.colmax[m])
+
+        def check_status(self):
+            """The plan's status, plus the peer gathers' (all ranks agree:
+            a timeout anywhere aborts the fit on every rank)."""
+            out = super().check_status()
+            self.comm.check_peers()
+            return out
 
         def final_sq_error(self, aux):
             torch = self.torch
@@ -385,6 +479,37 @@ def _sharded_problem_class():
     return ShardedProblem
 
 
+@dataclass
+class ShardedTensor:
+    """One rank's share of a dense order-3 tensor for ``distributed_fit``:
+    its three slabs X[I_p,:,:], X[:,J_p,:], X[:,:,K_p] under ``plan`` (torch
+    tensors, host (pinned) or device), so no rank ever holds the whole tensor
+    (SURVEY 8(e), 8(f) #2).  ``slab_boxes`` gives the boxes to fill, e.g. with
+    ``synth.generate_box`` or a CPDT reader."""
+
+    dims: tuple
+    plan: PartitionPlan
+    rank: int
+    slabs: list
+
+    @staticmethod
+    def slab_boxes(dims, plan: PartitionPlan, rank_id: int):
+        I, J, K = (int(d) for d in dims)
+        r = [plan.row_slice(m, rank_id) for m in (1, 2, 3)]
+        return [((r[0].start, 0, 0), (r[0].stop, J, K)), ((0, r[1].start, 0), (I, r[1].stop, K)),
+                ((0, 0, r[2].start), (I, J, r[2].stop))]
+
+    def validate(self) -> None:
+        if len(self.dims) != 3 or tuple(self.plan.dims) != tuple(self.dims):
+            raise ValueError("sharded tensor: plan and dims disagree (dense order 3 only)")
+        for s, (lo, hi) in zip(self.slabs, self.slab_boxes(self.dims, self.plan, self.rank)):
+            if tuple(s.shape) != tuple(h - l for l, h in zip(lo, hi)):
+                raise ValueError(f"sharded tensor: slab of shape {tuple(s.shape)} does not match "
+                                 f"its box {lo}..{hi}")
+            if s.dtype != self.slabs[0].dtype:
+                raise ValueError("sharded tensor: slabs must share one dtype")
+
+
 def make_slabs(values, plan: PartitionPlan, rank_id: int, device):
     """This rank's three slabs of a host tensor, uploaded to ``device``."""
     import torch
@@ -420,6 +545,8 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     config = config or SolverConfig()
     from .tensors import is_sparse
 
+    if isinstance(t, ShardedTensor):
+        return _fit_sharded_slabs(t, rank, specs, config, engine, group)
     if is_sparse(t):  # COO tensors run on one GPU
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
             raise NotImplementedError("sparse COO tensors are single-GPU (no sharded COO engine)")
@@ -445,6 +572,33 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     device = torch.device("cuda", torch.cuda.current_device())
     vals = t.values
     slabs = make_slabs(vals, plan, comm.rank, device)
+    return _fit_slabs(slabs, t.dims, rank, specs, config, engine, plan, comm)
+
+
+def _fit_sharded_slabs(t: ShardedTensor, rank: int, specs, config, engine, group) -> FitResult:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        raise ValueError("a ShardedTensor needs an initialised torch.distributed process group")
+    comm = Comm(group)
+    if set(t.plan.counts) != {comm.size} or t.rank != comm.rank:
+        raise ValueError("sharded tensor: plan must give every mode one block per rank, "
+                         "and the slabs must be this rank's")
+    t.validate()
+    specs = normalize_specs(specs, 3)
+    if rank < 1:
+        raise ValueError("rank must be >= 1")
+    if any(s.kind == "nonneg_card" for s in specs):
+        raise NotImplementedError("the cardinality constraint needs the whole factor on one GPU "
+                                  "(a global top-c selection); use fit()")
+    device = torch.device("cuda", torch.cuda.current_device())
+    slabs = [s.to(device, non_blocking=s.device.type == "cpu" and s.is_pinned()).contiguous()
+             for s in t.slabs]
+    return _fit_slabs(slabs, tuple(int(d) for d in t.dims), rank, specs, config, engine, t.plan, comm)
+
+
+def _fit_slabs(slabs, dims, rank, specs, config, engine, plan, comm) -> FitResult:
     # ||X||^2 from the mode-1 slabs
     from .engine import sq_error
 
@@ -456,10 +610,10 @@ def distributed_fit(t, rank: int, specs=None, config: SolverConfig | None = None
     cls = _sharded_problem_class()
     from .constraints import plan_codes
 
-    prob = cls(slabs, t.dims, rank, config, config.n_max, _engine_code(engine), plan, comm,
-               constraints=plan_codes(specs, t.dims, rank))
+    prob = cls(slabs, dims, rank, config, config.n_max, _engine_code(engine), plan, comm,
+               constraints=plan_codes(specs, dims, rank))
     try:
-        res = _run_fit(prob, slabs[0], t.dims, rank, config, x_norm, gather=prob.gather_state)
+        res = _run_fit(prob, slabs[0], dims, rank, config, x_norm, gather=prob.gather_state)
         comm.check_peers()
         return res
     finally:

@@ -351,7 +351,7 @@ class DeviceProblem:
         d.colmax = _ptr(self.colmax)
         d.rank = R
         d.engine = int(engine)
-        d.fuse_gram = 0 if self.sharded else 1
+        d.fuse_gram = 1  # the row update forms the Gram / column maxima of its rows (sharded: owned rows)
         d.eps_abs = float(config.eps_abs)
         d.eps_rel = float(config.eps_rel)
         d.mu = float(config.mu)

@@ -357,8 +357,19 @@ atexit.register(_release_at_exit)
 
 
 def release_plan_cache() -> None:
-    """Free the plan kept for the next same-geometry ``fit`` (see _PlanCache)."""
+    """Free the plan kept for the next same-geometry ``fit`` (see _PlanCache)
+    and return the device memory plans keep mapped in the stream-ordered
+    pool (ntf_trim_device_pool) to the device."""
     _PLAN_CACHE.release()
+    from . import _native as N
+
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            N.check(N.load().ntf_trim_device_pool())
+    except N.NativeUnavailable:  # pragma: no cover - nothing was allocated
+        pass
 
 
 def _run_fit(prob, x, dims, rank: int, config: SolverConfig, x_norm: float,

@@ -117,17 +117,16 @@ def small_fits():
 
 def c1_fixture():
     """BASELINE config c1 (100^3, R=10, fp64, 10 inner x 50 outer, 20 dB),
-    inputs from the SURVEY §8(d) generator (regenerated from seeds at test
-    time), fit with both rho^0 readings."""
+    inputs from the counter-based generator (oracle.synth_box_c, the host
+    restatement of csrc/synth.cu; regenerated at test time and checked by
+    sha256), fit with both rho^0 readings."""
     dseed = O.derive_seed(0, O.DATA_SALT, 0)
     fseed = O.derive_seed(0, O.FIT_SALT, 0)
     x, truth, sigma = O.generate((100, 100, 100), 10, 20.0, dseed)
     t = tensors.DenseTensor(x)
     st = {"data_seed": np.array(dseed), "fit_seed": np.array(fseed), "sigma": np.array(sigma),
           "x_norm": np.array(t.norm()), "x_sha256": np.array(hashlib.sha256(x.tobytes()).hexdigest())}
-    init = solver.init_state(t.dims, 10, solver.SolverConfig(seed=fseed))
-    g = (init.factors[2].T @ init.factors[2]) * (init.factors[1].T @ init.factors[1])
-    rho_tr = float(np.trace(g)) / 10
+    rho_tr = rho_trace((100, 100, 100), 10, fseed)
     for tag, rho0 in (("rho1", 1.0), ("rhotr", rho_tr)):
         cfg = solver.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=50, max_restarts=0,
                                   inner_sweeps=10, rho_init=rho0, track_factors=True)
@@ -135,6 +134,57 @@ def c1_fixture():
         pack_fit(tag, res, cfg, st, every=7)
         st[f"{tag}_rho0"] = np.array(rho0)
     np.savez_compressed(os.path.join(HERE, "c1.npz"), **st)
+
+
+def rho_trace(dims, rank, fseed):
+    """BASELINE.json's 'rho = trace(Gram)/R' from the reference's own seeded
+    initial factors (solver.init_state, solver.py:143-151)."""
+    init = solver.init_state(tuple(dims), rank, solver.SolverConfig(seed=fseed))
+    g = (init.factors[2].T @ init.factors[2]) * (init.factors[1].T @ init.factors[1])
+    return float(np.trace(g)) / rank
+
+
+# fp32 BASELINE configs (north star: final RFE within 1e-4 relative of the
+# reference) and the R=100 hard cases of SURVEY 7.3 #2 / 8(d).  The tensors
+# are the generator's fp32 values; the reference runs on them upcast to fp64
+# (SURVEY 8(d) mapping), stopping disabled, rho^0 by the trace rule.
+FP32_CASES = [
+    # name, dims, rank, snr_db, zero_frac, inner, outer
+    ("h200", (200, 200, 200), 100, 20.0, 0.0, 5, 20),
+    ("c2", (400, 400, 400), 20, 20.0, 0.0, 10, 100),
+    ("h400", (400, 400, 400), 100, 20.0, 0.0, 5, 20),
+    ("c4", (5000, 500, 200), 32, 20.0, 0.2, 10, 50),
+    ("c3", (1000, 1000, 1000), 50, 30.0, 0.0, 5, 50),
+    # c4 again with the paper's default rho^0 = 1 (SURVEY 8(d) companion run)
+    ("c4rho1", (5000, 500, 200), 32, 20.0, 0.2, 10, 50),
+]
+
+
+def fp32_fixture(name):
+    import time
+
+    (_, dims, rank, snr, zf, inner, outer), = [c for c in FP32_CASES if c[0] == name]
+    dseed = O.derive_seed(0, O.DATA_SALT, 0)
+    fseed = O.derive_seed(0, O.FIT_SALT, 0)
+    t0 = time.time()
+    x, truth, sigma = O.generate(dims, rank, snr, dseed, zf, dtype=np.float32)
+    sha = hashlib.sha256(x.tobytes()).hexdigest()
+    t = tensors.DenseTensor(x.astype(np.float64))
+    del x
+    rho0 = 1.0 if name.endswith("rho1") else rho_trace(dims, rank, fseed)
+    cfg = solver.SolverConfig(seed=fseed, eps_abs=0.0, eps_rel=0.0, n_max=outer, max_restarts=0,
+                              inner_sweeps=inner, rho_init=rho0)
+    t1 = time.time()
+    res = cpadmm.fit(t, rank, None, cfg)
+    t2 = time.time()
+    st = {"dims": np.array(dims), "rank": np.array(rank), "snr_db": np.array(snr),
+          "zero_frac": np.array(zf), "inner": np.array(inner), "outer": np.array(outer),
+          "data_seed": np.array(dseed), "fit_seed": np.array(fseed), "sigma": np.array(sigma),
+          "x_sha256": np.array(sha), "x_norm": np.array(t.norm()), "rho0": np.array(rho0),
+          "ref_fit_seconds": np.array(t2 - t1), "gen_seconds": np.array(t1 - t0)}
+    pack_fit("fit", res, cfg, st)
+    np.savez_compressed(os.path.join(HERE, f"fp32_{name}.npz"), **st)
+    print(f"{name}: rfe {res.rfe:.16f} fit {t2 - t1:.1f}s gen {t1 - t0:.1f}s", flush=True)
 
 
 CONSTRAINT_CASES = [
@@ -332,6 +382,13 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["sparse"]:
         sparse_fits()
+        sys.exit(0)
+    if sys.argv[1:] == ["c1"]:
+        c1_fixture()
+        sys.exit(0)
+    if sys.argv[1:2] == ["fp32"]:  # fp32 NAME ... (default: every FP32_CASES entry, ~30 min)
+        for name in sys.argv[2:] or [c[0] for c in FP32_CASES]:
+            fp32_fixture(name)
         sys.exit(0)
     algebra()
     small_fits()

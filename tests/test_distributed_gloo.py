@@ -66,7 +66,7 @@ class CpuShardProblem:
             self.norm_acc[10 * m: 10 * m + 10] = torch.tensor(acc, dtype=torch.float64)
             self.aux[m], self.duals[m] = a, y
 
-    def refresh_gram(self, m):
+    def sync_gram(self, m):
         pass
 
     def finalize(self):

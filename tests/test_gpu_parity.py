@@ -600,3 +600,39 @@ def test_sparse_order4_mttkrp_bitwise_and_fit():
         assert rel(res.model.factors[m], g[f"sp4_aux{m}"]) <= 1e-9
         for it in range(len(res.factor_history)):
             assert rel(res.factor_history[it][m], g[f"sp4_hist{m}"][it]) <= 1e-9
+
+
+def test_sharded_tensor_slabs_generated_per_rank(tmp_path):
+    """(f)2 slab delivery: a rank's ShardedTensor holds only its three slabs,
+    generated straight into HBM (synth.generate_box) or held in pinned host
+    memory; the one-rank sharded fit on them is bitwise the sharded fit on
+    the whole tensor, and the slabs are byte-identical to the whole tensor's
+    sub-arrays (the generator does not depend on the sharding)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1409_2383_b200 import synth
+
+    dims, R = (40, 30, 20), 5
+    spec = synth.SynthSpec.make(dims, R, 20.0, 77)
+    whole = synth.generate_box(spec, dtype="float32")
+    plan = P.PartitionPlan.uniform(dims, 1)
+    boxes = P.ShardedTensor.slab_boxes(dims, plan, 0)
+    dev = [synth.generate_box(spec, lo, hi, "float32") for lo, hi in boxes]
+    for s_, (lo, hi) in zip(dev, boxes):
+        assert torch.equal(s_, whole[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]])
+    host = [s_.cpu().pin_memory() for s_ in dev]
+    kw = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=6, max_restarts=0, inner_sweeps=2, track_factors=True)
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        ref = P.distributed_fit(whole.cpu().numpy(), R, None, P.SolverConfig(**kw), plan=1, sharded=True)
+        for slabs in (dev, host):
+            got = P.distributed_fit(P.ShardedTensor(dims, plan, 0, slabs), R, None, P.SolverConfig(**kw))
+            assert got.residual_history == ref.residual_history and got.rfe == ref.rfe
+            for a, b in zip(got.model.factors, ref.model.factors):
+                assert np.array_equal(np.asarray(a), np.asarray(b))
+        with pytest.raises(ValueError):
+            P.distributed_fit(P.ShardedTensor(dims, plan, 0, dev[:2] + [dev[0]]), R)
+    finally:
+        dist.destroy_process_group()

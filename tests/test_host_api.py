@@ -55,18 +55,62 @@ def test_partition_plan_uniform():
         P.PartitionPlan.uniform((2, 2, 2), 3)
 
 
-@pytest.mark.parametrize("name", ["c1", "c4"])
-def test_generator_matches_oracle(name):
+@pytest.mark.parametrize("name", ["c1", "c4", "c5"])
+def test_generator_host_parts_match_oracle(name):
+    """The host half of the synthetic generator (true factors, sigma, noise
+    key) equals the oracle's restatement bit for bit; sigma is a pure
+    function of the factors (exactly rounded sums, no BLAS)."""
     w = synth.CONFIGS[name]
     dims = tuple(min(d, 40) for d in w.dims)
-    a, fa = synth.generate(dims, w.rank, w.snr_db, 99, w.zero_frac, dtype=np.float64, slab_rows=3)
-    b, fb, _ = O.generate(dims, w.rank, w.snr_db, 99, w.zero_frac)
-    assert np.array_equal(a, b)
+    fa = synth.true_factors(dims, w.rank, 99, w.zero_frac)
+    fb = O.true_factors(dims, w.rank, 99, w.zero_frac)
     for x, y in zip(fa, fb):
         assert np.array_equal(x, y)
+    assert synth.noise_sigma(fa, w.snr_db) == O.noise_sigma(fb, w.snr_db)
+    for seed in (0, 99, synth.seeds()[0], 2**64 - 1):
+        assert synth.synth_key(seed) == O.synth_key(seed)
+    spec = synth.SynthSpec.of(synth.Workload("t", dims, w.rank, w.dtype, w.snr_db, 1, 1, w.zero_frac), 99)
+    assert spec.sigma == O.noise_sigma(fb, w.snr_db) and spec.key == O.synth_key(99)
     if w.zero_frac:
         frac = np.mean(np.concatenate([f.ravel() for f in fa]) == 0.0)
         assert 0.15 < frac < 0.25
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_generator_restatements_agree(dtype):
+    """The oracle's two restatements of the counter-based generator (numpy and
+    C) agree byte for byte on whole tensors and on boxes of them, and a box is
+    the same bytes as the whole tensor's sub-array (sharding-independent)."""
+    dims, R = (11, 13, 37), 6
+    truth = O.true_factors(dims, R, 4, 0.2)
+    sigma, key = O.noise_sigma(truth, 20.0), O.synth_key(4)
+    whole = O.synth_box(truth, dims, (0, 0, 0), dims, sigma, key, dtype)
+    assert np.array_equal(whole, O.synth_box_c(truth, dims, (0, 0, 0), dims, sigma, key, dtype))
+    for lo, hi in (((3, 0, 0), (7, 13, 37)), ((0, 5, 0), (11, 9, 37)), ((0, 0, 30), (11, 13, 37)),
+                   ((10, 12, 36), (11, 13, 37))):
+        box = O.synth_box_c(truth, dims, lo, hi, sigma, key, dtype)
+        assert np.array_equal(box, whole[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]])
+        assert np.array_equal(box, O.synth_box(truth, dims, lo, hi, sigma, key, dtype))
+
+
+def test_generator_noise_is_standard_normal():
+    """The polynomial Box-Muller equals the libm one to ~1e-15 and its
+    moments are those of N(0, 1)."""
+    import math
+
+    key = O.synth_key(7)
+    e = np.arange(400000, dtype=np.uint64)
+    z = O.synth_std_normal(key, e)
+    k = np.uint64(key)
+    with np.errstate(over="ignore"):
+        w1 = O._mix64(k + (np.uint64(2) * e + np.uint64(1)) * O._GAMMA)
+        w2 = O._mix64(k + (np.uint64(2) * e + np.uint64(2)) * O._GAMMA)
+    u1 = ((w1 >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+    u2 = (w2 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    zz = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * u2)
+    assert np.max(np.abs(z - zz)) <= 1e-13
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1.0) < 0.01
+    assert abs(np.mean(z ** 4) - 3.0) < 0.05
 
 
 def test_dense_tensor_dtypes():
@@ -122,3 +166,23 @@ def test_peer_rows_validates_blocks_before_any_cuda_call():
         _PeerRows(comm, full, [0, 6], [5, 4])
     with pytest.raises(ValueError, match="cover"):
         _PeerRows(comm, full, [0, 5], [5, 4])
+
+
+def test_sharded_tensor_boxes_and_validation():
+    """ShardedTensor (one rank's three slabs): the slab boxes
+    follow the uniform row plan, and slabs of the wrong shape or mixed dtypes
+    are rejected before any device work."""
+    import torch
+
+    plan = P.PartitionPlan.uniform((10, 7, 8), 3)
+    boxes = P.ShardedTensor.slab_boxes((10, 7, 8), plan, 1)
+    assert boxes == [((4, 0, 0), (7, 7, 8)), ((0, 3, 0), (10, 5, 8)), ((0, 0, 3), (10, 7, 6))]
+    x = torch.arange(560, dtype=torch.float32).reshape(10, 7, 8)
+    slabs = [x[4:7].contiguous(), x[:, 3:5].contiguous(), x[:, :, 3:6].contiguous()]
+    P.ShardedTensor((10, 7, 8), plan, 1, slabs).validate()
+    with pytest.raises(ValueError, match="does not match"):
+        P.ShardedTensor((10, 7, 8), plan, 0, slabs).validate()
+    with pytest.raises(ValueError, match="one dtype"):
+        P.ShardedTensor((10, 7, 8), plan, 1, [slabs[0], slabs[1].double(), slabs[2]]).validate()
+    with pytest.raises(ValueError, match="plan and dims"):
+        P.ShardedTensor((10, 7, 9), plan, 1, slabs).validate()

@@ -2,12 +2,15 @@
 ``ntf_peer_gather``), the sharded engine's exchange after every block-row mode
 update (reference blocks.py:171-196, mesh.py:149-237).
 
-One GPU is available, so a second rank is never run concurrently (its kernel
-would wait on ours).  Instead the other rank's side of the protocol -- its rows
-in our staging buffer and its CTAs' arrivals on our counter -- is written by
-the test before our kernel runs, and our pushes into its buffer are checked
-afterwards.  Both peer buffers are local allocations here; the kernel takes
-any device pointers (CUDA IPC mappings in a real multi-GPU run).
+One GPU is available.  Ranks that spin on one another must not run as
+separate launches on one GPU (nothing makes them co-resident; B200_PROFILING.md
+records Xid 109 from exactly that), so the protocol is exercised two ways:
+(1) one rank's kernel with the other rank's side -- its rows in our staging
+buffer and its CTAs' arrivals on our counter -- written by the test before
+our kernel runs, and (2) every rank live at once, all ranks' gathers in ONE
+cooperative launch (``ntf_peer_gather_group``).  The peer buffers are local
+allocations here; the kernel takes any device pointers (CUDA IPC mappings in
+a real multi-GPU run).
 """
 
 import numpy as np
@@ -147,3 +150,85 @@ def test_sharded_fit_peer_path_equals_nccl_path(golden_small, tmp_path, monkeypa
         assert p2p.rfe == nccl.rfe
     finally:
         dist.destroy_process_group()
+
+
+def _group_descs(lib, P, rows, R, ctas, offs, timeout_ns=int(5e9)):
+    nb = lib.ntf_peer_buffer_bytes(rows, R)
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(P)]
+    fulls = [torch.full((rows, R), float("nan"), dtype=torch.float64, device="cuda") for _ in range(P)]
+    status = torch.zeros(P, dtype=torch.int32, device="cuda")
+    descs = (_native.PeerGatherDesc * P)()
+    for q in range(P):
+        d = descs[q]
+        d.nranks, d.me, d.R, d.ctas = P, q, R, ctas
+        for r, o in enumerate(offs):
+            d.row_offset[r] = o
+        d.full = fulls[q].data_ptr()
+        for r in range(P):
+            d.peer_base[r] = bufs[r].data_ptr()
+        d.status = status.data_ptr() + 4 * q
+        d.timeout_ns = timeout_ns
+    return descs, bufs, fulls, status
+
+
+@pytest.mark.parametrize("P,rows,R,ctas", [(2, 37, 5, 3), (3, 400, 20, 2), (4, 2001, 100, 8),
+                                          (8, 1000, 1, 1), (8, 3, 7, 2), (5, 123, 33, 4)])
+def test_peer_gather_all_ranks_live(P, rows, R, ctas):
+    """The protocol with every rank live at once: all P ranks' gathers run as
+    ONE cooperative launch on the one GPU (ntf_peer_gather_group; ranks that
+    spin on one another may not be separate launches on one device).  Uneven
+    row blocks (empty ones too when rows < P), odd R, several CTAs per rank,
+    eight consecutive gathers (both staging parities, reuse): every rank ends
+    each gather with the whole factor, bitwise, and the counters agree."""
+    lib = _native.load()
+    ext = [rows // P + (1 if q < rows % P else 0) for q in range(P)]
+    offs = [0]
+    for e in ext:
+        offs.append(offs[-1] + e)
+    descs, bufs, fulls, status = _group_descs(lib, P, rows, R, ctas, offs)
+    g = torch.Generator(device="cuda").manual_seed(P * 1000 + rows)
+    s = torch.cuda.current_stream().cuda_stream
+    for it in range(8):
+        want = torch.rand(rows, R, dtype=torch.float64, device="cuda", generator=g)
+        for q in range(P):
+            fulls[q].fill_(float("nan"))
+            fulls[q][offs[q]:offs[q + 1]] = want[offs[q]:offs[q + 1]]
+        _native.check(lib.ntf_peer_gather_group(descs, P, s))
+        torch.cuda.synchronize()
+        assert int(status.abs().sum().item()) == 0
+        for q in range(P):
+            assert torch.equal(fulls[q], want), (it, q)
+            hdr = bufs[q][:HDR].view(torch.int32)
+            assert int(hdr[0].item()) == P * ctas * (it + 1)   # arrivals of every rank's CTAs
+            assert int(hdr[16].item()) == it + 1               # sequence advanced once per gather
+
+
+def test_peer_gather_status_set_makes_gathers_noops():
+    """After a timeout (status word set) a gather pushes nothing, arrives
+    nowhere and leaves the sequence alone, so a rank that fell out of step
+    cannot write into a staging parity its peers read."""
+    lib = _native.load()
+    P, rows, R, ctas = 2, 40, 4, 2
+    descs, bufs, fulls, status = _group_descs(lib, P, rows, R, ctas, [0, 20, 40])
+    status[0] = _native.NTF_PEER_TIMEOUT
+    status[1] = _native.NTF_PEER_TIMEOUT
+    for q in range(P):
+        fulls[q].fill_(float(q + 1))
+    _native.check(lib.ntf_peer_gather_group(descs, P, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    for q in range(P):
+        hdr = bufs[q][:HDR].view(torch.int32)
+        assert int(hdr[0].item()) == 0 and int(hdr[16].item()) == 0
+        assert torch.all(bufs[q][HDR:] == 0)
+        assert torch.all(fulls[q] == float(q + 1))
+
+
+def test_peer_gather_rejects_non_coresident_ctas():
+    """ctas beyond what the device keeps co-resident are rejected (the CTAs
+    spin on one another's arrivals)."""
+    lib = _native.load()
+    descs, _, _, _ = _group_descs(lib, 2, 64, 4, 1, [0, 32, 64])
+    for q in range(2):
+        descs[q].ctas = 100000
+    with pytest.raises(ValueError):
+        _native.check(lib.ntf_peer_gather_group(descs, 2, torch.cuda.current_stream().cuda_stream))

@@ -1,6 +1,8 @@
 """Time the dense MTTKRP alone (each mode) at a BASELINE config; ncu target."""
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _variant  # noqa: F401,E402  (NTF_VARIANT_LIB)
 import numpy as np
 import torch
 from paper_1409_2383_b200 import synth

@@ -2,6 +2,8 @@
 debug variants with garbage math cannot trip the stop flag)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _variant  # noqa: F401,E402  (NTF_VARIANT_LIB)
 import numpy as np
 import torch
 import paper_1409_2383_b200 as P
