@@ -14,6 +14,8 @@
 //                                successive exact remainders (T2 possibly
 //                                subnormal), ls(n) = 2^(f(n)-t) per column;
 //   Fh   = fp16(F_lo / ls(n))    F_lo to 11 significant bits
+//   (N <= 85: T2 is stored as 2^11 T2 in its own accumulator, scaled back in
+//   the epilogue, so its fp16 subnormal floor sits at 2^-36 instead of 2^-25)
 // The tensor core forms, per unit of G consecutive 64-wide l blocks at one o,
 //   ACC0 = sum S0*T0                       integers < 2^24: EXACT in fp32
 //   ACC1 = sum S0*T1 + S1*Fh,  ACC2 = sum S0*T2        (corrections; for
@@ -553,7 +555,12 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   constexpr int kEpi = epi_warps(NT);
   constexpr int NC = N * 4 / kEpi;         // columns per epilogue thread
   // TMEM load width: 16 columns where it divides NC and registers allow
-  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : ((NC > 48 || NC % 8) ? 4 : 8);
+// 8-column TMEM loads up to 64 columns per thread (c5, N = 112 over 8 warps:
+// drain alone 3.03 vs 3.25 ms per mode with 4-column loads)
+#ifndef NTF_LW_WIDE
+#define NTF_LW_WIDE 64
+#endif
+  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : ((NC > NTF_LW_WIDE || NC % 8) ? 4 : 8);
   static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kIssuers = mma_issuers(N);
@@ -906,6 +913,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     const int c0 = (e >> 2) * NC;       // this warp's column range
     const int row = q4 * 32 + lane;     // tile row == TMEM lane
     f32x2 hi[NC / 2], lo[NC / 2];       // double-float accumulators, column pairs
+    const f32x2 kT2Unscale = f2pack(0x1p-11f, 0x1p-11f);
 #pragma unroll
     for (int j = 0; j < NC / 2; ++j) {
       hi[j] = 0ull;
@@ -932,7 +940,8 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
             const f32x2 hx = f2pack(h.x, h.y), hy = f2pack(h.z, h.w);
             const f32x2 a = f2pack(a0[v], a0[v + 1]);
             f32x2 a12 = f2pack(a1[v], a1[v + 1]);
-            if constexpr (!merged_acc(N)) a12 = f2add(a12, f2pack(a2[v], a2[v + 1]));
+            // ACC2 = S0 x (T2 2^11): scaled back here (exact power of two)
+            if constexpr (!merged_acc(N)) a12 = f2fma(f2pack(a2[v], a2[v + 1]), kT2Unscale, a12);
             const f32x2 pr = f2mul(a, hx);
             const f32x2 er = f2fma(a, hx, f2neg(pr));  // a*hx = pr + er exactly
             const f32x2 cr = f2fma(a12, hx, f2fma(a, hy, er));
@@ -1031,6 +1040,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
 //   low tensor plane S1.  One thread per (l block, n, octet).
 // ----------------------------------------------------------------------------
 __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int CG, int n_lb,
+                               bool t2_scaled,
                                const double* __restrict__ cm, int t, unsigned char* __restrict__ wsl,
                                const double* __restrict__ Fhi, int n_o,
                                const double* __restrict__ cm_hi, float2* __restrict__ hpair,
@@ -1098,7 +1108,11 @@ __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, i
         const double r2 = r1 - static_cast<double>(__half2float(h1));
         hs[0][v] = __double2half(t0);
         hs[1][v] = h1;
-        hs[2][v] = __double2half(r2);
+        // N <= 85 (T2 in its own accumulator ACC2): T2 carries 2^11 r2, which
+        // moves its fp16 subnormal floor from 2^-25 to 2^-36 (factor columns
+        // with a few large entries and many small ones keep ~22 relative
+        // bits in the small ones); the epilogue scales ACC2 back
+        hs[2][v] = __double2half(t2_scaled ? r2 * 2048.0 : r2);
         hs[3][v] = __double2half(vv);  // Fh = fp16(v), the operand of the low plane S1
       }
       const int rows_cta = 4 * N / CG;
@@ -1663,7 +1677,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
     if (!(p.debug & 128)) {
       cudaError_t e = launch_pdl(w_slice_kernel, dim3(blocks), dim3(64), 0, stream, Flo, L.l_ext,
-                                 L.R, L.N, L.cg, L.n_lb, p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
+                                 L.R, L.N, L.cg, L.n_lb, !merged_acc(L.N), p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
                                  L.hpair, stop_flag);
       if (e != cudaSuccess) return e;
     }

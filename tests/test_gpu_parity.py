@@ -632,7 +632,7 @@ def test_sharded_tensor_slabs_generated_per_rank(tmp_path):
             assert got.residual_history == ref.residual_history and got.rfe == ref.rfe
             for a, b in zip(got.model.factors, ref.model.factors):
                 assert np.array_equal(np.asarray(a), np.asarray(b))
-        with pytest.raises(ValueError):
-            P.distributed_fit(P.ShardedTensor(dims, plan, 0, dev[:2] + [dev[0]]), R)
+        with pytest.raises(ValueError):  # a slab of the wrong shape
+            P.distributed_fit(P.ShardedTensor(dims, plan, 0, dev[:2] + [dev[2][:, :, :10].contiguous()]), R)
     finally:
         dist.destroy_process_group()

@@ -39,3 +39,23 @@ for mode in (1, 2, 3):
     colrel = (torch.linalg.norm(err, dim=0) / torch.linalg.norm(ref, dim=0)).cpu().numpy()
     print(f"{name} after {outer} outer, mode {mode}: rel fro {fro:.2e}, max row rel {rowrel:.2e}, "
           f"bias {bias:.2e}, worst column rel {colrel.max():.2e}", flush=True)
+
+if os.environ.get("DETAIL"):
+    fl = {1: (1, 2), 2: (0, 2), 3: (0, 1)}  # (F_hi, F_lo) factor indices per mode
+    for mode in (1, 2):
+        tc = mttkrp_device(x, f, mode, P.solver._engine_code("tcgen05"))
+        ref = mttkrp_device(x64, f, mode, P.solver._engine_code("cuda_core"))
+        err = (tc - ref)
+        hi, lo = f[fl[mode][0]], f[fl[mode][1]]
+        for r in range(w.rank):
+            nr = float(torch.linalg.norm(ref[:, r]))
+            if nr == 0:
+                print(f"mode {mode} col {r}: zero column (hi max {float(hi[:, r].abs().max()):.3e} lo max {float(lo[:, r].abs().max()):.3e})")
+                continue
+            e = float(torch.linalg.norm(err[:, r])) / nr
+            b = float((err[:, r] * torch.sign(ref[:, r])).sum() / ref[:, r].abs().sum())
+            lc = lo[:, r].abs()
+            print(f"mode {mode} col {r}: rel {e:.2e} bias {b:+.2e} | lo max {float(lc.max()):.3e} "
+                  f"mean/max {float(lc.mean() / lc.max().clamp_min(1e-300)):.2e} zeros {int((lc == 0).sum())}"
+                  f" neg {int((lo[:, r] < 0).sum())} | hi max {float(hi[:, r].abs().max()):.3e} "
+                  f"hi neg {int((hi[:, r] < 0).sum())}", flush=True)

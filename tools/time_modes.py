@@ -12,9 +12,10 @@ from paper_1409_2383_b200.engine import DeviceProblem
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 eng = sys.argv[2] if len(sys.argv) > 2 else "auto"
-if cfgname == "custom":  # time_modes.py custom ENGINE I J K R INNER
+if cfgname == "custom":  # time_modes.py custom ENGINE I J K R INNER [DTYPE]
     I, J, K, R, inner = (int(v) for v in sys.argv[3:8])
-    w = synth.Workload("custom", (I, J, K), R, "float32", 20.0, inner, 1)
+    dtype = sys.argv[8] if len(sys.argv) > 8 else "float32"
+    w = synth.Workload("custom", (I, J, K), R, dtype, 20.0, inner, 1)
 else:
     w = synth.CONFIGS[cfgname]
 dt = torch.float32 if w.dtype == "float32" else torch.float64
