@@ -453,8 +453,8 @@ def main():
         # Gram reduction (side stream); per step: 3 norm reductions + finalize
         tc = w.dtype == "float32" and args.engine != "cuda_core"
         launches_per_step = w.inner * 3 * (4 + (1 if tc else 0)) + 3 + 1
-        if sharded:  # + Gram refresh (partial + reduce) and column maxima per mode update
-            launches_per_step += w.inner * 3 * 3
+        if sharded and world > 1 and os.environ.get("NTF_B200_P2P", "0") in ("1", "force"):
+            launches_per_step += w.inner * 3  # + the peer row-gather kernel per mode update
         out = {
             "metric": "ntf_outer_iters_per_sec", "value": value, "unit": "outer_it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
