@@ -589,8 +589,6 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   uint64_t* acc_empty = acc_full + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 4);
   uint32_t* stop_slot = tmem_slot + 1;
-  // per-column scales, written by warp 2 after pdl_wait (see there)
-  double* wsc = reinterpret_cast<double*>(acc_empty + 6);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0: the pair's leader (issues the MMAs)
@@ -853,21 +851,6 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // Everything from here on reads what the preceding kernels produced
     // (w_slice_kernel formed both the W slices and the F_hi pair table).
     pdl_wait();
-    // per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
-    // max|F_hi[:,n]| < 2^e (the same clamps as w_slice_kernel)
-    for (int n = lane; n < N; n += 32) {
-      const int t = t_bits(G);
-      int f = 0, e = 0;
-      const double cl = n < R ? p.cm_lo[n] : 0.0, ch = n < R ? p.cm_hi[n] : 0.0;
-      if (cl > 0.0) frexp(cl, &f);
-      if (ch > 0.0) frexp(ch, &e);
-      // columns decayed to ~1e-300 (large penalties shrink factor columns
-      // geometrically) must not overflow the scales (2^(t+22-f) in the slice
-      // kernel): clamp, identically there (kFMin)
-      f = max(f, kFMin);
-      e = max(e, kFMin);
-      wsc[2 * N + n] = *p.xscale * ldexp(1.0, f - t + e);
-    }
     // this mode's column maxima are re-accumulated by the row update that follows
     if (blockIdx.x == 0 && p.cm_self)
       for (int n = lane; n < R; n += 32) p.cm_self[n] = 0.0;
@@ -968,6 +951,23 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // (a thread's own row is R doubles apart from its neighbours').
     const int rows_valid = static_cast<int>(p.M - m0 < p.tm ? p.M - m0 : p.tm);
     double* out0 = p.ws + (static_cast<int64_t>(split) * p.M + m0) * R;
+    // per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
+    // max|F_hi[:,n]| < 2^e (the clamps of w_slice_kernel).  Read here, after
+    // this thread's own wait on the preceding kernel (a CTA with no unit never
+    // synchronises with the W-loading warp, so the scales are not handed over
+    // through shared memory).
+    pdl_wait();
+    const double xs = *p.xscale;
+    const int tb = t_bits(G);
+    auto col_scale = [&](int n) {
+      int f = 0, e = 0;
+      const double cl = p.cm_lo[n], ch = p.cm_hi[n];
+      if (cl > 0.0) frexp(cl, &f);
+      if (ch > 0.0) frexp(ch, &e);
+      // columns decayed to ~1e-300 (large penalties shrink factor columns
+      // geometrically) must not overflow the scales: clamp as the slicer (kFMin)
+      return xs * ldexp(1.0, max(f, kFMin) - tb + max(e, kFMin));
+    };
     float hf[NC], lf[NC];
 #pragma unroll
     for (int j = 0; j < NC / 2; ++j) {
@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
         for (int j = 0; j < NC; ++j) {
           const int n = c0 + j;
           if (n < R)
-            stage[row * R + n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * wsc[2 * N + n];
+            stage[row * R + n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * col_scale(n);
         }
       }
       asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
@@ -993,7 +993,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       for (int j = 0; j < NC; ++j) {
         const int n = c0 + j;
         if (n < R)
-          out[n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * wsc[2 * N + n];
+          out[n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * col_scale(n);
       }
     }
   }
@@ -1296,7 +1296,10 @@ cudaError_t dispatch_tc(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
 // for its accumulator drain and handshakes, which grows with N.
 void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
   const int64_t units = static_cast<int64_t>(L.n_g) * L.n_o;
-  double unit_fixed = 2.0 + L.N / 32.0;  // measured: c2 best near 3, R = 64..100 near 4..6
+  // measured, single CTAs: c2 best near 3, R = 64..100 near 4..6; CTA pairs (the
+  // unit's drain is spread over two SMs): c5 7.35 / 7.43 / 7.69 ms per mode at
+  // 2.5 / 4 / 5.5, c2 and c3 flat
+  double unit_fixed = L.cg == 2 ? 2.5 : 2.0 + L.N / 32.0;
   if (const char* e = diag_env("NTF_TC_UNITCOST")) unit_fixed = atof(e);
   auto cost = [&](int g) {
     const int nl = std::min(L.G, L.n_lb - g * L.G);
@@ -1365,7 +1368,11 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   // CTA pairs (tcgen05 cta_group::2, M = 256 over two SMs of a TPC): each
   // CTA keeps only half of the W slices resident, so a unit (one TMEM
   // drain) spans more l blocks, and one MMA instruction serves both SMs.
-  L.cg = 2;
+  // Below ~1 GB of tensor per mode the pair kernel's longer prologue (cluster
+  // barrier, 2-CTA tensor maps) is not hidden behind the previous kernel
+  // (outer iteration, graph replay: c2 1.65 ms single vs 1.90 ms pairs; c4
+  // 10.50 vs 10.25, c3 12.2 vs 10.5, c5 137.8 vs 114.2).
+  L.cg = L.M * L.Q >= (int64_t(1) << 28) ? 2 : 1;
   if (const char* e = diag_env("NTF_TC_CG")) L.cg = atoi(e) == 1 ? 1 : 2;
   // Equal m-tiles of tm <= 128 rows (a multiple of 8, the core-matrix
   // height), so every CTA of a full tile streams the same bytes.  Pairs

@@ -144,9 +144,23 @@ def _gather_worker(rank, world, port, out_path):
         full[o:o + c] = torch.arange(o * 3, (o + c) * 3, dtype=torch.float64).reshape(c, 3)
         comm = Comm()
         comm.gather_rows(full, offs, cnts)
-        # CPU tensors: the NVLink peer-memory path is never selected (every
-        # rank decides alike, without a collective)
+        # a tagged (persistent) target takes the same path on CPU tensors: the
+        # NVLink peer-memory kernel is never selected (every rank decides
+        # alike, without a collective)
+        full2 = full.clone()
+        full2[[i for i in range(11) if not o <= i < o + c]] = -1.0
+        comm.gather_rows(full2, offs, cnts, tag=("factor", 0))
+        assert torch.equal(full2, full)
         assert comm.peer_ok(full.device) is False and not getattr(comm, "_peers", {})
+        assert comm.peer_failed() is False
+        # the sharded Gram / column-maxima closure (ShardedProblem.sync_gram):
+        # one sum and one max over the ranks, the same bits on every rank
+        g = torch.full((3, 3), float(rank + 1), dtype=torch.float64)
+        cm = torch.tensor([rank, 10.0 - rank, 0.5], dtype=torch.float64)
+        comm.all_reduce_(g)
+        comm.all_reduce_max_(cm)
+        assert torch.all(g == sum(range(1, world + 1)))
+        assert cm.tolist() == [world - 1.0, 10.0, 0.5]
         if rank == 0:
             np.save(out_path, full.numpy())
     finally:
