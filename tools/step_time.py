@@ -34,4 +34,15 @@ e0.record(prob.stream)
 prob.run(steps)
 e1.record(prob.stream)
 torch.cuda.synchronize()
-print(f"{name} {os.environ.get('NTF_TC_CG', 'default')}: {e0.elapsed_time(e1) / steps:.4f} ms/step", flush=True)
+plain = e0.elapsed_time(e1) / steps
+prob.set_timing(True)
+prob.run(1)
+e0.record(prob.stream)
+prob.run(1)
+e1.record(prob.stream)
+torch.cuda.synchronize()
+kt = prob.kernel_times()
+prob.set_timing(False)
+print(f"{name} {os.environ.get('NTF_TC_CG', 'default')}: {plain:.4f} ms/step; instrumented step "
+      f"{e0.elapsed_time(e1):.4f} ms, mttkrp {kt[:, 0].mean() * 1e3:.2f} us, row update {kt[:, 1].mean() * 1e3:.2f} us "
+      f"(x{len(kt)})", flush=True)
