@@ -42,7 +42,7 @@ int check_dims(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
   if (mode < 1 || mode > 3) return fail(NTF_ERR_INVALID, "mode must be 1..3");
   if (x_dtype != NTF_F32 && x_dtype != NTF_F64) return fail(NTF_ERR_INVALID, "bad dtype");
   if (I < 1 || J < 1 || K < 1) return fail(NTF_ERR_INVALID, "all extents must be >= 1");
-  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
+  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..256 (NTF_MAX_RANK)");
   const int64_t Q = mode == 1 ? J * K : (mode == 2 ? I * K : I * J);
   if (Q >= (int64_t(1) << 31)) return fail(NTF_ERR_UNSUPPORTED, "reduction length >= 2^31");
   return NTF_OK;
@@ -429,7 +429,7 @@ int ntf_mttkrp_coo(int order, const int64_t* dims, int mode, int64_t nnz, const 
   if (!dims || !factors || nnz < 0) return fail(NTF_ERR_INVALID, "bad shape");
   for (int m = 0; m < order; ++m)
     if (dims[m] < 1) return fail(NTF_ERR_INVALID, "bad shape");
-  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
+  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..256 (NTF_MAX_RANK)");
   if (!out || !rowptr || (nnz > 0 && (!idx || !vals || (mode > 1 && !perm))))
     return fail(NTF_ERR_INVALID, "null pointer");
   for (int m = 0; m < order; ++m)
@@ -513,7 +513,7 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   *out = nullptr;
   const ntf_plan_desc& d = *desc;
   const int R = d.rank;
-  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..128");
+  if (R < 1 || R > NTF_MAX_RANK) return fail(NTF_ERR_UNSUPPORTED, "rank must be in 1..256 (NTF_MAX_RANK)");
   if (d.inner_sweeps < 1) return fail(NTF_ERR_INVALID, "inner_sweeps must be >= 1");
   if (d.norm_all && d.norm_parts < 1) return fail(NTF_ERR_INVALID, "norm_parts must be >= 1");
   if (!d.rho || !d.norm_acc || !d.counters || !d.resid_history || !d.rho_history || !d.colmax)

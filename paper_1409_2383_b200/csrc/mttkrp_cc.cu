@@ -45,6 +45,7 @@ namespace {
 constexpr int kBQ = 32;
 constexpr int kStages = 3;
 constexpr int kClusterSplits = 8;
+constexpr int kColChunk = 128;  // output columns per CTA (8 warps x TR = 16)
 
 __device__ __forceinline__ void fast_two_sum_acc(float& hi, float& lo, float a) {
   // (hi, lo) += a with Fast2Sum: exact when |hi| >= |a|, which holds after the
@@ -74,7 +75,11 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // stage s: [X tile | hi rows (max_hi x R2 doubles) | lo rows (BQ x R2)]
-  const int R = p.R;
+  // Column chunk blockIdx.z: columns [c0, c0 + R) of the R_full-column
+  // factors and output (ranks above kColChunk; one chunk otherwise).
+  const int R_full = p.R;
+  const int c0 = static_cast<int>(blockIdx.z) * kColChunk;
+  const int R = R_full - c0 < kColChunk ? R_full - c0 : kColChunk;
   const int R2 = (R + 1) & ~1;
   const int R_pad = p.R_pad;
   unsigned char* stage_base = smem_raw;
@@ -161,7 +166,9 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
     const uint32_t l0 = q0 - h0 * L;
     double* hs = hi_rows(s);
     double* ls = lo_rows(s);
-    if ((R & 1) == 0) {
+    const double* Fhi = p.Fhi + c0;
+    const double* Flo = p.Flo + c0;
+    if (((R | R_full) & 1) == 0) {
       const int vpr = R >> 1;  // 16-byte vectors per row
       const int nh = p.max_hi * vpr;
       for (int e = tid; e < nh + kBQ * vpr; e += nthreads) {
@@ -169,14 +176,14 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
           const int row = e / vpr, v = e - (e / vpr) * vpr;
           const uint32_t h = h0 + row;
           const bool valid = h < p.hi_extent;
-          cp_async_cg16(hs + row * R2 + 2 * v, valid ? p.Fhi + static_cast<int64_t>(h) * R + 2 * v : p.Fhi,
+          cp_async_cg16(hs + row * R2 + 2 * v, valid ? Fhi + static_cast<int64_t>(h) * R_full + 2 * v : Fhi,
                         valid);
         } else {
           const int e2 = e - nh;
           const int qq = e2 / vpr, v = e2 - (e2 / vpr) * vpr;
           uint32_t lo = l0 + qq;
           lo = L >= kBQ ? (lo >= L ? lo - L : lo) : lo % L;
-          cp_async_cg16(ls + qq * R2 + 2 * v, p.Flo + static_cast<int64_t>(lo) * R + 2 * v, true);
+          cp_async_cg16(ls + qq * R2 + 2 * v, Flo + static_cast<int64_t>(lo) * R_full + 2 * v, true);
         }
       }
     } else {
@@ -186,13 +193,13 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
           const int row = e / R, r = e - (e / R) * R;
           const uint32_t h = h0 + row;
           const bool valid = h < p.hi_extent;
-          cp_async_ca<8>(hs + row * R2 + r, valid ? p.Fhi + static_cast<int64_t>(h) * R + r : p.Fhi,
+          cp_async_ca<8>(hs + row * R2 + r, valid ? Fhi + static_cast<int64_t>(h) * R_full + r : Fhi,
                          valid);
         } else {
           const int e2 = e - nh;
           const int qq = e2 / R, r = e2 - (e2 / R) * R;
           const uint32_t lo = (l0 + qq) % L;
-          cp_async_ca<8>(ls + qq * R2 + r, p.Flo + static_cast<int64_t>(lo) * R + r, true);
+          cp_async_ca<8>(ls + qq * R2 + r, Flo + static_cast<int64_t>(lo) * R_full + r, true);
         }
       }
     }
@@ -356,7 +363,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
   const int crank = static_cast<int>(cluster.block_rank());
   const int rows_per = BM / cs;
   const int64_t group = split / cs;
-  double* out = p.ws + group * p.M * R;
+  double* out = p.ws + group * p.M * R_full + c0;
   for (int e = tid; e < rows_per * R; e += nthreads) {
     const int lm = crank * rows_per + e / R;
     const int r = e - (e / R) * R;
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
       s += rp[lm * R + r];
     }
     const int64_t gm = m0 + lm;
-    if (gm < p.M) out[gm * R + r] = s;
+    if (gm < p.M) out[gm * R_full + r] = s;
   }
   cluster.sync();
 }
@@ -409,7 +416,7 @@ cudaError_t launch_variant(const MttkrpCCParams& p, const MttkrpCCLaunch& L, cud
     return cudaOccupancyMaxActiveClusters(&g_active_clusters, kern, &q);
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(L.n_mtiles, L.splits, 1);
+  cfg.gridDim = dim3(L.n_mtiles, L.splits, L.col_chunks);
   cfg.blockDim = dim3(L.threads, 1, 1);
   cfg.dynamicSmemBytes = L.smem_bytes;
   cfg.stream = stream;
@@ -499,8 +506,12 @@ void fill_params(MttkrpCCParams& p, int mode, const void* X, int64_t I, int64_t 
 // ---------------------------------------------------------------------------
 // host side: geometry and dispatch
 // ---------------------------------------------------------------------------
-MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R) {
+MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64_t K, int R_full) {
   MttkrpCCLaunch L{};
+  // ranks above kColChunk: one grid z-slice per 128-column chunk (each
+  // streams X again); the geometry below is that of one chunk
+  L.col_chunks = (R_full + kColChunk - 1) / kColChunk;
+  const int R = R_full < kColChunk ? R_full : kColChunk;
   const bool f32 = x_dtype == NTF_F32;
   const int esz = f32 ? 4 : 8;
   const int VW = 16 / esz;

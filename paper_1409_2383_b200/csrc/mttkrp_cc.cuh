@@ -17,7 +17,7 @@ struct MttkrpCCParams {
   const double* Fhi;    // KR slow factor (indexed by q / lo_extent)
   const double* Flo;    // KR fast factor (indexed by q % lo_extent)
   uint32_t lo_extent, hi_extent;
-  int R, R_pad;
+  int R, R_pad;         // R: all columns (factor / output row stride); R_pad: of one 128-column chunk
   int64_t n_chunks, chunks_per_split;
   int stage_bytes, max_hi;
   double* ws;           // [groups][M][R] fp64 partials (one per cluster)
@@ -25,7 +25,8 @@ struct MttkrpCCParams {
 };
 
 struct MttkrpCCLaunch {
-  int TM, TR, R_pad, threads;
+  int TM, TR, R_pad, threads;  // of one column chunk (<= 128 columns)
+  int col_chunks;               // ceil(R / 128): grid z
   int n_mtiles, splits, cluster, groups;
   int64_t M, Q, n_chunks, chunks_per_split;
   int stage_bytes, max_hi, smem_bytes;

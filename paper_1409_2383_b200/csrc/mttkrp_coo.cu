@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(kCooWarps * 32) mttkrp_coo_kernel(CooView t, i
   const double* F1 = F.f[c1];
   const double* F2 = N == 4 ? F.f[c2] : nullptr;
   const int lane = threadIdx.x & 31;
+  const int cb = static_cast<int>(blockIdx.y) * 128;  // column chunk (ranks above 128)
   const int64_t row = static_cast<int64_t>(blockIdx.x) * kCooWarps + (threadIdx.x >> 5);
   if (row >= t.dims[m]) return;
   const int64_t* perm = t.perm[m];
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(kCooWarps * 32) mttkrp_coo_kernel(CooView t, i
     const double v = t.vals[q];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int r = lane + 32 * u;
+      const int r = cb + lane + 32 * u;
       if (r < R) {  // explicit rounding: no FMA contraction, as numpy's multiply-then-add
         double p = __dmul_rn(F0[i0 * R + r], F1[i1 * R + r]);
         if (F2) p = __dmul_rn(p, F2[i2 * R + r]);
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kCooWarps * 32) mttkrp_coo_kernel(CooView t, i
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int r = lane + 32 * u;
+    const int r = cb + lane + 32 * u;
     if (r < R) out[row * R + r] = acc[u];
   }
 }
@@ -144,13 +145,13 @@ cudaError_t mttkrp_coo_launch(const CooView& t_in, int mode, const double* const
                               double* out, const int* stop_flag, cudaStream_t stream) {
   CooView t = t_in;
   if (t.order == 0) t.order = 3;
-  if (R < 1 || R > 128 || mode < 1 || mode > t.order) return cudaErrorInvalidValue;
+  if (R < 1 || R > NTF_MAX_RANK || mode < 1 || mode > t.order) return cudaErrorInvalidValue;
   Factors f{};
   for (int m = 0; m < t.order; ++m) f.f[m] = F[m];
   const int64_t rows = t.dims[mode - 1];
   const unsigned blocks = static_cast<unsigned>((rows + kCooWarps - 1) / kCooWarps);
-  return launch_pdl(mttkrp_coo_kernel, dim3(blocks), dim3(kCooWarps * 32), 0, stream, t, mode, f, R,
-                    out, stop_flag);
+  return launch_pdl(mttkrp_coo_kernel, dim3(blocks, (R + 127) / 128), dim3(kCooWarps * 32), 0, stream, t,
+                    mode, f, R, out, stop_flag);
 }
 
 size_t coo_sq_error_workspace_bytes(int64_t nnz, int R) {

@@ -1,5 +1,5 @@
-// Ridge factorisation shared by ridge_factor_kernel (side stream, CUDA-core
-// engine) and the extra CTA of the tensor-core MTTKRP.
+// Ridge factorisation of ridge_factor_kernel (one CTA on the plan's side
+// stream, concurrent with the mode's MTTKRP).
 #pragma once
 
 #include "common.cuh"
@@ -13,9 +13,12 @@ namespace ntf {
 // update uses the unscaled column (L[i][j] L[k][j] / pivot) and columns are
 // scaled at the end.  A non-positive or non-finite pivot raises NOT_PD.
 // ---------------------------------------------------------------------------
+// col (L in global memory): a shared-memory copy of the pivot column, so the
+// trailing update reads one global element per update instead of three.
 __device__ inline void build_and_factor(double* L, int ldl, int R, const double* __restrict__ Ga,
                                         const double* __restrict__ Gb, double rho, int* status,
-                                        bool* bad, const double* __restrict__ Gc = nullptr) {
+                                        bool* bad, const double* __restrict__ Gc = nullptr,
+                                        double* col = nullptr) {
   const int tid = threadIdx.x;
   for (int e = tid; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
@@ -37,11 +40,22 @@ __device__ inline void build_and_factor(double* L, int ldl, int R, const double*
     }
     const double inv = 1.0 / piv;
     const int n = R - j - 1;  // trailing order; update the lower triangle i >= k > j
-    for (int e = tid; e < n * n; e += blockDim.x) {
-      const int ii = e / n, kk = e - (e / n) * n;
-      if (kk > ii) continue;
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j] * inv;
+    if (col) {
+      for (int i = j + 1 + tid; i < R; i += blockDim.x) col[i] = L[i * ldl + j];
+      __syncthreads();
+      for (int e = tid; e < n * n; e += blockDim.x) {
+        const int ii = e / n, kk = e - (e / n) * n;
+        if (kk > ii) continue;
+        const int i = j + 1 + ii, k = j + 1 + kk;
+        L[i * ldl + k] -= col[i] * col[k] * inv;
+      }
+    } else {
+      for (int e = tid; e < n * n; e += blockDim.x) {
+        const int ii = e / n, kk = e - (e / n) * n;
+        if (kk > ii) continue;
+        const int i = j + 1 + ii, k = j + 1 + kk;
+        L[i * ldl + k] -= L[i * ldl + j] * L[k * ldl + j] * inv;
+      }
     }
     __syncthreads();
   }
@@ -60,17 +74,22 @@ __device__ inline void build_and_factor(double* L, int ldl, int R, const double*
 //   [R*R, R*R+R)        1 / diag(L)
 //   [R*R+R, 2R*R+R)     H^-1 = L^-T L^-1  (R <= 64 only)
 //   [2R*R+R, 3R*R+R)    H = G_a o G_b + rho I
+// Ranks above kRidgeSmemMaxR (R (R+1) doubles no longer fit the 227 KB of
+// shared memory) factor in place in `out` (global memory, L2-resident); the
+// kernel runs on the side stream, concurrently with the mode's MTTKRP.
+constexpr int kRidgeSmemMaxR = 160;
 __host__ __device__ inline int ridge_smem_doubles(int R) {
-  const int fact = (R <= 64 ? 2 : 1) * R * (R + 1) + R;
-  const int gram = R * R + 32 * R;  // gram_from_rows_block
-  return fact > gram ? fact : gram;
+  if (R > kRidgeSmemMaxR) return R;  // the pivot-column copy only
+  return (R <= 64 ? 2 : 1) * R * (R + 1) + R;
 }
+__host__ __device__ inline int ridge_threads(int R) { return R > kRidgeSmemMaxR ? 1024 : 256; }
 
 __device__ inline void ridge_factor_block(const double* Ga, const double* Gb, double rho, int R,
                                           double* out, int* status, double* sm,
                                           const double* Gc = nullptr) {
-  const int ldl = R + 1;
-  double* L = sm;
+  const bool in_place = R > kRidgeSmemMaxR;
+  const int ldl = in_place ? R : R + 1;
+  double* L = in_place ? out : sm;
   double* Li = L + R * ldl;  // L^-1 (lower), R <= 64
   __shared__ bool bad;
   if (threadIdx.x == 0) bad = false;
@@ -82,7 +101,7 @@ __device__ inline void ridge_factor_block(const double* Ga, const double* Gb, do
     if (Gc) h *= Gc[e];
     Hout[e] = h + (i == k ? rho : 0.0);
   }
-  build_and_factor(L, ldl, R, Ga, Gb, rho, status, &bad, Gc);
+  build_and_factor(L, ldl, R, Ga, Gb, rho, status, &bad, Gc, in_place ? sm : nullptr);
   if (bad) return;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, k = e - (e / R) * R;
@@ -116,51 +135,6 @@ __device__ inline void ridge_factor_block(const double* Ga, const double* Gb, do
     double s = 0.0;
     for (int i = a > b ? a : b; i < R; ++i) s += Li[i * ldl + a] * Li[i * ldl + b];
     Hinv[e] = s;
-  }
-}
-
-// G = F^T F (R x R) of a row-major factor by one block, rows streamed through
-// shared memory in chunks, fixed order (row-sequential sums; every element
-// has one owning thread), mirrored so G is exactly symmetric.  sm: >= R*R +
-// 32*R doubles.
-__device__ inline void gram_from_rows_block(const double* __restrict__ F, int64_t rows, int R,
-                                            double* __restrict__ G, double* sm) {
-  constexpr int kChunk = 32;
-  double* Gs = sm;                // [R][R] accumulators (upper triangle used)
-  double* Fs = sm + R * R;        // [kChunk][R]
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gs[e] = 0.0;
-  for (int64_t r0 = 0; r0 < rows; r0 += kChunk) {
-    const int nr = static_cast<int>(rows - r0 < kChunk ? rows - r0 : kChunk);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nr * R; e += blockDim.x) Fs[e] = F[r0 * R + e];
-    __syncthreads();
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      const int a = e / R, b = e - (e / R) * R;
-      if (b < a) continue;
-      double acc = Gs[e];
-      for (int i = 0; i < nr; ++i) acc = fma(Fs[i * R + a], Fs[i * R + b], acc);
-      Gs[e] = acc;
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int a = e / R, b = e - (e / R) * R;
-    G[e] = b >= a ? Gs[e] : Gs[b * R + a];
-  }
-}
-
-// G[e] = sum_b part[b][e] by one block, fixed order: each thread owns
-// elements e and sums all blocks with 8 independent loads in flight.
-__device__ inline void gram_reduce_block(const double* __restrict__ part, int nb, int n,
-                                         double* __restrict__ G) {
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int b0 = 0; b0 < nb; b0 += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (b0 + u < nb) a[u] += part[static_cast<int64_t>(b0 + u) * n + e];
-    }
-    G[e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   }
 }
 

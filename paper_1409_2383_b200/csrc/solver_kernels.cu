@@ -423,18 +423,25 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_gemv_kernel(FactorU
 }
 
 // R > 64: one row per warp, forward/backward substitution against L.
+constexpr int kUpdSmemMaxR = 128;
 template <int RT, int KIND>
 __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorUpdateParams p) {
   pdl_trigger();
   if (p.stop_flag && *p.stop_flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R;
-  const int ldl = R + 1;  // odd pitch: conflict-free row and column walks
+  // L in shared memory with an odd pitch (conflict-free row and column
+  // walks); above kUpdSmemMaxR it is read in place from the ridge buffer
+  // (global memory, L2-resident)
+  const bool l_global = R > kUpdSmemMaxR;
+  const int ldl = l_global ? R : R + 1;
   const int rpb = rows_per_block(R, p.rows);
   const int npm = rpb * R;
-  double* L = reinterpret_cast<double*>(smem_raw);
-  double* inv_diag = L + R * ldl;  // [R]
-  double* ms = inv_diag + R;       // [npm] MTTKRP row sums
+  double* Ls = reinterpret_cast<double*>(smem_raw);
+  double* inv_s = Ls + R * ldl;                // [R]
+  double* ms = l_global ? Ls : inv_s + R;      // [npm] MTTKRP row sums
+  const double* L = l_global ? p.Lg : Ls;
+  const double* inv_diag = l_global ? p.Lg + R * R : inv_s;
   double* xr = ms + npm;           // [npm] new rows
   double* scr = xr + npm;          // [kUpdThreads]
   double* gs = scr + kUpdThreads;  // [R + 8] g1 = (G + rho I)^-1 1 and its sum
@@ -448,11 +455,13 @@ __global__ void __launch_bounds__(kUpdThreads) factor_update_warp_kernel(FactorU
   pdl_wait();  // MTTKRP partials and ridge factor
   const int stopped = p.stop_flag ? *reinterpret_cast<const volatile int*>(p.stop_flag) : 0;
   if (*p.status == kDevNotPD || stopped) return;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, k = e - (e / R) * R;
-    L[i * ldl + k] = p.Lg[e];
+  if (!l_global) {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, k = e - (e / R) * R;
+      Ls[i * ldl + k] = p.Lg[e];
+    }
+    for (int j = threadIdx.x; j < R; j += blockDim.x) inv_s[j] = p.Lg[R * R + j];
   }
-  for (int j = threadIdx.x; j < R; j += blockDim.x) inv_diag[j] = p.Lg[R * R + j];
   split_sum(p, base, cnt, npm, ms, scr);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (rowstoch) {  // g1 = cho_solve(ones) (solver.py:190) by warp 0
@@ -955,7 +964,7 @@ size_t factor_update_smem(int R) {
   if (R <= 64)
     n = 2 * static_cast<size_t>(R) * R + 6 * npm + kUpdThreads + R + 8;
   else
-    n = static_cast<size_t>(R) * (R + 1) + R + 2 * npm + kUpdThreads + R + 8 +
+    n = (R > kUpdSmemMaxR ? 0 : static_cast<size_t>(R) * (R + 1) + R) + 2 * npm + kUpdThreads + R + 8 +
         2 * (kUpdThreads / 32) * static_cast<size_t>(R);
   return n * sizeof(double);
 }
@@ -965,7 +974,7 @@ size_t ridge_factor_smem(int R) { return static_cast<size_t>(ridge_smem_doubles(
 size_t ridge_buffer_doubles(int R) { return 3 * static_cast<size_t>(R) * R + R; }
 
 cudaError_t ridge_factor_launch(const RidgeParams& p, cudaStream_t stream) {
-  ridge_factor_kernel<<<1, 256, ridge_factor_smem(p.R), stream>>>(p);
+  ridge_factor_kernel<<<1, ridge_threads(p.R), ridge_factor_smem(p.R), stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -979,7 +988,9 @@ cudaError_t factor_update_prepare(int R) {
       reinterpret_cast<const void*>(factor_update_warp_kernel<3, kConstraintNonneg>),
       reinterpret_cast<const void*>(factor_update_warp_kernel<3, kConstraintRowStochastic>),
       reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintNonneg>),
-      reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintRowStochastic>)};
+      reinterpret_cast<const void*>(factor_update_warp_kernel<4, kConstraintRowStochastic>),
+      reinterpret_cast<const void*>(factor_update_warp_kernel<8, kConstraintNonneg>),
+      reinterpret_cast<const void*>(factor_update_warp_kernel<8, kConstraintRowStochastic>)};
   for (const void* k : kerns) {
     e = allow_dyn_smem(k, smem);
     if (e != cudaSuccess) return e;
@@ -1007,8 +1018,11 @@ cudaError_t factor_update_launch(const FactorUpdateParams& p_in, cudaStream_t st
   if (p.R <= 96)
     return rs ? launch(factor_update_warp_kernel<3, kConstraintRowStochastic>)
               : launch(factor_update_warp_kernel<3, kConstraintNonneg>);
-  return rs ? launch(factor_update_warp_kernel<4, kConstraintRowStochastic>)
-            : launch(factor_update_warp_kernel<4, kConstraintNonneg>);
+  if (p.R <= 128)
+    return rs ? launch(factor_update_warp_kernel<4, kConstraintRowStochastic>)
+              : launch(factor_update_warp_kernel<4, kConstraintNonneg>);
+  return rs ? launch(factor_update_warp_kernel<8, kConstraintRowStochastic>)
+            : launch(factor_update_warp_kernel<8, kConstraintNonneg>);
 }
 
 cudaError_t kr_merge_launch(const KrMergeParams& p, cudaStream_t stream) {

@@ -68,7 +68,7 @@ def test_desc_layout_matches_c(tmp_path, struct, cname):
 def test_invalid_arguments_rejected_without_gpu(lib):
     # argument validation happens before any CUDA call
     assert lib.ntf_mttkrp_workspace_bytes(0, 0, 2, 2, 2, 1, 0) == 0
-    assert lib.ntf_mttkrp_workspace_bytes(1, 0, 2, 2, 2, 200, 0) == 0
+    assert lib.ntf_mttkrp_workspace_bytes(1, 0, 2, 2, 2, 257, 0) == 0  # R > NTF_MAX_RANK
     rc = lib.ntf_mttkrp(4, 0, None, 2, 2, 2, None, None, None, 1, None, None, 0, 0, None)
     assert rc == 1 and b"mode" in lib.ntf_last_error()
     rc = lib.ntf_gram(None, 2, 2, None, None, 0, None)

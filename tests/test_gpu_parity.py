@@ -697,3 +697,65 @@ def test_ranks_generate_own_slabs_fp32(tmp_path):
     assert abs(float(got[0]["rfe"]) - want.rfe) <= 1e-4 * want.rfe
     for k in got[0]:
         assert np.array_equal(got[1][k], got[0][k]), k
+
+
+@pytest.mark.parametrize("dims,R", [((24, 20, 18), 131), ((17, 9, 33), 200), ((12, 10, 8), 256)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_mttkrp_rank_above_128(dims, R, dtype):
+    """Ranks above 128 (the reference only requires rank >= 1,
+    solver.py:355-356): the CUDA-core engine in 128-column chunks (grid z),
+    every mode, against the oracle at the bars of the rank <= 128 tests."""
+    rng = np.random.default_rng(21)
+    x = rng.random(dims).astype(dtype)
+    f = _factors(rng, dims, R)
+    t = O.OracleTensor(x.astype(np.float64))
+    for mode in (1, 2, 3):
+        got = P.mttkrp_factors(P.DenseTensor(x), f, mode)
+        # fp32: 32-term fp32 FMA chains folded into double-float; over these
+        # short contractions (<= 600 terms) their rounding averages out less
+        # than in test_mttkrp_fp32_accuracy (~0.5 fp32 ulp)
+        assert rel(got, O.mttkrp(t, f, mode)) <= (1e-12 if dtype == np.float64 else 6e-8)
+
+
+@pytest.mark.parametrize("R,specs", [(150, None), (200, None), (256, None),
+                                     (140, ["row_stochastic", "nonneg", "nonneg"])])
+def test_fit_rank_above_128_matches_oracle(R, specs):
+    """Fits at ranks above 128: row update against L read from the ridge
+    buffer (R > 128), ridge Cholesky in place in global memory (R > 160),
+    column-chunked MTTKRP; per-iteration factors within 1e-9 of the oracle
+    (penalties replayed, as the constraint tests)."""
+    rng = np.random.default_rng(R)
+    dims = (60, 50, 40)
+    x = O.reconstruct([rng.random((d, 6)) for d in dims]) + 0.01 * rng.standard_normal(dims)
+    kw = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=6, max_restarts=0, track_factors=True)
+    want = O.fit(x, R, O.Config(**kw), specs)
+    got = P.fit(x, R, [P.ConstraintSpec.parse(s) for s in specs] if specs else None,
+                P.SolverConfig(**kw), rho_schedule=np.array(want.rho_history))
+    assert len(got.factor_history) == len(want.factor_history)
+    for it in range(len(want.factor_history)):
+        for m in range(3):
+            assert rel(got.factor_history[it][m], want.factor_history[it][m]) <= 1e-9, (it, m)
+    assert abs(got.rfe - want.rfe) <= 1e-9 * want.rfe
+
+
+def test_sparse_and_order4_rank_above_128():
+    """COO MTTKRP in 128-column chunks (grid y) and an order-4 dense fit
+    at R = 150 against the oracle's dense fits."""
+    rng = np.random.default_rng(9)
+    R = 150
+    kw = dict(seed=4, eps_abs=0.0, eps_rel=0.0, n_max=5, max_restarts=0, track_factors=True)
+    dims = (15, 12, 10)
+    x = rng.random(dims) * (rng.random(dims) < 0.3)
+    idx = np.argwhere(x != 0)
+    coo = P.CooTensor(dims, idx, x[tuple(idx.T)])
+    want = O.fit(x, R, O.Config(**kw))
+    got = P.fit(coo, R, None, P.SolverConfig(**kw), rho_schedule=np.array(want.rho_history))
+    for it in range(len(want.factor_history)):
+        for m in range(3):
+            assert rel(got.factor_history[it][m], want.factor_history[it][m]) <= 1e-9, (it, m)
+    x4 = rng.random((7, 6, 5, 4))
+    want4 = O.fit(x4, R, O.Config(**kw))
+    got4 = P.fit(x4, R, None, P.SolverConfig(**kw), rho_schedule=np.array(want4.rho_history))
+    for it in range(len(want4.factor_history)):
+        for m in range(4):
+            assert rel(got4.factor_history[it][m], want4.factor_history[it][m]) <= 1e-9, (it, m)
