@@ -84,12 +84,19 @@ def _fit_case(g, engine=None):
 
 
 # c4 with BASELINE's literal rho^0 = trace(Gram)/R (11054): after 50 outer
-# iterations the fit is far from converged (RFE 0.92) and the trajectory
-# amplifies MTTKRP perturbations ~2e5-fold (the reference itself moves 2e-10
-# for 1e-15 input perturbations, tools/sensitivity.py); the tensor-core
-# path's ~1e-9 relative MTTKRP error then lands 2-3e-4 away.  The same
-# tensor with the paper's rho^0 = 1 (c4rho1) matches to 2e-10.
-SENSITIVE = {"c4": "c4 / trace-rule rho0: final RFE amplifies ~1e-9 MTTKRP rounding to 2-3e-4 (DESIGN 6b)"}
+# iterations the fit is far from converged (RFE 0.92) and its trajectory
+# amplifies any MTTKRP perturbation ~2e5-fold into the final RFE.  The fp64
+# CUDA-core engine (1e-16 arithmetic) reproduces the reference to 2e-11
+# (test_fp64_engine_matches_reference below); replacing only the first two or
+# three mode updates of the fit, taken while every factor is still
+# non-negative, by the tensor-core path (~1e-9 relative MTTKRP error) already
+# moves the final RFE by 4e-6 ... 1.9e-4, and all 1500 on the tensor cores by
+# 2.7e-4 (profiles/r02_c4_trace_rule_sensitivity.txt, tools/cancel_probe*.py).
+# The 1e-4 gate on this config therefore needs ~1e-10 MTTKRPs, which a 4-byte
+# image of an fp32 tensor does not give; the same tensor with the paper's
+# rho^0 = 1 (c4rho1) matches to 2e-10.
+SENSITIVE = {"c4": "c4 / trace-rule rho0: the trajectory amplifies ~1e-9 MTTKRP rounding 2e5-fold (DESIGN 6b)"}
+C4_TRACE_TOL = 1e-3  # what the tensor-core path does guarantee there
 
 
 @pytest.mark.parametrize("name", [pytest.param(c, marks=pytest.mark.xfail(reason=SENSITIVE[c], strict=False))
@@ -117,11 +124,31 @@ def test_fp32_config_final_rfe_matches_reference(name):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("name", [c for c in ("h200", "h400") if c in CASES])
-def test_fp64_engine_matches_reference_at_rank_100(name):
+def test_fp32_c4_trace_rule_within_sensitivity_bound():
+    """BASELINE c4 with its literal trace-rule rho^0 on the tensor-core path:
+    outside the 1e-4 gate (xfail above) but within 1e-3 of the reference, the
+    bound the trajectory's 2e5-fold amplification of ~1e-9 MTTKRP errors
+    allows; the fp64 engine closes the config (next test)."""
+    if "c4" not in CASES:
+        pytest.skip("no c4 fixture")
+    g = np.load(os.path.join(GOLDEN, "fp32_c4.npz"))
+    res, x = _fit_case(g, engine="tcgen05")
+    want = float(g["fit_rfe"])
+    d = abs(res.rfe - want) / want
+    print(f"fp32 c4 (trace-rule rho0) tcgen05: rfe {res.rfe:.12f} reference {want:.12f} rel {d:.2e}")
+    assert d <= C4_TRACE_TOL
+    del x
+    P.solver.release_plan_cache()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", [c for c in ("h200", "h400", "c4") if c in CASES])
+def test_fp64_engine_matches_reference(name):
     """First link of the c5 chain: the fp64 CUDA-core engine (the reference's
     own arithmetic, fp64 throughout, on the fp32 values upcast) against the
-    reference at R = 100."""
+    reference at R = 100 (h200, h400), and on BASELINE c4 with its literal
+    trace-rule rho^0, the config whose trajectory the tensor-core path's
+    ~1e-9 MTTKRP error does not survive (SENSITIVE above)."""
     g = np.load(os.path.join(GOLDEN, f"fp32_{name}.npz"))
     res, x = _fit_case(g)
     del res
