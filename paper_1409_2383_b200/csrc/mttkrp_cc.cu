@@ -58,18 +58,43 @@ __device__ __forceinline__ void fast_two_sum_acc(float& hi, float& lo, float a) 
 
 template <typename XT, int TM, bool KIND_M, bool VEC>
 struct Geom {
+  static constexpr bool kDmma = sizeof(XT) == 8;                   // fp64 tensors: DMMA fragments
   static constexpr int BM = 32 * TM;
   static constexpr int VW = 16 / sizeof(XT);                       // elements per 16 B
-  static constexpr int kPitchQ = VEC ? kBQ + VW : kBQ + 1;         // KIND_Q row pitch
-  static constexpr int kTileElems = KIND_M ? kBQ * BM : BM * kPitchQ;
+  // fp64: pitches of 4 (mod 16) doubles make the m8n8k4 A fragments (8 rows x
+  // 4 consecutive q, or 4 q-rows x 8 consecutive m) bank-conflict free
+  static constexpr int kPitchQ = kDmma ? kBQ + 4 : (VEC ? kBQ + VW : kBQ + 1);  // KIND_Q row pitch
+  static constexpr int kPitchM = kDmma ? BM + 4 : BM;              // KIND_M row pitch
+  static constexpr int kTileElems = KIND_M ? kBQ * kPitchM : BM * kPitchQ;
 };
 
+// D (8x8, fp64) += A (8x4, row) * B (4x8, col): lane (g = lane / 4, t = lane % 4)
+// holds A[g][t], B[t][g] and D[g][2t], D[g][2t + 1].  Full fp64 rate on sm_100a
+// (37 TFLOP/s measured, tools/ubench/f64_rate.cu) with one operand fetch per
+// 8 multiply-adds of a lane.
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int kProdWarps = 4;  // fp64: producer warps (stage loads + KR rows) beside the DMMA warps
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
 template <typename XT, int TM, int TR, bool KIND_M, bool VEC>
-__global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
+__global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
+    mttkrp_cc_kernel(MttkrpCCParams p) {
   using G = Geom<XT, TM, KIND_M, VEC>;
   constexpr int BM = G::BM;
   constexpr int VW = G::VW;
   constexpr bool kTwoLevel = sizeof(XT) == 4;
+  constexpr bool kDmma = G::kDmma;  // TR is then the number of 8-column blocks a warp holds
 
   if (p.stop_flag && *p.stop_flag) return;
 
@@ -84,7 +109,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
   const int R_pad = p.R_pad;
   unsigned char* stage_base = smem_raw;
   const int stage_bytes = p.stage_bytes;
-  XT* wbuf = reinterpret_cast<XT*>(smem_raw + kStages * stage_bytes);  // [2][BQ][R_pad]
+  XT* wbuf = reinterpret_cast<XT*>(smem_raw + p.n_stages * stage_bytes);  // [1 or 2][BQ][R_pad]
   auto x_tile = [&](int s) { return reinterpret_cast<XT*>(stage_base + s * stage_bytes); };
   auto hi_rows = [&](int s) {
     return reinterpret_cast<double*>(stage_base + s * stage_bytes + G::kTileElems * sizeof(XT));
@@ -97,6 +122,14 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
   const int warp = tid >> 5;
   const int nwarps = nthreads >> 5;
   const int r0 = warp * TR;
+  // fp64: warps [0, BM / 16) issue the DMMAs, the kProdWarps warps after them
+  // run the stage loads and form the KR rows (ltid / lthreads / fwarp /
+  // fnwarps: the loaders' thread and warp numbering); fp32: every warp does both
+  constexpr int kMathWarps = kDmma ? BM / 16 : 0;
+  const int ltid = kDmma ? tid - 32 * kMathWarps : tid;
+  const int lthreads = kDmma ? 32 * kProdWarps : nthreads;
+  const int fwarp = kDmma ? warp - kMathWarps : warp;
+  const int fnwarps = kDmma ? kProdWarps : nwarps;
 
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
   const int split = blockIdx.y;
@@ -114,25 +147,25 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
     if constexpr (!KIND_M) {
       if constexpr (VEC) {
         constexpr int VPR = kBQ / VW;  // vectors per row
-        const int vq = tid % VPR;
+        const int vq = ltid % VPR;
         const uint32_t q = q0 + vq * VW;
         const bool qv = q < p.Q;
         const uint32_t o = qv ? q / static_cast<uint32_t>(p.K) : 0u;
         const uint32_t k = qv ? q - o * static_cast<uint32_t>(p.K) : 0u;
         const int64_t base = static_cast<int64_t>(o) * p.s_o + k;
-        for (int m = tid / VPR; m < BM; m += nthreads / VPR) {
+        for (int m = ltid / VPR; m < BM; m += lthreads / VPR) {
           const int64_t gm = m0 + m;
           const bool valid = qv && gm < p.M;
           cp_async_cg16(xt + m * G::kPitchQ + vq * VW, valid ? X + gm * p.s_m + base : X, valid);
         }
       } else {
-        const int kk = tid % kBQ;
+        const int kk = ltid % kBQ;
         const uint32_t q = q0 + kk;
         const bool qv = q < p.Q;
         const uint32_t o = qv ? q / static_cast<uint32_t>(p.K) : 0u;
         const uint32_t k = qv ? q - o * static_cast<uint32_t>(p.K) : 0u;
         const int64_t base = static_cast<int64_t>(o) * p.s_o + k;
-        for (int m = tid / kBQ; m < BM; m += nthreads / kBQ) {
+        for (int m = ltid / kBQ; m < BM; m += lthreads / kBQ) {
           const int64_t gm = m0 + m;
           const bool valid = qv && gm < p.M;
           cp_async_ca<sizeof(XT)>(xt + m * G::kPitchQ + kk, valid ? X + gm * p.s_m + base : X,
@@ -142,22 +175,22 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
     } else {
       if constexpr (VEC) {
         constexpr int VPR = BM / VW;
-        const int vm = tid % VPR;
+        const int vm = ltid % VPR;
         const int64_t gm = m0 + vm * VW;
-        for (int qq = tid / VPR; qq < kBQ; qq += nthreads / VPR) {
+        for (int qq = ltid / VPR; qq < kBQ; qq += lthreads / VPR) {
           const uint32_t q = q0 + qq;
           const bool valid = q < p.Q && gm < p.M;  // host guarantees M % VW == 0
-          cp_async_cg16(xt + qq * BM + vm * VW, valid ? X + static_cast<int64_t>(q) * p.s_m + gm : X,
-                        valid);
+          cp_async_cg16(xt + qq * G::kPitchM + vm * VW,
+                        valid ? X + static_cast<int64_t>(q) * p.s_m + gm : X, valid);
         }
       } else {
-        for (int e = tid; e < kBQ * BM; e += nthreads) {
+        for (int e = ltid; e < kBQ * BM; e += lthreads) {
           const int qq = e / BM, m = e - (e / BM) * BM;
           const uint32_t q = q0 + qq;
           const int64_t gm = m0 + m;
           const bool valid = q < p.Q && gm < p.M;
-          cp_async_ca<sizeof(XT)>(xt + e, valid ? X + static_cast<int64_t>(q) * p.s_m + gm : X,
-                                  valid);
+          cp_async_ca<sizeof(XT)>(xt + qq * G::kPitchM + m,
+                                  valid ? X + static_cast<int64_t>(q) * p.s_m + gm : X, valid);
         }
       }
     }
@@ -171,7 +204,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
     if (((R | R_full) & 1) == 0) {
       const int vpr = R >> 1;  // 16-byte vectors per row
       const int nh = p.max_hi * vpr;
-      for (int e = tid; e < nh + kBQ * vpr; e += nthreads) {
+      for (int e = ltid; e < nh + kBQ * vpr; e += lthreads) {
         if (e < nh) {
           const int row = e / vpr, v = e - (e / vpr) * vpr;
           const uint32_t h = h0 + row;
@@ -188,7 +221,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
       }
     } else {
       const int nh = p.max_hi * R;
-      for (int e = tid; e < nh + kBQ * R; e += nthreads) {
+      for (int e = ltid; e < nh + kBQ * R; e += lthreads) {
         if (e < nh) {
           const int row = e / R, r = e - (e / R) * R;
           const uint32_t h = h0 + row;
@@ -215,7 +248,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
     const double* hs = hi_rows(s);
     const double* ls = lo_rows(s);
     // batches of 4 q-rows per warp: all shared loads issued before the math
-    for (int qb = warp * 4; qb < kBQ; qb += nwarps * 4) {
+    for (int qb = fwarp * 4; qb < kBQ; qb += fnwarps * 4) {
       for (int r = lane; r < R_pad; r += 32) {
         double a[4], b[4];
 #pragma unroll
@@ -238,23 +271,89 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
 
   // ---------------- accumulators ----------------
   using acc_t = XT;
-  acc_t acc[TM][TR];
+  // fp64 (DMMA): warp w owns rows [16w, 16w + 16) and all columns: two 8-row
+  // blocks x TR 8-column blocks of m8n8k4 accumulator fragments
+  double dacc[kDmma ? 2 : 1][kDmma ? TR : 1][2];
+  if constexpr (kDmma) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < TR; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
+  }
+  acc_t acc[kDmma ? 1 : TM][kDmma ? 1 : TR];
   float hi[kTwoLevel ? TM : 1][kTwoLevel ? TR : 1];
   float lo[kTwoLevel ? TM : 1][kTwoLevel ? TR : 1];
+  if constexpr (!kDmma) {
 #pragma unroll
-  for (int t = 0; t < TM; ++t)
+    for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int j = 0; j < TR; ++j) {
-      acc[t][j] = acc_t(0);
-      if constexpr (kTwoLevel) {
-        hi[t][j] = 0.f;
-        lo[t][j] = 0.f;
+      for (int j = 0; j < TR; ++j) {
+        acc[t][j] = acc_t(0);
+        if constexpr (kTwoLevel) {
+          hi[t][j] = 0.f;
+          lo[t][j] = 0.f;
+        }
+      }
+  }
+
+  const bool active_r = kDmma || r0 < R;  // warps entirely in the padding skip the math
+  const int nb8 = (R + 7) >> 3;           // fp64: 8-column blocks in use
+
+  if constexpr (kDmma) {
+    // Warp-specialised pipeline: the producers stay one chunk ahead with the
+    // KR rows (two buffers) and two chunks ahead with the loads (three
+    // stages), so the DMMA warps never wait on address arithmetic.  Named
+    // barriers 1-2: chunk ready (KR buffer parity), 3-4: chunk consumed,
+    // 5: the producers among themselves.
+    constexpr int kAll = (kMathWarps + kProdWarps) * 32;
+    const int n_it = static_cast<int>(c_end - c_begin);
+    const int ns = p.n_stages;  // 3; 2 where three stages do not fit (wide chunks over tiny extents)
+    if (n_it > 0 && warp >= kMathWarps) {
+      load_stage(c_begin, 0);
+      cp_async_commit();
+      if (ns == 3) {
+        if (n_it > 1) load_stage(c_begin + 1, 1);
+        cp_async_commit();
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int64_t c = c_begin + it;
+        if (ns == 3) cp_async_wait<1>();         // this thread's copies of chunk c
+        else cp_async_wait<0>();
+        named_bar_sync(5, 32 * kProdWarps);      // ... and every producer's
+        form_w(c, it % ns, it & 1);              // KR buffer it & 1: chunk c - 2 was consumed
+        named_bar_arrive(1 + (it & 1), kAll);
+        if (it >= 1) named_bar_sync(3 + ((it - 1) & 1), kAll);  // chunk c - 1 consumed: its stage is free
+        if (it + ns - 1 < n_it) load_stage(c + ns - 1, (it + ns - 1) % ns);
+        cp_async_commit();
+      }
+      named_bar_sync(3 + ((n_it - 1) & 1), kAll);
+      cp_async_wait<0>();
+    } else if (n_it > 0) {
+      const int g = lane >> 2, t4 = lane & 3;
+      for (int it = 0; it < n_it; ++it) {
+        named_bar_sync(1 + (it & 1), kAll);
+        const XT* xt = x_tile(it % ns);
+        const XT* xa = KIND_M ? xt + t4 * G::kPitchM + warp * 16 + g
+                              : xt + (warp * 16 + g) * G::kPitchQ + t4;
+        const XT* wb = wbuf + (it & 1) * kBQ * R_pad + t4 * R_pad + g;
+#pragma unroll 2
+        for (int k4 = 0; k4 < kBQ; k4 += 4) {
+          const double a0 = KIND_M ? xa[k4 * G::kPitchM] : xa[k4];
+          const double a1 = KIND_M ? xa[k4 * G::kPitchM + 8] : xa[8 * G::kPitchQ + k4];
+          double bv[TR];
+#pragma unroll
+          for (int j = 0; j < TR; ++j) bv[j] = j < nb8 ? wb[k4 * R_pad + 8 * j] : 0.0;
+#pragma unroll
+          for (int j = 0; j < TR; ++j)
+            if (j < nb8) {
+              dmma_m8n8k4(dacc[0][j], a0, bv[j]);
+              dmma_m8n8k4(dacc[1][j], a1, bv[j]);
+            }
+        }
+        named_bar_arrive(3 + (it & 1), kAll);
       }
     }
-
-  const bool active_r = r0 < R;  // warps entirely in the padding skip the math
-
-  if (c_begin < c_end) {
+  } else if (c_begin < c_end) {
     load_stage(c_begin, 0);
     cp_async_commit();
     if (c_begin + 1 < c_end) load_stage(c_begin + 1, 1);
@@ -313,7 +412,7 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
 #pragma unroll
             for (int t = 0; t < TM; ++t) {
               const int m = lane + 32 * t;
-              xv[t] = KIND_M ? xt[qq * BM + m] : xt[m * G::kPitchQ + qq];
+              xv[t] = KIND_M ? xt[qq * G::kPitchM + m] : xt[m * G::kPitchQ + qq];
             }
             fma_step(xv, qq);
           }
@@ -341,7 +440,19 @@ __global__ void __launch_bounds__(256, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
   cg::cluster_group cluster = cg::this_cluster();
   __syncthreads();
   double* part = reinterpret_cast<double*>(smem_raw);  // [BM][R], reuses the stage ring
-  if (active_r) {
+  if constexpr (kDmma) {
+    const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 2 && warp < kMathWarps; ++i) {
+      const int m = warp * 16 + 8 * i + g;
+#pragma unroll
+      for (int j = 0; j < TR; ++j) {
+        const int r = 8 * j + 2 * t4;
+        if (r < R) part[m * R + r] = dacc[i][j][0];
+        if (r + 1 < R) part[m * R + r + 1] = dacc[i][j][1];
+      }
+    }
+  } else if (active_r) {
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
       const int m = lane + 32 * t;
@@ -446,9 +557,10 @@ cudaError_t dispatch(int mode, int x_dtype, const MttkrpCCParams& p, const Mttkr
     if (L.TR == 16) return dispatch_kind<float, 4, 16>(mode, p, L, stream, prep);
     return dispatch_kind<float, 4, 8>(mode, p, L, stream, prep);
   }
+  // fp64: DMMA path, TR = 8-column blocks per warp, BM = 32 TM rows on BM / 16 warps
   if (L.TR == 16) return dispatch_kind<double, 2, 16>(mode, p, L, stream, prep);
-  if (L.TR == 8) return dispatch_kind<double, 2, 8>(mode, p, L, stream, prep);
-  return dispatch_kind<double, 2, 4>(mode, p, L, stream, prep);
+  if (L.TR == 8) return dispatch_kind<double, 4, 8>(mode, p, L, stream, prep);
+  return dispatch_kind<double, 4, 4>(mode, p, L, stream, prep);
 }
 
 int sm_count_cached() {
@@ -458,6 +570,18 @@ int sm_count_cached() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int smem_optin_cached() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || n <= 0)
+      n = 232448;  // sm_100a (no device: geometry queries on a CPU-only host)
+    cudaGetLastError();
   }
   return n;
 }
@@ -476,6 +600,7 @@ void fill_params(MttkrpCCParams& p, int mode, const void* X, int64_t I, int64_t 
   p.ws = ws;
   p.stop_flag = stop_flag;
   p.stage_bytes = L.stage_bytes;
+  p.n_stages = L.stages;
   p.max_hi = L.max_hi;
   if (mode == 1) {
     p.s_m = J * K;
@@ -515,12 +640,22 @@ MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   const bool f32 = x_dtype == NTF_F32;
   const int esz = f32 ? 4 : 8;
   const int VW = 16 / esz;
-  L.TM = f32 ? 4 : 2;
-  L.TR = (R > 64) ? 16 : (R > 32 || f32 ? 8 : 4);
+  if (f32) {
+    L.TM = 4;
+    L.TR = R > 64 ? 16 : 8;
+    L.R_pad = ((R + L.TR - 1) / L.TR) * L.TR;
+    L.threads = (L.R_pad / L.TR) * 32;
+    if (L.threads < 64) L.threads = 64;  // keep loaders busy; extra warps skip the math
+  } else {
+    // fp64 (DMMA fragments): each warp holds 16 rows x all columns; the KR
+    // buffer's pitch is 4 or 12 (mod 16) doubles (conflict-free B fragments)
+    L.TR = R > 64 ? 16 : (R > 32 ? 8 : 4);
+    L.TM = R > 64 ? 2 : 4;  // 64 rows above 64 columns (registers, shared memory)
+    L.R_pad = (R + 7) & ~7;
+    while (L.R_pad % 16 != 4 && L.R_pad % 16 != 12) ++L.R_pad;
+    L.threads = (32 * L.TM / 16 + kProdWarps) * 32;  // DMMA warps + producers
+  }
   const int BM = 32 * L.TM;
-  L.R_pad = ((R + L.TR - 1) / L.TR) * L.TR;
-  L.threads = (L.R_pad / L.TR) * 32;
-  if (L.threads < 64) L.threads = 64;  // keep loaders busy; extra warps skip the math
   const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
   const int64_t Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
   const int64_t lo_ext = mode == 3 ? J : K;
@@ -530,32 +665,56 @@ MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.n_chunks = (Q + kBQ - 1) / kBQ;
   // 16-byte cp.async needs whole vectors that never straddle a row/o boundary
   L.vec = (K % VW == 0) && (mode != 3 || M % VW == 0);
-  const int pitchQ = L.vec ? kBQ + VW : kBQ + 1;
-  const int tile = (mode == 3 ? kBQ * BM : BM * pitchQ) * esz;
+  const int pitchQ = f32 ? (L.vec ? kBQ + VW : kBQ + 1) : kBQ + 4;  // Geom::kPitchQ / kPitchM
+  const int tile = (mode == 3 ? kBQ * (f32 ? BM : BM + 4) : BM * pitchQ) * esz;
   L.max_hi = static_cast<int>(std::min<int64_t>(kBQ, (kBQ - 1) / lo_ext + 2));
   const int R2 = (R + 1) & ~1;
   int fac = (L.max_hi + kBQ) * R2 * 8;
   L.stage_bytes = ((tile + fac) + 15) & ~15;
-  const int wbytes = kBQ * L.R_pad * esz;  // one KR buffer (rebuilt after a barrier)
-  L.smem_bytes = kStages * L.stage_bytes + wbytes;
-  const int part_bytes = BM * R * 8;  // cluster-reduction tile reuses the stage ring
-  if (part_bytes > kStages * L.stage_bytes) L.smem_bytes = part_bytes + wbytes;
-  L.cluster = kClusterSplits;
-  // One wave: as many clusters as can be co-resident (whole clusters per GPC),
-  // spread over the m-tiles; splits are whole clusters.
-  int active = 0;
-  {
-    MttkrpCCParams p{};
-    if (dispatch(mode, x_dtype, p, L, nullptr, kQueryClusters) == cudaSuccess)
-      active = g_active_clusters;
-    cudaGetLastError();
+  // KR rows: one buffer rebuilt after a barrier (fp32), two for the fp64 producers
+  const int wbytes = kBQ * L.R_pad * esz * (f32 ? 1 : 2);
+  L.stages = kStages;
+  L.smem_bytes = L.stages * L.stage_bytes + wbytes;
+  if (!f32 && L.smem_bytes > smem_optin_cached()) {  // wide chunks over tiny extents (max_hi rows)
+    L.stages = 2;
+    L.smem_bytes = L.stages * L.stage_bytes + wbytes;
   }
-  if (active <= 0) active = sm_count_cached() / L.cluster;
-  int64_t per_tile = active / L.n_mtiles;
-  if (per_tile < 1) per_tile = 1;
-  int64_t splits = per_tile * L.cluster;
-  const int64_t max_splits = ((L.n_chunks + L.cluster - 1) / L.cluster) * L.cluster;
-  if (splits > max_splits) splits = max_splits;
+  const int part_bytes = BM * R * 8;  // cluster-reduction tile reuses the stage ring
+  if (part_bytes > L.stages * L.stage_bytes) L.smem_bytes = part_bytes + wbytes;
+  // One wave: as many clusters as can be co-resident (whole clusters per GPC),
+  // spread over the m-tiles; splits are whole clusters.  The cluster size
+  // (8, 4, 2 or 1 splits reduced through DSMEM) is the largest that keeps the
+  // most CTAs resident: 8-CTA clusters leave SMs idle when the co-resident
+  // cluster count is not a multiple of the tile count (1000 rows in 8 tiles
+  // of 128: 15 clusters of 8 give 64 CTAs, 72 pairs give 144).
+  const int64_t max_chunks = L.n_chunks;
+  int64_t splits = 1;
+  int best_cluster = kClusterSplits;
+  int64_t best_ctas = 0;
+  for (int cl = kClusterSplits; cl >= 1; cl >>= 1) {
+    L.cluster = cl;
+    int active = 0;
+    {
+      MttkrpCCParams p{};
+      if (dispatch(mode, x_dtype, p, L, nullptr, kQueryClusters) == cudaSuccess)
+        active = g_active_clusters;
+      cudaGetLastError();
+    }
+    if (active <= 0) active = sm_count_cached() / cl;
+    int64_t per_tile = active / L.n_mtiles;
+    if (per_tile < 1) per_tile = 1;
+    int64_t sp = per_tile * cl;
+    const int64_t max_splits = ((max_chunks + cl - 1) / cl) * cl;
+    if (sp > max_splits) sp = max_splits;
+    const int64_t ctas = sp * L.n_mtiles;
+    // a smaller cluster must win by more than 10% (its extra partials cost HBM traffic)
+    if (best_ctas == 0 || ctas * 10 > best_ctas * 11) {
+      best_ctas = ctas;
+      splits = sp;
+      best_cluster = cl;
+    }
+  }
+  L.cluster = best_cluster;
   L.chunks_per_split = (L.n_chunks + splits - 1) / splits;
   L.splits = static_cast<int>(splits);
   L.groups = L.splits / L.cluster;

@@ -20,6 +20,7 @@ struct MttkrpCCParams {
   int R, R_pad;         // R: all columns (factor / output row stride); R_pad: of one 128-column chunk
   int64_t n_chunks, chunks_per_split;
   int stage_bytes, max_hi;
+  int n_stages;         // fp64 pipeline: stage ring depth (3, or 2 where 3 do not fit)
   double* ws;           // [groups][M][R] fp64 partials (one per cluster)
   const int* stop_flag;
 };
@@ -29,7 +30,7 @@ struct MttkrpCCLaunch {
   int col_chunks;               // ceil(R / 128): grid z
   int n_mtiles, splits, cluster, groups;
   int64_t M, Q, n_chunks, chunks_per_split;
-  int stage_bytes, max_hi, smem_bytes;
+  int stage_bytes, max_hi, smem_bytes, stages;
   bool vec;
 };
 
