@@ -34,6 +34,8 @@
 // bitwise run-to-run deterministic.
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "mttkrp_cc.cuh"
 
 namespace cg = cooperative_groups;
@@ -73,9 +75,32 @@ struct Geom {
 // (37 TFLOP/s measured, tools/ubench/f64_rate.cu) with one operand fetch per
 // 8 multiply-adds of a lane.
 __device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+#if defined(NTF_DIAG) && defined(NTF_CC_SKIP_DMMA)  // diagnostic builds only: time the data path alone
+  d[0] += a;
+  d[1] += b;
+  return;
+#endif
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
+}
+
+// f(integral_constant<N>) for the N in [NMIN, NMAX] equal to nb (NMAX otherwise)
+template <int NMAX, int NMIN, typename F>
+__device__ __forceinline__ void dispatch_nb(int nb, F&& f) {
+  if constexpr (NMAX <= NMIN || NMAX <= 1) {
+    f(std::integral_constant<int, NMAX>{});
+  } else {
+    if (nb >= NMAX) f(std::integral_constant<int, NMAX>{});
+    else dispatch_nb<NMAX - 1, NMIN>(nb, f);
+  }
+}
+
+// a * b rounded to nearest, pinned in program order between the DMMAs
+__device__ __forceinline__ double dmul_rn_pinned(double a, double b) {
+  double r;
+  asm volatile("mul.rn.f64 %0, %1, %2;\n" : "=d"(r) : "d"(a), "d"(b));
+  return r;
 }
 
 constexpr int kProdWarps = 4;  // fp64: producer warps (stage loads + KR rows) beside the DMMA warps
@@ -105,11 +130,12 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
   const int R_full = p.R;
   const int c0 = static_cast<int>(blockIdx.z) * kColChunk;
   const int R = R_full - c0 < kColChunk ? R_full - c0 : kColChunk;
-  const int R2 = (R + 1) & ~1;
   const int R_pad = p.R_pad;
+  // pitch of the staged factor rows: fp64 uses the conflict-free fragment pitch (see the plan)
+  const int R2 = kDmma ? R_pad : ((R + 1) & ~1);
   unsigned char* stage_base = smem_raw;
   const int stage_bytes = p.stage_bytes;
-  XT* wbuf = reinterpret_cast<XT*>(smem_raw + p.n_stages * stage_bytes);  // [1 or 2][BQ][R_pad]
+  XT* wbuf = reinterpret_cast<XT*>(smem_raw + p.n_stages * stage_bytes);  // [BQ][R_pad] (fp32 tensors)
   auto x_tile = [&](int s) { return reinterpret_cast<XT*>(stage_base + s * stage_bytes); };
   auto hi_rows = [&](int s) {
     return reinterpret_cast<double*>(stage_base + s * stage_bytes + G::kTileElems * sizeof(XT));
@@ -204,16 +230,18 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
     if (((R | R_full) & 1) == 0) {
       const int vpr = R >> 1;  // 16-byte vectors per row
       const int nh = p.max_hi * vpr;
+      // e / vpr as a multiply-high: exact for e * (vpr - 1) < 2^32
+      const uint32_t vmagic = 0xFFFFFFFFu / static_cast<uint32_t>(vpr) + 1u;
       for (int e = ltid; e < nh + kBQ * vpr; e += lthreads) {
         if (e < nh) {
-          const int row = e / vpr, v = e - (e / vpr) * vpr;
+          const int row = vpr == 1 ? e : static_cast<int>(__umulhi(static_cast<uint32_t>(e), vmagic)), v = e - row * vpr;
           const uint32_t h = h0 + row;
           const bool valid = h < p.hi_extent;
           cp_async_cg16(hs + row * R2 + 2 * v, valid ? Fhi + static_cast<int64_t>(h) * R_full + 2 * v : Fhi,
                         valid);
         } else {
           const int e2 = e - nh;
-          const int qq = e2 / vpr, v = e2 - (e2 / vpr) * vpr;
+          const int qq = vpr == 1 ? e2 : static_cast<int>(__umulhi(static_cast<uint32_t>(e2), vmagic)), v = e2 - qq * vpr;
           uint32_t lo = l0 + qq;
           lo = L >= kBQ ? (lo >= L ? lo - L : lo) : lo % L;
           cp_async_cg16(ls + qq * R2 + 2 * v, Flo + static_cast<int64_t>(lo) * R_full + 2 * v, true);
@@ -300,11 +328,12 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
   const int nb8 = (R + 7) >> 3;           // fp64: 8-column blocks in use
 
   if constexpr (kDmma) {
-    // Warp-specialised pipeline: the producers stay one chunk ahead with the
-    // KR rows (two buffers) and two chunks ahead with the loads (three
-    // stages), so the DMMA warps never wait on address arithmetic.  Named
-    // barriers 1-2: chunk ready (KR buffer parity), 3-4: chunk consumed,
-    // 5: the producers among themselves.
+    // Warp-specialised pipeline: the producers keep the loads two chunks
+    // ahead (three stages); the DMMA warps read the X fragments and the F_lo
+    // rows straight from the stage and form each KR fragment as they load it
+    // (one DMUL per two DMMAs: F_lo[l, n] * F_hi[h, n], rounded once, as the
+    // reference's khatri_rao), so no warp ever waits on address arithmetic.
+    // Named barriers 1..3: stage landed, 4..6: stage consumed, 7: producers.
     constexpr int kAll = (kMathWarps + kProdWarps) * 32;
     const int n_it = static_cast<int>(c_end - c_begin);
     const int ns = p.n_stages;  // 3; 2 where three stages do not fit (wide chunks over tiny extents)
@@ -316,41 +345,97 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
         cp_async_commit();
       }
       for (int it = 0; it < n_it; ++it) {
-        const int64_t c = c_begin + it;
-        if (ns == 3) cp_async_wait<1>();         // this thread's copies of chunk c
+        if (ns == 3) cp_async_wait<1>();         // this thread's copies of chunk it
         else cp_async_wait<0>();
-        named_bar_sync(5, 32 * kProdWarps);      // ... and every producer's
-        form_w(c, it % ns, it & 1);              // KR buffer it & 1: chunk c - 2 was consumed
-        named_bar_arrive(1 + (it & 1), kAll);
-        if (it >= 1) named_bar_sync(3 + ((it - 1) & 1), kAll);  // chunk c - 1 consumed: its stage is free
-        if (it + ns - 1 < n_it) load_stage(c + ns - 1, (it + ns - 1) % ns);
+        named_bar_sync(7, 32 * kProdWarps);      // ... and every producer's
+        named_bar_arrive(1 + it % ns, kAll);
+        if (it >= 1) named_bar_sync(4 + (it - 1) % ns, kAll);  // chunk it - 1 consumed: its stage is free
+#if !(defined(NTF_DIAG) && defined(NTF_CC_SKIP_LOAD))  // diagnostic builds only: time the math alone
+        if (it + ns - 1 < n_it) load_stage(c_begin + it + ns - 1, (it + ns - 1) % ns);
+#endif
         cp_async_commit();
       }
-      named_bar_sync(3 + ((n_it - 1) & 1), kAll);
+      named_bar_sync(4 + (n_it - 1) % ns, kAll);
       cp_async_wait<0>();
     } else if (n_it > 0) {
       const int g = lane >> 2, t4 = lane & 3;
       for (int it = 0; it < n_it; ++it) {
-        named_bar_sync(1 + (it & 1), kAll);
-        const XT* xt = x_tile(it % ns);
+        const int st = it % ns;
+        const uint32_t q0 = static_cast<uint32_t>((c_begin + it) * kBQ);
+        const uint32_t l0 = q0 - (q0 / L) * L;
+        named_bar_sync(1 + st, kAll);
+        const XT* xt = x_tile(st);
         const XT* xa = KIND_M ? xt + t4 * G::kPitchM + warp * 16 + g
                               : xt + (warp * 16 + g) * G::kPitchQ + t4;
-        const XT* wb = wbuf + (it & 1) * kBQ * R_pad + t4 * R_pad + g;
-#pragma unroll 2
-        for (int k4 = 0; k4 < kBQ; k4 += 4) {
-          const double a0 = KIND_M ? xa[k4 * G::kPitchM] : xa[k4];
-          const double a1 = KIND_M ? xa[k4 * G::kPitchM + 8] : xa[8 * G::kPitchQ + k4];
-          double bv[TR];
+        const double* lb = lo_rows(st) + t4 * R2 + g;  // F_lo[l0 + k + t4][8 j + g]
+        const double* hb = hi_rows(st) + g;            // F_hi[h0 + row][8 j + g]
+        // fragments of K step k + 1 are fetched before the DMMAs of step k issue
+        // NB: 8-column blocks issued (exactly nb8 on the common path: a
+        // predicated-off DMMA still occupies the pipe; 33..64 columns all
+        // cost the same with a fixed TR = 8)
+        auto run_chunk = [&](auto straddle, auto nbtag) {
+          constexpr int NB = decltype(nbtag)::value;
+          constexpr bool kStraddle = decltype(straddle)::value;  // some q row belongs to a later F_hi row
+          auto hrow = [&](int k4) {
+            const uint32_t lsum = l0 + k4 + t4;
+            const int hoff = L >= kBQ ? (lsum >= L ? 1 : 0) : static_cast<int>(lsum / L);
+            return hb + hoff * R2;
+          };
+          // K step k: [shared loads of step k + 1] [DMMAs of the first row
+          // block] [KR products of step k + 1] [DMMAs of the second row block]:
+          // every multiply finds its operands loaded and every DMMA its KR
+          // value computed half a step earlier (the DMULs share the fp64 pipe
+          // with the DMMAs and issue in order)
+          double hv[NB];
+          if constexpr (!kStraddle) {
 #pragma unroll
-          for (int j = 0; j < TR; ++j) bv[j] = j < nb8 ? wb[k4 * R_pad + 8 * j] : 0.0;
+            for (int j = 0; j < NB; ++j) hv[j] = hb[8 * j];
+          } else {
+            const double* hr = hrow(0);
 #pragma unroll
-          for (int j = 0; j < TR; ++j)
-            if (j < nb8) {
-              dmma_m8n8k4(dacc[0][j], a0, bv[j]);
-              dmma_m8n8k4(dacc[1][j], a1, bv[j]);
+            for (int j = 0; j < NB; ++j) hv[j] = j < nb8 ? hr[8 * j] : 0.0;
+          }
+          double a0 = xa[0], a1 = KIND_M ? xa[8] : xa[8 * G::kPitchQ];
+          double w[NB];
+#pragma unroll
+          for (int j = 0; j < NB; ++j) w[j] = dmul_rn_pinned((!kStraddle || j < nb8) ? lb[8 * j] : 0.0, hv[j]);
+#pragma unroll
+          for (int k4 = 0; k4 < kBQ; k4 += 4) {
+            const bool more = k4 + 4 < kBQ;
+            double a0n = 0.0, a1n = 0.0, wn[NB];
+            if (more) {
+              a0n = KIND_M ? xa[(k4 + 4) * G::kPitchM] : xa[k4 + 4];
+              a1n = KIND_M ? xa[(k4 + 4) * G::kPitchM + 8] : xa[8 * G::kPitchQ + k4 + 4];
+#pragma unroll
+              for (int j = 0; j < NB; ++j)
+                wn[j] = (!kStraddle || j < nb8) ? lb[(k4 + 4) * R2 + 8 * j] : 0.0;
+              if constexpr (kStraddle) {
+                const double* hr = hrow(k4 + 4);
+#pragma unroll
+                for (int j = 0; j < NB; ++j) hv[j] = j < nb8 ? hr[8 * j] : 0.0;
+              }
             }
-        }
-        named_bar_arrive(3 + (it & 1), kAll);
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+              if (!kStraddle || j < nb8) dmma_m8n8k4(dacc[0][j], a0, w[j]);
+            if (more) {
+#pragma unroll
+              for (int j = 0; j < NB; ++j) wn[j] = dmul_rn_pinned(wn[j], hv[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+              if (!kStraddle || j < nb8) dmma_m8n8k4(dacc[1][j], a1, w[j]);
+            if (more) {
+              a0 = a0n;
+              a1 = a1n;
+#pragma unroll
+              for (int j = 0; j < NB; ++j) w[j] = wn[j];
+            }
+          }
+        };
+        if (l0 + kBQ > L) run_chunk(std::true_type{}, std::integral_constant<int, TR>{});
+        else dispatch_nb<TR, TR / 2 + 1>(nb8, [&](auto nbtag) { run_chunk(std::false_type{}, nbtag); });
+        named_bar_arrive(4 + st, kAll);
       }
     }
   } else if (c_begin < c_end) {
@@ -668,11 +753,11 @@ MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   const int pitchQ = f32 ? (L.vec ? kBQ + VW : kBQ + 1) : kBQ + 4;  // Geom::kPitchQ / kPitchM
   const int tile = (mode == 3 ? kBQ * (f32 ? BM : BM + 4) : BM * pitchQ) * esz;
   L.max_hi = static_cast<int>(std::min<int64_t>(kBQ, (kBQ - 1) / lo_ext + 2));
-  const int R2 = (R + 1) & ~1;
+  const int R2 = f32 ? ((R + 1) & ~1) : L.R_pad;  // staged factor-row pitch
   int fac = (L.max_hi + kBQ) * R2 * 8;
   L.stage_bytes = ((tile + fac) + 15) & ~15;
-  // KR rows: one buffer rebuilt after a barrier (fp32), two for the fp64 producers
-  const int wbytes = kBQ * L.R_pad * esz * (f32 ? 1 : 2);
+  // KR rows: one buffer rebuilt after a barrier (fp32); fp64 forms them in registers
+  const int wbytes = f32 ? kBQ * L.R_pad * esz : 0;
   L.stages = kStages;
   L.smem_bytes = L.stages * L.stage_bytes + wbytes;
   if (!f32 && L.smem_bytes > smem_optin_cached()) {  // wide chunks over tiny extents (max_hi rows)

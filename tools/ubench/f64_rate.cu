@@ -38,6 +38,41 @@ __global__ void dmma_kernel(double* out, int iters, double a, double b) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+template <int NACC>
+__global__ void dmma_chain_kernel(double* out, int iters, double a, double b) {
+  double c[NACC][2];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) c[i][0] = c[i][1] = threadIdx.x + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <int NACC>
+void chain(double* out, int threads) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000;
+  float ms;
+  dmma_chain_kernel<NACC><<<148, threads>>>(out, 100, 1.0000001, 1e-9);
+  cudaEventRecord(e0);
+  dmma_chain_kernel<NACC><<<148, threads>>>(out, iters, 1.0000001, 1e-9);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("DMMA  %d independent accumulators, %d warps/SM: %.2f TFLOP/s, %.1f ns per round of %d\n", NACC,
+         threads / 32, 512.0 * NACC * iters * 148 * (threads / 32) / (ms * 1e-3) / 1e12, ms * 1e6 / iters, NACC);
+}
+
 int main() {
   double* out;
   cudaMalloc(&out, 148 * 8 * 1024 * sizeof(double));
@@ -76,6 +111,14 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("DMMA  1 blk/SM x %4d thr (16 independent accumulators/warp): %.2f TFLOP/s\n", threads,
            512.0 * 16 * iters * blocks * (threads / 32) / (ms * 1e-3) / 1e12);
+  }
+  for (int threads : {128, 256}) {
+    chain<1>(out, threads);
+    chain<2>(out, threads);
+    chain<4>(out, threads);
+    chain<6>(out, threads);
+    chain<10>(out, threads);
+    chain<16>(out, threads);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
