@@ -1,4 +1,5 @@
-// Dense MTTKRP on CUDA cores (sm_100a), all three modes, fp32 or fp64 tensor.
+// Dense MTTKRP in fp64 arithmetic (sm_100a, fp64 tensor pipe), all three modes,
+// fp32 or fp64 tensor: the "cuda_core" engine (no tcgen05, no fp16 slicing).
 //
 // Replaces tensors.mttkrp_factors dense branch (reference tensors.py:254-262):
 //   M_n = X_(n) @ khatri_rao(companions, highest mode first)
@@ -13,19 +14,20 @@
 //       mode 2: m = j, o = i  (X(m,q) = X[i*JK + j*K + k]),  W = A[i] * C[k]
 //   KIND_M (mode 3):       q = p = i*J + j, m = k contiguous, L = J, W = A[i] * B[j]
 //
-// Tiling.  A CTA owns BM = 32*TM output rows and all R columns; warp w owns
-// columns [w*TR, (w+1)*TR); lane l owns rows l + 32*t (t < TM).  The
-// reduction range is cut into chunks of BQ = 32 q-values.  Each chunk's stage
-// (X tile + the fp64 factor rows its KR rows need) is streamed by 16-byte
-// cp.async through a 3-stage ring; the chunk's KR rows W (fp64 product rounded
-// once to the compute type) are formed from shared memory and read by the FMA
-// loop as warp broadcasts.  KIND_Q tiles keep the natural [m][q] layout with a
-// 16-byte row pad (pitch BQ+4 floats), which makes both the 16-byte cp.async
-// writes and the per-lane 16-byte row reads bank-conflict free.
+// Tiling.  A CTA owns BM = 32*TM output rows and all R columns (ranks above
+// 128: one grid z-slice per 128-column chunk).  The reduction range is cut
+// into chunks of BQ = 32 q-values; each chunk's stage (the X tile + the fp64
+// F_hi / F_lo rows its Khatri-Rao rows need) is streamed by 16-byte cp.async
+// through a 3-stage ring by four producer warps.  The math runs on the fp64
+// tensor pipe: DMMA warp w owns rows [16w, 16w + 16) and all columns as
+// m8n8k4 fragments (A = X, converted to fp64 when the tensor is fp32; B = the
+// KR row, F_lo[l, n] * F_hi[h, n] rounded once as the reference's khatri_rao,
+// formed in registers as the fragment is loaded; fp64 accumulators).  Tile
+// pitches are chosen so every fragment load is bank-conflict free.
 //
-// Precision (fp32 tensors): fp32 FMA chains of BQ terms folded
-// into a double-float (hi, lo) accumulator each chunk — no structured rounding
-// of the factors and no long fp32 chains.  fp64 tensors accumulate in fp64.
+// Precision: fp64 arithmetic throughout for fp32 and fp64 tensors alike (the
+// fp32 tensor values are exact in fp64), so this engine reproduces the
+// reference's arithmetic up to summation order whatever the tensor's type.
 //
 // Split-K.  CTAs of one m-tile stream contiguous chunk ranges.  The CTAs of a
 // thread-block cluster (CS splits) reduce their fp64 partial tiles through
@@ -49,24 +51,15 @@ constexpr int kStages = 3;
 constexpr int kClusterSplits = 8;
 constexpr int kColChunk = 128;  // output columns per CTA (8 warps x TR = 16)
 
-__device__ __forceinline__ void fast_two_sum_acc(float& hi, float& lo, float a) {
-  // (hi, lo) += a with Fast2Sum: exact when |hi| >= |a|, which holds after the
-  // first chunk because one output's chunk sums are a small share of the total.
-  const float s = hi + a;
-  const float err = a - (s - hi);
-  hi = s;
-  lo += err;
-}
-
 template <typename XT, int TM, bool KIND_M, bool VEC>
 struct Geom {
-  static constexpr bool kDmma = sizeof(XT) == 8;                   // fp64 tensors: DMMA fragments
   static constexpr int BM = 32 * TM;
-  static constexpr int VW = 16 / sizeof(XT);                       // elements per 16 B
-  // fp64: pitches of 4 (mod 16) doubles make the m8n8k4 A fragments (8 rows x
-  // 4 consecutive q, or 4 q-rows x 8 consecutive m) bank-conflict free
-  static constexpr int kPitchQ = kDmma ? kBQ + 4 : (VEC ? kBQ + VW : kBQ + 1);  // KIND_Q row pitch
-  static constexpr int kPitchM = kDmma ? BM + 4 : BM;              // KIND_M row pitch
+  static constexpr int VW = 16 / sizeof(XT);  // elements per 16 B
+  // Pitches that make the m8n8k4 A fragments (KIND_Q: 8 rows x 4 consecutive
+  // q; KIND_M: 4 q-rows x 8 consecutive m) bank-conflict free: 4 (mod 16)
+  // doubles, or 4 resp. 8 (mod 32) floats; all multiples of 16 bytes
+  static constexpr int kPitchQ = kBQ + 4;
+  static constexpr int kPitchM = BM + (sizeof(XT) == 8 ? 4 : 8);
   static constexpr int kTileElems = KIND_M ? kBQ * kPitchM : BM * kPitchQ;
 };
 
@@ -98,12 +91,15 @@ __device__ __forceinline__ void dispatch_nb(int nb, F&& f) {
 
 // a * b rounded to nearest, pinned in program order between the DMMAs
 __device__ __forceinline__ double dmul_rn_pinned(double a, double b) {
+#if defined(NTF_DIAG) && defined(NTF_CC_SKIP_DMUL)  // diagnostic builds only
+  return a;
+#endif
   double r;
   asm volatile("mul.rn.f64 %0, %1, %2;\n" : "=d"(r) : "d"(a), "d"(b));
   return r;
 }
 
-constexpr int kProdWarps = 4;  // fp64: producer warps (stage loads + KR rows) beside the DMMA warps
+constexpr int kProdWarps = 4;  // producer warps (stage loads) beside the DMMA warps
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
@@ -113,13 +109,11 @@ __device__ __forceinline__ void named_bar_arrive(int id, int count) {
 }
 
 template <typename XT, int TM, int TR, bool KIND_M, bool VEC>
-__global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
-    mttkrp_cc_kernel(MttkrpCCParams p) {
+__global__ void __launch_bounds__((32 * TM / 16 + kProdWarps) * 32, 1) mttkrp_cc_kernel(MttkrpCCParams p) {
   using G = Geom<XT, TM, KIND_M, VEC>;
   constexpr int BM = G::BM;
   constexpr int VW = G::VW;
-  constexpr bool kTwoLevel = sizeof(XT) == 4;
-  constexpr bool kDmma = G::kDmma;  // TR is then the number of 8-column blocks a warp holds
+  // TR: the 8-column blocks a DMMA warp can hold (4, 8 or 16)
 
   if (p.stop_flag && *p.stop_flag) return;
 
@@ -131,11 +125,10 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
   const int c0 = static_cast<int>(blockIdx.z) * kColChunk;
   const int R = R_full - c0 < kColChunk ? R_full - c0 : kColChunk;
   const int R_pad = p.R_pad;
-  // pitch of the staged factor rows: fp64 uses the conflict-free fragment pitch (see the plan)
-  const int R2 = kDmma ? R_pad : ((R + 1) & ~1);
+  // pitch of the staged factor rows: 4 or 12 (mod 16) doubles (see the plan)
+  const int R2 = R_pad;
   unsigned char* stage_base = smem_raw;
   const int stage_bytes = p.stage_bytes;
-  XT* wbuf = reinterpret_cast<XT*>(smem_raw + p.n_stages * stage_bytes);  // [BQ][R_pad] (fp32 tensors)
   auto x_tile = [&](int s) { return reinterpret_cast<XT*>(stage_base + s * stage_bytes); };
   auto hi_rows = [&](int s) {
     return reinterpret_cast<double*>(stage_base + s * stage_bytes + G::kTileElems * sizeof(XT));
@@ -146,16 +139,11 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
   const int nthreads = blockDim.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int nwarps = nthreads >> 5;
-  const int r0 = warp * TR;
-  // fp64: warps [0, BM / 16) issue the DMMAs, the kProdWarps warps after them
-  // run the stage loads and form the KR rows (ltid / lthreads / fwarp /
-  // fnwarps: the loaders' thread and warp numbering); fp32: every warp does both
-  constexpr int kMathWarps = kDmma ? BM / 16 : 0;
-  const int ltid = kDmma ? tid - 32 * kMathWarps : tid;
-  const int lthreads = kDmma ? 32 * kProdWarps : nthreads;
-  const int fwarp = kDmma ? warp - kMathWarps : warp;
-  const int fnwarps = kDmma ? kProdWarps : nwarps;
+  // warps [0, BM / 16) issue the DMMAs, the kProdWarps warps after them run
+  // the stage loads (ltid / lthreads: the loaders' thread numbering)
+  constexpr int kMathWarps = BM / 16;
+  const int ltid = tid - 32 * kMathWarps;
+  constexpr int lthreads = 32 * kProdWarps;
 
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
   const int split = blockIdx.y;
@@ -266,68 +254,17 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
     }
   };
 
-  // KR rows of chunk c from the staged factor rows: one warp per q-row,
-  // lanes along r (no per-element division).
-  auto form_w = [&](int64_t c, int s, int buf) {
-    XT* dst = wbuf + buf * kBQ * R_pad;
-    const uint32_t q0 = static_cast<uint32_t>(c * kBQ);
-    const uint32_t h0 = q0 / L;
-    const uint32_t l0 = q0 - h0 * L;
-    const double* hs = hi_rows(s);
-    const double* ls = lo_rows(s);
-    // batches of 4 q-rows per warp: all shared loads issued before the math
-    for (int qb = fwarp * 4; qb < kBQ; qb += fnwarps * 4) {
-      for (int r = lane; r < R_pad; r += 32) {
-        double a[4], b[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qq = qb + u;
-          const uint32_t lsum = l0 + qq;
-          const int hoff = L >= kBQ ? (lsum >= L ? 1 : 0) : static_cast<int>(lsum / L);
-          const bool ok = qq < kBQ && r < R;
-          a[u] = ok ? hs[hoff * R2 + r] : 0.0;
-          b[u] = ok ? ls[qq * R2 + r] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qq = qb + u;
-          if (qq < kBQ) dst[qq * R_pad + r] = (q0 + qq < p.Q) ? static_cast<XT>(a[u] * b[u]) : XT(0);
-        }
-      }
-    }
-  };
-
   // ---------------- accumulators ----------------
-  using acc_t = XT;
-  // fp64 (DMMA): warp w owns rows [16w, 16w + 16) and all columns: two 8-row
-  // blocks x TR 8-column blocks of m8n8k4 accumulator fragments
-  double dacc[kDmma ? 2 : 1][kDmma ? TR : 1][2];
-  if constexpr (kDmma) {
+  // DMMA warp w owns rows [16w, 16w + 16) and all columns: two 8-row blocks x
+  // TR 8-column blocks of m8n8k4 accumulator fragments
+  double dacc[2][TR][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < TR; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
-  }
-  acc_t acc[kDmma ? 1 : TM][kDmma ? 1 : TR];
-  float hi[kTwoLevel ? TM : 1][kTwoLevel ? TR : 1];
-  float lo[kTwoLevel ? TM : 1][kTwoLevel ? TR : 1];
-  if constexpr (!kDmma) {
-#pragma unroll
-    for (int t = 0; t < TM; ++t)
-#pragma unroll
-      for (int j = 0; j < TR; ++j) {
-        acc[t][j] = acc_t(0);
-        if constexpr (kTwoLevel) {
-          hi[t][j] = 0.f;
-          lo[t][j] = 0.f;
-        }
-      }
-  }
+    for (int j = 0; j < TR; ++j) dacc[i][j][0] = dacc[i][j][1] = 0.0;
+  const int nb8 = (R + 7) >> 3;  // 8-column blocks in use
 
-  const bool active_r = kDmma || r0 < R;  // warps entirely in the padding skip the math
-  const int nb8 = (R + 7) >> 3;           // fp64: 8-column blocks in use
-
-  if constexpr (kDmma) {
+  {
     // Warp-specialised pipeline: the producers keep the loads two chunks
     // ahead (three stages); the DMMA warps read the X fragments and the F_lo
     // rows straight from the stage and form each KR fragment as they load it
@@ -395,7 +332,8 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
 #pragma unroll
             for (int j = 0; j < NB; ++j) hv[j] = j < nb8 ? hr[8 * j] : 0.0;
           }
-          double a0 = xa[0], a1 = KIND_M ? xa[8] : xa[8 * G::kPitchQ];
+          double a0 = static_cast<double>(xa[0]);
+          double a1 = static_cast<double>(KIND_M ? xa[8] : xa[8 * G::kPitchQ]);
           double w[NB];
 #pragma unroll
           for (int j = 0; j < NB; ++j) w[j] = dmul_rn_pinned((!kStraddle || j < nb8) ? lb[8 * j] : 0.0, hv[j]);
@@ -404,8 +342,8 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
             const bool more = k4 + 4 < kBQ;
             double a0n = 0.0, a1n = 0.0, wn[NB];
             if (more) {
-              a0n = KIND_M ? xa[(k4 + 4) * G::kPitchM] : xa[k4 + 4];
-              a1n = KIND_M ? xa[(k4 + 4) * G::kPitchM + 8] : xa[8 * G::kPitchQ + k4 + 4];
+              a0n = static_cast<double>(KIND_M ? xa[(k4 + 4) * G::kPitchM] : xa[k4 + 4]);
+              a1n = static_cast<double>(KIND_M ? xa[(k4 + 4) * G::kPitchM + 8] : xa[8 * G::kPitchQ + k4 + 4]);
 #pragma unroll
               for (int j = 0; j < NB; ++j)
                 wn[j] = (!kStraddle || j < nb8) ? lb[(k4 + 4) * R2 + 8 * j] : 0.0;
@@ -438,94 +376,13 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
         named_bar_arrive(4 + st, kAll);
       }
     }
-  } else if (c_begin < c_end) {
-    load_stage(c_begin, 0);
-    cp_async_commit();
-    if (c_begin + 1 < c_end) load_stage(c_begin + 1, 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    form_w(c_begin, 0, 0);
-
-    for (int64_t c = c_begin; c < c_end; ++c) {
-      const int it = static_cast<int>(c - c_begin);
-      __syncthreads();
-      if (c + 2 < c_end) load_stage(c + 2, (it + 2) % kStages);
-      cp_async_commit();
-
-      if (active_r) {
-        const XT* xt = x_tile(it % kStages);
-        const XT* wt = wbuf + r0;
-        auto fma_step = [&](const XT (&xv)[TM], int qq) {
-          XT wv[TR];
-#pragma unroll
-          for (int j = 0; j < TR; j += VW) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(wt + qq * R_pad + j);
-            const XT* pv = reinterpret_cast<const XT*>(&raw);
-#pragma unroll
-            for (int u = 0; u < VW; ++u) wv[j + u] = pv[u];
-          }
-#pragma unroll
-          for (int t = 0; t < TM; ++t)
-#pragma unroll
-            for (int j = 0; j < TR; ++j) acc[t][j] = fma(xv[t], wv[j], acc[t][j]);
-        };
-        if constexpr (!KIND_M && VEC) {
-#pragma unroll 2
-          for (int q4 = 0; q4 < kBQ; q4 += VW) {
-            XT xr[TM][VW];
-#pragma unroll
-            for (int t = 0; t < TM; ++t) {
-              const uint4 raw =
-                  *reinterpret_cast<const uint4*>(xt + (lane + 32 * t) * G::kPitchQ + q4);
-              const XT* pv = reinterpret_cast<const XT*>(&raw);
-#pragma unroll
-              for (int u = 0; u < VW; ++u) xr[t][u] = pv[u];
-            }
-#pragma unroll
-            for (int u = 0; u < VW; ++u) {
-              XT xv[TM];
-#pragma unroll
-              for (int t = 0; t < TM; ++t) xv[t] = xr[t][u];
-              fma_step(xv, q4 + u);
-            }
-          }
-        } else {
-#pragma unroll 4
-          for (int qq = 0; qq < kBQ; ++qq) {
-            XT xv[TM];
-#pragma unroll
-            for (int t = 0; t < TM; ++t) {
-              const int m = lane + 32 * t;
-              xv[t] = KIND_M ? xt[qq * G::kPitchM + m] : xt[m * G::kPitchQ + qq];
-            }
-            fma_step(xv, qq);
-          }
-        }
-        if constexpr (kTwoLevel) {
-#pragma unroll
-          for (int t = 0; t < TM; ++t)
-#pragma unroll
-            for (int j = 0; j < TR; ++j) {
-              fast_two_sum_acc(hi[t][j], lo[t][j], acc[t][j]);
-              acc[t][j] = 0.f;
-            }
-        }
-      }
-      if (c + 1 < c_end) {
-        cp_async_wait<1>();
-        __syncthreads();
-        form_w(c + 1, (it + 1) % kStages, 0);
-      }
-    }
-    cp_async_wait<0>();
   }
 
   // ------------- cluster (DSMEM) reduction of the split partials -------------
   cg::cluster_group cluster = cg::this_cluster();
   __syncthreads();
   double* part = reinterpret_cast<double*>(smem_raw);  // [BM][R], reuses the stage ring
-  if constexpr (kDmma) {
+  {
     const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
     for (int i = 0; i < 2 && warp < kMathWarps; ++i) {
@@ -535,22 +392,6 @@ __global__ void __launch_bounds__((sizeof(XT) == 8 && TM == 4) ? 384 : 256, 1)
         const int r = 8 * j + 2 * t4;
         if (r < R) part[m * R + r] = dacc[i][j][0];
         if (r + 1 < R) part[m * R + r + 1] = dacc[i][j][1];
-      }
-    }
-  } else if (active_r) {
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      const int m = lane + 32 * t;
-#pragma unroll
-      for (int j = 0; j < TR; ++j) {
-        const int r = r0 + j;
-        if (r >= R) continue;
-        double v;
-        if constexpr (kTwoLevel)
-          v = static_cast<double>(hi[t][j]) + static_cast<double>(lo[t][j]);
-        else
-          v = static_cast<double>(acc[t][j]);
-        part[m * R + r] = v;
       }
     }
   }
@@ -638,11 +479,12 @@ cudaError_t dispatch_kind(int mode, const MttkrpCCParams& p, const MttkrpCCLaunc
 
 cudaError_t dispatch(int mode, int x_dtype, const MttkrpCCParams& p, const MttkrpCCLaunch& L,
                      cudaStream_t stream, int prep) {
+  // TR = 8-column blocks per warp; BM = 32 TM rows on BM / 16 DMMA warps
   if (x_dtype == NTF_F32) {
-    if (L.TR == 16) return dispatch_kind<float, 4, 16>(mode, p, L, stream, prep);
-    return dispatch_kind<float, 4, 8>(mode, p, L, stream, prep);
+    if (L.TR == 16) return dispatch_kind<float, 2, 16>(mode, p, L, stream, prep);
+    if (L.TR == 8) return dispatch_kind<float, 4, 8>(mode, p, L, stream, prep);
+    return dispatch_kind<float, 4, 4>(mode, p, L, stream, prep);
   }
-  // fp64: DMMA path, TR = 8-column blocks per warp, BM = 32 TM rows on BM / 16 warps
   if (L.TR == 16) return dispatch_kind<double, 2, 16>(mode, p, L, stream, prep);
   if (L.TR == 8) return dispatch_kind<double, 4, 8>(mode, p, L, stream, prep);
   return dispatch_kind<double, 4, 4>(mode, p, L, stream, prep);
@@ -725,21 +567,13 @@ MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   const bool f32 = x_dtype == NTF_F32;
   const int esz = f32 ? 4 : 8;
   const int VW = 16 / esz;
-  if (f32) {
-    L.TM = 4;
-    L.TR = R > 64 ? 16 : 8;
-    L.R_pad = ((R + L.TR - 1) / L.TR) * L.TR;
-    L.threads = (L.R_pad / L.TR) * 32;
-    if (L.threads < 64) L.threads = 64;  // keep loaders busy; extra warps skip the math
-  } else {
-    // fp64 (DMMA fragments): each warp holds 16 rows x all columns; the KR
-    // buffer's pitch is 4 or 12 (mod 16) doubles (conflict-free B fragments)
-    L.TR = R > 64 ? 16 : (R > 32 ? 8 : 4);
-    L.TM = R > 64 ? 2 : 4;  // 64 rows above 64 columns (registers, shared memory)
-    L.R_pad = (R + 7) & ~7;
-    while (L.R_pad % 16 != 4 && L.R_pad % 16 != 12) ++L.R_pad;
-    L.threads = (32 * L.TM / 16 + kProdWarps) * 32;  // DMMA warps + producers
-  }
+  // Each DMMA warp holds 16 rows x all columns (TR 8-column blocks); the
+  // staged factor rows' pitch is 4 or 12 (mod 16) doubles (conflict-free B fragments)
+  L.TR = R > 64 ? 16 : (R > 32 ? 8 : 4);
+  L.TM = R > 64 ? 2 : 4;  // 64 rows above 64 columns (registers, shared memory)
+  L.R_pad = (R + 7) & ~7;
+  while (L.R_pad % 16 != 4 && L.R_pad % 16 != 12) ++L.R_pad;
+  L.threads = (32 * L.TM / 16 + kProdWarps) * 32;  // DMMA warps + producers
   const int BM = 32 * L.TM;
   const int64_t M = mode == 1 ? I : (mode == 2 ? J : K);
   const int64_t Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
@@ -750,22 +584,18 @@ MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.n_chunks = (Q + kBQ - 1) / kBQ;
   // 16-byte cp.async needs whole vectors that never straddle a row/o boundary
   L.vec = (K % VW == 0) && (mode != 3 || M % VW == 0);
-  const int pitchQ = f32 ? (L.vec ? kBQ + VW : kBQ + 1) : kBQ + 4;  // Geom::kPitchQ / kPitchM
-  const int tile = (mode == 3 ? kBQ * (f32 ? BM : BM + 4) : BM * pitchQ) * esz;
+  const int tile = (mode == 3 ? kBQ * (BM + (f32 ? 8 : 4)) : BM * (kBQ + 4)) * esz;  // Geom::kPitchM / kPitchQ
   L.max_hi = static_cast<int>(std::min<int64_t>(kBQ, (kBQ - 1) / lo_ext + 2));
-  const int R2 = f32 ? ((R + 1) & ~1) : L.R_pad;  // staged factor-row pitch
-  int fac = (L.max_hi + kBQ) * R2 * 8;
+  int fac = (L.max_hi + kBQ) * L.R_pad * 8;  // staged factor rows
   L.stage_bytes = ((tile + fac) + 15) & ~15;
-  // KR rows: one buffer rebuilt after a barrier (fp32); fp64 forms them in registers
-  const int wbytes = f32 ? kBQ * L.R_pad * esz : 0;
   L.stages = kStages;
-  L.smem_bytes = L.stages * L.stage_bytes + wbytes;
-  if (!f32 && L.smem_bytes > smem_optin_cached()) {  // wide chunks over tiny extents (max_hi rows)
+  L.smem_bytes = L.stages * L.stage_bytes;
+  if (L.smem_bytes > smem_optin_cached()) {  // wide chunks over tiny extents (max_hi rows)
     L.stages = 2;
-    L.smem_bytes = L.stages * L.stage_bytes + wbytes;
+    L.smem_bytes = L.stages * L.stage_bytes;
   }
   const int part_bytes = BM * R * 8;  // cluster-reduction tile reuses the stage ring
-  if (part_bytes > L.stages * L.stage_bytes) L.smem_bytes = part_bytes + wbytes;
+  if (part_bytes > L.smem_bytes) L.smem_bytes = part_bytes;
   // One wave: as many clusters as can be co-resident (whole clusters per GPC),
   // spread over the m-tiles; splits are whole clusters.  The cluster size
   // (8, 4, 2 or 1 splits reduced through DSMEM) is the largest that keeps the

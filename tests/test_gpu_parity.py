@@ -711,10 +711,8 @@ def test_mttkrp_rank_above_128(dims, R, dtype):
     t = O.OracleTensor(x.astype(np.float64))
     for mode in (1, 2, 3):
         got = P.mttkrp_factors(P.DenseTensor(x), f, mode)
-        # fp32: 32-term fp32 FMA chains folded into double-float; over these
-        # short contractions (<= 600 terms) their rounding averages out less
-        # than in test_mttkrp_fp32_accuracy (~0.5 fp32 ulp)
-        assert rel(got, O.mttkrp(t, f, mode)) <= (1e-12 if dtype == np.float64 else 6e-8)
+        # fp64 arithmetic on either tensor type (fp32 values are exact in fp64)
+        assert rel(got, O.mttkrp(t, f, mode)) <= 1e-12
 
 
 @pytest.mark.parametrize("R,specs", [(150, None), (200, None), (256, None),
