@@ -38,7 +38,7 @@ extern "C" {
 #define NTF_ABI_VERSION 2
 #define NTF_MAX_ORDER 4
 /* Largest CP rank (the reference only requires rank >= 1, solver.py:355-356).
- * Ranks above 128 run the CUDA-core MTTKRP in 128-column chunks, the row
+ * Ranks above 128 run the fp64-arithmetic MTTKRP in 128-column chunks, the row
  * update and the ridge Cholesky against L held in global memory (L2). */
 #define NTF_MAX_RANK 256
 
