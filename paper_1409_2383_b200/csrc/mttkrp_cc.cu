@@ -36,6 +36,7 @@
 // bitwise run-to-run deterministic.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "mttkrp_cc.cuh"
@@ -47,7 +48,7 @@ namespace ntf {
 namespace {
 
 constexpr int kBQ = 32;
-constexpr int kStages = 3;
+constexpr int kMaxStages = 5;
 constexpr int kClusterSplits = 8;
 constexpr int kColChunk = 128;  // output columns per CTA (8 warps x TR = 16)
 
@@ -270,29 +271,32 @@ __global__ void __launch_bounds__((32 * TM / 16 + kProdWarps) * 32, 1) mttkrp_cc
     // rows straight from the stage and form each KR fragment as they load it
     // (one DMUL per two DMMAs: F_lo[l, n] * F_hi[h, n], rounded once, as the
     // reference's khatri_rao), so no warp ever waits on address arithmetic.
-    // Named barriers 1..3: stage landed, 4..6: stage consumed, 7: producers.
+    // Named barriers 1..5: stage landed, 8..12: stage consumed, 15: producers.
     constexpr int kAll = (kMathWarps + kProdWarps) * 32;
     const int n_it = static_cast<int>(c_end - c_begin);
-    const int ns = p.n_stages;  // 3; 2 where three stages do not fit (wide chunks over tiny extents)
+    const int ns = p.n_stages;  // 2..5: as many stages as fit (latency of the loads, see the plan)
     if (n_it > 0 && warp >= kMathWarps) {
       load_stage(c_begin, 0);
       cp_async_commit();
-      if (ns == 3) {
-        if (n_it > 1) load_stage(c_begin + 1, 1);
+      for (int k = 1; k < ns - 1; ++k) {  // prologue: ns - 1 chunks in flight
+        if (k < n_it) load_stage(c_begin + k, k);
         cp_async_commit();
       }
       for (int it = 0; it < n_it; ++it) {
-        if (ns == 3) cp_async_wait<1>();         // this thread's copies of chunk it
+        // this thread's copies of chunk it (ns - 2 younger groups may be pending)
+        if (ns >= 5) cp_async_wait<3>();
+        else if (ns == 4) cp_async_wait<2>();
+        else if (ns == 3) cp_async_wait<1>();
         else cp_async_wait<0>();
-        named_bar_sync(7, 32 * kProdWarps);      // ... and every producer's
+        named_bar_sync(15, 32 * kProdWarps);     // ... and every producer's
         named_bar_arrive(1 + it % ns, kAll);
-        if (it >= 1) named_bar_sync(4 + (it - 1) % ns, kAll);  // chunk it - 1 consumed: its stage is free
+        if (it >= 1) named_bar_sync(8 + (it - 1) % ns, kAll);  // chunk it - 1 consumed: its stage is free
 #if !(defined(NTF_DIAG) && defined(NTF_CC_SKIP_LOAD))  // diagnostic builds only: time the math alone
         if (it + ns - 1 < n_it) load_stage(c_begin + it + ns - 1, (it + ns - 1) % ns);
 #endif
         cp_async_commit();
       }
-      named_bar_sync(4 + (n_it - 1) % ns, kAll);
+      named_bar_sync(8 + (n_it - 1) % ns, kAll);
       cp_async_wait<0>();
     } else if (n_it > 0) {
       const int g = lane >> 2, t4 = lane & 3;
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__((32 * TM / 16 + kProdWarps) * 32, 1) mttkrp_cc
         };
         if (l0 + kBQ > L) run_chunk(std::true_type{}, std::integral_constant<int, TR>{});
         else dispatch_nb<TR, TR / 2 + 1>(nb8, [&](auto nbtag) { run_chunk(std::false_type{}, nbtag); });
-        named_bar_arrive(4 + st, kAll);
+        named_bar_arrive(8 + st, kAll);
       }
     }
   }
@@ -588,12 +592,12 @@ MttkrpCCLaunch mttkrp_cc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.max_hi = static_cast<int>(std::min<int64_t>(kBQ, (kBQ - 1) / lo_ext + 2));
   int fac = (L.max_hi + kBQ) * L.R_pad * 8;  // staged factor rows
   L.stage_bytes = ((tile + fac) + 15) & ~15;
-  L.stages = kStages;
+  // as many stages as fit, up to kMaxStages (the loads of ns - 1 chunks are in flight)
+  L.stages = std::min(kMaxStages, std::max(2, smem_optin_cached() / L.stage_bytes));
+#if defined(NTF_DIAG)
+  if (const char* e = getenv("NTF_CC_STAGES")) L.stages = std::min(L.stages, std::max(2, atoi(e)));
+#endif
   L.smem_bytes = L.stages * L.stage_bytes;
-  if (L.smem_bytes > smem_optin_cached()) {  // wide chunks over tiny extents (max_hi rows)
-    L.stages = 2;
-    L.smem_bytes = L.stages * L.stage_bytes;
-  }
   const int part_bytes = BM * R * 8;  // cluster-reduction tile reuses the stage ring
   if (part_bytes > L.smem_bytes) L.smem_bytes = part_bytes;
   // One wave: as many clusters as can be co-resident (whole clusters per GPC),
