@@ -468,7 +468,7 @@ def main():
             "config": workload_config(w, world, args.engine, rho0, sharded),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "MTTKRP op (fp32: W-slice + tcgen05 kernels; fp64: CUDA-core kernel), all modes: "
+                         "kernel": "MTTKRP op (fp32: W-slice + tcgen05 kernels; fp64 / engine cuda_core: the fp64-arithmetic DMMA kernel), all modes: "
                                    "CUDA events on the solver stream around each of the "
                                    f"{3 * w.inner} MTTKRP launches of the last timed step (kernels "
                                    "serialised, no PDL overlap)",

@@ -98,6 +98,25 @@ def main():
         open(os.path.join(OUT, f"r02_mttkrp_{cfg}_ncu.txt"), "w").write("\n".join(out) + "\n")
         traffic[cfg] = {"bytes_per_launch": rd + wr, "kernel": name,
                         "source": f"profiles/r02_mttkrp_{cfg}_ncu.txt"}
+    # the fp64-arithmetic engine (DMMA pipeline) at 1000^3 fp64, R = 50, mode 1
+    rep = os.path.join(GRO, "r02_mttkrp_cc64.ncu-rep")
+    if os.path.exists(rep):
+        vals, det, num = full_capture(rep)
+        name = vals.get("Kernel Name", ("", "?"))[1]
+        rd, wr, dur = num("dram__bytes_read.sum"), num("dram__bytes_write.sum"), num("gpu__time_duration.sum")
+        flops = 2.0 * 1e9 * 56  # 7 issued 8-column blocks
+        out = ["# ncu --set full --clock-control none --import-source on, one mode-1 launch of the fp64-arithmetic "
+               "engine (`tools/time_modes.py custom cuda_core 1000 1000 1000 50 1 float64`, -k regex:mttkrp_cc -s 2 -c 1)",
+               f"kernel: {name}",
+               f"dram bytes read {rd / 1e9:.4f} GB, written {wr / 1e6:.3f} MB, duration {dur * 1e3:.4f} ms, "
+               f"DRAM throughput {(rd + wr) / dur / 1e12:.3f} TB/s, issued DMMA flops {flops / dur / 1e12:.1f} TFLOP/s "
+               "of 37.0 measured (tools/ubench/f64_rate.cu)"]
+        for k in ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_tensor_op_dmma.sum", "smsp__inst_executed.sum"):
+            if k in vals:
+                out.append(f"{k} = {vals[k][1]} {vals[k][0]}")
+        out += [ln.rstrip() for ln in det.splitlines() if any(k in ln for k in keep)]
+        open(os.path.join(OUT, "r02_mttkrp_cc64_ncu.txt"), "w").write("\n".join(out) + "\n")
     json.dump(traffic, open(os.path.join(OUT, "ncu_traffic.json"), "w"), indent=1)
     print(json.dumps(traffic, indent=1))
 
