@@ -396,6 +396,14 @@ def _sharded_problem_class():
                 sharded_iteration(self, self.comm, self.config)
             self._eager_steps += 1
 
+        def run(self, n_iters: int, use_graph: bool = True) -> None:
+            """``n_iters`` outer iterations without a host synchronisation
+            (the stop flag lives on the device: iterations after a stop are
+            no-ops, as in the single-GPU plan); the caller checks the status
+            once per chunk."""
+            for _ in range(int(n_iters)):
+                self.step()
+
         def _capture(self):
             import warnings
 

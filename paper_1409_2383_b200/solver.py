@@ -376,7 +376,7 @@ def _run_fit(prob, x, dims, rank: int, config: SolverConfig, x_norm: float,
              gather=None) -> FitResult:
     """Restart loop shared by ``fit`` and ``distributed_fit``.  ``gather``
     (sharded runs) returns the full aux/dual matrices from the owned rows."""
-    per_iter_host = config.track_factors or config.track_rfe or gather is not None
+    per_iter_host = config.track_factors or config.track_rfe
     stoppable = config.eps_abs > 0 or config.eps_rel > 0
     total = 0
     converged = False

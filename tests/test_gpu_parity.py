@@ -42,6 +42,35 @@ def test_mttkrp_fp64_matches_oracle(dims, R, engine):
         assert rel(got, O.mttkrp(t, f, mode)) <= 1e-12
 
 
+@pytest.mark.parametrize("dims,R", [
+    ((130, 40, 64), 5),     # K a multiple of the chunk, one 8-column block, ragged second m-tile
+    ((70, 33, 31), 12),     # odd K < chunk: every chunk straddles F_hi rows, scalar copies
+    ((20, 200, 36), 17),    # odd R: 8-byte factor-row copies
+    ((96, 50, 48), 24), ((150, 30, 40), 40), ((64, 70, 34), 48), ((200, 24, 66), 56),
+    ((40, 90, 100), 64),    # block counts 3..8 of the 128-row kernels
+    ((90, 40, 44), 72), ((48, 64, 80), 100),  # 64-row kernels (9 and 13 blocks)
+    ((300, 6, 4), 128),     # 16 blocks over tiny extents (the stage ring shrinks)
+    ((4, 6, 1000), 20),     # two rows, long contraction
+])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_fp64_engine_geometries(dims, R, dtype):
+    """The fp64-arithmetic engine (DMMA fragments, DESIGN 4b) over its tile
+    geometries: every 8-column block count class, vector and scalar copies,
+    chunks that straddle F_hi rows, ragged m-tiles, fp32 and fp64 tensors —
+    all at the fp64 bar (fp32 values are exact in fp64)."""
+    rng = np.random.default_rng(sum(dims) + R)
+    x = (rng.random(dims) - 0.3).astype(dtype)
+    f = [rng.random((d, R)) - 0.4 for d in dims]
+    t = O.OracleTensor(x.astype(np.float64))
+    for mode in (1, 2, 3):
+        got = P.mttkrp_factors(P.DenseTensor(x), f, mode, engine="cuda_core")
+        want = O.mttkrp(t, f, mode)
+        # mixed signs: the bar is relative to |X_(n)| |KR| (the sums cancel)
+        kr = O.khatri_rao([f[m - 1] for m in O.companion_modes(mode, 3)])
+        scale = np.linalg.norm(np.abs(t.unfolding(mode)) @ np.abs(kr))
+        assert np.linalg.norm(got - want) <= 1e-12 * scale, (mode, dims, R)
+
+
 def test_mttkrp_golden_ones():  # reference test_tensors.py:143-146
     x = np.einsum("i,j,k->ijk", [1.0, 2.0], np.ones(2), np.ones(2))
     got = P.mttkrp_factors(P.DenseTensor(x), [np.ones((2, 1))] * 3, 1)
