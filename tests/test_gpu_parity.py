@@ -71,6 +71,26 @@ def test_fp64_engine_geometries(dims, R, dtype):
         assert np.linalg.norm(got - want) <= 1e-12 * scale, (mode, dims, R)
 
 
+@pytest.mark.parametrize("dims,R,dtype", [((300, 200, 150), 50, np.float64), ((257, 130, 96), 100, np.float32),
+                                          ((1000, 40, 30), 20, np.float64)])
+def test_fp64_engine_bitwise_repeatable(dims, R, dtype):
+    """The producer / DMMA-warp pipeline (named barriers, cp.async ring) and
+    the cluster reduction have no float atomics and a fixed order: 25 launches
+    per mode give bit-identical results (a race in the stage hand-over would
+    show up here), and they match the oracle."""
+    rng = np.random.default_rng(8)
+    x = rng.random(dims).astype(dtype)
+    f = _factors(rng, dims, R)
+    t = P.DenseTensor(x)
+    ot = O.OracleTensor(x.astype(np.float64))
+    for mode in (1, 2, 3):
+        first = P.mttkrp_factors(t, f, mode, engine="cuda_core")
+        assert rel(first, O.mttkrp(ot, f, mode)) <= 1e-12
+        for _ in range(24):
+            again = P.mttkrp_factors(t, f, mode, engine="cuda_core")
+            assert np.array_equal(first, again), mode
+
+
 def test_mttkrp_golden_ones():  # reference test_tensors.py:143-146
     x = np.einsum("i,j,k->ijk", [1.0, 2.0], np.ones(2), np.ones(2))
     got = P.mttkrp_factors(P.DenseTensor(x), [np.ones((2, 1))] * 3, 1)
