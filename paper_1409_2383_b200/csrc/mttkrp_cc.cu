@@ -18,7 +18,7 @@
 // 128: one grid z-slice per 128-column chunk).  The reduction range is cut
 // into chunks of BQ = 32 q-values; each chunk's stage (the X tile + the fp64
 // F_hi / F_lo rows its Khatri-Rao rows need) is streamed by 16-byte cp.async
-// through a 3-stage ring by four producer warps.  The math runs on the fp64
+// through a ring of up to five stages by four producer warps.  The math runs on the fp64
 // tensor pipe: DMMA warp w owns rows [16w, 16w + 16) and all columns as
 // m8n8k4 fragments (A = X, converted to fp64 when the tensor is fp32; B = the
 // KR row, F_lo[l, n] * F_hi[h, n] rounded once as the reference's khatri_rao,
@@ -50,7 +50,7 @@ namespace {
 constexpr int kBQ = 32;
 constexpr int kMaxStages = 5;
 constexpr int kClusterSplits = 8;
-constexpr int kColChunk = 128;  // output columns per CTA (8 warps x TR = 16)
+constexpr int kColChunk = 128;  // output columns per CTA (16 8-column blocks)
 
 template <typename XT, int TM, bool KIND_M, bool VEC>
 struct Geom {

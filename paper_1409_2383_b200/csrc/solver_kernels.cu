@@ -710,10 +710,14 @@ __global__ void finalize_kernel(FinalizeParams p) {
 // sum x^2 and sum (x - [[A,B,C]])^2 with fp64 accumulation (tensors.py:57-61,
 // 276-290).  Block = one i and kSqJ consecutive j; threads along k.
 // ---------------------------------------------------------------------------
-constexpr int kSqJ = 8;
+constexpr int kSqJ = 8;        // j values per block: narrow tensors
+constexpr int kSqJWide = 32;   // ... and the others (C^T is re-read from L2 once per block: 1/4 of the traffic)
 constexpr int kSqThreads = 256;
 
-template <typename XT>
+// the norm-only pass (no model) streams X: narrow tiles, more blocks per SM
+__host__ __device__ constexpr int sq_jt(int64_t J, bool model) { return model && J >= 24 ? kSqJWide : kSqJ; }
+
+template <typename XT, int JT>
 __global__ void __launch_bounds__(kSqThreads) sq_error_kernel(const XT* __restrict__ X, int64_t I,
                                                               int64_t J, int64_t K,
                                                               const double* __restrict__ A,
@@ -721,14 +725,14 @@ __global__ void __launch_bounds__(kSqThreads) sq_error_kernel(const XT* __restri
                                                               const double* __restrict__ CT,
                                                               int R, double* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* ab = reinterpret_cast<double*>(smem_raw);  // [kSqJ][R]
-  const int64_t nj_blocks = (J + kSqJ - 1) / kSqJ;
+  double* ab = reinterpret_cast<double*>(smem_raw);  // [R][JT]: A[i, r] * B[j0 + jj, r]
+  const int64_t nj_blocks = (J + JT - 1) / JT;
   const int64_t i = blockIdx.x / nj_blocks;
-  const int64_t j0 = (blockIdx.x - i * nj_blocks) * kSqJ;
+  const int64_t j0 = (blockIdx.x - i * nj_blocks) * JT;
   const bool model = A != nullptr;
   if (model) {
-    for (int e = threadIdx.x; e < kSqJ * R; e += blockDim.x) {
-      const int jj = e / R, r = e - (e / R) * R;
+    for (int e = threadIdx.x; e < JT * R; e += blockDim.x) {
+      const int r = e / JT, jj = e - r * JT;
       const int64_t j = j0 + jj;
       ab[e] = j < J ? A[i * R + r] * B[j * R + r] : 0.0;
     }
@@ -736,18 +740,23 @@ __global__ void __launch_bounds__(kSqThreads) sq_error_kernel(const XT* __restri
   __syncthreads();
   double sx = 0.0, se = 0.0;
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-    double rec[kSqJ];
+    double rec[JT];
 #pragma unroll
-    for (int jj = 0; jj < kSqJ; ++jj) rec[jj] = 0.0;
+    for (int jj = 0; jj < JT; ++jj) rec[jj] = 0.0;
     if (model) {
       for (int r = 0; r < R; ++r) {
         const double c = CT[static_cast<int64_t>(r) * K + k];
+        const double2* abr = reinterpret_cast<const double2*>(ab + r * JT);  // 16-byte broadcasts
 #pragma unroll
-        for (int jj = 0; jj < kSqJ; ++jj) rec[jj] = fma(ab[jj * R + r], c, rec[jj]);
+        for (int jj = 0; jj < JT; jj += 2) {
+          const double2 v = abr[jj >> 1];
+          rec[jj] = fma(v.x, c, rec[jj]);
+          rec[jj + 1] = fma(v.y, c, rec[jj + 1]);
+        }
       }
     }
 #pragma unroll
-    for (int jj = 0; jj < kSqJ; ++jj) {
+    for (int jj = 0; jj < JT; ++jj) {
       const int64_t j = j0 + jj;
       if (j < J) {
         const double x = static_cast<double>(X[(i * J + j) * K + k]);
@@ -1080,29 +1089,43 @@ cudaError_t finalize_launch(const FinalizeParams& p, cudaStream_t stream) {
 }
 
 size_t sq_error_workspace_bytes(int64_t I, int64_t J, int64_t K, int R) {
-  const int64_t nb = I * ((J + kSqJ - 1) / kSqJ);
+  const int64_t nb = I * ((J + kSqJ - 1) / kSqJ);  // the narrow tiling has the most blocks
   return static_cast<size_t>(nb) * 2 * sizeof(double) + static_cast<size_t>(K) * R * sizeof(double);
+}
+
+template <typename XT, int JT>
+cudaError_t sq_error_dispatch(const void* X, int64_t I, int64_t J, int64_t K, const double* A,
+                              const double* B, const double* CT, int R, double* part, int64_t nb,
+                              cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(JT) * (R > 0 ? R : 1) * sizeof(double);
+  auto kern = sq_error_kernel<XT, JT>;
+  if (smem > 48 * 1024) {  // 32 j values x ranks above 192
+    cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<static_cast<unsigned>(nb), kSqThreads, smem, stream>>>(static_cast<const XT*>(X), I, J, K, A, B, CT,
+                                                               R, part);
+  return cudaGetLastError();
 }
 
 cudaError_t sq_error_launch(int x_dtype, const void* X, int64_t I, int64_t J, int64_t K,
                             const double* A, const double* B, const double* C, int R, double* out2,
                             void* ws, cudaStream_t stream) {
-  const int64_t nb = I * ((J + kSqJ - 1) / kSqJ);
+  const int jt = sq_jt(J, A != nullptr);
+  const int64_t nb = I * ((J + jt - 1) / jt);
   double* part = static_cast<double*>(ws);
   double* CT = part + nb * 2;
   if (A) {
     transpose_kernel<<<static_cast<unsigned>(std::min<int64_t>((K * R + 255) / 256, 4096)), 256, 0,
                        stream>>>(C, K, R, CT);
   }
-  const size_t smem = static_cast<size_t>(kSqJ) * (R > 0 ? R : 1) * sizeof(double);
-  if (x_dtype == NTF_F32) {
-    sq_error_kernel<float><<<static_cast<unsigned>(nb), kSqThreads, smem, stream>>>(
-        static_cast<const float*>(X), I, J, K, A, B, CT, R, part);
-  } else {
-    sq_error_kernel<double><<<static_cast<unsigned>(nb), kSqThreads, smem, stream>>>(
-        static_cast<const double*>(X), I, J, K, A, B, CT, R, part);
-  }
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if (x_dtype == NTF_F32)
+    e = jt == kSqJWide ? sq_error_dispatch<float, kSqJWide>(X, I, J, K, A, B, CT, R, part, nb, stream)
+                       : sq_error_dispatch<float, kSqJ>(X, I, J, K, A, B, CT, R, part, nb, stream);
+  else
+    e = jt == kSqJWide ? sq_error_dispatch<double, kSqJWide>(X, I, J, K, A, B, CT, R, part, nb, stream)
+                       : sq_error_dispatch<double, kSqJ>(X, I, J, K, A, B, CT, R, part, nb, stream);
   if (e != cudaSuccess) return e;
   sum_pairs_kernel<<<1, 256, 0, stream>>>(part, nb, out2);
   return cudaGetLastError();
