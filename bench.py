@@ -339,6 +339,8 @@ def main():
     for i in range(args.warmup):
         prob.set_timing(timed_last and i == args.warmup - 1)
         prob.step()
+    if sharded:
+        prob.precapture()  # the plain graph too (captured lazily otherwise: inside the timed region)
     prob.stream.synchronize()
     if sharded:
         dist.barrier()

@@ -396,6 +396,19 @@ def _sharded_problem_class():
                 sharded_iteration(self, self.comm, self.config)
             self._eager_steps += 1
 
+        def precapture(self) -> None:
+            """Capture whichever of the two iteration graphs (plain /
+            instrumented) does not exist yet, without running an iteration:
+            a timed region then never contains a capture."""
+            if not self._graph_ok or self._eager_steps < 2:
+                return
+            keep = self._timing
+            for timing in (False, True):
+                if self._graphs[timing] is None:
+                    self.set_timing(timing)
+                    self._capture()
+            self.set_timing(keep)
+
         def run(self, n_iters: int, use_graph: bool = True) -> None:
             """``n_iters`` outer iterations without a host synchronisation
             (the stop flag lives on the device: iterations after a stop are
