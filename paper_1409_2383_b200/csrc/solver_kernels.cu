@@ -782,6 +782,105 @@ __global__ void __launch_bounds__(kSqThreads) sq_error_kernel(const XT* __restri
   }
 }
 
+// The same sums on the fp64 tensor pipe, for tensors at least kSqJWide wide
+// with a model: a block owns one i and kSqJWide j values and walks k in tiles
+// of 256; each warp reconstructs a 32 (j) x 32 (k) tile as m8n8k4 DMMA
+// fragments, D[j][k] += (A[i, r] B[j, r]) C[k, r] (A operand: the A*B rows in
+// shared memory, pitch 4 mod 16 doubles; B operand: C^T rows from L2, 64-byte
+// pieces), then subtracts it from X in the accumulator-fragment layout (each
+// lane reads two consecutive k of one j row: full 32-byte sectors).  The
+// products a*b are rounded once and the sums over r run in fp64, as
+// tensors.reconstruct; the order of the r sum differs from the FMA kernel's
+// at the 1e-16 level.  Per-thread partial sums in a fixed order: deterministic.
+template <typename XT>
+__global__ void __launch_bounds__(kSqThreads, 2) sq_error_dmma_kernel(const XT* __restrict__ X, int64_t I,
+                                                                      int64_t J, int64_t K,
+                                                                      const double* __restrict__ A,
+                                                                      const double* __restrict__ B,
+                                                                      const double* __restrict__ CT,
+                                                                      int R, int pitch,
+                                                                      double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* ab = reinterpret_cast<double*>(smem_raw);  // [kSqJWide][pitch]: A[i, r] * B[j0 + jj, r], zero padded
+  constexpr int JT = kSqJWide;
+  const int64_t nj_blocks = (J + JT - 1) / JT;
+  const int64_t i = blockIdx.x / nj_blocks;
+  const int64_t j0 = (blockIdx.x - i * nj_blocks) * JT;
+  const int R4 = (R + 3) & ~3;
+  for (int e = threadIdx.x; e < JT * R4; e += blockDim.x) {
+    const int jj = e / R4, r = e - jj * R4;
+    const int64_t j = j0 + jj;
+    ab[jj * pitch + r] = (j < J && r < R) ? A[i * R + r] * B[j * R + r] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  double sx = 0.0, se = 0.0;
+  for (int64_t kt = static_cast<int64_t>(warp) * 32; kt < K; kt += (kSqThreads / 32) * 32) {
+    double d[4][4][2];  // [j block][k block][2]
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+    // B fragment rows: C^T[r + t4][kt + 8 b + g] (zero outside K or R)
+    int64_t kb[4];
+    bool kv[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      kb[b] = kt + 8 * b + g;
+      kv[b] = kb[b] < K;
+    }
+    for (int r = 0; r < R4; r += 4) {
+      const bool rv = r + t4 < R;
+      const double* ctr = CT + static_cast<int64_t>(r + t4) * K;
+      double bf[4], af[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = (rv && kv[b]) ? ctr[kb[b]] : 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = ab[(8 * a + g) * pitch + r + t4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(d[a][b][0]), "+d"(d[a][b][1])
+                       : "d"(af[a]), "d"(bf[b]));
+    }
+    // D[j = 8 a + g][k = kt + 8 b + 2 t4 + {0, 1}] against X
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t j = j0 + 8 * a + g;
+      if (j >= J) continue;
+      const XT* xr = X + (i * J + j) * K;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t k = kt + 8 * b + 2 * t4;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (k + u < K) {
+            const double x = static_cast<double>(xr[k + u]);
+            const double df = x - d[a][b][u];
+            sx += x * x;
+            se += df * df;
+          }
+      }
+    }
+  }
+  __shared__ double red[2][kSqThreads / 32];
+  sx = warp_sum(sx);
+  se = warp_sum(se);
+  if (lane == 0) {
+    red[0][warp] = sx;
+    red[1][warp] = se;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double s = 0.0;
+    for (int w = 0; w < kSqThreads / 32; ++w) s += red[threadIdx.x][w];
+    part[static_cast<int64_t>(blockIdx.x) * 2 + threadIdx.x] = s;
+  }
+}
+
 __global__ void transpose_kernel(const double* __restrict__ C, int64_t K, int R,
                                  double* __restrict__ CT) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * R;
@@ -1120,12 +1219,29 @@ cudaError_t sq_error_launch(int x_dtype, const void* X, int64_t I, int64_t J, in
                        stream>>>(C, K, R, CT);
   }
   cudaError_t e;
-  if (x_dtype == NTF_F32)
-    e = jt == kSqJWide ? sq_error_dispatch<float, kSqJWide>(X, I, J, K, A, B, CT, R, part, nb, stream)
-                       : sq_error_dispatch<float, kSqJ>(X, I, J, K, A, B, CT, R, part, nb, stream);
-  else
-    e = jt == kSqJWide ? sq_error_dispatch<double, kSqJWide>(X, I, J, K, A, B, CT, R, part, nb, stream)
-                       : sq_error_dispatch<double, kSqJ>(X, I, J, K, A, B, CT, R, part, nb, stream);
+  if (jt == kSqJWide) {  // wide tensors with a model: the fp64 tensor pipe
+    int pitch = (R + 3) & ~3;
+    while (pitch % 16 != 4 && pitch % 16 != 12) ++pitch;  // conflict-free A fragments
+    const size_t smem = static_cast<size_t>(kSqJWide) * pitch * sizeof(double);
+    if (x_dtype == NTF_F32) {
+      auto kern = sq_error_dmma_kernel<float>;
+      e = smem > 48 * 1024 ? allow_dyn_smem(reinterpret_cast<const void*>(kern), smem) : cudaSuccess;
+      if (e == cudaSuccess)
+        kern<<<static_cast<unsigned>(nb), kSqThreads, smem, stream>>>(static_cast<const float*>(X), I, J, K, A,
+                                                                     B, CT, R, pitch, part);
+    } else {
+      auto kern = sq_error_dmma_kernel<double>;
+      e = smem > 48 * 1024 ? allow_dyn_smem(reinterpret_cast<const void*>(kern), smem) : cudaSuccess;
+      if (e == cudaSuccess)
+        kern<<<static_cast<unsigned>(nb), kSqThreads, smem, stream>>>(static_cast<const double*>(X), I, J, K, A,
+                                                                     B, CT, R, pitch, part);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+  } else if (x_dtype == NTF_F32) {
+    e = sq_error_dispatch<float, kSqJ>(X, I, J, K, A, B, CT, R, part, nb, stream);
+  } else {
+    e = sq_error_dispatch<double, kSqJ>(X, I, J, K, A, B, CT, R, part, nb, stream);
+  }
   if (e != cudaSuccess) return e;
   sum_pairs_kernel<<<1, 256, 0, stream>>>(part, nb, out2);
   return cudaGetLastError();

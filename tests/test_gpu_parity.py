@@ -208,6 +208,24 @@ def test_norm_and_rfe_kernel():
     assert out[1] == pytest.approx(np.linalg.norm(x - O.reconstruct(f)) ** 2, rel=1e-12)
 
 
+@pytest.mark.parametrize("dims,R,dtype", [((5, 24, 33), 3, np.float64), ((3, 40, 300), 10, np.float32),
+                                          ((2, 65, 257), 21, np.float64), ((4, 32, 64), 100, np.float32),
+                                          ((1, 100, 7), 256, np.float64)])
+def test_rfe_kernel_wide_tensors(dims, R, dtype):
+    """Tensors at least 24 wide in mode 2 take the DMMA reconstruction
+    kernel: ragged j and k tiles, ranks that are not multiples of 4, fp32 and
+    fp64 tensors, against the explicit reconstruction (tensors.py:276-290)."""
+    rng = np.random.default_rng(R)
+    f = [rng.random((d, R)) - 0.2 for d in dims]
+    x = (O.reconstruct(f) + 0.05 * rng.standard_normal(dims)).astype(dtype)
+    from paper_1409_2383_b200.engine import device_tensor, sq_error
+
+    out = sq_error(device_tensor(P.DenseTensor(x)), f).cpu().numpy()
+    x64 = x.astype(np.float64)
+    assert out[0] == pytest.approx(np.sum(x64 ** 2), rel=1e-12)
+    assert out[1] == pytest.approx(np.sum((x64 - O.reconstruct(f)) ** 2), rel=1e-11)
+
+
 def _cmp_fit(res, g, name, tol=1e-9):
     assert res.iterations == int(g[f"{name}_iterations"])
     assert res.restarts == int(g[f"{name}_restarts"])
