@@ -682,10 +682,12 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
     // order 4: of the mode's reshaped view)
     for (int m = 0; m < N; ++m) {
       if (!pl->op[m].tc) continue;
+      // one max|X| pass per distinct tensor (the unsharded plan's modes share one)
+      const ntf::TcTensor* same = pl->n_tct > 0 ? &pl->tct[0] : nullptr;
       ntf::TcTensor& slot = pl->tct[pl->n_tct++];
       const int64_t* xd = N == 4 ? vdims[m < 2 ? 0 : 1] : d.x_dims[m];
       if ((e = ntf::tc_tensor_create(pl->op[m].tcl, static_cast<const float*>(d.x_mode[m]), xd,
-                                     &slot, nullptr)) != cudaSuccess)
+                                     &slot, nullptr, same)) != cudaSuccess)
         return cleanup(cuda_fail(e, "tc split"));
       pl->op[m].tct = &slot;
       if ((e = ntf::mttkrp_tc_bind(pl->op[m].tcl, slot)) != cudaSuccess)
@@ -702,9 +704,12 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
 int ntf_plan_refresh_tensor(ntf_plan* pl, ntf_stream_t stream) {
   if (!pl) return fail(NTF_ERR_INVALID, "null plan");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const ntf::TcTensor* first = nullptr;
   for (int m = 0; m < pl->order; ++m) {
     const MttkrpOp& op = pl->op[m];
-    if (op.tc && op.tct) NTF_CUDA_TRY(ntf::tc_tensor_fill(op.tcl, *op.tct, s));
+    if (!op.tc || !op.tct) continue;
+    NTF_CUDA_TRY(ntf::tc_tensor_fill(op.tcl, *op.tct, s, first));
+    if (!first) first = op.tct;
   }
   return NTF_OK;
 }

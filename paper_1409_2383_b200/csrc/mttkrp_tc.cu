@@ -1488,12 +1488,18 @@ cudaError_t mttkrp_tc_prepare(const MttkrpTCLaunch& L) {
   return dispatch_tc(p, L, nullptr, true);
 }
 
-cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream) {
+cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream,
+                           const TcTensor* same_values) {
   const int64_t n = t.dims[0] * t.dims[1] * t.dims[2];
   unsigned* amax = reinterpret_cast<unsigned*>(t.xscale + 1);
-  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
-  if (e != cudaSuccess) return e;
-  absmax_kernel<<<4 * sm_count_tc(), 256, 0, stream>>>(t.src, n, amax);
+  if (same_values && same_values->src == t.src && same_values->xscale &&
+      same_values->dims[0] * same_values->dims[1] * same_values->dims[2] == n) {
+    amax = reinterpret_cast<unsigned*>(same_values->xscale + 1);  // max|X| of the same values
+  } else {
+    cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned), stream);
+    if (e != cudaSuccess) return e;
+    absmax_kernel<<<4 * sm_count_tc(), 256, 0, stream>>>(t.src, n, amax);
+  }
   ImgGeom g;
   g.mode = L.mode;
   g.I = t.dims[0];
@@ -1516,7 +1522,7 @@ cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStrea
 }
 
 cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
-                             TcTensor* out, cudaStream_t stream) {
+                             TcTensor* out, cudaStream_t stream, const TcTensor* same_values) {
   TcTensor t;
   for (int i = 0; i < 3; ++i) t.dims[i] = dims[i];
   t.mode = L.mode;
@@ -1528,7 +1534,7 @@ cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int6
     tc_tensor_destroy(&t);
     return e;
   }
-  if ((e = tc_tensor_fill(L, t, stream)) != cudaSuccess) {
+  if ((e = tc_tensor_fill(L, t, stream, same_values)) != cudaSuccess) {
     tc_tensor_destroy(&t);
     return e;
   }

@@ -25,11 +25,14 @@ struct TcTensor {
 };
 
 struct MttkrpTCLaunch;
+// same_values: an image already split (on this stream) from the same tensor
+// values; its max|X| is reused instead of another pass over the tensor.
 cudaError_t tc_tensor_create(const MttkrpTCLaunch& L, const float* X, const int64_t dims[3],
-                             TcTensor* out, cudaStream_t stream);
+                             TcTensor* out, cudaStream_t stream, const TcTensor* same_values = nullptr);
 void tc_tensor_destroy(TcTensor* t);
 // Re-split t.src into the existing image (the tensor's values changed in place).
-cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream);
+cudaError_t tc_tensor_fill(const MttkrpTCLaunch& L, const TcTensor& t, cudaStream_t stream,
+                           const TcTensor* same_values = nullptr);
 
 constexpr int kTcMaxSplits = 160;  // CTAs per m-tile
 constexpr int kTcMaxXStages = 32;  // X ring slots
