@@ -161,6 +161,25 @@ def _gather_worker(rank, world, port, out_path):
         comm.all_reduce_max_(cm)
         assert torch.all(g == sum(range(1, world + 1)))
         assert cm.tolist() == [world - 1.0, 10.0, 0.5]
+        # ... and the one-collective form of both (Comm.gather_rows_closing):
+        # rows, Gram and column maxima of the owned rows in one all-gather
+        full3 = torch.full((11, 3), -1.0, dtype=torch.float64)
+        full3[o:o + c] = full[o:o + c]
+        own = full3[o:o + c]
+        g3 = own.T @ own
+        cm3 = own.abs().amax(dim=0) if c else torch.zeros(3, dtype=torch.float64)
+        g_parts = [torch.zeros(3, 3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(g_parts, g3.clone())
+        for _ in range(2):  # the buffers are reused by the second call
+            gg, cc = g3.clone(), cm3.clone()
+            comm.gather_rows_closing(full3, offs, cnts, gg, cc)
+            assert torch.equal(full3, full)
+            want = g_parts[0].clone()
+            for q in range(1, world):
+                want += g_parts[q]
+            assert torch.equal(gg, want)  # rank-order sum: the same bits on every rank
+            assert torch.equal(cc, full.abs().amax(dim=0))
+            full3[[i for i in range(11) if not o <= i < o + c]] = -1.0
         if rank == 0:
             np.save(out_path, full.numpy())
     finally:
