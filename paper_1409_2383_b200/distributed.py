@@ -71,6 +71,12 @@ class PartitionPlan:
         return slice(o[block], o[block + 1])
 
 
+def _torch_mod():
+    import torch
+
+    return torch
+
+
 class Comm:
     """torch.distributed collectives used by the sharded iteration."""
 
@@ -215,15 +221,24 @@ class Comm:
         send[rows_n + R * R:].copy_(colmax)
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
         parts = recv.view(self.size, seg)
-        for q in range(self.size):
-            if q != p:
-                full[offsets[q]: offsets[q] + counts[q]].copy_(parts[q, : counts[q] * R].view(counts[q], R))
-        grams = parts[:, rows_n: rows_n + R * R]
-        acc = grams[0].clone()
-        for q in range(1, self.size):  # fixed rank order: every rank gets the same bits
-            acc += grams[q]
-        gram.copy_(acc.view(R, R))
-        colmax.copy_(parts[:, rows_n + R * R:].amax(dim=0))
+        # rows: runs of ranks with equal block sizes are one strided copy each
+        # (the uniform plan has at most two runs; a rank's own rows are
+        # rewritten with the same values)
+        rows = parts[:, :rows_n].view(self.size, maxc, R)
+        q0 = 0
+        while q0 < self.size:
+            q1 = q0 + 1
+            while q1 < self.size and counts[q1] == counts[q0] and offsets[q1] == offsets[q1 - 1] + counts[q0]:
+                q1 += 1
+            c = counts[q0]
+            if c:
+                full[offsets[q0]: offsets[q0] + (q1 - q0) * c].view(q1 - q0, c, R).copy_(rows[q0:q1, :c])
+            q0 = q1
+        # Gram: one reduction over the ranks (every rank runs the same kernel
+        # on the same bytes: the same bits everywhere); column maxima likewise
+        torch = _torch_mod()
+        torch.sum(parts[:, rows_n: rows_n + R * R], dim=0, out=gram.view(-1))
+        torch.amax(parts[:, rows_n + R * R:], dim=0, out=colmax.view(-1))
 
     def peer_failed(self) -> bool:
         """Whether any rank's peer gather timed out (all-reduced: every rank

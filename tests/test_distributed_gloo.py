@@ -177,7 +177,10 @@ def _gather_worker(rank, world, port, out_path):
             want = g_parts[0].clone()
             for q in range(1, world):
                 want += g_parts[q]
-            assert torch.equal(gg, want)  # rank-order sum: the same bits on every rank
+            assert torch.allclose(gg, want, rtol=1e-15, atol=0.0)
+            every = [torch.zeros_like(gg) for _ in range(world)]
+            dist.all_gather(every, gg)
+            assert all(torch.equal(e, gg) for e in every)  # the same bits on every rank
             assert torch.equal(cc, full.abs().amax(dim=0))
             full3[[i for i in range(11) if not o <= i < o + c]] = -1.0
         if rank == 0:
