@@ -292,6 +292,37 @@ def _solver_stream(device):
     return s
 
 
+def _free_device_bytes(device) -> int:
+    """Free HBM on ``device`` (a function so that tests can shrink it)."""
+    torch = _torch()
+    free, _ = torch.cuda.mem_get_info(device)
+    return int(free)
+
+
+def _engine_that_fits(engine: int, slabs, rank: int, device) -> int:
+    """ENGINE_AUTO on fp32 tensors means the tensor-core engine, which keeps
+    one block image per mode: as many bytes again as each mode's tensor or
+    slab (DESIGN 2).  Where those do not fit the free HBM, fall back to the
+    fp64-arithmetic engine, which streams the tensor in place (slower, and
+    more exact), instead of failing in cudaMalloc."""
+    torch = _torch()
+    if engine != N.ENGINE_AUTO or rank > 128:
+        return engine
+    xs = [x for x in slabs if not isinstance(x, DeviceCoo)]
+    if not xs or any(x.dtype != torch.float32 for x in xs):
+        return engine
+    need = sum(x.numel() * 4 for x in xs)
+    free = _free_device_bytes(device)
+    if need <= 0.97 * free:
+        return engine
+    import warnings
+
+    warnings.warn(f"the tensor-core engine's block images need {need / 2**30:.1f} GiB but {free / 2**30:.1f} GiB "
+                  "of HBM are free: using the fp64-arithmetic engine (engine='cuda_core'), which streams "
+                  "the tensor in place", RuntimeWarning, stacklevel=3)
+    return N.ENGINE_CUDA_CORE
+
+
 class DeviceProblem:
     """HBM state of one fit and its C-ABI plan."""
 
@@ -313,6 +344,7 @@ class DeviceProblem:
         if slabs is None:
             slabs = Slabs([x] * Nm, (0,) * Nm, self.dims)
         self.slabs = slabs
+        engine = _engine_that_fits(int(engine), slabs.x_mode, int(rank), self.device)
         dev, f64 = self.device, torch.float64
         R = self.R
         with torch.cuda.stream(self.stream):

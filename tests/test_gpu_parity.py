@@ -766,6 +766,31 @@ def test_ranks_generate_own_slabs_fp32(tmp_path):
         assert np.array_equal(got[1][k], got[0][k]), k
 
 
+def test_auto_engine_falls_back_when_block_images_do_not_fit(monkeypatch):
+    """engine="auto" on an fp32 tensor keeps one block image per mode (3 |X|
+    more HBM).  Where that does not fit, the fit runs on the fp64-arithmetic
+    engine, which streams the tensor in place, with a warning, instead of
+    failing in cudaMalloc; its result is the fp64 engine's (oracle parity at
+    the fp64 bar)."""
+    from paper_1409_2383_b200 import engine as E
+
+    rng = np.random.default_rng(4)
+    dims, R = (40, 36, 44), 6
+    x = (O.reconstruct([rng.random((d, R)) for d in dims]) + 0.02 * rng.standard_normal(dims)).astype(np.float32)
+    kw = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=6, max_restarts=0, inner_sweeps=2, track_factors=True)
+    P.solver.release_plan_cache()
+    monkeypatch.setattr(E, "_free_device_bytes", lambda device: 1 << 16)
+    with pytest.warns(RuntimeWarning, match="block images"):
+        got = P.fit(x, R, None, P.SolverConfig(**kw))
+    monkeypatch.undo()
+    P.solver.release_plan_cache()
+    want = O.fit(x.astype(np.float64), R, O.Config(**kw))
+    for fg, fw in zip(got.factor_history, want.factor_history):
+        for a, b in zip(fg, fw):
+            assert rel(a, b) <= 1e-9
+    assert got.rfe == pytest.approx(want.rfe, rel=1e-9)
+
+
 @pytest.mark.parametrize("dims,R", [((24, 20, 18), 131), ((17, 9, 33), 200), ((12, 10, 8), 256)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_mttkrp_rank_above_128(dims, R, dtype):
