@@ -423,6 +423,10 @@ def main():
             def call():
                 return P.fit(P.DenseTensor(host[0]), w.rank, None, cfg_e, engine=engine)
         n_e2e = args.e2e_steps or (2 if math.prod(w.dims) > 2e9 else 3)
+        # fit() picking another engine than the one `value` was measured on (its
+        # block images not fitting the free HBM) would make e2e a different metric
+        import warnings
+        warnings.filterwarnings("error", message=".*block images need.*", category=RuntimeWarning)
         call()  # warm-up
         torch.cuda.synchronize()
         if sharded:

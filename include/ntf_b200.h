@@ -231,6 +231,10 @@ int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out);
  * This returns every unused pool byte to the device (e.g. before allocating
  * a large tensor outside the library).  Synchronises the device. */
 int ntf_trim_device_pool(void);
+/* Bytes the pool holds mapped but unused right now (released plans leave
+ * their memory there): the next plan allocates from them first, so they count
+ * as free HBM although cudaMemGetInfo reports them as taken. */
+int ntf_device_pool_idle_bytes(size_t* bytes);
 /* Column maxima out[r] = max_i |F[i][r]| (sharded runs refresh colmax[m]
  * with this after gathering a factor, as they refresh grams[m]). */
 int ntf_colmax(const double* F, int64_t rows, int R, double* out, ntf_stream_t stream);

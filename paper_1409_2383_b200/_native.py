@@ -49,6 +49,7 @@ EXPORTED = (
     "ntf_khatri_rao_pair",
     "ntf_synth_dense",
     "ntf_trim_device_pool",
+    "ntf_device_pool_idle_bytes",
     "ntf_plan_create",
     "ntf_colmax",
     "ntf_plan_sync_grams",
@@ -187,6 +188,8 @@ def _declare(lib):
                                     ctypes.c_uint64, c_vp]
     lib.ntf_trim_device_pool.restype = c_int
     lib.ntf_trim_device_pool.argtypes = []
+    lib.ntf_device_pool_idle_bytes.restype = c_int
+    lib.ntf_device_pool_idle_bytes.argtypes = [ctypes.POINTER(ctypes.c_size_t)]
     lib.ntf_plan_create.restype = c_int
     lib.ntf_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(c_vp)]
     lib.ntf_colmax.restype = c_int

@@ -508,6 +508,19 @@ int ntf_trim_device_pool(void) {
   return NTF_OK;
 }
 
+int ntf_device_pool_idle_bytes(size_t* bytes) {
+  if (!bytes) return fail(NTF_ERR_INVALID, "null pointer");
+  int dev = 0;
+  cudaMemPool_t pool;
+  cuuint64_t reserved = 0, used = 0;
+  NTF_CUDA_TRY(cudaGetDevice(&dev));
+  NTF_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  NTF_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  NTF_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  *bytes = reserved > used ? static_cast<size_t>(reserved - used) : 0;
+  return NTF_OK;
+}
+
 int ntf_plan_create(const ntf_plan_desc* desc, ntf_plan** out) {
   if (!desc || !out) return fail(NTF_ERR_INVALID, "null pointer");
   *out = nullptr;

@@ -65,6 +65,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "mttkrp_tc.cuh"
 
@@ -390,7 +391,13 @@ __host__ __device__ constexpr uint32_t make_idesc(int N, bool a_mn_major, int cg
 // loses nothing (ACC1's own fp32 rounding dominates) and lets two sets fit.
 // As many sets as fit (up to 4) so the MMA runs ahead of the epilogue.
 __host__ __device__ constexpr bool merged_acc(int N) { return 3 * N > 256; }
-__host__ __device__ constexpr int set_cols(int N) { return merged_acc(N) ? 2 * N : 3 * N; }
+// Packed T0 / T1 ranges (merged sets only; NP = N - 8 when R <= N - 8, else
+// NP = N): the MMA N' must be a multiple of 16, but S0 x [T0|T1] only needs
+// 2 NP columns to be one: R = 100 runs it at N' = 208 instead of 224 (ACC0 in
+// columns [0, NP), ACC12 in [NP, NP + N)), and the epilogue drains NP instead
+// of N columns per accumulator.
+__host__ __device__ constexpr int set_cols(int N, int NP) { return merged_acc(N) ? NP + N : 3 * N; }
+__host__ __device__ constexpr int set_cols(int N) { return set_cols(N, N); }
 __host__ __device__ constexpr int acc_bufs_fit(int N) {
   return 512 / set_cols(N) >= 4 ? 4 : 512 / set_cols(N);
 }
@@ -408,25 +415,32 @@ __host__ __device__ constexpr int t_bits(int G) {
 }
 
 // The B operand (W slices) of one 64-wide l block, virtual rows
-// [T0 | T1 | T2 | Fh] (N rows each; Fh = F_lo rounded to fp16, the operand of
-// S1).  Per K step the MMAs read contiguous row ranges of it:
+// [T0 | T1 | T2 | Fh] (Fh = F_lo rounded to fp16, the operand of S1).  Per K
+// step the MMAs read contiguous row ranges of it:
 //   N <= 85: S0 x [T0|T1|T2] (rows [0, 3N)), S1 x Fh ([3N, 4N))
-//   N >  85: S0 x [T0|T1] ([0, 2N)), S0 x T2 ([2N, 3N)), S1 x Fh ([3N, 4N))
+//   N >  85: S0 x [T0|T1] ([0, 2NP): NP rows each), S0 x T2 (N rows), S1 x Fh (N rows)
 // For a CTA pair each MMA's N' rows are split in halves between the CTAs
 // (the leader's descriptor addresses both CTAs' shared memory at the same
 // offset), so CTA c stores the c-th half of every range, ranges in order:
-// 4N / CG rows per CTA and l block.  Returns CTA and row of virtual row v.
+// w_rows / CG rows per CTA and l block.  Returns CTA and row of virtual row v.
 __host__ __device__ constexpr int w_ranges(int N) { return merged_acc(N) ? 3 : 2; }
-__host__ __device__ constexpr int w_range_begin(int N, int k) {
-  return merged_acc(N) ? (k == 0 ? 0 : (k == 1 ? 2 * N : 3 * N)) : (k == 0 ? 0 : 3 * N);
+__host__ __device__ constexpr int w_range_begin(int N, int NP, int k) {
+  return merged_acc(N) ? (k == 0 ? 0 : (k == 1 ? 2 * NP : 2 * NP + N)) : (k == 0 ? 0 : 3 * N);
 }
-__host__ __device__ constexpr int w_range_end(int N, int k) {
-  return merged_acc(N) ? (k == 0 ? 2 * N : (k == 1 ? 3 * N : 4 * N)) : (k == 0 ? 3 * N : 4 * N);
+__host__ __device__ constexpr int w_range_end(int N, int NP, int k) {
+  return merged_acc(N) ? (k == 0 ? 2 * NP : (k == 1 ? 2 * NP + N : 2 * NP + 2 * N)) : (k == 0 ? 3 * N : 4 * N);
 }
-__host__ __device__ inline void w_row_slot(int N, int CG, int v, int& cta, int& row) {
+__host__ __device__ constexpr int w_rows(int N, int NP) { return merged_acc(N) ? 2 * NP + 2 * N : 4 * N; }
+// virtual row of column n of slice sl (0..3 = T0, T1, T2, Fh); -1: not stored
+// (a padding column of a packed range)
+__host__ __device__ constexpr int w_virtual_row(int N, int NP, int sl, int n) {
+  return !merged_acc(N) ? sl * N + n
+                        : (sl < 2 ? (n < NP ? sl * NP + n : -1) : (sl == 2 ? 2 * NP + n : 2 * NP + N + n));
+}
+__host__ __device__ inline void w_row_slot(int N, int NP, int CG, int v, int& cta, int& row) {
   int off = 0;
   for (int k = 0; k < w_ranges(N); ++k) {
-    const int b = w_range_begin(N, k), e = w_range_end(N, k), h = (e - b) / CG;
+    const int b = w_range_begin(N, NP, k), e = w_range_end(N, NP, k), h = (e - b) / CG;
     if (v < e) {
       cta = (v - b) / h;
       row = off + (v - b) - cta * h;
@@ -465,7 +479,7 @@ struct TcParams {
   int stage_bytes;           // X ring slot stride (slot_ks * 64 * r8_full bytes, 128 B aligned)
   const float2* hpair;       // [n_o][N/2] float4 {hi(n), hi(n+1), lo(n), lo(n+1)}, n even: F_hi[o, n] * 2^-e(n)
                              // as fp32 (hi, lo) pairs, packed by column pair for the f32x2 epilogue
-  const unsigned char* wsl;  // [CG][n_lb][4N / CG][128 B] W slices of F_lo (w_slice_kernel)
+  const unsigned char* wsl;  // [CG][n_lb][w_rows / CG][128 B] W slices of F_lo (w_slice_kernel)
   const double* cm_hi;       // [R] max |F_hi[:, n]| (kept current by the row update)
   const double* cm_lo;       // [R] max |F_lo[:, n]|
   const double* xscale;      // tensor split scale (device scalar)
@@ -549,23 +563,27 @@ __device__ __forceinline__ void two_sum2(f32x2& hi, f32x2& lo, f32x2 p) {
   hi = s;
 }
 
-template <int NT, int CG>  // N / 16; CTAs per MMA group (1, or 2: a CTA pair with M = 256)
+// N / 16; CTAs per MMA group (1, or 2: a CTA pair with M = 256); packed T0 / T1 ranges (R <= N - 8)
+template <int NT, int CG, int PK = 0>
 __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __grid_constant__ TcParams p) {
   constexpr int N = NT * 16;
+  constexpr int NP = N - 8 * PK;           // columns of ACC0 and of the T0 / T1 ranges (see set_cols)
+  static_assert(PK == 0 || merged_acc(N), "packed ranges exist for merged accumulator sets only");
   constexpr int kEpi = epi_warps(NT);
-  constexpr int NC = N * 4 / kEpi;         // columns per epilogue thread
+  constexpr int NC = NP * 4 / kEpi;        // columns per epilogue thread
   // TMEM load width: 16 columns where it divides NC and registers allow
 // 8-column TMEM loads up to 64 columns per thread (c5, N = 112 over 8 warps:
 // drain alone 3.03 vs 3.25 ms per mode with 4-column loads)
 #ifndef NTF_LW_WIDE
 #define NTF_LW_WIDE 64
 #endif
-  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : ((NC > NTF_LW_WIDE || NC % 8) ? 4 : 8);
-  static_assert(NC % LW == 0, "epilogue columns must be a multiple of the load width");
+  constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : ((NC > NTF_LW_WIDE || NC % 4) ? 4 : 8);
+  constexpr int LT = NC % LW;              // a last, narrower load (packed ranges: 52 = 6 x 8 + 4)
+  static_assert(LT == 0 || LT == 4, "epilogue columns must be a multiple of 4");
   constexpr int kAccBufs = acc_bufs(N);
   constexpr int kIssuers = mma_issuers(N);
   const int kXStage = p.stage_bytes;       // one X slot (slot_ks K steps of both planes), 128 B aligned
-  constexpr int kWrows = 4 * N / CG;       // W rows of one l block held by this CTA
+  constexpr int kWrows = w_rows(N, NP) / CG;  // W rows of one l block held by this CTA
   constexpr int kWlb = kWrows * kBK * 2;   // their bytes
   constexpr int kFirstEpi = 4;
   const uint64_t g_entry = gtimer();
@@ -766,10 +784,10 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // 8-element chunks r8*16 B apart (LBO); plane S1 follows plane S0.
     const bool no_mma = (dbg & 2) != 0, plain_arrive = (dbg & 64) != 0;
     constexpr bool kMerged = merged_acc(N);
-    const uint32_t idesc_a = make_idesc(kMerged ? 2 * N : 3 * N, false, CG);
+    const uint32_t idesc_a = make_idesc(kMerged ? 2 * NP : 3 * N, false, CG);
     const uint32_t idesc_n = make_idesc(N, false, CG);
     // B operand offsets (rows of this CTA's W block, descriptor units of 16 B)
-    constexpr uint64_t kB1 = ((w_range_end(N, 0) - w_range_begin(N, 0)) / CG) * 128 / 16;
+    constexpr uint64_t kB1 = ((w_range_end(N, NP, 0) - w_range_begin(N, NP, 0)) / CG) * 128 / 16;
     constexpr uint64_t kB2 = kMerged ? kB1 + (N / CG) * 128 / 16 : kB1;
     const uint32_t lbo = static_cast<uint32_t>(r8) * 16u;
     const uint64_t da_base = smem_desc_noswz(xbase, lbo, 128);
@@ -815,8 +833,8 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       }
       mbar_wait_p(&acc_empty[ar.idx], ar.phase ^ 1u, wm, wt[1]);  // (a pair: both CTAs drained)
       tc_fence_after();
-      const uint32_t d0 = tmem + ar.idx * set_cols(N);
-      const uint32_t d1 = d0 + N;
+      const uint32_t d0 = tmem + ar.idx * set_cols(N, NP);
+      const uint32_t d1 = d0 + NP;
       for (int j = 0; j < nl; ++j) {
         const int nks = (ui.g * G + j == n_lb - 1) ? ct / 2 : kBK / kUK;
         const uint64_t db = db_base + static_cast<uint64_t>((j * kWlb) >> 4);
@@ -911,37 +929,66 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       hi[j] = 0ull;
       lo[j] = 0ull;
     }
+    // Per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
+    // max|F_hi[:,n]| < 2^e (the clamps of w_slice_kernel).  Formed here, one
+    // column per thread, while the first unit's loads are in flight (off the
+    // kernel's tail), after this thread's own wait on the preceding kernel (a
+    // CTA with no unit never synchronises with the W-loading warp).
+    double* sc = reinterpret_cast<double*>(tmem_slot + 2);  // [N], 8-byte aligned after the two slot words
+    pdl_wait();
+    {
+      const int n = static_cast<int>(threadIdx.x) - kFirstEpi * 32;
+      if (n < N) {
+        double s = 0.0;
+        if (n < R) {
+          int f = 0, e2 = 0;
+          const double cl = p.cm_lo[n], ch = p.cm_hi[n];
+          if (cl > 0.0) frexp(cl, &f);
+          if (ch > 0.0) frexp(ch, &e2);
+          // columns decayed to ~1e-300 (large penalties shrink factor columns
+          // geometrically) must not overflow the scales: clamp as the slicer (kFMin)
+          s = *p.xscale * ldexp(1.0, max(f, kFMin) - t_bits(G) + max(e2, kFMin));
+        }
+        sc[n] = s;
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
     Ring ar, hr;
     for (int u = u_begin; u < u_end; ++u) {
       mbar_wait_p(&acc_full[ar.idx], ar.phase, wm, wt[0]);
       mbar_wait_p(&h_full[hr.idx], hr.phase, wm, wt[1]);
       tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * set_cols(N) + c0;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ar.idx * set_cols(N, NP) + c0;
       const float4* hs = reinterpret_cast<const float4*>(hbase + hr.idx * N + c0);
+      // W columns [off, off + W) of this thread's range: ACC0 (S0*T0, exact
+      // integers), ACC1 (S0*T1 + S1*Fh, + ACC2's terms when merged), ACC2 (S0*T2)
+      auto drain = [&](auto wtag, const int off) {
+        constexpr int W = decltype(wtag)::value;
+        float a0[W], a1[W], a2[W];
+        tmem_ld<W>(taddr + off, a0);
+        tmem_ld<W>(taddr + NP + off, a1);
+        if constexpr (!merged_acc(N)) tmem_ld<W>(taddr + 2 * N + off, a2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < W; v += 2) {
+          const float4 h = hs[(off + v) >> 1];  // {hi, hi', lo, lo'} of columns v, v+1
+          const f32x2 hx = f2pack(h.x, h.y), hy = f2pack(h.z, h.w);
+          const f32x2 a = f2pack(a0[v], a0[v + 1]);
+          f32x2 a12 = f2pack(a1[v], a1[v + 1]);
+          // ACC2 = S0 x (T2 2^11): scaled back here (exact power of two)
+          if constexpr (!merged_acc(N)) a12 = f2fma(f2pack(a2[v], a2[v + 1]), kT2Unscale, a12);
+          const f32x2 pr = f2mul(a, hx);
+          const f32x2 er = f2fma(a, hx, f2neg(pr));  // a*hx = pr + er exactly
+          const f32x2 cr = f2fma(a12, hx, f2fma(a, hy, er));
+          const int q = (off + v) >> 1;
+          two_sum2(hi[q], lo[q], pr);
+          lo[q] = f2add(lo[q], cr);
+        }
+      };
       if (!(dbg & 4)) {
 #pragma unroll
-        for (int j = 0; j < NC / LW; ++j) {
-          float a0[LW], a1[LW], a2[LW];
-          tmem_ld<LW>(taddr + j * LW, a0);           // ACC0: S0*T0 (exact integers)
-          tmem_ld<LW>(taddr + N + j * LW, a1);       // ACC1: S0*T1 + S1*Fh (+ ACC2 when merged)
-          if constexpr (!merged_acc(N)) tmem_ld<LW>(taddr + 2 * N + j * LW, a2);  // ACC2: S0*T2
-          tmem_wait_ld();
-#pragma unroll
-          for (int v = 0; v < LW; v += 2) {
-            const float4 h = hs[(j * LW + v) >> 1];  // {hi, hi', lo, lo'} of columns v, v+1
-            const f32x2 hx = f2pack(h.x, h.y), hy = f2pack(h.z, h.w);
-            const f32x2 a = f2pack(a0[v], a0[v + 1]);
-            f32x2 a12 = f2pack(a1[v], a1[v + 1]);
-            // ACC2 = S0 x (T2 2^11): scaled back here (exact power of two)
-            if constexpr (!merged_acc(N)) a12 = f2fma(f2pack(a2[v], a2[v + 1]), kT2Unscale, a12);
-            const f32x2 pr = f2mul(a, hx);
-            const f32x2 er = f2fma(a, hx, f2neg(pr));  // a*hx = pr + er exactly
-            const f32x2 cr = f2fma(a12, hx, f2fma(a, hy, er));
-            const int q = (j * LW + v) >> 1;
-            two_sum2(hi[q], lo[q], pr);
-            lo[q] = f2add(lo[q], cr);
-          }
-        }
+        for (int j = 0; j < NC / LW; ++j) drain(std::integral_constant<int, LW>{}, j * LW);
+        if constexpr (LT != 0) drain(std::integral_constant<int, LT>{}, (NC / LW) * LW);
       }
       tc_fence_before();
       __syncwarp();
@@ -960,23 +1007,6 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
     // (a thread's own row is R doubles apart from its neighbours').
     const int rows_valid = static_cast<int>(p.M - m0 < p.tm ? p.M - m0 : p.tm);
     double* out0 = p.ws + (static_cast<int64_t>(split) * p.M + m0) * R;
-    // per-column output scale xs * 2^(f-t) * 2^e, with max|F_lo[:,n]| < 2^f,
-    // max|F_hi[:,n]| < 2^e (the clamps of w_slice_kernel).  Read here, after
-    // this thread's own wait on the preceding kernel (a CTA with no unit never
-    // synchronises with the W-loading warp, so the scales are not handed over
-    // through shared memory).
-    pdl_wait();
-    const double xs = *p.xscale;
-    const int tb = t_bits(G);
-    auto col_scale = [&](int n) {
-      int f = 0, e = 0;
-      const double cl = p.cm_lo[n], ch = p.cm_hi[n];
-      if (cl > 0.0) frexp(cl, &f);
-      if (ch > 0.0) frexp(ch, &e);
-      // columns decayed to ~1e-300 (large penalties shrink factor columns
-      // geometrically) must not overflow the scales: clamp as the slicer (kFMin)
-      return xs * ldexp(1.0, max(f, kFMin) - tb + max(e, kFMin));
-    };
     float hf[NC], lf[NC];
 #pragma unroll
     for (int j = 0; j < NC / 2; ++j) {
@@ -990,7 +1020,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
         for (int j = 0; j < NC; ++j) {
           const int n = c0 + j;
           if (n < R)
-            stage[row * R + n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * col_scale(n);
+            stage[row * R + n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * sc[n];
         }
       }
       asm volatile("bar.sync 1, %0;\n" ::"r"(kEpi * 32) : "memory");
@@ -1002,7 +1032,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
       for (int j = 0; j < NC; ++j) {
         const int n = c0 + j;
         if (n < R)
-          out[n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * col_scale(n);
+          out[n] = (static_cast<double>(hf[j]) + static_cast<double>(lf[j])) * sc[n];
       }
     }
   }
@@ -1048,7 +1078,7 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
 //   exact, T2 possibly subnormal); Fh = fp16(v), the 11-bit operand of the
 //   low tensor plane S1.  One thread per (l block, n, octet).
 // ----------------------------------------------------------------------------
-__global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int CG, int n_lb,
+__global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, int N, int NP, int CG, int n_lb,
                                bool t2_scaled,
                                const double* __restrict__ cm, int t, unsigned char* __restrict__ wsl,
                                const double* __restrict__ Fhi, int n_o,
@@ -1124,11 +1154,13 @@ __global__ void w_slice_kernel(const double* __restrict__ F, int l_ext, int R, i
         hs[2][v] = __double2half(t2_scaled ? r2 * 2048.0 : r2);
         hs[3][v] = __double2half(vv);  // Fh = fp16(v), the operand of the low plane S1
       }
-      const int rows_cta = 4 * N / CG;
+      const int rows_cta = w_rows(N, NP) / CG;
 #pragma unroll
       for (int sl = 0; sl < 4; ++sl) {
         int cta = 0, row = 0;
-        w_row_slot(N, CG, sl * N + n, cta, row);
+        const int vr = w_virtual_row(N, NP, sl, n);
+        if (vr < 0) continue;  // a padding column (n >= R) of a packed range: not stored
+        w_row_slot(N, NP, CG, vr, cta, row);
         unsigned char* wb = wsl + (static_cast<int64_t>(cta) * n_lb + lb) * rows_cta * 128;
         *reinterpret_cast<uint4*>(wb + row * 128 + ((oct ^ (row & 7)) << 4)) =
             *reinterpret_cast<const uint4*>(hs[sl]);
@@ -1320,9 +1352,9 @@ int sm_count_tc() {
   return n;
 }
 
-template <int NT, int CG>
+template <int NT, int CG, int PK = 0>
 cudaError_t launch_nt(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t stream, bool prep) {
-  auto kern = mttkrp_tc_kernel<NT, CG>;
+  auto kern = mttkrp_tc_kernel<NT, CG, PK>;
   if (prep) return allow_dyn_smem(reinterpret_cast<const void*>(kern), L.smem_bytes);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(L.n_full * L.splits + L.splits_tail);
@@ -1357,7 +1389,11 @@ cudaError_t dispatch_cg(const TcParams& p, const MttkrpTCLaunch& L, cudaStream_t
     case 4: return launch_nt<4, CG>(p, L, stream, prep);
     case 5: return launch_nt<5, CG>(p, L, stream, prep);
     case 6: return launch_nt<6, CG>(p, L, stream, prep);
-    case 7: return launch_nt<7, CG>(p, L, stream, prep);
+    case 7:
+      if constexpr (CG == 2) {  // R <= 104 (c5: R = 100): packed T0 / T1 ranges
+        if (L.np != L.N) return launch_nt<7, CG, 1>(p, L, stream, prep);
+      }
+      return launch_nt<7, CG>(p, L, stream, prep);
     case 8: return launch_nt<8, CG>(p, L, stream, prep);
     default: return cudaErrorInvalidValue;
   }
@@ -1436,6 +1472,7 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   L.mode = mode;
   L.R = R;
   L.N = ((R + 15) / 16) * 16;
+  L.np = L.N;
   L.M = mode == 1 ? I : (mode == 2 ? J : K);
   L.Q = mode == 3 ? I * J : (mode == 1 ? J * K : I * K);
   L.l_ext = static_cast<int>(mode == 3 ? J : K);
@@ -1451,6 +1488,11 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   // 10.50 vs 10.25, c3 12.2 vs 10.5, c5 137.8 vs 114.2).
   L.cg = L.M * L.Q >= (int64_t(1) << 28) ? 2 : 1;
   if (const char* e = diag_env("NTF_TC_CG")) L.cg = atoi(e) == 1 ? 1 : 2;
+  // Packed T0 / T1 ranges (set_cols): instantiated where it pays, the pair
+  // kernel at N = 112 with R <= 104 (BASELINE c5, R = 100: 432 instead of 448
+  // MMA columns per K step, 104 instead of 112 columns drained per accumulator).
+  if (L.cg == 2 && L.N == 112 && R <= 104) L.np = 104;
+  if (const char* e = diag_env("NTF_TC_PACK")) { if (atoi(e) == 0) L.np = L.N; }
   // Equal m-tiles of tm <= 128 rows (a multiple of 8, the core-matrix
   // height), so every CTA of a full tile streams the same bytes.  Pairs
   // take two consecutive tiles: an even tile count, and every tile stored
@@ -1474,7 +1516,7 @@ MttkrpTCLaunch mttkrp_tc_plan(int mode, int x_dtype, int64_t I, int64_t J, int64
   const int xs = ((L.slot_ks * 64 * L.tm + 127) / 128) * 128;
   L.stage_bytes = xs;
   L.h_stages = 8;
-  const int wlb = 4 * L.N / L.cg * kBK * 2;  // W bytes of one l block in one CTA
+  const int wlb = w_rows(L.N, L.np) / L.cg * kBK * 2;  // W bytes of one l block in one CTA
   const int limit = 226 * 1024;  // the opt-in 227 KB less the kernel's 1 KB of static shared memory
   auto fixed_bytes = [&](int G) {
     return 1024 + G * wlb + L.h_stages * L.N * 8 + (2 * L.h_stages + 14) * 8 + 16 + 3 * L.N * 8;
@@ -1665,7 +1707,7 @@ cudaError_t mttkrp_tc_bind(MttkrpTCLaunch& L, const TcTensor& t) {
     if (e != cudaSuccess) return e;
   }
   if (L.cg == 2) {  // tensor maps of this image and of the W slices (CTA-pair loads)
-    const int wrows = 4 * L.N / 2;
+    const int wrows = w_rows(L.N, L.np) / 2;
     cudaError_t e = rows128_map(&L.map_full, t.img, L.img_bytes / 128, static_cast<uint32_t>(2 * L.r8_full));
     if (e == cudaSuccess)
       e = rows128_map(&L.map_tail, t.img, L.img_bytes / 128, static_cast<uint32_t>(L.ct * L.r8_full / 4));
@@ -1770,7 +1812,7 @@ cudaError_t mttkrp_tc_launch(MttkrpTCLaunch& L, const TcTensor& t, const double*
     const int blocks = std::min((total + 63) / 64, 8 * sm_count_tc());
     if (!(p.debug & 128)) {
       cudaError_t e = launch_pdl(w_slice_kernel, dim3(blocks), dim3(64), 0, stream, Flo, L.l_ext,
-                                 L.R, L.N, L.cg, L.n_lb, !merged_acc(L.N), p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
+                                 L.R, L.N, L.np, L.cg, L.n_lb, !merged_acc(L.N), p.cm_lo, t, L.wsl, Fhi, L.n_o, p.cm_hi,
                                  L.hpair, stop_flag);
       if (e != cudaSuccess) return e;
     }

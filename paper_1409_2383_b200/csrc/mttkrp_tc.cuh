@@ -41,6 +41,7 @@ struct MttkrpTCLaunch {
   CUtensorMap map_full, map_tail, map_w;  // cg == 2: the image's blocks and the W slices (mttkrp_tc_bind)
   int mode;
   int R, N;                 // rank and MMA N (R rounded up to 16)
+  int np;                   // columns of the T0 / T1 slice ranges and of ACC0 (N, or N - 8 packed)
   int64_t M, Q;
   int n_mtiles;             // m-tiles (cg == 2: even)
   int cg;                   // CTAs per MMA group: 2 = CTA pairs (tcgen05 cta_group::2)

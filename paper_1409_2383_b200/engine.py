@@ -292,11 +292,21 @@ def _solver_stream(device):
     return s
 
 
-def _free_device_bytes(device) -> int:
-    """Free HBM on ``device`` (a function so that tests can shrink it)."""
+def _free_device_bytes(device, reclaim: bool = False) -> int:
+    """HBM a new plan can take on ``device`` (a function so that tests can
+    shrink it): what the driver reports as free plus what the library's
+    stream-ordered pool holds mapped but idle (released plans leave their block
+    images there, and the next plan allocates from them first).  ``reclaim``
+    first hands torch's cached, unused blocks back to the driver."""
     torch = _torch()
-    free, _ = torch.cuda.mem_get_info(device)
-    return int(free)
+    if reclaim:
+        torch.cuda.synchronize(device)
+        torch.cuda.empty_cache()
+    idle = ctypes.c_size_t(0)
+    with torch.cuda.device(device):
+        free, _ = torch.cuda.mem_get_info(device)
+        N.check(N.load().ntf_device_pool_idle_bytes(ctypes.byref(idle)))
+    return int(free) + int(idle.value)
 
 
 def _engine_that_fits(engine: int, slabs, rank: int, device) -> int:
@@ -313,6 +323,8 @@ def _engine_that_fits(engine: int, slabs, rank: int, device) -> int:
         return engine
     need = sum(x.numel() * 4 for x in xs)
     free = _free_device_bytes(device)
+    if need > 0.97 * free:  # count torch's cached blocks before giving up the tensor cores
+        free = _free_device_bytes(device, reclaim=True)
     if need <= 0.97 * free:
         return engine
     import warnings

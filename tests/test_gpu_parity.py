@@ -779,7 +779,7 @@ def test_auto_engine_falls_back_when_block_images_do_not_fit(monkeypatch):
     x = (O.reconstruct([rng.random((d, R)) for d in dims]) + 0.02 * rng.standard_normal(dims)).astype(np.float32)
     kw = dict(seed=3, eps_abs=0.0, eps_rel=0.0, n_max=6, max_restarts=0, inner_sweeps=2, track_factors=True)
     P.solver.release_plan_cache()
-    monkeypatch.setattr(E, "_free_device_bytes", lambda device: 1 << 16)
+    monkeypatch.setattr(E, "_free_device_bytes", lambda device, reclaim=False: 1 << 16)
     with pytest.warns(RuntimeWarning, match="block images"):
         got = P.fit(x, R, None, P.SolverConfig(**kw))
     monkeypatch.undo()
@@ -789,6 +789,41 @@ def test_auto_engine_falls_back_when_block_images_do_not_fit(monkeypatch):
         for a, b in zip(fg, fw):
             assert rel(a, b) <= 1e-9
     assert got.rfe == pytest.approx(want.rfe, rel=1e-9)
+
+
+def test_free_hbm_counts_the_idle_pool_and_torch_cache():
+    """Released plans leave their block images mapped in the library's
+    stream-ordered pool, and freed torch tensors stay in torch's cache: the
+    driver reports both as taken, but the next plan can have them.  The
+    engine="auto" fit check must count them (a c5 fit() after another c5 plan
+    of the same process once fell back to the fp64 engine for this reason)."""
+    import torch
+
+    from paper_1409_2383_b200 import _native as Nat
+    from paper_1409_2383_b200 import engine as E
+
+    dev = torch.device("cuda:0")
+    P.solver.release_plan_cache()
+    x = torch.rand((256, 256, 256), dtype=torch.float32, device=dev)  # 64 MB: 192 MB of block images
+    kw = dict(seed=1, eps_abs=0.0, eps_rel=0.0, n_max=2, max_restarts=0, inner_sweeps=1)
+    import ctypes
+
+    prob = E.DeviceProblem(x, x.shape, 8, P.SolverConfig(**kw), history_capacity=2)
+    torch.cuda.synchronize()
+    prob.close()
+    torch.cuda.synchronize()
+    idle = ctypes.c_size_t(0)
+    Nat.check(Nat.load().ntf_device_pool_idle_bytes(ctypes.byref(idle)))
+    assert idle.value >= 3 * x.numel() * 4
+    raw, _ = torch.cuda.mem_get_info(dev)
+    assert E._free_device_bytes(dev) >= raw + 3 * x.numel() * 4
+    del x, prob  # (the problem keeps a reference to its tensor)
+    cached = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    assert cached >= 64 << 20
+    assert E._free_device_bytes(dev, reclaim=True) >= raw + 3 * 64 * (1 << 20) + (64 << 20)
+    P.solver.release_plan_cache()
+    Nat.check(Nat.load().ntf_device_pool_idle_bytes(ctypes.byref(idle)))
+    assert idle.value < 64 << 20  # release_plan_cache trims the pool
 
 
 @pytest.mark.parametrize("dims,R", [((24, 20, 18), 131), ((17, 9, 33), 200), ((12, 10, 8), 256)])
