@@ -195,6 +195,31 @@ def test_mttkrp_mode_consistency_large_configs(name):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("R", [97, 100, 104, 105])
+def test_mttkrp_pair_kernel_packed_ranges(R):
+    """CTA-pair kernel at N = 112 (tensors of 2^28 elements and more): for
+    R <= 104 the T0 / T1 slice ranges and ACC0 are packed to 104 columns (the
+    first MMA of a K step runs at N' = 208 instead of 224, the epilogue drains
+    52 columns per thread as 6 x 8 + 4); R = 105 is the unpacked instance.
+    Every mode, every element, against the fp64-arithmetic engine on the same
+    fp32 values, on a ragged shape (m-tiles of 96..128 rows, last l block
+    partly filled)."""
+    dims = (768, 650, 600)
+    g = torch.Generator(device="cuda").manual_seed(R)
+    x = torch.rand(dims, dtype=torch.float32, device="cuda", generator=g)
+    rng = np.random.default_rng(R)
+    f = _factors(rng, dims, R)
+    t = P.DenseTensor(x)
+    for m in (1, 2, 3):
+        got = np.asarray(P.mttkrp_factors(t, f, m, engine="tcgen05"))
+        want = np.asarray(P.mttkrp_factors(t, f, m, engine="cuda_core"))
+        assert got.shape == (dims[m - 1], R)
+        assert rel(got, want) <= 5e-9, (m, rel(got, want))
+        assert np.max(np.abs(got - want) / np.abs(want)) <= 1e-7, m
+    del x, t
+    torch.cuda.empty_cache()
+
+
 def test_norm_and_rfe_kernel():
     rng = np.random.default_rng(2)
     dims = (13, 9, 21)
