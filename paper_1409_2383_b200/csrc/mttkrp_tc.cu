@@ -1412,7 +1412,13 @@ void partition_units(const MttkrpTCLaunch& L, int parts, uint32_t* ub) {
   // measured, single CTAs: c2 best near 3, R = 64..100 near 4..6; CTA pairs (the
   // unit's drain is spread over two SMs): c5 7.35 / 7.43 / 7.69 ms per mode at
   // 2.5 / 4 / 5.5, c2 and c3 flat
-  double unit_fixed = L.cg == 2 ? 2.5 : 2.0 + L.N / 32.0;
+  // Merged sets (N > 85) are tensor-/epilogue-bound, not HBM-bound: a unit takes
+  // about the same time whatever its bytes (c5 timeline, tools/tc_timeline.py: the
+  // last group's 3.25-block units cost 3.71 us against 3.76 us for 4-block units,
+  // so the CTAs of the last split ran 1980 units against 1752 and finished 12%
+  // after the rest); per outer iteration 110.1 / 109.2 / 108.0 / 107.0 / 107.9 ms
+  // at 2.5 / 5 / 10 / 20 / 40.
+  double unit_fixed = L.cg == 2 ? (merged_acc(L.N) ? 20.0 : 2.5) : 2.0 + L.N / 32.0;
   if (const char* e = diag_env("NTF_TC_UNITCOST")) unit_fixed = atof(e);
   auto cost = [&](int g) {
     const int nl = std::min(L.G, L.n_lb - g * L.G);
