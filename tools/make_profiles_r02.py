@@ -71,6 +71,11 @@ def main():
     open(os.path.join(OUT, "r02_launches_c2.txt"), "w").write("\n".join(lines) + "\n")
     if tr:
         traffic["c2"] = {"bytes_per_launch": tr[1], "kernel": tr[0], "source": "profiles/r02_launches_c2.txt"}
+    if os.path.exists(os.path.join(GRO, "r02_launches_c5.csv")):
+        lines5, _ = launch_list("r02_launches_c5.csv",
+                                "ncu launch list of `python bench.py --steps 2 --warmup 3 --no-e2e "
+                                "--no-cpu-baseline` (c5, round 2, final tree)")
+        open(os.path.join(OUT, "r02_launches_c5.txt"), "w").write("\n".join(lines5) + "\n")
     keep = ("Duration", "SM Frequency", "DRAM Frequency", "DRAM Throughput", "Memory Throughput",
             "Executed Ipc", "Issue Slots Busy", "Registers Per Thread", "Grid Size", "Block Size",
             "Cluster Size", "Dynamic Shared Memory Per Block", "Achieved Occupancy", "L1/TEX Hit Rate",
