@@ -50,7 +50,8 @@ def kappa(factors):
     for f in factors:
         s = np.abs(f.sum(axis=0))
         a = np.abs(f).sum(axis=0)
-        q.append(np.where(a > 0, s / np.maximum(a, 1e-300), 1.0))
+        # (columns decayed to denormals count as dead: s / max(a, 1e-300) once reported ~1e9 for them)
+        q.append(np.where(a > 1e-290, s / np.maximum(a, 1e-290), 1.0))
     worst = 1.0
     for n in range(len(factors)):
         prod = np.ones_like(q[0])
