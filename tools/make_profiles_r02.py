@@ -53,6 +53,8 @@ def full_capture(rep):
     rows = list(csv.reader(io.StringIO(raw)))
     h, u, v = rows[0], rows[1], rows[2]
     vals = {a: (b, c) for a, b, c in zip(h, u, v)}
+    for a in list(vals):  # section-qualified names ("TPC.TriageCompute.sm__pipe_...") also under their metric name
+        vals.setdefault(a.rsplit(".Triage", 1)[-1].split(".", 1)[-1] if ".Triage" in a else a, vals[a])
     det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
 
     def num(k):
@@ -89,7 +91,9 @@ def main():
         rd, wr, dur = num("dram__bytes_read.sum"), num("dram__bytes_write.sum"), num("gpu__time_duration.sum")
         extra = []
         for k in ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                  "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
                   "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                  "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
                   "smsp__inst_executed.sum"):
             if k in vals:
                 extra.append(f"{k} = {vals[k][1]} {vals[k][0]}")
