@@ -217,10 +217,32 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 // D[tmem] (+)= A[smem] * B[smem]; CG = 2: M = 256 over the CTA pair (each
 // CTA's A rows and half of B's N rows at the same shared-memory offsets),
 // issued by the pair's leader only.
-template <int CG>
+// COLL: 0 plain; 1 keep A in the tensor core's operand collector for the next
+// MMA (collector::a::fill); 2 take A from the collector, last use
+// (collector::a::lastuse).  Only valid when ONE thread issues every MMA of the
+// CTA (pair): another issuer's MMAs would interleave and replace the kept A.
+template <int CG, int COLL = 0>
 __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                            uint32_t idesc, uint32_t accumulate) {
-  if constexpr (CG == 1) {
+  if constexpr (CG == 2 && COLL == 1) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else if constexpr (CG == 2 && COLL == 2) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else if constexpr (CG == 1) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -580,8 +602,17 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
   constexpr int LW = (NC % 16 == 0 && NC <= 32 && kEpi < 16) ? 16 : ((NC > NTF_LW_WIDE || NC % 4) ? 4 : 8);
   constexpr int LT = NC % LW;              // a last, narrower load (packed ranges: 52 = 6 x 8 + 4)
   static_assert(LT == 0 || LT == 4, "epilogue columns must be a multiple of 4");
-  constexpr int kAccBufs = acc_bufs(N);
-  constexpr int kIssuers = mma_issuers(N);
+#ifndef NTF_PK_COLLECT
+#define NTF_PK_COLLECT 1
+#endif
+  // Packed pair kernel: ONE issuer (its MMAs are long enough, 104 + 56 + 56
+  // cycles per K step, for a single thread to keep the pipe fed) on both
+  // accumulator sets, so the S0 operand of a K step's first MMA can stay in
+  // the collector for the second (tc_mma_f16 COLL) instead of being read from
+  // shared memory again.
+  constexpr bool kCollect = PK != 0 && CG == 2 && NTF_PK_COLLECT != 0;
+  constexpr int kAccBufs = kCollect ? 2 : acc_bufs(N);
+  constexpr int kIssuers = kCollect ? 1 : mma_issuers(N);
   const int kXStage = p.stage_bytes;       // one X slot (slot_ks K steps of both planes), 128 B aligned
   constexpr int kWrows = w_rows(N, NP) / CG;  // W rows of one l block held by this CTA
   constexpr int kWlb = kWrows * kBK * 2;   // their bytes
@@ -851,8 +882,13 @@ __global__ void __launch_bounds__(tc_threads(NT), 1) mttkrp_tc_kernel(const __gr
                 const uint32_t first = (j | ks) ? 1u : 0u;
                 const uint64_t a0 = da + kk * a_kstep, a1 = a0 + a_plane;
                 const uint64_t b = db + ks * (32 >> 4);
-                tc_mma_f16<CG>(d0, a0, b, idesc_a, first);
-                if constexpr (kMerged) tc_mma_f16<CG>(d1, a0, b + kB1, idesc_n, 1u);
+                if constexpr (kCollect) {
+                  tc_mma_f16<CG, 1>(d0, a0, b, idesc_a, first);
+                  tc_mma_f16<CG, 2>(d1, a0, b + kB1, idesc_n, 1u);
+                } else {
+                  tc_mma_f16<CG>(d0, a0, b, idesc_a, first);
+                  if constexpr (kMerged) tc_mma_f16<CG>(d1, a0, b + kB1, idesc_n, 1u);
+                }
                 tc_mma_f16<CG>(d1, a1, b + kB2, idesc_n, 1u);
               }
             }
