@@ -195,9 +195,11 @@ def test_mttkrp_mode_consistency_large_configs(name):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("R", [97, 100, 104, 105])
+@pytest.mark.parametrize("R", [88, 97, 100, 104, 105, 128])
 def test_mttkrp_pair_kernel_packed_ranges(R):
-    """CTA-pair kernel at N = 112 (tensors of 2^28 elements and more): for
+    """CTA-pair kernel with merged accumulator sets (N = 96, 112, 128; tensors
+    of 2^28 elements and more: R = 88 and 128 are the N = 96 / 128 instances
+    with 16 epilogue warps).  At N = 112: for
     R <= 104 the T0 / T1 slice ranges and ACC0 are packed to 104 columns (the
     first MMA of a K step runs at N' = 208 instead of 224, the epilogue drains
     52 columns per thread as 6 x 8 + 4); R = 105 is the unpacked instance.
